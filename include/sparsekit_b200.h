@@ -1,0 +1,197 @@
+/*
+ * sparsekit_b200.h -- C ABI of the B200-native activation-sparse MoE FFN layer.
+ *
+ * Drop-in boundary for the hot path of the reference `sparsekit` library
+ * (/root/reference/proj): the reference exposes this path as C++ free
+ * functions over value types and has no FFI of its own, so each entry point
+ * below names the reference interface it stands in for (file:line).  The C++
+ * facade in sparsekit_b200.hpp re-creates those reference signatures on top
+ * of this ABI; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no C++ or torch types.
+ *   - every function returns an skb_status; skb_last_error() gives the
+ *     thread-local message.  Codes map 1:1 onto the reference exception types
+ *     (proj/include/sparsekit/errors.hpp:12-43).
+ *   - "host" pointers are ordinary (pageable or pinned) CPU memory borrowed
+ *     for the duration of the call.  "device" pointers are CUDA device memory
+ *     on the layer's device.
+ *   - there is no CPU fallback: without a CUDA device every compute entry
+ *     point fails with SKB_ECUDA.
+ *
+ * Numeric contract: expert weights are rounded once to
+ * bf16 at layer creation, tokens are rounded to bf16 for the gate/up
+ * contraction, all accumulation is fp32, h = silu(g)*u stays fp32.  The
+ * router keeps fp32 weights and fp32 tokens and, unless
+ * SKB_FLAG_FAST_ROUTER is set, reproduces the reference's ascending-index
+ * float accumulation bit for bit, so expert ids equal the reference's.
+ */
+#ifndef SPARSEKIT_B200_H
+#define SPARSEKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKB_ABI_VERSION 1
+
+typedef enum skb_status {
+  SKB_OK = 0,
+  SKB_ESHAPE = 1,    /* sparsekit::ShapeError    */
+  SKB_ECONFIG = 2,   /* sparsekit::ConfigError   */
+  SKB_EINDEX = 3,    /* sparsekit::IndexError    */
+  SKB_EINTERNAL = 4, /* sparsekit::InternalError */
+  SKB_ECUDA = 5      /* no reference analogue: CUDA runtime/driver failure */
+} skb_status;
+
+/* MoEConfig, proj/include/sparsekit/model.hpp:15-29, as fixed-width ints. */
+typedef struct skb_config {
+  int32_t n_experts;   /* E */
+  int32_t top_k;       /* K */
+  int32_t d_model;     /* D */
+  int32_t d_ffn;       /* N */
+  int32_t has_shared;  /* bool */
+  int32_t d_shared;    /* S, 0 when absent */
+  int32_t renormalize; /* bool */
+  int32_t align_block; /* dispatch padding granularity (plan export only) */
+} skb_config;
+
+/* ForwardReport minus the output matrix, proj/include/sparsekit/engine.hpp:19-27,
+ * with MacCounter (linalg.hpp:51-70) flattened in. */
+typedef struct skb_report {
+  uint64_t gate_macs, up_macs, down_macs, other_macs;
+  uint64_t active_neurons_total;
+  double achieved_routed_sparsity;
+  uint64_t tiles_total, tiles_skipped;
+  int32_t path_used; /* ExecPath: 0 dense, 1 sparse */
+  int32_t reserved;
+} skb_report;
+
+/* Execution modes of skb_layer_forward*. */
+enum {
+  SKB_MODE_DENSE = 0,  /* forward_dense,        engine.hpp:38-39  */
+  SKB_MODE_TOPK = 1,   /* forward_masked_dense(build_topk_masks(s)) fused; skips masked W_down rows */
+  SKB_MODE_MASKED = 2  /* forward_masked_dense with caller masks, engine.hpp:43-44 */
+};
+
+/* Flags. */
+#define SKB_FLAG_FAST_ROUTER 0x1u  /* warp-parallel router dot products (not order-faithful) */
+#define SKB_FLAG_SIMT_GATEUP 0x2u  /* verification only: CUDA-core gate/up instead of tcgen05 */
+#define SKB_FLAG_TIME_STAGES 0x4u  /* record CUDA events around every stage (host API only) */
+#define SKB_FLAG_NO_PDL 0x8u       /* disable programmatic dependent launch between stages */
+
+#define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
+
+typedef struct skb_forward_args {
+  int32_t batch; /* B >= 1 */
+  int32_t mode;  /* SKB_MODE_* */
+  uint32_t flags;
+  int32_t reserved;
+  double s_routed; /* SparsityLevel for routed experts, [0,1] (TOPK mode) */
+  double s_shared; /* SparsityLevel for the shared expert, [0,1] (TOPK mode) */
+  const float* x;  /* [B][D] tokens */
+  float* y;        /* [B][D] outputs */
+  /* MASKED mode inputs (MaskSet, engine.hpp:31-34); shared may be NULL/0 => dense shared expert */
+  const uint8_t* routed_mask_in;
+  uint64_t routed_mask_len; /* must be B*K*N */
+  const uint8_t* shared_mask_in;
+  uint64_t shared_mask_len; /* 0 or B*S */
+  /* Optional captures (NULL to skip).  Host pointers for skb_layer_forward,
+   * ignored by skb_layer_forward_device. */
+  int32_t* ids_out;         /* [B][K]  RouteResult::ids,     router.hpp:20-32 */
+  float* weights_out;       /* [B][K]  RouteResult::weights */
+  uint8_t* routed_mask_out; /* [B][K][N] slot-major, 1 = kept (MaskSet::routed) */
+  uint8_t* shared_mask_out; /* [B][S] */
+  float* h_routed_out;      /* [B][K][N] pre-mask SwiGLU output */
+  float* h_shared_out;      /* [B][S] */
+} skb_forward_args;
+
+typedef struct skb_layer skb_layer;
+
+const char* skb_last_error(void);
+int skb_abi_version(void);
+/* Number of CUDA devices visible (0 when none); never fails. */
+int skb_device_count(void);
+
+/* MoEConfig::validate, proj/src/model.cpp:113-127 (same order, same messages). */
+int skb_config_validate(const skb_config* cfg);
+
+/* Builds the device weight image from a MoELayerWeights (model.hpp:34-43):
+ * router [E][D]; gate/up/down_t[e] each [N][D] row-major fp32 (down stored
+ * transposed exactly as the reference does); shared_* [S][D] or NULL. */
+int skb_layer_create(const skb_config* cfg, const float* router, const float* const* gate,
+                     const float* const* up, const float* const* down_t,
+                     const float* shared_gate, const float* shared_up,
+                     const float* shared_down_t, int device, skb_layer** out);
+
+/* generate_synthetic(cfg, seed, scale), proj/src/model.cpp:129-166, evaluated
+ * on the device with SplitMix64 jump-ahead: the image is bit-identical to
+ * uploading the reference's matrices, without materialising them on the host. */
+int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale, int device,
+                               skb_layer** out);
+
+void skb_layer_destroy(skb_layer* layer);
+
+/* Pre-sizes every workspace for batches up to max_batch (so that
+ * skb_layer_forward_device never allocates and can be stream-captured). */
+int skb_layer_reserve(skb_layer* layer, int max_batch);
+
+/* The layer forward with HOST buffers: copies x in, runs the stages, copies
+ * y (and any requested captures) out, synchronises.  Replaces
+ * forward_dense / forward_masked_dense (proj/src/engine.cpp:94-191, 219-227)
+ * and, in TOPK mode, build_topk_masks + forward_masked_dense
+ * (proj/src/profiler.cpp:101-150). */
+int skb_layer_forward(skb_layer* layer, const skb_forward_args* args, skb_report* report);
+
+/* Same stages with DEVICE x/y, enqueued asynchronously on `stream`
+ * (a cudaStream_t passed as void*; NULL = the layer's own stream).  No
+ * allocation, no synchronisation: safe inside CUDA-graph capture after
+ * skb_layer_reserve.  Capture pointers in args are ignored. */
+int skb_layer_forward_device(skb_layer* layer, const skb_forward_args* args, void* stream,
+                             skb_report* report);
+
+/* Per-stage milliseconds of the last skb_layer_forward call that carried
+ * SKB_FLAG_TIME_STAGES; ms must hold SKB_N_STAGES floats. */
+int skb_layer_stage_times(skb_layer* layer, float* ms);
+
+/* Kernel launches issued by the last forward call on this layer. */
+int skb_layer_last_launches(skb_layer* layer);
+
+/* Device bytes held by the weight image. */
+uint64_t skb_layer_weight_bytes(skb_layer* layer);
+
+/* ---- stage entry points (host buffers in and out; used by the parity tests) ---- */
+
+/* route(), proj/src/router.cpp:13-68: softmax + top-k, ties to the lower id. */
+int skb_route(const float* logits, int batch, int n_experts, int top_k, int renormalize,
+              int32_t* ids, float* weights);
+
+/* align_dispatch(), proj/src/router.cpp:70-107.  sorted_out needs
+ * batch*top_k + n_experts*(block-1) entries, expert_of_block the same / block. */
+int skb_align_dispatch(const int32_t* ids, int batch, int top_k, int n_experts, int block,
+                       int32_t* sorted_out, int32_t* expert_of_block, int32_t* n_padded,
+                       int32_t* n_blocks);
+
+/* combine(), proj/src/router.cpp:109-132. */
+int skb_combine(const float* slot_outputs, const float* weights, int batch, int top_k,
+                int d_model, float* y);
+
+/* mask_smallest_magnitudes(), proj/src/activation.cpp:31-52, row-wise:
+ * h is [rows][n]; counts is per-row (length rows) -- apply_budget's per-slot
+ * budgets (proj/src/budget.cpp:78-85) are the same call.  kept_idx (optional)
+ * is [rows][n] ascending survivors padded with -1; kept_count (optional) [rows]. */
+int skb_mask_smallest(const float* h, int rows, int n, const int32_t* counts, uint8_t* mask,
+                      int32_t* kept_idx, int32_t* kept_count);
+
+/* topk_mask(), proj/src/activation.cpp:54-60: count = floor(s*n + 0.5) in double. */
+int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask);
+
+/* round-half-up count used by topk_mask (host arithmetic, no device needed). */
+int skb_n_off(double s, int n, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEKIT_B200_H */

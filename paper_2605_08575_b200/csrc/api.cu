@@ -1,0 +1,825 @@
+// api.cu -- the C ABI of include/sparsekit_b200.h: host-side validation (same order and
+// messages as the reference), device weight image, workspaces, stage sequencing.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "../../include/sparsekit_b200.h"
+#include "skb_internal.cuh"
+
+using namespace skb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define SKB_CUDA(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(SKB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                                 \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled g_encode = nullptr;
+
+int load_encode() {
+  if (g_encode) return SKB_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  SKB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || fn == nullptr)
+    return fail(SKB_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  return SKB_OK;
+}
+
+// 2D bf16 tensor [rows][cols] row-major, box = {kBlockK cols, box_rows}, 128-byte swizzle.
+int encode_bf16_2d(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  int rc = load_encode();
+  if (rc) return rc;
+  cuuint64_t gdim[2] = {cols, rows};
+  cuuint64_t gstride[1] = {cols * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SKB_ECUDA, "cuTensorMapEncodeTiled failed with CUresult %d", (int)r);
+  return SKB_OK;
+}
+
+int n_off_of(double s, int n) {
+  // topk_mask, proj/src/activation.cpp:54-60
+  const long raw = static_cast<long>(std::floor(s * n + 0.5));
+  long c = raw < 0 ? 0 : raw;
+  if (c > n) c = n;
+  return static_cast<int>(c);
+}
+
+const int kTileCases[5] = {16, 32, 64, 128, 256};
+
+}  // namespace
+
+struct skb_layer {
+  skb_config cfg{};
+  Geometry g{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  // weight image
+  float* d_router = nullptr;
+  __nv_bfloat16* d_wgu = nullptr;
+  __nv_bfloat16* d_wd = nullptr;
+  __nv_bfloat16* d_wd_shared = nullptr;
+  uint64_t weight_bytes = 0;
+  CUtensorMap tmap_w{};
+
+  // workspaces, sized for cap_batch
+  int cap_batch = 0;
+  float* d_x = nullptr;
+  float* d_y = nullptr;
+  float* d_logits = nullptr;
+  int32_t* d_ids = nullptr;
+  float* d_wts = nullptr;
+  DispatchBuffers disp{};
+  __nv_bfloat16* d_xs = nullptr;
+  uint64_t xs_rows = 0;
+  CUtensorMap tmap_x[5]{};
+  float* d_h = nullptr;
+  int32_t* d_kidx = nullptr;
+  float* d_kval = nullptr;
+  int32_t* d_kcnt = nullptr;
+  float* d_part = nullptr;
+  uint8_t* d_mask_in_r = nullptr;
+  uint8_t* d_mask_in_s = nullptr;
+  uint8_t* d_mask_out_r = nullptr;
+  uint8_t* d_mask_out_s = nullptr;
+  int n_chunks = 0;
+
+  cudaEvent_t ev[SKB_N_STAGES + 1]{};
+  float stage_ms[SKB_N_STAGES]{};
+  bool have_stage_ms = false;
+  int last_launches = 0;
+};
+
+namespace {
+
+void free_workspace(skb_layer* L) {
+  void* ptrs[] = {L->d_x,        L->d_y,         L->d_logits,       L->d_ids,
+                  L->d_wts,      L->disp.perm,   L->disp.inv,       L->disp.row_expert,
+                  L->disp.expert_off, L->disp.tile_expert, L->disp.tile_row0, L->disp.tile_nrows,
+                  L->disp.n_tiles, L->d_xs,      L->d_h,            L->d_kidx,
+                  L->d_kval,     L->d_kcnt,      L->d_part,         L->d_mask_in_r,
+                  L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = L->d_part = nullptr;
+  L->d_ids = L->d_kidx = L->d_kcnt = nullptr;
+  L->disp = DispatchBuffers{};
+  L->d_xs = nullptr;
+  L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
+  L->cap_batch = 0;
+}
+
+template <typename T>
+int dmalloc(T** p, size_t count) {
+  SKB_CUDA(cudaMalloc(reinterpret_cast<void**>(p), (count ? count : 1) * sizeof(T)));
+  return SKB_OK;
+}
+
+int max_tiles_for(const Geometry& g, int B, int tn) {
+  const int BK = B * g.K;
+  return (g.E < BK ? g.E : BK) + BK / tn + (g.has_shared ? ceil_div(B, tn) : 0);
+}
+
+int reserve_locked(skb_layer* L, int B) {
+  if (B <= L->cap_batch) return SKB_OK;
+  SKB_CUDA(cudaSetDevice(L->device));
+  SKB_CUDA(cudaStreamSynchronize(L->stream));
+  free_workspace(L);
+  const Geometry& g = L->g;
+  int cap = 1;
+  while (cap < B) cap <<= 1;
+  const size_t BK = static_cast<size_t>(cap) * g.K;
+  const size_t rows = BK + (g.has_shared ? cap : 0);
+  int rc;
+#define SKB_TRY(x) \
+  if ((rc = (x)) != SKB_OK) return rc
+  SKB_TRY(dmalloc(&L->d_x, static_cast<size_t>(cap) * g.D));
+  SKB_TRY(dmalloc(&L->d_y, static_cast<size_t>(cap) * g.D));
+  SKB_TRY(dmalloc(&L->d_logits, static_cast<size_t>(cap) * g.E));
+  SKB_TRY(dmalloc(&L->d_ids, BK));
+  SKB_TRY(dmalloc(&L->d_wts, BK));
+  SKB_TRY(dmalloc(&L->disp.perm, BK));
+  SKB_TRY(dmalloc(&L->disp.inv, BK));
+  SKB_TRY(dmalloc(&L->disp.row_expert, rows));
+  SKB_TRY(dmalloc(&L->disp.expert_off, static_cast<size_t>(g.E) + 2));
+  const size_t max_tiles = static_cast<size_t>(max_tiles_for(g, cap, 16)) + 1;
+  SKB_TRY(dmalloc(&L->disp.tile_expert, max_tiles));
+  SKB_TRY(dmalloc(&L->disp.tile_row0, max_tiles));
+  SKB_TRY(dmalloc(&L->disp.tile_nrows, max_tiles));
+  SKB_TRY(dmalloc(&L->disp.n_tiles, 1));
+  L->xs_rows = rows;
+  SKB_TRY(dmalloc(&L->d_xs, rows * g.Dp));
+  SKB_CUDA(cudaMemsetAsync(L->d_xs, 0, rows * g.Dp * sizeof(__nv_bfloat16), L->stream));
+  for (int i = 0; i < 5; ++i)
+    SKB_TRY(encode_bf16_2d(&L->tmap_x[i], L->d_xs, rows, g.Dp, kTileCases[i]));
+  SKB_TRY(dmalloc(&L->d_h, rows * g.Nh));
+  SKB_TRY(dmalloc(&L->d_kidx, rows * g.Nh));
+  SKB_TRY(dmalloc(&L->d_kval, rows * g.Nh));
+  SKB_TRY(dmalloc(&L->d_kcnt, rows));
+  L->n_chunks = ceil_div(g.Nh, kDownChunk);
+  SKB_TRY(dmalloc(&L->d_part, rows * L->n_chunks * g.Dp));
+  SKB_TRY(dmalloc(&L->d_mask_in_r, BK * g.N));
+  SKB_TRY(dmalloc(&L->d_mask_out_r, BK * g.N));
+  if (g.has_shared) {
+    SKB_TRY(dmalloc(&L->d_mask_in_s, static_cast<size_t>(cap) * g.S));
+    SKB_TRY(dmalloc(&L->d_mask_out_s, static_cast<size_t>(cap) * g.S));
+  }
+#undef SKB_TRY
+  SKB_CUDA(cudaStreamSynchronize(L->stream));
+  L->cap_batch = cap;
+  return SKB_OK;
+}
+
+int validate_cfg(const skb_config* c) {
+  // MoEConfig::validate, proj/src/model.cpp:113-127
+  if (c == nullptr) return fail(SKB_ECONFIG, "config is null");
+  if (c->n_experts < 1) return fail(SKB_ECONFIG, "n_experts must be >= 1");
+  if (c->top_k < 1 || c->top_k > c->n_experts)
+    return fail(SKB_ECONFIG, "top_k must satisfy 1 <= K <= E, got K=%d E=%d", c->top_k,
+                c->n_experts);
+  if (c->d_model < 1) return fail(SKB_ECONFIG, "d_model must be >= 1");
+  if (c->d_ffn < 1) return fail(SKB_ECONFIG, "d_ffn must be >= 1");
+  if (c->d_shared < 0) return fail(SKB_ECONFIG, "d_shared must be >= 0");
+  if ((c->has_shared != 0) != (c->d_shared > 0))
+    return fail(SKB_ECONFIG, "has_shared must match d_shared > 0");
+  if (c->align_block < 1) return fail(SKB_ECONFIG, "align_block must be >= 1");
+  return SKB_OK;
+}
+
+int new_layer(const skb_config* cfg, int device, skb_layer** out) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (out == nullptr) return fail(SKB_EINTERNAL, "out pointer is null");
+  if (cfg->n_experts > kMaxExperts)
+    return fail(SKB_ECONFIG, "n_experts=%d exceeds the device router limit %d", cfg->n_experts,
+                kMaxExperts);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+    return fail(SKB_ECUDA, "no CUDA device: this library has no CPU path");
+  if (device < 0 || device >= ndev) return fail(SKB_ECUDA, "device %d outside [0, %d)", device, ndev);
+  SKB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SKB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(SKB_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a only", device,
+                prop.major, prop.minor);
+  skb_layer* L = new skb_layer();
+  L->cfg = *cfg;
+  L->device = device;
+  Geometry& g = L->g;
+  g.E = cfg->n_experts;
+  g.K = cfg->top_k;
+  g.D = cfg->d_model;
+  g.N = cfg->d_ffn;
+  g.S = cfg->has_shared ? cfg->d_shared : 0;
+  g.has_shared = cfg->has_shared ? 1 : 0;
+  g.renorm = cfg->renormalize ? 1 : 0;
+  g.Dp = round_up(g.D, kBlockK);
+  g.Np = round_up(g.N, kNeuronBlock);
+  g.Sp = g.has_shared ? round_up(g.S, kNeuronBlock) : 0;
+  g.Nh = g.Np > g.Sp ? g.Np : g.Sp;
+  cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete L;
+    return fail(SKB_ECUDA, "cudaStreamCreate failed: %s", cudaGetErrorString(e));
+  }
+  for (auto& ev : L->ev) cudaEventCreate(&ev);
+  const size_t gu_rows = static_cast<size_t>(g.E) * 2 * g.Np + 2 * static_cast<size_t>(g.Sp);
+  const size_t wd_rows = static_cast<size_t>(g.E) * g.Np + g.Sp;
+  rc = dmalloc(&L->d_router, static_cast<size_t>(g.E) * g.D);
+  if (!rc) rc = dmalloc(&L->d_wgu, gu_rows * g.Dp);
+  if (!rc) rc = dmalloc(&L->d_wd, wd_rows * g.Dp);
+  if (rc) {
+    skb_layer_destroy(L);
+    return rc;
+  }
+  L->d_wd_shared = g.has_shared ? L->d_wd + static_cast<size_t>(g.E) * g.Np * g.Dp : nullptr;
+  L->weight_bytes = static_cast<uint64_t>(g.E) * g.D * 4 + (gu_rows + wd_rows) * g.Dp * 2;
+  cudaMemsetAsync(L->d_wgu, 0, gu_rows * g.Dp * 2, L->stream);
+  cudaMemsetAsync(L->d_wd, 0, wd_rows * g.Dp * 2, L->stream);
+  rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows, g.Dp, 128);
+  if (rc) {
+    skb_layer_destroy(L);
+    return rc;
+  }
+  *out = L;
+  return SKB_OK;
+}
+
+struct StageTimer {
+  skb_layer* L;
+  bool on;
+  cudaStream_t s;
+  int i = 0;
+  void mark() {
+    if (on) cudaEventRecord(L->ev[i++], s);
+  }
+};
+
+// Enqueues every stage of one forward on `stream`.  x/y (and masks in MASKED mode) are device
+// pointers.  No allocation, no synchronisation.
+int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, float* d_y,
+                 const uint8_t* d_mask_r, const uint8_t* d_mask_s, uint8_t* d_mask_out_r,
+                 uint8_t* d_mask_out_s, cudaStream_t stream, bool timing) {
+  const Geometry& g = L->g;
+  const int B = a->batch;
+  const int BK = B * g.K;
+  const int rows = BK + (g.has_shared ? B : 0);
+  LaunchCtx ctx{stream, !timing && !(a->flags & SKB_FLAG_NO_PDL)};
+  StageTimer tm{L, timing, stream};
+  int launches = 0;
+
+  // tile size for the grouped GEMM: ~1.5x the mean tokens per expert, power of two in [16, 256]
+  int tn = 16;
+  {
+    const double want = 1.5 * static_cast<double>(BK) / g.E;
+    while (tn < 256 && tn < want) tn <<= 1;
+  }
+  int tn_idx = 0;
+  while (kTileCases[tn_idx] != tn) ++tn_idx;
+  const int max_tiles = max_tiles_for(g, B, tn);
+
+  tm.mark();
+  launches += launch_router_logits(ctx, d_x, L->d_router, B, g.E, g.D,
+                                   (a->flags & SKB_FLAG_FAST_ROUTER) != 0, L->d_logits);
+  launches += launch_route_topk(ctx, L->d_logits, B, g.E, g.K, g.renorm, L->d_ids, L->d_wts);
+  tm.mark();
+  launches += launch_dispatch(ctx, L->d_ids, B, g.K, g.E, g.has_shared, tn, L->disp);
+  launches += launch_permute_tokens(ctx, d_x, L->disp.perm, B, g.K, g.D, g.Dp, g.has_shared,
+                                    L->d_xs);
+  tm.mark();
+  if (a->flags & SKB_FLAG_SIMT_GATEUP)
+    launches += launch_gateup_simt(ctx, L->d_wgu, L->d_xs, L->disp.row_expert, rows, g, L->d_h);
+  else
+    launches += launch_gateup_tc(ctx, &L->tmap_w, &L->tmap_x[tn_idx], tn, L->disp, max_tiles, g,
+                                 L->d_h);
+  tm.mark();
+
+  SelectArgs sa{};
+  sa.h = L->d_h;
+  sa.rows = rows;
+  sa.BK = BK;
+  sa.N = g.N;
+  sa.S = g.S;
+  sa.Nh = g.Nh;
+  sa.K = g.K;
+  sa.perm = L->disp.perm;
+  sa.kept_idx = L->d_kidx;
+  sa.kept_val = L->d_kval;
+  sa.kept_cnt = L->d_kcnt;
+  sa.mask_out_routed = d_mask_out_r;
+  sa.mask_out_shared = d_mask_out_s;
+  int max_keep = g.N > g.S ? g.N : g.S;
+  if (a->mode == SKB_MODE_DENSE) {
+    sa.mode = kSelectAll;
+  } else if (a->mode == SKB_MODE_TOPK) {
+    sa.mode = kSelectTopk;
+    sa.n_off_routed = n_off_of(a->s_routed, g.N);
+    sa.n_off_shared = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
+    const int kr = g.N - sa.n_off_routed, ks = g.S - sa.n_off_shared;
+    max_keep = kr > ks ? kr : ks;
+  } else {
+    sa.mode = kSelectGiven;
+    sa.mask_in_routed = d_mask_r;
+    sa.mask_in_shared = d_mask_s;
+  }
+  launches += launch_select(ctx, sa);
+  tm.mark();
+
+  DownArgs da{};
+  da.wd = L->d_wd;
+  da.wd_shared = L->d_wd_shared;
+  da.row_expert = L->disp.row_expert;
+  da.kept_idx = L->d_kidx;
+  da.kept_val = L->d_kval;
+  da.kept_cnt = L->d_kcnt;
+  da.rows = rows;
+  da.max_keep = max_keep;
+  da.partial = L->d_part;
+  da.n_chunks = L->n_chunks;
+  launches += launch_down(ctx, da, g);
+  tm.mark();
+  launches += launch_combine(ctx, L->d_part, L->n_chunks, L->disp.inv, L->d_kcnt, L->d_wts, B, g,
+                             d_y);
+  tm.mark();
+  L->last_launches = launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SKB_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
+int check_args(const skb_layer* L, const skb_forward_args* a) {
+  if (L == nullptr) return fail(SKB_EINTERNAL, "layer is null");
+  if (a == nullptr) return fail(SKB_EINTERNAL, "args is null");
+  const Geometry& g = L->g;
+  if (a->x == nullptr || a->y == nullptr) return fail(SKB_ESHAPE, "forward: x and y must be non-null");
+  if (a->batch < 1) return fail(SKB_ESHAPE, "route: empty batch");  // router.cpp:16-18
+  if (a->mode != SKB_MODE_DENSE && a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_MASKED)
+    return fail(SKB_ECONFIG, "forward: unknown mode %d", a->mode);
+  if (a->mode == SKB_MODE_MASKED) {
+    // engine.cpp:107-117
+    const uint64_t want = static_cast<uint64_t>(a->batch) * g.K * g.N;
+    if (a->routed_mask_in == nullptr || a->routed_mask_len != want)
+      return fail(SKB_ESHAPE, "forward_masked_dense: routed masks must be B*K*d_ffn");
+    if (a->shared_mask_len != 0 &&
+        (a->shared_mask_in == nullptr ||
+         a->shared_mask_len != static_cast<uint64_t>(a->batch) * static_cast<uint64_t>(g.S)))
+      return fail(SKB_ESHAPE, "forward_masked_dense: shared masks must be B*d_shared");
+  }
+  if (a->mode == SKB_MODE_TOPK) {
+    // SparsityLevel, activation.hpp:18-22
+    if (!(a->s_routed >= 0.0 && a->s_routed <= 1.0) || !(a->s_shared >= 0.0 && a->s_shared <= 1.0))
+      return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
+  }
+  return SKB_OK;
+}
+
+void fill_report(const skb_layer* L, const skb_forward_args* a, skb_report* r,
+                 const uint8_t* host_routed_mask, const uint8_t* host_shared_mask) {
+  if (r == nullptr) return;
+  const Geometry& g = L->g;
+  const uint64_t B = a->batch, K = g.K, D = g.D, N = g.N, S = g.S, E = g.E;
+  const uint64_t routed_neurons = B * K * N;
+  std::memset(r, 0, sizeof(*r));
+  uint64_t active = routed_neurons, active_sh = B * S;
+  if (a->mode == SKB_MODE_TOPK) {
+    active = B * K * (N - n_off_of(a->s_routed, g.N));
+    if (g.has_shared) active_sh = B * (S - n_off_of(a->s_shared, g.S));
+  } else if (a->mode == SKB_MODE_MASKED && host_routed_mask != nullptr) {
+    active = 0;
+    for (uint64_t i = 0; i < routed_neurons; ++i) active += host_routed_mask[i] ? 1 : 0;
+    if (host_shared_mask != nullptr) {
+      active_sh = 0;
+      for (uint64_t i = 0; i < B * S; ++i) active_sh += host_shared_mask[i] ? 1 : 0;
+    }
+  }
+  r->gate_macs = B * K * D * N;
+  r->up_macs = B * K * D * N;
+  r->other_macs = B * E * D;
+  if (a->mode == SKB_MODE_TOPK) {
+    // executed work: only surviving W_down rows are touched
+    r->down_macs = active * D;
+    if (g.has_shared) r->other_macs += B * 2 * S * D + active_sh * D;
+    r->path_used = 1;
+  } else {
+    // forward_dense / forward_masked_dense charge full dense MACs (engine.hpp:41-42)
+    r->down_macs = B * K * D * N;
+    if (g.has_shared) r->other_macs += B * 3 * S * D;
+    r->path_used = 0;
+  }
+  r->active_neurons_total = active;
+  r->achieved_routed_sparsity =
+      1.0 - static_cast<double>(active) / static_cast<double>(routed_neurons);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skb_last_error(void) { return g_err.c_str(); }
+int skb_abi_version(void) { return SKB_ABI_VERSION; }
+
+int skb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int skb_config_validate(const skb_config* cfg) { return validate_cfg(cfg); }
+
+int skb_n_off(double s, int n, int32_t* out) {
+  if (!(s >= 0.0 && s <= 1.0)) return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
+  if (n < 0 || out == nullptr) return fail(SKB_ESHAPE, "n_off: bad arguments");
+  *out = n_off_of(s, n);
+  return SKB_OK;
+}
+
+int skb_layer_create(const skb_config* cfg, const float* router, const float* const* gate,
+                     const float* const* up, const float* const* down_t, const float* shared_gate,
+                     const float* shared_up, const float* shared_down_t, int device,
+                     skb_layer** out) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (router == nullptr || gate == nullptr || up == nullptr || down_t == nullptr)
+    return fail(SKB_ESHAPE, "layer_create: router/gate/up/down_t must be non-null");
+  if (cfg->has_shared && (shared_gate == nullptr || shared_up == nullptr || shared_down_t == nullptr))
+    return fail(SKB_ESHAPE, "layer_create: shared matrices missing while has_shared is set");
+  skb_layer* L = nullptr;
+  rc = new_layer(cfg, device, &L);
+  if (rc) return rc;
+  const Geometry& g = L->g;
+  const int rmax = g.N > g.S ? g.N : g.S;
+  float *sa = nullptr, *sb = nullptr;  // fp32 staging for one matrix pair
+  const size_t mat = static_cast<size_t>(rmax) * g.D;
+  if ((rc = dmalloc(&sa, mat)) || (rc = dmalloc(&sb, mat))) {
+    if (sa) cudaFree(sa);
+    skb_layer_destroy(L);
+    return rc;
+  }
+  cudaError_t e = cudaMemcpyAsync(L->d_router, router, static_cast<size_t>(g.E) * g.D * 4,
+                                  cudaMemcpyHostToDevice, L->stream);
+  for (int ex = 0; ex < g.E && e == cudaSuccess; ++ex) {
+    const size_t bytes = static_cast<size_t>(g.N) * g.D * 4;
+    e = cudaMemcpyAsync(sa, gate[ex], bytes, cudaMemcpyHostToDevice, L->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sb, up[ex], bytes, cudaMemcpyHostToDevice, L->stream);
+    launch_pack_gateup(L->stream, sa, sb, g.N, g.D, g.Dp,
+                       L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sa, down_t[ex], bytes, cudaMemcpyHostToDevice, L->stream);
+    launch_pack_rows(L->stream, sa, g.N, g.D, g.Dp, L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
+  }
+  if (g.has_shared && e == cudaSuccess) {
+    const size_t bytes = static_cast<size_t>(g.S) * g.D * 4;
+    e = cudaMemcpyAsync(sa, shared_gate, bytes, cudaMemcpyHostToDevice, L->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sb, shared_up, bytes, cudaMemcpyHostToDevice, L->stream);
+    launch_pack_gateup(L->stream, sa, sb, g.S, g.D, g.Dp,
+                       L->d_wgu + static_cast<size_t>(g.E) * 2 * g.Np * g.Dp);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sa, shared_down_t, bytes, cudaMemcpyHostToDevice, L->stream);
+    launch_pack_rows(L->stream, sa, g.S, g.D, g.Dp, L->d_wd_shared);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaFree(sa);
+  cudaFree(sb);
+  if (e != cudaSuccess) {
+    skb_layer_destroy(L);
+    return fail(SKB_ECUDA, "layer_create: upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = L;
+  return SKB_OK;
+}
+
+int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale, int device,
+                               skb_layer** out) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!(scale > 0.0f)) return fail(SKB_ECONFIG, "scale must be > 0");  // model.cpp:132-134
+  skb_layer* L = nullptr;
+  rc = new_layer(cfg, device, &L);
+  if (rc) return rc;
+  const Geometry& g = L->g;
+  const uint64_t ED = static_cast<uint64_t>(g.E) * g.D;
+  const uint64_t ND = static_cast<uint64_t>(g.N) * g.D;
+  const uint64_t SD = static_cast<uint64_t>(g.S) * g.D;
+  launch_synth_f32(L->stream, seed, scale, 0, ED, L->d_router);
+  for (int ex = 0; ex < g.E; ++ex) {
+    const uint64_t base = ED + static_cast<uint64_t>(ex) * 3 * ND;
+    launch_synth_gateup(L->stream, seed, scale, base, base + ND, g.N, g.Np, g.D, g.Dp,
+                        L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
+    launch_synth_rows_bf16(L->stream, seed, scale, base + 2 * ND, g.N, g.Np, g.D, g.Dp,
+                           L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
+  }
+  if (g.has_shared) {
+    const uint64_t base = ED + static_cast<uint64_t>(g.E) * 3 * ND;
+    launch_synth_gateup(L->stream, seed, scale, base, base + SD, g.S, g.Sp, g.D, g.Dp,
+                        L->d_wgu + static_cast<size_t>(g.E) * 2 * g.Np * g.Dp);
+    launch_synth_rows_bf16(L->stream, seed, scale, base + 2 * SD, g.S, g.Sp, g.D, g.Dp,
+                           L->d_wd_shared);
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    skb_layer_destroy(L);
+    return fail(SKB_ECUDA, "layer_create_synthetic failed: %s", cudaGetErrorString(e));
+  }
+  *out = L;
+  return SKB_OK;
+}
+
+void skb_layer_destroy(skb_layer* L) {
+  if (L == nullptr) return;
+  cudaSetDevice(L->device);
+  if (L->stream) cudaStreamSynchronize(L->stream);
+  free_workspace(L);
+  if (L->d_router) cudaFree(L->d_router);
+  if (L->d_wgu) cudaFree(L->d_wgu);
+  if (L->d_wd) cudaFree(L->d_wd);
+  for (auto& ev : L->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (L->stream) cudaStreamDestroy(L->stream);
+  delete L;
+}
+
+int skb_layer_reserve(skb_layer* L, int max_batch) {
+  if (L == nullptr) return fail(SKB_EINTERNAL, "layer is null");
+  if (max_batch < 1) return fail(SKB_ESHAPE, "reserve: max_batch must be >= 1");
+  std::lock_guard<std::mutex> lk(L->mu);
+  return reserve_locked(L, max_batch);
+}
+
+int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* report) {
+  int rc = check_args(L, a);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(L->mu);
+  SKB_CUDA(cudaSetDevice(L->device));
+  rc = reserve_locked(L, a->batch);
+  if (rc) return rc;
+  const Geometry& g = L->g;
+  const size_t B = a->batch, BK = B * g.K;
+  cudaStream_t s = L->stream;
+  SKB_CUDA(cudaMemcpyAsync(L->d_x, a->x, B * g.D * 4, cudaMemcpyHostToDevice, s));
+  const uint8_t *mr = nullptr, *ms = nullptr;
+  if (a->mode == SKB_MODE_MASKED) {
+    SKB_CUDA(cudaMemcpyAsync(L->d_mask_in_r, a->routed_mask_in, BK * g.N, cudaMemcpyHostToDevice, s));
+    mr = L->d_mask_in_r;
+    if (a->shared_mask_len != 0 && g.has_shared) {
+      SKB_CUDA(cudaMemcpyAsync(L->d_mask_in_s, a->shared_mask_in, B * g.S, cudaMemcpyHostToDevice, s));
+      ms = L->d_mask_in_s;
+    }
+  }
+  const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
+  rc = forward_core(L, a, L->d_x, L->d_y, mr, ms, a->routed_mask_out ? L->d_mask_out_r : nullptr,
+                    (a->shared_mask_out && g.has_shared) ? L->d_mask_out_s : nullptr, s, timing);
+  if (rc) return rc;
+  SKB_CUDA(cudaMemcpyAsync(a->y, L->d_y, B * g.D * 4, cudaMemcpyDeviceToHost, s));
+  if (a->ids_out) SKB_CUDA(cudaMemcpyAsync(a->ids_out, L->d_ids, BK * 4, cudaMemcpyDeviceToHost, s));
+  if (a->weights_out)
+    SKB_CUDA(cudaMemcpyAsync(a->weights_out, L->d_wts, BK * 4, cudaMemcpyDeviceToHost, s));
+  if (a->routed_mask_out)
+    SKB_CUDA(cudaMemcpyAsync(a->routed_mask_out, L->d_mask_out_r, BK * g.N, cudaMemcpyDeviceToHost, s));
+  if (a->shared_mask_out && g.has_shared)
+    SKB_CUDA(cudaMemcpyAsync(a->shared_mask_out, L->d_mask_out_s, B * g.S, cudaMemcpyDeviceToHost, s));
+  std::vector<float> hbuf;
+  std::vector<int32_t> inv;
+  if (a->h_routed_out || (a->h_shared_out && g.has_shared)) {
+    const size_t rows = BK + (g.has_shared ? B : 0);
+    hbuf.resize(rows * g.Nh);
+    inv.resize(BK);
+    SKB_CUDA(cudaMemcpyAsync(hbuf.data(), L->d_h, rows * g.Nh * 4, cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaMemcpyAsync(inv.data(), L->disp.inv, BK * 4, cudaMemcpyDeviceToHost, s));
+  }
+  SKB_CUDA(cudaStreamSynchronize(s));
+  if (a->h_routed_out)
+    for (size_t i = 0; i < BK; ++i)
+      std::memcpy(a->h_routed_out + i * g.N, hbuf.data() + static_cast<size_t>(inv[i]) * g.Nh,
+                  static_cast<size_t>(g.N) * 4);
+  if (a->h_shared_out && g.has_shared)
+    for (size_t t = 0; t < B; ++t)
+      std::memcpy(a->h_shared_out + t * g.S, hbuf.data() + (BK + t) * g.Nh,
+                  static_cast<size_t>(g.S) * 4);
+  if (timing) {
+    for (int i = 0; i < SKB_N_STAGES; ++i) cudaEventElapsedTime(&L->stage_ms[i], L->ev[i], L->ev[i + 1]);
+    L->have_stage_ms = true;
+  }
+  fill_report(L, a, report, a->routed_mask_in,
+              (a->shared_mask_len != 0) ? a->shared_mask_in : nullptr);
+  return SKB_OK;
+}
+
+int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stream,
+                             skb_report* report) {
+  int rc = check_args(L, a);
+  if (rc) return rc;
+  if (a->batch > L->cap_batch)
+    return fail(SKB_ESHAPE, "forward_device: batch %d exceeds reserved capacity %d; call skb_layer_reserve",
+                a->batch, L->cap_batch);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : L->stream;
+  rc = forward_core(L, a, a->x, a->y, a->mode == SKB_MODE_MASKED ? a->routed_mask_in : nullptr,
+                    (a->mode == SKB_MODE_MASKED && a->shared_mask_len) ? a->shared_mask_in : nullptr,
+                    nullptr, nullptr, s, false);
+  if (rc) return rc;
+  fill_report(L, a, report, nullptr, nullptr);
+  return SKB_OK;
+}
+
+int skb_layer_stage_times(skb_layer* L, float* ms) {
+  if (L == nullptr || ms == nullptr) return fail(SKB_EINTERNAL, "stage_times: null argument");
+  if (!L->have_stage_ms) return fail(SKB_EINTERNAL, "stage_times: no timed forward yet");
+  std::memcpy(ms, L->stage_ms, sizeof(L->stage_ms));
+  return SKB_OK;
+}
+
+int skb_layer_last_launches(skb_layer* L) { return L ? L->last_launches : 0; }
+uint64_t skb_layer_weight_bytes(skb_layer* L) { return L ? L->weight_bytes : 0; }
+
+// ---- stage entry points ----------------------------------------------------------------------
+
+static int stage_device_ready() {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(SKB_ECUDA, "no CUDA device: this library has no CPU path");
+  }
+  return SKB_OK;
+}
+
+int skb_route(const float* logits, int batch, int n_experts, int top_k, int renormalize,
+              int32_t* ids, float* weights) {
+  if (batch < 1) return fail(SKB_ESHAPE, "route: empty batch");
+  if (top_k < 1 || top_k > n_experts)
+    return fail(SKB_ECONFIG, "route: top_k=%d outside [1, %d]", top_k, n_experts);
+  if (n_experts > kMaxExperts)
+    return fail(SKB_ECONFIG, "route: n_experts=%d exceeds the device router limit %d", n_experts,
+                kMaxExperts);
+  if (logits == nullptr || ids == nullptr || weights == nullptr)
+    return fail(SKB_ESHAPE, "route: null buffer");
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  const size_t BE = static_cast<size_t>(batch) * n_experts, BK = static_cast<size_t>(batch) * top_k;
+  float *dl = nullptr, *dw = nullptr;
+  int32_t* di = nullptr;
+  if ((rc = dmalloc(&dl, BE)) || (rc = dmalloc(&dw, BK)) || (rc = dmalloc(&di, BK))) return rc;
+  cudaMemcpy(dl, logits, BE * 4, cudaMemcpyHostToDevice);
+  LaunchCtx ctx{nullptr, false};
+  launch_route_topk(ctx, dl, batch, n_experts, top_k, renormalize, di, dw);
+  cudaMemcpy(ids, di, BK * 4, cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaMemcpy(weights, dw, BK * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dl);
+  cudaFree(dw);
+  cudaFree(di);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "route: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
+int skb_align_dispatch(const int32_t* ids, int batch, int top_k, int n_experts, int block,
+                       int32_t* sorted_out, int32_t* expert_of_block, int32_t* n_padded,
+                       int32_t* n_blocks) {
+  if (block < 1) return fail(SKB_ECONFIG, "align_dispatch: block must be >= 1");
+  if (batch < 0 || top_k < 1 || n_experts < 1 || n_experts > kMaxExperts)
+    return fail(SKB_ESHAPE, "align_dispatch: bad shape");
+  const size_t BK = static_cast<size_t>(batch) * top_k;
+  for (size_t i = 0; i < BK; ++i)
+    if (ids[i] < 0 || ids[i] >= n_experts)
+      return fail(SKB_EINDEX, "align_dispatch: expert id %d outside [0, %d)", ids[i], n_experts);
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  DispatchBuffers d{};
+  int32_t *dids = nullptr, *dsorted = nullptr, *deob = nullptr, *dcounts = nullptr;
+  const size_t cap = BK + static_cast<size_t>(n_experts) * (block - 1) + 1;
+  const size_t max_tiles = static_cast<size_t>(n_experts) + BK / 16 + 2;
+  if ((rc = dmalloc(&dids, BK)) || (rc = dmalloc(&d.perm, BK)) || (rc = dmalloc(&d.inv, BK)) ||
+      (rc = dmalloc(&d.row_expert, BK)) || (rc = dmalloc(&d.expert_off, (size_t)n_experts + 2)) ||
+      (rc = dmalloc(&d.tile_expert, max_tiles)) || (rc = dmalloc(&d.tile_row0, max_tiles)) ||
+      (rc = dmalloc(&d.tile_nrows, max_tiles)) || (rc = dmalloc(&d.n_tiles, 1)) ||
+      (rc = dmalloc(&dsorted, cap)) || (rc = dmalloc(&deob, cap)) || (rc = dmalloc(&dcounts, 2)))
+    return rc;
+  cudaMemcpy(dids, ids, BK * 4, cudaMemcpyHostToDevice);
+  LaunchCtx ctx{nullptr, false};
+  launch_dispatch(ctx, dids, batch, top_k, n_experts, 0, 16, d);
+  launch_plan_export(ctx, d.perm, d.expert_off, n_experts, block, dsorted, deob, dcounts);
+  int32_t counts[2] = {0, 0};
+  cudaError_t e = cudaMemcpy(counts, dcounts, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && counts[0] > 0)
+    e = cudaMemcpy(sorted_out, dsorted, static_cast<size_t>(counts[0]) * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && counts[1] > 0)
+    e = cudaMemcpy(expert_of_block, deob, static_cast<size_t>(counts[1]) * 4, cudaMemcpyDeviceToHost);
+  void* ptrs[] = {dids, d.perm, d.inv, d.row_expert, d.expert_off, d.tile_expert, d.tile_row0,
+                  d.tile_nrows, d.n_tiles, dsorted, deob, dcounts};
+  for (void* p : ptrs) cudaFree(p);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "align_dispatch: %s", cudaGetErrorString(e));
+  *n_padded = counts[0];
+  *n_blocks = counts[1];
+  return SKB_OK;
+}
+
+int skb_combine(const float* slot_outputs, const float* weights, int batch, int top_k, int d_model,
+                float* y) {
+  if (batch < 1 || top_k < 1 || d_model < 1) return fail(SKB_ESHAPE, "combine: bad shape");
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  const size_t BK = static_cast<size_t>(batch) * top_k;
+  float *ds = nullptr, *dw = nullptr, *dy = nullptr;
+  if ((rc = dmalloc(&ds, BK * d_model)) || (rc = dmalloc(&dw, BK)) ||
+      (rc = dmalloc(&dy, static_cast<size_t>(batch) * d_model)))
+    return rc;
+  cudaMemcpy(ds, slot_outputs, BK * d_model * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dw, weights, BK * 4, cudaMemcpyHostToDevice);
+  LaunchCtx ctx{nullptr, false};
+  launch_combine_slots(ctx, ds, dw, batch, top_k, d_model, dy);
+  cudaError_t e = cudaMemcpy(y, dy, static_cast<size_t>(batch) * d_model * 4, cudaMemcpyDeviceToHost);
+  cudaFree(ds);
+  cudaFree(dw);
+  cudaFree(dy);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "combine: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
+int skb_mask_smallest(const float* h, int rows, int n, const int32_t* counts, uint8_t* mask,
+                      int32_t* kept_idx, int32_t* kept_count) {
+  if (rows < 1 || n < 1) return fail(SKB_ESHAPE, "mask_smallest: rows and n must be >= 1");
+  if (h == nullptr || counts == nullptr || mask == nullptr)
+    return fail(SKB_ESHAPE, "mask_smallest: null buffer");
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  const size_t total = static_cast<size_t>(rows) * n;
+  float* dh = nullptr;
+  int32_t *dc = nullptr, *dki = nullptr, *dkc = nullptr;
+  uint8_t* dm = nullptr;
+  if ((rc = dmalloc(&dh, total)) || (rc = dmalloc(&dc, (size_t)rows)) || (rc = dmalloc(&dki, total)) ||
+      (rc = dmalloc(&dkc, (size_t)rows)) || (rc = dmalloc(&dm, total)))
+    return rc;
+  cudaMemcpy(dh, h, total * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dc, counts, static_cast<size_t>(rows) * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dki, 0xFF, total * 4);
+  SelectArgs sa{};
+  sa.h = dh;
+  sa.rows = rows;
+  sa.BK = rows;
+  sa.N = n;
+  sa.S = 0;
+  sa.Nh = n;
+  sa.K = 1;
+  sa.mode = kSelectTopk;
+  sa.counts = dc;
+  sa.mask_out_routed = dm;
+  sa.kept_idx = dki;
+  sa.kept_cnt = dkc;
+  LaunchCtx ctx{nullptr, false};
+  launch_select(ctx, sa);
+  cudaError_t e = cudaMemcpy(mask, dm, total, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && kept_idx) e = cudaMemcpy(kept_idx, dki, total * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && kept_count)
+    e = cudaMemcpy(kept_count, dkc, static_cast<size_t>(rows) * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  cudaFree(dc);
+  cudaFree(dki);
+  cudaFree(dkc);
+  cudaFree(dm);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "mask_smallest: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
+int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask) {
+  if (!(s >= 0.0 && s <= 1.0)) return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
+  if (rows < 1 || n < 1) return fail(SKB_ESHAPE, "topk_mask: rows and n must be >= 1");
+  std::vector<int32_t> counts(static_cast<size_t>(rows), n_off_of(s, n));
+  return skb_mask_smallest(h, rows, n, counts.data(), mask, nullptr, nullptr);
+}
+
+}  // extern "C"

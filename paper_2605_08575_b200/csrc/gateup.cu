@@ -1,0 +1,385 @@
+// gateup.cu -- subsystem (2): the gate/up projection as a grouped bf16 GEMM on tcgen05 with
+// TMEM accumulators, fed by TMA, SwiGLU fused into the epilogue.
+//
+// Replaces the per-slot matvec pair + swiglu_rows of the reference
+// (proj/src/engine.cpp:147-149, proj/src/linalg.cpp:22-40, proj/src/activation.cpp:15-29).
+//
+// Shape of the contraction ("swap-AB"): for one expert e and one tile of TN token rows,
+//     D[128, TN] = A[128, Dp] * B[TN, Dp]^T
+//   A = 128 rows of the interleaved gate/up image of e (64 neurons: per TMEM lane quarter,
+//       16 gate rows then 16 up rows), K-major, streamed once from HBM by TMA;
+//   B = TN rows of the expert-sorted bf16 token matrix xs, K-major (L2 resident);
+//   D = fp32 accumulator in TMEM: lane = image row, column = token.
+// Neurons sit on the UMMA M axis so that a decode batch (1..256 tokens per expert) uses
+// UMMA N = 16..256 without padding the weight stream; the kernel is HBM-bound at decode sizes
+// and the design goal is bytes in flight per SM (8 stages x 18-24 KB), not tensor occupancy.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
+// warps 2-5 epilogue (TMEM lane quarter = warp_idx % 4).
+#include "skb_internal.cuh"
+
+namespace skb {
+
+namespace {
+
+constexpr int kGateupThreads = 192;
+constexpr int kATileBytes = 128 * kBlockK * 2;  // 16 KB: 128 rows x 128 B
+
+__host__ __device__ constexpr int b_tile_bytes(int tn) { return tn * kBlockK * 2; }
+__host__ __device__ constexpr int stage_bytes(int tn) { return kATileBytes + b_tile_bytes(tn); }
+__host__ __device__ constexpr int num_stages(int tn) {
+  return tn <= 32 ? 10 : (tn <= 64 ? 8 : (tn <= 128 ? 6 : 4));
+}
+__host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
+__host__ __device__ constexpr int gateup_smem_bytes(int tn) {
+  return num_stages(tn) * stage_bytes(tn) + 1024 /*alignment slack*/ + 256 /*barriers*/;
+}
+
+// ---- PTX wrappers -----------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra WAIT_DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "WAIT_DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+// 2D tiled TMA load: coordinate c0 = element along the contiguous (K) axis, c1 = row.
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, int c0, int c1,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+constexpr uint64_t kPolicyEvictFirst = 0x12F0000000000000ull;  // weights: streamed once
+constexpr uint64_t kPolicyEvictLast = 0x14F0000000000000ull;   // token tile: re-read by N/64 CTAs
+
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, bf16 inputs, fp32 accumulate, one CTA.
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// mbarrier arrive once every previously issued tcgen05.mma of this thread has completed
+// (implies tcgen05.fence::before_thread_sync).
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+// 32 lanes x 16 consecutive fp32 columns: thread i of the warp gets lane (base_lane + i).
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major, 128-byte-swizzled shared-memory operand descriptor (sm_100 "version 1"):
+//   [0,14) start address >> 4; [16,30) leading byte offset >> 4 (unused for swizzled K-major: 1);
+//   [32,46) stride byte offset >> 4 = 1024 B between 8-row groups; [46,48) version = 1;
+//   [61,64) layout = 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t make_smem_desc_sw128(uint32_t smem_addr) {
+  uint64_t desc = 0;
+  desc |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  desc |= static_cast<uint64_t>(1) << 16;
+  desc |= static_cast<uint64_t>(1024 >> 4) << 32;
+  desc |= static_cast<uint64_t>(1) << 46;
+  desc |= static_cast<uint64_t>(2) << 61;
+  return desc;
+}
+// kind::f16 instruction descriptor: D fp32 (bit 4), A bf16 (bit 7), B bf16 (bit 10), both
+// K-major (bits 15/16 = 0), N >> 3 at [17,23), M >> 4 at [24,29).
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+
+}  // namespace
+
+template <int TN>
+__global__ void __launch_bounds__(kGateupThreads, 1)
+gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                        const __grid_constant__ CUtensorMap tmap_x,
+                        const int32_t* __restrict__ tile_expert,
+                        const int32_t* __restrict__ tile_row0,
+                        const int32_t* __restrict__ tile_nrows,
+                        const int32_t* __restrict__ n_tiles_ptr, float* __restrict__ h,
+                        int h_stride, int n_experts, int np_blocks, int sp_blocks, int N, int S,
+                        int num_k_blocks) {
+  constexpr int kStages = num_stages(TN);
+  constexpr int kStageBytes = stage_bytes(TN);
+  constexpr uint32_t kTmemCols = tmem_cols(TN);
+  constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar_base = smem_base + kStages * kStageBytes;
+  // barriers: full[kStages], empty[kStages], tmem_full; then the TMEM base address word
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (kStages + s); };
+  const uint32_t tmem_full_bar = bar_base + 8u * (2 * kStages);
+  const uint32_t tmem_ptr_addr = bar_base + 8u * (2 * kStages + 1);
+  volatile uint32_t* tmem_ptr_generic = reinterpret_cast<volatile uint32_t*>(
+      smem_raw + (tmem_ptr_addr - smem_u32(smem_raw)));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- prologue: nothing here reads memory written by the previous kernel ----
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(tmem_full_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_ptr_addr, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_generic;
+
+  pdl_wait();
+  pdl_launch_dependents();
+
+  const int tile = blockIdx.y;
+  bool active = tile < *n_tiles_ptr;
+  int e = 0, row0 = 0, nrows = 0;
+  if (active) {
+    e = tile_expert[tile];
+    row0 = tile_row0[tile];
+    nrows = tile_nrows[tile];
+    const int nblocks = (e < n_experts) ? np_blocks : sp_blocks;
+    active = static_cast<int>(blockIdx.x) < nblocks;
+  }
+
+  if (active) {
+    // first image row of this (expert, neuron block): experts hold 2*Np rows each, the shared
+    // expert's 2*Sp rows follow the routed experts
+    const int a_row = ((e < n_experts) ? e * np_blocks : n_experts * np_blocks) * 128 +
+                      static_cast<int>(blockIdx.x) * 128;
+
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int kb = 0; kb < num_k_blocks; ++kb) {
+          const int s = kb % kStages;
+          const uint32_t ph = (kb / kStages) & 1u;
+          mbar_wait(empty_bar(s), ph ^ 1u);
+          mbar_arrive_expect_tx(full_bar(s), kStageBytes);
+          const uint32_t a_smem = smem_base + s * kStageBytes;
+          tma_load_2d(a_smem, &tmap_w, kb * kBlockK, a_row, full_bar(s), kPolicyEvictFirst);
+          tma_load_2d(a_smem + kATileBytes, &tmap_x, kb * kBlockK, row0, full_bar(s),
+                      kPolicyEvictLast);
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        for (int kb = 0; kb < num_k_blocks; ++kb) {
+          const int s = kb % kStages;
+          const uint32_t ph = (kb / kStages) & 1u;
+          mbar_wait(full_bar(s), ph);
+          tc_fence_after();
+          const uint32_t a_smem = smem_base + s * kStageBytes;
+          const uint64_t a_desc = make_smem_desc_sw128(a_smem);
+          const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes);
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k) {
+            // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
+            umma_bf16(tmem_base, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
+                      (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(empty_bar(s));
+        }
+        umma_commit(tmem_full_bar);
+      }
+    } else {
+      // ---- epilogue: TMEM -> registers -> SwiGLU -> h ----
+      const int q = warp & 3;  // TMEM lane quarter this warp may read
+      const int Ne = (e < n_experts) ? N : S;
+      const int n = static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15);
+      const bool is_gate_lane = lane < 16;
+      mbar_wait(tmem_full_bar, 0);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < TN; c0 += 16) {
+        if (c0 >= nrows) break;
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          // lanes 0-15 hold gate(n) for columns c, c+1; lanes 16-31 hold up(n).  One exchange:
+          // gate lanes finish column c, up lanes finish column c+1.
+          const float mine0 = __uint_as_float(v[c]);
+          const float mine1 = __uint_as_float(v[c + 1]);
+          const float send = is_gate_lane ? mine1 : mine0;
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+          const float g = is_gate_lane ? mine0 : recv;
+          const float u = is_gate_lane ? recv : mine1;
+          const int col = c0 + c + (is_gate_lane ? 0 : 1);
+          if (col < nrows && n < Ne)
+            h[static_cast<size_t>(row0 + col) * h_stride + n] = silu_f(g) * u;
+        }
+      }
+      tc_fence_before();
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+static int pick_tile_case(int tile_tokens) {
+  if (tile_tokens <= 16) return 16;
+  if (tile_tokens <= 32) return 32;
+  if (tile_tokens <= 64) return 64;
+  if (tile_tokens <= 128) return 128;
+  return 256;
+}
+
+template <int TN>
+static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* tmap_w,
+                           const CUtensorMap* tmap_x, const DispatchBuffers& d, int max_tiles,
+                           const Geometry& g, float* h) {
+  static bool attr_set = false;
+  constexpr int smem = gateup_smem_bytes(TN);
+  if (!attr_set) {
+    cudaFuncSetAttribute(gateup_swiglu_tc_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  cfg.stream = ctx.stream;
+  const int np_blocks = g.Np / kNeuronBlock, sp_blocks = g.Sp / kNeuronBlock;
+  cfg.gridDim = dim3(np_blocks > sp_blocks ? np_blocks : sp_blocks, max_tiles);
+  cfg.blockDim = dim3(kGateupThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchKernelEx(&cfg, gateup_swiglu_tc_kernel<TN>, *tmap_w, *tmap_x,
+                     (const int32_t*)d.tile_expert, (const int32_t*)d.tile_row0,
+                     (const int32_t*)d.tile_nrows, (const int32_t*)d.n_tiles, h, g.Nh, g.E,
+                     np_blocks, sp_blocks, g.N, g.S, g.Dp / kBlockK);
+}
+
+int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
+                     int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
+                     float* h) {
+  switch (pick_tile_case(tile_tokens)) {
+    case 16: launch_tc_case<16>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+    case 32: launch_tc_case<32>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+    case 64: launch_tc_case<64>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+    case 128: launch_tc_case<128>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+    default: launch_tc_case<256>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+  }
+  return 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Verification-only CUDA-core gate/up (SKB_FLAG_SIMT_GATEUP): one warp per (row, neuron), same
+// bf16 operands and fp32 accumulation.  Never selected implicitly; exists so that the tcgen05
+// path can be cross-checked on the device, operand for operand.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gateup_simt_kernel(const __nv_bfloat16* __restrict__ wgu,
+                                                          const __nv_bfloat16* __restrict__ xs,
+                                                          const int32_t* __restrict__ row_expert,
+                                                          int rows, Geometry g,
+                                                          float* __restrict__ h) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.y;
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int e = row_expert[row];
+  const int Ne = (e < g.E) ? g.N : g.S;
+  if (n >= Ne) return;
+  const size_t img_row0 =
+      (e < g.E) ? static_cast<size_t>(e) * 2 * g.Np : static_cast<size_t>(g.E) * 2 * g.Np;
+  const size_t blk = img_row0 + static_cast<size_t>(n / kNeuronBlock) * 128;
+  const __nv_bfloat16* wg = wgu + (blk + gateup_row(n % kNeuronBlock, 0)) * g.Dp;
+  const __nv_bfloat16* wu = wgu + (blk + gateup_row(n % kNeuronBlock, 1)) * g.Dp;
+  const __nv_bfloat16* xr = xs + static_cast<size_t>(row) * g.Dp;
+  float ag = 0.0f, au = 0.0f;
+  for (int d = lane; d < g.Dp; d += 32) {
+    const float xv = __bfloat162float(xr[d]);
+    ag = fmaf(__bfloat162float(wg[d]), xv, ag);
+    au = fmaf(__bfloat162float(wu[d]), xv, au);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ag += __shfl_xor_sync(0xffffffffu, ag, o);
+    au += __shfl_xor_sync(0xffffffffu, au, o);
+  }
+  if (lane == 0) h[static_cast<size_t>(row) * g.Nh + n] = silu_f(ag) * au;
+}
+
+int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
+                       const int32_t* row_expert, int rows, const Geometry& g, float* h) {
+  const int nmax = g.N > g.S ? g.N : g.S;
+  gateup_simt_kernel<<<dim3(ceil_div(nmax, 8), rows), 256, 0, ctx.stream>>>(wgu, xs, row_expert,
+                                                                           rows, g, h);
+  return 1;
+}
+
+}  // namespace skb

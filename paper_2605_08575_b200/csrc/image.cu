@@ -1,0 +1,102 @@
+// image.cu -- builds the device weight image.
+//
+//   router   fp32 [E][D]                         (kept in fp32: routing must match the reference)
+//   gateup   bf16 [E*2*Np + 2*Sp][Dp]            per 64-neuron block, 128 rows interleaved as
+//                                                gateup_row() describes; K-major for TMA/UMMA
+//   down     bf16 [E][Np][Dp] (+ shared [Sp][Dp]) one contiguous Dp*2-byte row per neuron,
+//                                                i.e. MoELayerWeights::down_t as stored by the
+//                                                reference (proj/include/sparsekit/model.hpp:34-43)
+//
+// The synthetic generators evaluate generate_synthetic (proj/src/model.cpp:129-166) element by
+// element with SplitMix64 jump-ahead (proj/include/sparsekit/rng.hpp:16-40): draw q of the
+// stream has state seed + (q+1)*0x9E3779B97F4A7C15.
+#include "skb_internal.cuh"
+
+namespace skb {
+
+namespace {
+
+__device__ __forceinline__ float splitmix_symmetric(uint64_t seed, uint64_t q, float scale) {
+  uint64_t z = seed + (q + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  const float u = __fmul_rn(static_cast<float>(z >> 40), 0x1.0p-24f);
+  return __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
+}
+
+__global__ void pack_gateup_kernel(const float* __restrict__ gate, const float* __restrict__ up,
+                                   int n_rows, int D, int Dp, __nv_bfloat16* __restrict__ dst) {
+  const int n = blockIdx.x;
+  const int which = blockIdx.y;
+  const float* src = (which ? up : gate) + static_cast<size_t>(n) * D;
+  const size_t img_row = static_cast<size_t>(n / kNeuronBlock) * 128 +
+                         gateup_row(n % kNeuronBlock, which);
+  __nv_bfloat16* out = dst + img_row * Dp;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) out[d] = __float2bfloat16_rn(src[d]);
+}
+
+__global__ void pack_rows_kernel(const float* __restrict__ src, int D, int Dp,
+                                 __nv_bfloat16* __restrict__ dst) {
+  const int n = blockIdx.x;
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    dst[static_cast<size_t>(n) * Dp + d] = __float2bfloat16_rn(src[static_cast<size_t>(n) * D + d]);
+}
+
+__global__ void synth_gateup_kernel(uint64_t seed, float scale, uint64_t off_gate, uint64_t off_up,
+                                    int D, int Dp, __nv_bfloat16* __restrict__ dst) {
+  const int n = blockIdx.x;
+  const int which = blockIdx.y;
+  const uint64_t off = (which ? off_up : off_gate) + static_cast<uint64_t>(n) * D;
+  const size_t img_row = static_cast<size_t>(n / kNeuronBlock) * 128 +
+                         gateup_row(n % kNeuronBlock, which);
+  __nv_bfloat16* out = dst + img_row * Dp;
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    out[d] = __float2bfloat16_rn(splitmix_symmetric(seed, off + d, scale));
+}
+
+__global__ void synth_rows_kernel(uint64_t seed, float scale, uint64_t off, int D, int Dp,
+                                  __nv_bfloat16* __restrict__ dst) {
+  const int n = blockIdx.x;
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    dst[static_cast<size_t>(n) * Dp + d] =
+        __float2bfloat16_rn(splitmix_symmetric(seed, off + static_cast<uint64_t>(n) * D + d, scale));
+}
+
+__global__ void synth_f32_kernel(uint64_t seed, float scale, uint64_t off, uint64_t count,
+                                 float* __restrict__ dst) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = splitmix_symmetric(seed, off + i, scale);
+}
+
+}  // namespace
+
+int launch_pack_gateup(cudaStream_t s, const float* gate, const float* up, int n_rows, int D,
+                       int Dp, __nv_bfloat16* dst_block_base) {
+  pack_gateup_kernel<<<dim3(n_rows, 2), 256, 0, s>>>(gate, up, n_rows, D, Dp, dst_block_base);
+  return 1;
+}
+int launch_pack_rows(cudaStream_t s, const float* src, int n_rows, int D, int Dp,
+                     __nv_bfloat16* dst) {
+  pack_rows_kernel<<<n_rows, 256, 0, s>>>(src, D, Dp, dst);
+  return 1;
+}
+int launch_synth_gateup(cudaStream_t s, uint64_t seed, float scale, uint64_t off_gate,
+                        uint64_t off_up, int n_rows, int /*n_rows_padded*/, int D, int Dp,
+                        __nv_bfloat16* dst) {
+  synth_gateup_kernel<<<dim3(n_rows, 2), 256, 0, s>>>(seed, scale, off_gate, off_up, D, Dp, dst);
+  return 1;
+}
+int launch_synth_rows_bf16(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows,
+                           int /*n_rows_padded*/, int D, int Dp, __nv_bfloat16* dst) {
+  synth_rows_kernel<<<n_rows, 256, 0, s>>>(seed, scale, off, D, Dp, dst);
+  return 1;
+}
+int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
+                     float* dst) {
+  synth_f32_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(seed, scale, off,
+                                                                             count, dst);
+  return 1;
+}
+
+}  // namespace skb

@@ -1,0 +1,145 @@
+// skb_internal.cuh -- shared declarations of the sm_100a kernels behind include/sparsekit_b200.h.
+//
+// Row space used by every stage after dispatch ("rows"):
+//   rows [0, B*K)        routed token-slots in expert-major order (the order
+//                        align_dispatch produces, proj/src/router.cpp:80-104,
+//                        without the padding entries)
+//   rows [B*K, B*K + B)  the shared expert, one row per token, when has_shared
+// perm[row] = flat slot t*K+s, inv[flat slot] = row.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skb {
+
+constexpr int kNeuronBlock = 64;   // neurons per gate/up tile (64 gate + 64 up rows = UMMA M 128)
+constexpr int kBlockK = 64;        // bf16 elements per TMA/UMMA K block (one 128-byte swizzle row)
+constexpr int kDownChunk = 128;    // kept entries per down-projection partial (8 warps x 16)
+constexpr int kDownSeg = 256;      // output columns per down-projection CTA (32 lanes x 8 bf16)
+constexpr int kSelectThreads = 256;
+constexpr int kMaxExperts = 1024;  // 32 probabilities per lane in the warp top-k
+
+__host__ __device__ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Geometry of one layer's device image.
+struct Geometry {
+  int E, K, D, N, S;
+  int has_shared, renorm;
+  int Dp;  // D rounded up to kBlockK (zero padded)
+  int Np;  // N rounded up to kNeuronBlock
+  int Sp;  // S rounded up to kNeuronBlock (0 when no shared expert)
+  int Nh;  // row stride of h / kept lists: max(Np, Sp)
+};
+
+// Per-call dispatch outputs (device pointers).
+struct DispatchBuffers {
+  int32_t* perm;         // [B*K]
+  int32_t* inv;          // [B*K]
+  int32_t* row_expert;   // [B*K + B]   expert id, E for shared rows
+  int32_t* expert_off;   // [E + 1]
+  int32_t* tile_expert;  // [max_tiles]
+  int32_t* tile_row0;    // [max_tiles]
+  int32_t* tile_nrows;   // [max_tiles]
+  int32_t* n_tiles;      // [1]
+};
+
+// ---- launchers (one per stage; each returns the number of kernels it launched) ----
+struct LaunchCtx {
+  cudaStream_t stream;
+  bool pdl;  // programmatic dependent launch between stages
+};
+
+int launch_router_logits(const LaunchCtx& ctx, const float* x, const float* router, int B, int E,
+                         int D, bool fast, float* logits);
+int launch_route_topk(const LaunchCtx& ctx, const float* logits, int B, int E, int K, int renorm,
+                      int32_t* ids, float* weights);
+int launch_dispatch(const LaunchCtx& ctx, const int32_t* ids, int B, int K, int E, int has_shared,
+                    int tile_tokens, const DispatchBuffers& d);
+int launch_permute_tokens(const LaunchCtx& ctx, const float* x, const int32_t* perm, int B, int K,
+                          int D, int Dp, int has_shared, __nv_bfloat16* xs);
+int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t* expert_off, int E,
+                       int block, int32_t* sorted_out, int32_t* expert_of_block, int32_t* counts2);
+
+int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
+                     int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
+                     float* h);
+int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
+                       const int32_t* row_expert, int rows, const Geometry& g, float* h);
+
+// select modes
+enum { kSelectTopk = 0, kSelectAll = 1, kSelectGiven = 2 };
+struct SelectArgs {
+  const float* h;  // [rows][Nh]
+  int rows, BK, N, S, Nh, K;
+  int mode;
+  int n_off_routed, n_off_shared;
+  const int32_t* counts;         // optional per-row n_off override (stage API), else NULL
+  const int32_t* perm;           // row -> flat slot (masks are slot-major); NULL = identity
+  const uint8_t* mask_in_routed; // kSelectGiven: [B*K][N] slot-major
+  const uint8_t* mask_in_shared; // kSelectGiven: [B][S] or NULL (=> keep all)
+  uint8_t* mask_out_routed;      // optional [B*K][N] slot-major
+  uint8_t* mask_out_shared;      // optional [B][S]
+  int32_t* kept_idx;             // [rows][Nh]
+  float* kept_val;               // [rows][Nh]
+  int32_t* kept_cnt;             // [rows]
+};
+int launch_select(const LaunchCtx& ctx, const SelectArgs& a);
+
+struct DownArgs {
+  const __nv_bfloat16* wd;         // [E][Np][Dp]
+  const __nv_bfloat16* wd_shared;  // [Sp][Dp] or NULL
+  const int32_t* row_expert;
+  const int32_t* kept_idx;
+  const float* kept_val;
+  const int32_t* kept_cnt;
+  int rows, max_keep;
+  float* partial;  // [rows][n_chunks][Dp]
+  int n_chunks;    // ceil(Nh / kDownChunk): partial row stride in chunks
+};
+int launch_down(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g);
+int launch_combine(const LaunchCtx& ctx, const float* partial, int n_chunks, const int32_t* inv,
+                   const int32_t* kept_cnt, const float* weights, int B, const Geometry& g,
+                   float* y);
+int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
+                         int B, int K, int D, float* y);
+
+// weight image construction
+int launch_pack_gateup(cudaStream_t s, const float* gate, const float* up, int n_rows, int D, int Dp,
+                       __nv_bfloat16* dst_block_base);
+int launch_pack_rows(cudaStream_t s, const float* src, int n_rows, int D, int Dp,
+                     __nv_bfloat16* dst);
+int launch_synth_gateup(cudaStream_t s, uint64_t seed, float scale, uint64_t off_gate,
+                        uint64_t off_up, int n_rows, int n_rows_padded, int D, int Dp,
+                        __nv_bfloat16* dst);
+int launch_synth_rows_bf16(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows,
+                           int n_rows_padded, int D, int Dp, __nv_bfloat16* dst);
+int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
+                     float* dst);
+
+// ---- device helpers ----
+#if defined(__CUDACC__)
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Position of neuron j of a 64-neuron block inside the interleaved 128-row
+// gate/up tile: 16 gate rows then 16 up rows per TMEM lane quarter, so that a
+// warp's 32 TMEM lanes hold gate (lanes 0-15) and up (lanes 16-31) of the
+// same 16 neurons.
+__host__ __device__ inline int gateup_row(int j /*0..63*/, int is_up) {
+  return 32 * (j >> 4) + 16 * is_up + (j & 15);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace skb

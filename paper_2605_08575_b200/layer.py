@@ -1,0 +1,406 @@
+"""Host-side mirror of the reference layer API over the C ABI (numpy in, numpy out).
+
+Names, argument meaning and error behaviour follow the reference headers
+(``proj/include/sparsekit/{model,router,activation,engine,profiler}.hpp``):
+``MoEConfig``, ``MoELayerWeights``, ``RouteResult``, ``MaskSet``, ``ForwardReport``,
+``SparsityLevel``, ``forward_dense``, ``forward_masked_dense``, ``route``, ``align_dispatch``,
+``combine``, ``topk_mask``, ``mask_smallest_magnitudes``, ``build_topk_masks``; plus
+``forward_topk_sparse`` -- the fused entry the reference lacks.
+
+Every function runs on the GPU through libsparsekit_b200.so; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (FLAG_FAST_ROUTER, FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,  # noqa: F401
+                   MODE_DENSE, MODE_MASKED, MODE_TOPK, STAGE_NAMES, SkbConfig, SkbForwardArgs,
+                   SkbReport)
+
+
+# ---- error types, proj/include/sparsekit/errors.hpp:12-43 ------------------------------------
+class ShapeError(ValueError):
+    pass
+
+
+class ConfigError(ValueError):
+    pass
+
+
+class IndexError_(IndexError):
+    pass
+
+
+class InternalError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERR = {_lib.SKB_ESHAPE: ShapeError, _lib.SKB_ECONFIG: ConfigError, _lib.SKB_EINDEX: IndexError_,
+        _lib.SKB_EINTERNAL: InternalError, _lib.SKB_ECUDA: CudaError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERR.get(rc, InternalError)(_lib.load().skb_last_error().decode())
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---- value types ------------------------------------------------------------------------------
+@dataclass
+class MoEConfig:
+    """proj/include/sparsekit/model.hpp:15-29"""
+    n_experts: int = 1
+    top_k: int = 1
+    d_model: int = 1
+    d_ffn: int = 1
+    has_shared: bool = False
+    d_shared: int = 0
+    renormalize: bool = True
+    align_block: int = 64
+    kTile = 64
+
+    def c(self) -> SkbConfig:
+        return SkbConfig(self.n_experts, self.top_k, self.d_model, self.d_ffn,
+                         int(self.has_shared), self.d_shared, int(self.renormalize),
+                         self.align_block)
+
+    def validate(self) -> None:
+        cfg = self.c()
+        _check(_lib.load().skb_config_validate(C.byref(cfg)))
+
+
+@dataclass
+class SparsityLevel:
+    """proj/include/sparsekit/activation.hpp:15-23"""
+    s: float = 0.0
+
+    def __post_init__(self):
+        if not (0.0 <= self.s <= 1.0):
+            raise ConfigError("sparsity must lie in [0, 1]")
+
+
+@dataclass
+class RouteResult:
+    """proj/include/sparsekit/router.hpp:20-32"""
+    batch: int
+    top_k: int
+    ids: np.ndarray      # [batch, top_k] int32
+    weights: np.ndarray  # [batch, top_k] float32
+
+
+@dataclass
+class DispatchPlan:
+    """proj/include/sparsekit/router.hpp:39-44"""
+    sorted_token_slots: np.ndarray
+    expert_of_block: np.ndarray
+    block_size: int
+    n_padded: int
+
+
+@dataclass
+class MaskSet:
+    """proj/include/sparsekit/engine.hpp:31-34"""
+    routed: np.ndarray                      # B*K*d_ffn uint8, slot-major per token
+    shared: Optional[np.ndarray] = None     # B*d_shared uint8 or None (dense shared expert)
+
+
+@dataclass
+class MacCounter:
+    gate_macs: int = 0
+    up_macs: int = 0
+    down_macs: int = 0
+    other_macs: int = 0
+
+    def total(self) -> int:
+        return self.gate_macs + self.up_macs + self.down_macs + self.other_macs
+
+
+@dataclass
+class ForwardReport:
+    """proj/include/sparsekit/engine.hpp:19-27"""
+    outputs: np.ndarray
+    macs: MacCounter
+    active_neurons_total: int = 0
+    achieved_routed_sparsity: float = 0.0
+    tiles_total: int = 0
+    tiles_skipped: int = 0
+    path_used: int = 0
+    routes: Optional[RouteResult] = None
+    masks: Optional[MaskSet] = None
+    h_routed: Optional[np.ndarray] = None
+    h_shared: Optional[np.ndarray] = None
+    stage_ms: Optional[dict] = None
+    launches: int = 0
+
+
+SWEEP_ROUTED_ONLY, SWEEP_ROUTED_AND_SHARED = 0, 1
+
+
+class MoELayerWeights:
+    """Device-resident counterpart of MoELayerWeights (proj/include/sparsekit/model.hpp:34-43).
+
+    Holds the opaque ``skb_layer*``; the bf16 weight image lives in HBM for the object's life.
+    """
+
+    def __init__(self, config: MoEConfig, handle: int):
+        self.config = config
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def from_arrays(cls, config: MoEConfig, router, gate, up, down_t, shared_gate=None,
+                    shared_up=None, shared_down_t=None, device: int = 0) -> "MoELayerWeights":
+        """gate/up/down_t: [E, N, D] arrays or sequences of E [N, D] matrices (fp32)."""
+        L = _lib.load()
+        config.validate()
+        E, N, D, S = config.n_experts, config.d_ffn, config.d_model, config.d_shared
+        keep = []
+
+        def mats(m):
+            out = []
+            for e in range(E):
+                a = np.ascontiguousarray(m[e], dtype=np.float32)
+                if a.shape != (N, D):
+                    raise ShapeError(f"expert matrix must be {N}x{D}, got {a.shape}")
+                keep.append(a)
+                out.append(a.ctypes.data)
+            return (C.c_void_p * E)(*out)
+
+        r = np.ascontiguousarray(router, dtype=np.float32)
+        if r.shape != (E, D):
+            raise ShapeError(f"router must be {E}x{D}, got {r.shape}")
+        g, u, d = mats(gate), mats(up), mats(down_t)
+        sh = [None, None, None]
+        if config.has_shared:
+            for i, m in enumerate((shared_gate, shared_up, shared_down_t)):
+                if m is None:
+                    raise ShapeError("shared matrices missing while has_shared is set")
+                sh[i] = np.ascontiguousarray(m, dtype=np.float32)
+                if sh[i].shape != (S, D):
+                    raise ShapeError(f"shared matrix must be {S}x{D}, got {sh[i].shape}")
+        cfg = config.c()
+        h = C.c_void_p()
+        _check(L.skb_layer_create(C.byref(cfg), _ptr(r), g, u, d, _ptr(sh[0]), _ptr(sh[1]),
+                                  _ptr(sh[2]), device, C.byref(h)))
+        return cls(config, h.value)
+
+    @classmethod
+    def generate_synthetic(cls, config: MoEConfig, seed: int, scale: float,
+                           device: int = 0) -> "MoELayerWeights":
+        """generate_synthetic, proj/src/model.cpp:129-166, evaluated on the device."""
+        L = _lib.load()
+        cfg = config.c()
+        h = C.c_void_p()
+        _check(L.skb_layer_create_synthetic(C.byref(cfg), seed & (2 ** 64 - 1), scale, device,
+                                            C.byref(h)))
+        return cls(config, h.value)
+
+    def reserve(self, max_batch: int) -> None:
+        _check(_lib.load().skb_layer_reserve(self._h, max_batch))
+
+    @property
+    def weight_bytes(self) -> int:
+        return int(_lib.load().skb_layer_weight_bytes(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            _lib.load().skb_layer_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device-pointer entry for the benchmark's value leg and for stream capture --
+    def forward_device(self, x_ptr: int, y_ptr: int, batch: int, mode: int = MODE_TOPK,
+                       s_routed: float = 0.0, s_shared: float = 0.0, flags: int = 0,
+                       stream: int = 0) -> None:
+        a = SkbForwardArgs()
+        a.batch, a.mode, a.flags = batch, mode, flags
+        a.s_routed, a.s_shared = s_routed, s_shared
+        a.x, a.y = x_ptr, y_ptr
+        _check(_lib.load().skb_layer_forward_device(self._h, C.byref(a), C.c_void_p(stream), None))
+
+
+def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_shared=0.0,
+             masks: Optional[MaskSet] = None, flags: int = 0, capture: bool = False,
+             y_out: Optional[np.ndarray] = None) -> ForwardReport:
+    L = _lib.load()
+    cfg = w.config
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2 or x.shape[1] != cfg.d_model:
+        # engine.cpp:98-101
+        raise ShapeError(f"forward: tokens are B x {x.shape[-1] if x.ndim else 0}, model expects "
+                         f"d_model={cfg.d_model}")
+    B, K, N, S = x.shape[0], cfg.top_k, cfg.d_ffn, cfg.d_shared
+    y = y_out if y_out is not None else np.empty((B, cfg.d_model), np.float32)
+    a = SkbForwardArgs()
+    a.batch, a.mode, a.flags = B, mode, flags
+    a.s_routed, a.s_shared = float(s_routed), float(s_shared)
+    a.x, a.y = x.ctypes.data, y.ctypes.data
+    keep = [x, y]
+    if mode == MODE_MASKED:
+        r = np.ascontiguousarray(masks.routed, dtype=np.uint8).reshape(-1)
+        a.routed_mask_in, a.routed_mask_len = r.ctypes.data, r.size
+        keep.append(r)
+        if masks.shared is not None and np.size(masks.shared) > 0:
+            sm = np.ascontiguousarray(masks.shared, dtype=np.uint8).reshape(-1)
+            a.shared_mask_in, a.shared_mask_len = sm.ctypes.data, sm.size
+            keep.append(sm)
+    cap = {}
+    if capture:
+        cap["ids"] = np.empty((B, K), np.int32)
+        cap["weights"] = np.empty((B, K), np.float32)
+        cap["routed"] = np.empty((B, K, N), np.uint8)
+        cap["h_routed"] = np.empty((B, K, N), np.float32)
+        a.ids_out, a.weights_out = cap["ids"].ctypes.data, cap["weights"].ctypes.data
+        a.routed_mask_out, a.h_routed_out = cap["routed"].ctypes.data, cap["h_routed"].ctypes.data
+        if cfg.has_shared:
+            cap["shared"] = np.empty((B, S), np.uint8)
+            cap["h_shared"] = np.empty((B, S), np.float32)
+            a.shared_mask_out, a.h_shared_out = cap["shared"].ctypes.data, cap["h_shared"].ctypes.data
+    rep = SkbReport()
+    _check(L.skb_layer_forward(w._h, C.byref(a), C.byref(rep)))
+    out = ForwardReport(
+        outputs=y, macs=MacCounter(rep.gate_macs, rep.up_macs, rep.down_macs, rep.other_macs),
+        active_neurons_total=rep.active_neurons_total,
+        achieved_routed_sparsity=rep.achieved_routed_sparsity, tiles_total=rep.tiles_total,
+        tiles_skipped=rep.tiles_skipped, path_used=rep.path_used,
+        launches=L.skb_layer_last_launches(w._h))
+    if capture:
+        out.routes = RouteResult(B, K, cap["ids"], cap["weights"])
+        out.masks = MaskSet(cap["routed"], cap.get("shared"))
+        out.h_routed, out.h_shared = cap["h_routed"], cap.get("h_shared")
+    if flags & FLAG_TIME_STAGES:
+        ms = (C.c_float * _lib.N_STAGES)()
+        _check(L.skb_layer_stage_times(w._h, ms))
+        out.stage_ms = dict(zip(STAGE_NAMES, [float(v) for v in ms]))
+    return out
+
+
+def forward_dense(w: MoELayerWeights, x, threads: int = 1, *, flags: int = 0,
+                  capture: bool = False) -> ForwardReport:
+    """engine.hpp:38-39.  `threads` is accepted for signature parity and ignored."""
+    return _forward(w, x, MODE_DENSE, flags=flags, capture=capture)
+
+
+def forward_masked_dense(w: MoELayerWeights, x, masks: MaskSet, threads: int = 1, *,
+                         flags: int = 0, capture: bool = False) -> ForwardReport:
+    """engine.hpp:43-44: dense execution with h zeroed where masked (here: rows not gathered)."""
+    return _forward(w, x, MODE_MASKED, masks=masks, flags=flags, capture=capture)
+
+
+def forward_topk_sparse(w: MoELayerWeights, x, s_routed: SparsityLevel,
+                        s_shared: Optional[SparsityLevel] = None, threads: int = 1, *,
+                        flags: int = 0, capture: bool = False, y_out=None) -> ForwardReport:
+    """== forward_masked_dense(w, x, build_topk_masks(w, x, s, mode)) with the selection done on
+    the device and masked W_down rows skipped.  s_shared=None => shared expert stays dense
+    (SweepMode::kRoutedOnly); pass the same level for kRoutedAndShared."""
+    ss = 0.0 if s_shared is None else s_shared.s
+    return _forward(w, x, MODE_TOPK, s_routed=s_routed.s, s_shared=ss, flags=flags,
+                    capture=capture, y_out=y_out)
+
+
+def build_topk_masks(w: MoELayerWeights, tokens, s: SparsityLevel,
+                     mode: int = SWEEP_ROUTED_AND_SHARED) -> MaskSet:
+    """profiler.hpp:71-72 / profiler.cpp:101-150."""
+    shared = s if (mode == SWEEP_ROUTED_AND_SHARED and w.config.has_shared) else None
+    rep = forward_topk_sparse(w, tokens, s, shared, capture=True)
+    return MaskSet(rep.masks.routed, rep.masks.shared if shared is not None else None)
+
+
+# ---- stage functions --------------------------------------------------------------------------
+def route(logits, top_k: int, renormalize: bool) -> RouteResult:
+    """router.hpp:34 / router.cpp:13-68."""
+    logits = np.ascontiguousarray(logits, dtype=np.float32)
+    if logits.ndim != 2:
+        raise ShapeError("route: logits must be batch x n_experts")
+    B, E = logits.shape
+    ids = np.empty((max(B, 0), max(top_k, 0)), np.int32)
+    wts = np.empty((max(B, 0), max(top_k, 0)), np.float32)
+    _check(_lib.load().skb_route(_ptr(logits), B, E, top_k, int(renormalize), _ptr(ids), _ptr(wts)))
+    return RouteResult(B, top_k, ids, wts)
+
+
+def align_dispatch(r: RouteResult, n_experts: int, block: int) -> DispatchPlan:
+    """router.hpp:46-47 / router.cpp:70-107."""
+    ids = np.ascontiguousarray(r.ids, dtype=np.int32).reshape(-1)
+    cap = ids.size + n_experts * max(block - 1, 0) + 1
+    sorted_out = np.empty(cap, np.int32)
+    eob = np.empty(cap, np.int32)
+    n_padded, n_blocks = C.c_int32(), C.c_int32()
+    _check(_lib.load().skb_align_dispatch(_ptr(ids), r.batch, r.top_k, n_experts, block,
+                                          _ptr(sorted_out), _ptr(eob), C.byref(n_padded),
+                                          C.byref(n_blocks)))
+    return DispatchPlan(sorted_out[:n_padded.value].copy(), eob[:n_blocks.value].copy(), block,
+                        n_padded.value)
+
+
+def combine(slot_outputs, r: RouteResult, d_model: int) -> np.ndarray:
+    """router.hpp:52-53 / router.cpp:109-132."""
+    so = np.ascontiguousarray(slot_outputs, dtype=np.float32).reshape(-1)
+    if so.size != r.batch * r.top_k * d_model:
+        raise InternalError(f"combine: got {so.size} values, expected {r.batch * r.top_k * d_model}")
+    wts = np.ascontiguousarray(r.weights, dtype=np.float32)
+    y = np.empty((r.batch, d_model), np.float32)
+    _check(_lib.load().skb_combine(_ptr(so), _ptr(wts), r.batch, r.top_k, d_model, _ptr(y)))
+    return y
+
+
+def mask_smallest_magnitudes(h, count) -> np.ndarray:
+    """activation.hpp:35-36.  h: [n] or [rows, n]; count: int or per-row sequence."""
+    h = np.ascontiguousarray(h, dtype=np.float32)
+    one = h.ndim == 1
+    h2 = h.reshape(1, -1) if one else h
+    rows, n = h2.shape
+    counts = np.ascontiguousarray(np.broadcast_to(np.asarray(count, np.int32), (rows,)))
+    mask = np.empty((rows, n), np.uint8)
+    _check(_lib.load().skb_mask_smallest(_ptr(h2), rows, n, _ptr(counts), _ptr(mask), None, None))
+    return mask[0] if one else mask
+
+
+def select_survivors(h, count):
+    """Like mask_smallest_magnitudes but also returns the ascending survivor lists the
+    down-projection consumes: (mask, kept_idx padded with -1, kept_count)."""
+    h2 = np.ascontiguousarray(h, dtype=np.float32)
+    rows, n = h2.shape
+    counts = np.ascontiguousarray(np.broadcast_to(np.asarray(count, np.int32), (rows,)))
+    mask = np.empty((rows, n), np.uint8)
+    kidx = np.empty((rows, n), np.int32)
+    kcnt = np.empty(rows, np.int32)
+    _check(_lib.load().skb_mask_smallest(_ptr(h2), rows, n, _ptr(counts), _ptr(mask), _ptr(kidx),
+                                         _ptr(kcnt)))
+    return mask, kidx, kcnt
+
+
+def topk_mask(h, s: SparsityLevel) -> np.ndarray:
+    """activation.hpp:39 / activation.cpp:54-60."""
+    h = np.ascontiguousarray(h, dtype=np.float32)
+    one = h.ndim == 1
+    h2 = h.reshape(1, -1) if one else h
+    mask = np.empty(h2.shape, np.uint8)
+    _check(_lib.load().skb_topk_mask(_ptr(h2), h2.shape[0], h2.shape[1], s.s, _ptr(mask)))
+    return mask[0] if one else mask
+
+
+def n_off(s: float, n: int) -> int:
+    out = C.c_int32()
+    _check(_lib.load().skb_n_off(s, n, C.byref(out)))
+    return out.value
+
+
+def device_count() -> int:
+    return _lib.load().skb_device_count()

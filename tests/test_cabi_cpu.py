@@ -1,0 +1,136 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every declared symbol, validates
+arguments on the host exactly like the reference, and refuses to compute without a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sparsekit_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__ as g
+    g.build()
+    from paper_2605_08575_b200 import _lib
+    return _lib
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(skb_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_symbols_are_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 15
+    L = lib.load()
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in include/sparsekit_b200.h but not exported"
+    assert sorted(lib.EXPORTS) == names
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True)
+    exported = set(re.findall(r" T (skb_\w+)", out.stdout))
+    assert exported == set(names)
+    assert L.skb_abi_version() == 1
+
+
+def test_library_does_not_link_the_oracle_or_torch(lib):
+    out = subprocess.run(["ldd", lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in out and "torch" not in out and "sparsekit_ref" not in out
+
+
+def test_struct_layouts_match_header(lib):
+    assert C.sizeof(lib.SkbConfig) == 32
+    assert C.sizeof(lib.SkbReport) == 72
+    assert C.sizeof(lib.SkbForwardArgs) == 16 + 16 + 8 * 12
+
+
+def test_config_validate_matches_reference_messages(lib):
+    # proj/src/model.cpp:113-127
+    L = lib.load()
+    cases = [
+        ((0, 1, 1, 1, 0, 0, 1, 64), "n_experts must be >= 1"),
+        ((4, 0, 1, 1, 0, 0, 1, 64), "top_k must satisfy 1 <= K <= E, got K=0 E=4"),
+        ((4, 5, 1, 1, 0, 0, 1, 64), "top_k must satisfy 1 <= K <= E, got K=5 E=4"),
+        ((4, 2, 0, 1, 0, 0, 1, 64), "d_model must be >= 1"),
+        ((4, 2, 8, 0, 0, 0, 1, 64), "d_ffn must be >= 1"),
+        ((4, 2, 8, 8, 0, -1, 1, 64), "d_shared must be >= 0"),
+        ((4, 2, 8, 8, 1, 0, 1, 64), "has_shared must match d_shared > 0"),
+        ((4, 2, 8, 8, 0, 3, 1, 64), "has_shared must match d_shared > 0"),
+        ((4, 2, 8, 8, 0, 0, 1, 0), "align_block must be >= 1"),
+    ]
+    for fields, msg in cases:
+        cfg = lib.SkbConfig(*fields)
+        assert L.skb_config_validate(C.byref(cfg)) == lib.SKB_ECONFIG
+        assert L.skb_last_error().decode() == msg
+    ok = lib.SkbConfig(4, 2, 8, 8, 1, 3, 0, 1)
+    assert L.skb_config_validate(C.byref(ok)) == lib.SKB_OK
+
+
+def test_n_off_matches_oracle(lib, oracle):
+    L = lib.load()
+    out = C.c_int32()
+    for n in list(range(0, 70)) + [511, 512, 1024, 2880, 8192]:
+        for s in (0.0, 0.1, 0.25, 0.5, 0.75, 0.9, 0.999, 1.0):
+            assert L.skb_n_off(s, n, C.byref(out)) == 0
+            assert out.value == oracle.n_off(s, n)
+    assert L.skb_n_off(1.5, 8, C.byref(out)) == lib.SKB_ECONFIG
+    assert L.skb_n_off(float("nan"), 8, C.byref(out)) == lib.SKB_ECONFIG
+
+
+def test_argument_validation_precedes_device_work(lib):
+    L = lib.load()
+    logits = np.zeros((2, 4), np.float32)
+    ids = np.zeros((2, 5), np.int32)
+    w = np.zeros((2, 5), np.float32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    assert L.skb_route(p(logits), 0, 4, 1, 1, p(ids), p(w)) == lib.SKB_ESHAPE
+    assert L.skb_route(p(logits), 2, 4, 5, 1, p(ids), p(w)) == lib.SKB_ECONFIG
+    assert b"outside [1, 4]" in L.skb_last_error()
+    bad = np.array([[0, 9]], np.int32)
+    n1, n2 = C.c_int32(), C.c_int32()
+    assert L.skb_align_dispatch(p(bad), 1, 2, 4, 4, p(ids), p(ids), C.byref(n1), C.byref(n2)) == lib.SKB_EINDEX
+    assert L.skb_align_dispatch(p(bad), 1, 2, 4, 0, p(ids), p(ids), C.byref(n1), C.byref(n2)) == lib.SKB_ECONFIG
+
+
+def test_no_cpu_fallback(lib):
+    """Without a CUDA device every compute entry point fails loudly with SKB_ECUDA."""
+    L = lib.load()
+    if L.skb_device_count() > 0:
+        pytest.skip("a GPU is present; the refusal path is exercised on CPU-only hosts")
+    cfg = lib.SkbConfig(4, 2, 8, 8, 0, 0, 1, 64)
+    h = C.c_void_p()
+    assert L.skb_layer_create_synthetic(C.byref(cfg), 1, C.c_float(0.1), 0, C.byref(h)) == lib.SKB_ECUDA
+    assert b"no CUDA device" in L.skb_last_error()
+    logits = np.zeros((2, 4), np.float32)
+    ids = np.zeros((2, 2), np.int32)
+    w = np.zeros((2, 2), np.float32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    assert L.skb_route(p(logits), 2, 4, 2, 1, p(ids), p(w)) == lib.SKB_ECUDA
+    hrow = np.zeros((1, 8), np.float32)
+    mask = np.zeros((1, 8), np.uint8)
+    assert L.skb_topk_mask(p(hrow), 1, 8, 0.5, p(mask)) == lib.SKB_ECUDA
+
+
+def test_python_mirror_validates_like_the_reference():
+    import paper_2605_08575_b200 as skb
+    with pytest.raises(skb.ConfigError):
+        skb.SparsityLevel(-0.1)
+    with pytest.raises(skb.ConfigError):
+        skb.MoEConfig(4, 9, 8, 8).validate()
+    skb.MoEConfig(4, 2, 8, 8).validate()
+    assert skb.n_off(0.5, 1024) == 512 and skb.n_off(0.9, 1024) == 922
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2605_08575_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".hpp", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "pyoracle" not in text and "moe_oracle" not in text and "libsparsekit_ref" not in text, f
