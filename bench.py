@@ -1,0 +1,506 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-layer tokens/s and achieved HBM GB/s vs intra-expert sparsity (decode).
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]`` prints
+ONE JSON line on rank 0.  A "step" is one forward of the activation-sparse MoE FFN layer over
+one batch of synthetic tokens.
+
+  value     tokens/s of the whole job with tokens resident in HBM (device entry point of the
+            C ABI, CUDA-graph replay, L2 flushed between steps, CUDA events per step).
+  e2e       the same metric through the host-buffer entry point skb_layer_forward (the call a
+            user of the reference's forward_* makes): pinned host tokens in, host outputs out,
+            H2D/D2H inside the timed region.
+  roofline  dominant kernel (gate/up grouped GEMM): algorithmic weight bytes of the launch
+             / its CUDA-event duration, against MEASURED_PEAKS.json's HBM GB/s.
+  sweep     tokens/s, layer GB/s and roofline fraction at s in {0,.25,.5,.75,.9} plus the
+            north-star point (OLMoE shape, batch 1, s=0.5).
+  cpu_baseline / --impl reference
+            the UNMODIFIED reference (oracle/_ref/libsparsekit_ref.so: build_topk_masks +
+            forward_masked_dense, the path this layer replaces) on the host cores.
+
+The oracle is imported only by the cpu_baseline / reference legs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# shape table: BASELINE.json configs (d_model / d_shared as assumed in SURVEY.md 8d)
+WORKLOADS = {
+    "olmoe": dict(name="OLMoE-1B-7B", E=64, K=8, D=2048, N=1024, S=0),
+    "granite": dict(name="Granite-1B-A400M", E=32, K=8, D=1024, N=512, S=0),
+    "qwen35": dict(name="Qwen3.5-35B-A3B", E=256, K=8, D=2048, N=512, S=512),
+    "gptoss": dict(name="GPT-OSS-20B", E=32, K=4, D=2880, N=2880, S=0),
+    "maverick": dict(name="Llama-4-Maverick", E=128, K=1, D=5120, N=8192, S=8192),
+}
+SEED, SCALE = 1, 0.05          # generate_synthetic defaults of the reference CLI (tools/main.cpp:157)
+SWEEP_S = (0.0, 0.25, 0.5, 0.75, 0.9)
+W_BYTES = 2                    # bf16 weight image
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def n_off(s, n):
+    # topk_mask, proj/src/activation.cpp:54-60
+    return int(min(max(np.floor(s * n + 0.5), 0), n))
+
+
+def make_tokens(B, D, seed):
+    """Synthetic N(0,1) tokens, rounded to bf16-representable fp32 (both arms see the same)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, D), dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).reshape(B, D)
+
+
+def algorithmic_bytes(shape, B, ids, routed_mask, shared_mask):
+    """SURVEY.md 8d, computed exactly from the realised routing and masks (integers)."""
+    E, K, D, N, S = (shape[k] for k in "EKDNS")
+    ids = np.asarray(ids).reshape(B, K)
+    routed_mask = np.asarray(routed_mask).reshape(B * K, N)
+    flat = ids.reshape(-1)
+    experts = np.unique(flat)
+    r_down = 0
+    for e in experts:
+        r_down += int(np.count_nonzero(routed_mask[flat == e].any(axis=0)))
+    router = E * D * W_BYTES
+    gateup = len(experts) * 2 * N * D * W_BYTES
+    down = r_down * D * W_BYTES
+    sh_gateup = sh_down = 0
+    if S:
+        sh_gateup = 2 * S * D * W_BYTES
+        if shared_mask is None:
+            r_sh = S
+        else:
+            r_sh = int(np.count_nonzero(np.asarray(shared_mask).reshape(B, S).any(axis=0)))
+        sh_down = r_sh * D * W_BYTES
+    io = B * D * (4 + 4)
+    return dict(total=router + gateup + down + sh_gateup + sh_down + io,
+                gateup=gateup + sh_gateup, down=down + sh_down, router=router, io=io,
+                distinct_experts=int(len(experts)), r_down=r_down)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.lines, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "50", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._pump, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+class Point:
+    """One (shape, batch, sparsity) measurement set-up on the current device."""
+
+    RING = 8
+
+    def __init__(self, skb, torch, layer, shape, B):
+        self.skb, self.torch, self.layer, self.shape, self.B = skb, torch, layer, shape, B
+        D = shape["D"]
+        self.x_host = [make_tokens(B, D, 2 + i) for i in range(self.RING)]
+        self.x_ring = [torch.from_numpy(x).cuda() for x in self.x_host]
+        self.x = torch.empty((B, D), dtype=torch.float32, device="cuda")
+        self.y = torch.empty((B, D), dtype=torch.float32, device="cuda")
+        self.flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+        layer.reserve(B)
+
+    def bytes_for(self, s):
+        """Exact algorithmic bytes per ring slot (one capture forward each; untimed)."""
+        skb, S = self.skb, self.shape["S"]
+        lvl = skb.SparsityLevel(s)
+        out = []
+        for x in self.x_host:
+            rep = skb.forward_topk_sparse(self.layer, x, lvl, lvl if S else None, capture=True)
+            out.append(algorithmic_bytes(self.shape, self.B, rep.routes.ids, rep.masks.routed,
+                                         rep.masks.shared if S else None))
+        return out
+
+    def _enqueue(self, s, flags=0):
+        S = self.shape["S"]
+        self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
+                                  mode=self.skb.MODE_TOPK, s_routed=s, s_shared=s if S else 0.0,
+                                  flags=flags,
+                                  stream=self.torch.cuda.current_stream().cuda_stream)
+
+    def time_device(self, s, steps, warmup, use_graph=True):
+        """Per-step CUDA-event times (ms) of the device entry point; L2 flushed and the token
+        batch rotated between steps, both outside the per-step event pair."""
+        torch = self.torch
+        graph = None
+        if use_graph:
+            try:
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    self._enqueue(s)  # warm (module load, attribute set) before capture
+                torch.cuda.current_stream().wait_stream(side)
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    self._enqueue(s)
+            except Exception as exc:  # capture unsupported: direct launches
+                print(f"[bench] CUDA graph capture failed ({exc}); timing direct launches",
+                      file=sys.stderr)
+                graph = None
+                torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        for i in range(warmup + steps):
+            self.x.copy_(self.x_ring[i % self.RING])
+            self.flush.zero_()
+            if i >= warmup:
+                ev[i - warmup][0].record()
+            if graph is not None:
+                graph.replay()
+            else:
+                self._enqueue(s)
+            if i >= warmup:
+                ev[i - warmup][1].record()
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in ev], graph is not None
+
+    def time_stages(self, s, steps, warmup):
+        """Per-stage CUDA-event times (ms, mean over steps), stages serialised (no PDL)."""
+        torch, skb = self.torch, self.skb
+        acc = np.zeros(len(skb.STAGE_NAMES))
+        for i in range(warmup + steps):
+            self.x.copy_(self.x_ring[i % self.RING])
+            self.flush.zero_()
+            self._enqueue(s, flags=skb.FLAG_TIME_STAGES)
+            ms = self.layer.stage_times()
+            if i >= warmup:
+                acc += np.asarray(ms)
+        return dict(zip(skb.STAGE_NAMES, (acc / steps).tolist()))
+
+    def time_e2e(self, s, steps, warmup):
+        """Wall-clock per-step times (ms) of the host-buffer entry point (H2D + stages + D2H +
+        synchronise inside), pinned host buffers, L2 flushed between steps."""
+        torch, skb, S = self.torch, self.skb, self.shape["S"]
+        D = self.shape["D"]
+        xin = [torch.from_numpy(x).pin_memory() for x in self.x_host]
+        yout = torch.empty((self.B, D), dtype=torch.float32).pin_memory()
+        lvl = skb.SparsityLevel(s)
+        times = []
+        for i in range(warmup + steps):
+            self.flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            skb.forward_topk_sparse(self.layer, xin[i % self.RING].numpy(), lvl,
+                                    lvl if S else None, y_out=yout.numpy())
+            t1 = time.perf_counter()
+            if i >= warmup:
+                times.append((t1 - t0) * 1e3)
+        return times, self.B * D * 4, self.B * D * 4
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (this layer has no CPU path)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2605_08575_b200 as skb
+
+    shape = WORKLOADS[args.workload]
+    B, s = args.batch, args.sparsity
+    hbm_peak, peak_src = peaks()
+
+    def mk_layer(sh):
+        cfg = skb.MoEConfig(sh["E"], sh["K"], sh["D"], sh["N"], sh["S"] > 0, sh["S"], True, 64)
+        return skb.MoELayerWeights.generate_synthetic(cfg, SEED, SCALE, device=local)
+
+    layer = mk_layer(shape)
+    pt = Point(skb, torch, layer, shape, B)
+    bytes_ring = pt.bytes_for(s)
+
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+
+    # ---- headline: device-resident value ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, graphed = pt.time_device(s, args.steps, args.warmup, use_graph=not args.no_graph)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B / (ms_per_step * 1e-3)
+
+    # ---- dominant kernel, live: per-stage events ----
+    stage_steps = max(10, min(args.steps, 50))
+    stages = pt.time_stages(s, stage_steps, 3)
+    launches_per_step = layer.last_launches()
+    mean_bytes = {k: float(np.mean([b[k] for b in bytes_ring])) for k in bytes_ring[0]}
+    dom = max(("gateup", "down"), key=lambda k: stages[k])
+    dom_bytes = mean_bytes[dom]
+    dom_gbs = dom_bytes / (stages[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": {"gateup": "gateup_swiglu_tc_kernel",
+                                            "down": "gather_down_kernel"}[dom],
+                "achieved": round(dom_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(dom_gbs / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": int(dom_bytes),
+                "kernel_ms": round(stages[dom], 5),
+                "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
+    layer_gbs = mean_bytes["total"] / (ms_per_step * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer entry point ----
+    e2e_steps = max(10, min(args.steps, 100))
+    e2e_times, h2d, d2h = pt.time_e2e(s, e2e_steps, args.warmup)
+    e2e_ms = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": round(world * B / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
+           "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- sparsity sweep on this workload + the north-star point ----
+    sweep = []
+    if not args.no_sweep and rank == 0:
+        sw_steps = max(20, min(args.steps, 100))
+        for ss in SWEEP_S:
+            br = bytes_ring if ss == s else pt.bytes_for(ss)
+            tms, _ = pt.time_device(ss, sw_steps, 3, use_graph=not args.no_graph)
+            m = float(np.mean(tms))
+            tot = float(np.mean([b["total"] for b in br]))
+            sweep.append({"workload": shape["name"], "batch": B, "sparsity": ss,
+                          "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
+                          "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                          "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+        if args.workload != "olmoe" or B != 1:
+            sh = WORKLOADS["olmoe"]
+            l2 = mk_layer(sh)
+            p2 = Point(skb, torch, l2, sh, 1)
+            for ss in SWEEP_S:
+                br = p2.bytes_for(ss)
+                tms, _ = p2.time_device(ss, sw_steps, 3, use_graph=not args.no_graph)
+                m = float(np.mean(tms))
+                tot = float(np.mean([b["total"] for b in br]))
+                sweep.append({"workload": sh["name"], "batch": 1, "sparsity": ss,
+                              "ms_per_step": round(m, 5), "tokens_per_s": round(1 / (m * 1e-3), 1),
+                              "bytes_alg": int(tot),
+                              "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                              "layer_frac_of_hbm_roofline":
+                                  round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
+                              **({"north_star_point": True} if ss == 0.5 else {})})
+            del p2, l2
+
+    clocks = sampler.stop() if rank == 0 else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(shape, B, s, reps=2)
+
+    if rank == 0:
+        line = {
+            "metric": "MoE-layer tokens/s (decode) at intra-expert sparsity s; HBM GB/s in roofline/sweep",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{shape['name']} shape, E={shape['E']} top-{shape['K']} "
+                                   f"d_model={shape['D']} d_ffn={shape['N']} d_shared={shape['S']}, "
+                                   f"batch {B} decode per GPU, top-k neuron selection s={s}",
+                       "sparsity": s, "batch_per_gpu": B,
+                       "weights": f"generate_synthetic(seed={SEED}, scale={SCALE}) as bf16 image",
+                       "parallelism": "single GPU" if world == 1 else f"token-sharded replicas x{world}",
+                       "l2": "512 MiB memset between steps (outside the per-step event pair) + "
+                             "ring of 8 token batches",
+                       "launch": "CUDA graph replay" if graphed else "direct launches + PDL",
+                       "accumulation": "fp32 (h kept fp32; 1e-5 parity mode)"},
+            "layer_gbs": round(layer_gbs, 1), "layer_frac_of_hbm_roofline": round(layer_gbs / hbm_peak, 4),
+            "bytes_alg_per_step": int(mean_bytes["total"]),
+            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
+            "launches_per_step": int(launches_per_step), "clocks": clocks,
+            "cpu_baseline": cpu, "sweep": sweep,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------------
+# the reference's CPU implementation (oracle/_ref, built from /root/reference unmodified)
+# ---------------------------------------------------------------------------------------------
+def _ref_layer(shape):
+    from oracle.pyoracle import Config, Ref, RefLayer
+    if not Ref.available():
+        return None, None
+    cfg = Config(shape["E"], shape["K"], shape["D"], shape["N"], shape["S"], True)
+    lay = RefLayer.synthetic(cfg, SEED, SCALE).round_bf16()
+    return lay, cfg
+
+
+def _ref_step(lay, x, s, shared, threads):
+    routed, sh = lay.build_topk_masks(x, s, 1 if shared else 0)
+    lay.forward_masked_dense(x, routed, sh, threads=threads)
+
+
+def cpu_reference(shape, B, s, reps):
+    """build_topk_masks + forward_masked_dense of the unmodified reference on the host cores."""
+    cores = os.cpu_count() or 1
+    fp32_bytes = (shape["E"] * 3 * shape["N"] + 3 * shape["S"]) * shape["D"] * 4
+    if fp32_bytes > 24 << 30:
+        return {"value": None, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                "sample": "skipped: fp32 model does not fit the bounded-sample budget"}
+    lay, _ = _ref_layer(shape)
+    if lay is None:
+        return {"value": None, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                "sample": "oracle/_ref/libsparsekit_ref.so missing"}
+    x = make_tokens(B, shape["D"], 2)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _ref_step(lay, x, s, shape["S"] > 0, cores)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": round(B / t, 2), "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "ms_per_step": round(t * 1e3, 2),
+            "sample": f"full batch {B}, build_topk_masks(s={s}) + forward_masked_dense, "
+                      f"threads={cores}, median of {reps}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    shape = WORKLOADS[args.workload]
+    B, s = args.batch, args.sparsity
+    cores = os.cpu_count() or 1
+    lay, _ = _ref_layer(shape)
+    if lay is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsparsekit_ref.so missing"}))
+        return
+    steps, warmup = min(args.steps, 5), min(args.warmup, 1)
+    xs = [make_tokens(B, shape["D"], 2 + i) for i in range(8)]
+    ts = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        _ref_step(lay, xs[i % 8], s, shape["S"] > 0, cores)
+        if i >= warmup:
+            ts.append(time.perf_counter() - t0)
+    ms = float(np.mean(ts)) * 1e3
+    val = round(B / (ms * 1e-3), 2)
+    line = {
+        "impl": "reference",
+        "metric": "MoE-layer tokens/s (decode) at intra-expert sparsity s; HBM GB/s in roofline/sweep",
+        "value": val, "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{shape['name']} shape, E={shape['E']} top-{shape['K']} "
+                               f"d_model={shape['D']} d_ffn={shape['N']} d_shared={shape['S']}, "
+                               f"batch {B} decode per GPU, top-k neuron selection s={s}",
+                   "sparsity": s, "batch_per_gpu": B,
+                   "note": "reference CPU layer (unmodified sources), rank 0 only; steps capped at 5"},
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                         "sample": f"full batch {B}, build_topk_masks + forward_masked_dense, "
+                                   f"threads={cores}, mean of {steps}"},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="granite", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

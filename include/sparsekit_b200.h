@@ -79,7 +79,7 @@ enum {
 /* Flags. */
 #define SKB_FLAG_FAST_ROUTER 0x1u  /* warp-parallel router dot products (not order-faithful) */
 #define SKB_FLAG_SIMT_GATEUP 0x2u  /* verification only: CUDA-core gate/up instead of tcgen05 */
-#define SKB_FLAG_TIME_STAGES 0x4u  /* record CUDA events around every stage (host API only) */
+#define SKB_FLAG_TIME_STAGES 0x4u  /* record CUDA events around every stage; disables PDL */
 #define SKB_FLAG_NO_PDL 0x8u       /* disable programmatic dependent launch between stages */
 
 #define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
@@ -152,8 +152,9 @@ int skb_layer_forward(skb_layer* layer, const skb_forward_args* args, skb_report
 int skb_layer_forward_device(skb_layer* layer, const skb_forward_args* args, void* stream,
                              skb_report* report);
 
-/* Per-stage milliseconds of the last skb_layer_forward call that carried
- * SKB_FLAG_TIME_STAGES; ms must hold SKB_N_STAGES floats. */
+/* Per-stage milliseconds of the last forward call (host or device entry) that
+ * carried SKB_FLAG_TIME_STAGES; waits for that forward to finish.  ms must
+ * hold SKB_N_STAGES floats. */
 int skb_layer_stage_times(skb_layer* layer, float* ms);
 
 /* Kernel launches issued by the last forward call on this layer. */

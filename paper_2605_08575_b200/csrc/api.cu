@@ -117,6 +117,7 @@ struct skb_layer {
   cudaEvent_t ev[SKB_N_STAGES + 1]{};
   float stage_ms[SKB_N_STAGES]{};
   bool have_stage_ms = false;
+  bool stage_ms_pending = false;
   int last_launches = 0;
 };
 
@@ -629,10 +630,7 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
     for (size_t t = 0; t < B; ++t)
       std::memcpy(a->h_shared_out + t * g.S, hbuf.data() + (BK + t) * g.Nh,
                   static_cast<size_t>(g.S) * 4);
-  if (timing) {
-    for (int i = 0; i < SKB_N_STAGES; ++i) cudaEventElapsedTime(&L->stage_ms[i], L->ev[i], L->ev[i + 1]);
-    L->have_stage_ms = true;
-  }
+  if (timing) L->stage_ms_pending = true;
   fill_report(L, a, report, a->routed_mask_in,
               (a->shared_mask_len != 0) ? a->shared_mask_in : nullptr);
   return SKB_OK;
@@ -646,16 +644,26 @@ int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stre
     return fail(SKB_ESHAPE, "forward_device: batch %d exceeds reserved capacity %d; call skb_layer_reserve",
                 a->batch, L->cap_batch);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : L->stream;
+  const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
   rc = forward_core(L, a, a->x, a->y, a->mode == SKB_MODE_MASKED ? a->routed_mask_in : nullptr,
                     (a->mode == SKB_MODE_MASKED && a->shared_mask_len) ? a->shared_mask_in : nullptr,
-                    nullptr, nullptr, s, false);
+                    nullptr, nullptr, s, timing);
   if (rc) return rc;
+  if (timing) L->stage_ms_pending = true;
   fill_report(L, a, report, nullptr, nullptr);
   return SKB_OK;
 }
 
 int skb_layer_stage_times(skb_layer* L, float* ms) {
   if (L == nullptr || ms == nullptr) return fail(SKB_EINTERNAL, "stage_times: null argument");
+  if (L->stage_ms_pending) {
+    // waits for the last stage of the timed forward (the device entry point does not synchronise)
+    SKB_CUDA(cudaEventSynchronize(L->ev[SKB_N_STAGES]));
+    for (int i = 0; i < SKB_N_STAGES; ++i)
+      SKB_CUDA(cudaEventElapsedTime(&L->stage_ms[i], L->ev[i], L->ev[i + 1]));
+    L->stage_ms_pending = false;
+    L->have_stage_ms = true;
+  }
   if (!L->have_stage_ms) return fail(SKB_EINTERNAL, "stage_times: no timed forward yet");
   std::memcpy(ms, L->stage_ms, sizeof(L->stage_ms));
   return SKB_OK;

@@ -213,6 +213,15 @@ class MoELayerWeights:
     def weight_bytes(self) -> int:
         return int(_lib.load().skb_layer_weight_bytes(self._h))
 
+    def stage_times(self) -> list:
+        """Milliseconds per stage (STAGE_NAMES order) of the last FLAG_TIME_STAGES forward."""
+        ms = (C.c_float * _lib.N_STAGES)()
+        _check(_lib.load().skb_layer_stage_times(self._h, ms))
+        return [float(v) for v in ms]
+
+    def last_launches(self) -> int:
+        return int(_lib.load().skb_layer_last_launches(self._h))
+
     def close(self) -> None:
         if self._h:
             _lib.load().skb_layer_destroy(self._h)
