@@ -231,6 +231,7 @@ class Point:
         for i in range(warmup + steps):
             self.x.copy_(self.x_ring[i % self.RING])
             self.flush.zero_()
+            torch.cuda.synchronize()  # stage events must not straddle the flush
             self._enqueue(s, flags=skb.FLAG_TIME_STAGES)
             ms = self.layer.stage_times()
             if i >= warmup:

@@ -75,6 +75,7 @@ int n_off_of(double s, int n) {
 
 const int kTileCases[5] = {16, 32, 64, 128, 256};
 
+
 }  // namespace
 
 struct skb_layer {
@@ -100,6 +101,7 @@ struct skb_layer {
   int32_t* d_ids = nullptr;
   float* d_wts = nullptr;
   DispatchBuffers disp{};
+  unsigned* d_counters = nullptr;
   __nv_bfloat16* d_xs = nullptr;
   uint64_t xs_rows = 0;
   CUtensorMap tmap_x[5]{};
@@ -107,12 +109,10 @@ struct skb_layer {
   int32_t* d_kidx = nullptr;
   float* d_kval = nullptr;
   int32_t* d_kcnt = nullptr;
-  float* d_part = nullptr;
   uint8_t* d_mask_in_r = nullptr;
   uint8_t* d_mask_in_s = nullptr;
   uint8_t* d_mask_out_r = nullptr;
   uint8_t* d_mask_out_s = nullptr;
-  int n_chunks = 0;
 
   cudaEvent_t ev[SKB_N_STAGES + 1]{};
   float stage_ms[SKB_N_STAGES]{};
@@ -128,14 +128,15 @@ void free_workspace(skb_layer* L) {
                   L->d_wts,      L->disp.perm,   L->disp.inv,       L->disp.row_expert,
                   L->disp.expert_off, L->disp.tile_expert, L->disp.tile_row0, L->disp.tile_nrows,
                   L->disp.n_tiles, L->d_xs,      L->d_h,            L->d_kidx,
-                  L->d_kval,     L->d_kcnt,      L->d_part,         L->d_mask_in_r,
-                  L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s};
+                  L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
+                  L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = L->d_part = nullptr;
+  L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
   L->d_ids = L->d_kidx = L->d_kcnt = nullptr;
   L->disp = DispatchBuffers{};
   L->d_xs = nullptr;
+  L->d_counters = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -178,6 +179,11 @@ int reserve_locked(skb_layer* L, int B) {
   SKB_TRY(dmalloc(&L->disp.tile_row0, max_tiles));
   SKB_TRY(dmalloc(&L->disp.tile_nrows, max_tiles));
   SKB_TRY(dmalloc(&L->disp.n_tiles, 1));
+  {
+    const size_t n_counters = 2 + static_cast<size_t>(cap);
+    SKB_TRY(dmalloc(&L->d_counters, n_counters));
+    SKB_CUDA(cudaMemsetAsync(L->d_counters, 0, n_counters * sizeof(unsigned), L->stream));
+  }
   L->xs_rows = rows;
   SKB_TRY(dmalloc(&L->d_xs, rows * g.Dp));
   SKB_CUDA(cudaMemsetAsync(L->d_xs, 0, rows * g.Dp * sizeof(__nv_bfloat16), L->stream));
@@ -187,8 +193,6 @@ int reserve_locked(skb_layer* L, int B) {
   SKB_TRY(dmalloc(&L->d_kidx, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kval, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kcnt, rows));
-  L->n_chunks = ceil_div(g.Nh, kDownChunk);
-  SKB_TRY(dmalloc(&L->d_part, rows * L->n_chunks * g.Dp));
   SKB_TRY(dmalloc(&L->d_mask_in_r, BK * g.N));
   SKB_TRY(dmalloc(&L->d_mask_out_r, BK * g.N));
   if (g.has_shared) {
@@ -311,11 +315,26 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   const int max_tiles = max_tiles_for(g, B, tn);
 
   tm.mark();
-  launches += launch_router_logits(ctx, d_x, L->d_router, B, g.E, g.D,
-                                   (a->flags & SKB_FLAG_FAST_ROUTER) != 0, L->d_logits);
-  launches += launch_route_topk(ctx, L->d_logits, B, g.E, g.K, g.renorm, L->d_ids, L->d_wts);
+  {
+    RouterLaunch r{};
+    r.x = d_x;
+    r.router = L->d_router;
+    r.B = B;
+    r.E = g.E;
+    r.D = g.D;
+    r.K = g.K;
+    r.renorm = g.renorm;
+    r.fast = (a->flags & SKB_FLAG_FAST_ROUTER) != 0;
+    r.logits = L->d_logits;
+    r.ids = L->d_ids;
+    r.weights = L->d_wts;
+    r.counters = L->d_counters;
+    r.dispatch = &L->disp;
+    r.has_shared = g.has_shared;
+    r.tile_tokens = tn;
+    launches += launch_router(ctx, r);
+  }
   tm.mark();
-  launches += launch_dispatch(ctx, L->d_ids, B, g.K, g.E, g.has_shared, tn, L->disp);
   launches += launch_permute_tokens(ctx, d_x, L->disp.perm, B, g.K, g.D, g.Dp, g.has_shared,
                                     L->d_xs);
   tm.mark();
@@ -326,52 +345,74 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                                  L->d_h);
   tm.mark();
 
-  SelectArgs sa{};
-  sa.h = L->d_h;
-  sa.rows = rows;
-  sa.BK = BK;
-  sa.N = g.N;
-  sa.S = g.S;
-  sa.Nh = g.Nh;
-  sa.K = g.K;
-  sa.perm = L->disp.perm;
-  sa.kept_idx = L->d_kidx;
-  sa.kept_val = L->d_kval;
-  sa.kept_cnt = L->d_kcnt;
-  sa.mask_out_routed = d_mask_out_r;
-  sa.mask_out_shared = d_mask_out_s;
+  int sel_mode, n_off_r = 0, n_off_s = 0;
   int max_keep = g.N > g.S ? g.N : g.S;
   if (a->mode == SKB_MODE_DENSE) {
-    sa.mode = kSelectAll;
+    sel_mode = kSelectAll;
   } else if (a->mode == SKB_MODE_TOPK) {
-    sa.mode = kSelectTopk;
-    sa.n_off_routed = n_off_of(a->s_routed, g.N);
-    sa.n_off_shared = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
-    const int kr = g.N - sa.n_off_routed, ks = g.S - sa.n_off_shared;
+    sel_mode = kSelectTopk;
+    n_off_r = n_off_of(a->s_routed, g.N);
+    n_off_s = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
+    const int kr = g.N - n_off_r, ks = g.S - n_off_s;
     max_keep = kr > ks ? kr : ks;
   } else {
-    sa.mode = kSelectGiven;
+    sel_mode = kSelectGiven;
+  }
+  // The selection runs inside the down kernel; the stand-alone selection kernel only serves
+  // mask captures (MaskSet export).
+  if (d_mask_out_r != nullptr || d_mask_out_s != nullptr) {
+    SelectArgs sa{};
+    sa.h = L->d_h;
+    sa.rows = rows;
+    sa.BK = BK;
+    sa.N = g.N;
+    sa.S = g.S;
+    sa.Nh = g.Nh;
+    sa.K = g.K;
+    sa.perm = L->disp.perm;
+    sa.kept_idx = L->d_kidx;
+    sa.kept_val = nullptr;
+    sa.kept_cnt = L->d_kcnt;
+    sa.mask_out_routed = d_mask_out_r;
+    sa.mask_out_shared = d_mask_out_s;
+    sa.mode = sel_mode;
+    sa.n_off_routed = n_off_r;
+    sa.n_off_shared = n_off_s;
     sa.mask_in_routed = d_mask_r;
     sa.mask_in_shared = d_mask_s;
+    launches += launch_select(ctx, sa);
   }
-  launches += launch_select(ctx, sa);
   tm.mark();
 
   DownArgs da{};
   da.wd = L->d_wd;
   da.wd_shared = L->d_wd_shared;
   da.row_expert = L->disp.row_expert;
-  da.kept_idx = L->d_kidx;
-  da.kept_val = L->d_kval;
-  da.kept_cnt = L->d_kcnt;
-  da.rows = rows;
+  da.inv = L->disp.inv;
+  da.weights = L->d_wts;
+  da.B = B;
+  da.K = g.K;
+  da.BK = BK;
+  da.has_shared = g.has_shared;
+  da.h = L->d_h;
+  da.Nh = g.Nh;
+  da.N = g.N;
+  da.S = g.S;
+  da.sel_mode = sel_mode;
+  da.n_off_routed = n_off_r;
+  da.n_off_shared = n_off_s;
+  da.mask_in_routed = d_mask_r;
+  da.mask_in_shared = d_mask_s;
   da.max_keep = max_keep;
-  da.partial = L->d_part;
-  da.n_chunks = L->n_chunks;
-  launches += launch_down(ctx, da, g);
+  da.y = d_y;
+  {
+    const int n = launch_down(ctx, da, g);
+    if (n < 0)
+      return fail(SKB_ECONFIG, "forward: top_k * d_ffn too large for the down-projection kernel's "
+                               "shared-memory lists (K=%d, N=%d, S=%d)", g.K, g.N, g.S);
+    launches += n;
+  }
   tm.mark();
-  launches += launch_combine(ctx, L->d_part, L->n_chunks, L->disp.inv, L->d_kcnt, L->d_wts, B, g,
-                             d_y);
   tm.mark();
   L->last_launches = launches;
   cudaError_t e = cudaGetLastError();
@@ -698,15 +739,30 @@ int skb_route(const float* logits, int batch, int n_experts, int top_k, int reno
   const size_t BE = static_cast<size_t>(batch) * n_experts, BK = static_cast<size_t>(batch) * top_k;
   float *dl = nullptr, *dw = nullptr;
   int32_t* di = nullptr;
-  if ((rc = dmalloc(&dl, BE)) || (rc = dmalloc(&dw, BK)) || (rc = dmalloc(&di, BK))) return rc;
+  unsigned* dc = nullptr;
+  const size_t n_counters = 2 + static_cast<size_t>(batch);
+  if ((rc = dmalloc(&dl, BE)) || (rc = dmalloc(&dw, BK)) || (rc = dmalloc(&di, BK)) ||
+      (rc = dmalloc(&dc, n_counters)))
+    return rc;
   cudaMemcpy(dl, logits, BE * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dc, 0, n_counters * sizeof(unsigned));
   LaunchCtx ctx{nullptr, false};
-  launch_route_topk(ctx, dl, batch, n_experts, top_k, renormalize, di, dw);
+  RouterLaunch r{};
+  r.B = batch;
+  r.E = n_experts;
+  r.K = top_k;
+  r.renorm = renormalize;
+  r.logits = dl;
+  r.ids = di;
+  r.weights = dw;
+  r.counters = dc;
+  launch_router(ctx, r);
   cudaMemcpy(ids, di, BK * 4, cudaMemcpyDeviceToHost);
   cudaError_t e = cudaMemcpy(weights, dw, BK * 4, cudaMemcpyDeviceToHost);
   cudaFree(dl);
   cudaFree(dw);
   cudaFree(di);
+  cudaFree(dc);
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
     return fail(SKB_ECUDA, "route: %s", cudaGetErrorString(e));
   return SKB_OK;

@@ -10,70 +10,321 @@
 namespace skb {
 
 // ---------------------------------------------------------------------------------------------
-// Router logits, order-faithful: logits[t][e] = sum_d router[e][d] * x[t][d] with a float
-// accumulator, d ascending, multiply and add rounded separately (the reference is built with
-// -ffp-contract=off, proj/CMakeLists.txt:26-27).  One thread per expert, TT tokens per CTA so
-// that TT independent dependent-add chains fill the 4-cycle FADD latency.
+// Fused router: logits (order-faithful) -> softmax/top-k -> dispatch, one launch.
+//
+// logits[t][e] = sum_d router[e][d] * x[t][d] with a float accumulator, d ascending, multiply
+// and add rounded separately (the reference is built with -ffp-contract=off,
+// proj/CMakeLists.txt:26-27).  That chain is inherently serial (D dependent FADDs), so the
+// kernel is organised around it: one single-warp CTA per (8 experts x 4 tokens) runs 32
+// chains, one per lane, and feeds itself through an 8-deep cp.async ring of 128-float
+// sub-chunks (no block barriers at all).  The CTA that completes a token block's logits
+// ("last arriver" on a global counter) runs route() for those tokens; the CTA that completes
+// the last token block builds the dispatch when B*K is small (decode).
 // ---------------------------------------------------------------------------------------------
-constexpr int kLogitChunk = 1024;
+constexpr int kRfEB = 8;        // experts per CTA
+constexpr int kRfTB = 4;        // tokens per CTA
+constexpr int kRfSub = 128;     // floats per sub-chunk
+constexpr int kRfStages = 8;    // ring depth
+constexpr int kRfRow = kRfSub + 4;  // padded row stride (floats): conflict-free LDS.128
+constexpr int kRfRows = kRfEB + kRfTB;
+constexpr int kRfSmemFloats = kRfStages * kRfRows * kRfRow;
+constexpr int kRfSmemBytes = kRfSmemFloats * 4 + 2 * kRfStages * 8;  // ring + full/empty barriers
 
-template <int TT>
-__global__ void __launch_bounds__(1024) router_logits_exact_kernel(const float* __restrict__ x,
-                                                                  const float* __restrict__ router,
-                                                                  int B, int E, int D,
-                                                                  float* __restrict__ logits) {
-  __shared__ float xs[TT][kLogitChunk];
-  const int e = threadIdx.x;
-  const int t0 = blockIdx.x * TT;
-  float acc[TT];
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// route() for one token by one warp (proj/src/router.cpp:13-68): softmax with max
+// subtraction, exp evaluated in double and rounded to float (what glibc's expf returns),
+// ascending float sum for the denominator, IEEE division, then K rounds of warp arg-max under
+// the reference's total order (probability descending, expert id ascending on ties).
+// `sc` is E floats of shared scratch private to the warp.
+__device__ void warp_route_token(const float* __restrict__ row, int E, int K, int renorm,
+                                 float* sc, int32_t* out_ids, float* out_w) {
+  const int lane = threadIdx.x & 31;
+  float mx = -INFINITY;
+  for (int e = lane; e < E; e += 32) {
+    const float l = __ldcg(row + e);
+    sc[e] = l;
+    mx = fmaxf(mx, l);
+  }
 #pragma unroll
-  for (int tt = 0; tt < TT; ++tt) acc[tt] = 0.0f;
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int e = lane; e < E; e += 32)
+    sc[e] = static_cast<float>(exp(static_cast<double>(__fsub_rn(sc[e], mx))));
+  __syncwarp();
+  float denom = 0.0f;
+  if (lane == 0)
+    for (int e = 0; e < E; ++e) denom = __fadd_rn(denom, sc[e]);
+  denom = __shfl_sync(0xffffffffu, denom, 0);
+  for (int e = lane; e < E; e += 32) sc[e] = __fdiv_rn(sc[e], denom);
+  __syncwarp();
+  float selected_sum = 0.0f;
+  for (int s = 0; s < K; ++s) {
+    float bp = -3.0f;
+    int be = 0x7fffffff;
+    for (int e = lane; e < E; e += 32) {  // e ascending => lowest id kept on equal probability
+      const float v = sc[e];
+      if (v > bp) {
+        bp = v;
+        be = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (op > bp || (op == bp && oe < be)) {
+        bp = op;
+        be = oe;
+      }
+    }
+    if (lane == 0) {
+      sc[be] = -1.0f;  // selected: never wins again (probabilities are >= 0)
+      out_ids[s] = be;
+      out_w[s] = bp;
+    }
+    selected_sum = __fadd_rn(selected_sum, bp);
+    __syncwarp();
+  }
+  if (renorm)
+    for (int s = lane; s < K; s += 32) out_w[s] = __fdiv_rn(out_w[s], selected_sum);
+  __syncwarp();
+}
+
+// Dispatch for B*K <= kSmallSlots by one warp: stable counting sort by expert and the tile list,
+// by direct counting (O((B*K)^2 / 32), no scans).  Same outputs as dispatch_kernel.
+__device__ void warp_small_dispatch(const int32_t* __restrict__ ids, int B, int K, int E,
+                                    int has_shared, int tile_tokens, const DispatchBuffers& d,
+                                    int32_t* sc /* >= 4 * kSmallSlots ints */) {
+  const int lane = threadIdx.x & 31;
+  const int BK = B * K;
+  int32_t* ids_s = sc;
+  int32_t* rank_s = sc + kSmallSlots;
+  int32_t* pos_s = sc + 2 * kSmallSlots;
+  int32_t* cnt_s = sc + 3 * kSmallSlots;
+  for (int i = lane; i < BK; i += 32) ids_s[i] = __ldcg(ids + i);
+  __syncwarp();
+  for (int i = lane; i < BK; i += 32) {
+    const int e = ids_s[i];
+    int lower = 0, before = 0, cnt = 0;
+    for (int j = 0; j < BK; ++j) {
+      const int ej = ids_s[j];
+      lower += (ej < e);
+      before += (ej == e && j < i);
+      cnt += (ej == e);
+    }
+    const int pos = lower + before;
+    rank_s[i] = before;
+    pos_s[i] = pos;
+    cnt_s[i] = ((before % tile_tokens) == 0) ? cnt : -cnt;  // sign marks tile heads
+    d.perm[pos] = i;
+    d.inv[i] = pos;
+    d.row_expert[pos] = e;
+  }
+  __syncwarp();
+  int heads = 0;
+  for (int i = lane; i < BK; i += 32) {
+    if (cnt_s[i] > 0) {
+      const int e = ids_s[i], r = rank_s[i];
+      int ti = 0;
+      for (int j = 0; j < BK; ++j)
+        ti += (cnt_s[j] > 0 && (ids_s[j] < e || (ids_s[j] == e && rank_s[j] < r)));
+      d.tile_expert[ti] = e;
+      d.tile_row0[ti] = pos_s[i];
+      d.tile_nrows[ti] = min(tile_tokens, cnt_s[i] - r);
+      ++heads;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) heads += __shfl_xor_sync(0xffffffffu, heads, o);
+  int n_tiles = heads;
+  if (has_shared) {
+    const int nsh = ceil_div(B, tile_tokens);
+    for (int j = lane; j < nsh; j += 32) {
+      d.tile_expert[n_tiles + j] = E;
+      d.tile_row0[n_tiles + j] = BK + j * tile_tokens;
+      d.tile_nrows[n_tiles + j] = min(tile_tokens, B - j * tile_tokens);
+    }
+    for (int t = lane; t < B; t += 32) d.row_expert[BK + t] = E;
+    n_tiles += nsh;
+  }
+  if (lane == 0) *d.n_tiles = n_tiles;
+}
+
+struct RouterFusedArgs {
+  const float* x;
+  const float* router;
+  int B, E, D, K, renorm;
+  int logits_ready;   // 1: logits were produced by the fast kernel; skip the chains
+  int fuse_dispatch;  // 1: the last CTA also builds the dispatch (B*K <= kSmallSlots)
+  int has_shared, tile_tokens;
+  float* logits;
+  int32_t* ids;
+  float* weights;
+  unsigned* counters;  // [0] = finished token blocks, [1 + tb] = finished expert blocks of tb
+  DispatchBuffers d;
+};
+
+__device__ long long g_rf_dbg[16];
+#define RF_T(i) do { if (lane == 0 && warp == 0) g_rf_dbg[i] = clock64(); } while (0)
+
+__global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
+  extern __shared__ __align__(16) float rf_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e0 = blockIdx.x * kRfEB, t0 = blockIdx.y * kRfTB;
+  const int D = a.D;
+  const uint32_t bar_base = smem_u32(rf_smem + kRfSmemFloats);
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (kRfStages + s); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRfStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    fence_barrier_init();
+  }
+  RF_T(0);
+  __syncthreads();
   pdl_wait();
   pdl_launch_dependents();
-  const bool vec_ok = (D % 4) == 0;
-  for (int d0 = 0; d0 < D; d0 += kLogitChunk) {
-    const int len = min(kLogitChunk, D - d0);
-    __syncthreads();
-#pragma unroll
-    for (int tt = 0; tt < TT; ++tt) {
-      const int t = t0 + tt;
-      for (int i = threadIdx.x; i < len; i += blockDim.x)
-        xs[tt][i] = (t < B) ? x[static_cast<size_t>(t) * D + d0 + i] : 0.0f;
-    }
-    __syncthreads();
-    if (e < E) {
-      const float* wr = router + static_cast<size_t>(e) * D + d0;
-      int i = 0;
+  RF_T(1);
+
+  if (!a.logits_ready) {
+    const int nsub = ceil_div(D, kRfSub);
+    const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
+    const int n_e = min(kRfEB, a.E - e0), n_t = min(kRfTB, a.B - t0);  // valid rows
+    if (warp == 1) {
+      // ---- producer: one elected lane feeds the ring with 1-D bulk copies (TMA engine); the
+      // chain warp never spends an issue slot on staging ----
       if (vec_ok) {
-        const float4* wr4 = reinterpret_cast<const float4*>(wr);
-        const int n4 = len / 4;
-#pragma unroll 4
-        for (int q = 0; q < n4; ++q) {
-          const float4 w = __ldg(wr4 + q);
-#pragma unroll
-          for (int tt = 0; tt < TT; ++tt) {
-            const float4 xv = *reinterpret_cast<const float4*>(&xs[tt][4 * q]);
-            acc[tt] = __fadd_rn(acc[tt], __fmul_rn(w.x, xv.x));
-            acc[tt] = __fadd_rn(acc[tt], __fmul_rn(w.y, xv.y));
-            acc[tt] = __fadd_rn(acc[tt], __fmul_rn(w.z, xv.z));
-            acc[tt] = __fadd_rn(acc[tt], __fmul_rn(w.w, xv.w));
+        if (lane == 0) {
+          const float* wsrc = a.router + static_cast<size_t>(e0) * D;
+          const float* xsrc = a.x + static_cast<size_t>(t0) * D;
+#pragma unroll 1
+          for (int sc = 0; sc < nsub; ++sc) {
+            const int slot = sc % kRfStages;
+            mbar_wait(empty_bar(slot), ((sc / kRfStages) & 1u) ^ 1u);
+            const int d0 = sc * kRfSub;
+            const uint32_t bytes = static_cast<uint32_t>(min(kRfSub, D - d0)) * 4u;
+            mbar_arrive_expect_tx(full_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
+            const uint32_t dst = smem_u32(rf_smem + slot * kRfRows * kRfRow);
+#pragma unroll 1
+            for (int r = 0; r < n_e; ++r)
+              bulk_copy_g2s(dst + r * kRfRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
+                            full_bar(slot));
+#pragma unroll 1
+            for (int r = 0; r < n_t; ++r)
+              bulk_copy_g2s(dst + (kRfEB + r) * kRfRow * 4, xsrc + static_cast<size_t>(r) * D + d0,
+                            bytes, full_bar(slot));
           }
         }
-        i = n4 * 4;
+      } else {
+        // unaligned / odd d_model: plain loads by the whole producer warp
+#pragma unroll 1
+        for (int sc = 0; sc < nsub; ++sc) {
+          const int slot = sc % kRfStages;
+          mbar_wait(empty_bar(slot), ((sc / kRfStages) & 1u) ^ 1u);
+          const int d0 = sc * kRfSub;
+          const int n = min(kRfSub, D - d0);
+          float* dst = rf_smem + slot * kRfRows * kRfRow;
+#pragma unroll 1
+          for (int r = 0; r < n_e + n_t; ++r) {
+            const float* src = (r < n_e) ? a.router + static_cast<size_t>(e0 + r) * D + d0
+                                         : a.x + static_cast<size_t>(t0 + r - n_e) * D + d0;
+            float* drow = dst + ((r < n_e) ? r : kRfEB + r - n_e) * kRfRow;
+#pragma unroll 1
+            for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full_bar(slot));
+        }
       }
-      for (; i < len; ++i) {
-        const float w = __ldg(wr + i);
-#pragma unroll
-        for (int tt = 0; tt < TT; ++tt) acc[tt] = __fadd_rn(acc[tt], __fmul_rn(w, xs[tt][i]));
-      }
+      return;
     }
+
+    // ---- consumer: 32 chains, one per lane ----
+    const int e_i = lane / kRfTB, t_j = lane % kRfTB;
+    const bool valid = (e_i < n_e) && (t_j < n_t);
+    float acc = 0.0f;
+    long long t_wait = 0;
+#pragma unroll 1
+    for (int sc = 0; sc < nsub; ++sc) {
+      const int slot = sc % kRfStages;
+      const long long tw0 = clock64();
+      mbar_wait(full_bar(slot), (sc / kRfStages) & 1u);
+      t_wait += clock64() - tw0;
+      if (sc == 0) RF_T(8);
+      const float* base = rf_smem + slot * kRfRows * kRfRow;
+      const float* wr = base + e_i * kRfRow;
+      const float* xr = base + (kRfEB + t_j) * kRfRow;
+      const int n = min(kRfSub, D - sc * kRfSub);
+      const int n4 = n >> 2;
+#pragma unroll 8
+      for (int q = 0; q < n4; ++q) {
+        const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
+        const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
+        acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
+        acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
+        acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
+        acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
+      }
+#pragma unroll 1
+      for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar(slot));
+    }
+    RF_T(2);
+    if (lane == 0) g_rf_dbg[9] = t_wait;
+    if (valid) a.logits[static_cast<size_t>(t0 + t_j) * a.E + e0 + e_i] = acc;
+
+    // last arriver of this token block runs route() for its tokens
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(&a.counters[1 + blockIdx.y], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    RF_T(3);
+    if (prev != gridDim.x - 1) return;
+    if (lane == 0) a.counters[1 + blockIdx.y] = 0;  // at rest again for the next forward
+    __threadfence();
+    RF_T(4);
+  } else if (warp == 1) {
+    return;
   }
-  if (e < E) {
-#pragma unroll
-    for (int tt = 0; tt < TT; ++tt)
-      if (t0 + tt < B) logits[static_cast<size_t>(t0 + tt) * E + e] = acc[tt];
+
+  for (int tt = 0; tt < kRfTB; ++tt) {
+    const int t = t0 + tt;
+    if (t >= a.B) break;
+    warp_route_token(a.logits + static_cast<size_t>(t) * a.E, a.E, a.K, a.renorm, rf_smem,
+                     a.ids + static_cast<size_t>(t) * a.K, a.weights + static_cast<size_t>(t) * a.K);
   }
+  RF_T(5);
+  if (!a.fuse_dispatch) return;
+
+  __threadfence();
+  __syncwarp();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(&a.counters[0], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != gridDim.y - 1) return;
+  if (lane == 0) a.counters[0] = 0;
+  __threadfence();
+  RF_T(6);
+  warp_small_dispatch(a.ids, a.B, a.K, a.E, a.has_shared, a.tile_tokens, a.d,
+                      reinterpret_cast<int32_t*>(rf_smem));
+  RF_T(7);
 }
+
+extern "C" void skb_debug_rf(long long* out) { cudaMemcpyFromSymbol(out, g_rf_dbg, sizeof(g_rf_dbg)); }
 
 // Fast variant (SKB_FLAG_FAST_ROUTER): one warp per (token, expert), lanes stride d, fp32 FMA,
 // shuffle tree.  Not order-faithful: ids can differ from the reference when two probabilities
@@ -109,8 +360,7 @@ __global__ void __launch_bounds__(256) router_logits_fast_kernel(const float* __
   if (lane == 0) logits[static_cast<size_t>(t) * E + e] = acc;
 }
 
-int launch_router_logits(const LaunchCtx& ctx, const float* x, const float* router, int B, int E,
-                         int D, bool fast, float* logits) {
+int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -118,140 +368,45 @@ int launch_router_logits(const LaunchCtx& ctx, const float* x, const float* rout
   cfg.attrs = attr;
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
-  if (fast) {
-    const long warps = static_cast<long>(B) * E;
+  int launches = 0;
+  if (r.fast && r.x != nullptr) {
+    const long warps = static_cast<long>(r.B) * r.E;
     cfg.gridDim = dim3(static_cast<unsigned>((warps * 32 + 255) / 256));
     cfg.blockDim = dim3(256);
-    cudaLaunchKernelEx(&cfg, router_logits_fast_kernel, x, router, B, E, D, logits);
-    return 1;
+    cudaLaunchKernelEx(&cfg, router_logits_fast_kernel, r.x, r.router, r.B, r.E, r.D, r.logits);
+    ++launches;
   }
-  cfg.blockDim = dim3(round_up(E, 32));
-  if (B == 1) {
-    cfg.gridDim = dim3(1);
-    cudaLaunchKernelEx(&cfg, router_logits_exact_kernel<1>, x, router, B, E, D, logits);
-  } else {
-    cfg.gridDim = dim3(ceil_div(B, 2));
-    cudaLaunchKernelEx(&cfg, router_logits_exact_kernel<2>, x, router, B, E, D, logits);
+  static bool attr_set = false;
+  constexpr int smem = kRfSmemBytes;
+  if (!attr_set) {
+    cudaFuncSetAttribute(router_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = true;
   }
-  return 1;
-}
-
-// ---------------------------------------------------------------------------------------------
-// route(): one warp per token.  Softmax with max subtraction, exp evaluated in double and
-// rounded to float (what glibc's expf does internally), ascending float sum for the
-// denominator, IEEE division, then K rounds of warp arg-max under the reference's total order
-// (probability descending, expert id ascending on ties).
-// ---------------------------------------------------------------------------------------------
-template <int EPL>  // experts per lane, E <= 32 * EPL
-__global__ void __launch_bounds__(128) route_topk_kernel(const float* __restrict__ logits, int B,
-                                                         int E, int K, int renorm,
-                                                         int32_t* __restrict__ ids,
-                                                         float* __restrict__ weights) {
-  extern __shared__ float smem_probs[];  // [warps][E]
-  const int warp_in_block = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
-  pdl_wait();
-  pdl_launch_dependents();
-  if (t >= B) return;
-  float* ex_s = smem_probs + static_cast<size_t>(warp_in_block) * E;
-  const float* row = logits + static_cast<size_t>(t) * E;
-
-  float l[EPL];
-  float mx = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) {
-    const int e = j * 32 + lane;
-    l[j] = (e < E) ? row[e] : -INFINITY;
-    mx = fmaxf(mx, l[j]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-
-  float p[EPL];
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) {
-    const int e = j * 32 + lane;
-    if (e < E) {
-      p[j] = static_cast<float>(exp(static_cast<double>(__fsub_rn(l[j], mx))));
-      ex_s[e] = p[j];
-    } else {
-      p[j] = 0.0f;
-    }
-  }
-  __syncwarp();
-  float denom = 0.0f;
-  if (lane == 0) {
-    for (int e = 0; e < E; ++e) denom = __fadd_rn(denom, ex_s[e]);
-  }
-  denom = __shfl_sync(0xffffffffu, denom, 0);
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) {
-    const int e = j * 32 + lane;
-    p[j] = (e < E) ? __fdiv_rn(p[j], denom) : -2.0f;
-  }
-
-  int32_t* out_ids = ids + static_cast<size_t>(t) * K;
-  float* out_w = weights + static_cast<size_t>(t) * K;
-  float selected_sum = 0.0f;
-  for (int s = 0; s < K; ++s) {
-    float bp = -3.0f;
-    int be = 0x7fffffff;
-#pragma unroll
-    for (int j = 0; j < EPL; ++j) {
-      if (p[j] > bp) {  // j ascending => lowest id kept on equal probability
-        bp = p[j];
-        be = j * 32 + lane;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float op = __shfl_xor_sync(0xffffffffu, bp, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-      if (op > bp || (op == bp && oe < be)) {
-        bp = op;
-        be = oe;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < EPL; ++j)
-      if (j * 32 + lane == be) p[j] = -1.0f;  // selected: never wins again (probabilities >= 0)
-    selected_sum = __fadd_rn(selected_sum, bp);
-    if (lane == 0) {
-      out_ids[s] = be;
-      out_w[s] = bp;
-    }
-  }
-  __syncwarp();
-  if (renorm) {
-    for (int s = lane; s < K; s += 32) out_w[s] = __fdiv_rn(out_w[s], selected_sum);
-  }
-}
-
-int launch_route_topk(const LaunchCtx& ctx, const float* logits, int B, int E, int K, int renorm,
-                      int32_t* ids, float* weights) {
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = ctx.pdl ? 1 : 0;
-  cfg.stream = ctx.stream;
-  const int warps = (E > 256) ? 1 : 4;  // keep dynamic smem small for wide routers
-  cfg.blockDim = dim3(32 * warps);
-  cfg.gridDim = dim3(ceil_div(B, warps));
-  cfg.dynamicSmemBytes = static_cast<size_t>(warps) * E * sizeof(float);
-  const int epl = ceil_div(E, 32);
-#define SKB_ROUTE_CASE(N)                                                                       \
-  cudaLaunchKernelEx(&cfg, route_topk_kernel<N>, logits, B, E, K, renorm, ids, weights)
-  if (epl <= 1) SKB_ROUTE_CASE(1);
-  else if (epl <= 2) SKB_ROUTE_CASE(2);
-  else if (epl <= 4) SKB_ROUTE_CASE(4);
-  else if (epl <= 8) SKB_ROUTE_CASE(8);
-  else if (epl <= 16) SKB_ROUTE_CASE(16);
-  else SKB_ROUTE_CASE(32);
-#undef SKB_ROUTE_CASE
-  return 1;
+  RouterFusedArgs a{};
+  a.x = r.x;
+  a.router = r.router;
+  a.B = r.B;
+  a.E = r.E;
+  a.D = r.D;
+  a.K = r.K;
+  a.renorm = r.renorm;
+  a.logits_ready = (r.fast || r.x == nullptr) ? 1 : 0;
+  a.fuse_dispatch = (r.dispatch != nullptr && r.B * r.K <= kSmallSlots) ? 1 : 0;
+  a.has_shared = r.has_shared;
+  a.tile_tokens = r.tile_tokens;
+  a.logits = r.logits;
+  a.ids = r.ids;
+  a.weights = r.weights;
+  a.counters = r.counters;
+  if (r.dispatch) a.d = *r.dispatch;
+  cfg.gridDim = dim3(a.logits_ready ? 1 : ceil_div(r.E, kRfEB), ceil_div(r.B, kRfTB));
+  cfg.blockDim = dim3(64);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchKernelEx(&cfg, router_fused_kernel, a);
+  ++launches;
+  if (r.dispatch != nullptr && !a.fuse_dispatch)
+    launches += launch_dispatch(ctx, r.ids, r.B, r.K, r.E, r.has_shared, r.tile_tokens, *r.dispatch);
+  return launches;
 }
 
 // ---------------------------------------------------------------------------------------------

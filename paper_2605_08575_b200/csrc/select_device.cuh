@@ -1,0 +1,115 @@
+// select_device.cuh -- CTA-wide neuron selection shared by select.cu (stand-alone selection:
+// masks and survivor lists in global memory) and down.cu (selection fused in front of the
+// gather).  256 threads per CTA.
+//
+// Bit-exact restatement of mask_smallest_magnitudes / topk_mask
+// (proj/src/activation.cpp:31-60): key = bits(h) & 0x7fffffff is monotone in |h|; the n_off
+// smallest keys are dropped; among keys equal to the pivot the LOWER indices are dropped first
+// (stable_sort, activation.cpp:42-50).  No sort: an 8-ary search over the key value finds the
+// pivot, a ballot/popc prefix orders the survivors.
+#pragma once
+
+#include "skb_internal.cuh"
+
+namespace skb {
+
+constexpr int kSelWarps = kSelectThreads / 32;
+
+struct SelScratch {
+  int kcnt[2][kSelWarps];      // per-threshold counts of the k-ary search (double buffered)
+  int warp_cnt[2][kSelWarps];  // ballot prefix scratch of sel_block_rank (double buffered)
+};
+
+// What survives in one row: keys > pivot, plus keys == pivot whose rank among the ties (by
+// ascending index) is >= ties_to_drop.
+struct RowPick {
+  uint32_t pivot;
+  int ties_to_drop;
+  bool drop_all_ties;
+};
+
+// Exclusive prefix of `flag` over the CTA in thread order; `buf` alternates between calls so a
+// single __syncthreads per scan suffices.
+__device__ __forceinline__ int sel_block_rank(bool flag, SelScratch& sc, int buf, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) sc.warp_cnt[buf][warp] = __popc(b);
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kSelWarps; ++w) {
+    const int c = sc.warp_cnt[buf][w];
+    if (w < warp) base += c;
+    tot += c;
+  }
+  total = tot;
+  return base + __popc(b & ((1u << lane) - 1u));
+}
+
+// keys[0..n) in shared memory; 0 < n_off < n.  Every thread returns the same RowPick.
+//
+// 8-ary search on the key VALUE (31 bits, 3 bits per step, 11 steps): warp w counts the keys
+// below threshold lo + (w+1) << shift; the counts are monotone in w, so the digit is the number
+// of thresholds whose count is still below the wanted rank.  Pure compare + warp reduce: no
+// shared-memory atomics (a 256-bin atomic histogram costs ~2 cycles per key per pass on the
+// SM's single shared-memory pipe and made the selection the slowest part of decode).
+// For n <= 1024 every warp keeps all keys in registers (32 per lane).
+__device__ __forceinline__ RowPick sel_kary_pick(const uint32_t* keys, int n, int n_off,
+                                                 SelScratch& sc) {
+  static_assert(kSelWarps == 8, "one threshold per warp, 3 bits per step");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool in_regs = n <= 1024;
+  uint32_t kr[32];
+  if (in_regs) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int i = j * 32 + lane;
+      kr[j] = (i < n) ? keys[i] : 0xffffffffu;  // padding never falls below a threshold
+    }
+  }
+  uint32_t lo = 0;
+  int below = 0, equal = 0, bits = 31, buf = 0;
+#pragma unroll 1
+  while (bits > 0) {
+    const int b = bits >= 3 ? 3 : bits;
+    const int shift = bits - b;
+    const int n_thr = 1 << b;  // thresholds lo + (q+1) << shift, q < n_thr; the last one is hi
+    if (warp < n_thr) {
+      const uint32_t T = lo + (static_cast<uint32_t>(warp + 1) << shift);
+      int c = 0;
+      if (in_regs) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) c += (kr[j] < T) ? 1 : 0;
+      } else {
+#pragma unroll 8
+        for (int i = lane; i < n; i += 32) c += (keys[i] < T) ? 1 : 0;
+      }
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0) sc.kcnt[buf][warp] = c;
+    }
+    __syncthreads();
+    int d = 0, nb = below;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      if (q < n_thr - 1) {
+        const int cq = sc.kcnt[buf][q];
+        if (cq < n_off) {
+          d = q + 1;
+          nb = cq;
+        }
+      }
+    }
+    equal = sc.kcnt[buf][d] - nb;  // keys inside the chosen sub-interval
+    lo += static_cast<uint32_t>(d) << shift;
+    below = nb;
+    bits -= b;
+    buf ^= 1;
+  }
+  RowPick p;
+  p.pivot = lo;                  // the n_off-th smallest key
+  p.ties_to_drop = n_off - below;  // keys < pivot are all dropped; then the first ties
+  p.drop_all_ties = (p.ties_to_drop == equal);
+  return p;
+}
+
+}  // namespace skb

@@ -17,10 +17,9 @@ namespace skb {
 
 constexpr int kNeuronBlock = 64;   // neurons per gate/up tile (64 gate + 64 up rows = UMMA M 128)
 constexpr int kBlockK = 64;        // bf16 elements per TMA/UMMA K block (one 128-byte swizzle row)
-constexpr int kDownChunk = 128;    // kept entries per down-projection partial (8 warps x 16)
-constexpr int kDownSeg = 256;      // output columns per down-projection CTA (32 lanes x 8 bf16)
 constexpr int kSelectThreads = 256;
-constexpr int kMaxExperts = 1024;  // 32 probabilities per lane in the warp top-k
+constexpr int kMaxExperts = 1024;
+constexpr int kSmallSlots = 64;    // B*K up to which the router kernel builds the dispatch itself  // 32 probabilities per lane in the warp top-k
 
 __host__ __device__ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -53,10 +52,23 @@ struct LaunchCtx {
   bool pdl;  // programmatic dependent launch between stages
 };
 
-int launch_router_logits(const LaunchCtx& ctx, const float* x, const float* router, int B, int E,
-                         int D, bool fast, float* logits);
-int launch_route_topk(const LaunchCtx& ctx, const float* logits, int B, int E, int K, int renorm,
-                      int32_t* ids, float* weights);
+// Router stage: logits (x == nullptr: `logits` already holds them), route(), and -- when
+// `dispatch` is given -- the dispatch (inside the router kernel for B*K <= kSmallSlots, else by
+// dispatch_kernel).  `counters` is 1 + ceil(B / 4) zero-initialised words that the kernel
+// leaves zeroed.
+struct RouterLaunch {
+  const float* x;
+  const float* router;
+  int B, E, D, K, renorm;
+  bool fast;
+  float* logits;
+  int32_t* ids;
+  float* weights;
+  unsigned* counters;
+  const DispatchBuffers* dispatch;
+  int has_shared, tile_tokens;
+};
+int launch_router(const LaunchCtx& ctx, const RouterLaunch& r);
 int launch_dispatch(const LaunchCtx& ctx, const int32_t* ids, int B, int K, int E, int has_shared,
                     int tile_tokens, const DispatchBuffers& d);
 int launch_permute_tokens(const LaunchCtx& ctx, const float* x, const int32_t* perm, int B, int K,
@@ -92,18 +104,20 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a);
 struct DownArgs {
   const __nv_bfloat16* wd;         // [E][Np][Dp]
   const __nv_bfloat16* wd_shared;  // [Sp][Dp] or NULL
-  const int32_t* row_expert;
-  const int32_t* kept_idx;
-  const float* kept_val;
-  const int32_t* kept_cnt;
-  int rows, max_keep;
-  float* partial;  // [rows][n_chunks][Dp]
-  int n_chunks;    // ceil(Nh / kDownChunk): partial row stride in chunks
+  const int32_t* row_expert;       // [rows]
+  const int32_t* inv;              // [B*K] flat slot -> row
+  const float* weights;            // [B*K] router weights
+  int B, K, BK, has_shared;
+  const float* h;  // [rows][Nh]
+  int Nh, N, S;
+  // selection (kSelect*), done inside the kernel
+  int sel_mode, n_off_routed, n_off_shared;
+  const uint8_t* mask_in_routed;  // kSelectGiven: [B*K][N] slot-major
+  const uint8_t* mask_in_shared;  // kSelectGiven: [B][S] or NULL (=> keep all)
+  int max_keep;                   // upper bound of survivors per row
+  float* y;                       // [B][D]
 };
 int launch_down(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g);
-int launch_combine(const LaunchCtx& ctx, const float* partial, int n_chunks, const int32_t* inv,
-                   const int32_t* kept_cnt, const float* weights, int B, const Geometry& g,
-                   float* y);
 int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
                          int B, int K, int D, float* y);
 
@@ -130,6 +144,44 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier / bulk-copy (TMA) wrappers ----
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra WAIT_DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "WAIT_DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine, no tensor map): `bytes` and both addresses are
+// multiples of 16; completion is signalled on `bar` as complete_tx(bytes).
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void* src, uint32_t bytes,
+                                              uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_smem),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
 }
 
 // Position of neuron j of a 64-neuron block inside the interleaved 128-row
