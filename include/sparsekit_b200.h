@@ -81,6 +81,10 @@ enum {
 #define SKB_FLAG_SIMT_GATEUP 0x2u  /* verification only: CUDA-core gate/up instead of tcgen05 */
 #define SKB_FLAG_TIME_STAGES 0x4u  /* record CUDA events around every stage; disables PDL */
 #define SKB_FLAG_NO_PDL 0x8u       /* disable programmatic dependent launch between stages */
+#define SKB_FLAG_GATHER_DOWN 0x10u /* force the row-gather down projection (decode path) */
+#define SKB_FLAG_DENSE_DOWN 0x20u  /* force the dense masked tcgen05 down projection (batch path) */
+#define SKB_FLAG_BF16_H 0x40u      /* dense down projection: h rounded to bf16 (1e-2 mode) instead
+                                      of the exact three-term bf16 split (1e-5 mode) */
 
 #define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
 

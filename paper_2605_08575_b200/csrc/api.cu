@@ -90,8 +90,11 @@ struct skb_layer {
   __nv_bfloat16* d_wgu = nullptr;
   __nv_bfloat16* d_wd = nullptr;
   __nv_bfloat16* d_wd_shared = nullptr;
+  __nv_bfloat16* d_wdt = nullptr;         // W_down^T image [E][Dp128][Np] (dense down projection)
+  __nv_bfloat16* d_wdt_shared = nullptr;  // [Dp128][Sp]
   uint64_t weight_bytes = 0;
   CUtensorMap tmap_w{};
+  CUtensorMap tmap_wdt{}, tmap_wdt_shared{};
 
   // workspaces, sized for cap_batch
   int cap_batch = 0;
@@ -106,6 +109,9 @@ struct skb_layer {
   uint64_t xs_rows = 0;
   CUtensorMap tmap_x[5]{};
   float* d_h = nullptr;
+  __nv_bfloat16* d_hb = nullptr;  // masked activations, [3][rows][Nh] bf16 terms
+  CUtensorMap tmap_hb[5][3]{};
+  float* d_slot_out = nullptr;    // [rows][Dp]
   int32_t* d_kidx = nullptr;
   float* d_kval = nullptr;
   int32_t* d_kcnt = nullptr;
@@ -129,7 +135,8 @@ void free_workspace(skb_layer* L) {
                   L->disp.expert_off, L->disp.tile_expert, L->disp.tile_row0, L->disp.tile_nrows,
                   L->disp.n_tiles, L->d_xs,      L->d_h,            L->d_kidx,
                   L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
-                  L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters};
+                  L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
+                  L->d_hb,       L->d_slot_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -137,6 +144,8 @@ void free_workspace(skb_layer* L) {
   L->disp = DispatchBuffers{};
   L->d_xs = nullptr;
   L->d_counters = nullptr;
+  L->d_hb = nullptr;
+  L->d_slot_out = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -190,6 +199,13 @@ int reserve_locked(skb_layer* L, int B) {
   for (int i = 0; i < 5; ++i)
     SKB_TRY(encode_bf16_2d(&L->tmap_x[i], L->d_xs, rows, g.Dp, kTileCases[i]));
   SKB_TRY(dmalloc(&L->d_h, rows * g.Nh));
+  SKB_TRY(dmalloc(&L->d_hb, 3 * rows * g.Nh));
+  SKB_CUDA(cudaMemsetAsync(L->d_hb, 0, 3 * rows * g.Nh * sizeof(__nv_bfloat16), L->stream));
+  for (int i = 0; i < 5; ++i)
+    for (int sp = 0; sp < 3; ++sp)
+      SKB_TRY(encode_bf16_2d(&L->tmap_hb[i][sp], L->d_hb + sp * rows * g.Nh, rows, g.Nh,
+                             kTileCases[i]));
+  SKB_TRY(dmalloc(&L->d_slot_out, rows * g.Dp));
   SKB_TRY(dmalloc(&L->d_kidx, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kval, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kcnt, rows));
@@ -250,6 +266,7 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out) {
   g.has_shared = cfg->has_shared ? 1 : 0;
   g.renorm = cfg->renormalize ? 1 : 0;
   g.Dp = round_up(g.D, kBlockK);
+  g.Dp128 = round_up(g.D, 128);
   g.Np = round_up(g.N, kNeuronBlock);
   g.Sp = g.has_shared ? round_up(g.S, kNeuronBlock) : 0;
   g.Nh = g.Np > g.Sp ? g.Np : g.Sp;
@@ -268,11 +285,23 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out) {
     skb_layer_destroy(L);
     return rc;
   }
+  const size_t wdt_elems = static_cast<size_t>(g.E) * g.Dp128 * g.Np + static_cast<size_t>(g.Dp128) * g.Sp;
+  if (!rc) rc = dmalloc(&L->d_wdt, wdt_elems);
+  if (rc) {
+    skb_layer_destroy(L);
+    return rc;
+  }
   L->d_wd_shared = g.has_shared ? L->d_wd + static_cast<size_t>(g.E) * g.Np * g.Dp : nullptr;
-  L->weight_bytes = static_cast<uint64_t>(g.E) * g.D * 4 + (gu_rows + wd_rows) * g.Dp * 2;
+  L->d_wdt_shared = g.has_shared ? L->d_wdt + static_cast<size_t>(g.E) * g.Dp128 * g.Np : nullptr;
+  L->weight_bytes = static_cast<uint64_t>(g.E) * g.D * 4 + (gu_rows + wd_rows) * g.Dp * 2 + wdt_elems * 2;
+  cudaMemsetAsync(L->d_wdt, 0, wdt_elems * 2, L->stream);
   cudaMemsetAsync(L->d_wgu, 0, gu_rows * g.Dp * 2, L->stream);
   cudaMemsetAsync(L->d_wd, 0, wd_rows * g.Dp * 2, L->stream);
   rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows, g.Dp, 128);
+  if (!rc)
+    rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt, static_cast<uint64_t>(g.E) * g.Dp128, g.Np, 128);
+  if (!rc && g.has_shared)
+    rc = encode_bf16_2d(&L->tmap_wdt_shared, L->d_wdt_shared, g.Dp128, g.Sp, 128);
   if (rc) {
     skb_layer_destroy(L);
     return rc;
@@ -304,11 +333,45 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   StageTimer tm{L, timing, stream};
   int launches = 0;
 
-  // tile size for the grouped GEMM: ~1.5x the mean tokens per expert, power of two in [16, 256]
+  int sel_mode, n_off_r = 0, n_off_s = 0;
+  int max_keep = g.N > g.S ? g.N : g.S;
+  if (a->mode == SKB_MODE_DENSE) {
+    sel_mode = kSelectAll;
+  } else if (a->mode == SKB_MODE_TOPK) {
+    sel_mode = kSelectTopk;
+    n_off_r = n_off_of(a->s_routed, g.N);
+    n_off_s = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
+    const int kr = g.N - n_off_r, ks = g.S - n_off_s;
+    max_keep = kr > ks ? kr : ks;
+  } else {
+    sel_mode = kSelectGiven;
+  }
+
+  // Down-projection path.  Gathering surviving rows per (token, slot) moves B*K*keep rows out
+  // of L2; the dense masked GEMM reads each routed expert's W_down once from HBM.  The gather
+  // wins while a batch routes ~one token to each active expert (decode), the GEMM as soon as
+  // experts are shared by several tokens.  The decision depends only on (shape, batch, s), so
+  // it is identical for forward_dense and forward_topk_sparse at s = 0.
+  bool dense_down;
+  {
+    const double keep_r = sel_mode == kSelectTopk ? g.N - n_off_r : g.N;
+    const double keep_s = sel_mode == kSelectTopk ? g.S - n_off_s : g.S;
+    const double gather_rows = static_cast<double>(BK) * keep_r + (g.has_shared ? B * keep_s : 0.0);
+    const double dense_rows =
+        static_cast<double>(g.E < BK ? g.E : BK) * g.N + (g.has_shared ? g.S : 0.0);
+    dense_down = gather_rows > 1.5 * dense_rows;
+    if (a->flags & SKB_FLAG_GATHER_DOWN) dense_down = false;
+    if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
+  }
+  const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
+
+  // tile size for the grouped GEMMs: ~1.5x the mean tokens per expert, power of two in
+  // [16, 256] (at most 128 when the dense down projection shares the tile list)
   int tn = 16;
   {
     const double want = 1.5 * static_cast<double>(BK) / g.E;
-    while (tn < 256 && tn < want) tn <<= 1;
+    const int cap = dense_down ? 128 : 256;
+    while (tn < cap && tn < want) tn <<= 1;
   }
   int tn_idx = 0;
   while (kTileCases[tn_idx] != tn) ++tn_idx;
@@ -345,22 +408,10 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                                  L->d_h);
   tm.mark();
 
-  int sel_mode, n_off_r = 0, n_off_s = 0;
-  int max_keep = g.N > g.S ? g.N : g.S;
-  if (a->mode == SKB_MODE_DENSE) {
-    sel_mode = kSelectAll;
-  } else if (a->mode == SKB_MODE_TOPK) {
-    sel_mode = kSelectTopk;
-    n_off_r = n_off_of(a->s_routed, g.N);
-    n_off_s = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
-    const int kr = g.N - n_off_r, ks = g.S - n_off_s;
-    max_keep = kr > ks ? kr : ks;
-  } else {
-    sel_mode = kSelectGiven;
-  }
-  // The selection runs inside the down kernel; the stand-alone selection kernel only serves
-  // mask captures (MaskSet export).
-  if (d_mask_out_r != nullptr || d_mask_out_s != nullptr) {
+  // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel
+  // then only serves mask captures (MaskSet export).  Dense path: it writes the masked
+  // activations the GEMM consumes.
+  if (dense_down || d_mask_out_r != nullptr || d_mask_out_s != nullptr) {
     SelectArgs sa{};
     sa.h = L->d_h;
     sa.rows = rows;
@@ -370,9 +421,6 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sa.Nh = g.Nh;
     sa.K = g.K;
     sa.perm = L->disp.perm;
-    sa.kept_idx = L->d_kidx;
-    sa.kept_val = nullptr;
-    sa.kept_cnt = L->d_kcnt;
     sa.mask_out_routed = d_mask_out_r;
     sa.mask_out_shared = d_mask_out_s;
     sa.mode = sel_mode;
@@ -380,40 +428,54 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sa.n_off_shared = n_off_s;
     sa.mask_in_routed = d_mask_r;
     sa.mask_in_shared = d_mask_s;
+    if (dense_down) {
+      sa.hb = L->d_hb;
+      sa.hb_split_stride = static_cast<size_t>(L->xs_rows) * g.Nh;
+      sa.nsplit = nsplit;
+      sa.kext_routed = g.Np;
+      sa.kext_shared = g.Sp;
+    }
     launches += launch_select(ctx, sa);
   }
   tm.mark();
 
-  DownArgs da{};
-  da.wd = L->d_wd;
-  da.wd_shared = L->d_wd_shared;
-  da.row_expert = L->disp.row_expert;
-  da.inv = L->disp.inv;
-  da.weights = L->d_wts;
-  da.B = B;
-  da.K = g.K;
-  da.BK = BK;
-  da.has_shared = g.has_shared;
-  da.h = L->d_h;
-  da.Nh = g.Nh;
-  da.N = g.N;
-  da.S = g.S;
-  da.sel_mode = sel_mode;
-  da.n_off_routed = n_off_r;
-  da.n_off_shared = n_off_s;
-  da.mask_in_routed = d_mask_r;
-  da.mask_in_shared = d_mask_s;
-  da.max_keep = max_keep;
-  da.y = d_y;
-  {
+  if (dense_down) {
+    launches += launch_down_tc(ctx, &L->tmap_wdt, g.has_shared ? &L->tmap_wdt_shared : nullptr,
+                               L->tmap_hb[tn_idx], nsplit, tn, L->disp, max_tiles, g,
+                               L->d_slot_out);
+    tm.mark();
+    launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y);
+    tm.mark();
+  } else {
+    DownArgs da{};
+    da.wd = L->d_wd;
+    da.wd_shared = L->d_wd_shared;
+    da.row_expert = L->disp.row_expert;
+    da.inv = L->disp.inv;
+    da.weights = L->d_wts;
+    da.B = B;
+    da.K = g.K;
+    da.BK = BK;
+    da.has_shared = g.has_shared;
+    da.h = L->d_h;
+    da.Nh = g.Nh;
+    da.N = g.N;
+    da.S = g.S;
+    da.sel_mode = sel_mode;
+    da.n_off_routed = n_off_r;
+    da.n_off_shared = n_off_s;
+    da.mask_in_routed = d_mask_r;
+    da.mask_in_shared = d_mask_s;
+    da.max_keep = max_keep;
+    da.y = d_y;
     const int n = launch_down(ctx, da, g);
     if (n < 0)
       return fail(SKB_ECONFIG, "forward: top_k * d_ffn too large for the down-projection kernel's "
                                "shared-memory lists (K=%d, N=%d, S=%d)", g.K, g.N, g.S);
     launches += n;
+    tm.mark();
+    tm.mark();
   }
-  tm.mark();
-  tm.mark();
   L->last_launches = launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SKB_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -541,6 +603,8 @@ int skb_layer_create(const skb_config* cfg, const float* router, const float* co
                        L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
     if (e == cudaSuccess) e = cudaMemcpyAsync(sa, down_t[ex], bytes, cudaMemcpyHostToDevice, L->stream);
     launch_pack_rows(L->stream, sa, g.N, g.D, g.Dp, L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
+    launch_pack_down_t(L->stream, sa, g.N, g.D, g.Np,
+                       L->d_wdt + static_cast<size_t>(ex) * g.Dp128 * g.Np);
   }
   if (g.has_shared && e == cudaSuccess) {
     const size_t bytes = static_cast<size_t>(g.S) * g.D * 4;
@@ -550,6 +614,7 @@ int skb_layer_create(const skb_config* cfg, const float* router, const float* co
                        L->d_wgu + static_cast<size_t>(g.E) * 2 * g.Np * g.Dp);
     if (e == cudaSuccess) e = cudaMemcpyAsync(sa, shared_down_t, bytes, cudaMemcpyHostToDevice, L->stream);
     launch_pack_rows(L->stream, sa, g.S, g.D, g.Dp, L->d_wd_shared);
+    launch_pack_down_t(L->stream, sa, g.S, g.D, g.Sp, L->d_wdt_shared);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(L->stream);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -582,6 +647,8 @@ int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale
                         L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
     launch_synth_rows_bf16(L->stream, seed, scale, base + 2 * ND, g.N, g.Np, g.D, g.Dp,
                            L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
+    launch_synth_down_t(L->stream, seed, scale, base + 2 * ND, g.N, g.D, g.Np,
+                        L->d_wdt + static_cast<size_t>(ex) * g.Dp128 * g.Np);
   }
   if (g.has_shared) {
     const uint64_t base = ED + static_cast<uint64_t>(g.E) * 3 * ND;
@@ -589,6 +656,7 @@ int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale
                         L->d_wgu + static_cast<size_t>(g.E) * 2 * g.Np * g.Dp);
     launch_synth_rows_bf16(L->stream, seed, scale, base + 2 * SD, g.S, g.Sp, g.D, g.Dp,
                            L->d_wd_shared);
+    launch_synth_down_t(L->stream, seed, scale, base + 2 * SD, g.S, g.D, g.Sp, L->d_wdt_shared);
   }
   cudaError_t e = cudaStreamSynchronize(L->stream);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -608,6 +676,7 @@ void skb_layer_destroy(skb_layer* L) {
   if (L->d_router) cudaFree(L->d_router);
   if (L->d_wgu) cudaFree(L->d_wgu);
   if (L->d_wd) cudaFree(L->d_wd);
+  if (L->d_wdt) cudaFree(L->d_wdt);
   for (auto& ev : L->ev)
     if (ev) cudaEventDestroy(ev);
   if (L->stream) cudaStreamDestroy(L->stream);

@@ -16,6 +16,16 @@
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2-5 epilogue (TMEM lane quarter = warp_idx % 4).
+//
+// The same kernel, MODE 1, is the dense down projection used when a batch routes enough tokens
+// to every expert that gathering rows per token would re-read W_down from L2 many times over:
+//     D[128, TN] = A[128, Np] * B[TN, Np]^T
+//   A = 128 output columns of the expert's W_down^T image ([Dp128][Np], K-major);
+//   B = TN rows of the MASKED activations (dropped neurons are zeros) as bf16.  To keep the
+//       fp32-accumulation parity mode (1e-5), h is split into three bf16 terms b0+b1+b2 == h
+//       exactly; the three products accumulate into the same TMEM tile (nsplit = 3).  nsplit = 1
+//       is the bf16 mode (1e-2).
+//   D is stored un-weighted per row (slot); combine_rows_kernel applies the router weights.
 #include "skb_internal.cuh"
 
 namespace skb {
@@ -25,14 +35,18 @@ namespace {
 constexpr int kGateupThreads = 192;
 constexpr int kATileBytes = 128 * kBlockK * 2;  // 16 KB: 128 rows x 128 B
 
+constexpr int kMaxSplit = 3;
 __host__ __device__ constexpr int b_tile_bytes(int tn) { return tn * kBlockK * 2; }
-__host__ __device__ constexpr int stage_bytes(int tn) { return kATileBytes + b_tile_bytes(tn); }
-__host__ __device__ constexpr int num_stages(int tn) {
-  return tn <= 32 ? 10 : (tn <= 64 ? 8 : (tn <= 128 ? 6 : 4));
+__host__ __device__ constexpr int stage_bytes(int tn, int mode) {
+  return kATileBytes + (mode == 0 ? 1 : kMaxSplit) * b_tile_bytes(tn);
+}
+__host__ __device__ constexpr int num_stages(int tn, int mode) {
+  return mode == 0 ? (tn <= 32 ? 10 : (tn <= 64 ? 8 : (tn <= 128 ? 6 : 4)))
+                   : (tn <= 16 ? 9 : (tn <= 32 ? 7 : (tn <= 64 ? 5 : 3)));
 }
 __host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
-__host__ __device__ constexpr int gateup_smem_bytes(int tn) {
-  return num_stages(tn) * stage_bytes(tn) + 1024 /*alignment slack*/ + 256 /*barriers*/;
+__host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode) {
+  return num_stages(tn, mode) * stage_bytes(tn, mode) + 1024 /*alignment slack*/ + 256 /*barriers*/;
 }
 
 // ---- PTX wrappers (mbarrier helpers live in skb_internal.cuh) ----
@@ -125,18 +139,31 @@ __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g));
 
 }  // namespace
 
-template <int TN>
+struct TcArgs {
+  const int32_t* tile_expert;
+  const int32_t* tile_row0;
+  const int32_t* tile_nrows;
+  const int32_t* n_tiles;
+  float* out;       // MODE 0: h [rows][out_stride];  MODE 1: slot outputs [rows][out_stride]
+  int out_stride;
+  int n_experts;
+  int mblocks_routed, mblocks_shared;  // 128-row A blocks per routed expert / of the shared expert
+  int m_routed, m_shared;              // valid outputs: MODE 0 neurons (N, S); MODE 1 columns (D, D)
+  int kblocks_routed, kblocks_shared;  // 64-element K blocks
+  int rows_per_expert;                 // A-image rows per routed expert
+  int nsplit;                          // MODE 1: B operands accumulated per K block (1 or 3)
+};
+
+template <int TN, int MODE>
 __global__ void __launch_bounds__(kGateupThreads, 1)
-gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                        const __grid_constant__ CUtensorMap tmap_x,
-                        const int32_t* __restrict__ tile_expert,
-                        const int32_t* __restrict__ tile_row0,
-                        const int32_t* __restrict__ tile_nrows,
-                        const int32_t* __restrict__ n_tiles_ptr, float* __restrict__ h,
-                        int h_stride, int n_experts, int np_blocks, int sp_blocks, int N, int S,
-                        int num_k_blocks) {
-  constexpr int kStages = num_stages(TN);
-  constexpr int kStageBytes = stage_bytes(TN);
+grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                  const __grid_constant__ CUtensorMap tmap_a_shared,
+                  const __grid_constant__ CUtensorMap tmap_b0,
+                  const __grid_constant__ CUtensorMap tmap_b1,
+                  const __grid_constant__ CUtensorMap tmap_b2, const TcArgs a) {
+  constexpr int kStages = num_stages(TN, MODE);
+  constexpr int kStageBytes = stage_bytes(TN, MODE);
+  constexpr int kBTile = b_tile_bytes(TN);
   constexpr uint32_t kTmemCols = tmem_cols(TN);
   constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
 
@@ -156,8 +183,8 @@ gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
 
   // ---- prologue: nothing here reads memory written by the previous kernel ----
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmap_w);
-    tma_prefetch_desc(&tmap_x);
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b0);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
@@ -175,20 +202,26 @@ gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
   pdl_launch_dependents();
 
   const int tile = blockIdx.y;
-  bool active = tile < *n_tiles_ptr;
+  bool active = tile < *a.n_tiles;
   int e = 0, row0 = 0, nrows = 0;
+  bool shared_expert = false;
   if (active) {
-    e = tile_expert[tile];
-    row0 = tile_row0[tile];
-    nrows = tile_nrows[tile];
-    const int nblocks = (e < n_experts) ? np_blocks : sp_blocks;
-    active = static_cast<int>(blockIdx.x) < nblocks;
+    e = a.tile_expert[tile];
+    row0 = a.tile_row0[tile];
+    nrows = a.tile_nrows[tile];
+    shared_expert = e >= a.n_experts;
+    active = static_cast<int>(blockIdx.x) < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
   }
 
   if (active) {
-    // first image row of this (expert, neuron block): experts hold 2*Np rows each, the shared
-    // expert's 2*Sp rows follow the routed experts
-    const int a_row = ((e < n_experts) ? e * np_blocks : n_experts * np_blocks) * 128 +
+    const int num_k_blocks = shared_expert ? a.kblocks_shared : a.kblocks_routed;
+    const int nsplit = (MODE == 0) ? 1 : a.nsplit;
+    // first A-image row of this (expert, block).  MODE 0: the shared expert's rows follow the
+    // routed experts in one image; MODE 1: the shared expert has its own tensor map (its K
+    // extent differs).
+    const bool own_map = (MODE == 1) && shared_expert;
+    const CUtensorMap* map_a = own_map ? &tmap_a_shared : &tmap_a;
+    const int a_row = (own_map ? 0 : (shared_expert ? a.n_experts : e) * a.rows_per_expert) +
                       static_cast<int>(blockIdx.x) * 128;
 
     if (warp == 0) {
@@ -197,11 +230,17 @@ gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
           const int s = kb % kStages;
           const uint32_t ph = (kb / kStages) & 1u;
           mbar_wait(empty_bar(s), ph ^ 1u);
-          mbar_arrive_expect_tx(full_bar(s), kStageBytes);
+          mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * kBTile);
           const uint32_t a_smem = smem_base + s * kStageBytes;
-          tma_load_2d(a_smem, &tmap_w, kb * kBlockK, a_row, full_bar(s), kPolicyEvictFirst);
-          tma_load_2d(a_smem + kATileBytes, &tmap_x, kb * kBlockK, row0, full_bar(s),
+          tma_load_2d(a_smem, map_a, kb * kBlockK, a_row, full_bar(s), kPolicyEvictFirst);
+          tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s),
                       kPolicyEvictLast);
+          if (MODE == 1 && nsplit > 1) {
+            tma_load_2d(a_smem + kATileBytes + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
+                        kPolicyEvictLast);
+            tma_load_2d(a_smem + kATileBytes + 2 * kBTile, &tmap_b2, kb * kBlockK, row0,
+                        full_bar(s), kPolicyEvictLast);
+          }
         }
       }
     } else if (warp == 1) {
@@ -213,44 +252,64 @@ gateup_swiglu_tc_kernel(const __grid_constant__ CUtensorMap tmap_w,
           tc_fence_after();
           const uint32_t a_smem = smem_base + s * kStageBytes;
           const uint64_t a_desc = make_smem_desc_sw128(a_smem);
-          const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes);
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k) {
-            // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
-            umma_bf16(tmem_base, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
-                      (kb | k) != 0 ? 1u : 0u);
+          for (int sp = 0; sp < (MODE == 0 ? 1 : kMaxSplit); ++sp) {
+            if (sp < nsplit) {
+              const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes + sp * kBTile);
+#pragma unroll
+              for (int k = 0; k < kBlockK / 16; ++k) {
+                // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
+                umma_bf16(tmem_base, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
+                          (kb | k | sp) != 0 ? 1u : 0u);
+              }
+            }
           }
           umma_commit(empty_bar(s));
         }
         umma_commit(tmem_full_bar);
       }
     } else {
-      // ---- epilogue: TMEM -> registers -> SwiGLU -> h ----
+      // ---- epilogue: TMEM -> registers -> (SwiGLU) -> global ----
       const int q = warp & 3;  // TMEM lane quarter this warp may read
-      const int Ne = (e < n_experts) ? N : S;
-      const int n = static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15);
-      const bool is_gate_lane = lane < 16;
+      const int m_valid = shared_expert ? a.m_shared : a.m_routed;
       mbar_wait(tmem_full_bar, 0);
       tc_fence_after();
+      if (MODE == 0) {
+        const int n = static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15);
+        const bool is_gate_lane = lane < 16;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TN; c0 += 16) {
-        if (c0 >= nrows) break;
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
-        tmem_ld_wait();
+        for (int c0 = 0; c0 < TN; c0 += 16) {
+          if (c0 >= nrows) break;
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          // lanes 0-15 hold gate(n) for columns c, c+1; lanes 16-31 hold up(n).  One exchange:
-          // gate lanes finish column c, up lanes finish column c+1.
-          const float mine0 = __uint_as_float(v[c]);
-          const float mine1 = __uint_as_float(v[c + 1]);
-          const float send = is_gate_lane ? mine1 : mine0;
-          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-          const float g = is_gate_lane ? mine0 : recv;
-          const float u = is_gate_lane ? recv : mine1;
-          const int col = c0 + c + (is_gate_lane ? 0 : 1);
-          if (col < nrows && n < Ne)
-            h[static_cast<size_t>(row0 + col) * h_stride + n] = silu_f(g) * u;
+          for (int c = 0; c < 16; c += 2) {
+            // lanes 0-15 hold gate(n) for columns c, c+1; lanes 16-31 hold up(n).  One
+            // exchange: gate lanes finish column c, up lanes finish column c+1.
+            const float mine0 = __uint_as_float(v[c]);
+            const float mine1 = __uint_as_float(v[c + 1]);
+            const float send = is_gate_lane ? mine1 : mine0;
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+            const float g = is_gate_lane ? mine0 : recv;
+            const float u = is_gate_lane ? recv : mine1;
+            const int col = c0 + c + (is_gate_lane ? 0 : 1);
+            if (col < nrows && n < m_valid)
+              a.out[static_cast<size_t>(row0 + col) * a.out_stride + n] = silu_f(g) * u;
+          }
+        }
+      } else {
+        const int d = static_cast<int>(blockIdx.x) * 128 + 32 * q + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TN; c0 += 16) {
+          if (c0 >= nrows) break;
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c0 + c < nrows && d < m_valid)
+              a.out[static_cast<size_t>(row0 + c0 + c) * a.out_stride + d] = __uint_as_float(v[c]);
         }
       }
       tc_fence_before();
@@ -272,14 +331,14 @@ static int pick_tile_case(int tile_tokens) {
   return 256;
 }
 
-template <int TN>
-static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* tmap_w,
-                           const CUtensorMap* tmap_x, const DispatchBuffers& d, int max_tiles,
-                           const Geometry& g, float* h) {
+template <int TN, int MODE>
+static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
+                           const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
+                           const TcArgs& a, int grid_x, int max_tiles) {
   static bool attr_set = false;
-  constexpr int smem = gateup_smem_bytes(TN);
+  constexpr int smem = gateup_smem_bytes(TN, MODE);
   if (!attr_set) {
-    cudaFuncSetAttribute(gateup_swiglu_tc_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(grouped_tc_kernel<TN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     attr_set = true;
   }
@@ -290,25 +349,66 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* tmap_w,
   cfg.attrs = attr;
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
-  const int np_blocks = g.Np / kNeuronBlock, sp_blocks = g.Sp / kNeuronBlock;
-  cfg.gridDim = dim3(np_blocks > sp_blocks ? np_blocks : sp_blocks, max_tiles);
+  cfg.gridDim = dim3(grid_x, max_tiles);
   cfg.blockDim = dim3(kGateupThreads);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, gateup_swiglu_tc_kernel<TN>, *tmap_w, *tmap_x,
-                     (const int32_t*)d.tile_expert, (const int32_t*)d.tile_row0,
-                     (const int32_t*)d.tile_nrows, (const int32_t*)d.n_tiles, h, g.Nh, g.E,
-                     np_blocks, sp_blocks, g.N, g.S, g.Dp / kBlockK);
+  cudaLaunchKernelEx(&cfg, grouped_tc_kernel<TN, MODE>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
 }
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
                      float* h) {
+  TcArgs a{};
+  a.tile_expert = d.tile_expert;
+  a.tile_row0 = d.tile_row0;
+  a.tile_nrows = d.tile_nrows;
+  a.n_tiles = d.n_tiles;
+  a.out = h;
+  a.out_stride = g.Nh;
+  a.n_experts = g.E;
+  a.mblocks_routed = g.Np / kNeuronBlock;
+  a.mblocks_shared = g.Sp / kNeuronBlock;
+  a.m_routed = g.N;
+  a.m_shared = g.S;
+  a.kblocks_routed = a.kblocks_shared = g.Dp / kBlockK;
+  a.rows_per_expert = 2 * g.Np;
+  a.nsplit = 1;
+  const int gx = a.mblocks_routed > a.mblocks_shared ? a.mblocks_routed : a.mblocks_shared;
   switch (pick_tile_case(tile_tokens)) {
-    case 16: launch_tc_case<16>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
-    case 32: launch_tc_case<32>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
-    case 64: launch_tc_case<64>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
-    case 128: launch_tc_case<128>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
-    default: launch_tc_case<256>(ctx, tmap_w, tmap_x, d, max_tiles, g, h); break;
+    case 16: launch_tc_case<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    case 32: launch_tc_case<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    case 64: launch_tc_case<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    case 128: launch_tc_case<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    default: launch_tc_case<256, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+  }
+  return 1;
+}
+
+int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
+                   const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
+                   int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
+                   const Geometry& g, float* slot_out) {
+  TcArgs a{};
+  a.tile_expert = d.tile_expert;
+  a.tile_row0 = d.tile_row0;
+  a.tile_nrows = d.tile_nrows;
+  a.n_tiles = d.n_tiles;
+  a.out = slot_out;
+  a.out_stride = g.Dp;
+  a.n_experts = g.E;
+  a.mblocks_routed = a.mblocks_shared = g.Dp128 / 128;
+  a.m_routed = a.m_shared = g.D;
+  a.kblocks_routed = g.Np / kBlockK;
+  a.kblocks_shared = g.Sp / kBlockK;
+  a.rows_per_expert = g.Dp128;
+  a.nsplit = nsplit;
+  const CUtensorMap* sh = tmap_wdt_shared ? tmap_wdt_shared : tmap_wdt;
+  const int gx = a.mblocks_routed;
+  switch (pick_tile_case(tile_tokens)) {
+    case 16: launch_tc_case<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+    case 32: launch_tc_case<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+    case 64: launch_tc_case<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+    default: launch_tc_case<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
   }
   return 1;
 }

@@ -63,6 +63,31 @@ __global__ void synth_rows_kernel(uint64_t seed, float scale, uint64_t off, int 
         __float2bfloat16_rn(splitmix_symmetric(seed, off + static_cast<uint64_t>(n) * D + d, scale));
 }
 
+// W_down^T image for the dense down projection: dst[d][n] = bf16(down_t[n][d]), [Dp128][Kp]
+// (rows d >= D and columns n >= n_rows stay zero from the memset).
+__global__ void pack_down_t_kernel(const float* __restrict__ src, int n_rows, int D, int Kp,
+                                   __nv_bfloat16* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int n = n0 + j, d = d0 + threadIdx.x;
+    tile[j][threadIdx.x] = (n < n_rows && d < D) ? src[static_cast<size_t>(n) * D + d] : 0.0f;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int d = d0 + j, n = n0 + threadIdx.x;
+    if (d < D && n < n_rows) dst[static_cast<size_t>(d) * Kp + n] = __float2bfloat16_rn(tile[threadIdx.x][j]);
+  }
+}
+
+__global__ void synth_down_t_kernel(uint64_t seed, float scale, uint64_t off, int n_rows, int D,
+                                    int Kp, __nv_bfloat16* __restrict__ dst) {
+  const int d = blockIdx.x;
+  for (int n = threadIdx.x; n < n_rows; n += blockDim.x)
+    dst[static_cast<size_t>(d) * Kp + n] =
+        __float2bfloat16_rn(splitmix_symmetric(seed, off + static_cast<uint64_t>(n) * D + d, scale));
+}
+
 __global__ void synth_f32_kernel(uint64_t seed, float scale, uint64_t off, uint64_t count,
                                  float* __restrict__ dst) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -90,6 +115,17 @@ int launch_synth_gateup(cudaStream_t s, uint64_t seed, float scale, uint64_t off
 int launch_synth_rows_bf16(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows,
                            int /*n_rows_padded*/, int D, int Dp, __nv_bfloat16* dst) {
   synth_rows_kernel<<<n_rows, 256, 0, s>>>(seed, scale, off, D, Dp, dst);
+  return 1;
+}
+int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, int Kp,
+                       __nv_bfloat16* dst) {
+  pack_down_t_kernel<<<dim3(ceil_div(n_rows, 32), ceil_div(D, 32)), dim3(32, 8), 0, s>>>(
+      down_t, n_rows, D, Kp, dst);
+  return 1;
+}
+int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
+                        int Kp, __nv_bfloat16* dst) {
+  synth_down_t_kernel<<<D, 256, 0, s>>>(seed, scale, off, n_rows, D, Kp, dst);
   return 1;
 }
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,

@@ -655,6 +655,55 @@ __global__ void __launch_bounds__(256) combine_slots_kernel(const float* __restr
   y[static_cast<size_t>(t) * D + dd] = acc;
 }
 
+// Combine after the dense down projection: y[t] = sum_s w(t,s) * slot_out[row(t,s)] (slots
+// ascending, multiply and add rounded separately, router.cpp:119-130), shared expert last
+// (engine.cpp:168-173).  One thread per (token, 4 columns).
+__global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restrict__ slot_out,
+                                                           const int32_t* __restrict__ inv,
+                                                           const float* __restrict__ weights,
+                                                           int B, int K, int D, int Dp,
+                                                           int has_shared, float* __restrict__ y) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int t = blockIdx.y;
+  const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c4 >= D) return;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const bool vec = (c4 + 3 < D);
+#pragma unroll 4
+  for (int s = 0; s < K + has_shared; ++s) {
+    const int r = s < K ? inv[t * K + s] : B * K + t;
+    const float w = s < K ? weights[t * K + s] : 1.0f;
+    const float* p = slot_out + static_cast<size_t>(r) * Dp + c4;
+    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (vec) {
+      const float4 q = *reinterpret_cast<const float4*>(p);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      for (int i = 0; i < 4; ++i) if (c4 + i < D) v[i] = p[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w, v[i]));
+  }
+  for (int i = 0; i < 4; ++i) if (c4 + i < D) y[static_cast<size_t>(t) * D + c4 + i] = acc[i];
+}
+
+int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
+                        const float* weights, int B, const Geometry& g, float* y) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  cfg.stream = ctx.stream;
+  cfg.gridDim = dim3(ceil_div(ceil_div(g.D, 4), 256), B);
+  cfg.blockDim = dim3(256);
+  cudaLaunchKernelEx(&cfg, combine_rows_kernel, slot_out, inv, weights, B, g.K, g.D, g.Dp,
+                     g.has_shared, y);
+  return 1;
+}
+
 int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
                          int B, int K, int D, float* y) {
   combine_slots_kernel<<<dim3(ceil_div(D, 256), B), 256, 0, ctx.stream>>>(slot_outputs, weights,

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 
   const int slot = routed ? (a.perm ? a.perm[row] : row) : row - a.BK;
   const float* hrow = a.h + static_cast<size_t>(row) * a.Nh;
-  int32_t* kidx = a.kept_idx + static_cast<size_t>(row) * a.Nh;
+  int32_t* kidx = a.kept_idx ? a.kept_idx + static_cast<size_t>(row) * a.Nh : nullptr;
+  __nv_bfloat16* hb = a.hb ? a.hb + static_cast<size_t>(row) * a.Nh : nullptr;
   float* kval = a.kept_val ? a.kept_val + static_cast<size_t>(row) * a.Nh : nullptr;
   uint8_t* mout = routed ? (a.mask_out_routed ? a.mask_out_routed + static_cast<size_t>(slot) * n
                                               : nullptr)
@@ -65,7 +66,9 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 
   // ---- ordered compaction: rounds of 256 consecutive indices ----
   int kept_base = 0, tie_base = 0, buf = 0;
-  const int rounds = ceil_div(n, kSelectThreads);
+  // the dense down projection reads the masked row up to the K extent of its expert image
+  const int kext = hb ? (routed ? a.kext_routed : a.kext_shared) : n;
+  const int rounds = ceil_div(kext, kSelectThreads);
 #pragma unroll 1
   for (int r = 0; r < rounds; ++r) {
     const int i = r * kSelectThreads + tid;
@@ -99,13 +102,110 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
     const int pos = kept_base + sel_block_rank(keep, sc, buf, kept_total);
     buf ^= 1;
     kept_base += kept_total;
-    if (keep) {
+    if (keep && kidx) {
       kidx[pos] = i;
       if (kval) kval[pos] = hv;
     }
     if (mout && valid) mout[i] = keep ? 1 : 0;
+    if (hb && i < kext) {
+      // masked activation as bf16 terms b0 + b1 + b2 == h exactly (8 + 8 + 8 mantissa bits);
+      // nsplit == 1 keeps only the leading term (bf16 mode)
+      float v = keep ? hv : 0.0f;
+      for (int sp = 0; sp < a.nsplit; ++sp) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        hb[static_cast<size_t>(sp) * a.hb_split_stride + i] = b;
+        v = __fsub_rn(v, __bfloat162float(b));
+      }
+    }
   }
-  if (tid == 0) a.kept_cnt[row] = kept_base;
+  if (tid == 0 && a.kept_cnt) a.kept_cnt[row] = kept_base;
+}
+
+// One warp per row, 8 rows per CTA, keys and values in registers (rows of up to 1024 neurons).
+// Same outputs as select_rows_kernel, bit for bit; no block barriers.
+template <int NPL>
+__global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(SelectArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * kSelWarps + warp;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (row >= a.rows) return;
+  const bool routed = row < a.BK;
+  const int n = routed ? a.N : a.S;
+  const int slot = routed ? (a.perm ? a.perm[row] : row) : row - a.BK;
+  const float* hrow = a.h + static_cast<size_t>(row) * a.Nh;
+  int32_t* kidx = a.kept_idx ? a.kept_idx + static_cast<size_t>(row) * a.Nh : nullptr;
+  float* kval = a.kept_val ? a.kept_val + static_cast<size_t>(row) * a.Nh : nullptr;
+  __nv_bfloat16* hb = a.hb ? a.hb + static_cast<size_t>(row) * a.Nh : nullptr;
+  uint8_t* mout = routed ? (a.mask_out_routed ? a.mask_out_routed + static_cast<size_t>(slot) * n
+                                              : nullptr)
+                         : (a.mask_out_shared ? a.mask_out_shared + static_cast<size_t>(slot) * n
+                                              : nullptr);
+  const uint8_t* min_ = nullptr;
+  int mode = a.mode;
+  if (mode == kSelectGiven) {
+    min_ = routed ? a.mask_in_routed + static_cast<size_t>(slot) * n
+                  : (a.mask_in_shared ? a.mask_in_shared + static_cast<size_t>(slot) * n : nullptr);
+    if (min_ == nullptr) mode = kSelectAll;
+  }
+  int n_off = 0;
+  if (mode == kSelectTopk) {
+    n_off = a.counts ? a.counts[row] : (routed ? a.n_off_routed : a.n_off_shared);
+    if (n_off <= 0) mode = kSelectAll;  // activation.cpp:35
+  }
+  const bool drop_everything = (mode == kSelectTopk) && n_off >= n;  // activation.cpp:36-39
+
+  float hv[NPL];
+  uint32_t kr[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int i = j * 32 + lane;
+    hv[j] = (i < n) ? hrow[i] : 0.0f;
+    kr[j] = (i < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
+  }
+  RowPick pk{0u, 0, true};
+  if (mode == kSelectTopk && !drop_everything) pk = warp_binary_pick<NPL>(kr, n_off);
+
+  const int kext = hb ? (routed ? a.kext_routed : a.kext_shared) : n;
+  const unsigned lt = (1u << lane) - 1u;
+  int kept_base = 0, tie_base = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int i = j * 32 + lane;
+    if (j * 32 >= kext && j * 32 >= n) break;  // warp-uniform
+    const bool valid = i < n;
+    bool keep;
+    if (mode == kSelectAll) {
+      keep = valid;
+    } else if (mode == kSelectGiven) {
+      keep = valid && (min_[i] != 0);
+    } else if (drop_everything) {
+      keep = false;
+    } else {
+      const bool tie = valid && kr[j] == pk.pivot;
+      const unsigned tb = __ballot_sync(0xffffffffu, tie);
+      const int tie_rank = tie_base + __popc(tb & lt);
+      tie_base += __popc(tb);
+      keep = valid && (kr[j] > pk.pivot || (tie && tie_rank >= pk.ties_to_drop));
+    }
+    const unsigned kb = __ballot_sync(0xffffffffu, keep);
+    const int pos = kept_base + __popc(kb & lt);
+    kept_base += __popc(kb);
+    if (keep && kidx) {
+      kidx[pos] = i;
+      if (kval) kval[pos] = hv[j];
+    }
+    if (mout && valid) mout[i] = keep ? 1 : 0;
+    if (hb && i < kext) {
+      float v = keep ? hv[j] : 0.0f;
+      for (int sp = 0; sp < a.nsplit; ++sp) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        hb[static_cast<size_t>(sp) * a.hb_split_stride + i] = b;
+        v = __fsub_rn(v, __bfloat162float(b));
+      }
+    }
+  }
+  if (lane == 0 && a.kept_cnt) a.kept_cnt[row] = kept_base;
 }
 
 int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
@@ -116,9 +216,20 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
   cfg.attrs = attr;
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
-  cfg.gridDim = dim3(a.rows);
   cfg.blockDim = dim3(kSelectThreads);
   const int nmax = a.N > a.S ? a.N : a.S;
+  const int kmax = a.hb ? (a.kext_routed > a.kext_shared ? a.kext_routed : a.kext_shared) : nmax;
+  const int span = nmax > kmax ? nmax : kmax;
+  // Many rows: one warp per row (throughput).  Few rows, or rows too long for registers: one
+  // CTA per row (latency).
+  if (span <= 1024 && a.rows >= 64) {
+    cfg.gridDim = dim3(ceil_div(a.rows, kSelWarps));
+    if (span <= 256) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<8>, a);
+    else if (span <= 512) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<16>, a);
+    else cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<32>, a);
+    return 1;
+  }
+  cfg.gridDim = dim3(a.rows);
   cfg.dynamicSmemBytes = static_cast<size_t>(nmax) * sizeof(uint32_t);
   cudaLaunchKernelEx(&cfg, select_rows_kernel, a);
   return 1;

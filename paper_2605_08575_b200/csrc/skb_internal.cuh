@@ -29,6 +29,7 @@ struct Geometry {
   int E, K, D, N, S;
   int has_shared, renorm;
   int Dp;  // D rounded up to kBlockK (zero padded)
+  int Dp128;  // D rounded up to 128: rows per expert of the W_down^T image
   int Np;  // N rounded up to kNeuronBlock
   int Sp;  // S rounded up to kNeuronBlock (0 when no shared expert)
   int Nh;  // row stride of h / kept lists: max(Np, Sp)
@@ -79,6 +80,12 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
                      float* h);
+int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
+                   const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
+                   int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
+                   const Geometry& g, float* slot_out);
+int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
+                        const float* weights, int B, const Geometry& g, float* y);
 int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
                        const int32_t* row_expert, int rows, const Geometry& g, float* h);
 
@@ -95,9 +102,14 @@ struct SelectArgs {
   const uint8_t* mask_in_shared; // kSelectGiven: [B][S] or NULL (=> keep all)
   uint8_t* mask_out_routed;      // optional [B*K][N] slot-major
   uint8_t* mask_out_shared;      // optional [B][S]
-  int32_t* kept_idx;             // [rows][Nh]
-  float* kept_val;               // [rows][Nh]
-  int32_t* kept_cnt;             // [rows]
+  int32_t* kept_idx;             // optional [rows][Nh]
+  float* kept_val;               // optional [rows][Nh]
+  int32_t* kept_cnt;             // optional [rows]
+  // dense down projection: masked activations as nsplit bf16 terms, [nsplit][rows][Nh]
+  __nv_bfloat16* hb;
+  size_t hb_split_stride;        // rows * Nh
+  int nsplit;
+  int kext_routed, kext_shared;  // columns written per row (Np / Sp; pad columns are zeros)
 };
 int launch_select(const LaunchCtx& ctx, const SelectArgs& a);
 
@@ -131,6 +143,10 @@ int launch_synth_gateup(cudaStream_t s, uint64_t seed, float scale, uint64_t off
                         __nv_bfloat16* dst);
 int launch_synth_rows_bf16(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows,
                            int n_rows_padded, int D, int Dp, __nv_bfloat16* dst);
+int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, int Kp,
+                       __nv_bfloat16* dst);
+int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
+                        int Kp, __nv_bfloat16* dst);
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
                      float* dst);
 

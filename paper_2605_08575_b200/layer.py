@@ -18,7 +18,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import (FLAG_FAST_ROUTER, FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,  # noqa: F401
+from ._lib import (FLAG_BF16_H, FLAG_DENSE_DOWN, FLAG_FAST_ROUTER, FLAG_GATHER_DOWN,  # noqa: F401
+                   FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,
                    MODE_DENSE, MODE_MASKED, MODE_TOPK, STAGE_NAMES, SkbConfig, SkbForwardArgs,
                    SkbReport)
 
