@@ -41,7 +41,10 @@ __host__ __device__ constexpr int stage_bytes(int tn, int mode) {
   return kATileBytes + (mode == 0 ? 1 : kMaxSplit) * b_tile_bytes(tn);
 }
 __host__ __device__ constexpr int num_stages(int tn, int mode) {
-  return mode == 0 ? (tn <= 32 ? 10 : (tn <= 64 ? 8 : (tn <= 128 ? 6 : 4)))
+  // MODE 0: <= ~110 KB per CTA so that two CTAs share an SM (grids larger than the SM count then
+  // run in one wave and one CTA's prologue/epilogue overlaps the other's stream); ~100 KB in
+  // flight per CTA is still several times the latency-bandwidth product per SM.
+  return mode == 0 ? (tn <= 16 ? 6 : (tn <= 32 ? 5 : (tn <= 64 ? 4 : (tn <= 128 ? 3 : 2))))
                    : (tn <= 16 ? 9 : (tn <= 32 ? 7 : (tn <= 64 ? 5 : 3)));
 }
 __host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
@@ -155,7 +158,7 @@ struct TcArgs {
 };
 
 template <int TN, int MODE>
-__global__ void __launch_bounds__(kGateupThreads, 1)
+__global__ void __launch_bounds__(kGateupThreads, MODE == 0 ? 2 : 1)
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,

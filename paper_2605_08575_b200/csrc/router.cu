@@ -66,6 +66,40 @@ __device__ void warp_route_token(const float* __restrict__ row, int E, int K, in
   for (int e = lane; e < E; e += 32) sc[e] = __fdiv_rn(sc[e], denom);
   __syncwarp();
   float selected_sum = 0.0f;
+  if (E <= 128) {
+    // rank of every probability under the reference's total order (probability descending,
+    // expert id ascending on ties) by direct counting: no serial arg-max rounds.  Each lane
+    // owns experts lane, lane+32, ...; the E probabilities are read as shared-memory broadcasts.
+    float mine[4];
+    int rank[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mine[j] = (j * 32 + lane < E) ? sc[j * 32 + lane] : -1.0f;
+      rank[j] = 0;
+    }
+    for (int e = 0; e < E; ++e) {
+      const float v = sc[e];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int me = j * 32 + lane;
+        rank[j] += (v > mine[j] || (v == mine[j] && e < me)) ? 1 : 0;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int me = j * 32 + lane;
+      if (me < E && rank[j] < K) {
+        out_ids[rank[j]] = me;
+        out_w[rank[j]] = mine[j];
+        sc[E + rank[j]] = mine[j];  // scratch holds E + K floats
+      }
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int s = 0; s < K; ++s) selected_sum = __fadd_rn(selected_sum, sc[E + s]);
+    selected_sum = __shfl_sync(0xffffffffu, selected_sum, 0);
+  } else {
   for (int s = 0; s < K; ++s) {
     float bp = -3.0f;
     int be = 0x7fffffff;
@@ -92,6 +126,7 @@ __device__ void warp_route_token(const float* __restrict__ row, int E, int K, in
     }
     selected_sum = __fadd_rn(selected_sum, bp);
     __syncwarp();
+  }
   }
   if (renorm)
     for (int s = lane; s < K; s += 32) out_w[s] = __fdiv_rn(out_w[s], selected_sum);
@@ -158,11 +193,28 @@ __device__ void warp_small_dispatch(const int32_t* __restrict__ ids, int B, int 
   if (lane == 0) *d.n_tiles = n_tiles;
 }
 
+// route() for batches: one warp per token, 4 tokens per CTA.
+__global__ void __launch_bounds__(128) route_tokens_kernel(const float* __restrict__ logits, int B,
+                                                           int E, int K, int renorm,
+                                                           int32_t* __restrict__ ids,
+                                                           float* __restrict__ weights) {
+  extern __shared__ float rt_smem[];  // [4][E + K]
+  const int warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 4 + warp;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (t >= B) return;
+  warp_route_token(logits + static_cast<size_t>(t) * E, E, K, renorm,
+                   rt_smem + static_cast<size_t>(warp) * (E + K), ids + static_cast<size_t>(t) * K,
+                   weights + static_cast<size_t>(t) * K);
+}
+
 struct RouterFusedArgs {
   const float* x;
   const float* router;
   int B, E, D, K, renorm;
   int logits_ready;   // 1: logits were produced by the fast kernel; skip the chains
+  int fuse_route;     // 1: the last CTA of a token block runs route() (decode); 0: route_tokens_kernel
   int fuse_dispatch;  // 1: the last CTA also builds the dispatch (B*K <= kSmallSlots)
   int has_shared, tile_tokens;
   float* logits;
@@ -286,6 +338,7 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
     if (lane == 0) g_rf_dbg[9] = t_wait;
     if (valid) a.logits[static_cast<size_t>(t0 + t_j) * a.E + e0 + e_i] = acc;
 
+    if (!a.fuse_route) return;
     // last arriver of this token block runs route() for its tokens
     __threadfence();
     __syncwarp();
@@ -391,7 +444,10 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   a.K = r.K;
   a.renorm = r.renorm;
   a.logits_ready = (r.fast || r.x == nullptr) ? 1 : 0;
-  a.fuse_dispatch = (r.dispatch != nullptr && r.B * r.K <= kSmallSlots) ? 1 : 0;
+  // decode batches: everything in the router kernel (no launch boundaries); larger batches:
+  // route() and the dispatch are parallel kernels of their own
+  a.fuse_route = (r.B <= 2 * kRfTB) ? 1 : 0;
+  a.fuse_dispatch = (a.fuse_route && r.dispatch != nullptr && r.B * r.K <= kSmallSlots) ? 1 : 0;
   a.has_shared = r.has_shared;
   a.tile_tokens = r.tile_tokens;
   a.logits = r.logits;
@@ -399,11 +455,21 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   a.weights = r.weights;
   a.counters = r.counters;
   if (r.dispatch) a.d = *r.dispatch;
-  cfg.gridDim = dim3(a.logits_ready ? 1 : ceil_div(r.E, kRfEB), ceil_div(r.B, kRfTB));
-  cfg.blockDim = dim3(64);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, router_fused_kernel, a);
-  ++launches;
+  if (!(a.logits_ready && !a.fuse_route)) {
+    cfg.gridDim = dim3(a.logits_ready ? 1 : ceil_div(r.E, kRfEB), ceil_div(r.B, kRfTB));
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchKernelEx(&cfg, router_fused_kernel, a);
+    ++launches;
+  }
+  if (!a.fuse_route) {
+    cfg.gridDim = dim3(ceil_div(r.B, 4));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = 4 * static_cast<size_t>(r.E + r.K) * sizeof(float);
+    cudaLaunchKernelEx(&cfg, route_tokens_kernel, (const float*)r.logits, r.B, r.E, r.K, r.renorm,
+                       r.ids, r.weights);
+    ++launches;
+  }
   if (r.dispatch != nullptr && !a.fuse_dispatch)
     launches += launch_dispatch(ctx, r.ids, r.B, r.K, r.E, r.has_shared, r.tile_tokens, *r.dispatch);
   return launches;
