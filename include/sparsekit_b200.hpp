@@ -1,0 +1,305 @@
+// sparsekit_b200.hpp -- C++ facade: the reference's layer API on top of the C ABI.
+//
+// Same names, signatures, value types and exception types as the reference
+// (proj/include/sparsekit/{engine,router,activation,profiler}.hpp), in namespace
+// sparsekit::b200, so a call site switches with one `using` / namespace change:
+//
+//     sparsekit::forward_dense(w, x, threads)        ->  sparsekit::b200::forward_dense(w, x, threads)
+//     sparsekit::forward_masked_dense(w, x, masks)   ->  sparsekit::b200::forward_masked_dense(...)
+//     sparsekit::build_topk_masks(w, x, s, mode)     ->  sparsekit::b200::build_topk_masks(...)
+//     route / align_dispatch / combine / topk_mask / mask_smallest_magnitudes likewise
+//
+// plus forward_topk_sparse(w, x, s_routed, s_shared), the fused entry the reference lacks
+// (== forward_masked_dense(w, x, build_topk_masks(w, x, s, mode)) with the selection done on
+// the device and the masked W_down rows never read).
+//
+// Header-only; link libsparsekit_b200.so.  With the reference tree on the include path the
+// reference's own headers provide the types, otherwise sparsekit_b200_types.hpp does.
+//
+// The device weight image is cached per MoELayerWeights instance (keyed on its address, shape
+// and a content stamp) so repeated forwards upload nothing; release(w) or clear_cache() drops it.
+#pragma once
+
+#if __has_include("sparsekit/engine.hpp")
+#include "sparsekit/activation.hpp"
+#include "sparsekit/engine.hpp"
+#include "sparsekit/profiler.hpp"
+#include "sparsekit/router.hpp"
+#else
+#include "sparsekit_b200_types.hpp"
+#endif
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sparsekit_b200.h"
+
+namespace sparsekit {
+namespace b200 {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+
+// C status codes back to the reference exception types (errors.hpp:12-43)
+inline void check(int rc) {
+  if (rc == SKB_OK) return;
+  const std::string msg = skb_last_error();
+  switch (rc) {
+    case SKB_ESHAPE: throw ShapeError(msg);
+    case SKB_ECONFIG: throw ConfigError(msg);
+    case SKB_EINDEX: throw IndexError(msg);
+    case SKB_EINTERNAL: throw InternalError(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+inline skb_config to_c(const MoEConfig& c) {
+  return skb_config{c.n_experts, c.top_k,    c.d_model,          c.d_ffn,
+                    c.has_shared ? 1 : 0, c.d_shared, c.renormalize ? 1 : 0, c.align_block};
+}
+
+struct Entry {
+  skb_layer* layer = nullptr;
+  std::uint64_t stamp = 0;
+};
+
+inline std::mutex& cache_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<const MoELayerWeights*, Entry>& cache() {
+  static std::map<const MoELayerWeights*, Entry> c;
+  return c;
+}
+
+// cheap content stamp: shape + a few words of every matrix (weights are immutable after load,
+// SPEC.md:124; the stamp only guards against an address being reused by another model)
+inline std::uint64_t stamp_of(const MoELayerWeights& w) {
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, std::size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  const skb_config c = to_c(w.config);
+  mix(&c, sizeof(c));
+  auto sample = [&](const Matrix& m) {
+    const std::size_t n = m.data.size();
+    if (n == 0) return;
+    const std::size_t k = n < 16 ? n : 16;
+    mix(m.data.data(), k * sizeof(float));
+    mix(m.data.data() + (n - k), k * sizeof(float));
+    const void* addr = m.data.data();
+    mix(&addr, sizeof(addr));
+  };
+  sample(w.router);
+  for (const Matrix& m : w.gate) sample(m);
+  for (const Matrix& m : w.up) sample(m);
+  for (const Matrix& m : w.down_t) sample(m);
+  sample(w.shared_gate);
+  sample(w.shared_up);
+  sample(w.shared_down_t);
+  return h;
+}
+
+inline skb_layer* layer_for(const MoELayerWeights& w, int device = 0) {
+  std::lock_guard<std::mutex> lk(cache_mutex());
+  const std::uint64_t st = stamp_of(w);
+  Entry& e = cache()[&w];
+  if (e.layer != nullptr && e.stamp == st) return e.layer;
+  if (e.layer != nullptr) {
+    skb_layer_destroy(e.layer);
+    e.layer = nullptr;
+  }
+  const MoEConfig& c = w.config;
+  const skb_config cc = to_c(c);
+  check(skb_config_validate(&cc));
+  const std::size_t E = static_cast<std::size_t>(c.n_experts);
+  auto want = [&](const Matrix& m, int r, const char* what) {
+    if (m.rows != r || m.cols != c.d_model ||
+        m.data.size() != static_cast<std::size_t>(r) * c.d_model)
+      throw ShapeError(std::string("weights: ") + what + " has the wrong shape");
+  };
+  want(w.router, c.n_experts, "router");
+  if (w.gate.size() != E || w.up.size() != E || w.down_t.size() != E)
+    throw ShapeError("weights: expected one gate/up/down_t matrix per expert");
+  std::vector<const float*> g(E), u(E), d(E);
+  for (std::size_t i = 0; i < E; ++i) {
+    want(w.gate[i], c.d_ffn, "gate");
+    want(w.up[i], c.d_ffn, "up");
+    want(w.down_t[i], c.d_ffn, "down_t");
+    g[i] = w.gate[i].data.data();
+    u[i] = w.up[i].data.data();
+    d[i] = w.down_t[i].data.data();
+  }
+  const float *sg = nullptr, *su = nullptr, *sd = nullptr;
+  if (c.has_shared) {
+    want(w.shared_gate, c.d_shared, "shared_gate");
+    want(w.shared_up, c.d_shared, "shared_up");
+    want(w.shared_down_t, c.d_shared, "shared_down_t");
+    sg = w.shared_gate.data.data();
+    su = w.shared_up.data.data();
+    sd = w.shared_down_t.data.data();
+  }
+  skb_layer* L = nullptr;
+  check(skb_layer_create(&cc, w.router.data.data(), g.data(), u.data(), d.data(), sg, su, sd,
+                         device, &L));
+  e.layer = L;
+  e.stamp = st;
+  return L;
+}
+
+inline ForwardReport run(const MoELayerWeights& w, const Matrix& x, skb_forward_args a,
+                         MaskSet* masks_out = nullptr) {
+  const MoEConfig& c = w.config;
+  if (x.cols != c.d_model)  // engine.cpp:98-101
+    throw ShapeError("forward: token width does not match d_model");
+  skb_layer* L = layer_for(w);
+  ForwardReport rep;
+  rep.outputs = Matrix(x.rows, c.d_model);
+  a.batch = x.rows;
+  a.x = x.data.data();
+  a.y = rep.outputs.data.data();
+  if (masks_out != nullptr) {
+    masks_out->routed.assign(static_cast<std::size_t>(x.rows) * c.top_k * c.d_ffn, 0);
+    a.routed_mask_out = masks_out->routed.data();
+    if (c.has_shared) {
+      masks_out->shared.assign(static_cast<std::size_t>(x.rows) * c.d_shared, 0);
+      a.shared_mask_out = masks_out->shared.data();
+    }
+  }
+  skb_report r{};
+  check(skb_layer_forward(L, &a, &r));
+  rep.macs.gate_macs = r.gate_macs;
+  rep.macs.up_macs = r.up_macs;
+  rep.macs.down_macs = r.down_macs;
+  rep.macs.other_macs = r.other_macs;
+  rep.active_neurons_total = r.active_neurons_total;
+  rep.achieved_routed_sparsity = r.achieved_routed_sparsity;
+  rep.tiles_total = r.tiles_total;
+  rep.tiles_skipped = r.tiles_skipped;
+  rep.path_used = r.path_used ? ExecPath::kSparse : ExecPath::kDense;
+  return rep;
+}
+
+}  // namespace detail
+
+// Drops the cached device image of `w` (call before destroying or mutating it).
+inline void release(const MoELayerWeights& w) {
+  std::lock_guard<std::mutex> lk(detail::cache_mutex());
+  auto it = detail::cache().find(&w);
+  if (it != detail::cache().end()) {
+    skb_layer_destroy(it->second.layer);
+    detail::cache().erase(it);
+  }
+}
+inline void clear_cache() {
+  std::lock_guard<std::mutex> lk(detail::cache_mutex());
+  for (auto& kv : detail::cache()) skb_layer_destroy(kv.second.layer);
+  detail::cache().clear();
+}
+
+// engine.hpp:38-39.  `threads` is accepted for signature parity and ignored.
+inline ForwardReport forward_dense(const MoELayerWeights& w, const Matrix& x, int /*threads*/ = 1) {
+  skb_forward_args a{};
+  a.mode = SKB_MODE_DENSE;
+  return detail::run(w, x, a);
+}
+
+// engine.hpp:43-44
+inline ForwardReport forward_masked_dense(const MoELayerWeights& w, const Matrix& x,
+                                          const MaskSet& masks, int /*threads*/ = 1) {
+  skb_forward_args a{};
+  a.mode = SKB_MODE_MASKED;
+  a.routed_mask_in = masks.routed.data();
+  a.routed_mask_len = masks.routed.size();
+  a.shared_mask_in = masks.shared.empty() ? nullptr : masks.shared.data();
+  a.shared_mask_len = masks.shared.size();
+  return detail::run(w, x, a);
+}
+
+// The fused top-k path.  s_shared = 0 leaves the shared expert dense (SweepMode::kRoutedOnly);
+// pass the same level as s_routed for kRoutedAndShared.
+inline ForwardReport forward_topk_sparse(const MoELayerWeights& w, const Matrix& x,
+                                         SparsityLevel s_routed,
+                                         SparsityLevel s_shared = SparsityLevel(0.0),
+                                         int /*threads*/ = 1, MaskSet* masks_out = nullptr) {
+  skb_forward_args a{};
+  a.mode = SKB_MODE_TOPK;
+  a.s_routed = s_routed.s;
+  a.s_shared = s_shared.s;
+  return detail::run(w, x, a, masks_out);
+}
+
+// profiler.hpp:71-72
+inline MaskSet build_topk_masks(const MoELayerWeights& w, const Matrix& tokens, SparsityLevel s,
+                                SweepMode mode) {
+  MaskSet m;
+  const bool rs = mode == SweepMode::kRoutedAndShared && w.config.has_shared;
+  forward_topk_sparse(w, tokens, s, rs ? s : SparsityLevel(0.0), 1, &m);
+  if (!rs) m.shared.clear();
+  return m;
+}
+
+// router.hpp:34
+inline RouteResult route(const Matrix& logits, int top_k, bool renormalize) {
+  RouteResult r;
+  r.batch = logits.rows;
+  r.top_k = top_k;
+  const std::size_t n = static_cast<std::size_t>(logits.rows > 0 ? logits.rows : 0) *
+                        static_cast<std::size_t>(top_k > 0 ? top_k : 0);
+  r.ids.assign(n, 0);
+  r.weights.assign(n, 0.0f);
+  detail::check(skb_route(logits.data.data(), logits.rows, logits.cols, top_k, renormalize ? 1 : 0,
+                          r.ids.data(), r.weights.data()));
+  return r;
+}
+
+// router.hpp:46-47
+inline DispatchPlan align_dispatch(const RouteResult& r, int n_experts, int block) {
+  DispatchPlan p;
+  p.block_size = block;
+  const std::size_t cap = r.ids.size() + static_cast<std::size_t>(n_experts) *
+                                             static_cast<std::size_t>(block > 1 ? block - 1 : 0) + 1;
+  p.sorted_token_slots.assign(cap, 0);
+  p.expert_of_block.assign(cap, 0);
+  std::int32_t n_padded = 0, n_blocks = 0;
+  detail::check(skb_align_dispatch(r.ids.data(), r.batch, r.top_k, n_experts, block,
+                                   p.sorted_token_slots.data(), p.expert_of_block.data(),
+                                   &n_padded, &n_blocks));
+  p.sorted_token_slots.resize(static_cast<std::size_t>(n_padded));
+  p.expert_of_block.resize(static_cast<std::size_t>(n_blocks));
+  p.n_padded = n_padded;
+  return p;
+}
+
+// router.hpp:52-53 (pointer + length instead of std::span so that C++17 callers compile too)
+inline Matrix combine(const float* slot_outputs, std::size_t n, const RouteResult& r, int d_model) {
+  if (n != static_cast<std::size_t>(r.batch) * r.top_k * d_model)
+    throw InternalError("combine: slot output count does not match batch * top_k * d_model");
+  Matrix y(r.batch, d_model);
+  detail::check(skb_combine(slot_outputs, r.weights.data(), r.batch, r.top_k, d_model,
+                            y.data.data()));
+  return y;
+}
+
+// activation.hpp:35-39
+inline std::vector<std::uint8_t> mask_smallest_magnitudes(const float* h, std::size_t n, int count) {
+  std::vector<std::uint8_t> mask(n);
+  const std::int32_t c = count;
+  detail::check(skb_mask_smallest(h, 1, static_cast<int>(n), &c, mask.data(), nullptr, nullptr));
+  return mask;
+}
+inline std::vector<std::uint8_t> topk_mask(const float* h, std::size_t n, SparsityLevel s) {
+  std::vector<std::uint8_t> mask(n);
+  detail::check(skb_topk_mask(h, 1, static_cast<int>(n), s.s, mask.data()));
+  return mask;
+}
+
+}  // namespace b200
+}  // namespace sparsekit

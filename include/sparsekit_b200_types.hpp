@@ -1,0 +1,101 @@
+// sparsekit_b200_types.hpp -- stand-in value types for building the C++ facade WITHOUT the
+// reference headers (this repository's own tests, the GPU box).
+//
+// When the reference tree is on the include path, sparsekit_b200.hpp includes the reference's
+// own headers instead and this file is not used.  Field names and meanings follow
+//   MoEConfig / MoELayerWeights   proj/include/sparsekit/model.hpp:15-43
+//   Matrix / MacCounter           proj/include/sparsekit/linalg.hpp:17-70
+//   RouteResult / DispatchPlan    proj/include/sparsekit/router.hpp:20-44
+//   SparsityLevel                 proj/include/sparsekit/activation.hpp:15-23
+//   ForwardReport / MaskSet       proj/include/sparsekit/engine.hpp:19-34
+//   SweepMode                     proj/include/sparsekit/profiler.hpp:38
+//   exception types               proj/include/sparsekit/errors.hpp:12-43
+// so that code written against the reference compiles against either.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sparsekit {
+
+struct ShapeError : std::invalid_argument {
+  explicit ShapeError(const std::string& m) : std::invalid_argument(m) {}
+};
+struct IndexError : std::out_of_range {
+  explicit IndexError(const std::string& m) : std::out_of_range(m) {}
+};
+struct ConfigError : std::invalid_argument {
+  explicit ConfigError(const std::string& m) : std::invalid_argument(m) {}
+};
+struct InternalError : std::logic_error {
+  explicit InternalError(const std::string& m) : std::logic_error(m) {}
+};
+
+struct Matrix {
+  int rows = 0, cols = 0;
+  std::vector<float> data;
+  Matrix() = default;
+  Matrix(int r, int c) : rows(r), cols(c), data(static_cast<std::size_t>(r) * c, 0.0f) {}
+  float& at(int r, int c) { return data[static_cast<std::size_t>(r) * cols + c]; }
+  float at(int r, int c) const { return data[static_cast<std::size_t>(r) * cols + c]; }
+};
+
+struct MacCounter {
+  std::uint64_t gate_macs = 0, up_macs = 0, down_macs = 0, other_macs = 0;
+  std::uint64_t total() const { return gate_macs + up_macs + down_macs + other_macs; }
+};
+
+struct MoEConfig {
+  int n_experts = 1, top_k = 1, d_model = 1, d_ffn = 1;
+  bool has_shared = false;
+  int d_shared = 0;
+  bool renormalize = true;
+  int align_block = 64;
+  static constexpr int kTile = 64;
+};
+
+struct MoELayerWeights {
+  MoEConfig config;
+  Matrix router;
+  std::vector<Matrix> gate, up, down_t;
+  Matrix shared_gate, shared_up, shared_down_t;
+};
+
+struct RouteResult {
+  int batch = 0, top_k = 0;
+  std::vector<std::int32_t> ids;
+  std::vector<float> weights;
+};
+
+struct DispatchPlan {
+  std::vector<std::int32_t> sorted_token_slots, expert_of_block;
+  int block_size = 0, n_padded = 0;
+};
+
+struct SparsityLevel {
+  double s = 0.0;
+  explicit SparsityLevel(double v) : s(v) {
+    if (!(v >= 0.0 && v <= 1.0)) throw ConfigError("sparsity must lie in [0, 1]");
+  }
+};
+
+enum class ExecPath { kDense, kSparse };
+enum class SweepMode { kRoutedOnly, kRoutedAndShared };
+
+struct ForwardReport {
+  Matrix outputs;
+  MacCounter macs;
+  std::uint64_t active_neurons_total = 0;
+  double achieved_routed_sparsity = 0.0;
+  std::uint64_t tiles_total = 0, tiles_skipped = 0;
+  ExecPath path_used = ExecPath::kDense;
+};
+
+struct MaskSet {
+  std::vector<std::uint8_t> routed, shared;
+};
+
+}  // namespace sparsekit

@@ -28,6 +28,8 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     "-I", INCLUDE,
 ]
+if os.environ.get("SKB_DEBUG_TIMING"):
+    NVCC_FLAGS.append("-DSKB_DEBUG_TIMING")  # in-kernel phase timestamps (tools/dbg_rf.py)
 
 
 def _nvcc() -> str:

@@ -100,8 +100,12 @@ static_assert(sizeof(RowMeta) == 32, "RowMeta is 32 bytes");
 
 }  // namespace
 
+#ifdef SKB_DEBUG_TIMING  // phase timestamps for tools/dbg_rf.py
 __device__ long long g_dn_dbg[16];
 #define DN_T(i) do { if (tid == 0 && blockIdx.x == 1 && blockIdx.y == 0 && blockIdx.z == 0) g_dn_dbg[i] = clock64(); } while (0)
+#else
+#define DN_T(i) do { } while (0)
+#endif
 
 template <int SEG>
 __global__ void __launch_bounds__(256, 1)
@@ -382,7 +386,9 @@ down_cluster_kernel(DownArgs a, int E, int Np, int D, int Dp, int R, int cmax, i
   DN_T(9);
 }
 
+#ifdef SKB_DEBUG_TIMING
 extern "C" void skb_debug_dn(long long* out) { cudaMemcpyFromSymbol(out, g_dn_dbg, sizeof(g_dn_dbg)); }
+#endif
 
 template <int SEG>
 static int launch_down_seg(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g, int R,

@@ -224,8 +224,14 @@ struct RouterFusedArgs {
   DispatchBuffers d;
 };
 
+// clock64() timestamps of the kernel's phases, read back by tools/dbg_rf.py; compiled in only
+// with -DSKB_DEBUG_TIMING (SKB_DEBUG_TIMING=1 python -m paper_2605_08575_b200.build --force)
+#ifdef SKB_DEBUG_TIMING
 __device__ long long g_rf_dbg[16];
 #define RF_T(i) do { if (lane == 0 && warp == 0) g_rf_dbg[i] = clock64(); } while (0)
+#else
+#define RF_T(i) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   extern __shared__ __align__(16) float rf_smem[];
@@ -307,13 +313,19 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
     const int e_i = lane / kRfTB, t_j = lane % kRfTB;
     const bool valid = (e_i < n_e) && (t_j < n_t);
     float acc = 0.0f;
+#ifdef SKB_DEBUG_TIMING
     long long t_wait = 0;
+#endif
 #pragma unroll 1
     for (int sc = 0; sc < nsub; ++sc) {
       const int slot = sc % kRfStages;
+#ifdef SKB_DEBUG_TIMING
       const long long tw0 = clock64();
+#endif
       mbar_wait(full_bar(slot), (sc / kRfStages) & 1u);
+#ifdef SKB_DEBUG_TIMING
       t_wait += clock64() - tw0;
+#endif
       if (sc == 0) RF_T(8);
       const float* base = rf_smem + slot * kRfRows * kRfRow;
       const float* wr = base + e_i * kRfRow;
@@ -335,7 +347,9 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
       if (lane == 0) mbar_arrive(empty_bar(slot));
     }
     RF_T(2);
+#ifdef SKB_DEBUG_TIMING
     if (lane == 0) g_rf_dbg[9] = t_wait;
+#endif
     if (valid) a.logits[static_cast<size_t>(t0 + t_j) * a.E + e0 + e_i] = acc;
 
     if (!a.fuse_route) return;
@@ -377,7 +391,9 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   RF_T(7);
 }
 
+#ifdef SKB_DEBUG_TIMING
 extern "C" void skb_debug_rf(long long* out) { cudaMemcpyFromSymbol(out, g_rf_dbg, sizeof(g_rf_dbg)); }
+#endif
 
 // Fast variant (SKB_FLAG_FAST_ROUTER): one warp per (token, expert), lanes stride d, fp32 FMA,
 // shuffle tree.  Not order-faithful: ids can differ from the reference when two probabilities

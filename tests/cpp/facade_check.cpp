@@ -1,0 +1,100 @@
+// Exercises the C++ facade (include/sparsekit_b200.hpp) the way reference client code would.
+// Built against the stand-in types here and, when /root/reference exists, syntax-checked
+// against the reference's own headers (tests/test_cabi_cpu.py).  On a GPU it prints
+// "facade ok <checksum>"; the Python test compares the checksum with the ctypes path.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "sparsekit_b200.hpp"
+
+using namespace sparsekit;
+
+static float lcg(std::uint64_t& s) {  // same generator as tests/test_gpu_parity.py::_lcg_fill
+  s = s * 6364136223846793005ull + 1442695040888963407ull;
+  return (static_cast<float>((s >> 40) & 0xFFFF) / 65536.0f - 0.5f) * 0.25f;
+}
+static void fill(Matrix& m, int r, int c, std::uint64_t& s) {
+  m = Matrix(r, c);
+  for (float& v : m.data) v = lcg(s);
+}
+
+int main() {
+  MoELayerWeights w;
+  w.config.n_experts = 8;
+  w.config.top_k = 2;
+  w.config.d_model = 128;
+  w.config.d_ffn = 192;
+  w.config.has_shared = true;
+  w.config.d_shared = 64;
+  std::uint64_t s = 12345;
+  fill(w.router, 8, 128, s);
+  w.gate.resize(8);
+  w.up.resize(8);
+  w.down_t.resize(8);
+  for (int e = 0; e < 8; ++e) {
+    fill(w.gate[e], 192, 128, s);
+    fill(w.up[e], 192, 128, s);
+    fill(w.down_t[e], 192, 128, s);
+  }
+  fill(w.shared_gate, 64, 128, s);
+  fill(w.shared_up, 64, 128, s);
+  fill(w.shared_down_t, 64, 128, s);
+  Matrix x;
+  fill(x, 5, 128, s);
+
+  if (skb_device_count() < 1) {
+    std::printf("facade built; no CUDA device\n");
+    return 0;
+  }
+  const ForwardReport dense = b200::forward_dense(w, x, 4);
+  const ForwardReport zero = b200::forward_topk_sparse(w, x, SparsityLevel(0.0), SparsityLevel(0.0));
+  if (std::memcmp(dense.outputs.data.data(), zero.outputs.data.data(),
+                  dense.outputs.data.size() * sizeof(float)) != 0) {
+    std::printf("FAIL: s=0 differs from forward_dense\n");
+    return 1;
+  }
+  const MaskSet masks = b200::build_topk_masks(w, x, SparsityLevel(0.5), SweepMode::kRoutedAndShared);
+  const ForwardReport fused = b200::forward_topk_sparse(w, x, SparsityLevel(0.5), SparsityLevel(0.5));
+  const ForwardReport masked = b200::forward_masked_dense(w, x, masks);
+  double diff = 0.0;
+  for (std::size_t i = 0; i < fused.outputs.data.size(); ++i)
+    diff = std::fmax(diff, std::fabs(fused.outputs.data[i] - masked.outputs.data[i]));
+  if (diff > 1e-6) {
+    std::printf("FAIL: fused top-k vs masked dense on its own masks: %g\n", diff);
+    return 1;
+  }
+  std::uint64_t kept = 0;
+  for (auto b : masks.routed) kept += b;
+  if (kept != 5u * 2u * 96u || fused.active_neurons_total != kept) {
+    std::printf("FAIL: survivor count %llu\n", static_cast<unsigned long long>(kept));
+    return 1;
+  }
+  bool threw = false;
+  try {
+    Matrix bad(2, 64);
+    b200::forward_dense(w, bad);
+  } catch (const ShapeError&) {
+    threw = true;
+  }
+  if (!threw) {
+    std::printf("FAIL: ShapeError not raised\n");
+    return 1;
+  }
+  threw = false;
+  try {
+    Matrix logits(1, 4);
+    b200::route(logits, 9, true);
+  } catch (const ConfigError&) {
+    threw = true;
+  }
+  if (!threw) {
+    std::printf("FAIL: ConfigError not raised\n");
+    return 1;
+  }
+  double sum = 0.0;
+  for (float v : fused.outputs.data) sum += v;
+  std::printf("facade ok %.9e\n", sum);
+  b200::clear_cache();
+  return 0;
+}

@@ -134,3 +134,36 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".hpp", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "pyoracle" not in text and "moe_oracle" not in text and "libsparsekit_ref" not in text, f
+
+
+# ---------------------------------------------------------------------------------------------
+# C++ facade (include/sparsekit_b200.hpp)
+# ---------------------------------------------------------------------------------------------
+FACADE_SRC = os.path.join(ROOT, "tests", "cpp", "facade_check.cpp")
+
+
+def build_facade_check(lib, out):
+    libdir = os.path.dirname(lib.LIB_PATH)
+    cmd = ["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), FACADE_SRC, "-o", out,
+           "-L", libdir, "-lsparsekit_b200", f"-Wl,-rpath,{libdir}"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    return out
+
+
+def test_cpp_facade_builds_against_stand_in_types(lib, tmp_path):
+    exe = build_facade_check(lib, str(tmp_path / "facade_check"))
+    res = subprocess.run([exe], capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "facade" in res.stdout
+
+
+@pytest.mark.skipif(not os.path.exists("/root/reference/proj/include/sparsekit/engine.hpp"),
+                    reason="reference headers not present (GPU box)")
+def test_cpp_facade_compiles_against_the_reference_headers():
+    """Drop-in proof: with the reference tree on the include path the facade takes its value and
+    exception types from the reference's own headers, and the same client code compiles."""
+    cmd = ["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+           "-I", "/root/reference/proj/include", FACADE_SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr

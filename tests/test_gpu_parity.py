@@ -508,3 +508,43 @@ def test_full_shapes_properties(skb, oracle, shape, B, s):
         y_same, _ = oracle.forward(w, x[sel], rep.masks.routed[sel],
                                    rep.masks.shared[sel] if S else None)
         assert max_rel_diff(rep.outputs[sel], y_same) <= TOL_FP32_ACCUM
+
+
+# ---------------------------------------------------------------------------------------------
+# C++ facade on the device
+# ---------------------------------------------------------------------------------------------
+def _lcg_fill(shape, state):
+    """Twin of lcg() in tests/cpp/facade_check.cpp."""
+    n = int(np.prod(shape))
+    out = np.empty(n, np.float32)
+    s = state[0]
+    for i in range(n):
+        s = (s * 6364136223846793005 + 1442695040888963407) & ((1 << 64) - 1)
+        out[i] = np.float32((np.float32((s >> 40) & 0xFFFF) / np.float32(65536.0) - np.float32(0.5))
+                            * np.float32(0.25))
+    state[0] = s
+    return out.reshape(shape)
+
+
+def test_cpp_facade_matches_python_path(skb, tmp_path):
+    import subprocess
+    from paper_2605_08575_b200 import _lib
+    from tests.test_cabi_cpu import build_facade_check
+    exe = build_facade_check(_lib, str(tmp_path / "facade_check"))
+    res = subprocess.run([exe], capture_output=True, text=True)
+    assert res.returncode == 0 and "facade ok" in res.stdout, res.stdout + res.stderr
+    checksum = float(res.stdout.split()[-1])
+    st = [12345]
+    cfg = skb.MoEConfig(8, 2, 128, 192, True, 64, True, 64)
+    router = _lcg_fill((8, 128), st)
+    gate, up, down = [], [], []
+    for _ in range(8):
+        gate.append(_lcg_fill((192, 128), st))
+        up.append(_lcg_fill((192, 128), st))
+        down.append(_lcg_fill((192, 128), st))
+    sg, su, sd = (_lcg_fill((64, 128), st) for _ in range(3))
+    x = _lcg_fill((5, 128), st)
+    layer = skb.MoELayerWeights.from_arrays(cfg, router, gate, up, down, sg, su, sd)
+    lvl = skb.SparsityLevel(0.5)
+    y = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
+    assert float(np.sum(y.astype(np.float64))) == pytest.approx(checksum, rel=1e-6, abs=1e-7)
