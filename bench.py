@@ -185,7 +185,9 @@ class Point:
         self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
                                   mode=self.skb.MODE_TOPK, s_routed=s, s_shared=s if S else 0.0,
                                   flags=flags,
-                                  stream=self.torch.cuda.current_stream().cuda_stream)
+                                  # NULL would mean "the layer's own stream": name torch's
+                                  # default stream explicitly (cudaStreamLegacy == 0x1)
+                                  stream=self.torch.cuda.current_stream().cuda_stream or 1)
 
     def time_device(self, s, steps, warmup, use_graph=True):
         """Per-step CUDA-event times (ms) of the device entry point; L2 flushed and the token

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKB_ABI_VERSION 1
+#define SKB_ABI_VERSION 2
 
 typedef enum skb_status {
   SKB_OK = 0,
@@ -73,7 +73,9 @@ typedef struct skb_report {
 enum {
   SKB_MODE_DENSE = 0,  /* forward_dense,        engine.hpp:38-39  */
   SKB_MODE_TOPK = 1,   /* forward_masked_dense(build_topk_masks(s)) fused; skips masked W_down rows */
-  SKB_MODE_MASKED = 2  /* forward_masked_dense with caller masks, engine.hpp:43-44 */
+  SKB_MODE_MASKED = 2, /* forward_masked_dense with caller masks, engine.hpp:43-44 */
+  SKB_MODE_ROUTE_ONLY = 3 /* route_logits + route only (engine.cpp:121-122): x -> ids_out, weights_out;
+                             the home-rank half of expert parallelism */
 };
 
 /* Flags. */
@@ -110,6 +112,14 @@ typedef struct skb_forward_args {
   uint8_t* shared_mask_out; /* [B][S] */
   float* h_routed_out;      /* [B][K][N] pre-mask SwiGLU output */
   float* h_shared_out;      /* [B][S] */
+  /* External routing (expert parallelism: the owner rank computes slots routed elsewhere).
+   * When ids_in is non-NULL the router stage is skipped: ids_in [B][K] are expert ids of THIS
+   * layer, weights_in [B][K] the combine weights (NULL = 1.0, i.e. un-weighted slot outputs
+   * for K = 1).  Host pointers for skb_layer_forward, device pointers for
+   * skb_layer_forward_device (which then also honours ids_out / weights_out as device
+   * pointers in SKB_MODE_ROUTE_ONLY). */
+  const int32_t* ids_in;
+  const float* weights_in;
 } skb_forward_args;
 
 typedef struct skb_layer skb_layer;
@@ -136,6 +146,21 @@ int skb_layer_create(const skb_config* cfg, const float* router, const float* co
 int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale, int device,
                                skb_layer** out);
 
+/* Expert-parallel slices of generate_synthetic(full, seed, scale), built on the device with
+ * the same SplitMix64 jump-ahead (bit-identical to slicing the full model):
+ *   which = 0: experts [e_lo, e_hi) of the full model as a layer with
+ *              {n_experts = e_hi - e_lo, top_k = 1, no shared expert};
+ *   which = 1: the shared expert as a layer with {n_experts = 1, top_k = 1, d_ffn = d_shared}.
+ * Either slice also carries the FULL router (E x D, top_k of the full model) for
+ * SKB_MODE_ROUTE_ONLY. */
+int skb_layer_create_synthetic_slice(const skb_config* full, uint64_t seed, float scale, int e_lo,
+                                     int e_hi, int which, int device, skb_layer** out);
+
+/* Attaches a router for SKB_MODE_ROUTE_ONLY that differs from the layer's own (expert-parallel
+ * slices built with skb_layer_create from real weights): router is host fp32 [n_experts][D]. */
+int skb_layer_set_router(skb_layer* layer, const float* router, int n_experts, int top_k,
+                         int renormalize);
+
 void skb_layer_destroy(skb_layer* layer);
 
 /* Pre-sizes every workspace for batches up to max_batch (so that
@@ -150,7 +175,8 @@ int skb_layer_reserve(skb_layer* layer, int max_batch);
 int skb_layer_forward(skb_layer* layer, const skb_forward_args* args, skb_report* report);
 
 /* Same stages with DEVICE x/y, enqueued asynchronously on `stream`
- * (a cudaStream_t passed as void*; NULL = the layer's own stream).  No
+ * (a cudaStream_t passed as void*; NULL = the layer's own stream -- pass
+ * cudaStreamLegacy / cudaStreamPerThread to name a default stream).  No
  * allocation, no synchronisation: safe inside CUDA-graph capture after
  * skb_layer_reserve.  Capture pointers in args are ignored. */
 int skb_layer_forward_device(skb_layer* layer, const skb_forward_args* args, void* stream,

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libsparsekit_b200.so")
 
 SKB_OK, SKB_ESHAPE, SKB_ECONFIG, SKB_EINDEX, SKB_EINTERNAL, SKB_ECUDA = range(6)
-MODE_DENSE, MODE_TOPK, MODE_MASKED = 0, 1, 2
+MODE_DENSE, MODE_TOPK, MODE_MASKED, MODE_ROUTE_ONLY = 0, 1, 2, 3
 FLAG_FAST_ROUTER, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES, FLAG_NO_PDL = 1, 2, 4, 8
 FLAG_GATHER_DOWN, FLAG_DENSE_DOWN, FLAG_BF16_H = 16, 32, 64
 N_STAGES = 6
@@ -20,7 +20,8 @@ STAGE_NAMES = ("router", "dispatch", "gateup", "select", "down", "combine")
 # every symbol include/sparsekit_b200.h declares
 EXPORTS = (
     "skb_last_error", "skb_abi_version", "skb_device_count", "skb_config_validate",
-    "skb_layer_create", "skb_layer_create_synthetic", "skb_layer_destroy", "skb_layer_reserve",
+    "skb_layer_create", "skb_layer_create_synthetic", "skb_layer_create_synthetic_slice",
+    "skb_layer_set_router", "skb_layer_destroy", "skb_layer_reserve",
     "skb_layer_forward", "skb_layer_forward_device", "skb_layer_stage_times",
     "skb_layer_last_launches", "skb_layer_weight_bytes", "skb_route", "skb_align_dispatch",
     "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off",
@@ -50,6 +51,7 @@ class SkbForwardArgs(C.Structure):
         ("ids_out", C.c_void_p), ("weights_out", C.c_void_p),
         ("routed_mask_out", C.c_void_p), ("shared_mask_out", C.c_void_p),
         ("h_routed_out", C.c_void_p), ("h_shared_out", C.c_void_p),
+        ("ids_in", C.c_void_p), ("weights_in", C.c_void_p),
     ]
 
 
@@ -75,6 +77,9 @@ def load() -> C.CDLL:
                                    C.POINTER(vp)]
     L.skb_layer_create_synthetic.argtypes = [C.POINTER(SkbConfig), u64, C.c_float, C.c_int,
                                              C.POINTER(vp)]
+    L.skb_layer_create_synthetic_slice.argtypes = [C.POINTER(SkbConfig), u64, C.c_float, C.c_int,
+                                                   C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.skb_layer_set_router.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
     L.skb_layer_destroy.argtypes = [vp]
     L.skb_layer_destroy.restype = None
     L.skb_layer_reserve.argtypes = [vp, C.c_int]

@@ -85,6 +85,8 @@ struct skb_layer {
   cudaStream_t stream = nullptr;
   std::mutex mu;
 
+  // router used by the router stage: the layer's own, or the full model's for EP slices
+  int route_E = 0, route_K = 0, route_renorm = 1;
   // weight image
   float* d_router = nullptr;
   __nv_bfloat16* d_wgu = nullptr;
@@ -105,6 +107,8 @@ struct skb_layer {
   float* d_wts = nullptr;
   DispatchBuffers disp{};
   unsigned* d_counters = nullptr;
+  int32_t* d_ids_stage = nullptr;  // host-API staging of external routing
+  float* d_wts_stage = nullptr;
   __nv_bfloat16* d_xs = nullptr;
   uint64_t xs_rows = 0;
   CUtensorMap tmap_x[5]{};
@@ -136,7 +140,7 @@ void free_workspace(skb_layer* L) {
                   L->disp.n_tiles, L->d_xs,      L->d_h,            L->d_kidx,
                   L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
-                  L->d_hb,       L->d_slot_out};
+                  L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -146,6 +150,8 @@ void free_workspace(skb_layer* L) {
   L->d_counters = nullptr;
   L->d_hb = nullptr;
   L->d_slot_out = nullptr;
+  L->d_ids_stage = nullptr;
+  L->d_wts_stage = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -176,9 +182,14 @@ int reserve_locked(skb_layer* L, int B) {
   if ((rc = (x)) != SKB_OK) return rc
   SKB_TRY(dmalloc(&L->d_x, static_cast<size_t>(cap) * g.D));
   SKB_TRY(dmalloc(&L->d_y, static_cast<size_t>(cap) * g.D));
-  SKB_TRY(dmalloc(&L->d_logits, static_cast<size_t>(cap) * g.E));
-  SKB_TRY(dmalloc(&L->d_ids, BK));
-  SKB_TRY(dmalloc(&L->d_wts, BK));
+  SKB_TRY(dmalloc(&L->d_logits, static_cast<size_t>(cap) * (L->route_E > g.E ? L->route_E : g.E)));
+  {
+    const size_t rk = static_cast<size_t>(cap) * (L->route_K > g.K ? L->route_K : g.K);
+    SKB_TRY(dmalloc(&L->d_ids, rk));
+    SKB_TRY(dmalloc(&L->d_wts, rk));
+  }
+  SKB_TRY(dmalloc(&L->d_ids_stage, BK));
+  SKB_TRY(dmalloc(&L->d_wts_stage, BK));
   SKB_TRY(dmalloc(&L->disp.perm, BK));
   SKB_TRY(dmalloc(&L->disp.inv, BK));
   SKB_TRY(dmalloc(&L->disp.row_expert, rows));
@@ -237,7 +248,7 @@ int validate_cfg(const skb_config* c) {
   return SKB_OK;
 }
 
-int new_layer(const skb_config* cfg, int device, skb_layer** out) {
+int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 0, int route_K = 0) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if (out == nullptr) return fail(SKB_EINTERNAL, "out pointer is null");
@@ -270,6 +281,13 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out) {
   g.Np = round_up(g.N, kNeuronBlock);
   g.Sp = g.has_shared ? round_up(g.S, kNeuronBlock) : 0;
   g.Nh = g.Np > g.Sp ? g.Np : g.Sp;
+  L->route_E = route_E > 0 ? route_E : g.E;
+  L->route_K = route_K > 0 ? route_K : g.K;
+  L->route_renorm = g.renorm;
+  if (L->route_E > kMaxExperts) {
+    delete L;
+    return fail(SKB_ECONFIG, "n_experts=%d exceeds the device router limit %d", route_E, kMaxExperts);
+  }
   cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete L;
@@ -278,7 +296,7 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out) {
   for (auto& ev : L->ev) cudaEventCreate(&ev);
   const size_t gu_rows = static_cast<size_t>(g.E) * 2 * g.Np + 2 * static_cast<size_t>(g.Sp);
   const size_t wd_rows = static_cast<size_t>(g.E) * g.Np + g.Sp;
-  rc = dmalloc(&L->d_router, static_cast<size_t>(g.E) * g.D);
+  rc = dmalloc(&L->d_router, static_cast<size_t>(L->route_E) * g.D);
   if (!rc) rc = dmalloc(&L->d_wgu, gu_rows * g.Dp);
   if (!rc) rc = dmalloc(&L->d_wd, wd_rows * g.Dp);
   if (rc) {
@@ -297,11 +315,14 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out) {
   cudaMemsetAsync(L->d_wdt, 0, wdt_elems * 2, L->stream);
   cudaMemsetAsync(L->d_wgu, 0, gu_rows * g.Dp * 2, L->stream);
   cudaMemsetAsync(L->d_wd, 0, wd_rows * g.Dp * 2, L->stream);
-  rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows, g.Dp, 128);
+  // tiled images: the tensor maps see them as [n_tiles * 128][64] (tiled_index())
+  rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows * (g.Dp / kBlockK), kBlockK, 128);
   if (!rc)
-    rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt, static_cast<uint64_t>(g.E) * g.Dp128, g.Np, 128);
+    rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt,
+                        static_cast<uint64_t>(g.E) * g.Dp128 * (g.Np / kBlockK), kBlockK, 128);
   if (!rc && g.has_shared)
-    rc = encode_bf16_2d(&L->tmap_wdt_shared, L->d_wdt_shared, g.Dp128, g.Sp, 128);
+    rc = encode_bf16_2d(&L->tmap_wdt_shared, L->d_wdt_shared,
+                        static_cast<uint64_t>(g.Dp128) * (g.Sp / kBlockK), kBlockK, 128);
   if (rc) {
     skb_layer_destroy(L);
     return rc;
@@ -324,7 +345,9 @@ struct StageTimer {
 // pointers.  No allocation, no synchronisation.
 int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, float* d_y,
                  const uint8_t* d_mask_r, const uint8_t* d_mask_s, uint8_t* d_mask_out_r,
-                 uint8_t* d_mask_out_s, cudaStream_t stream, bool timing) {
+                 uint8_t* d_mask_out_s, cudaStream_t stream, bool timing,
+                 const int32_t* d_ids_in = nullptr, const float* d_w_in = nullptr,
+                 int32_t* d_ids_out = nullptr, float* d_w_out = nullptr) {
   const Geometry& g = L->g;
   const int B = a->batch;
   const int BK = B * g.K;
@@ -332,6 +355,28 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   LaunchCtx ctx{stream, !timing && !(a->flags & SKB_FLAG_NO_PDL)};
   StageTimer tm{L, timing, stream};
   int launches = 0;
+
+  if (a->mode == SKB_MODE_ROUTE_ONLY) {
+    RouterLaunch r{};
+    r.x = d_x;
+    r.router = L->d_router;
+    r.B = B;
+    r.E = L->route_E;
+    r.D = g.D;
+    r.K = L->route_K;
+    r.renorm = L->route_renorm;
+    r.fast = (a->flags & SKB_FLAG_FAST_ROUTER) != 0;
+    r.logits = L->d_logits;
+    r.ids = d_ids_out ? d_ids_out : L->d_ids;
+    r.weights = d_w_out ? d_w_out : L->d_wts;
+    r.counters = L->d_counters;
+    r.dispatch = nullptr;
+    launches += launch_router(ctx, r);
+    L->last_launches = launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SKB_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return SKB_OK;
+  }
 
   int sel_mode, n_off_r = 0, n_off_s = 0;
   int max_keep = g.N > g.S ? g.N : g.S;
@@ -378,7 +423,16 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   const int max_tiles = max_tiles_for(g, B, tn);
 
   tm.mark();
-  {
+  if (d_ids_in != nullptr) {
+    // external routing: ids (and weights, default 1) are given; only the dispatch runs
+    ctx.pdl = false;  // memcpy nodes in between: plain stream order for this call
+    cudaMemcpyAsync(L->d_ids, d_ids_in, static_cast<size_t>(BK) * 4, cudaMemcpyDeviceToDevice, stream);
+    if (d_w_in != nullptr)
+      cudaMemcpyAsync(L->d_wts, d_w_in, static_cast<size_t>(BK) * 4, cudaMemcpyDeviceToDevice, stream);
+    else
+      launches += launch_fill_f32(stream, L->d_wts, 1.0f, static_cast<size_t>(BK));
+    launches += launch_dispatch(ctx, L->d_ids, B, g.K, g.E, g.has_shared, tn, L->disp);
+  } else {
     RouterLaunch r{};
     r.x = d_x;
     r.router = L->d_router;
@@ -486,10 +540,16 @@ int check_args(const skb_layer* L, const skb_forward_args* a) {
   if (L == nullptr) return fail(SKB_EINTERNAL, "layer is null");
   if (a == nullptr) return fail(SKB_EINTERNAL, "args is null");
   const Geometry& g = L->g;
-  if (a->x == nullptr || a->y == nullptr) return fail(SKB_ESHAPE, "forward: x and y must be non-null");
+  if (a->x == nullptr || (a->y == nullptr && a->mode != SKB_MODE_ROUTE_ONLY))
+    return fail(SKB_ESHAPE, "forward: x and y must be non-null");
   if (a->batch < 1) return fail(SKB_ESHAPE, "route: empty batch");  // router.cpp:16-18
-  if (a->mode != SKB_MODE_DENSE && a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_MASKED)
+  if (a->mode != SKB_MODE_DENSE && a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_MASKED &&
+      a->mode != SKB_MODE_ROUTE_ONLY)
     return fail(SKB_ECONFIG, "forward: unknown mode %d", a->mode);
+  if (a->mode == SKB_MODE_ROUTE_ONLY && (a->ids_out == nullptr || a->weights_out == nullptr))
+    return fail(SKB_ESHAPE, "route-only forward: ids_out and weights_out must be non-null");
+  if (a->mode != SKB_MODE_ROUTE_ONLY && a->ids_in == nullptr && L->route_E != g.E)
+    return fail(SKB_ECONFIG, "forward: an expert-parallel slice needs external routing (ids_in)");
   if (a->mode == SKB_MODE_MASKED) {
     // engine.cpp:107-117
     const uint64_t want = static_cast<uint64_t>(a->batch) * g.K * g.N;
@@ -668,6 +728,87 @@ int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale
   return SKB_OK;
 }
 
+int skb_layer_create_synthetic_slice(const skb_config* full, uint64_t seed, float scale, int e_lo,
+                                     int e_hi, int which, int device, skb_layer** out) {
+  int rc = validate_cfg(full);
+  if (rc) return rc;
+  if (!(scale > 0.0f)) return fail(SKB_ECONFIG, "scale must be > 0");
+  if (which != 0 && which != 1) return fail(SKB_ECONFIG, "slice: which must be 0 or 1");
+  if (which == 0 && (e_lo < 0 || e_hi <= e_lo || e_hi > full->n_experts))
+    return fail(SKB_EINDEX, "slice: expert range [%d, %d) outside [0, %d)", e_lo, e_hi,
+                full->n_experts);
+  if (which == 1 && !full->has_shared)
+    return fail(SKB_ECONFIG, "slice: the model has no shared expert");
+  skb_config loc = *full;
+  loc.n_experts = which == 0 ? e_hi - e_lo : 1;
+  loc.top_k = 1;
+  loc.d_ffn = which == 0 ? full->d_ffn : full->d_shared;
+  loc.has_shared = 0;
+  loc.d_shared = 0;
+  skb_layer* L = nullptr;
+  rc = new_layer(&loc, device, &L, full->n_experts, full->top_k);
+  if (rc) return rc;
+  const Geometry& g = L->g;
+  const uint64_t ED = static_cast<uint64_t>(full->n_experts) * g.D;
+  const uint64_t ND = static_cast<uint64_t>(full->d_ffn) * g.D;
+  const uint64_t SD = static_cast<uint64_t>(full->d_shared) * g.D;
+  launch_synth_f32(L->stream, seed, scale, 0, ED, L->d_router);
+  for (int j = 0; j < g.E; ++j) {
+    // draw offsets inside generate_synthetic's stream (model.cpp:129-166)
+    uint64_t og, ou, od;
+    if (which == 0) {
+      const uint64_t base = ED + static_cast<uint64_t>(e_lo + j) * 3 * ND;
+      og = base;
+      ou = base + ND;
+      od = base + 2 * ND;
+    } else {
+      const uint64_t base = ED + static_cast<uint64_t>(full->n_experts) * 3 * ND;
+      og = base;
+      ou = base + SD;
+      od = base + 2 * SD;
+    }
+    launch_synth_gateup(L->stream, seed, scale, og, ou, g.N, g.Np, g.D, g.Dp,
+                        L->d_wgu + static_cast<size_t>(j) * 2 * g.Np * g.Dp);
+    launch_synth_rows_bf16(L->stream, seed, scale, od, g.N, g.Np, g.D, g.Dp,
+                           L->d_wd + static_cast<size_t>(j) * g.Np * g.Dp);
+    launch_synth_down_t(L->stream, seed, scale, od, g.N, g.D, g.Np,
+                        L->d_wdt + static_cast<size_t>(j) * g.Dp128 * g.Np);
+  }
+  cudaError_t e = cudaStreamSynchronize(L->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    skb_layer_destroy(L);
+    return fail(SKB_ECUDA, "layer_create_synthetic_slice failed: %s", cudaGetErrorString(e));
+  }
+  *out = L;
+  return SKB_OK;
+}
+
+int skb_layer_set_router(skb_layer* L, const float* router, int n_experts, int top_k,
+                         int renormalize) {
+  if (L == nullptr || router == nullptr) return fail(SKB_EINTERNAL, "set_router: null argument");
+  if (n_experts < 1 || top_k < 1 || top_k > n_experts)
+    return fail(SKB_ECONFIG, "set_router: top_k must satisfy 1 <= K <= E, got K=%d E=%d", top_k,
+                n_experts);
+  if (n_experts > kMaxExperts)
+    return fail(SKB_ECONFIG, "set_router: n_experts=%d exceeds the device router limit %d",
+                n_experts, kMaxExperts);
+  std::lock_guard<std::mutex> lk(L->mu);
+  SKB_CUDA(cudaSetDevice(L->device));
+  SKB_CUDA(cudaStreamSynchronize(L->stream));
+  float* nr = nullptr;
+  int rc = dmalloc(&nr, static_cast<size_t>(n_experts) * L->g.D);
+  if (rc) return rc;
+  SKB_CUDA(cudaMemcpy(nr, router, static_cast<size_t>(n_experts) * L->g.D * 4, cudaMemcpyHostToDevice));
+  cudaFree(L->d_router);
+  L->d_router = nr;
+  L->route_E = n_experts;
+  L->route_K = top_k;
+  L->route_renorm = renormalize ? 1 : 0;
+  free_workspace(L);  // logits / ids workspaces depend on the router shape
+  return SKB_OK;
+}
+
 void skb_layer_destroy(skb_layer* L) {
   if (L == nullptr) return;
   cudaSetDevice(L->device);
@@ -711,8 +852,33 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
     }
   }
   const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
+  if (a->mode == SKB_MODE_ROUTE_ONLY) {
+    rc = forward_core(L, a, L->d_x, nullptr, nullptr, nullptr, nullptr, nullptr, s, false);
+    if (rc) return rc;
+    const size_t rk = B * static_cast<size_t>(L->route_K);
+    SKB_CUDA(cudaMemcpyAsync(a->ids_out, L->d_ids, rk * 4, cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaMemcpyAsync(a->weights_out, L->d_wts, rk * 4, cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaStreamSynchronize(s));
+    if (report) std::memset(report, 0, sizeof(*report));
+    return SKB_OK;
+  }
+  const int32_t* d_ids_in = nullptr;
+  const float* d_w_in = nullptr;
+  if (a->ids_in != nullptr) {
+    for (size_t i = 0; i < BK; ++i)
+      if (a->ids_in[i] < 0 || a->ids_in[i] >= g.E)
+        return fail(SKB_EINDEX, "forward: external expert id %d outside [0, %d)", a->ids_in[i], g.E);
+    // staged through the mask-input buffer's neighbours: ids/weights workspaces are the targets
+    SKB_CUDA(cudaMemcpyAsync(L->d_ids_stage, a->ids_in, BK * 4, cudaMemcpyHostToDevice, s));
+    d_ids_in = L->d_ids_stage;
+    if (a->weights_in != nullptr) {
+      SKB_CUDA(cudaMemcpyAsync(L->d_wts_stage, a->weights_in, BK * 4, cudaMemcpyHostToDevice, s));
+      d_w_in = L->d_wts_stage;
+    }
+  }
   rc = forward_core(L, a, L->d_x, L->d_y, mr, ms, a->routed_mask_out ? L->d_mask_out_r : nullptr,
-                    (a->shared_mask_out && g.has_shared) ? L->d_mask_out_s : nullptr, s, timing);
+                    (a->shared_mask_out && g.has_shared) ? L->d_mask_out_s : nullptr, s, timing,
+                    d_ids_in, d_w_in);
   if (rc) return rc;
   SKB_CUDA(cudaMemcpyAsync(a->y, L->d_y, B * g.D * 4, cudaMemcpyDeviceToHost, s));
   if (a->ids_out) SKB_CUDA(cudaMemcpyAsync(a->ids_out, L->d_ids, BK * 4, cudaMemcpyDeviceToHost, s));
@@ -757,10 +923,12 @@ int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stre
   const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
   rc = forward_core(L, a, a->x, a->y, a->mode == SKB_MODE_MASKED ? a->routed_mask_in : nullptr,
                     (a->mode == SKB_MODE_MASKED && a->shared_mask_len) ? a->shared_mask_in : nullptr,
-                    nullptr, nullptr, s, timing);
+                    nullptr, nullptr, s, timing, a->ids_in, a->weights_in,
+                    a->mode == SKB_MODE_ROUTE_ONLY ? a->ids_out : nullptr,
+                    a->mode == SKB_MODE_ROUTE_ONLY ? a->weights_out : nullptr);
   if (rc) return rc;
   if (timing) L->stage_ms_pending = true;
-  fill_report(L, a, report, nullptr, nullptr);
+  if (a->mode != SKB_MODE_ROUTE_ONLY) fill_report(L, a, report, nullptr, nullptr);
   return SKB_OK;
 }
 

@@ -235,7 +235,9 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           mbar_wait(empty_bar(s), ph ^ 1u);
           mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * kBTile);
           const uint32_t a_smem = smem_base + s * kStageBytes;
-          tma_load_2d(a_smem, map_a, kb * kBlockK, a_row, full_bar(s), kPolicyEvictFirst);
+          // tiled image: tile (a_row / 128, kb) is 128 consecutive rows of the 64-column view
+          tma_load_2d(a_smem, map_a, 0, ((a_row >> 7) * num_k_blocks + kb) * 128, full_bar(s),
+                      kPolicyEvictFirst);
           tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s),
                       kPolicyEvictLast);
           if (MODE == 1 && nsplit > 1) {
@@ -437,14 +439,13 @@ __global__ void __launch_bounds__(256) gateup_simt_kernel(const __nv_bfloat16* _
   const size_t img_row0 =
       (e < g.E) ? static_cast<size_t>(e) * 2 * g.Np : static_cast<size_t>(g.E) * 2 * g.Np;
   const size_t blk = img_row0 + static_cast<size_t>(n / kNeuronBlock) * 128;
-  const __nv_bfloat16* wg = wgu + (blk + gateup_row(n % kNeuronBlock, 0)) * g.Dp;
-  const __nv_bfloat16* wu = wgu + (blk + gateup_row(n % kNeuronBlock, 1)) * g.Dp;
+  const size_t rg = blk + gateup_row(n % kNeuronBlock, 0), ru = blk + gateup_row(n % kNeuronBlock, 1);
   const __nv_bfloat16* xr = xs + static_cast<size_t>(row) * g.Dp;
   float ag = 0.0f, au = 0.0f;
   for (int d = lane; d < g.Dp; d += 32) {
     const float xv = __bfloat162float(xr[d]);
-    ag = fmaf(__bfloat162float(wg[d]), xv, ag);
-    au = fmaf(__bfloat162float(wu[d]), xv, au);
+    ag = fmaf(__bfloat162float(wgu[tiled_index(rg, d, g.Dp)]), xv, ag);
+    au = fmaf(__bfloat162float(wgu[tiled_index(ru, d, g.Dp)]), xv, au);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

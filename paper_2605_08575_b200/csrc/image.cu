@@ -2,7 +2,9 @@
 //
 //   router   fp32 [E][D]                         (kept in fp32: routing must match the reference)
 //   gateup   bf16 [E*2*Np + 2*Sp][Dp]            per 64-neuron block, 128 rows interleaved as
-//                                                gateup_row() describes; K-major for TMA/UMMA
+//                                                gateup_row() describes; K-major for TMA/UMMA,
+//                                                stored tiled (tiled_index(): 16 KB tiles)
+//   down^T   bf16 [E][Dp128][Np] (+ [Dp128][Sp])  A operand of the dense down projection, tiled
 //   down     bf16 [E][Np][Dp] (+ shared [Sp][Dp]) one contiguous Dp*2-byte row per neuron,
 //                                                i.e. MoELayerWeights::down_t as stored by the
 //                                                reference (proj/include/sparsekit/model.hpp:34-43)
@@ -32,8 +34,8 @@ __global__ void pack_gateup_kernel(const float* __restrict__ gate, const float* 
   const float* src = (which ? up : gate) + static_cast<size_t>(n) * D;
   const size_t img_row = static_cast<size_t>(n / kNeuronBlock) * 128 +
                          gateup_row(n % kNeuronBlock, which);
-  __nv_bfloat16* out = dst + img_row * Dp;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) out[d] = __float2bfloat16_rn(src[d]);
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    dst[tiled_index(img_row, d, Dp)] = __float2bfloat16_rn(src[d]);
 }
 
 __global__ void pack_rows_kernel(const float* __restrict__ src, int D, int Dp,
@@ -50,9 +52,8 @@ __global__ void synth_gateup_kernel(uint64_t seed, float scale, uint64_t off_gat
   const uint64_t off = (which ? off_up : off_gate) + static_cast<uint64_t>(n) * D;
   const size_t img_row = static_cast<size_t>(n / kNeuronBlock) * 128 +
                          gateup_row(n % kNeuronBlock, which);
-  __nv_bfloat16* out = dst + img_row * Dp;
   for (int d = threadIdx.x; d < D; d += blockDim.x)
-    out[d] = __float2bfloat16_rn(splitmix_symmetric(seed, off + d, scale));
+    dst[tiled_index(img_row, d, Dp)] = __float2bfloat16_rn(splitmix_symmetric(seed, off + d, scale));
 }
 
 __global__ void synth_rows_kernel(uint64_t seed, float scale, uint64_t off, int D, int Dp,
@@ -76,7 +77,7 @@ __global__ void pack_down_t_kernel(const float* __restrict__ src, int n_rows, in
   __syncthreads();
   for (int j = threadIdx.y; j < 32; j += blockDim.y) {
     const int d = d0 + j, n = n0 + threadIdx.x;
-    if (d < D && n < n_rows) dst[static_cast<size_t>(d) * Kp + n] = __float2bfloat16_rn(tile[threadIdx.x][j]);
+    if (d < D && n < n_rows) dst[tiled_index(d, n, Kp)] = __float2bfloat16_rn(tile[threadIdx.x][j]);
   }
 }
 
@@ -84,7 +85,7 @@ __global__ void synth_down_t_kernel(uint64_t seed, float scale, uint64_t off, in
                                     int Kp, __nv_bfloat16* __restrict__ dst) {
   const int d = blockIdx.x;
   for (int n = threadIdx.x; n < n_rows; n += blockDim.x)
-    dst[static_cast<size_t>(d) * Kp + n] =
+    dst[tiled_index(d, n, Kp)] =
         __float2bfloat16_rn(splitmix_symmetric(seed, off + static_cast<uint64_t>(n) * D + d, scale));
 }
 
@@ -126,6 +127,15 @@ int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, i
 int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
                         int Kp, __nv_bfloat16* dst) {
   synth_down_t_kernel<<<D, 256, 0, s>>>(seed, scale, off, n_rows, D, Kp, dst);
+  return 1;
+}
+__global__ void fill_f32_kernel(float* __restrict__ dst, float value, size_t count) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = value;
+}
+int launch_fill_f32(cudaStream_t s, float* dst, float value, size_t count) {
+  if (count == 0) return 0;
+  fill_f32_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, value, count);
   return 1;
 }
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,

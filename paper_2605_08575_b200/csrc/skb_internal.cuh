@@ -22,6 +22,15 @@ constexpr int kMaxExperts = 1024;
 constexpr int kSmallSlots = 64;    // B*K up to which the router kernel builds the dispatch itself  // 32 probabilities per lane in the warp top-k
 
 __host__ __device__ inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// GEMM operand images are stored TILED: 128-row x 64-column tiles (one TMA box = one UMMA
+// A tile), each tile 16 KB contiguous, tiles of one 128-row block consecutive along K.  A TMA
+// tile load is then one contiguous HBM read instead of 128 segments of 128 B at a row-stride
+// apart.  Element (r, d) of an image whose rows have Kp (multiple of 64) columns:
+__host__ __device__ inline size_t tiled_index(size_t r, int d, int Kp) {
+  return ((r / 128) * static_cast<size_t>(Kp / 64) + static_cast<size_t>(d / 64)) * (128 * 64) +
+         (r % 128) * 64 + static_cast<size_t>(d % 64);
+}
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
 // Geometry of one layer's device image.
@@ -147,6 +156,7 @@ int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, i
                        __nv_bfloat16* dst);
 int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
                         int Kp, __nv_bfloat16* dst);
+int launch_fill_f32(cudaStream_t s, float* dst, float value, size_t count);
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
                      float* dst);
 

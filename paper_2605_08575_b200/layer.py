@@ -20,7 +20,8 @@ import numpy as np
 from . import _lib
 from ._lib import (FLAG_BF16_H, FLAG_DENSE_DOWN, FLAG_FAST_ROUTER, FLAG_GATHER_DOWN,  # noqa: F401
                    FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,
-                   MODE_DENSE, MODE_MASKED, MODE_TOPK, STAGE_NAMES, SkbConfig, SkbForwardArgs,
+                   MODE_DENSE, MODE_MASKED, MODE_ROUTE_ONLY, MODE_TOPK, STAGE_NAMES, SkbConfig,
+                   SkbForwardArgs,
                    SkbReport)
 
 
@@ -207,6 +208,36 @@ class MoELayerWeights:
                                             C.byref(h)))
         return cls(config, h.value)
 
+    @classmethod
+    def synthetic_slice(cls, full: MoEConfig, seed: int, scale: float, e_lo: int = 0,
+                        e_hi: int = 0, shared: bool = False, device: int = 0) -> "MoELayerWeights":
+        """Expert-parallel slice of generate_synthetic(full, seed, scale): experts [e_lo, e_hi)
+        as a top-1 layer without shared expert, or (shared=True) the shared expert as a
+        one-expert layer.  Carries the full router for route_only()."""
+        cfg = full.c()
+        h = C.c_void_p()
+        _check(_lib.load().skb_layer_create_synthetic_slice(
+            C.byref(cfg), seed & (2 ** 64 - 1), scale, e_lo, e_hi, 1 if shared else 0, device,
+            C.byref(h)))
+        if shared:
+            loc = MoEConfig(1, 1, full.d_model, full.d_shared, False, 0, full.renormalize,
+                            full.align_block)
+        else:
+            loc = MoEConfig(e_hi - e_lo, 1, full.d_model, full.d_ffn, False, 0, full.renormalize,
+                            full.align_block)
+        out = cls(loc, h.value)
+        out.route_shape = (full.n_experts, full.top_k)
+        return out
+
+    def set_router(self, router, top_k: int, renormalize: bool = True) -> None:
+        """Attach the full model's router to an expert-parallel slice built from arrays."""
+        r = np.ascontiguousarray(router, dtype=np.float32)
+        if r.ndim != 2 or r.shape[1] != self.config.d_model:
+            raise ShapeError(f"router must be E x {self.config.d_model}, got {r.shape}")
+        _check(_lib.load().skb_layer_set_router(self._h, _ptr(r), r.shape[0], top_k,
+                                                int(renormalize)))
+        self.route_shape = (r.shape[0], top_k)
+
     def reserve(self, max_batch: int) -> None:
         _check(_lib.load().skb_layer_reserve(self._h, max_batch))
 
@@ -237,11 +268,23 @@ class MoELayerWeights:
     # -- device-pointer entry for the benchmark's value leg and for stream capture --
     def forward_device(self, x_ptr: int, y_ptr: int, batch: int, mode: int = MODE_TOPK,
                        s_routed: float = 0.0, s_shared: float = 0.0, flags: int = 0,
-                       stream: int = 0) -> None:
+                       stream: int = 0, ids_in_ptr: int = 0, weights_in_ptr: int = 0) -> None:
+        """All pointers are device pointers.  ids_in_ptr: external routing ([batch][top_k] int32
+        expert ids of this layer); weights_in_ptr 0 => un-weighted slot outputs."""
         a = SkbForwardArgs()
         a.batch, a.mode, a.flags = batch, mode, flags
         a.s_routed, a.s_shared = s_routed, s_shared
         a.x, a.y = x_ptr, y_ptr
+        a.ids_in, a.weights_in = ids_in_ptr or None, weights_in_ptr or None
+        _check(_lib.load().skb_layer_forward_device(self._h, C.byref(a), C.c_void_p(stream), None))
+
+    def route_device(self, x_ptr: int, ids_out_ptr: int, weights_out_ptr: int, batch: int,
+                     flags: int = 0, stream: int = 0) -> None:
+        """SKB_MODE_ROUTE_ONLY on device pointers: x [batch][D] -> ids / weights [batch][K_route]."""
+        a = SkbForwardArgs()
+        a.batch, a.mode, a.flags = batch, MODE_ROUTE_ONLY, flags
+        a.x = x_ptr
+        a.ids_out, a.weights_out = ids_out_ptr, weights_out_ptr
         _check(_lib.load().skb_layer_forward_device(self._h, C.byref(a), C.c_void_p(stream), None))
 
 
@@ -299,6 +342,48 @@ def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_share
         _check(L.skb_layer_stage_times(w._h, ms))
         out.stage_ms = dict(zip(STAGE_NAMES, [float(v) for v in ms]))
     return out
+
+
+def route_tokens(w: MoELayerWeights, x) -> RouteResult:
+    """route_logits + route (engine.cpp:121-122) with the router attached to `w` (its own, or
+    the full model's on an expert-parallel slice); host buffers."""
+    L = _lib.load()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2 or x.shape[1] != w.config.d_model:
+        raise ShapeError(f"route_tokens: tokens must be B x {w.config.d_model}")
+    E, K = getattr(w, "route_shape", (w.config.n_experts, w.config.top_k))
+    B = x.shape[0]
+    ids = np.empty((B, K), np.int32)
+    wts = np.empty((B, K), np.float32)
+    a = SkbForwardArgs()
+    a.batch, a.mode = B, MODE_ROUTE_ONLY
+    a.x = x.ctypes.data
+    a.ids_out, a.weights_out = ids.ctypes.data, wts.ctypes.data
+    _check(L.skb_layer_forward(w._h, C.byref(a), None))
+    return RouteResult(B, K, ids, wts)
+
+
+def forward_routed(w: MoELayerWeights, x, ids, weights=None, s_routed: float = 0.0, *,
+                   flags: int = 0) -> np.ndarray:
+    """External routing (the owner-rank half of expert parallelism): row t of x goes through
+    experts ids[t, :] of THIS layer with combine weights `weights` (None = 1.0, i.e. the
+    un-weighted slot output for top_k = 1), top-k selection at s_routed."""
+    L = _lib.load()
+    cfg = w.config
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    ids = np.ascontiguousarray(ids, dtype=np.int32).reshape(x.shape[0], cfg.top_k)
+    y = np.empty((x.shape[0], cfg.d_model), np.float32)
+    a = SkbForwardArgs()
+    a.batch, a.mode, a.flags = x.shape[0], MODE_TOPK, flags
+    a.s_routed, a.s_shared = float(s_routed), 0.0
+    a.x, a.y, a.ids_in = x.ctypes.data, y.ctypes.data, ids.ctypes.data
+    keep = [x, y, ids]
+    if weights is not None:
+        wt = np.ascontiguousarray(weights, dtype=np.float32).reshape(ids.shape)
+        a.weights_in = wt.ctypes.data
+        keep.append(wt)
+    _check(L.skb_layer_forward(w._h, C.byref(a), None))
+    return y
 
 
 def forward_dense(w: MoELayerWeights, x, threads: int = 1, *, flags: int = 0,

@@ -1,0 +1,127 @@
+"""Expert parallelism, host-side logic: 2 (and 3) gloo ranks on CPU tensors with an oracle
+backend against the single-process oracle layer.  Covers destination sorting, the counts and
+rows all-to-all-v, un-sorting, combine order and the replicated shared expert -- everything of
+paper_2605_08575_b200/ep.py except the CUDA kernels behind the backend (tests/test_gpu_parity.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.pyoracle import Config, Oracle
+
+
+class OracleBackend:
+    """Backend of ExpertParallelLayer made of oracle calls (TEST INFRASTRUCTURE)."""
+
+    def __init__(self, w, rank, world):
+        from paper_2605_08575_b200.ep import owner_ranges
+        self.o = Oracle.get()
+        self.w = w
+        cfg = w.cfg
+        self.n_experts, self.top_k = cfg.n_experts, cfg.top_k
+        self.e_lo, self.e_hi = owner_ranges(cfg.n_experts, world)[rank]
+        self.has_shared = cfg.has_shared
+        self.calls = 0
+
+    def route(self, x):
+        xn = x.numpy()
+        logits = np.stack([self.o.matvec(self.w.router, xn[t]) for t in range(xn.shape[0])])
+        rc, ids, wts = self.o.route(logits, self.top_k, self.w.cfg.renormalize)
+        assert rc == 0
+        return torch.from_numpy(ids.copy()), torch.from_numpy(wts.copy())
+
+    def _ffn(self, g, u, d, x, s):
+        o = self.o
+        h = o.swiglu_rows(o.matvec(g, x), o.matvec(u, x))
+        mask = o.mask_smallest(h, o.n_off(s, h.size))
+        h = np.where(mask != 0, h, np.float32(0.0)).astype(np.float32)
+        rc, y = o.gathered_matvec_t(d, np.arange(h.size, dtype=np.int32), h)
+        assert rc == 0
+        return y
+
+    def experts(self, rows, local_ids, s):
+        self.calls += 1
+        out = np.empty(tuple(rows.shape), np.float32)
+        for i in range(rows.shape[0]):
+            e = self.e_lo + int(local_ids[i])
+            assert self.e_lo <= e < self.e_hi
+            out[i] = self._ffn(self.w.gate[e], self.w.up[e], self.w.down_t[e], rows[i].numpy(), s)
+        return torch.from_numpy(out)
+
+    def shared(self, x, s):
+        w = self.w
+        return torch.from_numpy(np.stack([
+            self._ffn(w.shared_gate, w.shared_up, w.shared_down_t, x[t].numpy(), s)
+            for t in range(x.shape[0])]))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_08575_b200.ep import ExpertParallelLayer
+        E, K, D, N, S, B, s = case
+        o = Oracle.get()
+        cfg = Config(E, K, D, N, S, True)
+        w = o.generate_synthetic(cfg, 5, 0.1)
+        x = o.generate_tokens(B, D, 7)
+        # ragged home batches: rank r takes tokens [lo, hi)
+        cuts = np.linspace(0, B, world + 1).astype(int)
+        cuts[1] = min(B, cuts[1] + 1) if world > 1 else cuts[1]
+        mine = x[cuts[rank]:cuts[rank + 1]]
+        layer = ExpertParallelLayer(OracleBackend(w, rank, world))
+        y = layer.forward(torch.from_numpy(mine.copy()), s, s if S else 0.0)
+        np.save(os.path.join(out_dir, f"y{rank}.npy"), y.numpy())
+        np.save(os.path.join(out_dir, f"stats{rank}.npy"),
+                np.array([sum(layer.last_stats["sent_rows"]), sum(layer.last_stats["recv_rows"])]))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [
+    (8, 2, 16, 24, 0, 9, 0.5),
+    (6, 3, 12, 20, 10, 7, 0.25),   # shared expert, E not divisible by 4
+    (4, 1, 8, 16, 8, 5, 0.9),      # top-1: some ranks may receive nothing
+]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", CASES)
+def test_ep_matches_single_process_oracle(tmp_path, world, case):
+    E, K, D, N, S, B, s = case
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, case, str(tmp_path)), nprocs=world, join=True)
+    o = Oracle.get()
+    cfg = Config(E, K, D, N, S, True)
+    w = o.generate_synthetic(cfg, 5, 0.1)
+    x = o.generate_tokens(B, D, 7)
+    routed, shared = o.build_topk_masks(w, x, s, mode=1 if S else 0)
+    y_ref, _ = o.forward(w, x, routed, shared)
+    y = np.concatenate([np.load(tmp_path / f"y{r}.npy") for r in range(world)])
+    # identical arithmetic in identical order: bit for bit
+    np.testing.assert_array_equal(y, y_ref)
+    sent = sum(int(np.load(tmp_path / f"stats{r}.npy")[0]) for r in range(world))
+    recv = sum(int(np.load(tmp_path / f"stats{r}.npy")[1]) for r in range(world))
+    assert sent == recv == B * K
+
+
+def test_owner_ranges_cover_all_experts():
+    from paper_2605_08575_b200.ep import owner_ranges
+    for E in (1, 7, 8, 128, 130):
+        for world in (1, 2, 3, 8):
+            r = owner_ranges(E, world)
+            assert r[0][0] == 0 and r[-1][1] == E
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [hi - lo for lo, hi in r]
+            assert max(sizes) - min(sizes) <= 1

@@ -548,3 +548,78 @@ def test_cpp_facade_matches_python_path(skb, tmp_path):
     lvl = skb.SparsityLevel(0.5)
     y = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
     assert float(np.sum(y.astype(np.float64))) == pytest.approx(checksum, rel=1e-6, abs=1e-7)
+
+
+# ---------------------------------------------------------------------------------------------
+# expert parallelism: the CUDA halves (route-only, external routing, synthetic slices)
+# ---------------------------------------------------------------------------------------------
+def test_route_only_and_external_routing(skb, oracle):
+    cfg = Config(8, 2, 96, 160, 0, True)
+    w, x = rounded_case(oracle, cfg, 4, 0.1, 19, 6)
+    w.router = oracle.generate_synthetic(cfg, 4, 0.1).router
+    layer = make_layer(skb, w)
+    logits = np.stack([oracle.matvec(w.router, x[t]) for t in range(x.shape[0])])
+    _, ids_ref, wts_ref = oracle.route(logits, 2, True)
+    r = skb.route_tokens(layer, x)
+    np.testing.assert_array_equal(r.ids, ids_ref)
+    np.testing.assert_allclose(r.weights, wts_ref, rtol=1e-6)
+    # experts [4, 8) as an expert-parallel slice built from arrays, with the full router attached
+    lo, hi = 4, 8
+    sl_cfg = skb.MoEConfig(hi - lo, 1, 96, 160, False, 0, True, 64)
+    sl = skb.MoELayerWeights.from_arrays(sl_cfg, w.router[lo:hi], w.gate[lo:hi], w.up[lo:hi],
+                                         w.down_t[lo:hi])
+    with pytest.raises(skb.IndexError_):
+        skb.forward_routed(sl, x[:2], np.array([0, 4], np.int32))
+    sl.set_router(w.router, 2, True)
+    np.testing.assert_array_equal(skb.route_tokens(sl, x).ids, ids_ref)
+    with pytest.raises(skb.ConfigError):
+        skb.forward_dense(sl, x)              # a slice has no routing of its own
+    rng = np.random.default_rng(1)
+    local = rng.integers(0, hi - lo, x.shape[0]).astype(np.int32)
+    for s in (0.0, 0.5):
+        y = skb.forward_routed(sl, x, local, s_routed=s)
+        for t in range(x.shape[0]):
+            e = lo + int(local[t])
+            h = oracle.swiglu_rows(oracle.matvec(w.gate[e], x[t]), oracle.matvec(w.up[e], x[t]))
+            m = oracle.mask_smallest(h, oracle.n_off(s, 160))
+            _, ref = oracle.gathered_matvec_t(w.down_t[e], np.arange(160, dtype=np.int32),
+                                              np.where(m != 0, h, np.float32(0)).astype(np.float32))
+            assert max_rel_diff(y[t], ref) <= TOL_FP32_ACCUM
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_ep_slices_reproduce_the_single_gpu_layer(skb, world):
+    """ExpertParallelLayer over `world` CUDA backends living on this one GPU (the all-to-all is
+    replaced by slicing, everything else is the production code path) against the whole
+    synthetic layer: identical expert ids, outputs to the fp32 tolerance."""
+    import torch
+    from paper_2605_08575_b200 import ep
+    full = skb.MoEConfig(16, 4, 256, 192, True, 64, True, 64)
+    B, s = 24, 0.5
+    x = np.random.default_rng(3).standard_normal((B, 256)).astype(np.float32)
+    whole = skb.MoELayerWeights.generate_synthetic(full, 1, 0.05)
+    lvl = skb.SparsityLevel(s)
+    ref = skb.forward_topk_sparse(whole, x, lvl, lvl, capture=True)
+    backs = [ep.CudaBackend(skb, full, 1, 0.05, r, world) for r in range(world)]
+    xd = torch.from_numpy(x).cuda()
+    ids, wts = backs[0].route(xd)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy(), ref.routes.ids)
+    slot = torch.empty((B, 4, 256), device="cuda")
+    for b in backs:
+        sel = (ids >= b.e_lo) & (ids < b.e_hi)
+        t_idx, s_idx = torch.nonzero(sel, as_tuple=True)
+        if t_idx.numel() == 0:
+            continue
+        out = b.experts(xd[t_idx], (ids[t_idx, s_idx] - b.e_lo).to(torch.int32), s)
+        slot[t_idx, s_idx] = out
+    y = torch.zeros((B, 256), device="cuda")
+    for k in range(4):
+        y = y + wts[:, k:k + 1] * slot[:, k]
+    y = y + backs[0].shared(xd, s)
+    torch.cuda.synchronize()
+    assert max_rel_diff(y.cpu().numpy(), ref.outputs) <= TOL_FP32_ACCUM
+    if world == 1:   # the production wrapper itself (no process group: world 1)
+        y1 = ep.ExpertParallelLayer(backs[0]).forward(xd, s, s)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y1.cpu().numpy(), y.cpu().numpy())
