@@ -261,6 +261,109 @@ class Point:
         return times, self.B * D * 4, self.B * D * 4
 
 
+def run_ep(args, torch, dist, skb, rank, world, local):
+    """Expert-parallel arm (north-star: GPT-OSS and Maverick shapes): experts sharded over the
+    ranks, tokens home-sharded, dispatch/combine as NCCL all-to-all-v (paper_2605_08575_b200/ep.py).
+    With one rank the same code path runs with local slicing instead of the collective."""
+    from paper_2605_08575_b200 import ep
+    shape = WORKLOADS[args.workload]
+    B, s = args.batch, args.sparsity
+    hbm_peak, peak_src = peaks()
+    cfg = skb.MoEConfig(shape["E"], shape["K"], shape["D"], shape["N"], shape["S"] > 0, shape["S"],
+                        True, 64)
+    backend = ep.CudaBackend(skb, cfg, SEED, SCALE, rank, world, device=local,
+                             max_rows=max(64, 4 * B * shape["K"]))
+    layer = ep.ExpertParallelLayer(backend)
+    xs = [torch.from_numpy(make_tokens(B, shape["D"], 2 + 17 * rank + i)).cuda() for i in range(8)]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    ssh = s if shape["S"] else 0.0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        if i >= args.warmup:
+            ev[i - args.warmup][0].record()
+        y = layer.forward(xs[i % 8], s, ssh)
+        if i >= args.warmup:
+            ev[i - args.warmup][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    # end to end: pinned host tokens in, host outputs out, per step
+    xin = [x.cpu().pin_memory() for x in xs]
+    yout = torch.empty((B, shape["D"]), dtype=torch.float32).pin_memory()
+    xdev = torch.empty_like(xs[0])
+    e2e_t = []
+    for i in range(3 + min(args.steps, 50)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xdev.copy_(xin[i % 8], non_blocking=True)
+        yout.copy_(layer.forward(xdev, s, ssh), non_blocking=True)
+        torch.cuda.synchronize()
+        if i >= 3:
+            e2e_t.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = float(np.mean(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    # algorithmic bytes of this rank's step (upper bound on the union of kept rows)
+    ids, _ = backend.route(xs[0])
+    torch.cuda.synchronize()
+    idn = ids.cpu().numpy().reshape(-1)
+    keep_r = shape["N"] - n_off(s, shape["N"])
+    keep_s = shape["S"] - n_off(ssh, shape["S"]) if shape["S"] else 0
+    cnt = np.bincount(idn, minlength=shape["E"])
+    r_down = int(np.minimum(shape["N"], cnt * keep_r).sum())
+    D = shape["D"]
+    bytes_alg = (shape["E"] * D * 2 + int((cnt > 0).sum()) * 2 * shape["N"] * D * 2 + r_down * D * 2
+                 + (2 * shape["S"] * D * 2 + min(shape["S"], B * keep_s) * D * 2 if shape["S"] else 0)
+                 + B * D * 8)
+    clocks = sampler.stop() if rank == 0 else None
+    if rank == 0:
+        gbs = bytes_alg / (ms * 1e-3) / 1e9
+        print(json.dumps({
+            "metric": "MoE-layer tokens/s (decode) at intra-expert sparsity s; HBM GB/s in roofline/sweep",
+            "value": round(world * B / (ms * 1e-3), 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"{shape['name']} shape, E={shape['E']} top-{shape['K']} "
+                                   f"d_model={D} d_ffn={shape['N']} d_shared={shape['S']}, "
+                                   f"batch {B} decode per GPU, top-k neuron selection s={s}",
+                       "sparsity": s, "batch_per_gpu": B,
+                       "parallelism": f"expert parallel x{world}: experts sharded, all-to-all-v "
+                                      "dispatch/combine over NCCL, shared expert replicated",
+                       "l2": "512 MiB memset between steps (inside the timed pair is only the "
+                             "layer) + ring of 8 token batches",
+                       "launch": "direct launches; the counts exchange synchronises once per step"},
+            "bytes_alg_per_step_rank0_upper_bound": int(bytes_alg),
+            "roofline": {"bound": "hbm", "kernel": "whole EP step (rank 0)", "achieved": round(gbs, 1),
+                         "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+                         "traffic": None, "peak_source": peak_src},
+            "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
+                    "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": B * D * 4,
+                    "d2h_bytes_per_step": B * D * 4},
+            "gpu_launches": None, "clocks": clocks, "cpu_baseline": None,
+            "ep_stats": layer.last_stats}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -276,6 +379,9 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2605_08575_b200 as skb
+
+    if args.ep or (world > 1 and args.workload in ("maverick", "gptoss")):
+        return run_ep(args, torch, dist, skb, rank, world, local)
 
     shape = WORKLOADS[args.workload]
     B, s = args.batch, args.sparsity
@@ -497,6 +603,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel arm (ep.py) at any rank count")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

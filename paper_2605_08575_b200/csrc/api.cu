@@ -112,6 +112,8 @@ struct skb_layer {
   __nv_bfloat16* d_xs = nullptr;
   uint64_t xs_rows = 0;
   CUtensorMap tmap_x[5]{};
+  __nv_bfloat16* d_xb = nullptr;  // decode: bf16 token rows [max(cap,16)][Dp] (token-indexed tiles)
+  CUtensorMap tmap_xb{};
   float* d_h = nullptr;
   __nv_bfloat16* d_hb = nullptr;  // masked activations, [3][rows][Nh] bf16 terms
   CUtensorMap tmap_hb[5][3]{};
@@ -140,7 +142,8 @@ void free_workspace(skb_layer* L) {
                   L->disp.n_tiles, L->d_xs,      L->d_h,            L->d_kidx,
                   L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
-                  L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage};
+                  L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
+                  L->d_xb,       L->disp.tile_colrow};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -152,6 +155,7 @@ void free_workspace(skb_layer* L) {
   L->d_slot_out = nullptr;
   L->d_ids_stage = nullptr;
   L->d_wts_stage = nullptr;
+  L->d_xb = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -199,6 +203,13 @@ int reserve_locked(skb_layer* L, int B) {
   SKB_TRY(dmalloc(&L->disp.tile_row0, max_tiles));
   SKB_TRY(dmalloc(&L->disp.tile_nrows, max_tiles));
   SKB_TRY(dmalloc(&L->disp.n_tiles, 1));
+  SKB_TRY(dmalloc(&L->disp.tile_colrow, max_tiles * 16));
+  {
+    const size_t xb_rows = cap > 16 ? cap : 16;
+    SKB_TRY(dmalloc(&L->d_xb, xb_rows * g.Dp));
+    SKB_CUDA(cudaMemsetAsync(L->d_xb, 0, xb_rows * g.Dp * sizeof(__nv_bfloat16), L->stream));
+    SKB_TRY(encode_bf16_2d(&L->tmap_xb, L->d_xb, xb_rows, g.Dp, 16));
+  }
   {
     const size_t n_counters = 2 + static_cast<size_t>(cap);
     SKB_TRY(dmalloc(&L->d_counters, n_counters));
@@ -418,6 +429,11 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     const int cap = dense_down ? 128 : 256;
     while (tn < cap && tn < want) tn <<= 1;
   }
+  // decode: token-indexed tiles built inside the router kernel (no expert-sorted token copy)
+  // (the dense down projection walks the same tile list and needs it expert-sorted)
+  const bool token_tiles = d_ids_in == nullptr && tn == 16 && !dense_down &&
+                           !(a->flags & SKB_FLAG_SIMT_GATEUP) &&
+                           !(a->flags & SKB_FLAG_FAST_ROUTER) && router_token_tiles(B, g.K, true);
   int tn_idx = 0;
   while (kTileCases[tn_idx] != tn) ++tn_idx;
   const int max_tiles = max_tiles_for(g, B, tn);
@@ -449,17 +465,20 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     r.dispatch = &L->disp;
     r.has_shared = g.has_shared;
     r.tile_tokens = tn;
+    r.xb = token_tiles ? L->d_xb : nullptr;
+    r.Dp = g.Dp;
     launches += launch_router(ctx, r);
   }
   tm.mark();
-  launches += launch_permute_tokens(ctx, d_x, L->disp.perm, B, g.K, g.D, g.Dp, g.has_shared,
-                                    L->d_xs);
+  if (!token_tiles)
+    launches += launch_permute_tokens(ctx, d_x, L->disp.perm, B, g.K, g.D, g.Dp, g.has_shared,
+                                      L->d_xs);
   tm.mark();
   if (a->flags & SKB_FLAG_SIMT_GATEUP)
     launches += launch_gateup_simt(ctx, L->d_wgu, L->d_xs, L->disp.row_expert, rows, g, L->d_h);
   else
-    launches += launch_gateup_tc(ctx, &L->tmap_w, &L->tmap_x[tn_idx], tn, L->disp, max_tiles, g,
-                                 L->d_h);
+    launches += launch_gateup_tc(ctx, &L->tmap_w, token_tiles ? &L->tmap_xb : &L->tmap_x[tn_idx],
+                                 tn, L->disp, max_tiles, g, L->d_h, token_tiles);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel

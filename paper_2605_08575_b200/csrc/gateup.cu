@@ -147,6 +147,7 @@ struct TcArgs {
   const int32_t* tile_row0;
   const int32_t* tile_nrows;
   const int32_t* n_tiles;
+  const int32_t* tile_colrow;  // token-indexed tiles (MODE 0, TN 16): [tile][16] h row or -1
   float* out;       // MODE 0: h [rows][out_stride];  MODE 1: slot outputs [rows][out_stride]
   int out_stride;
   int n_experts;
@@ -299,8 +300,11 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
             const float g = is_gate_lane ? mine0 : recv;
             const float u = is_gate_lane ? recv : mine1;
             const int col = c0 + c + (is_gate_lane ? 0 : 1);
-            if (col < nrows && n < m_valid)
-              a.out[static_cast<size_t>(row0 + col) * a.out_stride + n] = silu_f(g) * u;
+            if (col < nrows && n < m_valid) {
+              const int r = (TN == 16 && a.tile_colrow != nullptr) ? a.tile_colrow[tile * 16 + col]
+                                                                   : row0 + col;
+              if (r >= 0) a.out[static_cast<size_t>(r) * a.out_stride + n] = silu_f(g) * u;
+            }
           }
         }
       } else {
@@ -362,8 +366,9 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h) {
+                     float* h, bool token_tiles) {
   TcArgs a{};
+  a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;
   a.tile_expert = d.tile_expert;
   a.tile_row0 = d.tile_row0;
   a.tile_nrows = d.tile_nrows;

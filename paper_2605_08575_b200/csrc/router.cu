@@ -16,15 +16,17 @@ namespace skb {
 // and add rounded separately (the reference is built with -ffp-contract=off,
 // proj/CMakeLists.txt:26-27).  That chain is inherently serial (D dependent FADDs), so the
 // kernel is organised around it: one single-warp CTA per (8 experts x 4 tokens) runs 32
-// chains, one per lane, and feeds itself through an 8-deep cp.async ring of 128-float
-// sub-chunks (no block barriers at all).  The CTA that completes a token block's logits
+// chains, one per lane, fed by a second warp through a 4-deep ring of 512-float sub-chunks
+// (1-D TMA bulk copies, mbarrier hand-off, no block barriers in the loop).  Measured on B200: a
+// dependent fp32 add chain advances one element per ~5.5-6.5 cycles (tools/micro/chain_lat.cu).  The CTA that completes a token block's logits
 // ("last arriver" on a global counter) runs route() for those tokens; the CTA that completes
 // the last token block builds the dispatch when B*K is small (decode).
 // ---------------------------------------------------------------------------------------------
 constexpr int kRfEB = 8;        // experts per CTA
 constexpr int kRfTB = 4;        // tokens per CTA
-constexpr int kRfSub = 128;     // floats per sub-chunk
-constexpr int kRfStages = 8;    // ring depth
+constexpr int kRfSub = 512;     // floats per sub-chunk (one mbarrier wait costs ~300 cycles of the
+                                // chain: measured 18.0k cycles at 128, so waits are kept rare)
+constexpr int kRfStages = 4;    // ring depth
 constexpr int kRfRow = kRfSub + 4;  // padded row stride (floats): conflict-free LDS.128
 constexpr int kRfRows = kRfEB + kRfTB;
 constexpr int kRfSmemFloats = kRfStages * kRfRows * kRfRow;
@@ -137,7 +139,7 @@ __device__ void warp_route_token(const float* __restrict__ row, int E, int K, in
 // by direct counting (O((B*K)^2 / 32), no scans).  Same outputs as dispatch_kernel.
 __device__ void warp_small_dispatch(const int32_t* __restrict__ ids, int B, int K, int E,
                                     int has_shared, int tile_tokens, const DispatchBuffers& d,
-                                    int32_t* sc /* >= 4 * kSmallSlots ints */) {
+                                    int32_t* sc /* >= 4 * kSmallSlots ints */, bool token_tiles) {
   const int lane = threadIdx.x & 31;
   const int BK = B * K;
   int32_t* ids_s = sc;
@@ -164,6 +166,45 @@ __device__ void warp_small_dispatch(const int32_t* __restrict__ ids, int B, int 
     d.row_expert[pos] = e;
   }
   __syncwarp();
+  if (token_tiles) {
+    // Token-indexed tiles (B <= 16): one tile per distinct expert; column c of the tile is
+    // token c, tile_colrow names the h row of (token c, this expert) or -1.  The GEMM reads
+    // the bf16 token rows directly.
+    int heads = 0;
+    for (int i = lane; i < BK; i += 32) {
+      if (rank_s[i] == 0) {  // first slot of its expert
+        const int e = ids_s[i];
+        int ti = 0;
+        for (int j = 0; j < BK; ++j) ti += (rank_s[j] == 0 && ids_s[j] < e);
+        d.tile_expert[ti] = e;
+        d.tile_row0[ti] = 0;
+        d.tile_nrows[ti] = B;
+        for (int c = 0; c < 16; ++c) {
+          int r = -1;
+          if (c < B)
+            for (int s2 = 0; s2 < K; ++s2)
+              if (ids_s[c * K + s2] == e) r = pos_s[c * K + s2];
+          d.tile_colrow[ti * 16 + c] = r;
+        }
+        ++heads;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) heads += __shfl_xor_sync(0xffffffffu, heads, o);
+    int n_tiles = heads;
+    if (has_shared) {
+      if (lane < 16) d.tile_colrow[n_tiles * 16 + lane] = lane < B ? BK + lane : -1;
+      if (lane == 0) {
+        d.tile_expert[n_tiles] = E;
+        d.tile_row0[n_tiles] = 0;
+        d.tile_nrows[n_tiles] = B;
+      }
+      for (int t = lane; t < B; t += 32) d.row_expert[BK + t] = E;
+      n_tiles += 1;
+    }
+    if (lane == 0) *d.n_tiles = n_tiles;
+    return;
+  }
   int heads = 0;
   for (int i = lane; i < BK; i += 32) {
     if (cnt_s[i] > 0) {
@@ -217,6 +258,9 @@ struct RouterFusedArgs {
   int fuse_route;     // 1: the last CTA of a token block runs route() (decode); 0: route_tokens_kernel
   int fuse_dispatch;  // 1: the last CTA also builds the dispatch (B*K <= kSmallSlots)
   int has_shared, tile_tokens;
+  int n_eb;            // expert blocks (CTAs per token block that run chains)
+  __nv_bfloat16* xb;   // token tiles: bf16 copy of x, [B][Dp]; written by CTA column n_eb
+  int Dp;
   float* logits;
   int32_t* ids;
   float* weights;
@@ -254,6 +298,19 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   pdl_wait();
   pdl_launch_dependents();
   RF_T(1);
+
+  if (a.xb != nullptr && static_cast<int>(blockIdx.x) == a.n_eb) {
+    // conversion CTAs (token tiles): xb[t] = bf16(x[t]) for this token block, in parallel with
+    // the chains of the other CTAs; pad columns [D, Dp) stay zero
+    for (int tt = 0; tt < kRfTB; ++tt) {
+      const int t = t0 + tt;
+      if (t >= a.B) break;
+      const float* src = a.x + static_cast<size_t>(t) * D;
+      __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * a.Dp;
+      for (int d = threadIdx.x; d < D; d += 64) dst[d] = __float2bfloat16_rn(__ldg(src + d));
+    }
+    return;
+  }
 
   if (!a.logits_ready) {
     const int nsub = ceil_div(D, kRfSub);
@@ -360,7 +417,7 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
     if (lane == 0) prev = atomicAdd(&a.counters[1 + blockIdx.y], 1u);
     prev = __shfl_sync(0xffffffffu, prev, 0);
     RF_T(3);
-    if (prev != gridDim.x - 1) return;
+    if (prev != static_cast<unsigned>(a.n_eb - 1)) return;
     if (lane == 0) a.counters[1 + blockIdx.y] = 0;  // at rest again for the next forward
     __threadfence();
     RF_T(4);
@@ -377,17 +434,20 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   RF_T(5);
   if (!a.fuse_dispatch) return;
 
-  __threadfence();
+  if (gridDim.y > 1) {  // a single token block is its own last arriver
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(&a.counters[0], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != gridDim.y - 1) return;
+    if (lane == 0) a.counters[0] = 0;
+    __threadfence();
+  }
   __syncwarp();
-  unsigned prev = 0;
-  if (lane == 0) prev = atomicAdd(&a.counters[0], 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != gridDim.y - 1) return;
-  if (lane == 0) a.counters[0] = 0;
-  __threadfence();
   RF_T(6);
   warp_small_dispatch(a.ids, a.B, a.K, a.E, a.has_shared, a.tile_tokens, a.d,
-                      reinterpret_cast<int32_t*>(rf_smem));
+                      reinterpret_cast<int32_t*>(rf_smem), a.xb != nullptr);
   RF_T(7);
 }
 
@@ -427,6 +487,10 @@ __global__ void __launch_bounds__(256) router_logits_fast_kernel(const float* __
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) logits[static_cast<size_t>(t) * E + e] = acc;
+}
+
+bool router_token_tiles(int B, int K, bool want) {
+  return want && B <= 16 && B <= 2 * kRfTB && B * K <= kSmallSlots;
 }
 
 int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
@@ -471,8 +535,12 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   a.weights = r.weights;
   a.counters = r.counters;
   if (r.dispatch) a.d = *r.dispatch;
+  a.n_eb = a.logits_ready ? 1 : ceil_div(r.E, kRfEB);
+  const bool token_tiles = a.fuse_dispatch && router_token_tiles(r.B, r.K, r.xb != nullptr);
+  a.xb = token_tiles ? r.xb : nullptr;
+  a.Dp = r.Dp;
   if (!(a.logits_ready && !a.fuse_route)) {
-    cfg.gridDim = dim3(a.logits_ready ? 1 : ceil_div(r.E, kRfEB), ceil_div(r.B, kRfTB));
+    cfg.gridDim = dim3(a.n_eb + (token_tiles ? 1 : 0), ceil_div(r.B, kRfTB));
     cfg.blockDim = dim3(64);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchKernelEx(&cfg, router_fused_kernel, a);

@@ -54,6 +54,7 @@ struct DispatchBuffers {
   int32_t* tile_row0;    // [max_tiles]
   int32_t* tile_nrows;   // [max_tiles]
   int32_t* n_tiles;      // [1]
+  int32_t* tile_colrow;  // [max_tiles][16] token-indexed tiles (decode): h row of column c, or -1
 };
 
 // ---- launchers (one per stage; each returns the number of kernels it launched) ----
@@ -77,7 +78,14 @@ struct RouterLaunch {
   unsigned* counters;
   const DispatchBuffers* dispatch;
   int has_shared, tile_tokens;
+  // decode (B <= 16, dispatch built inside the router kernel): extra CTAs convert the tokens to
+  // bf16 rows xb[B][Dp] while the chains run, and the tile list is token-indexed -- the gate/up
+  // GEMM reads token rows directly, no expert-sorted copy (no permute kernel)
+  __nv_bfloat16* xb;
+  int Dp;
 };
+// true when launch_router() will build token-indexed tiles for this call
+bool router_token_tiles(int B, int K, bool want);
 int launch_router(const LaunchCtx& ctx, const RouterLaunch& r);
 int launch_dispatch(const LaunchCtx& ctx, const int32_t* ids, int B, int K, int E, int has_shared,
                     int tile_tokens, const DispatchBuffers& d);
@@ -88,7 +96,7 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h);
+                     float* h, bool token_tiles);
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
