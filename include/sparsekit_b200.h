@@ -88,6 +88,9 @@ enum {
 #define SKB_FLAG_BF16_H 0x40u      /* dense down projection: h rounded to bf16 (1e-2 mode) instead
                                       of the exact three-term bf16 split (1e-5 mode) */
 
+#define SKB_FLAG_NO_FUSED_DECODE 0x80u /* batches <= 16: use the staged kernels instead of the
+                                          single persistent decode kernel */
+
 #define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
 
 typedef struct skb_forward_args {

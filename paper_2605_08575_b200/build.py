@@ -18,8 +18,10 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libsparsekit_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["api.cu", "router.cu", "gateup.cu", "select.cu", "down.cu", "image.cu"]
-HEADERS = [os.path.join(CSRC, "skb_internal.cuh"), os.path.join(INCLUDE, "sparsekit_b200.h")]
+SOURCES = ["api.cu", "router.cu", "gateup.cu", "select.cu", "down.cu", "image.cu", "decode.cu"]
+HEADERS = [os.path.join(CSRC, h) for h in ("skb_internal.cuh", "tc_ptx.cuh", "route_device.cuh",
+                                           "select_device.cuh")] + [
+    os.path.join(INCLUDE, "sparsekit_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -66,7 +68,7 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
         for f in os.listdir(OBJ_DIR):
             os.remove(os.path.join(OBJ_DIR, f))
     log: list[str] = []
-    with ThreadPoolExecutor(max_workers=6) as pool:
+    with ThreadPoolExecutor(max_workers=8) as pool:
         objs = list(pool.map(lambda s: _compile(s, log), SOURCES))
     if _stale(LIB_PATH, objs):
         cmd = [_nvcc(), "-shared", "-cudart", "static", "-o", LIB_PATH, *objs,

@@ -126,6 +126,15 @@ struct skb_layer {
   uint8_t* d_mask_out_r = nullptr;
   uint8_t* d_mask_out_s = nullptr;
 
+  // fused decode kernel (decode.cu)
+  int n_sms = 0;
+  float* d_dec_lf = nullptr;
+  float* d_dec_lm = nullptr;
+  float* d_dec_hc = nullptr;
+  uint32_t* d_dec_hist = nullptr;
+  float* d_dec_part = nullptr;
+  unsigned* d_dec_ctr = nullptr;
+
   cudaEvent_t ev[SKB_N_STAGES + 1]{};
   float stage_ms[SKB_N_STAGES]{};
   bool have_stage_ms = false;
@@ -143,7 +152,8 @@ void free_workspace(skb_layer* L) {
                   L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
                   L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
-                  L->d_xb,       L->disp.tile_colrow};
+                  L->d_xb,       L->disp.tile_colrow, L->d_dec_lf,    L->d_dec_lm,
+                  L->d_dec_hc,   L->d_dec_hist,  L->d_dec_part,     L->d_dec_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -156,6 +166,9 @@ void free_workspace(skb_layer* L) {
   L->d_ids_stage = nullptr;
   L->d_wts_stage = nullptr;
   L->d_xb = nullptr;
+  L->d_dec_lf = L->d_dec_lm = L->d_dec_hc = L->d_dec_part = nullptr;
+  L->d_dec_hist = nullptr;
+  L->d_dec_ctr = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -214,6 +227,18 @@ int reserve_locked(skb_layer* L, int B) {
     const size_t n_counters = 2 + static_cast<size_t>(cap);
     SKB_TRY(dmalloc(&L->d_counters, n_counters));
     SKB_CUDA(cudaMemsetAsync(L->d_counters, 0, n_counters * sizeof(unsigned), L->stream));
+  }
+  if (decode_fused_eligible(g, 1)) {
+    const size_t crow = 16 * static_cast<size_t>(decode_cand_rows(g.K)) + 16;
+    SKB_TRY(dmalloc(&L->d_dec_lf, 16 * static_cast<size_t>(g.E)));
+    SKB_TRY(dmalloc(&L->d_dec_lm, 16 * static_cast<size_t>(g.E)));
+    SKB_TRY(dmalloc(&L->d_dec_hc, crow * g.Nh));
+    SKB_TRY(dmalloc(&L->d_dec_hist, crow * 512));
+    SKB_TRY(dmalloc(&L->d_dec_part,
+                    16 * (static_cast<size_t>(L->n_sms) + g.K + 1) * g.Dp));
+    SKB_TRY(dmalloc(&L->d_dec_ctr, static_cast<size_t>(decode_counter_words())));
+    SKB_CUDA(cudaMemsetAsync(L->d_dec_ctr, 0, decode_counter_words() * sizeof(unsigned), L->stream));
+    SKB_CUDA(cudaMemsetAsync(L->d_dec_hist, 0, crow * 512 * sizeof(uint32_t), L->stream));
   }
   L->xs_rows = rows;
   SKB_TRY(dmalloc(&L->d_xs, rows * g.Dp));
@@ -279,6 +304,7 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
   skb_layer* L = new skb_layer();
   L->cfg = *cfg;
   L->device = device;
+  L->n_sms = prop.multiProcessorCount;
   Geometry& g = L->g;
   g.E = cfg->n_experts;
   g.K = cfg->top_k;
@@ -358,7 +384,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                  const uint8_t* d_mask_r, const uint8_t* d_mask_s, uint8_t* d_mask_out_r,
                  uint8_t* d_mask_out_s, cudaStream_t stream, bool timing,
                  const int32_t* d_ids_in = nullptr, const float* d_w_in = nullptr,
-                 int32_t* d_ids_out = nullptr, float* d_w_out = nullptr) {
+                 int32_t* d_ids_out = nullptr, float* d_w_out = nullptr, bool capture_h = false) {
   const Geometry& g = L->g;
   const int B = a->batch;
   const int BK = B * g.K;
@@ -420,6 +446,73 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
   }
   const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
+
+  // Decode batches: the whole layer as one persistent launch (decode.cu).
+  if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
+      !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
+                    SKB_FLAG_NO_FUSED_DECODE))) {
+    const bool want_masks = d_mask_out_r != nullptr || d_mask_out_s != nullptr;
+    DecodeLaunch dl{};
+    dl.x = d_x;
+    dl.router = L->d_router;
+    dl.wd = L->d_wd;
+    dl.wd_shared = L->d_wd_shared;
+    dl.B = B;
+    dl.sel_mode = sel_mode;
+    dl.n_off_r = n_off_r;
+    dl.n_off_s = n_off_s;
+    dl.mask_r = d_mask_r;
+    dl.mask_s = d_mask_s;
+    dl.CH = decode_chunks(g, B, max_keep, L->n_sms);
+    dl.capture = capture_h || want_masks;
+    dl.xb = L->d_xb;
+    dl.lf = L->d_dec_lf;
+    dl.lm = L->d_dec_lm;
+    dl.logits = L->d_logits;
+    dl.ids = L->d_ids;
+    dl.wts = L->d_wts;
+    dl.hc = L->d_dec_hc;
+    dl.hist = L->d_dec_hist;
+    dl.part = L->d_dec_part;
+    dl.ctr = L->d_dec_ctr;
+    dl.y = d_y;
+    dl.h_cap = L->d_h;
+    dl.inv = L->disp.inv;
+    dl.perm = L->disp.perm;
+    dl.row_expert = L->disp.row_expert;
+    tm.mark();
+    tm.mark();
+    tm.mark();
+    launches += launch_decode_fused(ctx, &L->tmap_w, &L->tmap_xb, dl, g, L->n_sms);
+    tm.mark();
+    if (want_masks) {
+      SelectArgs sa{};
+      sa.h = L->d_h;
+      sa.rows = rows;
+      sa.BK = BK;
+      sa.N = g.N;
+      sa.S = g.S;
+      sa.Nh = g.Nh;
+      sa.K = g.K;
+      sa.perm = L->disp.perm;
+      sa.mask_out_routed = d_mask_out_r;
+      sa.mask_out_shared = d_mask_out_s;
+      sa.mode = sel_mode;
+      sa.n_off_routed = n_off_r;
+      sa.n_off_shared = n_off_s;
+      sa.mask_in_routed = d_mask_r;
+      sa.mask_in_shared = d_mask_s;
+      LaunchCtx plain{stream, false};
+      launches += launch_select(plain, sa);
+    }
+    tm.mark();
+    tm.mark();
+    tm.mark();
+    L->last_launches = launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SKB_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return SKB_OK;
+  }
 
   // tile size for the grouped GEMMs: ~1.5x the mean tokens per expert, power of two in
   // [16, 256] (at most 128 when the dense down projection shares the tile list)
@@ -897,7 +990,8 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
   }
   rc = forward_core(L, a, L->d_x, L->d_y, mr, ms, a->routed_mask_out ? L->d_mask_out_r : nullptr,
                     (a->shared_mask_out && g.has_shared) ? L->d_mask_out_s : nullptr, s, timing,
-                    d_ids_in, d_w_in);
+                    d_ids_in, d_w_in, nullptr, nullptr,
+                    a->h_routed_out != nullptr || a->h_shared_out != nullptr);
   if (rc) return rc;
   SKB_CUDA(cudaMemcpyAsync(a->y, L->d_y, B * g.D * 4, cudaMemcpyDeviceToHost, s));
   if (a->ids_out) SKB_CUDA(cudaMemcpyAsync(a->ids_out, L->d_ids, BK * 4, cudaMemcpyDeviceToHost, s));

@@ -1,0 +1,1164 @@
+// decode.cu -- the whole layer for decode batches (B <= 16) as ONE persistent launch.
+//
+// Why one kernel: at decode sizes the layer moves ~10-100 MB, i.e. 10-20 us of HBM time, and
+// every kernel boundary (launch, drain, refill of the memory pipeline) costs 2-5 us of that.
+// The stages of the reference path (proj/src/engine.cpp:94-191) map onto phases of one grid of
+// numSMs CTAs (one per SM, all co-resident), chained by counters in global memory:
+//
+//   P0  fast router logits.  lf[t][e] = x[t].router[e] by a parallel (not order-faithful)
+//       reduction, together with A[t][e] = sum |x.router|.  The reference's logit (ascending-index
+//       float accumulation, proj/src/linalg.cpp:22-40) differs from lf by at most
+//       m = 2*gamma_D*A (gamma_D = D*u/(1-D*u), u = 2^-24: the standard recursive-summation
+//       bound, applied to both sums).  Every expert whose interval [lf-m, lf+m] reaches the K-th
+//       largest lower end is a CANDIDATE of the token; the reference's top-K set is provably a
+//       subset.  Typically K candidates, sometimes K+1.  (More than K+4, non-finite values, or
+//       a threshold more than 60 below the maximum -- the exp underflow region where
+//       probabilities tie -- and the CTA simply waits for the exact routing instead.)
+//   CH  exact routing, concurrently.  Two dedicated warps per CTA run the order-faithful logit
+//       chains (the D dependent float adds of the reference, ~6 cycles each) while the gate/up
+//       stream runs; the last chain to finish a token block runs route() (proj/src/router.cpp:
+//       13-68) for it.  Expert ids, slot order and weights are therefore the reference's bit for
+//       bit, and their latency (5-10 us) is hidden behind P1.
+//   P1  gate/up + SwiGLU for the union of candidate experts: work item = (expert, 64 neurons);
+//       tcgen05.mma 128x16x16 (gate and up rows interleaved on M, the <=16 tokens on N),
+//       TMEM accumulators double-buffered, weights streamed once by TMA through a 9-stage ring
+//       (~160 KB in flight per SM).  The epilogue stores h and, in top-k mode, adds each value
+//       to a 512-bin histogram of its row (bins = exponent + 3 mantissa bits of |h|).
+//   P2  neuron selection + down projection.  Work unit = (token, slot, row chunk).  The unit
+//       loads its h row, locates the pivot bucket from the histogram, ranks only the bucket's
+//       members (bit-exact mask_smallest_magnitudes, proj/src/activation.cpp:31-52, including the
+//       lower-index-first tie rule), takes its share of the survivors in ascending index order
+//       and streams exactly those W_down rows (coalesced 128-bit loads, fp32 accumulation in
+//       registers).  Dropped neurons cost no HBM bytes.
+//   P3  combine: y[t] = sum_s w(t,s) * (sum_chunks partial), slots ascending, shared expert
+//       last with weight 1 (proj/src/router.cpp:109-132, engine.cpp:168-173), fixed order.
+//
+// No float atomics anywhere: results are deterministic and, for a given (shape, batch), do not
+// depend on timing.
+#include "route_device.cuh"
+#include "select_device.cuh"
+#include "tc_ptx.cuh"
+
+namespace skb {
+
+namespace {
+
+constexpr int kDecThreads = 256;
+constexpr int kDecTokens = 16;                     // MMA N
+constexpr int kDecATile = 128 * kBlockK * 2;       // 16 KB
+constexpr int kDecBTile = kDecTokens * kBlockK * 2;  // 2 KB
+constexpr int kDecStageBytes = kDecATile + kDecBTile;
+constexpr int kDecStages = 9;
+constexpr int kDecWork = kDecStages * kDecStageBytes;  // 165888 B, reused by P0 / P2 scratch
+constexpr int kHistBins = 512;
+constexpr int kHistBase = (135 << 3) - (kHistBins - 1);  // top bin = |h| >= 2^8
+constexpr int kMemberCap = 1024;
+constexpr int kMaxKpt = 32;  // keys per thread: N, S <= 8192
+
+// exact-chain ring (per CTA): 8 experts + 4 tokens per unit, 256-float sub-chunks
+constexpr int kChEB = 8, kChTB = 4, kChSub = 256, kChStages = 3;
+constexpr int kChRow = kChSub + 4;
+constexpr int kChRows = kChEB + kChTB;
+constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 37440
+
+constexpr int kDecMaxE = 256;
+constexpr int kDecMaxU = 256;  // union of candidate experts
+
+// counters (unsigned words)
+enum { kCtrP0 = 0, kCtrExit = 1, kCtrRoute = 2, kCtrP2 = 3, kCtrChain = 4 /*[4]*/, kCtrH = 8 };
+
+struct DecSmem {
+  // offsets from the 1024-aligned base
+  static constexpr int work = 0;
+  static constexpr int chain = kDecWork;
+  static constexpr int rowtab = chain + kChBytes;                  // int16 [kDecMaxU + 1][16]
+  static constexpr int uidx = rowtab + (kDecMaxU + 1) * 16 * 2;    // int16 [kDecMaxE]
+  static constexpr int ulist = uidx + kDecMaxE * 2;                // int16 [kDecMaxU]
+  static constexpr int cmask = ulist + kDecMaxU * 2;               // uint32 [kDecMaxE]
+  static constexpr int rscr = cmask + kDecMaxE * 4;                // float [E + K + 8] route() scratch
+  static constexpr int bars = rscr + 1152;                         // 8-byte aligned
+  static constexpr int n_bars = 2 * kDecStages + 4 + 2 * kChStages;
+  static constexpr int misc = bars + n_bars * 8;                   // ints
+  static constexpr int total = misc + 64 * 4;
+};
+static_assert(DecSmem::bars % 8 == 0, "barrier alignment");
+constexpr int kDecSmemBytes = DecSmem::total + 1024;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const unsigned* p, unsigned target) {
+  while (ld_acquire_u32(p) < target) __nanosleep(32);
+}
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int hist_bin(uint32_t key) {
+  const int b = static_cast<int>(key >> 20) - kHistBase;
+  return b < 0 ? 0 : (b > kHistBins - 1 ? kHistBins - 1 : b);
+}
+__device__ __forceinline__ void fma8(const uint4& u, float hk, float* a) {
+  a[0] = fmaf(__uint_as_float(u.x << 16), hk, a[0]);
+  a[1] = fmaf(__uint_as_float(u.x & 0xffff0000u), hk, a[1]);
+  a[2] = fmaf(__uint_as_float(u.y << 16), hk, a[2]);
+  a[3] = fmaf(__uint_as_float(u.y & 0xffff0000u), hk, a[3]);
+  a[4] = fmaf(__uint_as_float(u.z << 16), hk, a[4]);
+  a[5] = fmaf(__uint_as_float(u.z & 0xffff0000u), hk, a[5]);
+  a[6] = fmaf(__uint_as_float(u.w << 16), hk, a[6]);
+  a[7] = fmaf(__uint_as_float(u.w & 0xffff0000u), hk, a[7]);
+}
+
+}  // namespace
+
+#ifdef SKB_DEBUG_TIMING
+__device__ long long g_dec_dbg[160 * 16];
+#define DEC_T(i) do { if (threadIdx.x == 0) g_dec_dbg[blockIdx.x * 16 + (i)] = clock64(); } while (0)
+#define DEC_TW(w, i) do { if (threadIdx.x == (w) * 32) g_dec_dbg[blockIdx.x * 16 + (i)] = clock64(); } while (0)
+extern "C" void skb_debug_dec(long long* out) { cudaMemcpyFromSymbol(out, g_dec_dbg, sizeof(g_dec_dbg)); }
+#else
+#define DEC_T(i) do { } while (0)
+#define DEC_TW(w, i) do { } while (0)
+#endif
+
+// Column tiles of 2048 (256 threads x 8 columns) per W_down row: NT = ceil(Dp / 2048).
+template <int NT>
+__device__ __forceinline__ void gather_rows(const __nv_bfloat16* __restrict__ wb, int Dp, int m,
+                                            const int32_t* lst_idx, const float* lst_val, int G,
+                                            int g, int l, bool lane_ok, float (&acc)[NT][8]) {
+  constexpr int U = NT == 1 ? 16 : (NT == 2 ? 8 : 4);
+  const int LPR = Dp >> 3;
+#pragma unroll 1
+  for (int p0 = g; p0 < m; p0 += G * U) {
+    uint4 v[U][NT];
+    float hv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * G;
+      const bool ok = p < m && lane_ok;
+      hv[u] = ok ? lst_val[p] : 0.0f;
+      const __nv_bfloat16* row = wb + static_cast<size_t>(ok ? lst_idx[p] : 0) * Dp;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c8 = nt * 256 + l;
+        if (ok && c8 < LPR)
+          v[u][nt] = ldg_nc_v4(row + c8 * 8);
+        else
+          v[u][nt] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) fma8(v[u][nt], hv[u], acc[nt]);
+  }
+}
+
+struct DecodeArgs {
+  const float* x;
+  const float* router;
+  const __nv_bfloat16* wd;
+  const __nv_bfloat16* wd_shared;
+  int B, E, K, D, Dp, N, Np, S, Sp, Nh, has_shared, renorm;
+  int sel_mode, n_off_r, n_off_s;
+  const uint8_t* mask_r;
+  const uint8_t* mask_s;
+  int CM, CH, capture;
+  __nv_bfloat16* xb;
+  float* lf;
+  float* lm;
+  float* logits;
+  int32_t* ids;
+  float* wts;
+  float* hc;
+  uint32_t* hist;
+  float* part;
+  unsigned* ctr;
+  float* y;
+  float* h_cap;
+  int32_t* inv;
+  int32_t* perm;
+  int32_t* row_expert;
+};
+
+__global__ void __launch_bounds__(kDecThreads, 1)
+decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                    const __grid_constant__ CUtensorMap tmap_xb, const DecodeArgs a) {
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
+  const uint32_t sm_u32 = smem_u32(sm);
+  uint8_t* work = sm + DecSmem::work;
+  int16_t* rowtab = reinterpret_cast<int16_t*>(sm + DecSmem::rowtab);
+  int16_t* uidx = reinterpret_cast<int16_t*>(sm + DecSmem::uidx);
+  int16_t* ulist = reinterpret_cast<int16_t*>(sm + DecSmem::ulist);
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(sm + DecSmem::cmask);
+  int* misc = reinterpret_cast<int*>(sm + DecSmem::misc);
+  const uint32_t bar0 = sm_u32 + DecSmem::bars;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kDecStages + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * kDecStages + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * kDecStages + 2 + b); };
+  auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + s); };
+  auto cempty_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + kChStages + s); };
+  // misc ints: 0 tmem ptr, 1 overflow flag, 2 n_u, 3.. P2 scalars
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grid = gridDim.x, bid = blockIdx.x;
+  const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp;
+  const int R = K + (a.has_shared ? 1 : 0);
+  const int n_tb = ceil_div(B, kChTB), n_eb = ceil_div(E, kChEB);
+
+  DEC_T(0);
+  // ---- prologue ----
+  if (tid == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_xb);
+    for (int s = 0; s < kDecStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 4);
+    }
+    for (int s = 0; s < kChStages; ++s) {
+      mbar_init(cfull_bar(s), 1);
+      mbar_init(cempty_bar(s), 1);
+    }
+    fence_barrier_init();
+    misc[1] = 0;
+  }
+  if (warp == 1) tmem_alloc(sm_u32 + DecSmem::misc, 32);
+  for (int e = tid; e < kDecMaxE; e += kDecThreads) cmask[e] = 0u;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(misc);
+
+  // =====================================================================================
+  // P0: histogram zeroing, bf16 token rows, fast logits with error bounds
+  // =====================================================================================
+  const int hist_on = (a.sel_mode == kSelectTopk) ? 1 : 0;
+  if (hist_on) {
+    // rows [0, B*CM) routed candidates, rows [16*CM, 16*CM + B) shared expert
+    uint4* h4 = reinterpret_cast<uint4*>(a.hist);
+    const int per_row = kHistBins / 4;
+    const int n1 = B * a.CM * per_row;
+    const int n2 = a.has_shared ? B * per_row : 0;
+    for (int i = bid * kDecThreads + tid; i < n1 + n2; i += grid * kDecThreads) {
+      const int j = i < n1 ? i : (kDecTokens * a.CM * per_row + (i - n1));
+      h4[j] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  // token t is converted by CTA grid-1-t (the low CTAs carry the logit units)
+  for (int t = grid - 1 - bid; t < B; t += grid) {
+    const float* src = a.x + static_cast<size_t>(t) * D;
+    __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
+    for (int d = tid; d < D; d += kDecThreads) dst[d] = __float2bfloat16_rn(__ldg(src + d));
+  }
+  {
+    float* red = reinterpret_cast<float*>(work);  // [8 warps][16 tokens][2]
+    const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
+    // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
+    const double u24 = 5.9604644775390625e-8;
+    const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
+    for (int e = bid; e < E; e += grid) {
+      float pl[kDecTokens], pa[kDecTokens];
+#pragma unroll
+      for (int t = 0; t < kDecTokens; ++t) pl[t] = pa[t] = 0.0f;
+      const float* wr = a.router + static_cast<size_t>(e) * D;
+      if (vec_ok) {
+        const float4* w4 = reinterpret_cast<const float4*>(wr);
+        for (int q = tid; q < D / 4; q += kDecThreads) {
+          const float4 w = __ldg(w4 + q);
+#pragma unroll
+          for (int t = 0; t < kDecTokens; ++t) {
+            if (t < B) {
+              const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t) * D) + q);
+              pl[t] = fmaf(w.x, xv.x, pl[t]);
+              pl[t] = fmaf(w.y, xv.y, pl[t]);
+              pl[t] = fmaf(w.z, xv.z, pl[t]);
+              pl[t] = fmaf(w.w, xv.w, pl[t]);
+              pa[t] = fmaf(fabsf(w.x), fabsf(xv.x), pa[t]);
+              pa[t] = fmaf(fabsf(w.y), fabsf(xv.y), pa[t]);
+              pa[t] = fmaf(fabsf(w.z), fabsf(xv.z), pa[t]);
+              pa[t] = fmaf(fabsf(w.w), fabsf(xv.w), pa[t]);
+            }
+          }
+        }
+      } else {
+        for (int d = tid; d < D; d += kDecThreads) {
+          const float w = __ldg(wr + d);
+#pragma unroll
+          for (int t = 0; t < kDecTokens; ++t) {
+            if (t < B) {
+              const float xv = __ldg(a.x + static_cast<size_t>(t) * D + d);
+              pl[t] = fmaf(w, xv, pl[t]);
+              pa[t] = fmaf(fabsf(w), fabsf(xv), pa[t]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kDecTokens; ++t) {
+        if (t < B) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            pl[t] += __shfl_xor_sync(0xffffffffu, pl[t], o);
+            pa[t] += __shfl_xor_sync(0xffffffffu, pa[t], o);
+          }
+          if (lane == 0) {
+            red[(warp * kDecTokens + t) * 2 + 0] = pl[t];
+            red[(warp * kDecTokens + t) * 2 + 1] = pa[t];
+          }
+        }
+      }
+      __syncthreads();
+      if (tid < B) {
+        float s = 0.0f, sa = 0.0f;
+        for (int w = 0; w < kDecThreads / 32; ++w) {
+          s += red[(w * kDecTokens + tid) * 2 + 0];
+          sa += red[(w * kDecTokens + tid) * 2 + 1];
+        }
+        a.lf[static_cast<size_t>(tid) * E + e] = s;
+        a.lm[static_cast<size_t>(tid) * E + e] = sa * mfac + 2e-5f;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    fence_proxy_async_all();
+    atomicAdd(&a.ctr[kCtrP0], 1u);
+  }
+  DEC_T(1);
+
+  // =====================================================================================
+  // Exact routing chains: warps 6 (consumer) and 7 (producer) -- independent of everything
+  // below until P2.  They start before the P0 barrier: they only read x and the router.
+  // =====================================================================================
+  if (warp >= 6) {
+    float* ring = reinterpret_cast<float*>(sm + DecSmem::chain);
+    const int n_cu = n_eb * n_tb;
+    const int nsub = ceil_div(D, kChSub);
+    const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
+    int gsc = 0;  // ring position, continues across units
+    for (int cu = bid; cu < n_cu; cu += grid) {
+      const int eb = cu % n_eb, tb = cu / n_eb;
+      const int e0 = eb * kChEB, t0 = tb * kChTB;
+      const int n_e = min(kChEB, E - e0), n_t = min(kChTB, B - t0);
+      if (warp == 7) {
+        const float* wsrc = a.router + static_cast<size_t>(e0) * D;
+        const float* xsrc = a.x + static_cast<size_t>(t0) * D;
+        int psc = gsc;
+        if (vec_ok) {
+          if (lane == 0) {
+#pragma unroll 1
+            for (int sc = 0; sc < nsub; ++sc, ++psc) {
+              const int slot = psc % kChStages;
+              mbar_wait(cempty_bar(slot), ((psc / kChStages) & 1u) ^ 1u);
+              const int d0 = sc * kChSub;
+              const uint32_t bytes = static_cast<uint32_t>(min(kChSub, D - d0)) * 4u;
+              mbar_arrive_expect_tx(cfull_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
+              const uint32_t dst = smem_u32(ring + slot * kChRows * kChRow);
+#pragma unroll 1
+              for (int r = 0; r < n_e; ++r)
+                bulk_copy_g2s(dst + r * kChRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
+                              cfull_bar(slot));
+#pragma unroll 1
+              for (int r = 0; r < n_t; ++r)
+                bulk_copy_g2s(dst + (kChEB + r) * kChRow * 4, xsrc + static_cast<size_t>(r) * D + d0,
+                              bytes, cfull_bar(slot));
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int sc = 0; sc < nsub; ++sc, ++psc) {
+            const int slot = psc % kChStages;
+            mbar_wait(cempty_bar(slot), ((psc / kChStages) & 1u) ^ 1u);
+            const int d0 = sc * kChSub;
+            const int n = min(kChSub, D - d0);
+            float* dst = ring + slot * kChRows * kChRow;
+#pragma unroll 1
+            for (int r = 0; r < n_e + n_t; ++r) {
+              const float* src = (r < n_e) ? wsrc + static_cast<size_t>(r) * D + d0
+                                           : xsrc + static_cast<size_t>(r - n_e) * D + d0;
+              float* drow = dst + ((r < n_e) ? r : kChEB + r - n_e) * kChRow;
+#pragma unroll 1
+              for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(cfull_bar(slot));
+          }
+        }
+      } else {
+        const int e_i = lane / kChTB, t_j = lane % kChTB;
+        const bool valid = (e_i < n_e) && (t_j < n_t);
+        float acc = 0.0f;
+        int csc = gsc;
+#pragma unroll 1
+        for (int sc = 0; sc < nsub; ++sc, ++csc) {
+          const int slot = csc % kChStages;
+          mbar_wait(cfull_bar(slot), (csc / kChStages) & 1u);
+          const float* base = ring + slot * kChRows * kChRow;
+          const float* wr = base + e_i * kChRow;
+          const float* xr = base + (kChEB + t_j) * kChRow;
+          const int n = min(kChSub, D - sc * kChSub);
+          const int n4 = n >> 2;
+#pragma unroll 8
+          for (int q = 0; q < n4; ++q) {
+            const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
+            const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
+            acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
+            acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
+            acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
+            acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
+          }
+#pragma unroll 1
+          for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(cempty_bar(slot));
+        }
+        if (valid) a.logits[static_cast<size_t>(t0 + t_j) * E + e0 + e_i] = acc;
+        __threadfence();
+        __syncwarp();
+        unsigned prev = 0;
+        if (lane == 0) prev = atomicAdd(&a.ctr[kCtrChain + tb], 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == static_cast<unsigned>(n_eb - 1)) {
+          // last chain of this token block: route() for its tokens
+          __threadfence();
+          float* scr = reinterpret_cast<float*>(sm + DecSmem::rscr);
+          for (int tt = 0; tt < n_t; ++tt) {
+            const int t = t0 + tt;
+            warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, scr,
+                             a.ids + static_cast<size_t>(t) * K, a.wts + static_cast<size_t>(t) * K);
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(&a.ctr[kCtrRoute], 1u);
+        }
+      }
+      gsc += nsub;
+    }
+    DEC_TW(6, 10);
+  }
+
+  // =====================================================================================
+  // P0 barrier, candidates (every CTA computes the same tables)
+  // =====================================================================================
+  if (warp < 6) {
+    if (tid == 0) {
+      spin_until(&a.ctr[kCtrP0], static_cast<unsigned>(grid));
+      fence_proxy_async_all();
+    }
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    DEC_T(2);
+    float* slf = reinterpret_cast<float*>(work + 2048);  // [B][E]
+    float* slm = slf + B * E;
+    for (int i = tid; i < B * E; i += 192) {
+      slf[i] = __ldcg(a.lf + i);
+      slm[i] = __ldcg(a.lm + i);
+    }
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    constexpr int kVpl = kDecMaxE / 32;
+    for (int t = warp; t < B; t += 6) {
+      float lo[kVpl], hi[kVpl];
+      bool bad = false;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kVpl; ++i) {
+        const int e = i * 32 + lane;
+        if (e < E) {
+          const float f = slf[t * E + e], m = slm[t * E + e];
+          lo[i] = f - m;
+          hi[i] = f + m;
+          mx = fmaxf(mx, f);
+          bad |= !(fabsf(f) < 1e30f) || !(m < 1e30f);
+        } else {
+          lo[i] = -INFINITY;
+          hi[i] = -INFINITY;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      // K-th largest lower end: K rounds of warp arg-max, removing one instance per round
+      float thr = -INFINITY;
+      for (int s = 0; s < K; ++s) {
+        float bv = -INFINITY;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < kVpl; ++i)
+          if (lo[i] > bv) {
+            bv = lo[i];
+            bi = i * 32 + lane;
+          }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        thr = bv;
+#pragma unroll
+        for (int i = 0; i < kVpl; ++i)
+          if (i * 32 + lane == bi) lo[i] = -INFINITY;
+      }
+      int cnt = 0;
+      unsigned mine = 0;
+#pragma unroll
+      for (int i = 0; i < kVpl; ++i) {
+        const bool c = hi[i] >= thr && (i * 32 + lane) < E;
+        cnt += __popc(__ballot_sync(0xffffffffu, c));
+        if (c) mine |= 1u << i;
+      }
+      bad = __any_sync(0xffffffffu, bad) || !(thr > -1e30f) || (thr < mx - 60.0f) || cnt > a.CM ||
+            cnt < K;
+      if (bad) {
+        if (lane == 0) misc[1] = 1;
+      } else {
+#pragma unroll
+        for (int i = 0; i < kVpl; ++i)
+          if (mine & (1u << i)) atomicOr(&cmask[i * 32 + lane], 1u << t);
+      }
+    }
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    if (misc[1] != 0) {
+      // rare: the bound could not separate the candidates -- wait for the exact routing
+      if (tid == 0) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+      for (int e = tid; e < E; e += 192) cmask[e] = 0u;
+      asm volatile("bar.sync 2, 192;" ::: "memory");
+      for (int i = tid; i < B * K; i += 192) atomicOr(&cmask[__ldcg(a.ids + i)], 1u << (i / K));
+      asm volatile("bar.sync 2, 192;" ::: "memory");
+    }
+    // union list (ascending expert id) by warp 0, row table by all
+    if (warp == 0) {
+      int run = 0;
+      for (int base = 0; base < E; base += 32) {
+        const int e = base + lane;
+        const bool f = e < E && cmask[e] != 0u;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        const int pos = run + __popc(b & ((1u << lane) - 1u));
+        if (e < E) uidx[e] = f ? static_cast<int16_t>(pos) : static_cast<int16_t>(-1);
+        if (f) ulist[pos] = static_cast<int16_t>(e);
+        run += __popc(b);
+      }
+      if (lane == 0) misc[2] = run;
+    }
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    const int n_u0 = misc[2];
+    for (int i = tid; i < (n_u0 + 1) * 16; i += 192) rowtab[i] = -1;
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    for (int t = warp; t < B; t += 6) {
+      int run = 0;
+      for (int base = 0; base < E; base += 32) {
+        const int e = base + lane;
+        const bool f = e < E && ((cmask[e] >> t) & 1u);
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        if (f) rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * a.CM + run + __popc(b & ((1u << lane) - 1u)));
+        run += __popc(b);
+      }
+      if (a.has_shared && lane == 0) rowtab[n_u0 * 16 + t] = static_cast<int16_t>(kDecTokens * a.CM + t);
+    }
+    asm volatile("bar.sync 2, 192;" ::: "memory");
+    DEC_T(3);
+
+    // ===================================================================================
+    // P1: gate/up + SwiGLU over (union expert, 64-neuron block) items
+    // ===================================================================================
+    const int n_u = n_u0;
+    const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
+    const int n_items = n_u * NB + NBs;
+    const int KB = Dp / kBlockK;
+    if (warp == 0) {
+      if (lane == 0) {
+        int gk = 0;
+        for (int it = bid; it < n_items; it += grid) {
+          const bool sh = it >= n_u * NB;
+          const int u = sh ? n_u : it / NB;
+          const int nb = sh ? it - n_u * NB : it % NB;
+          const int e = sh ? E : ulist[u];
+          const int a_row = e * 2 * a.Np + nb * 128;
+          for (int kb = 0; kb < KB; ++kb, ++gk) {
+            const int s = gk % kDecStages;
+            mbar_wait(empty_bar(s), ((gk / kDecStages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(full_bar(s), kDecStageBytes);
+            const uint32_t dst = sm_u32 + s * kDecStageBytes;
+            tma_load_2d(dst, &tmap_w, 0, ((a_row >> 7) * KB + kb) * 128, full_bar(s),
+                        kPolicyEvictFirst);
+            tma_load_2d(dst + kDecATile, &tmap_xb, kb * kBlockK, 0, full_bar(s), kPolicyEvictLast);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        constexpr uint32_t kIdesc = make_idesc_bf16(128, kDecTokens);
+        int gk = 0, li = 0;
+        for (int it = bid; it < n_items; it += grid, ++li) {
+          const int buf = li & 1;
+          mbar_wait(tempty_bar(buf), (((li >> 1) & 1u) ^ 1u));
+          tc_fence_after();
+          for (int kb = 0; kb < KB; ++kb, ++gk) {
+            const int s = gk % kDecStages;
+            mbar_wait(full_bar(s), (gk / kDecStages) & 1u);
+            tc_fence_after();
+            const uint32_t a_smem = sm_u32 + s * kDecStageBytes;
+            const uint64_t a_desc = make_smem_desc_sw128(a_smem);
+            const uint64_t b_desc = make_smem_desc_sw128(a_smem + kDecATile);
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k)
+              umma_bf16(tmem_base + buf * kDecTokens, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
+                        (kb | k) != 0 ? 1u : 0u);
+            umma_commit(empty_bar(s));
+          }
+          umma_commit(tfull_bar(buf));
+        }
+      }
+    } else {
+      const int q = warp & 3;
+      const bool is_gate_lane = lane < 16;
+      int li = 0;
+      for (int it = bid; it < n_items; it += grid, ++li) {
+        const bool sh = it >= n_u * NB;
+        const int u = sh ? n_u : it / NB;
+        const int nb = sh ? it - n_u * NB : it % NB;
+        const int m_valid = sh ? a.S : a.N;
+        const int buf = li & 1;
+        mbar_wait(tfull_bar(buf), (li >> 1) & 1u);
+        tc_fence_after();
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + buf * kDecTokens, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(buf));
+        const int n = nb * kNeuronBlock + 16 * q + (lane & 15);
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          if (c < B) {
+            const float mine0 = __uint_as_float(v[c]);
+            const float mine1 = __uint_as_float(v[c + 1]);
+            const float send = is_gate_lane ? mine1 : mine0;
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+            const float g = is_gate_lane ? mine0 : recv;
+            const float up = is_gate_lane ? recv : mine1;
+            const int col = c + (is_gate_lane ? 0 : 1);
+            if (col < B && n < m_valid) {
+              const int r = rowtab[u * 16 + col];
+              if (r >= 0) {
+                const float hval = silu_f(g) * up;
+                a.hc[static_cast<size_t>(r) * a.Nh + n] = hval;
+                if (hist_on)
+                  atomicAdd(&a.hist[static_cast<size_t>(r) * kHistBins +
+                                    hist_bin(__float_as_uint(hval) & 0x7fffffffu)],
+                            1u);
+              }
+            }
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          atomicAdd(&a.ctr[kCtrH + u], 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  DEC_T(4);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 32);
+  }
+
+  // =====================================================================================
+  // P2: selection + down projection over (token, slot, row chunk) units.  Units are dealt in
+  // contiguous ranges, chunk index fastest, so a CTA that holds several chunks of one (token,
+  // slot) selects once.  The chunking depends on the shape only -- not on the batch -- so the
+  // reduction tree of a token does not depend on what else is in the batch.
+  // =====================================================================================
+  {
+    const int n_u = misc[2];
+    const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
+    const int CH = a.CH;
+    const int n_units = B * R * CH;
+    // scratch (the GEMM stages are idle now)
+    int32_t* lst_idx = reinterpret_cast<int32_t*>(work);           // [8192]
+    float* lst_val = reinterpret_cast<float*>(work + 32768);       // [8192]
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(work + 65536);  // [8192] (fallback search)
+    uint32_t* mlist = reinterpret_cast<uint32_t*>(work + 98304);   // [kMemberCap + 4]
+    int* wc = reinterpret_cast<int*>(work + 98304 + 4352);         // [kMaxKpt * 8] + [8]
+    float* gred = reinterpret_cast<float*>(work + 106496);         // [G][Dp] <= 8 KB (NT == 1)
+    __shared__ SelScratch sel_sc;
+    int* p2 = misc + 8;  // 0 row, 1 e, 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount, 9 total
+    bool route_ready = false;
+    const int LPR = Dp >> 3;
+    const int NT = ceil_div(LPR, 256);
+    const int G = NT == 1 ? (256 / LPR > 0 ? 256 / LPR : 1) : 1;
+    const int v0 = static_cast<int>(static_cast<long long>(bid) * n_units / grid);
+    const int v1 = static_cast<int>(static_cast<long long>(bid + 1) * n_units / grid);
+
+    int cur_tj = -1;
+    int row = 0, e = 0, n = 0, kpt = 0, cnt = 0;
+    bool routed = true;
+    unsigned flags = 0;       // keep flag of key jj of this thread
+    uint32_t hb[kMaxKpt];     // raw bits of this thread's h values: element jj * 256 + tid
+
+    for (int v = v0; v < v1; ++v) {
+      const int c = v % CH;
+      const int tj = v / CH;
+      const int j = tj % R;
+      const int t = tj / R;
+      if (tj != cur_tj) {
+        cur_tj = tj;
+        routed = j < K;
+        if (tid == 0) {
+          if (!route_ready) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+          int ee, u, rr;
+          if (routed) {
+            ee = __ldcg(a.ids + t * K + j);
+            u = uidx[ee];
+            if (u < 0) asm volatile("trap;");  // the candidate bound is a theorem: never taken
+            rr = rowtab[u * 16 + t];
+            spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NB));
+          } else {
+            ee = E;
+            u = n_u;
+            rr = kDecTokens * a.CM + t;
+            spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NBs));
+          }
+          p2[0] = rr;
+          p2[1] = ee;
+          p2[8] = 0;
+        }
+        route_ready = true;
+        __syncthreads();
+        row = p2[0];
+        e = p2[1];
+        n = routed ? a.N : a.S;
+        const int slot = routed ? t * K + j : t;
+        int mode = a.sel_mode;
+        const uint8_t* min_ = nullptr;
+        if (mode == kSelectGiven) {
+          min_ = routed ? a.mask_r + static_cast<size_t>(slot) * n
+                        : (a.mask_s ? a.mask_s + static_cast<size_t>(slot) * n : nullptr);
+          if (min_ == nullptr) mode = kSelectAll;
+        }
+        int n_off = 0;
+        if (mode == kSelectTopk) {
+          n_off = routed ? a.n_off_r : a.n_off_s;
+          if (n_off <= 0) mode = kSelectAll;
+        }
+        kpt = ceil_div(n, kDecThreads);
+        const float* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
+#pragma unroll
+        for (int jj = 0; jj < kMaxKpt; ++jj) {
+          if (jj < kpt) {
+            const int i = jj * kDecThreads + tid;
+            hb[jj] = i < n ? __float_as_uint(__ldcg(hrow + i)) : 0u;
+          }
+        }
+        if (a.capture) {
+          float* dst = a.h_cap + static_cast<size_t>(routed ? slot : B * K + t) * a.Nh;
+#pragma unroll
+          for (int jj = 0; jj < kMaxKpt; ++jj)
+            if (jj < kpt && jj * kDecThreads + tid < n)
+              dst[jj * kDecThreads + tid] = __uint_as_float(hb[jj]);
+          if (tid == 0) {
+            if (routed) {
+              a.inv[slot] = slot;
+              a.perm[slot] = slot;
+              a.row_expert[slot] = e;
+            } else {
+              a.row_expert[B * K + t] = E;
+            }
+          }
+        }
+
+        RowPick pk{0u, 0, true};
+        if (mode == kSelectAll) {
+          cnt = n;
+        } else if (mode == kSelectGiven) {
+          cnt = 0;  // counted by the prefix below
+        } else {
+          cnt = n_off >= n ? 0 : n - n_off;
+          if (cnt > 0) {
+            // ---- pivot bucket from the row's histogram ----
+            const uint2 hh = __ldcg(
+                reinterpret_cast<const uint2*>(a.hist + static_cast<size_t>(row) * kHistBins) + tid);
+            int incl = static_cast<int>(hh.x + hh.y);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int up = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += up;
+            }
+            if (lane == 31) wc[warp] = incl;
+            __syncthreads();
+            int base = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+              if (w < warp) base += wc[w];
+            incl += base;
+            const int excl = incl - static_cast<int>(hh.x + hh.y);
+            if (excl < n_off && n_off <= incl) {
+              const bool first = n_off <= excl + static_cast<int>(hh.x);
+              p2[2] = 2 * tid + (first ? 0 : 1);
+              p2[3] = first ? excl : excl + static_cast<int>(hh.x);
+              p2[4] = first ? static_cast<int>(hh.x) : static_cast<int>(hh.y);
+            }
+            __syncthreads();
+            const int bstar = p2[2], below_bins = p2[3], M = p2[4];
+            if (M <= kMemberCap) {
+              for (int i = tid; i < kMemberCap + 4; i += kDecThreads) mlist[i] = 0xffffffffu;
+              __syncthreads();
+#pragma unroll
+              for (int jj = 0; jj < kMaxKpt; ++jj) {
+                if (jj < kpt && jj * kDecThreads + tid < n) {
+                  const uint32_t k = hb[jj] & 0x7fffffffu;
+                  if (hist_bin(k) == bstar) mlist[atomicAdd(&p2[8], 1)] = k;
+                }
+              }
+              __syncthreads();
+              const int rr = n_off - below_bins;  // 1-based rank inside the bucket
+              const int M4 = (M + 3) >> 2;
+#pragma unroll
+              for (int jj = 0; jj < kMaxKpt; ++jj) {
+                if (jj < kpt && jj * kDecThreads + tid < n) {
+                  const uint32_t k = hb[jj] & 0x7fffffffu;
+                  if (hist_bin(k) == bstar) {
+                    int lt = 0, le = 0;
+                    for (int q4 = 0; q4 < M4; ++q4) {
+                      const uint4 mm = *reinterpret_cast<const uint4*>(mlist + 4 * q4);
+                      lt += (mm.x < k) + (mm.y < k) + (mm.z < k) + (mm.w < k);
+                      le += (mm.x <= k) + (mm.y <= k) + (mm.z <= k) + (mm.w <= k);
+                    }
+                    if (lt < rr && rr <= le) {
+                      p2[5] = static_cast<int>(k);
+                      p2[6] = below_bins + lt;
+                      p2[7] = le - lt;
+                    }
+                  }
+                }
+              }
+              __syncthreads();
+              pk.pivot = static_cast<uint32_t>(p2[5]);
+              pk.ties_to_drop = n_off - p2[6];
+              pk.drop_all_ties = (pk.ties_to_drop == p2[7]);
+            } else {
+              // huge bucket (many equal / clamped values): the general search
+#pragma unroll
+              for (int jj = 0; jj < kMaxKpt; ++jj)
+                if (jj < kpt && jj * kDecThreads + tid < n)
+                  keys_s[jj * kDecThreads + tid] = hb[jj] & 0x7fffffffu;
+              __syncthreads();
+              pk = sel_kary_pick(keys_s, n, n_off, sel_sc);
+            }
+          }
+        }
+
+        // ---- keep flags and their exclusive prefix in index order (wc[jj * 8 + warp]) ----
+        flags = 0;
+        if (mode != kSelectTopk || cnt > 0) {
+          const bool need_ties = (mode == kSelectTopk) && !pk.drop_all_ties;
+          unsigned keepbits = 0;
+          for (int pass = need_ties ? 0 : 1; pass < 2; ++pass) {
+            // pass 0: prefix over tie flags (only when some but not all ties are dropped);
+            // pass 1: prefix over keep flags
+            unsigned fl = 0;
+#pragma unroll
+            for (int jj = 0; jj < kMaxKpt; ++jj) {
+              if (jj < kpt) {
+                const int i = jj * kDecThreads + tid;
+                const bool valid = i < n;
+                const uint32_t k = hb[jj] & 0x7fffffffu;
+                bool f;
+                if (pass == 0) {
+                  f = valid && k == pk.pivot;
+                } else if (mode == kSelectAll) {
+                  f = valid;
+                } else if (mode == kSelectGiven) {
+                  f = valid && min_[i] != 0;
+                } else if (pk.drop_all_ties) {
+                  f = valid && k > pk.pivot;
+                } else {
+                  f = valid && (k > pk.pivot || ((keepbits >> jj) & 1u));
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                if (lane == 0) wc[jj * 8 + warp] = __popc(bal);
+                if (f) fl |= 1u << jj;
+              }
+            }
+            __syncthreads();
+            {
+              // exclusive scan of wc[0 .. kpt*8) in (jj, warp) order: one entry per thread
+              const int ne = kpt * 8;
+              const int val = tid < ne ? wc[tid] : 0;
+              int incl = val;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int up = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += up;
+              }
+              if (lane == 31) wc[kMaxKpt * 8 + warp] = incl;
+              __syncthreads();
+              int base = 0;
+#pragma unroll
+              for (int w = 0; w < 8; ++w)
+                if (w < warp) base += wc[kMaxKpt * 8 + w];
+              if (tid < ne) wc[tid] = base + incl - val;
+              if (tid == kDecThreads - 1) p2[9] = base + incl;  // total
+              __syncthreads();
+            }
+            if (pass == 0) {
+#pragma unroll
+              for (int jj = 0; jj < kMaxKpt; ++jj) {
+                if (jj < kpt) {
+                  const bool f = (fl >> jj) & 1u;
+                  const unsigned bal = __ballot_sync(0xffffffffu, f);
+                  const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
+                  if (f && rank >= pk.ties_to_drop) keepbits |= 1u << jj;
+                }
+              }
+              __syncthreads();
+            } else {
+              flags = fl;
+              if (mode == kSelectGiven) cnt = p2[9];
+            }
+          }
+        }
+      }
+
+      // ---- survivors [lo, hi) of this chunk, ascending index ----
+      const int C = ceil_div(cnt > 0 ? cnt : 1, CH);
+      const int lo = c * C;
+      const int hi_ = min(cnt, lo + C);
+      const int m = hi_ > lo ? hi_ - lo : 0;
+      if (m > 0) {
+#pragma unroll
+        for (int jj = 0; jj < kMaxKpt; ++jj) {
+          if (jj < kpt) {
+            const bool f = (flags >> jj) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
+            if (f && rank >= lo && rank < hi_) {
+              lst_idx[rank - lo] = jj * kDecThreads + tid;
+              lst_val[rank - lo] = __uint_as_float(hb[jj]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- gather this chunk's W_down rows ----
+      const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
+      float* pout = a.part + (static_cast<size_t>(t * R + j) * CH + c) * Dp;
+      if (NT == 1) {
+        const int g = tid / LPR, l = tid % LPR;
+        const bool lane_ok = g < G;
+        float acc[1][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[0][i] = 0.0f;
+        gather_rows<1>(wb, Dp, m, lst_idx, lst_val, G, g, l, lane_ok, acc);
+        if (G > 1) {
+          if (lane_ok) {
+            float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
+            d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+            d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+          }
+          __syncthreads();
+          for (int d = tid; d < Dp; d += kDecThreads) {
+            float s = gred[d];
+            for (int gg = 1; gg < G; ++gg) s = __fadd_rn(s, gred[gg * Dp + d]);
+            pout[d] = s;
+          }
+        } else if (lane_ok) {
+          float4* d4 = reinterpret_cast<float4*>(pout + l * 8);
+          d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+          d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+        }
+      } else {
+        float acc[4][8];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
+        if (NT == 2) {
+          float (&a2)[2][8] = reinterpret_cast<float (&)[2][8]>(acc);
+          gather_rows<2>(wb, Dp, m, lst_idx, lst_val, 1, 0, tid, true, a2);
+        } else {
+          gather_rows<4>(wb, Dp, m, lst_idx, lst_val, 1, 0, tid, true, acc);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int c8 = nt * 256 + tid;
+          if (nt < NT && c8 < LPR) {
+            float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
+            d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
+            d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+          }
+        }
+      }
+      __syncthreads();  // scratch is reused by the next unit
+    }
+  }
+  DEC_T(5);
+
+  // =====================================================================================
+  // P3: grid barrier, then the ordered combine
+  // =====================================================================================
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(&a.ctr[kCtrP2], 1u);
+    spin_until(&a.ctr[kCtrP2], static_cast<unsigned>(grid));
+  }
+  __syncthreads();
+  DEC_T(6);
+  {
+    const int CH = a.CH;
+    const int D4 = Dp / 4;
+    const int total4 = B * D4;
+    const bool y_vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
+    for (int q = tid * grid + bid; q < total4; q += grid * kDecThreads) {
+      const int t = q / D4, d4 = q % D4;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      for (int j = 0; j < R; ++j) {
+        const float* pj = a.part + (static_cast<size_t>(t * R + j) * CH) * Dp + d4 * 4;
+        float4 s = __ldcg(reinterpret_cast<const float4*>(pj));
+        for (int c = 1; c < CH; ++c) {
+          const float4 pv = __ldcg(reinterpret_cast<const float4*>(pj + static_cast<size_t>(c) * Dp));
+          s.x = __fadd_rn(s.x, pv.x);
+          s.y = __fadd_rn(s.y, pv.y);
+          s.z = __fadd_rn(s.z, pv.z);
+          s.w = __fadd_rn(s.w, pv.w);
+        }
+        const float w = j < K ? __ldcg(a.wts + t * K + j) : 1.0f;
+        acc.x = __fadd_rn(acc.x, __fmul_rn(w, s.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(w, s.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(w, s.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(w, s.w));
+      }
+      float* yo = a.y + static_cast<size_t>(t) * D + d4 * 4;
+      if (y_vec && d4 * 4 + 3 < D) {
+        *reinterpret_cast<float4*>(yo) = acc;
+      } else {
+        if (d4 * 4 + 0 < D) yo[0] = acc.x;
+        if (d4 * 4 + 1 < D) yo[1] = acc.y;
+        if (d4 * 4 + 2 < D) yo[2] = acc.z;
+        if (d4 * 4 + 3 < D) yo[3] = acc.w;
+      }
+    }
+  }
+  // the last CTA to leave puts every counter back to rest for the next forward
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicInc(&a.ctr[kCtrExit], static_cast<unsigned>(grid - 1));
+    if (prev == static_cast<unsigned>(grid - 1)) {
+      a.ctr[kCtrP0] = 0u;
+      a.ctr[kCtrRoute] = 0u;
+      a.ctr[kCtrP2] = 0u;
+      for (int i = 0; i < 4; ++i) a.ctr[kCtrChain + i] = 0u;
+      for (int i = 0; i <= kDecMaxU; ++i) a.ctr[kCtrH + i] = 0u;
+      __threadfence();
+    }
+  }
+  DEC_T(7);
+}
+
+bool decode_fused_eligible(const Geometry& g, int B) {
+  const int nmax = g.N > g.S ? g.N : g.S;
+  return B >= 1 && B <= kDecTokens && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxKpt * kDecThreads &&
+         g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288;
+}
+
+int decode_counter_words() { return kCtrH + kDecMaxU + 8; }
+int decode_cand_rows(int K) { return K + 4; }
+int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
+  // Batch-invariant by design (B is ignored): one token's units fill the grid once.
+  (void)B;
+  const int R = g.K + (g.has_shared ? 1 : 0);
+  int ch = n_sms / R;
+  int cap = keep_max / 8;  // at least ~8 rows per unit
+  if (cap < 1) cap = 1;
+  if (ch > cap) ch = cap;
+  if (ch > 64) ch = 64;
+  if (ch < 1) ch = 1;
+  return ch;
+}
+
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_xb,
+                        const DecodeLaunch& d, const Geometry& g, int n_sms) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kDecSmemBytes);
+    attr_set = true;
+  }
+  DecodeArgs a{};
+  a.x = d.x;
+  a.router = d.router;
+  a.wd = d.wd;
+  a.wd_shared = d.wd_shared;
+  a.B = d.B;
+  a.E = g.E;
+  a.K = g.K;
+  a.D = g.D;
+  a.Dp = g.Dp;
+  a.N = g.N;
+  a.Np = g.Np;
+  a.S = g.S;
+  a.Sp = g.Sp;
+  a.Nh = g.Nh;
+  a.has_shared = g.has_shared;
+  a.renorm = g.renorm;
+  a.sel_mode = d.sel_mode;
+  a.n_off_r = d.n_off_r;
+  a.n_off_s = d.n_off_s;
+  a.mask_r = d.mask_r;
+  a.mask_s = d.mask_s;
+  a.CM = decode_cand_rows(g.K);
+  a.CH = d.CH;
+  a.capture = d.capture ? 1 : 0;
+  a.xb = d.xb;
+  a.lf = d.lf;
+  a.lm = d.lm;
+  a.logits = d.logits;
+  a.ids = d.ids;
+  a.wts = d.wts;
+  a.hc = d.hc;
+  a.hist = d.hist;
+  a.part = d.part;
+  a.ctr = d.ctr;
+  a.y = d.y;
+  a.h_cap = d.h_cap;
+  a.inv = d.inv;
+  a.perm = d.perm;
+  a.row_expert = d.row_expert;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.stream = ctx.stream;
+  cfg.gridDim = dim3(n_sms);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = kDecSmemBytes;
+  cudaLaunchKernelEx(&cfg, decode_fused_kernel, *tmap_w, *tmap_xb, a);
+  return 1;
+}
+
+}  // namespace skb

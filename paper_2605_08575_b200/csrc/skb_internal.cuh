@@ -150,6 +150,41 @@ int launch_down(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g);
 int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
                          int B, int K, int D, float* y);
 
+// Fused decode kernel (decode.cu): the whole layer for B <= 16 in one persistent launch.
+struct DecodeLaunch {
+  const float* x;                  // [B][D]
+  const float* router;             // [E][D]
+  const __nv_bfloat16* wd;         // [E][Np][Dp]
+  const __nv_bfloat16* wd_shared;  // [Sp][Dp] or NULL
+  int B;
+  int sel_mode, n_off_r, n_off_s;  // kSelect*
+  const uint8_t* mask_r;           // kSelectGiven: [B*K][N]
+  const uint8_t* mask_s;           // kSelectGiven: [B][S] or NULL
+  int CH;                          // row chunks per (token, slot): decode_chunks()
+  bool capture;                    // also write h / inv / perm / row_expert in slot order
+  __nv_bfloat16* xb;               // [16][Dp] bf16 token rows (TMA source)
+  float* lf;                       // [B][E] fast logits
+  float* lm;                       // [B][E] their error bounds
+  float* logits;                   // [B][E] exact logits
+  int32_t* ids;                    // [B][K]
+  float* wts;                      // [B][K]
+  float* hc;                       // [16 * CM + 16][Nh] candidate rows
+  uint32_t* hist;                  // [16 * CM + 16][512]
+  float* part;                     // [B][R][CH][Dp]
+  unsigned* ctr;                   // decode_counter_words() zeroed words
+  float* y;                        // [B][D]
+  float* h_cap;                    // capture: [B*K + B][Nh]
+  int32_t* inv;
+  int32_t* perm;
+  int32_t* row_expert;
+};
+bool decode_fused_eligible(const Geometry& g, int B);
+int decode_counter_words();
+int decode_cand_rows(int K);
+int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms);
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_xb,
+                        const DecodeLaunch& d, const Geometry& g, int n_sms);
+
 // weight image construction
 int launch_pack_gateup(cudaStream_t s, const float* gate, const float* up, int n_rows, int D, int Dp,
                        __nv_bfloat16* dst_block_base);
