@@ -235,7 +235,8 @@ int reserve_locked(skb_layer* L, int B) {
     SKB_TRY(dmalloc(&L->d_dec_hc, crow * g.Nh));
     SKB_TRY(dmalloc(&L->d_dec_hist, crow * 512));
     SKB_TRY(dmalloc(&L->d_dec_part,
-                    16 * (static_cast<size_t>(L->n_sms) + g.K + 1) * g.Dp));
+                    16 * static_cast<size_t>(decode_cand_rows(g.K) + 1) *
+                        decode_chunks(g, 1, g.N > g.S ? g.N : g.S, L->n_sms) * g.Dp));
     SKB_TRY(dmalloc(&L->d_dec_ctr, static_cast<size_t>(decode_counter_words())));
     SKB_CUDA(cudaMemsetAsync(L->d_dec_ctr, 0, decode_counter_words() * sizeof(unsigned), L->stream));
     SKB_CUDA(cudaMemsetAsync(L->d_dec_hist, 0, crow * 512 * sizeof(uint32_t), L->stream));

@@ -56,10 +56,10 @@ constexpr int kMemberCap = 1024;
 constexpr int kMaxKpt = 32;  // keys per thread: N, S <= 8192
 
 // exact-chain ring (per CTA): 8 experts + 4 tokens per unit, 256-float sub-chunks
-constexpr int kChEB = 8, kChTB = 4, kChSub = 256, kChStages = 3;
+constexpr int kChEB = 8, kChTB = 4, kChSub = 256, kChStages = 4;
 constexpr int kChRow = kChSub + 4;
 constexpr int kChRows = kChEB + kChTB;
-constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 37440
+constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 49920
 
 constexpr int kDecMaxE = 256;
 constexpr int kDecMaxU = 256;  // union of candidate experts
@@ -74,7 +74,8 @@ struct DecSmem {
   static constexpr int rowtab = chain + kChBytes;                  // int16 [kDecMaxU + 1][16]
   static constexpr int uidx = rowtab + (kDecMaxU + 1) * 16 * 2;    // int16 [kDecMaxE]
   static constexpr int ulist = uidx + kDecMaxE * 2;                // int16 [kDecMaxU]
-  static constexpr int cmask = ulist + kDecMaxU * 2;               // uint32 [kDecMaxE]
+  static constexpr int cande = ulist + kDecMaxU * 2;               // int16 [16][20] candidate experts
+  static constexpr int cmask = cande + 16 * 20 * 2;                // uint32 [kDecMaxE]
   static constexpr int rscr = cmask + kDecMaxE * 4;                // float [E + K + 8] route() scratch
   static constexpr int bars = rscr + 1152;                         // 8-byte aligned
   static constexpr int n_bars = 2 * kDecStages + 4 + 2 * kChStages;
@@ -120,13 +121,20 @@ __device__ __forceinline__ void fma8(const uint4& u, float hk, float* a) {
 }  // namespace
 
 #ifdef SKB_DEBUG_TIMING
-__device__ long long g_dec_dbg[160 * 16];
-#define DEC_T(i) do { if (threadIdx.x == 0) g_dec_dbg[blockIdx.x * 16 + (i)] = clock64(); } while (0)
-#define DEC_TW(w, i) do { if (threadIdx.x == (w) * 32) g_dec_dbg[blockIdx.x * 16 + (i)] = clock64(); } while (0)
+__device__ long long g_dec_dbg[160 * 24];
+__device__ __forceinline__ long long dec_gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DEC_T(i) do { if (threadIdx.x == 0) g_dec_dbg[blockIdx.x * 24 + (i)] = clock64(); } while (0)
+#define DEC_TW(w, i) do { if (threadIdx.x == (w) * 32) g_dec_dbg[blockIdx.x * 24 + (i)] = clock64(); } while (0)
+#define DEC_G(i) do { if (threadIdx.x == 0) g_dec_dbg[blockIdx.x * 24 + (i)] = dec_gtime(); } while (0)
 extern "C" void skb_debug_dec(long long* out) { cudaMemcpyFromSymbol(out, g_dec_dbg, sizeof(g_dec_dbg)); }
 #else
 #define DEC_T(i) do { } while (0)
 #define DEC_TW(w, i) do { } while (0)
+#define DEC_G(i) do { } while (0)
 #endif
 
 // Column tiles of 2048 (256 threads x 8 columns) per W_down row: NT = ceil(Dp / 2048).
@@ -134,7 +142,7 @@ template <int NT>
 __device__ __forceinline__ void gather_rows(const __nv_bfloat16* __restrict__ wb, int Dp, int m,
                                             const int32_t* lst_idx, const float* lst_val, int G,
                                             int g, int l, bool lane_ok, float (&acc)[NT][8]) {
-  constexpr int U = NT == 1 ? 16 : (NT == 2 ? 8 : 4);
+  constexpr int U = NT == 1 ? 24 : 6;
   const int LPR = Dp >> 3;
 #pragma unroll 1
   for (int p0 = g; p0 < m; p0 += G * U) {
@@ -189,6 +197,15 @@ struct DecodeArgs {
   int32_t* row_expert;
 };
 
+// order-preserving map float -> uint32 (so that warp REDUX max works on floats) and back
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 __global__ void __launch_bounds__(kDecThreads, 1)
 decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
                     const __grid_constant__ CUtensorMap tmap_xb, const DecodeArgs a) {
@@ -199,8 +216,12 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   int16_t* rowtab = reinterpret_cast<int16_t*>(sm + DecSmem::rowtab);
   int16_t* uidx = reinterpret_cast<int16_t*>(sm + DecSmem::uidx);
   int16_t* ulist = reinterpret_cast<int16_t*>(sm + DecSmem::ulist);
+  int16_t* cande = reinterpret_cast<int16_t*>(sm + DecSmem::cande);
   uint32_t* cmask = reinterpret_cast<uint32_t*>(sm + DecSmem::cmask);
   int* misc = reinterpret_cast<int*>(sm + DecSmem::misc);
+  // misc: 0 tmem ptr, 1 overflow flag, 2 n_u, 8.. P2 scalars, 24.. ncand[16], 40.. pairoff[17]
+  int* ncand = misc + 24;
+  int* pairoff = misc + 40;
   const uint32_t bar0 = sm_u32 + DecSmem::bars;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kDecStages + s); };
@@ -208,14 +229,15 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * kDecStages + 2 + b); };
   auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + s); };
   auto cempty_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + kChStages + s); };
-  // misc ints: 0 tmem ptr, 1 overflow flag, 2 n_u, 3.. P2 scalars
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grid = gridDim.x, bid = blockIdx.x;
-  const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp;
-  const int R = K + (a.has_shared ? 1 : 0);
+  const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp, CM = a.CM;
   const int n_tb = ceil_div(B, kChTB), n_eb = ceil_div(E, kChEB);
+  const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
 
   DEC_T(0);
+  DEC_G(16);
   // ---- prologue ----
   if (tid == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -250,88 +272,89 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     // rows [0, B*CM) routed candidates, rows [16*CM, 16*CM + B) shared expert
     uint4* h4 = reinterpret_cast<uint4*>(a.hist);
     const int per_row = kHistBins / 4;
-    const int n1 = B * a.CM * per_row;
+    const int n1 = B * CM * per_row;
     const int n2 = a.has_shared ? B * per_row : 0;
     for (int i = bid * kDecThreads + tid; i < n1 + n2; i += grid * kDecThreads) {
-      const int j = i < n1 ? i : (kDecTokens * a.CM * per_row + (i - n1));
+      const int j = i < n1 ? i : (kDecTokens * CM * per_row + (i - n1));
       h4[j] = make_uint4(0u, 0u, 0u, 0u);
     }
   }
-  // token t is converted by CTA grid-1-t (the low CTAs carry the logit units)
-  for (int t = grid - 1 - bid; t < B; t += grid) {
+  for (int t = (bid - E % grid + grid) % grid; t < B; t += grid) {
     const float* src = a.x + static_cast<size_t>(t) * D;
     __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
     for (int d = tid; d < D; d += kDecThreads) dst[d] = __float2bfloat16_rn(__ldg(src + d));
   }
   {
-    float* red = reinterpret_cast<float*>(work);  // [8 warps][16 tokens][2]
-    const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
-                        ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
+    float* red = reinterpret_cast<float*>(work);  // [8 warps][4 tokens][2]
     // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
     const double u24 = 5.9604644775390625e-8;
     const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
+#pragma unroll 1
     for (int e = bid; e < E; e += grid) {
-      float pl[kDecTokens], pa[kDecTokens];
-#pragma unroll
-      for (int t = 0; t < kDecTokens; ++t) pl[t] = pa[t] = 0.0f;
       const float* wr = a.router + static_cast<size_t>(e) * D;
-      if (vec_ok) {
-        const float4* w4 = reinterpret_cast<const float4*>(wr);
-        for (int q = tid; q < D / 4; q += kDecThreads) {
-          const float4 w = __ldg(w4 + q);
+#pragma unroll 1
+      for (int t0 = 0; t0 < B; t0 += 4) {
+        float pl[4] = {0.0f, 0.0f, 0.0f, 0.0f}, pa[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (vec_ok) {
+          const float4* w4 = reinterpret_cast<const float4*>(wr);
+#pragma unroll 2
+          for (int q = tid; q < D / 4; q += kDecThreads) {
+            const float4 w = __ldg(w4 + q);
 #pragma unroll
-          for (int t = 0; t < kDecTokens; ++t) {
-            if (t < B) {
-              const float4 xv = __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t) * D) + q);
-              pl[t] = fmaf(w.x, xv.x, pl[t]);
-              pl[t] = fmaf(w.y, xv.y, pl[t]);
-              pl[t] = fmaf(w.z, xv.z, pl[t]);
-              pl[t] = fmaf(w.w, xv.w, pl[t]);
-              pa[t] = fmaf(fabsf(w.x), fabsf(xv.x), pa[t]);
-              pa[t] = fmaf(fabsf(w.y), fabsf(xv.y), pa[t]);
-              pa[t] = fmaf(fabsf(w.z), fabsf(xv.z), pa[t]);
-              pa[t] = fmaf(fabsf(w.w), fabsf(xv.w), pa[t]);
+            for (int tt = 0; tt < 4; ++tt) {
+              if (t0 + tt < B) {
+                const float4 xv =
+                    __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t0 + tt) * D) + q);
+                pl[tt] = fmaf(w.x, xv.x, pl[tt]);
+                pl[tt] = fmaf(w.y, xv.y, pl[tt]);
+                pl[tt] = fmaf(w.z, xv.z, pl[tt]);
+                pl[tt] = fmaf(w.w, xv.w, pl[tt]);
+                pa[tt] = fmaf(fabsf(w.x), fabsf(xv.x), pa[tt]);
+                pa[tt] = fmaf(fabsf(w.y), fabsf(xv.y), pa[tt]);
+                pa[tt] = fmaf(fabsf(w.z), fabsf(xv.z), pa[tt]);
+                pa[tt] = fmaf(fabsf(w.w), fabsf(xv.w), pa[tt]);
+              }
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int d = tid; d < D; d += kDecThreads) {
+            const float w = __ldg(wr + d);
+#pragma unroll
+            for (int tt = 0; tt < 4; ++tt) {
+              if (t0 + tt < B) {
+                const float xv = __ldg(a.x + static_cast<size_t>(t0 + tt) * D + d);
+                pl[tt] = fmaf(w, xv, pl[tt]);
+                pa[tt] = fmaf(fabsf(w), fabsf(xv), pa[tt]);
+              }
             }
           }
         }
-      } else {
-        for (int d = tid; d < D; d += kDecThreads) {
-          const float w = __ldg(wr + d);
 #pragma unroll
-          for (int t = 0; t < kDecTokens; ++t) {
-            if (t < B) {
-              const float xv = __ldg(a.x + static_cast<size_t>(t) * D + d);
-              pl[t] = fmaf(w, xv, pl[t]);
-              pa[t] = fmaf(fabsf(w), fabsf(xv), pa[t]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < kDecTokens; ++t) {
-        if (t < B) {
+        for (int tt = 0; tt < 4; ++tt) {
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
-            pl[t] += __shfl_xor_sync(0xffffffffu, pl[t], o);
-            pa[t] += __shfl_xor_sync(0xffffffffu, pa[t], o);
+            pl[tt] += __shfl_xor_sync(0xffffffffu, pl[tt], o);
+            pa[tt] += __shfl_xor_sync(0xffffffffu, pa[tt], o);
           }
           if (lane == 0) {
-            red[(warp * kDecTokens + t) * 2 + 0] = pl[t];
-            red[(warp * kDecTokens + t) * 2 + 1] = pa[t];
+            red[(warp * 4 + tt) * 2 + 0] = pl[tt];
+            red[(warp * 4 + tt) * 2 + 1] = pa[tt];
           }
         }
-      }
-      __syncthreads();
-      if (tid < B) {
-        float s = 0.0f, sa = 0.0f;
-        for (int w = 0; w < kDecThreads / 32; ++w) {
-          s += red[(w * kDecTokens + tid) * 2 + 0];
-          sa += red[(w * kDecTokens + tid) * 2 + 1];
+        __syncthreads();
+        if (tid < 4 && t0 + tid < B) {
+          float s = 0.0f, sa = 0.0f;
+#pragma unroll
+          for (int w = 0; w < kDecThreads / 32; ++w) {
+            s += red[(w * 4 + tid) * 2 + 0];
+            sa += red[(w * 4 + tid) * 2 + 1];
+          }
+          a.lf[static_cast<size_t>(t0 + tid) * E + e] = s;
+          a.lm[static_cast<size_t>(t0 + tid) * E + e] = sa * mfac + 2e-5f;
         }
-        a.lf[static_cast<size_t>(tid) * E + e] = s;
-        a.lm[static_cast<size_t>(tid) * E + e] = sa * mfac + 2e-5f;
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   __syncthreads();
@@ -343,17 +366,17 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   DEC_T(1);
 
   // =====================================================================================
-  // Exact routing chains: warps 6 (consumer) and 7 (producer) -- independent of everything
-  // below until P2.  They start before the P0 barrier: they only read x and the router.
+  // Exact routing chains: warps 6 (consumer) and 7 (producer), on the LAST CTAs of the grid
+  // (the first ones carry the logit units and, at decode sizes, all the gate/up items).  They
+  // only read x and the router, so they start right away; their result is needed by P3.
   // =====================================================================================
   if (warp >= 6) {
     float* ring = reinterpret_cast<float*>(sm + DecSmem::chain);
     const int n_cu = n_eb * n_tb;
     const int nsub = ceil_div(D, kChSub);
-    const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
-                        ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
     int gsc = 0;  // ring position, continues across units
-    for (int cu = bid; cu < n_cu; cu += grid) {
+#pragma unroll 1
+    for (int cu = grid - 1 - bid; cu < n_cu; cu += grid) {
       const int eb = cu % n_eb, tb = cu / n_eb;
       const int e0 = eb * kChEB, t0 = tb * kChTB;
       const int n_e = min(kChEB, E - e0), n_t = min(kChTB, B - t0);
@@ -406,6 +429,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         const bool valid = (e_i < n_e) && (t_j < n_t);
         float acc = 0.0f;
         int csc = gsc;
+        DEC_TW(6, 14);
 #pragma unroll 1
         for (int sc = 0; sc < nsub; ++sc, ++csc) {
           const int slot = csc % kChStages;
@@ -429,6 +453,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           __syncwarp();
           if (lane == 0) mbar_arrive(cempty_bar(slot));
         }
+        DEC_TW(6, 15);
         if (valid) a.logits[static_cast<size_t>(t0 + t_j) * E + e0 + e_i] = acc;
         __threadfence();
         __syncwarp();
@@ -439,6 +464,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           // last chain of this token block: route() for its tokens
           __threadfence();
           float* scr = reinterpret_cast<float*>(sm + DecSmem::rscr);
+#pragma unroll 1
           for (int tt = 0; tt < n_t; ++tt) {
             const int t = t0 + tt;
             warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, scr,
@@ -455,7 +481,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   }
 
   // =====================================================================================
-  // P0 barrier, candidates (every CTA computes the same tables)
+  // P0 barrier, candidates (every CTA computes the same tables), P1
   // =====================================================================================
   if (warp < 6) {
     if (tid == 0) {
@@ -472,51 +498,41 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     }
     asm volatile("bar.sync 2, 192;" ::: "memory");
     constexpr int kVpl = kDecMaxE / 32;
+#pragma unroll 1
     for (int t = warp; t < B; t += 6) {
-      float lo[kVpl], hi[kVpl];
+      uint32_t lo[kVpl];
+      float hi[kVpl];
       bool bad = false;
-      float mx = -INFINITY;
+      uint32_t mxk = 0u;
 #pragma unroll
       for (int i = 0; i < kVpl; ++i) {
         const int e = i * 32 + lane;
         if (e < E) {
           const float f = slf[t * E + e], m = slm[t * E + e];
-          lo[i] = f - m;
+          lo[i] = f2ord(f - m);
           hi[i] = f + m;
-          mx = fmaxf(mx, f);
+          mxk = max(mxk, f2ord(f));
           bad |= !(fabsf(f) < 1e30f) || !(m < 1e30f);
         } else {
-          lo[i] = -INFINITY;
+          lo[i] = 0u;
           hi[i] = -INFINITY;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      // K-th largest lower end: K rounds of warp arg-max, removing one instance per round
-      float thr = -INFINITY;
+      const float mx = ord2f(__reduce_max_sync(0xffffffffu, mxk));
+      // K-th largest lower end: K rounds of warp max, all instances of the maximum removed per
+      // round (duplicates can only lower the threshold, i.e. enlarge the candidate set)
+      uint32_t thrk = 0u;
+#pragma unroll 1
       for (int s = 0; s < K; ++s) {
-        float bv = -INFINITY;
-        int bi = 0x7fffffff;
+        uint32_t m = 0u;
+#pragma unroll
+        for (int i = 0; i < kVpl; ++i) m = max(m, lo[i]);
+        thrk = __reduce_max_sync(0xffffffffu, m);
 #pragma unroll
         for (int i = 0; i < kVpl; ++i)
-          if (lo[i] > bv) {
-            bv = lo[i];
-            bi = i * 32 + lane;
-          }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        thr = bv;
-#pragma unroll
-        for (int i = 0; i < kVpl; ++i)
-          if (i * 32 + lane == bi) lo[i] = -INFINITY;
+          if (lo[i] == thrk) lo[i] = 0u;
       }
+      const float thr = thrk == 0u ? -INFINITY : ord2f(thrk);
       int cnt = 0;
       unsigned mine = 0;
 #pragma unroll
@@ -525,7 +541,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         cnt += __popc(__ballot_sync(0xffffffffu, c));
         if (c) mine |= 1u << i;
       }
-      bad = __any_sync(0xffffffffu, bad) || !(thr > -1e30f) || (thr < mx - 60.0f) || cnt > a.CM ||
+      bad = __any_sync(0xffffffffu, bad) || !(thr > -1e30f) || (thr < mx - 60.0f) || cnt > CM ||
             cnt < K;
       if (bad) {
         if (lane == 0) misc[1] = 1;
@@ -544,9 +560,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       for (int i = tid; i < B * K; i += 192) atomicOr(&cmask[__ldcg(a.ids + i)], 1u << (i / K));
       asm volatile("bar.sync 2, 192;" ::: "memory");
     }
-    // union list (ascending expert id) by warp 0, row table by all
+    // union list (ascending expert id) by warp 0
     if (warp == 0) {
       int run = 0;
+#pragma unroll 1
       for (int base = 0; base < E; base += 32) {
         const int e = base + lane;
         const bool f = e < E && cmask[e] != 0u;
@@ -559,39 +576,55 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       if (lane == 0) misc[2] = run;
     }
     asm volatile("bar.sync 2, 192;" ::: "memory");
-    const int n_u0 = misc[2];
-    for (int i = tid; i < (n_u0 + 1) * 16; i += 192) rowtab[i] = -1;
+    const int n_u = misc[2];
+    for (int i = tid; i < (n_u + 1) * 16; i += 192) rowtab[i] = -1;
     asm volatile("bar.sync 2, 192;" ::: "memory");
+#pragma unroll 1
     for (int t = warp; t < B; t += 6) {
       int run = 0;
+#pragma unroll 1
       for (int base = 0; base < E; base += 32) {
         const int e = base + lane;
         const bool f = e < E && ((cmask[e] >> t) & 1u);
         const unsigned b = __ballot_sync(0xffffffffu, f);
-        if (f) rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * a.CM + run + __popc(b & ((1u << lane) - 1u)));
+        if (f) {
+          const int r = run + __popc(b & ((1u << lane) - 1u));
+          rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * CM + r);
+          cande[t * CM + r] = static_cast<int16_t>(e);
+        }
         run += __popc(b);
       }
-      if (a.has_shared && lane == 0) rowtab[n_u0 * 16 + t] = static_cast<int16_t>(kDecTokens * a.CM + t);
+      if (lane == 0) {
+        ncand[t] = run;
+        if (a.has_shared) rowtab[n_u * 16 + t] = static_cast<int16_t>(kDecTokens * CM + t);
+      }
     }
     asm volatile("bar.sync 2, 192;" ::: "memory");
+    if (tid == 0) {
+      int run = 0;
+      for (int t = 0; t < B; ++t) {
+        pairoff[t] = run;
+        run += ncand[t] + (a.has_shared ? 1 : 0);
+      }
+      pairoff[B] = run;
+    }
     DEC_T(3);
 
-    // ===================================================================================
-    // P1: gate/up + SwiGLU over (union expert, 64-neuron block) items
-    // ===================================================================================
-    const int n_u = n_u0;
+    // ---- P1: gate/up + SwiGLU over (union expert, 64-neuron block) items ----
     const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
     const int n_items = n_u * NB + NBs;
     const int KB = Dp / kBlockK;
     if (warp == 0) {
       if (lane == 0) {
         int gk = 0;
+#pragma unroll 1
         for (int it = bid; it < n_items; it += grid) {
           const bool sh = it >= n_u * NB;
           const int u = sh ? n_u : it / NB;
           const int nb = sh ? it - n_u * NB : it % NB;
           const int e = sh ? E : ulist[u];
           const int a_row = e * 2 * a.Np + nb * 128;
+#pragma unroll 1
           for (int kb = 0; kb < KB; ++kb, ++gk) {
             const int s = gk % kDecStages;
             mbar_wait(empty_bar(s), ((gk / kDecStages) & 1u) ^ 1u);
@@ -607,10 +640,12 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       if (lane == 0) {
         constexpr uint32_t kIdesc = make_idesc_bf16(128, kDecTokens);
         int gk = 0, li = 0;
+#pragma unroll 1
         for (int it = bid; it < n_items; it += grid, ++li) {
           const int buf = li & 1;
           mbar_wait(tempty_bar(buf), (((li >> 1) & 1u) ^ 1u));
           tc_fence_after();
+#pragma unroll 1
           for (int kb = 0; kb < KB; ++kb, ++gk) {
             const int s = gk % kDecStages;
             mbar_wait(full_bar(s), (gk / kDecStages) & 1u);
@@ -631,6 +666,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       const int q = warp & 3;
       const bool is_gate_lane = lane < 16;
       int li = 0;
+#pragma unroll 1
       for (int it = bid; it < n_items; it += grid, ++li) {
         const bool sh = it >= n_u * NB;
         const int u = sh ? n_u : it / NB;
@@ -679,83 +715,101 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   }
   __syncthreads();
   DEC_T(4);
+  DEC_G(17);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 32);
   }
 
   // =====================================================================================
-  // P2: selection + down projection over (token, slot, row chunk) units.  Units are dealt in
-  // contiguous ranges, chunk index fastest, so a CTA that holds several chunks of one (token,
-  // slot) selects once.  The chunking depends on the shape only -- not on the batch -- so the
-  // reduction tree of a token does not depend on what else is in the batch.
+  // P2: selection + down projection over (token, candidate, row chunk) units.  Units are dealt
+  // in contiguous ranges, chunk index fastest, so a CTA that holds several chunks of one row
+  // selects once.  The chunking depends on the shape only -- not on the batch -- so the
+  // reduction tree of a token does not depend on what else is in the batch.  Candidates that the
+  // exact routing later rejects (rare) are computed and ignored by P3.
   // =====================================================================================
+  const int n_u = misc[2];
+  const int CH = a.CH;
   {
-    const int n_u = misc[2];
     const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
-    const int CH = a.CH;
-    const int n_units = B * R * CH;
-    // scratch (the GEMM stages are idle now)
+    const int n_units = pairoff[B] * CH;
     int32_t* lst_idx = reinterpret_cast<int32_t*>(work);           // [8192]
     float* lst_val = reinterpret_cast<float*>(work + 32768);       // [8192]
-    uint32_t* keys_s = reinterpret_cast<uint32_t*>(work + 65536);  // [8192] (fallback search)
-    uint32_t* mlist = reinterpret_cast<uint32_t*>(work + 98304);   // [kMemberCap + 4]
-    int* wc = reinterpret_cast<int*>(work + 98304 + 4352);         // [kMaxKpt * 8] + [8]
-    float* gred = reinterpret_cast<float*>(work + 106496);         // [G][Dp] <= 8 KB (NT == 1)
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(work + 65536);  // [8192] raw bits of h
+    uint8_t* kf = work + 98304;                                    // [8192] keep flags
+    uint32_t* mlist = reinterpret_cast<uint32_t*>(work + 106496);  // [kMemberCap + 4]
+    int* wc = reinterpret_cast<int*>(work + 110848);               // [kMaxKpt * 8] + [8]
+    float* gred = reinterpret_cast<float*>(work + 112128);         // [G][Dp] <= 8 KB (NT == 1)
     __shared__ SelScratch sel_sc;
-    int* p2 = misc + 8;  // 0 row, 1 e, 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount, 9 total
+    int* p2 = misc + 8;  // 0 row, 1 e, 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount, 9 total, 10 slot
     bool route_ready = false;
     const int LPR = Dp >> 3;
     const int NT = ceil_div(LPR, 256);
     const int G = NT == 1 ? (256 / LPR > 0 ? 256 / LPR : 1) : 1;
-    const int v0 = static_cast<int>(static_cast<long long>(bid) * n_units / grid);
-    const int v1 = static_cast<int>(static_cast<long long>(bid + 1) * n_units / grid);
+    // CTAs that host exact-routing chains (the last ones) take units only when the others
+    // cannot hold them all in one wave: their P2 would start after the chains
+    const int n_chain_ctas = min(n_eb * n_tb, grid);
+    const int gp = (n_units <= grid - n_chain_ctas) ? grid - n_chain_ctas : grid;
+    const int v0 = bid < gp ? static_cast<int>(static_cast<long long>(bid) * n_units / gp) : 0;
+    const int v1 = bid < gp ? static_cast<int>(static_cast<long long>(bid + 1) * n_units / gp) : 0;
 
-    int cur_tj = -1;
-    int row = 0, e = 0, n = 0, kpt = 0, cnt = 0;
+    int cur_pr = -1;
+    int e = 0, n = 0, kpt = 0, cnt = 0, t = 0, q = 0;
     bool routed = true;
-    unsigned flags = 0;       // keep flag of key jj of this thread
-    uint32_t hb[kMaxKpt];     // raw bits of this thread's h values: element jj * 256 + tid
 
+#pragma unroll 1
     for (int v = v0; v < v1; ++v) {
       const int c = v % CH;
-      const int tj = v / CH;
-      const int j = tj % R;
-      const int t = tj / R;
-      if (tj != cur_tj) {
-        cur_tj = tj;
-        routed = j < K;
+      const int pr = v / CH;
+      if (pr != cur_pr) {
+        cur_pr = pr;
+        t = 0;
+        while (t + 1 < B && pairoff[t + 1] <= pr) ++t;
+        q = pr - pairoff[t];
+        routed = q < ncand[t];
         if (tid == 0) {
-          if (!route_ready) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
-          int ee, u, rr;
+          int ee, u, rr, slot = -1;
           if (routed) {
-            ee = __ldcg(a.ids + t * K + j);
+            ee = cande[t * CM + q];
             u = uidx[ee];
-            if (u < 0) asm volatile("trap;");  // the candidate bound is a theorem: never taken
-            rr = rowtab[u * 16 + t];
+            rr = t * CM + q;
             spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NB));
+            if (a.sel_mode == kSelectGiven) {
+              // caller masks are indexed by slot: the exact routing is needed here
+              if (!route_ready) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+              for (int j = 0; j < K; ++j)
+                if (__ldcg(a.ids + t * K + j) == ee) slot = t * K + j;
+            }
           } else {
             ee = E;
             u = n_u;
-            rr = kDecTokens * a.CM + t;
+            rr = kDecTokens * CM + t;
+            slot = t;
             spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NBs));
           }
           p2[0] = rr;
           p2[1] = ee;
           p2[8] = 0;
+          p2[10] = slot;
         }
         route_ready = true;
         __syncthreads();
-        row = p2[0];
+        DEC_T(8);
+        DEC_G(18);
+        const int row = p2[0];
         e = p2[1];
+        const int slot = p2[10];
         n = routed ? a.N : a.S;
-        const int slot = routed ? t * K + j : t;
         int mode = a.sel_mode;
         const uint8_t* min_ = nullptr;
         if (mode == kSelectGiven) {
-          min_ = routed ? a.mask_r + static_cast<size_t>(slot) * n
-                        : (a.mask_s ? a.mask_s + static_cast<size_t>(slot) * n : nullptr);
-          if (min_ == nullptr) mode = kSelectAll;
+          if (routed) {
+            min_ = slot >= 0 ? a.mask_r + static_cast<size_t>(slot) * n : nullptr;
+            if (slot < 0) mode = -1;  // a candidate the exact routing rejected: nothing to do
+          } else {
+            min_ = a.mask_s ? a.mask_s + static_cast<size_t>(slot) * n : nullptr;
+            if (min_ == nullptr) mode = kSelectAll;
+          }
         }
         int n_off = 0;
         if (mode == kSelectTopk) {
@@ -764,41 +818,23 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         }
         kpt = ceil_div(n, kDecThreads);
         const float* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
-#pragma unroll
-        for (int jj = 0; jj < kMaxKpt; ++jj) {
-          if (jj < kpt) {
-            const int i = jj * kDecThreads + tid;
-            hb[jj] = i < n ? __float_as_uint(__ldcg(hrow + i)) : 0u;
-          }
-        }
-        if (a.capture) {
-          float* dst = a.h_cap + static_cast<size_t>(routed ? slot : B * K + t) * a.Nh;
-#pragma unroll
-          for (int jj = 0; jj < kMaxKpt; ++jj)
-            if (jj < kpt && jj * kDecThreads + tid < n)
-              dst[jj * kDecThreads + tid] = __uint_as_float(hb[jj]);
-          if (tid == 0) {
-            if (routed) {
-              a.inv[slot] = slot;
-              a.perm[slot] = slot;
-              a.row_expert[slot] = e;
-            } else {
-              a.row_expert[B * K + t] = E;
-            }
-          }
-        }
+        uint2 hh = make_uint2(0u, 0u);
+        if (mode == kSelectTopk && n_off < n)
+          hh = __ldcg(reinterpret_cast<const uint2*>(a.hist + static_cast<size_t>(row) * kHistBins) + tid);
+#pragma unroll 4
+        for (int i = tid; i < n; i += kDecThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
 
         RowPick pk{0u, 0, true};
         if (mode == kSelectAll) {
           cnt = n;
         } else if (mode == kSelectGiven) {
           cnt = 0;  // counted by the prefix below
+        } else if (mode < 0) {
+          cnt = 0;
         } else {
           cnt = n_off >= n ? 0 : n - n_off;
           if (cnt > 0) {
             // ---- pivot bucket from the row's histogram ----
-            const uint2 hh = __ldcg(
-                reinterpret_cast<const uint2*>(a.hist + static_cast<size_t>(row) * kHistBins) + tid);
             int incl = static_cast<int>(hh.x + hh.y);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -806,6 +842,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
               if (lane >= o) incl += up;
             }
             if (lane == 31) wc[warp] = incl;
+            for (int i = tid; i < kMemberCap + 4; i += kDecThreads) mlist[i] = 0xffffffffu;
             __syncthreads();
             int base = 0;
 #pragma unroll
@@ -822,35 +859,29 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             __syncthreads();
             const int bstar = p2[2], below_bins = p2[3], M = p2[4];
             if (M <= kMemberCap) {
-              for (int i = tid; i < kMemberCap + 4; i += kDecThreads) mlist[i] = 0xffffffffu;
-              __syncthreads();
-#pragma unroll
-              for (int jj = 0; jj < kMaxKpt; ++jj) {
-                if (jj < kpt && jj * kDecThreads + tid < n) {
-                  const uint32_t k = hb[jj] & 0x7fffffffu;
-                  if (hist_bin(k) == bstar) mlist[atomicAdd(&p2[8], 1)] = k;
-                }
+#pragma unroll 1
+              for (int i = tid; i < n; i += kDecThreads) {
+                const uint32_t k = keys_s[i] & 0x7fffffffu;
+                if (hist_bin(k) == bstar) mlist[atomicAdd(&p2[8], 1)] = k;
               }
               __syncthreads();
               const int rr = n_off - below_bins;  // 1-based rank inside the bucket
               const int M4 = (M + 3) >> 2;
-#pragma unroll
-              for (int jj = 0; jj < kMaxKpt; ++jj) {
-                if (jj < kpt && jj * kDecThreads + tid < n) {
-                  const uint32_t k = hb[jj] & 0x7fffffffu;
-                  if (hist_bin(k) == bstar) {
-                    int lt = 0, le = 0;
-                    for (int q4 = 0; q4 < M4; ++q4) {
-                      const uint4 mm = *reinterpret_cast<const uint4*>(mlist + 4 * q4);
-                      lt += (mm.x < k) + (mm.y < k) + (mm.z < k) + (mm.w < k);
-                      le += (mm.x <= k) + (mm.y <= k) + (mm.z <= k) + (mm.w <= k);
-                    }
-                    if (lt < rr && rr <= le) {
-                      p2[5] = static_cast<int>(k);
-                      p2[6] = below_bins + lt;
-                      p2[7] = le - lt;
-                    }
-                  }
+              // one member per thread (the bucket rarely holds more than a few dozen keys)
+#pragma unroll 1
+              for (int mi = tid; mi < M; mi += kDecThreads) {
+                const uint32_t k = mlist[mi];
+                int lt = 0, le = 0;
+#pragma unroll 1
+                for (int q4 = 0; q4 < M4; ++q4) {
+                  const uint4 mm = *reinterpret_cast<const uint4*>(mlist + 4 * q4);
+                  lt += (mm.x < k) + (mm.y < k) + (mm.z < k) + (mm.w < k);
+                  le += (mm.x <= k) + (mm.y <= k) + (mm.z <= k) + (mm.w <= k);
+                }
+                if (lt < rr && rr <= le) {
+                  p2[5] = static_cast<int>(k);
+                  p2[6] = below_bins + lt;
+                  p2[7] = le - lt;
                 }
               }
               __syncthreads();
@@ -859,47 +890,46 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
               pk.drop_all_ties = (pk.ties_to_drop == p2[7]);
             } else {
               // huge bucket (many equal / clamped values): the general search
-#pragma unroll
-              for (int jj = 0; jj < kMaxKpt; ++jj)
-                if (jj < kpt && jj * kDecThreads + tid < n)
-                  keys_s[jj * kDecThreads + tid] = hb[jj] & 0x7fffffffu;
+#pragma unroll 1
+              for (int i = tid; i < n; i += kDecThreads) keys_s[i] &= 0x7fffffffu;
               __syncthreads();
               pk = sel_kary_pick(keys_s, n, n_off, sel_sc);
+              __syncthreads();
+#pragma unroll 1
+              for (int i = tid; i < n; i += kDecThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
             }
           }
         }
+        __syncthreads();
+        DEC_T(9);
 
-        // ---- keep flags and their exclusive prefix in index order (wc[jj * 8 + warp]) ----
-        flags = 0;
-        if (mode != kSelectTopk || cnt > 0) {
+        // ---- keep flags kf[i] and their exclusive prefix in index order (wc[jj * 8 + warp]) ----
+        if (cnt > 0 || mode == kSelectGiven) {
           const bool need_ties = (mode == kSelectTopk) && !pk.drop_all_ties;
-          unsigned keepbits = 0;
+#pragma unroll 1
           for (int pass = need_ties ? 0 : 1; pass < 2; ++pass) {
             // pass 0: prefix over tie flags (only when some but not all ties are dropped);
             // pass 1: prefix over keep flags
-            unsigned fl = 0;
-#pragma unroll
-            for (int jj = 0; jj < kMaxKpt; ++jj) {
-              if (jj < kpt) {
-                const int i = jj * kDecThreads + tid;
-                const bool valid = i < n;
-                const uint32_t k = hb[jj] & 0x7fffffffu;
-                bool f;
-                if (pass == 0) {
-                  f = valid && k == pk.pivot;
-                } else if (mode == kSelectAll) {
-                  f = valid;
-                } else if (mode == kSelectGiven) {
-                  f = valid && min_[i] != 0;
-                } else if (pk.drop_all_ties) {
-                  f = valid && k > pk.pivot;
-                } else {
-                  f = valid && (k > pk.pivot || ((keepbits >> jj) & 1u));
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, f);
-                if (lane == 0) wc[jj * 8 + warp] = __popc(bal);
-                if (f) fl |= 1u << jj;
+#pragma unroll 1
+            for (int jj = 0; jj < kpt; ++jj) {
+              const int i = jj * kDecThreads + tid;
+              const bool valid = i < n;
+              const uint32_t k = valid ? (keys_s[i] & 0x7fffffffu) : 0u;
+              bool f;
+              if (pass == 0) {
+                f = valid && k == pk.pivot;
+              } else if (mode == kSelectAll) {
+                f = valid;
+              } else if (mode == kSelectGiven) {
+                f = valid && min_[i] != 0;
+              } else if (pk.drop_all_ties) {
+                f = valid && k > pk.pivot;
+              } else {
+                f = valid && (k > pk.pivot || (k == pk.pivot && kf[i] != 0));
               }
+              const unsigned bal = __ballot_sync(0xffffffffu, f);
+              if (lane == 0) wc[jj * 8 + warp] = __popc(bal);
+              if (pass == 1 && valid) kf[i] = f ? 1 : 0;
             }
             __syncthreads();
             {
@@ -923,23 +953,23 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
               __syncthreads();
             }
             if (pass == 0) {
-#pragma unroll
-              for (int jj = 0; jj < kMaxKpt; ++jj) {
-                if (jj < kpt) {
-                  const bool f = (fl >> jj) & 1u;
-                  const unsigned bal = __ballot_sync(0xffffffffu, f);
-                  const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
-                  if (f && rank >= pk.ties_to_drop) keepbits |= 1u << jj;
-                }
+              // a tie survives when its rank among the ties (ascending index) >= ties_to_drop
+#pragma unroll 1
+              for (int jj = 0; jj < kpt; ++jj) {
+                const int i = jj * kDecThreads + tid;
+                const bool f = i < n && (keys_s[i] & 0x7fffffffu) == pk.pivot;
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
+                if (f) kf[i] = rank >= pk.ties_to_drop ? 1 : 0;
               }
               __syncthreads();
-            } else {
-              flags = fl;
-              if (mode == kSelectGiven) cnt = p2[9];
+            } else if (mode == kSelectGiven) {
+              cnt = p2[9];
             }
           }
         }
       }
+      DEC_T(11);
 
       // ---- survivors [lo, hi) of this chunk, ascending index ----
       const int C = ceil_div(cnt > 0 ? cnt : 1, CH);
@@ -947,24 +977,24 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       const int hi_ = min(cnt, lo + C);
       const int m = hi_ > lo ? hi_ - lo : 0;
       if (m > 0) {
-#pragma unroll
-        for (int jj = 0; jj < kMaxKpt; ++jj) {
-          if (jj < kpt) {
-            const bool f = (flags >> jj) & 1u;
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
-            if (f && rank >= lo && rank < hi_) {
-              lst_idx[rank - lo] = jj * kDecThreads + tid;
-              lst_val[rank - lo] = __uint_as_float(hb[jj]);
-            }
+#pragma unroll 1
+        for (int jj = 0; jj < kpt; ++jj) {
+          const int i = jj * kDecThreads + tid;
+          const bool f = i < n && kf[i] != 0;
+          const unsigned bal = __ballot_sync(0xffffffffu, f);
+          const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
+          if (f && rank >= lo && rank < hi_) {
+            lst_idx[rank - lo] = i;
+            lst_val[rank - lo] = __uint_as_float(keys_s[i]);
           }
         }
       }
       __syncthreads();
+      DEC_T(12);
 
       // ---- gather this chunk's W_down rows ----
       const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
-      float* pout = a.part + (static_cast<size_t>(t * R + j) * CH + c) * Dp;
+      float* pout = a.part + (static_cast<size_t>(t * (CM + 1) + (routed ? q : CM)) * CH + c) * Dp;
       if (NT == 1) {
         const int g = tid / LPR, l = tid % LPR;
         const bool lane_ok = g < G;
@@ -995,70 +1025,138 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
-        if (NT == 2) {
-          float (&a2)[2][8] = reinterpret_cast<float (&)[2][8]>(acc);
-          gather_rows<2>(wb, Dp, m, lst_idx, lst_val, 1, 0, tid, true, a2);
-        } else {
-          gather_rows<4>(wb, Dp, m, lst_idx, lst_val, 1, 0, tid, true, acc);
-        }
+        gather_rows<4>(wb, Dp, m, lst_idx, lst_val, 1, 0, tid, true, acc);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           const int c8 = nt * 256 + tid;
-          if (nt < NT && c8 < LPR) {
+          if (c8 < LPR) {
             float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
             d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
             d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
           }
         }
       }
+      DEC_T(13);
       __syncthreads();  // scratch is reused by the next unit
     }
   }
   DEC_T(5);
 
   // =====================================================================================
-  // P3: grid barrier, then the ordered combine
+  // P3: grid barrier (partials + exact routing), then the ordered combine.  Each CTA owns a
+  // contiguous range of (token, 4 columns) outputs: all partials of a batch of 8 outputs are
+  // fetched at once into shared memory, summed per slot over the chunks (ascending), then over
+  // the slots (ascending, shared expert last with weight 1: router.cpp:109-132,
+  // engine.cpp:168-173).
   // =====================================================================================
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    atomicAdd(&a.ctr[kCtrP2], 1u);
-    spin_until(&a.ctr[kCtrP2], static_cast<unsigned>(grid));
-  }
-  __syncthreads();
-  DEC_T(6);
+  int* srow = reinterpret_cast<int*>(work);          // [B][R] candidate rank of every slot
+  float* swt = reinterpret_cast<float*>(work + 2048);  // [B][R] combine weights
   {
-    const int CH = a.CH;
+    const int R = K + (a.has_shared ? 1 : 0);
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&a.ctr[kCtrP2], 1u);
+      spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+    }
+    __syncthreads();
+    // slot tables (the exact routing is known now); overlaps the wait for the other CTAs
+    for (int i = tid; i < B * R; i += kDecThreads) {
+      const int t = i / R, j = i % R;
+      if (j < K) {
+        const int ee = __ldcg(a.ids + t * K + j);
+        srow[i] = rowtab[uidx[ee] * 16 + t] - t * CM;
+        swt[i] = __ldcg(a.wts + t * K + j);
+      } else {
+        srow[i] = CM;
+        swt[i] = 1.0f;
+      }
+    }
+    if (tid == 0) spin_until(&a.ctr[kCtrP2], static_cast<unsigned>(grid));
+    __syncthreads();
+    DEC_T(6);
+    const int RC = R * CH;
     const int D4 = Dp / 4;
     const int total4 = B * D4;
+    constexpr int QB = 8;
+    float4* buf = reinterpret_cast<float4*>(work + 4096);  // [QB][R][CH]
+    float4* sj = buf + QB * RC;                            // [QB][R]
     const bool y_vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
-    for (int q = tid * grid + bid; q < total4; q += grid * kDecThreads) {
-      const int t = q / D4, d4 = q % D4;
-      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      for (int j = 0; j < R; ++j) {
-        const float* pj = a.part + (static_cast<size_t>(t * R + j) * CH) * Dp + d4 * 4;
-        float4 s = __ldcg(reinterpret_cast<const float4*>(pj));
-        for (int c = 1; c < CH; ++c) {
-          const float4 pv = __ldcg(reinterpret_cast<const float4*>(pj + static_cast<size_t>(c) * Dp));
-          s.x = __fadd_rn(s.x, pv.x);
-          s.y = __fadd_rn(s.y, pv.y);
-          s.z = __fadd_rn(s.z, pv.z);
-          s.w = __fadd_rn(s.w, pv.w);
-        }
-        const float w = j < K ? __ldcg(a.wts + t * K + j) : 1.0f;
-        acc.x = __fadd_rn(acc.x, __fmul_rn(w, s.x));
-        acc.y = __fadd_rn(acc.y, __fmul_rn(w, s.y));
-        acc.z = __fadd_rn(acc.z, __fmul_rn(w, s.z));
-        acc.w = __fadd_rn(acc.w, __fmul_rn(w, s.w));
+    const int q0 = static_cast<int>(static_cast<long long>(bid) * total4 / grid);
+    const int q1 = static_cast<int>(static_cast<long long>(bid + 1) * total4 / grid);
+#pragma unroll 1
+    for (int qb = q0; qb < q1; qb += QB) {
+      const int nq = min(QB, q1 - qb);
+#pragma unroll 2
+      for (int idx = tid; idx < nq * RC; idx += kDecThreads) {
+        const int qi = idx / RC, rem = idx % RC;
+        const int j = rem / CH, c = rem % CH;
+        const int qq = qb + qi;
+        const int t = qq / D4, d4 = qq % D4;
+        const int r = srow[t * R + j];
+        buf[idx] = __ldcg(reinterpret_cast<const float4*>(
+            a.part + (static_cast<size_t>(t * (CM + 1) + r) * CH + c) * Dp + d4 * 4));
       }
-      float* yo = a.y + static_cast<size_t>(t) * D + d4 * 4;
-      if (y_vec && d4 * 4 + 3 < D) {
-        *reinterpret_cast<float4*>(yo) = acc;
-      } else {
-        if (d4 * 4 + 0 < D) yo[0] = acc.x;
-        if (d4 * 4 + 1 < D) yo[1] = acc.y;
-        if (d4 * 4 + 2 < D) yo[2] = acc.z;
-        if (d4 * 4 + 3 < D) yo[3] = acc.w;
+      __syncthreads();
+      for (int idx = tid; idx < nq * R; idx += kDecThreads) {
+        const float4* pb = buf + static_cast<size_t>(idx) * CH;
+        float4 sacc = pb[0];
+#pragma unroll 1
+        for (int c = 1; c < CH; ++c) {
+          const float4 pv = pb[c];
+          sacc.x = __fadd_rn(sacc.x, pv.x);
+          sacc.y = __fadd_rn(sacc.y, pv.y);
+          sacc.z = __fadd_rn(sacc.z, pv.z);
+          sacc.w = __fadd_rn(sacc.w, pv.w);
+        }
+        sj[idx] = sacc;
+      }
+      __syncthreads();
+      if (tid < nq) {
+        const int qq = qb + tid;
+        const int t = qq / D4, d4 = qq % D4;
+        float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll 1
+        for (int j = 0; j < R; ++j) {
+          const float w = swt[t * R + j];
+          const float4 sv = sj[tid * R + j];
+          acc.x = __fadd_rn(acc.x, __fmul_rn(w, sv.x));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(w, sv.y));
+          acc.z = __fadd_rn(acc.z, __fmul_rn(w, sv.z));
+          acc.w = __fadd_rn(acc.w, __fmul_rn(w, sv.w));
+        }
+        float* yo = a.y + static_cast<size_t>(t) * D + d4 * 4;
+        if (y_vec && d4 * 4 + 3 < D) {
+          *reinterpret_cast<float4*>(yo) = acc;
+        } else {
+          if (d4 * 4 + 0 < D) yo[0] = acc.x;
+          if (d4 * 4 + 1 < D) yo[1] = acc.y;
+          if (d4 * 4 + 2 < D) yo[2] = acc.z;
+          if (d4 * 4 + 3 < D) yo[3] = acc.w;
+        }
+      }
+      __syncthreads();
+    }
+    if (a.capture) {
+      // h in slot order for the MaskSet / activation captures of the host API
+      const int BK = B * K;
+#pragma unroll 1
+      for (int sl = bid; sl < BK + (a.has_shared ? B : 0); sl += grid) {
+        const bool rt = sl < BK;
+        const int t = rt ? sl / K : sl - BK;
+        const int ee = rt ? __ldcg(a.ids + sl) : E;
+        const int row = rt ? rowtab[uidx[ee] * 16 + t] : kDecTokens * CM + t;
+        const int n = rt ? a.N : a.S;
+        const float* src = a.hc + static_cast<size_t>(row) * a.Nh;
+        float* dst = a.h_cap + static_cast<size_t>(sl) * a.Nh;
+        for (int i = tid; i < n; i += kDecThreads) dst[i] = __ldcg(src + i);
+        if (tid == 0) {
+          a.row_expert[sl] = ee;
+          if (rt) {
+            a.inv[sl] = sl;
+            a.perm[sl] = sl;
+          }
+        }
       }
     }
   }
@@ -1071,11 +1169,12 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       a.ctr[kCtrRoute] = 0u;
       a.ctr[kCtrP2] = 0u;
       for (int i = 0; i < 4; ++i) a.ctr[kCtrChain + i] = 0u;
-      for (int i = 0; i <= kDecMaxU; ++i) a.ctr[kCtrH + i] = 0u;
+      for (int i = 0; i <= n_u; ++i) a.ctr[kCtrH + i] = 0u;
       __threadfence();
     }
   }
   DEC_T(7);
+  DEC_G(19);
 }
 
 bool decode_fused_eligible(const Geometry& g, int B) {
@@ -1090,11 +1189,11 @@ int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
   // Batch-invariant by design (B is ignored): one token's units fill the grid once.
   (void)B;
   const int R = g.K + (g.has_shared ? 1 : 0);
-  int ch = n_sms / R;
+  int ch = n_sms / (R + 1);  // room for one extra candidate per token in a single wave
   int cap = keep_max / 8;  // at least ~8 rows per unit
   if (cap < 1) cap = 1;
   if (ch > cap) ch = cap;
-  if (ch > 64) ch = 64;
+  if (ch > 32) ch = 32;  // P3 reduces the chunks of a slot across the lanes of one warp
   if (ch < 1) ch = 1;
   return ch;
 }

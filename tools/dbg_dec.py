@@ -1,0 +1,31 @@
+import ctypes as C, numpy as np, sys
+sys.path.insert(0,'/root/repo')
+import paper_2605_08575_b200 as skb
+from paper_2605_08575_b200 import _lib
+L=_lib.load()
+shape = sys.argv[1] if len(sys.argv) > 1 else "olmoe"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+shapes = {"olmoe": (64,8,2048,1024,False,0), "granite": (32,8,1024,512,False,0), "qwen": (256,8,2048,512,True,512)}
+E,K,D,N,hs,S = shapes[shape]
+cfg=skb.MoEConfig(E,K,D,N,hs,S,True,64)
+layer=skb.MoELayerWeights.generate_synthetic(cfg,1,0.05)
+x=np.random.default_rng(0).standard_normal((B,D)).astype(np.float32)
+lvl=skb.SparsityLevel(0.5)
+ref=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None,flags=skb.FLAG_NO_FUSED_DECODE)
+for i in range(3):
+    rep=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None)
+    print('launches', rep.launches, 'ref launches', ref.launches, 'maxdiff', float(np.abs(rep.outputs-ref.outputs).max()))
+    if hasattr(L, 'skb_debug_dec'):
+        out=(C.c_longlong*(160*24))()
+        L.skb_debug_dec(out)
+        t=np.array(list(out)).reshape(160,24)
+        names={14:'chain start',15:'chain end',0:'start',1:'p0 arrive',2:'p0 barrier',3:'cand done',4:'p1 done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p2 barrier',7:'exit',10:'chain done'}
+        for k in (1,2,3,14,15,10,4,8,9,11,12,13,5,6,7):
+            col=t[:148,k]-t[:148,0]
+            col=col[t[:148,k]>0]
+            if col.size: print(f'  {names[k]:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}')
+        g=t[:148,16:20]
+        g0=g[:,0].min()
+        for k,nm in enumerate(['g start','g p1 done','g p2 ready','g exit']):
+            col=g[:,k]; col=col[col>0]-g0
+            if col.size: print(f'  {nm:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d} (ns)')
