@@ -420,11 +420,17 @@ def run_ours(args):
     stages = pt.time_stages(s, stage_steps, 3)
     launches_per_step = layer.last_launches()
     mean_bytes = {k: float(np.mean([b[k] for b in bytes_ring])) for k in bytes_ring[0]}
-    dom = max(("gateup", "down"), key=lambda k: stages[k])
-    dom_bytes = mean_bytes[dom]
+    if launches_per_step == 1:
+        # decode batches: the whole layer is ONE persistent launch (decode_fused_kernel); its
+        # algorithmic bytes are the layer's, its duration the single stage the library reports
+        dom, dom_name, dom_bytes = "gateup", "decode_fused_kernel", mean_bytes["total"]
+    else:
+        dom = max(("gateup", "down"), key=lambda k: stages[k])
+        dom_name = {"gateup": "grouped_tc_kernel<TN,0> (gate/up + SwiGLU)",
+                    "down": "grouped_tc_kernel<TN,1> / down_cluster_kernel"}[dom]
+        dom_bytes = mean_bytes[dom]
     dom_gbs = dom_bytes / (stages[dom] * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "kernel": {"gateup": "gateup_swiglu_tc_kernel",
-                                            "down": "gather_down_kernel"}[dom],
+    roofline = {"bound": "hbm", "kernel": dom_name,
                 "achieved": round(dom_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(dom_gbs / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(dom_bytes),

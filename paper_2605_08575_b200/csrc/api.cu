@@ -451,7 +451,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
-                    SKB_FLAG_NO_FUSED_DECODE))) {
+                    SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE))) {
     const bool want_masks = d_mask_out_r != nullptr || d_mask_out_s != nullptr;
     DecodeLaunch dl{};
     dl.x = d_x;

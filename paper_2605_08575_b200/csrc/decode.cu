@@ -283,6 +283,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
 
   DEC_T(0);
   DEC_G(16);
+  // the P2 barrier counter is monotonic: this launch waits for base + grid.  Read first thing
+  // (nobody can have passed P0 yet); the latency hides behind the prologue.
+  unsigned p2_base = 0;
+  if (tid == 0) p2_base = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrP2]);
   // ---- prologue ----
   if (tid == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -314,17 +318,6 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   // P0: histogram zeroing, bf16 token rows, fast logits with error bounds
   // =====================================================================================
   const int hist_on = (a.sel_mode == kSelectTopk) ? 1 : 0;
-  if (hist_on) {
-    // rows [0, B*CM) routed candidates, rows [16*CM, 16*CM + B) shared expert
-    uint4* h4 = reinterpret_cast<uint4*>(a.hist);
-    const int per_row = kHistBins / 4;
-    const int n1 = B * CM * per_row;
-    const int n2 = a.has_shared ? B * per_row : 0;
-    for (int i = bid * kDecThreads + tid; i < n1 + n2; i += grid * kDecThreads) {
-      const int j = i < n1 ? i : (kDecTokens * CM * per_row + (i - n1));
-      h4[j] = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
   for (int t = (bid - E % grid + grid) % grid; t < B; t += grid) {
     const float* src = a.x + static_cast<size_t>(t) * D;
     __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
@@ -404,9 +397,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     }
   }
   __syncthreads();
-  unsigned p2_base = 0;  // the P2 barrier counter is monotonic: this launch waits for base + grid
   if (tid == 0) {
-    p2_base = ld_acquire_u32(&a.ctr[kCtrP2]);  // read before anyone can have passed P0
     __threadfence();
     fence_proxy_async_all();
     atomicAdd(&a.ctr[kCtrP0], 1u);
@@ -575,39 +566,43 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     }
     asm volatile("bar.sync 2, 192;" ::: "memory");
     const int n_u = misc[2];
-    // per token: its column of the row table, its candidate list and count
+    // The TMA warp only needs the union list: it starts streaming now.  Warps 1-5 build the
+    // per-token tables (row table column, candidate list and count) meanwhile; the MMA issuer
+    // and the epilogue warps take up their roles after barrier 3.
+    if (warp != 0) {
 #pragma unroll 1
-    for (int t = warp; t < kDecTokens; t += 6) {
-      for (int u = lane; u <= n_u; u += 32) rowtab[u * 16 + t] = -1;
-      __syncwarp();
-      if (t < B) {
-        int run = 0;
+      for (int t = warp - 1; t < kDecTokens; t += 5) {
+        for (int u = lane; u <= n_u; u += 32) rowtab[u * 16 + t] = -1;
+        __syncwarp();
+        if (t < B) {
+          int run = 0;
 #pragma unroll 1
-        for (int base = 0; base < E; base += 32) {
-          const int e = base + lane;
-          const bool f = e < E && ((cmask[e] >> t) & 1u);
-          const unsigned b = __ballot_sync(0xffffffffu, f);
-          if (f) {
-            const int r = run + __popc(b & ((1u << lane) - 1u));
-            rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * CM + r);
-            cande[t * CM + r] = static_cast<int16_t>(e);
+          for (int base = 0; base < E; base += 32) {
+            const int e = base + lane;
+            const bool f = e < E && ((cmask[e] >> t) & 1u);
+            const unsigned b = __ballot_sync(0xffffffffu, f);
+            if (f) {
+              const int r = run + __popc(b & ((1u << lane) - 1u));
+              rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * CM + r);
+              cande[t * CM + r] = static_cast<int16_t>(e);
+            }
+            run += __popc(b);
           }
-          run += __popc(b);
-        }
-        if (lane == 0) {
-          ncand[t] = run;
-          if (a.has_shared) rowtab[n_u * 16 + t] = static_cast<int16_t>(kDecTokens * CM + t);
+          if (lane == 0) {
+            ncand[t] = run;
+            if (a.has_shared) rowtab[n_u * 16 + t] = static_cast<int16_t>(kDecTokens * CM + t);
+          }
         }
       }
-    }
-    asm volatile("bar.sync 2, 192;" ::: "memory");
-    if (tid == 0) {
-      int run = 0;
-      for (int t = 0; t < B; ++t) {
-        pairoff[t] = run;
-        run += ncand[t] + (a.has_shared ? 1 : 0);
+      asm volatile("bar.sync 3, 160;" ::: "memory");
+      if (tid == 32) {
+        int run = 0;
+        for (int t = 0; t < B; ++t) {
+          pairoff[t] = run;
+          run += ncand[t] + (a.has_shared ? 1 : 0);
+        }
+        pairoff[B] = run;
       }
-      pairoff[B] = run;
     }
     DEC_T(3);
 
@@ -1159,6 +1154,20 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     }
     __syncthreads();
     DEC_T(6);
+    // the histograms were last read before the barrier: zero the rows this launch used, for
+    // the next one (they are zero after skb_layer_reserve)
+    if (hist_on) {
+    // rows [0, B*CM) routed candidates, rows [16*CM, 16*CM + B) shared expert
+    uint4* h4 = reinterpret_cast<uint4*>(a.hist);
+    const int per_row = kHistBins / 4;
+    const int n1 = B * CM * per_row;
+    const int n2 = a.has_shared ? B * per_row : 0;
+    for (int i = bid * kDecThreads + tid; i < n1 + n2; i += grid * kDecThreads) {
+      const int j = i < n1 ? i : (kDecTokens * CM * per_row + (i - n1));
+      h4[j] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    }
+
     const int RC = R * CH;
     const int D4 = Dp / 4;
     const int total4 = B * D4;

@@ -360,7 +360,7 @@ def test_invariants(skb, oracle):
         np.testing.assert_array_equal(half.outputs, whole.outputs[:3])
     half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl)
     full = skb.forward_topk_sparse(layer, x, lvl, lvl)
-    assert max_rel_diff(half.outputs, full.outputs[:3]) <= TOL_FP32_ACCUM
+    np.testing.assert_array_equal(half.outputs, full.outputs[:3])  # both: the fused decode kernel
     # PDL on/off and repeated calls are bit-identical
     again = skb.forward_topk_sparse(layer, x, skb.SparsityLevel(0.5), skb.SparsityLevel(0.5),
                                     flags=skb.FLAG_NO_PDL)
@@ -623,3 +623,125 @@ def test_ep_slices_reproduce_the_single_gpu_layer(skb, world):
         y1 = ep.ExpertParallelLayer(backs[0]).forward(xd, s, s)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(y1.cpu().numpy(), y.cpu().numpy())
+
+
+# ---------------------------------------------------------------------------------------------
+# the fused decode kernel (batches <= 16): its own edge cases
+# ---------------------------------------------------------------------------------------------
+DECODE_CASES = [
+    # E, K, D, N, S, renorm, B
+    (64, 8, 256, 256, 0, True, 1),
+    (64, 8, 256, 256, 0, True, 16),
+    (32, 8, 1024, 512, 0, True, 7),        # Granite shape
+    (128, 1, 320, 1100, 1100, True, 5),    # top-1 + shared expert, ragged N (several keys/thread)
+    (256, 8, 192, 128, 64, False, 16),     # widest router the kernel takes, raw weights
+    (16, 16, 64, 64, 0, True, 3),          # K == E: every expert is routed
+]
+
+
+@pytest.mark.parametrize("case", DECODE_CASES)
+def test_fused_decode_matches_oracle_and_staged_kernels(skb, oracle, case):
+    E, K, D, N, S, renorm, B = case
+    cfg = Config(E, K, D, N, S, renorm)
+    w, x = rounded_case(oracle, cfg, seed=E + 3 * N, scale=0.1, batch=B, token_seed=21)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True)
+    assert rep.launches <= 2, "batches <= 16 must take the single persistent launch (+ mask export)"
+    # exact routing (ids, slot order, weights) out of the chains hidden behind the stream
+    y_ref, _, cap = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if S else None,
+                                   capture=True)
+    np.testing.assert_array_equal(rep.routes.ids, cap["ids"])
+    np.testing.assert_allclose(rep.routes.weights, cap["weights"], rtol=1e-6)
+    # selection bit-exact on the device's own activations
+    for t in range(B):
+        for k in range(K):
+            np.testing.assert_array_equal(rep.masks.routed[t, k],
+                                          oracle.mask_smallest(rep.h_routed[t, k], oracle.n_off(0.5, N)))
+        if S:
+            np.testing.assert_array_equal(rep.masks.shared[t],
+                                          oracle.mask_smallest(rep.h_shared[t], oracle.n_off(0.5, S)))
+    assert max_rel_diff(rep.outputs, y_ref) <= TOL_FP32_ACCUM
+    # the staged kernels (what larger batches run) agree to the same bar
+    staged = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None,
+                                     flags=skb.FLAG_NO_FUSED_DECODE, capture=True)
+    assert staged.launches >= 3
+    np.testing.assert_array_equal(staged.routes.ids, rep.routes.ids)
+    np.testing.assert_array_equal(staged.masks.routed, rep.masks.routed)
+    assert max_rel_diff(rep.outputs, staged.outputs) <= TOL_FP32_ACCUM
+    # dense and caller-mask modes through the same kernel
+    dense = skb.forward_dense(layer, x)
+    y_dense, _ = oracle.forward(w, x)
+    assert max_rel_diff(dense.outputs, y_dense) <= TOL_FP32_ACCUM
+    masked = skb.forward_masked_dense(
+        layer, x, skb.MaskSet(rep.masks.routed, rep.masks.shared if S else None))
+    # (the row chunking follows the number of rows a mode can keep, so the two modes may differ
+    # in summation order: same survivors, same bar)
+    assert max_rel_diff(masked.outputs, rep.outputs) <= TOL_FP32_ACCUM
+
+
+def test_fused_decode_is_batch_invariant_bit_for_bit(skb, oracle):
+    # the row chunking depends on the shape only: a token's result does not depend on the batch
+    cfg = Config(32, 4, 192, 320, 96, True)
+    w, x = rounded_case(oracle, cfg, seed=5, scale=0.1, batch=16, token_seed=11)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.75)
+    whole = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
+    for b in (1, 2, 5, 9):
+        part = skb.forward_topk_sparse(layer, x[:b], lvl, lvl).outputs
+        np.testing.assert_array_equal(part, whole[:b])
+    again = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
+    np.testing.assert_array_equal(again, whole)
+
+
+def test_fused_decode_falls_back_to_exact_routing_when_the_bound_cannot_decide(skb, oracle):
+    """Identical router rows make every logit equal: the candidate bound cannot separate the
+    experts and the kernel waits for the exact routing (ties -> lowest ids, router_test.cpp:17-24).
+    Zero tokens do the same, and must give exact zeros."""
+    cfg = Config(32, 4, 128, 128, 0, True)
+    w, x = rounded_case(oracle, cfg, seed=9, scale=0.1, batch=6, token_seed=3)
+    w.router[:] = w.router[0]
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    rep = skb.forward_topk_sparse(layer, x, lvl, None, capture=True)
+    np.testing.assert_array_equal(rep.routes.ids, np.tile(np.arange(4, dtype=np.int32), (6, 1)))
+    y_ref, _, cap = oracle.forward(w, x, rep.masks.routed, None, capture=True)
+    np.testing.assert_array_equal(rep.routes.ids, cap["ids"])
+    assert max_rel_diff(rep.outputs, y_ref) <= TOL_FP32_ACCUM
+    zero = skb.forward_topk_sparse(layer, np.zeros_like(x), lvl, None, capture=True)
+    assert not zero.outputs.any()
+    np.testing.assert_array_equal(zero.routes.ids, np.tile(np.arange(4, dtype=np.int32), (6, 1)))
+    # huge logits: probabilities underflow to ties at zero, the bound steps aside as well
+    big = skb.forward_topk_sparse(layer, x * np.float32(4096.0), lvl, None, capture=True)
+    w2 = w
+    _, _, cap_big = oracle.forward(w2, x * np.float32(4096.0), big.masks.routed, None, capture=True)
+    np.testing.assert_array_equal(big.routes.ids, cap_big["ids"])
+
+
+@pytest.mark.parametrize("shape,B,s", [
+    ((64, 8, 2048, 1024, 0), 4, 0.5),       # OLMoE shape, small decode batch
+    ((32, 4, 2880, 2880, 0), 2, 0.75),      # GPT-OSS-20B shape (two column tiles per W_down row)
+    ((256, 8, 2048, 512, 512), 16, 0.9),    # Qwen3.5-35B-A3B shape, R+S
+])
+def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
+    E, K, D, N, S = shape
+    cfg = Config(E, K, D, N, S, True)
+    layer = skb.MoELayerWeights.generate_synthetic(to_cfg(skb, cfg), 1, 0.05)
+    x = oracle.round_bf16(oracle.generate_tokens(B, D, 4))
+    lvl = skb.SparsityLevel(s)
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True)
+    assert rep.launches <= 2
+    keep = N - oracle.n_off(s, N)
+    assert np.all(rep.masks.routed.sum(axis=2) == keep)
+    for t in range(B):
+        for k in range(K):
+            np.testing.assert_array_equal(
+                rep.masks.routed[t, k], oracle.mask_smallest(rep.h_routed[t, k], oracle.n_off(s, N)))
+    router = oracle.fill_symmetric(E * D, 1, 0, 0.05).reshape(E, D)
+    logits = np.stack([oracle.matvec(router, x[t]) for t in range(B)])
+    _, ids, wts = oracle.route(logits, K, True)
+    np.testing.assert_array_equal(rep.routes.ids, ids)
+    np.testing.assert_allclose(rep.routes.weights, wts, rtol=1e-6)
+    staged = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None,
+                                     flags=skb.FLAG_NO_FUSED_DECODE)
+    assert max_rel_diff(rep.outputs, staged.outputs) <= TOL_FP32_ACCUM

@@ -1,2 +1,2 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x --timeout 120 2>&1 | tail -40
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 180 2>&1 | tail -30
