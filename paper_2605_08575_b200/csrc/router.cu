@@ -147,14 +147,15 @@ __global__ void __launch_bounds__(128) route_tokens_kernel(const float* __restri
                                                            int E, int K, int renorm,
                                                            int32_t* __restrict__ ids,
                                                            float* __restrict__ weights) {
-  extern __shared__ float rt_smem[];  // [4][E + K]
+  extern __shared__ __align__(16) float rt_smem[];  // [4][round_up(E, 4) + round_up(K, 4)]
   const int warp = threadIdx.x >> 5;
   const int t = blockIdx.x * 4 + warp;
   pdl_wait();
   pdl_launch_dependents();
   if (t >= B) return;
   warp_route_token(logits + static_cast<size_t>(t) * E, E, K, renorm,
-                   rt_smem + static_cast<size_t>(warp) * (E + K), ids + static_cast<size_t>(t) * K,
+                   rt_smem + static_cast<size_t>(warp) * (round_up(E, 4) + round_up(K, 4)),
+                   ids + static_cast<size_t>(t) * K,
                    weights + static_cast<size_t>(t) * K);
 }
 
@@ -457,7 +458,7 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   if (!a.fuse_route) {
     cfg.gridDim = dim3(ceil_div(r.B, 4));
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = 4 * static_cast<size_t>(r.E + r.K) * sizeof(float);
+    cfg.dynamicSmemBytes = 4 * static_cast<size_t>(round_up(r.E, 4) + round_up(r.K, 4)) * sizeof(float);
     cudaLaunchKernelEx(&cfg, route_tokens_kernel, (const float*)r.logits, r.B, r.E, r.K, r.renorm,
                        r.ids, r.weights);
     ++launches;
