@@ -478,6 +478,20 @@ def run_ours(args):
                               "layer_frac_of_hbm_roofline":
                                   round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
                               **({"north_star_point": True} if ss == 0.5 else {})})
+            # decode batch sizes on the same shape (the single persistent launch), s = 0.5
+            for bb in (2, 4, 8, 16):
+                pb = Point(skb, torch, l2, sh, bb)
+                br = pb.bytes_for(0.5)
+                tms, _ = pb.time_device(0.5, sw_steps, 3, use_graph=not args.no_graph)
+                m = float(np.mean(tms))
+                tot = float(np.mean([b["total"] for b in br]))
+                sweep.append({"workload": sh["name"], "batch": bb, "sparsity": 0.5,
+                              "ms_per_step": round(m, 5), "tokens_per_s": round(bb / (m * 1e-3), 1),
+                              "bytes_alg": int(tot),
+                              "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                              "layer_frac_of_hbm_roofline":
+                                  round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+                del pb
             del p2, l2
 
     clocks = sampler.stop() if rank == 0 else None

@@ -93,7 +93,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void spin_until(const unsigned* p, unsigned target) {
-  while (ld_acquire_u32(p) < target) __nanosleep(32);
+  while (ld_acquire_u32(p) < target) {
+  }
 }
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
@@ -1143,7 +1144,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       }
     }
     if (tid == 0) {
-      while (ld_acquire_u32(&a.ctr[kCtrP2]) - p2_base < static_cast<unsigned>(grid)) __nanosleep(32);
+      while (ld_acquire_u32(&a.ctr[kCtrP2]) - p2_base < static_cast<unsigned>(grid)) {
+      }
       if (bid == 0) {
         // every CTA is past its last read of these: back to rest for the next forward
         a.ctr[kCtrP0] = 0u;
