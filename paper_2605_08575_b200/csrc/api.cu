@@ -232,14 +232,13 @@ int reserve_locked(skb_layer* L, int B) {
     const size_t crow = 16 * static_cast<size_t>(decode_cand_rows(g.K)) + 16;
     SKB_TRY(dmalloc(&L->d_dec_lf, 16 * static_cast<size_t>(g.E)));
     SKB_TRY(dmalloc(&L->d_dec_lm, 16 * static_cast<size_t>(g.E)));
-    SKB_TRY(dmalloc(&L->d_dec_hc, crow * g.Nh));
-    SKB_TRY(dmalloc(&L->d_dec_hist, crow * 512));
+    SKB_TRY(dmalloc(&L->d_dec_hc, 2 * crow * g.Nh));
+    SKB_CUDA(cudaMemsetAsync(L->d_dec_hc, 0, 2 * crow * g.Nh * sizeof(float), L->stream));
     SKB_TRY(dmalloc(&L->d_dec_part,
                     16 * static_cast<size_t>(decode_cand_rows(g.K) + 1) *
                         decode_chunks(g, 1, g.N > g.S ? g.N : g.S, L->n_sms) * g.Dp));
     SKB_TRY(dmalloc(&L->d_dec_ctr, static_cast<size_t>(decode_counter_words())));
     SKB_CUDA(cudaMemsetAsync(L->d_dec_ctr, 0, decode_counter_words() * sizeof(unsigned), L->stream));
-    SKB_CUDA(cudaMemsetAsync(L->d_dec_hist, 0, crow * 512 * sizeof(uint32_t), L->stream));
   }
   L->xs_rows = rows;
   SKB_TRY(dmalloc(&L->d_xs, rows * g.Dp));
@@ -473,7 +472,6 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dl.ids = L->d_ids;
     dl.wts = L->d_wts;
     dl.hc = L->d_dec_hc;
-    dl.hist = L->d_dec_hist;
     dl.part = L->d_dec_part;
     dl.ctr = L->d_dec_ctr;
     dl.y = d_y;

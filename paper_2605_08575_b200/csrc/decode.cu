@@ -96,6 +96,11 @@ __device__ __forceinline__ void spin_until(const unsigned* p, unsigned target) {
   while (ld_acquire_u32(p) < target) {
   }
 }
+__device__ __forceinline__ uint2 ld_volatile_u2(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
@@ -173,8 +178,7 @@ struct DecodeArgs {
   float* logits;
   int32_t* ids;
   float* wts;
-  float* hc;
-  uint32_t* hist;
+  uint2* hc;  // [16 * CM + 16][Nh] of {bits of h, launch epoch}: data and flag in one 8-byte word
   float* part;
   unsigned* ctr;
   float* y;
@@ -287,7 +291,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   // the P2 barrier counter is monotonic: this launch waits for base + grid.  Read first thing
   // (nobody can have passed P0 yet); the latency hides behind the prologue.
   unsigned p2_base = 0;
-  if (tid == 0) p2_base = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrP2]);
+  if (tid == 0) {
+    p2_base = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrP2]);
+    misc[3] = static_cast<int>(p2_base + 1u);
+  }
   // ---- prologue ----
   if (tid == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -314,11 +321,14 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(misc);
+  // Tag of this launch's activations: h values travel from the P1 epilogue to P2 as 8-byte
+  // {bits, epoch} words, so a consumer that reads the right epoch has the value -- no fence, no
+  // counter, no polling thread between the two phases.
+  const uint32_t epoch = static_cast<uint32_t>(misc[3]);
 
   // =====================================================================================
   // P0: histogram zeroing, bf16 token rows, fast logits with error bounds
   // =====================================================================================
-  const int hist_on = (a.sel_mode == kSelectTopk) ? 1 : 0;
   for (int t = (bid - E % grid + grid) % grid; t < B; t += grid) {
     const float* src = a.x + static_cast<size_t>(t) * D;
     __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
@@ -693,19 +703,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
               const int r = rowtab[u * 16 + col];
               if (r >= 0) {
                 const float hval = silu_f(g) * up;
-                a.hc[static_cast<size_t>(r) * a.Nh + n] = hval;
-                if (hist_on)
-                  atomicAdd(&a.hist[static_cast<size_t>(r) * kHistBins +
-                                    hist_bin(__float_as_uint(hval) & 0x7fffffffu)],
-                            1u);
+                a.hc[static_cast<size_t>(r) * a.Nh + n] = make_uint2(__float_as_uint(hval), epoch);
               }
             }
           }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == 2 && lane == 0) {
-          __threadfence();
-          atomicAdd(&a.ctr[kCtrH + u], 1u);
         }
       }
     }
@@ -745,6 +746,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     so += 1280;
     float* gred = reinterpret_cast<float*>(work + so);         // [G][Dp] <= 8 KB (NT == 1)
     so += 8192;
+    int* hist_s = reinterpret_cast<int*>(work + so);           // [kHistBins] histogram of the row
+    so += kHistBins * 4;
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(work + so); // [nmax_pad] raw bits of h
     so += nmax_pad * 4;
     uint8_t* kf = work + so;                                   // [nmax_pad] keep flags
@@ -787,7 +790,6 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             ee = cande[t * CM + q];
             u = uidx[ee];
             rr = t * CM + q;
-            spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NB));
             if (a.sel_mode == kSelectGiven) {
               // caller masks are indexed by slot: the exact routing is needed here
               if (!route_ready) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
@@ -799,7 +801,6 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             u = n_u;
             rr = kDecTokens * CM + t;
             slot = t;
-            spin_until(&a.ctr[kCtrH + u], static_cast<unsigned>(NBs));
           }
           p2[0] = rr;
           p2[1] = ee;
@@ -831,12 +832,35 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           if (n_off <= 0) mode = kSelectAll;
         }
         kpt = ceil_div(n, kDecThreads);
-        const float* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
-        uint2 hh = make_uint2(0u, 0u);
-        if (mode == kSelectTopk && n_off < n)
-          hh = __ldcg(reinterpret_cast<const uint2*>(a.hist + static_cast<size_t>(row) * kHistBins) + tid);
-#pragma unroll 4
-        for (int i = tid; i < n; i += kDecThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
+        const uint2* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
+        const bool want_hist = mode == kSelectTopk && n_off < n;
+        hist_s[2 * tid] = 0;
+        hist_s[2 * tid + 1] = 0;
+        __syncthreads();
+        // every element is read until it carries this launch's epoch (usually at once: the
+        // loads of a thread are issued back to back, four in flight)
+#pragma unroll 1
+        for (int i0 = tid; i0 < n; i0 += 4 * kDecThreads) {
+          uint2 v4[4];
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int i = i0 + u4 * kDecThreads;
+            v4[u4] = i < n ? ld_volatile_u2(hrow + i) : make_uint2(0u, epoch);
+          }
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int i = i0 + u4 * kDecThreads;
+            if (i < n) {
+              while (v4[u4].y != epoch) v4[u4] = ld_volatile_u2(hrow + i);
+              keys_s[i] = v4[u4].x;
+              if (want_hist) atomicAdd(&hist_s[hist_bin(v4[u4].x & 0x7fffffffu)], 1);
+            }
+          }
+        }
+        __syncthreads();
+        const uint2 hh = want_hist ? make_uint2(static_cast<unsigned>(hist_s[2 * tid]),
+                                                static_cast<unsigned>(hist_s[2 * tid + 1]))
+                                   : make_uint2(0u, 0u);
 
         RowPick pk{0u, 0, true};
         if (mode == kSelectAll) {
@@ -910,7 +934,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
               pk = sel_kary_pick(keys_s, n, n_off, sel_sc);
               __syncthreads();
 #pragma unroll 1
-              for (int i = tid; i < n; i += kDecThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
+              for (int i = tid; i < n; i += kDecThreads) keys_s[i] = ld_volatile_u2(hrow + i).x;
             }
           }
         }
@@ -1151,25 +1175,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         a.ctr[kCtrP0] = 0u;
         a.ctr[kCtrRoute] = 0u;
         for (int i = 0; i < 4; ++i) a.ctr[kCtrChain + i] = 0u;
-        for (int i = 0; i <= n_u; ++i) a.ctr[kCtrH + i] = 0u;
       }
     }
     __syncthreads();
     DEC_T(6);
-    // the histograms were last read before the barrier: zero the rows this launch used, for
-    // the next one (they are zero after skb_layer_reserve)
-    if (hist_on) {
-    // rows [0, B*CM) routed candidates, rows [16*CM, 16*CM + B) shared expert
-    uint4* h4 = reinterpret_cast<uint4*>(a.hist);
-    const int per_row = kHistBins / 4;
-    const int n1 = B * CM * per_row;
-    const int n2 = a.has_shared ? B * per_row : 0;
-    for (int i = bid * kDecThreads + tid; i < n1 + n2; i += grid * kDecThreads) {
-      const int j = i < n1 ? i : (kDecTokens * CM * per_row + (i - n1));
-      h4[j] = make_uint4(0u, 0u, 0u, 0u);
-    }
-    }
-
     const int RC = R * CH;
     const int D4 = Dp / 4;
     const int total4 = B * D4;
@@ -1242,9 +1251,9 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         const int ee = rt ? __ldcg(a.ids + sl) : E;
         const int row = rt ? rowtab[uidx[ee] * 16 + t] : kDecTokens * CM + t;
         const int n = rt ? a.N : a.S;
-        const float* src = a.hc + static_cast<size_t>(row) * a.Nh;
+        const uint2* src = a.hc + static_cast<size_t>(row) * a.Nh;
         float* dst = a.h_cap + static_cast<size_t>(sl) * a.Nh;
-        for (int i = tid; i < n; i += kDecThreads) dst[i] = __ldcg(src + i);
+        for (int i = tid; i < n; i += kDecThreads) dst[i] = __uint_as_float(ld_volatile_u2(src + i).x);
         if (tid == 0) {
           a.row_expert[sl] = ee;
           if (rt) {
@@ -1267,7 +1276,7 @@ bool decode_fused_eligible(const Geometry& g, int B) {
     return false;
   // the gather ring needs at least kGBatches W_down rows of shared memory (P2 scratch layout)
   const int nmax_pad = round_up(nmax, 256);
-  const int so = round_up(2 * kMaxChunkRows * 4 + 4352 + 1280 + 8192 + 5 * nmax_pad, 1024);
+  const int so = round_up(2 * kMaxChunkRows * 4 + 4352 + 1280 + 8192 + kHistBins * 4 + 5 * nmax_pad, 1024);
   return (kDecWork - so) / (g.Dp * 2) >= kGBatches;
 }
 
@@ -1326,8 +1335,7 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const C
   a.logits = d.logits;
   a.ids = d.ids;
   a.wts = d.wts;
-  a.hc = d.hc;
-  a.hist = d.hist;
+  a.hc = reinterpret_cast<uint2*>(d.hc);
   a.part = d.part;
   a.ctr = d.ctr;
   a.y = d.y;

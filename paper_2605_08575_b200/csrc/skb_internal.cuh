@@ -168,8 +168,7 @@ struct DecodeLaunch {
   float* logits;                   // [B][E] exact logits
   int32_t* ids;                    // [B][K]
   float* wts;                      // [B][K]
-  float* hc;                       // [16 * CM + 16][Nh] candidate rows
-  uint32_t* hist;                  // [16 * CM + 16][512]
+  float* hc;                       // [16 * CM + 16][Nh][2] candidate rows of {h bits, epoch} words
   float* part;                     // [B][R][CH][Dp]
   unsigned* ctr;                   // decode_counter_words() zeroed words
   float* y;                        // [B][D]
