@@ -1059,13 +1059,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       const int g = NT == 1 ? tid / LPR : 0, l = NT == 1 ? tid % LPR : tid;
       const bool lane_ok = g < G;
       for (int b = 0; b < nbatch && b < kGBatches; ++b) issue(b);
-      DEC_T(20);
 #pragma unroll 1
       for (int b = 0; b < nbatch; ++b) {
         const int pos = (gb + b) % kGBatches;
         mbar_wait(gbar(pos), ((gb + b) / kGBatches) & 1u);
-        if (b == 0) DEC_T(21);
-        if (b == 1) DEC_T(22);
         const int p0 = b * H, p1 = min(m, p0 + H);
         const uint8_t* base = rows_s + static_cast<size_t>(pos * H) * row_bytes;
         if (NT == 1) {
@@ -1101,7 +1098,6 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       }
       __syncthreads();
       gb += nbatch;
-      DEC_T(23);
       if (NT == 1) {
         if (G > 1) {
           if (lane_ok) {
