@@ -722,6 +722,8 @@ def test_fused_decode_falls_back_to_exact_routing_when_the_bound_cannot_decide(s
     ((64, 8, 2048, 1024, 0), 4, 0.5),       # OLMoE shape, small decode batch
     ((32, 4, 2880, 2880, 0), 2, 0.75),      # GPT-OSS-20B shape (two column tiles per W_down row)
     ((256, 8, 2048, 512, 512), 16, 0.9),    # Qwen3.5-35B-A3B shape, R+S
+    ((8, 1, 5120, 8192, 8192), 3, 0.9),     # Llama-4-Maverick shape with 8 of its 128 experts:
+                                            # 32 keys per thread, three column tiles per row
 ])
 def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
     E, K, D, N, S = shape

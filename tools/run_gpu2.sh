@@ -1,2 +1,2 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 180 2>&1 | tail -30
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 2>&1 | tail -30
