@@ -722,27 +722,48 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
                                                            const float* __restrict__ weights,
                                                            int B, int K, int D, int Dp,
                                                            int has_shared, float* __restrict__ y) {
+  // The token's row indices and weights first (one round trip for all slots), then the slot
+  // rows eight at a time with every load in flight before the first add: the kernel is two or
+  // three memory round trips long instead of two per slot.
+  __shared__ int32_t rs[kMaxExperts + 1];
+  __shared__ float ws[kMaxExperts + 1];
   pdl_wait();
   pdl_launch_dependents();
   const int t = blockIdx.y;
+  const int R = K + has_shared;
+  for (int s = threadIdx.x; s < R; s += blockDim.x) {
+    rs[s] = s < K ? inv[t * K + s] : B * K + t;
+    ws[s] = s < K ? weights[t * K + s] : 1.0f;
+  }
+  __syncthreads();
   const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (c4 >= D) return;
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
   const bool vec = (c4 + 3 < D);
-#pragma unroll 4
-  for (int s = 0; s < K + has_shared; ++s) {
-    const int r = s < K ? inv[t * K + s] : B * K + t;
-    const float w = s < K ? weights[t * K + s] : 1.0f;
-    const float* p = slot_out + static_cast<size_t>(r) * Dp + c4;
-    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    if (vec) {
-      const float4 q = *reinterpret_cast<const float4*>(p);
-      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-    } else {
-      for (int i = 0; i < 4; ++i) if (c4 + i < D) v[i] = p[i];
+#pragma unroll 1
+  for (int s0 = 0; s0 < R; s0 += 8) {
+    float v[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0f;
+      if (s0 + u < R) {
+        const float* p = slot_out + static_cast<size_t>(rs[s0 + u]) * Dp + c4;
+        if (vec) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+          v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+        } else {
+          for (int i = 0; i < 4; ++i) if (c4 + i < D) v[u][i] = p[i];
+        }
+      }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w, v[i]));
+    for (int u = 0; u < 8; ++u) {
+      if (s0 + u < R) {
+        const float w = ws[s0 + u];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(w, v[u][i]));
+      }
+    }
   }
   for (int i = 0; i < 4; ++i) if (c4 + i < D) y[static_cast<size_t>(t) * D + c4 + i] = acc[i];
 }

@@ -148,6 +148,31 @@ int main(int argc, char** argv) {
     }
     printf("\n");
   }
+  {
+    // L2-resident: the same 48 MB region over and over (after a warm pass it is all hits)
+    const size_t bytes = 48ull << 20;
+    const int chunk = 16384, stages = 8;
+    for (int grid : {32, 64, 148}) {
+      const size_t per_cta = bytes / grid / chunk * chunk;
+      const size_t smem = (size_t)stages * chunk + 16 * stages + 1024;
+      for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0);
+        k_ring<1><<<grid, 64, smem>>>(buf, tm, per_cta, chunk, stages, 1, 0);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (rep >= 2) report("tma2d L2-resident 48 MB", per_cta * grid, ms, grid);
+      }
+      for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0);
+        k_ldg<16><<<grid * 4, 1024>>>((const uint4*)buf, bytes / 16, sink);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (rep >= 2) report("ldg L2-resident 48 MB (4 CTAs/SM-slot)", bytes, ms, grid);
+      }
+    }
+  }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
