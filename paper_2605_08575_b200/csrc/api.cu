@@ -131,7 +131,6 @@ struct skb_layer {
   float* d_dec_lf = nullptr;
   float* d_dec_lm = nullptr;
   float* d_dec_hc = nullptr;
-  uint32_t* d_dec_hist = nullptr;
   float* d_dec_part = nullptr;
   unsigned* d_dec_ctr = nullptr;
 
@@ -153,7 +152,7 @@ void free_workspace(skb_layer* L) {
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
                   L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
                   L->d_xb,       L->disp.tile_colrow, L->d_dec_lf,    L->d_dec_lm,
-                  L->d_dec_hc,   L->d_dec_hist,  L->d_dec_part,     L->d_dec_ctr};
+                  L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -167,7 +166,6 @@ void free_workspace(skb_layer* L) {
   L->d_wts_stage = nullptr;
   L->d_xb = nullptr;
   L->d_dec_lf = L->d_dec_lm = L->d_dec_hc = L->d_dec_part = nullptr;
-  L->d_dec_hist = nullptr;
   L->d_dec_ctr = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;

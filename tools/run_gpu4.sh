@@ -1,4 +1,3 @@
-set -x
 for wl in olmoe granite; do
 timeout 300 python bench.py --workload $wl --batch 1 --no-cpu --no-sweep > gpurun_out/bench_${wl}_b1.json 2> gpurun_out/bench_${wl}_b1.err; python -c "
 import json; d=json.load(open('gpurun_out/bench_${wl}_b1.json')); print('${wl}', d['ms_per_step'], d['layer_frac_of_hbm_roofline'], d['e2e']['ms_per_step'])"
