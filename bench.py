@@ -430,9 +430,20 @@ def run_ours(args):
                     "down": "grouped_tc_kernel<TN,1> / down_cluster_kernel"}[dom]
         dom_bytes = mean_bytes[dom]
     dom_gbs = dom_bytes / (stages[dom] * 1e-3) / 1e9
+    # DRAM traffic of that kernel from the committed ncu --set full capture of this workload
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        key = f"{args.workload}:{B}:{'decode_fused' if launches_per_step == 1 else dom}"
+        if key in tr and abs(s - 0.5) < 1e-9:
+            traffic, traffic_src = int(tr[key]["bytes"]), tr[key]["capture"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "achieved": round(dom_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(dom_gbs / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                "frac": round(dom_gbs / hbm_peak, 4), "traffic": traffic,
+                "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(dom_bytes),
                 "kernel_ms": round(stages[dom], 5),
                 "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
