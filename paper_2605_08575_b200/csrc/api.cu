@@ -427,11 +427,14 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sel_mode = kSelectGiven;
   }
 
-  // Down-projection path.  Gathering surviving rows per (token, slot) moves B*K*keep rows out
-  // of L2; the dense masked GEMM reads each routed expert's W_down once from HBM.  The gather
-  // wins while a batch routes ~one token to each active expert (decode), the GEMM as soon as
-  // experts are shared by several tokens.  The decision depends only on (shape, batch, s), so
-  // it is identical for forward_dense and forward_topk_sparse at s = 0.
+  // Down-projection path of the staged kernels (batches above 16; smaller ones take the fused
+  // decode kernel).  Gathering surviving rows per (token, slot) moves B*K*keep rows through L2;
+  // the dense masked GEMM streams each routed expert's W_down once.  Measured on B200
+  // (tools/path_probe.py, L2 flushed): Qwen3.5 shape B=64 s=.5 gather 482 us / dense 353 us, s=.9
+  // 463 / 371; B=32 295 / 278; OLMoE shape B=32 261 / 232; Granite shape B=32 99 / 69 -- the
+  // gather only pays when it touches a small fraction of the rows the GEMM would stream.  The
+  // decision depends only on (shape, batch, s), so it is identical for forward_dense and
+  // forward_topk_sparse at s = 0.
   bool dense_down;
   {
     const double keep_r = sel_mode == kSelectTopk ? g.N - n_off_r : g.N;
@@ -439,7 +442,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     const double gather_rows = static_cast<double>(BK) * keep_r + (g.has_shared ? B * keep_s : 0.0);
     const double dense_rows =
         static_cast<double>(g.E < BK ? g.E : BK) * g.N + (g.has_shared ? g.S : 0.0);
-    dense_down = gather_rows > 1.5 * dense_rows;
+    dense_down = gather_rows > 0.15 * dense_rows;
     if (a->flags & SKB_FLAG_GATHER_DOWN) dense_down = false;
     if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
   }
