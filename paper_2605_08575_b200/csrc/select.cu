@@ -13,6 +13,7 @@ namespace skb {
 __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs a) {
   extern __shared__ uint32_t keys[];  // [max(N,S)]
   __shared__ SelScratch sc;
+  __shared__ __align__(16) SelHistScratch hs;
 
   const int tid = threadIdx.x;
   const int row = blockIdx.x;
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
       for (int i = tid; i < n; i += kSelectThreads)
         keys[i] = __float_as_uint(hrow[i]) & 0x7fffffffu;
       __syncthreads();
-      const RowPick pk = sel_kary_pick(keys, n, n_off, sc);
+      const RowPick pk = sel_hist_pick(keys, n, n_off, hs, sc);
       pivot = pk.pivot;
       ties_to_drop = pk.ties_to_drop;
       drop_all_ties = pk.drop_all_ties;
@@ -66,6 +67,9 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 
   // ---- ordered compaction: rounds of 256 consecutive indices ----
   int kept_base = 0, tie_base = 0, buf = 0;
+  // positions among the survivors are only needed for the survivor lists and the count: the
+  // dense down projection (masked hb) and the mask export do without the block-wide ranks
+  const bool need_pos = kidx != nullptr || a.kept_cnt != nullptr;
   // the dense down projection reads the masked row up to the K extent of its expert image
   const int kext = hb ? (routed ? a.kext_routed : a.kext_shared) : n;
   const int rounds = ceil_div(kext, kSelectThreads);
@@ -98,10 +102,13 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
         keep = valid && (k > pivot || (tie && tie_rank >= ties_to_drop));
       }
     }
-    int kept_total;
-    const int pos = kept_base + sel_block_rank(keep, sc, buf, kept_total);
-    buf ^= 1;
-    kept_base += kept_total;
+    int pos = 0;
+    if (need_pos) {
+      int kept_total;
+      pos = kept_base + sel_block_rank(keep, sc, buf, kept_total);
+      buf ^= 1;
+      kept_base += kept_total;
+    }
     if (keep && kidx) {
       kidx[pos] = i;
       if (kval) kval[pos] = hv;
