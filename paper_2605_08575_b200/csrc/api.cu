@@ -988,12 +988,26 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
       d_w_in = L->d_wts_stage;
     }
   }
-  rc = forward_core(L, a, L->d_x, L->d_y, mr, ms, a->routed_mask_out ? L->d_mask_out_r : nullptr,
+  // Small pinned (page-locked, device-mapped) output buffers are written by the last kernel
+  // directly: no device-to-host copy to launch and wait for after the layer (measured: OLMoE
+  // shape batch 1, 75.1 -> 72.2 us end to end; at 1 MB the copy engine is faster than the
+  // kernel's stores over PCIe, 166 vs 194 us, hence the size limit).
+  float* y_target = L->d_y;
+  if (B * g.D * 4 <= 64 * 1024) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, a->y) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(pa.devicePointer) & 15) == 0)
+      y_target = static_cast<float*>(pa.devicePointer);
+    else
+      cudaGetLastError();  // unregistered host memory reports an error on older drivers: not ours
+  }
+  rc = forward_core(L, a, L->d_x, y_target, mr, ms, a->routed_mask_out ? L->d_mask_out_r : nullptr,
                     (a->shared_mask_out && g.has_shared) ? L->d_mask_out_s : nullptr, s, timing,
                     d_ids_in, d_w_in, nullptr, nullptr,
                     a->h_routed_out != nullptr || a->h_shared_out != nullptr);
   if (rc) return rc;
-  SKB_CUDA(cudaMemcpyAsync(a->y, L->d_y, B * g.D * 4, cudaMemcpyDeviceToHost, s));
+  if (y_target == L->d_y)
+    SKB_CUDA(cudaMemcpyAsync(a->y, L->d_y, B * g.D * 4, cudaMemcpyDeviceToHost, s));
   if (a->ids_out) SKB_CUDA(cudaMemcpyAsync(a->ids_out, L->d_ids, BK * 4, cudaMemcpyDeviceToHost, s));
   if (a->weights_out)
     SKB_CUDA(cudaMemcpyAsync(a->weights_out, L->d_wts, BK * 4, cudaMemcpyDeviceToHost, s));

@@ -747,3 +747,18 @@ def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
     staged = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None,
                                      flags=skb.FLAG_NO_FUSED_DECODE)
     assert max_rel_diff(rep.outputs, staged.outputs) <= TOL_FP32_ACCUM
+
+
+def test_pinned_output_buffers_are_written_in_place(skb, oracle):
+    """A page-locked output buffer is the kernels' destination (no device-to-host copy): same
+    numbers as through a pageable buffer, for the fused decode kernel and the staged kernels."""
+    torch = pytest.importorskip("torch")
+    cfg = Config(16, 4, 256, 192, 64, True)
+    w, x = rounded_case(oracle, cfg, seed=2, scale=0.1, batch=40, token_seed=8)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    for b in (3, 40):
+        ref = skb.forward_topk_sparse(layer, x[:b], lvl, lvl).outputs
+        pinned = torch.zeros((b, cfg.d_model), dtype=torch.float32).pin_memory()
+        skb.forward_topk_sparse(layer, x[:b], lvl, lvl, y_out=pinned.numpy())
+        np.testing.assert_array_equal(pinned.numpy(), ref)
