@@ -473,6 +473,20 @@ def run_ours(args):
                           "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
                           "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
                           "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+        # the other batch sizes of this workload's range (configs[1]: batch 1-256), s = 0.5
+        for bb in (1, 16, 64):
+            if bb == B:
+                continue
+            pb = Point(skb, torch, layer, shape, bb)
+            br = pb.bytes_for(0.5)
+            tms, _ = pb.time_device(0.5, sw_steps, 3, use_graph=not args.no_graph)
+            m = float(np.mean(tms))
+            tot = float(np.mean([b["total"] for b in br]))
+            sweep.append({"workload": shape["name"], "batch": bb, "sparsity": 0.5,
+                          "ms_per_step": round(m, 5), "tokens_per_s": round(bb / (m * 1e-3), 1),
+                          "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                          "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+            del pb
         if args.workload != "olmoe" or B != 1:
             sh = WORKLOADS["olmoe"]
             l2 = mk_layer(sh)

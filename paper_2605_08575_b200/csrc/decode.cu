@@ -104,13 +104,6 @@ __device__ __forceinline__ uint2 ld_volatile_u2(const uint2* p) {
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
-__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
 __device__ __forceinline__ int hist_bin(uint32_t key) {
   const int b = static_cast<int>(key >> 20) - kHistBase;
   return b < 0 ? 0 : (b > kHistBins - 1 ? kHistBins - 1 : b);
@@ -729,17 +722,13 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
   const int n_u = misc[2];
   const int CH = a.CH;
   {
-    const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
-    const int n_units = pairoff[B] * CH;
+        const int n_units = pairoff[B] * CH;
     // scratch inside the (now idle) GEMM stage area, sized by the shape so that as many W_down
     // rows as possible can be in flight
     const int nmax_pad = round_up(a.N > a.S ? a.N : a.S, 256);
-    const int lst_cap = round_up(ceil_div(nmax_pad, CH), 32);
     int so = 0;
-    int32_t* lst_idx = reinterpret_cast<int32_t*>(work + so);  // [lst_cap] survivors of a chunk
-    so += lst_cap * 4;
-    float* lst_val = reinterpret_cast<float*>(work + so);      // [lst_cap]
-    so += lst_cap * 4;
+    uint16_t* lst_idx = reinterpret_cast<uint16_t*>(work + so);  // [nmax_pad] survivors of a run
+    so += nmax_pad * 2;
     uint32_t* mlist = reinterpret_cast<uint32_t*>(work + so);  // [kMemberCap + 4] pivot bucket
     so += 4352;
     int* wc = reinterpret_cast<int*>(work + so);               // [kMaxKpt * 8] + [8]
@@ -770,25 +759,30 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     const int v0 = bid < gp ? static_cast<int>(static_cast<long long>(bid) * n_units / gp) : 0;
     const int v1 = bid < gp ? static_cast<int>(static_cast<long long>(bid + 1) * n_units / gp) : 0;
 
-    int cur_pr = -1;
     int e = 0, n = 0, kpt = 0, cnt = 0, t = 0, q = 0;
     bool routed = true;
 
+    // A CTA's units are consecutive: they form RUNS of chunks [c_a, c_b) of one row.  A run
+    // selects once and streams its rows through the gather ring without draining it between
+    // chunks; every chunk still produces its own partial, so the reduction tree is the same
+    // whatever the batch (and the run boundaries) -- only the latency of a chunk is paid once
+    // per run instead of once per chunk.
 #pragma unroll 1
-    for (int v = v0; v < v1; ++v) {
-      const int c = v % CH;
+    for (int v = v0; v < v1;) {
       const int pr = v / CH;
-      if (pr != cur_pr) {
-        cur_pr = pr;
+      const int c_a = v % CH;
+      const int vb = min(v1, (pr + 1) * CH);
+      const int c_b = c_a + (vb - v);
+      v = vb;
+      {
         t = 0;
         while (t + 1 < B && pairoff[t + 1] <= pr) ++t;
         q = pr - pairoff[t];
         routed = q < ncand[t];
         if (tid == 0) {
-          int ee, u, rr, slot = -1;
+          int ee, rr, slot = -1;
           if (routed) {
             ee = cande[t * CM + q];
-            u = uidx[ee];
             rr = t * CM + q;
             if (a.sel_mode == kSelectGiven) {
               // caller masks are indexed by slot: the exact routing is needed here
@@ -798,7 +792,6 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             }
           } else {
             ee = E;
-            u = n_u;
             rr = kDecTokens * CM + t;
             slot = t;
           }
@@ -1009,10 +1002,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       }
       DEC_T(11);
 
-      // ---- survivors [lo, hi) of this chunk, ascending index ----
+      // ---- survivors of the run's chunks, ascending index: ranks [c_a * C, min(cnt, c_b * C)) ----
       const int C = ceil_div(cnt > 0 ? cnt : 1, CH);
-      const int lo = c * C;
-      const int hi_ = min(cnt, lo + C);
+      const int lo = c_a * C;
+      const int hi_ = min(cnt, c_b * C);
       const int m = hi_ > lo ? hi_ - lo : 0;
       if (m > 0) {
 #pragma unroll 1
@@ -1021,28 +1014,33 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           const bool f = i < n && kf[i] != 0;
           const unsigned bal = __ballot_sync(0xffffffffu, f);
           const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
-          if (f && rank >= lo && rank < hi_) {
-            lst_idx[rank - lo] = i;
-            lst_val[rank - lo] = __uint_as_float(keys_s[i]);
-          }
+          if (f && rank >= lo && rank < hi_) lst_idx[rank - lo] = static_cast<uint16_t>(i);
         }
       }
       __syncthreads();
       DEC_T(12);
 
-      // ---- gather this chunk's W_down rows: one 1-D bulk copy (TMA engine) per surviving row
-      // into a two-half ring in shared memory, accumulated from there ----
-      const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
-      float* pout = a.part + (static_cast<size_t>(t * (CM + 1) + (routed ? q : CM)) * CH + c) * Dp;
-      // ring of kGBatches batches of H rows, one mbarrier each; when the chunk fits (decode sizes)
-      // every row is in flight at once and the first rows are consumed while the rest arrive.
+      // ---- gather: one 1-D bulk copy (TMA engine) per surviving W_down row into a ring of
+      // kGBatches batches of H rows (one mbarrier each) in shared memory, accumulated from there.
+      // Batches never straddle a chunk; the ring runs ahead across the chunks of the run.
       // (Measured alternatives for a 32-row chunk: 32 direct 128-bit loads per thread, all in
-      // flight: 7.7 us; two-batch ring: 7.3 us; this ring: 6.9 us.)
-      const int H = max(1, min(ceil_div(m, kGBatches), n_slots / kGBatches));
-      const int nbatch = ceil_div(m, H);
-      auto issue = [&](int b) {
-        const int pos = (gb + b) % kGBatches;
-        const int p0 = b * H, p1 = min(m, p0 + H);
+      // flight: 7.7 us; two-batch ring: 7.3 us; this ring: 6.9 us.  16-byte cp.async by all
+      // threads instead of bulk copies for 2 KB rows: 106 vs 96 us at Granite shape, batch 16.)
+      const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
+      const int H = max(1, min(C, n_slots / kGBatches));
+      const int nb_c = ceil_div(C, H);                 // batches of a full chunk
+      const int n_ch = ceil_div(m, C);                 // chunks of the run that have rows
+      const int Q = n_ch > 0 ? (n_ch - 1) * nb_c + ceil_div(m - (n_ch - 1) * C, H) : 0;
+      auto batch_rows = [&](int qq, int& p0, int& p1) {
+        const int j = min(qq / nb_c, n_ch - 1);
+        const int b = qq - j * nb_c;
+        p0 = j * C + b * H;
+        p1 = min(min(m, (j + 1) * C), p0 + H);
+      };
+      auto issue = [&](int qq) {
+        const int pos = (gb + qq) % kGBatches;
+        int p0, p1;
+        batch_rows(qq, p0, p1);
         if (tid == 0) mbar_arrive_expect_tx(gbar(pos), static_cast<uint32_t>((p1 - p0) * row_bytes));
         // convergent issue: lane l of warp w copies row p0 + w + 8 * l
         for (int p = p0 + warp + 8 * lane; p < p1; p += kDecThreads)
@@ -1051,84 +1049,96 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
                         gbar(pos));
         __syncwarp();
       };
-      float acc[4][8];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
       const int g = NT == 1 ? tid / LPR : 0, l = NT == 1 ? tid % LPR : tid;
       const bool lane_ok = g < G;
-      for (int b = 0; b < nbatch && b < kGBatches; ++b) issue(b);
+      for (int qq = 0; qq < Q && qq < kGBatches; ++qq) issue(qq);
+      int qn = 0;  // next batch to consume
 #pragma unroll 1
-      for (int b = 0; b < nbatch; ++b) {
-        const int pos = (gb + b) % kGBatches;
-        mbar_wait(gbar(pos), ((gb + b) / kGBatches) & 1u);
-        const int p0 = b * H, p1 = min(m, p0 + H);
-        const uint8_t* base = rows_s + static_cast<size_t>(pos * H) * row_bytes;
-        if (NT == 1) {
-          // group g owns the rows p with p % G == g (ascending); 4 rows are loaded before their
-          // FMAs so that the shared-memory latency is paid once per 4 rows
-          if (lane_ok) {
-#pragma unroll 1
-            for (int p = p0 + ((g - p0 % G) + G) % G; p < p1; p += 4 * G) {
-              uint4 v[4];
-              float hv[4];
+      for (int j = 0; j < c_b - c_a; ++j) {
+        float acc[4][8];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int pp = p + u * G;
-                const bool ok = pp < p1;
-                hv[u] = ok ? lst_val[pp] : 0.0f;
-                v[u] = ok ? *reinterpret_cast<const uint4*>(base + static_cast<size_t>(pp - p0) * row_bytes +
-                                                           static_cast<size_t>(l) * 16)
-                          : make_uint4(0u, 0u, 0u, 0u);
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
+        const int cbase = j * C;  // first row of this chunk in the run's list
+        const int nb_j = j < n_ch ? ceil_div(min(C, m - cbase), H) : 0;
+#pragma unroll 1
+        for (int b = 0; b < nb_j; ++b, ++qn) {
+          const int pos = (gb + qn) % kGBatches;
+          mbar_wait(gbar(pos), ((gb + qn) / kGBatches) & 1u);
+          int p0, p1;
+          batch_rows(qn, p0, p1);
+          const uint8_t* base = rows_s + static_cast<size_t>(pos * H) * row_bytes;
+          if (NT == 1) {
+            // group g owns the chunk's rows r with r % G == g (ascending); 4 rows are loaded
+            // before their FMAs so that the shared-memory latency is paid once per 4 rows
+            if (lane_ok) {
+              const int r0 = p0 - cbase;
+#pragma unroll 1
+              for (int p = p0 + ((g - r0 % G) + G) % G; p < p1; p += 4 * G) {
+                uint4 v4[4];
+                float hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int pp = p + u * G;
+                  const bool ok = pp < p1;
+                  hv[u] = ok ? __uint_as_float(keys_s[lst_idx[pp]]) : 0.0f;
+                  v4[u] = ok ? *reinterpret_cast<const uint4*>(base + static_cast<size_t>(pp - p0) * row_bytes +
+                                                              static_cast<size_t>(l) * 16)
+                             : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) fma8(v4[u], hv[u], acc[0]);
               }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) fma8(v[u], hv[u], acc[0]);
             }
-          }
-        } else {
+          } else {
 #pragma unroll 2
-          for (int p = p0; p < p1; ++p)
-            consume_row<4>(base + static_cast<size_t>(p - p0) * row_bytes, lst_val[p], LPR, l, acc);
+            for (int p = p0; p < p1; ++p)
+              consume_row<4>(base + static_cast<size_t>(p - p0) * row_bytes,
+                             __uint_as_float(keys_s[lst_idx[p]]), LPR, l, acc);
+          }
+          if (qn + kGBatches < Q) {
+            __syncthreads();  // this ring position is free again
+            issue(qn + kGBatches);
+          }
         }
-        if (b + kGBatches < nbatch) {
-          __syncthreads();  // this ring position is free again
-          issue(b + kGBatches);
-        }
-      }
-      __syncthreads();
-      gb += nbatch;
-      if (NT == 1) {
-        if (G > 1) {
-          if (lane_ok) {
-            float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
+        // ---- this chunk's partial ----
+        float* pout =
+            a.part + (static_cast<size_t>(t * (CM + 1) + (routed ? q : CM)) * CH + (c_a + j)) * Dp;
+        if (NT == 1) {
+          if (G > 1) {
+            __syncthreads();  // gred of the previous chunk has been read
+            if (lane_ok) {
+              float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
+              d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+              d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+            }
+            __syncthreads();
+            for (int d = tid; d < Dp; d += kDecThreads) {
+              float sacc = gred[d];
+              for (int gg = 1; gg < G; ++gg) sacc = __fadd_rn(sacc, gred[gg * Dp + d]);
+              pout[d] = sacc;
+            }
+          } else if (lane_ok) {
+            float4* d4 = reinterpret_cast<float4*>(pout + l * 8);
             d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
             d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
           }
-          __syncthreads();
-          for (int d = tid; d < Dp; d += kDecThreads) {
-            float sacc = gred[d];
-            for (int gg = 1; gg < G; ++gg) sacc = __fadd_rn(sacc, gred[gg * Dp + d]);
-            pout[d] = sacc;
-          }
-        } else if (lane_ok) {
-          float4* d4 = reinterpret_cast<float4*>(pout + l * 8);
-          d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
-          d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
-        }
-      } else {
+        } else {
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int c8 = nt * 256 + tid;
-          if (c8 < LPR) {
-            float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
-            d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
-            d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+          for (int nt = 0; nt < 4; ++nt) {
+            const int c8 = nt * 256 + tid;
+            if (c8 < LPR) {
+              float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
+              d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
+              d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+            }
           }
         }
       }
+      gb += Q;
       DEC_T(13);
-      __syncthreads();  // scratch is reused by the next unit
+      __syncthreads();  // scratch is reused by the next run
     }
   }
   DEC_T(5);
@@ -1272,7 +1282,7 @@ bool decode_fused_eligible(const Geometry& g, int B) {
     return false;
   // the gather ring needs at least kGBatches W_down rows of shared memory (P2 scratch layout)
   const int nmax_pad = round_up(nmax, 256);
-  const int so = round_up(2 * kMaxChunkRows * 4 + 4352 + 1280 + 8192 + kHistBins * 4 + 5 * nmax_pad, 1024);
+  const int so = round_up(2 * nmax_pad + 4352 + 1280 + 8192 + kHistBins * 4 + 5 * nmax_pad, 1024);
   return (kDecWork - so) / (g.Dp * 2) >= kGBatches;
 }
 
