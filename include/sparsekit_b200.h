@@ -91,6 +91,9 @@ enum {
 #define SKB_FLAG_NO_FUSED_DECODE 0x80u /* batches <= 16: use the staged kernels instead of the
                                           single persistent decode kernel */
 
+#define SKB_FLAG_FUSED_DECODE 0x100u   /* batches <= 16: take the persistent decode kernel even where
+                                          the cost model prefers the staged kernels */
+
 #define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
 
 typedef struct skb_forward_args {

@@ -376,6 +376,24 @@ struct StageTimer {
   }
 };
 
+// Fused decode kernel or staged kernels for a batch <= 16?  Both are correct for every eligible
+// shape; which is faster depends on how much the per-(token, slot) row gather of the fused
+// kernel moves against one pass over the routed experts' W_down.  Linear models fitted to
+// measurements on B200 (tools/fused_vs_staged.py: Granite, OLMoE, Qwen3.5 and GPT-OSS shapes,
+// batches 1-16, s = 0.5; the fused model is within 5 % of every point): microseconds from MB.
+bool decode_fused_preferred(const Geometry& g, int B, double keep_r, double keep_s) {
+  const double E = g.E, K = g.K;
+  const double U = E * (1.0 - std::pow(1.0 - K / E, B));  // expected distinct routed experts
+  const double row_mb = g.Dp * 2.0 / 1e6;
+  const double gup = (U * 2.0 * g.N + (g.has_shared ? 2.0 * g.S : 0.0)) * row_mb;
+  const double vg = (B * K * keep_r + (g.has_shared ? B * keep_s : 0.0)) * row_mb;
+  const double vd = (U * g.N + (g.has_shared ? g.S : 0.0)) * row_mb;
+  const double R = K + (g.has_shared ? 1.0 : 0.0);
+  const double fused = 27.9 + 0.248 * gup + (g.Dp <= 2048 ? 0.237 : 0.519) * vg + 0.232 * B * R;
+  const double staged = 59.4 + 0.222 * gup + 0.111 * vd;
+  return fused <= 1.04 * staged;
+}
+
 // Enqueues every stage of one forward on `stream`.  x/y (and masks in MASKED mode) are device
 // pointers.  No allocation, no synchronisation.
 int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, float* d_y,
@@ -451,7 +469,10 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
-                    SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE))) {
+                    SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
+      ((a->flags & SKB_FLAG_FUSED_DECODE) ||
+       decode_fused_preferred(g, B, sel_mode == kSelectTopk ? g.N - n_off_r : g.N,
+                              sel_mode == kSelectTopk ? g.S - n_off_s : g.S))) {
     const bool want_masks = d_mask_out_r != nullptr || d_mask_out_s != nullptr;
     DecodeLaunch dl{};
     dl.x = d_x;

@@ -646,8 +646,9 @@ def test_fused_decode_matches_oracle_and_staged_kernels(skb, oracle, case):
     w, x = rounded_case(oracle, cfg, seed=E + 3 * N, scale=0.1, batch=B, token_seed=21)
     layer = make_layer(skb, w)
     lvl = skb.SparsityLevel(0.5)
-    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True)
-    assert rep.launches <= 2, "batches <= 16 must take the single persistent launch (+ mask export)"
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True,
+                                  flags=skb.FLAG_FUSED_DECODE)
+    assert rep.launches <= 2, "the single persistent launch (+ mask export)"
     # exact routing (ids, slot order, weights) out of the chains hidden behind the stream
     y_ref, _, cap = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if S else None,
                                    capture=True)
@@ -686,11 +687,12 @@ def test_fused_decode_is_batch_invariant_bit_for_bit(skb, oracle):
     w, x = rounded_case(oracle, cfg, seed=5, scale=0.1, batch=16, token_seed=11)
     layer = make_layer(skb, w)
     lvl = skb.SparsityLevel(0.75)
-    whole = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
+    f = skb.FLAG_FUSED_DECODE
+    whole = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=f).outputs
     for b in (1, 2, 5, 9):
-        part = skb.forward_topk_sparse(layer, x[:b], lvl, lvl).outputs
+        part = skb.forward_topk_sparse(layer, x[:b], lvl, lvl, flags=f).outputs
         np.testing.assert_array_equal(part, whole[:b])
-    again = skb.forward_topk_sparse(layer, x, lvl, lvl).outputs
+    again = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=f).outputs
     np.testing.assert_array_equal(again, whole)
 
 
@@ -731,7 +733,8 @@ def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
     layer = skb.MoELayerWeights.generate_synthetic(to_cfg(skb, cfg), 1, 0.05)
     x = oracle.round_bf16(oracle.generate_tokens(B, D, 4))
     lvl = skb.SparsityLevel(s)
-    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True)
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True,
+                                  flags=skb.FLAG_FUSED_DECODE)
     assert rep.launches <= 2
     keep = N - oracle.n_off(s, N)
     assert np.all(rep.masks.routed.sum(axis=2) == keep)
