@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SKB_ABI_VERSION 2
+#define SKB_ABI_VERSION 3
 
 typedef enum skb_status {
   SKB_OK = 0,
@@ -74,8 +74,12 @@ enum {
   SKB_MODE_DENSE = 0,  /* forward_dense,        engine.hpp:38-39  */
   SKB_MODE_TOPK = 1,   /* forward_masked_dense(build_topk_masks(s)) fused; skips masked W_down rows */
   SKB_MODE_MASKED = 2, /* forward_masked_dense with caller masks, engine.hpp:43-44 */
-  SKB_MODE_ROUTE_ONLY = 3 /* route_logits + route only (engine.cpp:121-122): x -> ids_out, weights_out;
-                             the home-rank half of expert parallelism */
+  SKB_MODE_ROUTE_ONLY = 3, /* route_logits + route only (engine.cpp:121-122): x -> ids_out, weights_out;
+                              the home-rank half of expert parallelism */
+  SKB_MODE_THRESHOLD = 4   /* forward_sparse, engine.hpp:46-51 / engine.cpp:229-369: a routed neuron
+                              is kept iff |silu(gate)| >= tau (threshold_mask, activation.cpp:62-72);
+                              the shared expert stays dense; ForwardReport carries the 64-neuron tile
+                              accounting of the reference (engine.cpp:341-348) */
 };
 
 /* Flags. */
@@ -126,6 +130,8 @@ typedef struct skb_forward_args {
    * pointers in SKB_MODE_ROUTE_ONLY). */
   const int32_t* ids_in;
   const float* weights_in;
+  float tau;        /* SKB_MODE_THRESHOLD: the activation threshold, >= 0 (NaN is rejected) */
+  int32_t reserved2;
 } skb_forward_args;
 
 typedef struct skb_layer skb_layer;

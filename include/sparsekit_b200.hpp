@@ -223,6 +223,17 @@ inline ForwardReport forward_masked_dense(const MoELayerWeights& w, const Matrix
   return detail::run(w, x, a);
 }
 
+// engine.hpp:46-51: the threshold runtime path.  A routed neuron is kept iff
+// |silu(gate)| >= threshold; the shared expert stays dense; the report carries the reference's
+// tile accounting (tiles_total / tiles_skipped, padded up/down MACs, path_used = kSparse).
+inline ForwardReport forward_sparse(const MoELayerWeights& w, const Matrix& x, float threshold,
+                                    int /*threads*/ = 1) {
+  skb_forward_args a{};
+  a.mode = SKB_MODE_THRESHOLD;
+  a.tau = threshold;
+  return detail::run(w, x, a);
+}
+
 // The fused top-k path.  s_shared = 0 leaves the shared expert dense (SweepMode::kRoutedOnly);
 // pass the same level as s_routed for kRoutedAndShared.
 inline ForwardReport forward_topk_sparse(const MoELayerWeights& w, const Matrix& x,

@@ -10,4 +10,4 @@ _lib.load()  # fail loudly when the CUDA library has not been built
 
 from .layer import *  # noqa: E402,F401,F403
 from .layer import (MoEConfig, MoELayerWeights, SparsityLevel, forward_dense,  # noqa: E402,F401
-                    forward_masked_dense, forward_topk_sparse)
+                    forward_masked_dense, forward_sparse, forward_topk_sparse)

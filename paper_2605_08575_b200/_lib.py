@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libsparsekit_b200.so")
 
 SKB_OK, SKB_ESHAPE, SKB_ECONFIG, SKB_EINDEX, SKB_EINTERNAL, SKB_ECUDA = range(6)
-MODE_DENSE, MODE_TOPK, MODE_MASKED, MODE_ROUTE_ONLY = 0, 1, 2, 3
+MODE_DENSE, MODE_TOPK, MODE_MASKED, MODE_ROUTE_ONLY, MODE_THRESHOLD = 0, 1, 2, 3, 4
 FLAG_FAST_ROUTER, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES, FLAG_NO_PDL = 1, 2, 4, 8
 FLAG_GATHER_DOWN, FLAG_DENSE_DOWN, FLAG_BF16_H, FLAG_NO_FUSED_DECODE = 16, 32, 64, 128
 FLAG_FUSED_DECODE = 256
@@ -53,6 +53,7 @@ class SkbForwardArgs(C.Structure):
         ("routed_mask_out", C.c_void_p), ("shared_mask_out", C.c_void_p),
         ("h_routed_out", C.c_void_p), ("h_shared_out", C.c_void_p),
         ("ids_in", C.c_void_p), ("weights_in", C.c_void_p),
+        ("tau", C.c_float), ("reserved2", C.c_int32),
     ]
 
 

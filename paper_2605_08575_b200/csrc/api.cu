@@ -115,6 +115,7 @@ struct skb_layer {
   __nv_bfloat16* d_xb = nullptr;  // decode: bf16 token rows [max(cap,16)][Dp] (token-indexed tiles)
   CUtensorMap tmap_xb{};
   float* d_h = nullptr;
+  float* d_sg = nullptr;  // silu(gate) of every row (threshold selection, forward_sparse)
   __nv_bfloat16* d_hb = nullptr;  // masked activations, [3][rows][Nh] bf16 terms
   CUtensorMap tmap_hb[5][3]{};
   float* d_slot_out = nullptr;    // [rows][Dp]
@@ -152,7 +153,7 @@ void free_workspace(skb_layer* L) {
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
                   L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
                   L->d_xb,       L->disp.tile_colrow, L->d_dec_lf,    L->d_dec_lm,
-                  L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr};
+                  L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr,      L->d_sg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
@@ -167,6 +168,7 @@ void free_workspace(skb_layer* L) {
   L->d_xb = nullptr;
   L->d_dec_lf = L->d_dec_lm = L->d_dec_hc = L->d_dec_part = nullptr;
   L->d_dec_ctr = nullptr;
+  L->d_sg = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
   L->cap_batch = 0;
 }
@@ -244,6 +246,7 @@ int reserve_locked(skb_layer* L, int B) {
   for (int i = 0; i < 5; ++i)
     SKB_TRY(encode_bf16_2d(&L->tmap_x[i], L->d_xs, rows, g.Dp, kTileCases[i]));
   SKB_TRY(dmalloc(&L->d_h, rows * g.Nh));
+  SKB_TRY(dmalloc(&L->d_sg, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_hb, 3 * rows * g.Nh));
   SKB_CUDA(cudaMemsetAsync(L->d_hb, 0, 3 * rows * g.Nh * sizeof(__nv_bfloat16), L->stream));
   for (int i = 0; i < 5; ++i)
@@ -441,6 +444,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     n_off_s = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
     const int kr = g.N - n_off_r, ks = g.S - n_off_s;
     max_keep = kr > ks ? kr : ks;
+  } else if (a->mode == SKB_MODE_THRESHOLD) {
+    sel_mode = kSelectThreshold;
   } else {
     sel_mode = kSelectGiven;
   }
@@ -463,11 +468,14 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dense_down = gather_rows > 0.15 * dense_rows;
     if (a->flags & SKB_FLAG_GATHER_DOWN) dense_down = false;
     if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
+    // threshold selection: the survivor count is data dependent; the masked GEMM covers every case
+    if (sel_mode == kSelectThreshold) dense_down = true;
   }
   const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
 
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
+      sel_mode != kSelectThreshold &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
                     SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
       ((a->flags & SKB_FLAG_FUSED_DECODE) ||
@@ -592,7 +600,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     launches += launch_gateup_simt(ctx, L->d_wgu, L->d_xs, L->disp.row_expert, rows, g, L->d_h);
   else
     launches += launch_gateup_tc(ctx, &L->tmap_w, token_tiles ? &L->tmap_xb : &L->tmap_x[tn_idx],
-                                 tn, L->disp, max_tiles, g, L->d_h, token_tiles);
+                                 tn, L->disp, max_tiles, g, L->d_h, token_tiles,
+                                 sel_mode == kSelectThreshold ? L->d_sg : nullptr);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel
@@ -615,6 +624,11 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sa.n_off_shared = n_off_s;
     sa.mask_in_routed = d_mask_r;
     sa.mask_in_shared = d_mask_s;
+    if (sel_mode == kSelectThreshold) {
+      sa.sg = L->d_sg;
+      sa.tau = a->tau;
+      sa.kept_cnt = L->d_kcnt;  // per-row survivor counts: the report's tile accounting
+    }
     if (dense_down) {
       sa.hb = L->d_hb;
       sa.hb_split_stride = static_cast<size_t>(L->xs_rows) * g.Nh;
@@ -677,7 +691,7 @@ int check_args(const skb_layer* L, const skb_forward_args* a) {
     return fail(SKB_ESHAPE, "forward: x and y must be non-null");
   if (a->batch < 1) return fail(SKB_ESHAPE, "route: empty batch");  // router.cpp:16-18
   if (a->mode != SKB_MODE_DENSE && a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_MASKED &&
-      a->mode != SKB_MODE_ROUTE_ONLY)
+      a->mode != SKB_MODE_ROUTE_ONLY && a->mode != SKB_MODE_THRESHOLD)
     return fail(SKB_ECONFIG, "forward: unknown mode %d", a->mode);
   if (a->mode == SKB_MODE_ROUTE_ONLY && (a->ids_out == nullptr || a->weights_out == nullptr))
     return fail(SKB_ESHAPE, "route-only forward: ids_out and weights_out must be non-null");
@@ -692,6 +706,12 @@ int check_args(const skb_layer* L, const skb_forward_args* a) {
         (a->shared_mask_in == nullptr ||
          a->shared_mask_len != static_cast<uint64_t>(a->batch) * static_cast<uint64_t>(g.S)))
       return fail(SKB_ESHAPE, "forward_masked_dense: shared masks must be B*d_shared");
+  }
+  if (a->mode == SKB_MODE_THRESHOLD) {
+    // engine.cpp:238-240 (NaN fails the comparison as well)
+    if (!(a->tau >= 0.0f)) return fail(SKB_ECONFIG, "forward_sparse: threshold must be >= 0");
+    if (a->flags & SKB_FLAG_SIMT_GATEUP)
+      return fail(SKB_ECONFIG, "forward_sparse: the verification gate/up kernel has no threshold mode");
   }
   if (a->mode == SKB_MODE_TOPK) {
     // SparsityLevel, activation.hpp:18-22
@@ -737,6 +757,39 @@ void fill_report(const skb_layer* L, const skb_forward_args* a, skb_report* r,
   r->active_neurons_total = active;
   r->achieved_routed_sparsity =
       1.0 - static_cast<double>(active) / static_cast<double>(routed_neurons);
+}
+
+// ForwardReport of forward_sparse (engine.cpp:341-368) from the per-row survivor counts: the
+// reference charges its gathered up/down stage in 64-neuron tiles of the compacted index list.
+void fill_report_threshold(const skb_layer* L, const skb_forward_args* a, skb_report* r,
+                           const int32_t* kcnt, const int32_t* inv) {
+  if (r == nullptr) return;
+  const Geometry& g = L->g;
+  const uint64_t B = a->batch, K = g.K, D = g.D, N = g.N, S = g.S, E = g.E;
+  std::memset(r, 0, sizeof(*r));
+  const uint64_t capacity = (K * N + 31) / 32 * 32;  // default_capacity, activation.cpp:74-77
+  const uint64_t token_tiles = (capacity + 63) / 64;   // tiles_per_token, engine.cpp:209-212
+  uint64_t active = 0, padded = 0, skipped = 0;
+  if (kcnt != nullptr) {
+    for (uint64_t t = 0; t < B; ++t) {
+      uint64_t at = 0;
+      for (uint64_t s = 0; s < K; ++s) at += static_cast<uint64_t>(kcnt[inv[t * K + s]]);
+      const uint64_t tiles = (at + 63) / 64;  // tiles_executed, engine.cpp:214-217
+      active += at;
+      padded += tiles * 64;
+      skipped += token_tiles - tiles;
+    }
+  }
+  r->gate_macs = B * K * D * N;
+  r->up_macs = padded * D;
+  r->down_macs = padded * D;
+  r->other_macs = B * E * D + (g.has_shared ? B * 3 * S * D : 0);
+  r->active_neurons_total = active;
+  r->tiles_total = B * token_tiles;
+  r->tiles_skipped = skipped;
+  r->achieved_routed_sparsity =
+      1.0 - static_cast<double>(active) / static_cast<double>(B * K * N);
+  r->path_used = 1;
 }
 
 }  // namespace
@@ -1036,6 +1089,13 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
     SKB_CUDA(cudaMemcpyAsync(a->routed_mask_out, L->d_mask_out_r, BK * g.N, cudaMemcpyDeviceToHost, s));
   if (a->shared_mask_out && g.has_shared)
     SKB_CUDA(cudaMemcpyAsync(a->shared_mask_out, L->d_mask_out_s, B * g.S, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> kcnt_host, inv_host;
+  if (a->mode == SKB_MODE_THRESHOLD) {
+    kcnt_host.resize(BK + (g.has_shared ? B : 0));
+    inv_host.resize(BK);
+    SKB_CUDA(cudaMemcpyAsync(kcnt_host.data(), L->d_kcnt, kcnt_host.size() * 4, cudaMemcpyDeviceToHost, s));
+    SKB_CUDA(cudaMemcpyAsync(inv_host.data(), L->disp.inv, BK * 4, cudaMemcpyDeviceToHost, s));
+  }
   std::vector<float> hbuf;
   std::vector<int32_t> inv;
   if (a->h_routed_out || (a->h_shared_out && g.has_shared)) {
@@ -1055,8 +1115,11 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
       std::memcpy(a->h_shared_out + t * g.S, hbuf.data() + (BK + t) * g.Nh,
                   static_cast<size_t>(g.S) * 4);
   if (timing) L->stage_ms_pending = true;
-  fill_report(L, a, report, a->routed_mask_in,
-              (a->shared_mask_len != 0) ? a->shared_mask_in : nullptr);
+  if (a->mode == SKB_MODE_THRESHOLD)
+    fill_report_threshold(L, a, report, kcnt_host.data(), inv_host.data());
+  else
+    fill_report(L, a, report, a->routed_mask_in,
+                (a->shared_mask_len != 0) ? a->shared_mask_in : nullptr);
   return SKB_OK;
 }
 
@@ -1076,7 +1139,10 @@ int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stre
                     a->mode == SKB_MODE_ROUTE_ONLY ? a->weights_out : nullptr);
   if (rc) return rc;
   if (timing) L->stage_ms_pending = true;
-  if (a->mode != SKB_MODE_ROUTE_ONLY) fill_report(L, a, report, nullptr, nullptr);
+  if (a->mode == SKB_MODE_THRESHOLD)
+    fill_report_threshold(L, a, report, nullptr, nullptr);  // data-dependent fields need the host entry
+  else if (a->mode != SKB_MODE_ROUTE_ONLY)
+    fill_report(L, a, report, nullptr, nullptr);
   return SKB_OK;
 }
 

@@ -62,6 +62,7 @@ struct TcArgs {
   const int32_t* n_tiles;
   const int32_t* tile_colrow;  // token-indexed tiles (MODE 0, TN 16): [tile][16] h row or -1
   float* out;       // MODE 0: h [rows][out_stride];  MODE 1: slot outputs [rows][out_stride]
+  float* sg_out;    // MODE 0, optional: silu(gate) [rows][out_stride] (threshold selection)
   int out_stride;
   int n_experts;
   int mblocks_routed, mblocks_shared;  // 128-row A blocks per routed expert / of the shared expert
@@ -216,7 +217,11 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
             if (col < nrows && n < m_valid) {
               const int r = (TN == 16 && a.tile_colrow != nullptr) ? a.tile_colrow[tile * 16 + col]
                                                                    : row0 + col;
-              if (r >= 0) a.out[static_cast<size_t>(r) * a.out_stride + n] = silu_f(g) * u;
+              if (r >= 0) {
+                const float sgv = silu_f(g);
+                a.out[static_cast<size_t>(r) * a.out_stride + n] = sgv * u;
+                if (a.sg_out != nullptr) a.sg_out[static_cast<size_t>(r) * a.out_stride + n] = sgv;
+              }
             }
           }
         }
@@ -279,8 +284,9 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles) {
+                     float* h, bool token_tiles, float* sg) {
   TcArgs a{};
+  a.sg_out = sg;
   a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;
   a.tile_expert = d.tile_expert;
   a.tile_row0 = d.tile_row0;

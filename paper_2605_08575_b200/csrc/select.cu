@@ -39,6 +39,13 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
                   : (a.mask_in_shared ? a.mask_in_shared + static_cast<size_t>(slot) * n : nullptr);
     if (min_ == nullptr) mode = kSelectAll;
   }
+  // threshold selection (forward_sparse): |silu(gate)| >= tau on routed rows, the shared expert
+  // stays dense (engine.cpp:352)
+  const float* sgrow = nullptr;
+  if (mode == kSelectThreshold) {
+    if (routed) sgrow = a.sg + static_cast<size_t>(row) * a.Nh;
+    else mode = kSelectAll;
+  }
 
   int n_off = 0;
   if (mode == kSelectTopk) {
@@ -84,6 +91,9 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
       if (valid) hv = hrow[i];
     } else if (mode == kSelectGiven) {
       keep = valid && (min_[i] != 0);
+      if (valid) hv = hrow[i];
+    } else if (mode == kSelectThreshold) {
+      keep = valid && fabsf(sgrow[i]) >= a.tau;
       if (valid) hv = hrow[i];
     } else if (!drop_everything) {
       uint32_t k = 0;
@@ -155,6 +165,13 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
                   : (a.mask_in_shared ? a.mask_in_shared + static_cast<size_t>(slot) * n : nullptr);
     if (min_ == nullptr) mode = kSelectAll;
   }
+  // threshold selection (forward_sparse): |silu(gate)| >= tau on routed rows, the shared expert
+  // stays dense (engine.cpp:352)
+  const float* sgrow = nullptr;
+  if (mode == kSelectThreshold) {
+    if (routed) sgrow = a.sg + static_cast<size_t>(row) * a.Nh;
+    else mode = kSelectAll;
+  }
   int n_off = 0;
   if (mode == kSelectTopk) {
     n_off = a.counts ? a.counts[row] : (routed ? a.n_off_routed : a.n_off_shared);
@@ -186,6 +203,8 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
       keep = valid;
     } else if (mode == kSelectGiven) {
       keep = valid && (min_[i] != 0);
+    } else if (mode == kSelectThreshold) {
+      keep = valid && fabsf(sgrow[i]) >= a.tau;
     } else if (drop_everything) {
       keep = false;
     } else {

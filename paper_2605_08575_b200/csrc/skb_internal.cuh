@@ -96,7 +96,7 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles);
+                     float* h, bool token_tiles, float* sg = nullptr);
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
@@ -107,12 +107,14 @@ int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __n
                        const int32_t* row_expert, int rows, const Geometry& g, float* h);
 
 // select modes
-enum { kSelectTopk = 0, kSelectAll = 1, kSelectGiven = 2 };
+enum { kSelectTopk = 0, kSelectAll = 1, kSelectGiven = 2, kSelectThreshold = 3 };
 struct SelectArgs {
   const float* h;  // [rows][Nh]
   int rows, BK, N, S, Nh, K;
   int mode;
   int n_off_routed, n_off_shared;
+  const float* sg;               // kSelectThreshold: silu(gate) [rows][Nh]; a routed neuron is kept
+  float tau;                     //   iff |sg| >= tau (activation.cpp:62-72); shared rows keep all
   const int32_t* counts;         // optional per-row n_off override (stage API), else NULL
   const int32_t* perm;           // row -> flat slot (masks are slot-major); NULL = identity
   const uint8_t* mask_in_routed; // kSelectGiven: [B*K][N] slot-major

@@ -20,7 +20,8 @@ import numpy as np
 from . import _lib
 from ._lib import (FLAG_BF16_H, FLAG_DENSE_DOWN, FLAG_FAST_ROUTER, FLAG_GATHER_DOWN,  # noqa: F401
                    FLAG_FUSED_DECODE, FLAG_NO_FUSED_DECODE, FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,
-                   MODE_DENSE, MODE_MASKED, MODE_ROUTE_ONLY, MODE_TOPK, STAGE_NAMES, SkbConfig,
+                   MODE_DENSE, MODE_MASKED, MODE_ROUTE_ONLY, MODE_THRESHOLD, MODE_TOPK, STAGE_NAMES,
+                   SkbConfig,
                    SkbForwardArgs,
                    SkbReport)
 
@@ -290,7 +291,7 @@ class MoELayerWeights:
 
 def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_shared=0.0,
              masks: Optional[MaskSet] = None, flags: int = 0, capture: bool = False,
-             y_out: Optional[np.ndarray] = None) -> ForwardReport:
+             y_out: Optional[np.ndarray] = None, tau: float = 0.0) -> ForwardReport:
     L = _lib.load()
     cfg = w.config
     x = np.ascontiguousarray(x, dtype=np.float32)
@@ -303,6 +304,7 @@ def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_share
     a = SkbForwardArgs()
     a.batch, a.mode, a.flags = B, mode, flags
     a.s_routed, a.s_shared = float(s_routed), float(s_shared)
+    a.tau = float(tau)
     a.x, a.y = x.ctypes.data, y.ctypes.data
     keep = [x, y]
     if mode == MODE_MASKED:
@@ -407,6 +409,17 @@ def forward_topk_sparse(w: MoELayerWeights, x, s_routed: SparsityLevel,
     ss = 0.0 if s_shared is None else s_shared.s
     return _forward(w, x, MODE_TOPK, s_routed=s_routed.s, s_shared=ss, flags=flags,
                     capture=capture, y_out=y_out)
+
+
+def forward_sparse(w: MoELayerWeights, x, threshold: float, threads: int = 1, *, flags: int = 0,
+                   capture: bool = False, y_out=None) -> ForwardReport:
+    """engine.hpp:46-51 / engine.cpp:229-369: a routed neuron is kept iff |silu(gate)| >= threshold
+    (threshold_mask, activation.cpp:62-72); the shared expert stays dense; the report carries
+    the reference's 64-neuron tile accounting.  `threads` is accepted and ignored."""
+    if not (threshold >= 0.0):  # also rejects NaN, like the reference's !(t >= 0)
+        raise ConfigError("forward_sparse: threshold must be >= 0")
+    return _forward(w, x, MODE_THRESHOLD, flags=flags, capture=capture, y_out=y_out,
+                    tau=float(threshold))
 
 
 def build_topk_masks(w: MoELayerWeights, tokens, s: SparsityLevel,

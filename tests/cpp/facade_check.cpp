@@ -70,6 +70,28 @@ int main() {
     std::printf("FAIL: survivor count %llu\n", static_cast<unsigned long long>(kept));
     return 1;
   }
+  // the threshold runtime path: tau = 0 keeps every neuron, a huge tau keeps none, tau < 0 throws
+  const ForwardReport thr0 = b200::forward_sparse(w, x, 0.0f);
+  const ForwardReport thr1 = b200::forward_sparse(w, x, 1e9f);
+  diff = 0.0;
+  for (std::size_t i = 0; i < thr0.outputs.data.size(); ++i)
+    diff = std::fmax(diff, std::fabs(thr0.outputs.data[i] - dense.outputs.data[i]));
+  if (diff > 1e-5 || thr0.active_neurons_total != 5u * 2u * 192u || thr0.tiles_skipped != 0 ||
+      thr1.active_neurons_total != 0 || thr1.tiles_skipped != thr1.tiles_total ||
+      thr0.path_used != ExecPath::kSparse) {
+    std::printf("FAIL: forward_sparse limits: %g\n", diff);
+    return 1;
+  }
+  bool neg = false;
+  try {
+    b200::forward_sparse(w, x, -0.5f);
+  } catch (const ConfigError&) {
+    neg = true;
+  }
+  if (!neg) {
+    std::printf("FAIL: forward_sparse accepted a negative threshold\n");
+    return 1;
+  }
   bool threw = false;
   try {
     Matrix bad(2, 64);

@@ -36,7 +36,7 @@ def test_header_symbols_are_exported(lib):
     out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True)
     exported = set(re.findall(r" T (skb_\w+)", out.stdout))
     assert exported == set(names)
-    assert L.skb_abi_version() == 2
+    assert L.skb_abi_version() == 3
 
 
 def test_library_does_not_link_the_oracle_or_torch(lib):
@@ -47,7 +47,7 @@ def test_library_does_not_link_the_oracle_or_torch(lib):
 def test_struct_layouts_match_header(lib):
     assert C.sizeof(lib.SkbConfig) == 32
     assert C.sizeof(lib.SkbReport) == 72
-    assert C.sizeof(lib.SkbForwardArgs) == 16 + 16 + 8 * 14
+    assert C.sizeof(lib.SkbForwardArgs) == 16 + 16 + 8 * 14 + 8  # + tau, reserved2 (ABI 3)
 
 
 def test_config_validate_matches_reference_messages(lib):

@@ -765,3 +765,82 @@ def test_pinned_output_buffers_are_written_in_place(skb, oracle):
         pinned = torch.zeros((b, cfg.d_model), dtype=torch.float32).pin_memory()
         skb.forward_topk_sparse(layer, x[:b], lvl, lvl, y_out=pinned.numpy())
         np.testing.assert_array_equal(pinned.numpy(), ref)
+
+
+# ---------------------------------------------------------------------------------------------
+# the threshold runtime path, forward_sparse (engine.hpp:46-51, engine.cpp:229-369)
+# ---------------------------------------------------------------------------------------------
+def _sparse_accounting(cfg, masks_routed):
+    """Closed forms of engine.cpp:341-368 from the per-slot masks."""
+    B, K, N = masks_routed.shape
+    D = cfg.d_model
+    capacity = (K * N + 31) // 32 * 32
+    token_tiles = (capacity + 63) // 64
+    active_t = masks_routed.reshape(B, -1).sum(axis=1).astype(np.int64)
+    tiles = (active_t + 63) // 64
+    return dict(active=int(active_t.sum()), padded_macs=int((tiles * 64).sum()) * D,
+                tiles_total=B * token_tiles, tiles_skipped=int((token_tiles - tiles).sum()))
+
+
+@pytest.mark.parametrize("case", [SMALL_CASES[1], SMALL_CASES[3], SMALL_CASES[4], SMALL_CASES[6]])
+@pytest.mark.parametrize("tau", [0.0, 0.02, 0.2])
+def test_forward_sparse_vs_oracle(skb, oracle, case, tau):
+    E, K, D, N, S, renorm, B = case
+    cfg = Config(E, K, D, N, S, renorm)
+    w, x = rounded_case(oracle, cfg, seed=E * 13 + N, scale=0.1, batch=B, token_seed=4)
+    layer = make_layer(skb, w)
+    rep = skb.forward_sparse(layer, x, tau, capture=True)
+    rc, y_ref, rep_ref = oracle.forward_sparse(w, x, tau)
+    assert rc == 0
+    # masks: |silu(gate)| >= tau with the gate of the oracle's own fp32 matvec; values within
+    # float noise of tau may land on either side (the bar of the north star: >= 99.9 %)
+    ref_masks = np.zeros((B, K, N), np.uint8)
+    _, _, cap = oracle.forward(w, x, capture=True)
+    for t in range(B):
+        for k in range(K):
+            e = cap["ids"][t, k]
+            g = oracle.matvec(w.gate[e], x[t])
+            ref_masks[t, k] = oracle.threshold_mask(g, tau)[1]
+    np.testing.assert_array_equal(rep.routes.ids, cap["ids"])
+    agree = np.mean(rep.masks.routed == ref_masks)
+    assert agree >= MASK_AGREEMENT, agree
+    if S:
+        assert rep.masks.shared.all()  # the shared expert stays dense (engine.cpp:352)
+    # outputs: the oracle's masked-dense layer on the device's masks isolates the arithmetic
+    y_same, _ = oracle.forward(w, x, rep.masks.routed, None)
+    assert max_rel_diff(rep.outputs, y_same) <= TOL_FP32_ACCUM
+    assert max_rel_diff(rep.outputs, y_ref) <= (TOL_FP32_ACCUM if agree == 1.0 else TOL_BF16)
+    # accounting: the reference's closed forms on the device's masks; equal to the reference's
+    # report when the masks agree
+    acc = _sparse_accounting(cfg, rep.masks.routed)
+    assert rep.active_neurons_total == acc["active"]
+    assert rep.macs.up_macs == acc["padded_macs"] and rep.macs.down_macs == acc["padded_macs"]
+    assert rep.macs.gate_macs == B * K * D * N
+    assert rep.tiles_total == acc["tiles_total"] and rep.tiles_skipped == acc["tiles_skipped"]
+    assert rep.path_used == 1
+    if agree == 1.0:
+        assert rep.active_neurons_total == rep_ref.active_neurons_total
+        assert rep.macs.up_macs == rep_ref.up_macs and rep.macs.other_macs == rep_ref.other_macs
+        assert rep.tiles_total == rep_ref.tiles_total and rep.tiles_skipped == rep_ref.tiles_skipped
+
+
+def test_forward_sparse_limits_and_errors(skb, oracle):
+    # engine_test.cpp:191-218: tau = 0 is the dense layer, a huge tau leaves the shared expert
+    cfg = Config(8, 2, 96, 160, 48, True)
+    w, x = rounded_case(oracle, cfg, seed=3, scale=0.1, batch=21, token_seed=5)
+    layer = make_layer(skb, w)
+    dense = skb.forward_dense(layer, x)
+    zero = skb.forward_sparse(layer, x, 0.0)
+    assert max_rel_diff(zero.outputs, dense.outputs) <= TOL_FP32_ACCUM
+    assert zero.active_neurons_total == 21 * 2 * 160 and zero.tiles_skipped == 0
+    huge = skb.forward_sparse(layer, x, 1e9)
+    y_ref, _ = oracle.forward(w, x, np.zeros((21, 2, 160), np.uint8), None)
+    assert max_rel_diff(huge.outputs, y_ref) <= TOL_FP32_ACCUM
+    assert huge.active_neurons_total == 0 and huge.tiles_skipped == huge.tiles_total
+    for bad in (-1.0, float("nan")):
+        with pytest.raises(skb.ConfigError):
+            skb.forward_sparse(layer, x, bad)
+    # small batches take the same (staged) kernels
+    one = skb.forward_sparse(layer, x[:1], 0.05, capture=True)
+    y_same, _ = oracle.forward(w, x[:1], one.masks.routed, None)
+    assert max_rel_diff(one.outputs, y_same) <= TOL_FP32_ACCUM
