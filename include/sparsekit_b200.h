@@ -234,6 +234,12 @@ int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask);
 /* round-half-up count used by topk_mask (host arithmetic, no device needed). */
 int skb_n_off(double s, int n, int32_t* out);
 
+/* generate_tokens(), proj/src/model.cpp:168-178 over SplitMix64::next_gaussian
+ * (proj/include/sparsekit/rng.hpp:42-55): batch*d_model standard normals, Box-Muller in double
+ * (pairs: cos value first, the sin value on the next draw), cast to float.  Host arithmetic with
+ * the host's libm, no device needed; used by profile_tipping for its probe batches. */
+int skb_generate_tokens(int32_t batch, int32_t d_model, uint64_t seed, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,10 @@
 #include "sparsekit_b200_types.hpp"
 #endif
 
+#include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -255,6 +258,83 @@ inline MaskSet build_topk_masks(const MoELayerWeights& w, const Matrix& tokens, 
   forward_topk_sparse(w, tokens, s, rs ? s : SparsityLevel(0.0), 1, &m);
   if (!rs) m.shared.clear();
   return m;
+}
+
+// model.cpp:168-178: the standard-normal token batch profile_tipping probes with (host libm,
+// bit-identical to the reference's generate_tokens on the same host).
+inline Matrix generate_tokens(int batch, int d_model, std::uint64_t seed) {
+  if (batch < 1 || d_model < 1) throw ConfigError("token batch needs batch >= 1 and d_model >= 1");
+  Matrix x(batch, d_model);
+  detail::check(skb_generate_tokens(batch, d_model, seed, x.data.data()));
+  return x;
+}
+
+// Wall clock around the synchronous host entry points (each returns after its device work and
+// the copy back have completed, so host time IS layer time as a caller sees it).
+class SteadyClock final : public Stopwatch {
+ public:
+  double now_ms() override {
+    using clock = std::chrono::steady_clock;
+    return std::chrono::duration<double, std::milli>(clock::now().time_since_epoch()).count();
+  }
+};
+
+namespace detail {
+inline double median(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  const std::size_t n = v.size();
+  return n % 2 == 1 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+}  // namespace detail
+
+// engine.hpp:76-83, engine.cpp:371-412: smallest batch of the (ascending) grid whose dense median
+// is at or below the sparse median, else kSparseAlways.  Per grid point: `repetitions` sparse
+// runs, then `repetitions` dense runs, one now_ms() before and one after each; probe tokens are
+// generate_tokens(batch, d_model, token_seed + grid index).  Grid: any contiguous int container
+// (std::vector, std::array, std::span).
+template <class Grid>
+inline SwitchTable profile_tipping(const MoELayerWeights& w, float threshold, const Grid& batch_grid,
+                                   int repetitions = 5, Stopwatch* clock = nullptr,
+                                   std::uint64_t token_seed = 0) {
+  const std::size_t n_grid = batch_grid.size();
+  if (n_grid == 0) throw ConfigError("profile_tipping: empty batch grid");
+  const int* grid = batch_grid.data();
+  for (std::size_t i = 0; i < n_grid; ++i)
+    if (grid[i] < 1 || (i > 0 && grid[i] <= grid[i - 1]))
+      throw ConfigError("profile_tipping: grid must be ascending, >= 1");
+  if (repetitions < 1) throw ConfigError("profile_tipping: repetitions must be >= 1");
+  SteadyClock own;
+  if (clock == nullptr) clock = &own;
+  for (std::size_t gi = 0; gi < n_grid; ++gi) {
+    const Matrix tokens = b200::generate_tokens(grid[gi], w.config.d_model, token_seed + gi);
+    std::vector<double> sparse_ms, dense_ms;
+    for (int r = 0; r < repetitions; ++r) {
+      const double t0 = clock->now_ms();
+      b200::forward_sparse(w, tokens, threshold);
+      sparse_ms.push_back(clock->now_ms() - t0);
+    }
+    for (int r = 0; r < repetitions; ++r) {
+      const double t0 = clock->now_ms();
+      b200::forward_dense(w, tokens);
+      dense_ms.push_back(clock->now_ms() - t0);
+    }
+    if (detail::median(dense_ms) <= detail::median(sparse_ms))
+      return SwitchTable{static_cast<std::size_t>(grid[gi])};
+  }
+  return SwitchTable{SwitchTable::kSparseAlways};
+}
+
+inline SwitchTable profile_tipping(const MoELayerWeights& w, float threshold,
+                                   std::initializer_list<int> batch_grid, int repetitions = 5,
+                                   Stopwatch* clock = nullptr, std::uint64_t token_seed = 0) {
+  return profile_tipping(w, threshold, std::vector<int>(batch_grid), repetitions, clock, token_seed);
+}
+
+// engine.hpp:85-89, engine.cpp:414-420
+inline ForwardReport step(const MoELayerWeights& w, const Matrix& x, float threshold,
+                          const SwitchTable& table, int threads = 1) {
+  if (table.use_dense(static_cast<std::size_t>(x.rows))) return b200::forward_dense(w, x, threads);
+  return b200::forward_sparse(w, x, threshold, threads);
 }
 
 // router.hpp:34

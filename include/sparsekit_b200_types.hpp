@@ -8,6 +8,7 @@
 //   RouteResult / DispatchPlan    proj/include/sparsekit/router.hpp:20-44
 //   SparsityLevel                 proj/include/sparsekit/activation.hpp:15-23
 //   ForwardReport / MaskSet       proj/include/sparsekit/engine.hpp:19-34
+//   SwitchTable / Stopwatch       proj/include/sparsekit/engine.hpp:52-69
 //   SweepMode                     proj/include/sparsekit/profiler.hpp:38
 //   exception types               proj/include/sparsekit/errors.hpp:12-43
 // so that code written against the reference compiles against either.
@@ -15,6 +16,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <limits>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -96,6 +98,20 @@ struct ForwardReport {
 
 struct MaskSet {
   std::vector<std::uint8_t> routed, shared;
+};
+
+// batches of at least tipping_batch run dense; kSparseAlways = never
+struct SwitchTable {
+  static constexpr std::size_t kSparseAlways = std::numeric_limits<std::size_t>::max();
+  std::size_t tipping_batch = kSparseAlways;
+  bool use_dense(std::size_t batch) const { return batch >= tipping_batch; }
+};
+
+// injectable monotonic clock (milliseconds)
+class Stopwatch {
+ public:
+  virtual ~Stopwatch() = default;
+  virtual double now_ms() = 0;
 };
 
 }  // namespace sparsekit

@@ -25,7 +25,7 @@ EXPORTS = (
     "skb_layer_set_router", "skb_layer_destroy", "skb_layer_reserve",
     "skb_layer_forward", "skb_layer_forward_device", "skb_layer_stage_times",
     "skb_layer_last_launches", "skb_layer_weight_bytes", "skb_route", "skb_align_dispatch",
-    "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off",
+    "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off", "skb_generate_tokens",
 )
 
 
@@ -98,5 +98,6 @@ def load() -> C.CDLL:
     L.skb_mask_smallest.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp]
     L.skb_topk_mask.argtypes = [vp, C.c_int, C.c_int, C.c_double, vp]
     L.skb_n_off.argtypes = [C.c_double, C.c_int, C.POINTER(i32)]
+    L.skb_generate_tokens.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp]
     _lib = L
     return L

@@ -817,6 +817,32 @@ int skb_n_off(double s, int n, int32_t* out) {
   return SKB_OK;
 }
 
+int skb_generate_tokens(int32_t batch, int32_t d_model, uint64_t seed, float* out) {
+  if (batch < 1 || d_model < 1)
+    return fail(SKB_ECONFIG, "token batch needs batch >= 1 and d_model >= 1");
+  if (out == nullptr) return fail(SKB_ESHAPE, "generate_tokens: null output");
+  uint64_t state = seed;
+  auto unit = [&state]() {  // SplitMix64 step, top 53 bits as a double in [0, 1)
+    uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return static_cast<double>(z >> 11) * 0x1.0p-53;
+  };
+  const size_t n = static_cast<size_t>(batch) * static_cast<size_t>(d_model);
+  for (size_t i = 0; i < n; i += 2) {
+    double u1 = unit();
+    const double u2 = unit();
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
+    const double second = radius * std::sin(angle);
+    out[i] = static_cast<float>(radius * std::cos(angle));
+    if (i + 1 < n) out[i + 1] = static_cast<float>(second);
+  }
+  return SKB_OK;
+}
+
 int skb_layer_create(const skb_config* cfg, const float* router, const float* const* gate,
                      const float* const* up, const float* const* down_t, const float* shared_gate,
                      const float* shared_up, const float* shared_down_t, int device,

@@ -12,6 +12,7 @@ Every function runs on the GPU through libsparsekit_b200.so; nothing here comput
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -420,6 +421,87 @@ def forward_sparse(w: MoELayerWeights, x, threshold: float, threads: int = 1, *,
         raise ConfigError("forward_sparse: threshold must be >= 0")
     return _forward(w, x, MODE_THRESHOLD, flags=flags, capture=capture, y_out=y_out,
                     tau=float(threshold))
+
+
+# ---- the dense/sparse switch (engine.hpp:52-89, engine.cpp:371-420) ---------------------------
+SPARSE_ALWAYS = (1 << 64) - 1  # SwitchTable::kSparseAlways
+
+
+@dataclass
+class SwitchTable:
+    """Batches of at least `tipping_batch` take the dense path (engine.hpp:54-61)."""
+    tipping_batch: int = SPARSE_ALWAYS
+
+    def use_dense(self, batch: int) -> bool:
+        return batch >= self.tipping_batch
+
+
+class Stopwatch:
+    """Injectable monotonic clock in milliseconds (engine.hpp:63-69)."""
+
+    def now_ms(self) -> float:
+        raise NotImplementedError
+
+
+class SteadyStopwatch(Stopwatch):
+    """Host wall clock; the forward entry points return after their device work and the copy
+    back, so host time is layer time as the caller sees it."""
+
+    def now_ms(self) -> float:
+        return time.perf_counter() * 1e3
+
+
+def generate_tokens(batch: int, d_model: int, seed: int) -> np.ndarray:
+    """model.cpp:168-178: standard normals by Box-Muller over SplitMix64 (host libm)."""
+    x = np.empty((max(batch, 0), max(d_model, 0)), np.float32)
+    _check(_lib.load().skb_generate_tokens(batch, d_model, seed & ((1 << 64) - 1), _ptr(x)))
+    return x
+
+
+def _median(values):
+    v = sorted(values)
+    n = len(v)
+    return v[n // 2] if n % 2 else 0.5 * (v[n // 2 - 1] + v[n // 2])
+
+
+def profile_tipping(w: MoELayerWeights, threshold: float, batch_grid, repetitions: int = 5,
+                    clock: Optional[Stopwatch] = None, token_seed: int = 0) -> SwitchTable:
+    """engine.cpp:371-412: the smallest batch of the ascending grid whose dense median is at or
+    below the sparse median, else kSparseAlways.  Per grid point `repetitions` sparse runs then
+    `repetitions` dense runs, one now_ms() before and after each."""
+    grid = [int(b) for b in batch_grid]
+    if not grid:
+        raise ConfigError("profile_tipping: empty batch grid")
+    for i, b in enumerate(grid):
+        if b < 1 or (i > 0 and b <= grid[i - 1]):
+            raise ConfigError("profile_tipping: grid must be ascending, >= 1")
+    if repetitions < 1:
+        raise ConfigError("profile_tipping: repetitions must be >= 1")
+    clock = clock or SteadyStopwatch()
+    for gi, batch in enumerate(grid):
+        tokens = generate_tokens(batch, w.config.d_model, token_seed + gi)
+        sparse_ms, dense_ms = [], []
+        for _ in range(repetitions):
+            t0 = clock.now_ms()
+            forward_sparse(w, tokens, threshold)
+            sparse_ms.append(clock.now_ms() - t0)
+        for _ in range(repetitions):
+            t0 = clock.now_ms()
+            forward_dense(w, tokens)
+            dense_ms.append(clock.now_ms() - t0)
+        if _median(dense_ms) <= _median(sparse_ms):
+            return SwitchTable(batch)
+    return SwitchTable(SPARSE_ALWAYS)
+
+
+def step(w: MoELayerWeights, x, threshold: float, table: SwitchTable,
+         threads: int = 1) -> ForwardReport:
+    """engine.cpp:414-420: forward_dense when the table says so for this batch, else
+    forward_sparse."""
+    rows = np.asarray(x).shape[0]
+    if table.use_dense(rows):
+        return forward_dense(w, x, threads)
+    return forward_sparse(w, x, threshold, threads)
 
 
 def build_topk_masks(w: MoELayerWeights, tokens, s: SparsityLevel,

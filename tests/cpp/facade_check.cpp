@@ -92,6 +92,41 @@ int main() {
     std::printf("FAIL: forward_sparse accepted a negative threshold\n");
     return 1;
   }
+  // the dense/sparse switch (engine_test.cpp:355-408): scripted clock, then step()
+  struct Scripted final : Stopwatch {
+    std::vector<double> durations;
+    std::size_t calls = 0;
+    double t = 0.0;
+    explicit Scripted(std::vector<double> d) : durations(std::move(d)) {}
+    double now_ms() override {
+      if (calls % 2 == 1) t += durations[calls / 2];
+      ++calls;
+      return t;
+    }
+  };
+  {
+    const std::vector<int> grid = {1, 2};
+    Scripted never({1.0, 2.0, 1.0, 2.0}), second({1.0, 2.0, 2.0, 2.0}), med({1.0, 9.0, 1.0, 0.5, 0.6, 20.0});
+    const std::vector<int> single = {4};
+    if (b200::profile_tipping(w, 0.01f, grid, 1, &never, 0).tipping_batch != SwitchTable::kSparseAlways ||
+        b200::profile_tipping(w, 0.01f, grid, 1, &second, 0).tipping_batch != 2 ||
+        b200::profile_tipping(w, 0.01f, single, 3, &med, 0).tipping_batch != 4 || med.calls != 12) {
+      std::printf("FAIL: profile_tipping with scripted timings\n");
+      return 1;
+    }
+    bool empty_thrown = false;
+    try {
+      b200::profile_tipping(w, 0.01f, {}, 1, nullptr, 0);
+    } catch (const ConfigError&) {
+      empty_thrown = true;
+    }
+    if (!empty_thrown || b200::step(w, x, 0.01f, SwitchTable{6}).path_used != ExecPath::kSparse ||
+        b200::step(w, x, 0.01f, SwitchTable{5}).path_used != ExecPath::kDense ||
+        b200::step(w, x, 0.01f, SwitchTable{}).path_used != ExecPath::kSparse) {
+      std::printf("FAIL: step() / empty grid\n");
+      return 1;
+    }
+  }
   bool threw = false;
   try {
     Matrix bad(2, 64);

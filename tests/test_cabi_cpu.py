@@ -167,3 +167,20 @@ def test_cpp_facade_compiles_against_the_reference_headers():
            "-I", "/root/reference/proj/include", FACADE_SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
+
+
+# ---------------------------------------------------------------------------------------------
+# host-side pieces of the dense/sparse switch (no device needed)
+# ---------------------------------------------------------------------------------------------
+def test_generate_tokens_matches_the_oracle_bit_for_bit(lib):
+    """skb_generate_tokens vs the oracle's restatement of model.cpp:168-178 / rng.hpp:42-55."""
+    from oracle.pyoracle import Oracle
+    ork = Oracle.get()
+    L = lib.load()
+    for batch, d, seed in [(1, 1, 0), (3, 7, 2), (4, 96, 9), (16, 2048, 3), (5, 33, (1 << 64) - 1)]:
+        out = np.empty((batch, d), np.float32)
+        assert L.skb_generate_tokens(batch, d, seed, out.ctypes.data) == 0
+        ref = ork.generate_tokens(batch, d, seed)
+        assert out.tobytes() == np.asarray(ref, np.float32).tobytes()
+    assert L.skb_generate_tokens(0, 8, 1, None) == 2  # ConfigError, model.cpp:169-171
+    assert b"batch >= 1" in L.skb_last_error()

@@ -844,3 +844,53 @@ def test_forward_sparse_limits_and_errors(skb, oracle):
     one = skb.forward_sparse(layer, x[:1], 0.05, capture=True)
     y_same, _ = oracle.forward(w, x[:1], one.masks.routed, None)
     assert max_rel_diff(one.outputs, y_same) <= TOL_FP32_ACCUM
+
+
+# ---------------------------------------------------------------------------------------------
+# the dense/sparse switch: profile_tipping / step (engine_test.cpp:355-408)
+# ---------------------------------------------------------------------------------------------
+class _ScriptedClock:
+    """One scripted duration per timed run: now_ms() is called once before and once after."""
+
+    def __init__(self, durations):
+        self.durations, self.calls, self.t = list(durations), 0, 0.0
+
+    def now_ms(self):
+        if self.calls % 2 == 1:
+            self.t += self.durations[self.calls // 2]
+        self.calls += 1
+        return self.t
+
+
+def test_profile_tipping_with_scripted_timings(skb, oracle):
+    cfg = Config(8, 2, 96, 160, 48, True)
+    w, _ = rounded_case(oracle, cfg, seed=29, scale=0.1, batch=1, token_seed=1)
+    layer = make_layer(skb, w)
+    tip = lambda grid, reps, d: skb.profile_tipping(layer, 0.01, grid, reps, _ScriptedClock(d), 0)
+    assert tip([1, 2], 1, [1.0, 2.0, 1.0, 2.0]).tipping_batch == skb.SPARSE_ALWAYS
+    assert tip([1, 2], 1, [1.0, 2.0, 2.0, 2.0]).tipping_batch == 2
+    assert tip([8], 1, [5.0, 4.0]).tipping_batch == 8
+    # medians decide: sparse 1, 9, 1 -> 1; dense 0.5, 0.6, 20 -> 0.6
+    clock = _ScriptedClock([1.0, 9.0, 1.0, 0.5, 0.6, 20.0])
+    assert skb.profile_tipping(layer, 0.01, [4], 3, clock, 0).tipping_batch == 4
+    assert clock.calls == 12  # `repetitions` sparse runs then `repetitions` dense runs, 2 reads each
+    for bad in ([], [4, 2], [0, 1], [2, 2]):
+        with pytest.raises(skb.ConfigError):
+            skb.profile_tipping(layer, 0.01, bad, 1, None, 0)
+    with pytest.raises(skb.ConfigError):
+        skb.profile_tipping(layer, 0.01, [1], 0, None, 0)
+    # the real clock returns a table of the right type on a real grid
+    real = skb.profile_tipping(layer, 0.01, [1, 4], 2)
+    assert real.tipping_batch in (1, 4, skb.SPARSE_ALWAYS)
+
+
+def test_step_obeys_the_tipping_rule(skb, oracle):
+    cfg = Config(8, 2, 96, 160, 48, True)
+    w, _ = rounded_case(oracle, cfg, seed=31, scale=0.1, batch=1, token_seed=1)
+    layer = make_layer(skb, w)
+    x = skb.generate_tokens(4, cfg.d_model, 9)
+    assert x.tobytes() == np.asarray(oracle.generate_tokens(4, cfg.d_model, 9), np.float32).tobytes()
+    assert skb.step(layer, x, 0.01, skb.SwitchTable(5)).path_used == 1
+    assert skb.step(layer, x, 0.01, skb.SwitchTable(4)).path_used == 0
+    assert skb.step(layer, x, 0.01, skb.SwitchTable(1)).path_used == 0
+    assert skb.step(layer, x, 0.01, skb.SwitchTable()).path_used == 1
