@@ -139,9 +139,13 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 }
 
 // One warp per row, 8 rows per CTA, keys and values in registers (rows of up to 1024 neurons).
-// Same outputs as select_rows_kernel, bit for bit; no block barriers.
+// Lane l owns the NPL consecutive neurons [l * NPL, (l + 1) * NPL): 128-bit loads and stores,
+// index order = (lane, j) order, so tie ranks and survivor positions come from one warp scan of
+// per-lane counts instead of a ballot per element.  Same outputs as select_rows_kernel, bit for
+// bit; no block barriers.
 template <int NPL>
 __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(SelectArgs a) {
+  __shared__ uint32_t pick_scratch[kSelWarps][36];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x * kSelWarps + warp;
   pdl_wait();
@@ -179,59 +183,108 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
   }
   const bool drop_everything = (mode == kSelectTopk) && n_off >= n;  // activation.cpp:36-39
 
+  const int i0 = lane * NPL;
+  const bool vec = (a.Nh & 3) == 0;  // rows start 16-byte aligned
+  auto load_row = [&](const float* src, float (&dst)[NPL]) {
+#pragma unroll
+    for (int v = 0; v < NPL; v += 4) {
+      if (vec && i0 + v + 4 <= n) {
+        const float4 q = *reinterpret_cast<const float4*>(src + i0 + v);
+        dst[v] = q.x;
+        dst[v + 1] = q.y;
+        dst[v + 2] = q.z;
+        dst[v + 3] = q.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[v + q] = (i0 + v + q < n) ? src[i0 + v + q] : 0.0f;
+      }
+    }
+  };
   float hv[NPL];
-  uint32_t kr[NPL];
+  load_row(hrow, hv);
+  unsigned keepbits = 0u;  // bit j: neuron i0 + j survives
+  if (mode == kSelectAll) {
 #pragma unroll
-  for (int j = 0; j < NPL; ++j) {
-    const int i = j * 32 + lane;
-    hv[j] = (i < n) ? hrow[i] : 0.0f;
-    kr[j] = (i < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
+    for (int j = 0; j < NPL; ++j) keepbits |= (i0 + j < n) ? (1u << j) : 0u;
+  } else if (mode == kSelectGiven) {
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) keepbits |= (i0 + j < n && min_[i0 + j] != 0) ? (1u << j) : 0u;
+  } else if (mode == kSelectThreshold) {
+    float sg[NPL];
+    load_row(sgrow, sg);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      keepbits |= (i0 + j < n && fabsf(sg[j]) >= a.tau) ? (1u << j) : 0u;
+  } else if (!drop_everything) {
+    uint32_t kr[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      kr[j] = (i0 + j < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
+    const RowPick pk = warp_binary_pick<NPL>(kr, n, n_off, pick_scratch[warp]);
+    int my_ties = 0;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) my_ties += (kr[j] == pk.pivot) ? 1 : 0;
+    int tie_rank = warp_excl_scan(my_ties);  // ties at lower indices
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const bool tie = kr[j] == pk.pivot;
+      const bool above = kr[j] > pk.pivot && kr[j] != 0xffffffffu;
+      keepbits |= (above || (tie && tie_rank >= pk.ties_to_drop)) ? (1u << j) : 0u;
+      tie_rank += tie ? 1 : 0;
+    }
   }
-  RowPick pk{0u, 0, true};
-  if (mode == kSelectTopk && !drop_everything) pk = warp_binary_pick<NPL>(kr, n_off);
 
-  const int kext = hb ? (routed ? a.kext_routed : a.kext_shared) : n;
-  const unsigned lt = (1u << lane) - 1u;
-  int kept_base = 0, tie_base = 0;
+  const int my_kept = __popc(keepbits);
+  if (kidx) {
+    int pos = warp_excl_scan(my_kept);
 #pragma unroll
-  for (int j = 0; j < NPL; ++j) {
-    const int i = j * 32 + lane;
-    if (j * 32 >= kext && j * 32 >= n) break;  // warp-uniform
-    const bool valid = i < n;
-    bool keep;
-    if (mode == kSelectAll) {
-      keep = valid;
-    } else if (mode == kSelectGiven) {
-      keep = valid && (min_[i] != 0);
-    } else if (mode == kSelectThreshold) {
-      keep = valid && fabsf(sgrow[i]) >= a.tau;
-    } else if (drop_everything) {
-      keep = false;
-    } else {
-      const bool tie = valid && kr[j] == pk.pivot;
-      const unsigned tb = __ballot_sync(0xffffffffu, tie);
-      const int tie_rank = tie_base + __popc(tb & lt);
-      tie_base += __popc(tb);
-      keep = valid && (kr[j] > pk.pivot || (tie && tie_rank >= pk.ties_to_drop));
-    }
-    const unsigned kb = __ballot_sync(0xffffffffu, keep);
-    const int pos = kept_base + __popc(kb & lt);
-    kept_base += __popc(kb);
-    if (keep && kidx) {
-      kidx[pos] = i;
-      if (kval) kval[pos] = hv[j];
-    }
-    if (mout && valid) mout[i] = keep ? 1 : 0;
-    if (hb && i < kext) {
-      float v = keep ? hv[j] : 0.0f;
-      for (int sp = 0; sp < a.nsplit; ++sp) {
-        const __nv_bfloat16 b = __float2bfloat16_rn(v);
-        hb[static_cast<size_t>(sp) * a.hb_split_stride + i] = b;
-        v = __fsub_rn(v, __bfloat162float(b));
+    for (int j = 0; j < NPL; ++j) {
+      if ((keepbits >> j) & 1u) {
+        kidx[pos] = i0 + j;
+        if (kval) kval[pos] = hv[j];
+        ++pos;
       }
     }
   }
-  if (lane == 0 && a.kept_cnt) a.kept_cnt[row] = kept_base;
+  if (mout) {
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (i0 + j < n) mout[i0 + j] = static_cast<uint8_t>((keepbits >> j) & 1u);
+  }
+  if (hb) {
+    const int kext = routed ? a.kext_routed : a.kext_shared;
+    const bool vec8 = (a.Nh & 7) == 0 && (kext & 7) == 0;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) hv[j] = ((keepbits >> j) & 1u) ? hv[j] : 0.0f;
+    for (int sp = 0; sp < a.nsplit; ++sp) {
+      __nv_bfloat16* dst = hb + static_cast<size_t>(sp) * a.hb_split_stride;
+#pragma unroll
+      for (int v = 0; v < NPL; v += 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat16 lo = __float2bfloat16_rn(hv[v + 2 * q]);
+          const __nv_bfloat16 hi = __float2bfloat16_rn(hv[v + 2 * q + 1]);
+          hv[v + 2 * q] = __fsub_rn(hv[v + 2 * q], __bfloat162float(lo));
+          hv[v + 2 * q + 1] = __fsub_rn(hv[v + 2 * q + 1], __bfloat162float(hi));
+          w[q] = static_cast<uint32_t>(__bfloat16_as_ushort(lo)) |
+                 (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16);
+        }
+        if (vec8) {
+          if (i0 + v < kext) *reinterpret_cast<uint4*>(dst + i0 + v) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (i0 + v + q < kext)
+              dst[i0 + v + q] = __ushort_as_bfloat16(static_cast<unsigned short>(w[q >> 1] >> ((q & 1) * 16)));
+        }
+      }
+    }
+  }
+  if (a.kept_cnt) {
+    const int total = __reduce_add_sync(0xffffffffu, my_kept);
+    if (lane == 0) a.kept_cnt[row] = total;
+  }
 }
 
 int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {

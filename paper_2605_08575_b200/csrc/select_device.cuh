@@ -204,17 +204,42 @@ __device__ __forceinline__ RowPick sel_hist_pick(const uint32_t* keys, int n, in
   return p;
 }
 
-// One warp, keys in registers: kr[j] is the key of element j * 32 + lane (0xffffffff past the
-// end of the row), 0 < n_off < n.  Bit-by-bit search for the n_off-th smallest key: 31 counting
-// steps of NPL compares + one warp reduce each, no barriers and no shared memory.  In total
-// instructions this is ~5x cheaper than the CTA-wide 8-ary search (which trades work for
-// latency), so it is what batch-sized selections use; every lane returns the same RowPick.
+// One warp, keys in registers (any assignment of elements to lanes; 0xffffffff marks slots past
+// the end of the row), 0 < n_off < n.  Finds the n_off-th smallest key:
+//   1. the bits all keys share are skipped (warp min / max);
+//   2. bit-by-bit counting steps (NPL compares + one warp reduce each) narrow the pivot's value
+//      interval until it holds at most 32 keys -- typically ~8 steps for a 512-neuron row;
+//   3. those keys are compacted one per lane through `scratch` (33 words of shared memory owned
+//      by this warp) and the remaining bits cost one compare + ballot each.
+// Every lane returns the same RowPick.  Instruction count is what bounds a batch-sized
+// selection (2048 rows: the 31-step version was 4000 warp instructions per row, 49 % issue
+// utilisation over 19 us -- profiles/README.md), hence the effort to cut steps.
 template <int NPL>
-__device__ __forceinline__ RowPick warp_binary_pick(const uint32_t (&kr)[NPL], int n_off) {
-  uint32_t p = 0;
-  int below = 0;
+__device__ __forceinline__ RowPick warp_binary_pick(const uint32_t (&kr)[NPL], int n, int n_off,
+                                                    uint32_t* scratch) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mn = 0xffffffffu;
+  int mx = -1;  // signed: the 0xffffffff fillers are -1 and never win
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    mn = min(mn, kr[j]);
+    mx = max(mx, static_cast<int>(kr[j]));
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  RowPick pk;
+  if (mn == static_cast<uint32_t>(mx)) {  // one value: the lowest n_off indices go
+    pk.pivot = mn;
+    pk.ties_to_drop = n_off;
+    pk.drop_all_ties = false;
+    return pk;
+  }
+  int b = 31 - __clz(mn ^ static_cast<uint32_t>(mx));  // highest bit in which two keys differ
+  uint32_t p = mn & ~((2u << b) - 1u);
+  int below = 0, upper = n;
+  // invariant: the pivot lies in [p, p + 2^(b+1)); below = #keys < p; upper = #keys < p + 2^(b+1)
 #pragma unroll 1
-  for (int b = 30; b >= 0; --b) {
+  while (b >= 0 && upper - below > 32) {
     const uint32_t T = p | (1u << b);
     int c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // partial counts: no NPL-deep dependent add chain
 #pragma unroll
@@ -224,21 +249,55 @@ __device__ __forceinline__ RowPick warp_binary_pick(const uint32_t (&kr)[NPL], i
       c2 += (kr[j + 2] < T) ? 1 : 0;
       c3 += (kr[j + 3] < T) ? 1 : 0;
     }
-    int c = __reduce_add_sync(0xffffffffu, (c0 + c1) + (c2 + c3));
+    const int c = __reduce_add_sync(0xffffffffu, (c0 + c1) + (c2 + c3));
     if (c < n_off) {  // fewer than n_off keys below T: the pivot is >= T
       p = T;
       below = c;
+    } else {
+      upper = c;
     }
+    --b;
   }
-  int c = 0;
+  int ties = upper - below;
+  if (b >= 0) {
+    // at most 32 keys left in the interval: one per lane
+    if (lane == 0) scratch[32] = 0u;
+    __syncwarp();
+    const uint32_t width = 2u << b;
 #pragma unroll
-  for (int j = 0; j < NPL; ++j) c += (kr[j] <= p) ? 1 : 0;
-  c = __reduce_add_sync(0xffffffffu, c);
-  RowPick pk;
+    for (int j = 0; j < NPL; ++j)
+      if (kr[j] - p < width) scratch[atomicAdd(&scratch[32], 1u)] = kr[j];
+    __syncwarp();
+    const uint32_t mine = lane < upper - below ? scratch[lane] : 0xffffffffu;
+    __syncwarp();
+    const int outside = below;  // keys below the interval; `mine` holds everything inside it
+#pragma unroll 1
+    for (; b >= 0; --b) {
+      const uint32_t T = p | (1u << b);
+      const int c = outside + __popc(__ballot_sync(0xffffffffu, mine < T));
+      if (c < n_off) {
+        p = T;
+        below = c;
+      }
+    }
+    ties = __popc(__ballot_sync(0xffffffffu, mine == p));
+  }
   pk.pivot = p;
   pk.ties_to_drop = n_off - below;
-  pk.drop_all_ties = (pk.ties_to_drop == c - below);
+  pk.drop_all_ties = (pk.ties_to_drop == ties);
   return pk;
+}
+
+// exclusive prefix sum over the lanes of a warp
+__device__ __forceinline__ int warp_excl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+  int s = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += t;
+  }
+  return s - v;
 }
 
 }  // namespace skb
