@@ -592,6 +592,143 @@ __global__ void __launch_bounds__(kDispatchThreads) dispatch_kernel(
   if (tid == 0) *d.n_tiles = n_tiles;
 }
 
+// Same outputs by 32-slot chunks: every chunk of 32 consecutive flat slots is its own segment, so
+// the per-segment counts need no atomics (one __match_any per chunk), the bases are one warp scan
+// per expert over the chunks, and ids are read from global memory once (expert id and in-chunk
+// rank stay in registers for the scatter).  4 block barriers instead of 7; used whenever the
+// [chunks][E + 1] table fits shared memory and each warp owns at most kDcPerWarp chunks.
+constexpr int kDcPerWarp = 4;
+
+__global__ void __launch_bounds__(kDispatchThreads) dispatch_chunks_kernel(
+    const int32_t* __restrict__ ids, int B, int K, int E, int has_shared, int tile_tokens,
+    DispatchBuffers d) {
+  extern __shared__ int32_t sm[];
+  const int BK = B * K;
+  const int chunks = ceil_div(BK, 32);
+  const int ES = E + 1;                 // padded row: column walks hit distinct banks
+  int32_t* chist = sm;                  // [chunks][ES] counts, later exclusive bases
+  int32_t* cnt = chist + chunks * ES;   // [E]
+  int32_t* off = cnt + E;               // [E + 1]
+  int32_t* tile_off = off + E + 1;      // [E + 1]
+  __shared__ int32_t wsum_a[32], wsum_b[32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < chunks * ES; i += kDispatchThreads) chist[i] = 0;
+  pdl_wait();
+  pdl_launch_dependents();
+  __syncthreads();
+
+  int my_e[kDcPerWarp], my_rank[kDcPerWarp];
+#pragma unroll
+  for (int r = 0; r < kDcPerWarp; ++r) {
+    const int i = (warp + 32 * r) * 32 + lane;
+    my_e[r] = (i < BK) ? __ldcg(ids + i) : -1 - lane;  // distinct negatives: no false matches
+  }
+#pragma unroll
+  for (int r = 0; r < kDcPerWarp; ++r) {
+    const int c = warp + 32 * r;
+    if (c < chunks) {  // warp-uniform
+      const unsigned peers = __match_any_sync(0xffffffffu, my_e[r]);
+      my_rank[r] = __popc(peers & ((1u << lane) - 1u));
+      if (my_e[r] >= 0 && my_rank[r] == 0) chist[c * ES + my_e[r]] = __popc(peers);
+    }
+  }
+  __syncthreads();
+
+  // per expert: exclusive scan of the chunk counts (chunk order = flat slot order)
+  for (int e = warp; e < E; e += 32) {
+    int run = 0;
+    for (int c0 = 0; c0 < chunks; c0 += 32) {
+      const int c = c0 + lane;
+      const int v = (c < chunks) ? chist[c * ES + e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (c < chunks) chist[c * ES + e] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) cnt[e] = run;
+  }
+  __syncthreads();
+
+  // exclusive scans over experts (E <= 1024 = blockDim): row offsets and tile offsets
+  {
+    const int c = (tid < E) ? cnt[tid] : 0;
+    const int tl = ceil_div(c, tile_tokens);
+    int a = c, b = tl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ua = __shfl_up_sync(0xffffffffu, a, o);
+      const int ub = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) {
+        a += ua;
+        b += ub;
+      }
+    }
+    if (E > 32) {  // block-uniform
+      if (lane == 31) {
+        wsum_a[warp] = a;
+        wsum_b[warp] = b;
+      }
+      __syncthreads();
+      for (int w = 0; w < warp; ++w) {
+        a += wsum_a[w];
+        b += wsum_b[w];
+      }
+    }
+    if (tid < E) {
+      off[tid] = a - c;
+      tile_off[tid] = b - tl;
+      if (tid == E - 1) {
+        off[E] = a;
+        tile_off[E] = b;
+      }
+    }
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int r = 0; r < kDcPerWarp; ++r) {
+    const int c = warp + 32 * r;
+    const int i = c * 32 + lane;
+    if (i < BK) {
+      const int e = my_e[r];
+      const int pos = off[e] + chist[c * ES + e] + my_rank[r];
+      d.perm[pos] = i;
+      d.inv[i] = pos;
+      d.row_expert[pos] = e;
+    }
+  }
+  for (int e = tid; e <= E; e += kDispatchThreads) d.expert_off[e] = off[e];
+
+  // tile list: expert-major, tile_tokens rows per tile, then the shared expert's tiles
+  for (int e = tid; e < E; e += kDispatchThreads) {
+    const int c = cnt[e];
+    const int nt = ceil_div(c, tile_tokens);
+    for (int j = 0; j < nt; ++j) {
+      const int ti = tile_off[e] + j;
+      d.tile_expert[ti] = e;
+      d.tile_row0[ti] = off[e] + j * tile_tokens;
+      d.tile_nrows[ti] = min(tile_tokens, c - j * tile_tokens);
+    }
+  }
+  int n_tiles = tile_off[E];
+  if (has_shared) {
+    const int nsh = ceil_div(B, tile_tokens);
+    for (int j = tid; j < nsh; j += kDispatchThreads) {
+      d.tile_expert[n_tiles + j] = E;
+      d.tile_row0[n_tiles + j] = BK + j * tile_tokens;
+      d.tile_nrows[n_tiles + j] = min(tile_tokens, B - j * tile_tokens);
+    }
+    for (int t = tid; t < B; t += kDispatchThreads) d.row_expert[BK + t] = E;
+    n_tiles += nsh;
+  }
+  if (tid == 0) *d.n_tiles = n_tiles;
+}
+
 static int dispatch_warps(int E) {
   int w = 8192 / (E > 0 ? E : 1);
   if (w > 32) w = 32;
@@ -608,9 +745,16 @@ int launch_dispatch(const LaunchCtx& ctx, const int32_t* ids, int B, int K, int 
   cfg.attrs = attr;
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
-  const int W = dispatch_warps(E);
   cfg.blockDim = dim3(kDispatchThreads);
   cfg.gridDim = dim3(1);
+  const int chunks = ceil_div(B * K, 32);
+  const size_t chunk_smem = (static_cast<size_t>(chunks) * (E + 1) + 3 * E + 2) * sizeof(int32_t);
+  if (chunks <= 32 * kDcPerWarp && chunk_smem <= 48 * 1024) {
+    cfg.dynamicSmemBytes = chunk_smem;
+    cudaLaunchKernelEx(&cfg, dispatch_chunks_kernel, ids, B, K, E, has_shared, tile_tokens, d);
+    return 1;
+  }
+  const int W = dispatch_warps(E);
   cfg.dynamicSmemBytes = (static_cast<size_t>(W) * E + 3 * E + 2) * sizeof(int32_t);
   cudaLaunchKernelEx(&cfg, dispatch_kernel, ids, B, K, E, has_shared, tile_tokens, W, d);
   return 1;
