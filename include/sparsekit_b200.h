@@ -132,6 +132,12 @@ typedef struct skb_forward_args {
   const float* weights_in;
   float tau;        /* SKB_MODE_THRESHOLD: the activation threshold, >= 0 (NaN is rejected) */
   int32_t reserved2;
+  /* SKB_MODE_TOPK with neuron budgets (budget.hpp:31-44 + the analysis mode of the reference CLI,
+   * tools/main.cpp:271-345): slot_n_off [K] (host pointer) gives, per routing slot, how many of
+   * the smallest-|h| neurons are dropped (d_ffn - keep_count of apply_budget) in place of
+   * n_off(s_routed).  Slots are in descending router weight, so slot s IS rank s of
+   * group_experts.  NULL = plain top-k.  skb_layer_forward only. */
+  const int32_t* slot_n_off;
 } skb_forward_args;
 
 typedef struct skb_layer skb_layer;

@@ -22,6 +22,7 @@
 
 #if __has_include("sparsekit/engine.hpp")
 #include "sparsekit/activation.hpp"
+#include "sparsekit/budget.hpp"
 #include "sparsekit/engine.hpp"
 #include "sparsekit/profiler.hpp"
 #include "sparsekit/router.hpp"
@@ -31,6 +32,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <numeric>
 #include <cstring>
 #include <initializer_list>
 #include <map>
@@ -390,6 +393,80 @@ inline std::vector<std::uint8_t> topk_mask(const float* h, std::size_t n, Sparsi
   std::vector<std::uint8_t> mask(n);
   detail::check(skb_topk_mask(h, 1, static_cast<int>(n), s.s, mask.data()));
   return mask;
+}
+
+// ---- neuron budgets (budget.hpp:29-44, budget.cpp) ----
+// Weights: any contiguous float container (std::vector, std::array, std::span).
+template <class Weights>
+inline ExpertGroups group_experts(const Weights& topk_weights) {
+  const int k = static_cast<int>(topk_weights.size());
+  if (k < 1) throw ConfigError("group_experts: need at least one slot");
+  std::vector<int> order(static_cast<std::size_t>(k));
+  std::iota(order.begin(), order.end(), 0);
+  const float* wt = topk_weights.data();
+  std::stable_sort(order.begin(), order.end(), [wt](int a, int b) { return wt[a] > wt[b]; });
+  const int third = k / 3;
+  ExpertGroups g;
+  g.g0.assign(order.begin(), order.begin() + third);
+  g.g1.assign(order.begin() + third, order.begin() + 2 * third);
+  g.g2.assign(order.begin() + 2 * third, order.end());
+  return g;
+}
+
+inline std::vector<int> allocate_budget(int top_k, int d_ffn, double s_active,
+                                        const ExpertGroups& groups, const BudgetRatios& ratios) {
+  if (!(s_active >= 0.0 && s_active <= 1.0))
+    throw ConfigError("allocate_budget: s_active must lie in [0, 1]");
+  if (ratios.r0 < 0.0 || ratios.r1 < 0.0 || ratios.r2 < 0.0)
+    throw ConfigError("allocate_budget: ratios must be non-negative");
+  const std::vector<int>* members[3] = {&groups.g0, &groups.g1, &groups.g2};
+  const double ratio[3] = {ratios.r0, ratios.r1, ratios.r2};
+  double denom = 0.0;
+  for (int x = 0; x < 3; ++x) denom += ratio[x] * static_cast<double>(members[x]->size());
+  if (!(denom > 0.0)) throw ConfigError("allocate_budget: no ratio mass on non-empty groups");
+  const double budget = s_active * top_k * d_ffn;
+  std::vector<int> counts(static_cast<std::size_t>(top_k), 0);
+  int assigned = 0;
+  for (int x = 0; x < 3; ++x) {
+    long n_e = static_cast<long>(std::floor(budget * ratio[x] / denom + 0.5));
+    n_e = n_e < 0 ? 0 : (n_e > d_ffn ? d_ffn : n_e);
+    for (int slot : *members[x]) {
+      if (slot < 0 || slot >= top_k)
+        throw IndexError("allocate_budget: slot " + std::to_string(slot) + " outside [0, " +
+                         std::to_string(top_k) + ")");
+      counts[static_cast<std::size_t>(slot)] = static_cast<int>(n_e);
+      ++assigned;
+    }
+  }
+  if (assigned != top_k) throw ConfigError("allocate_budget: groups must partition the slots");
+  return counts;
+}
+
+inline std::vector<std::uint8_t> apply_budget(const float* h, std::size_t n, int keep_count) {
+  if (keep_count < 0 || static_cast<std::size_t>(keep_count) > n)
+    throw ConfigError("apply_budget: keep_count outside [0, N]");
+  return b200::mask_smallest_magnitudes(h, n, static_cast<int>(n) - keep_count);
+}
+
+// The budget analysis mode of the reference CLI (tools/main.cpp:271-345) as one device forward:
+// slot s of every token keeps the count allocate_budget gives rank s (slots are in descending
+// router weight); mask_shared: the shared expert gets a plain top-k mask at `sparsity`.
+inline ForwardReport forward_budget_sparse(const MoELayerWeights& w, const Matrix& x,
+                                           SparsityLevel sparsity, const BudgetRatios& ratios,
+                                           bool mask_shared = false, MaskSet* masks_out = nullptr) {
+  const int K = w.config.top_k, N = w.config.d_ffn;
+  std::vector<float> rank_weights(static_cast<std::size_t>(K > 0 ? K : 0));
+  for (int sl = 0; sl < K; ++sl) rank_weights[static_cast<std::size_t>(sl)] = static_cast<float>(K - sl);
+  const std::vector<int> counts =
+      b200::allocate_budget(K, N, 1.0 - sparsity.s, b200::group_experts(rank_weights), ratios);
+  std::vector<std::int32_t> n_off(counts.size());
+  for (std::size_t i = 0; i < counts.size(); ++i) n_off[i] = N - counts[i];
+  skb_forward_args a{};
+  a.mode = SKB_MODE_TOPK;
+  a.s_routed = sparsity.s;
+  a.s_shared = (mask_shared && w.config.has_shared) ? sparsity.s : 0.0;
+  a.slot_n_off = n_off.data();
+  return detail::run(w, x, a, masks_out);
 }
 
 }  // namespace b200

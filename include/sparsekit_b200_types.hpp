@@ -10,6 +10,7 @@
 //   ForwardReport / MaskSet       proj/include/sparsekit/engine.hpp:19-34
 //   SwitchTable / Stopwatch       proj/include/sparsekit/engine.hpp:52-69
 //   SweepMode                     proj/include/sparsekit/profiler.hpp:38
+//   BudgetRatios / ExpertGroups   proj/include/sparsekit/budget.hpp:15-28
 //   exception types               proj/include/sparsekit/errors.hpp:12-43
 // so that code written against the reference compiles against either.
 #pragma once
@@ -105,6 +106,14 @@ struct SwitchTable {
   static constexpr std::size_t kSparseAlways = std::numeric_limits<std::size_t>::max();
   std::size_t tipping_batch = kSparseAlways;
   bool use_dense(std::size_t batch) const { return batch >= tipping_batch; }
+};
+
+// distribution ratios of the three router-weight groups; slot indices by router weight
+struct BudgetRatios {
+  double r0 = 1.0, r1 = 1.0, r2 = 1.0;
+};
+struct ExpertGroups {
+  std::vector<int> g0, g1, g2;
 };
 
 // injectable monotonic clock (milliseconds)

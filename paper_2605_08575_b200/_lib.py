@@ -53,7 +53,7 @@ class SkbForwardArgs(C.Structure):
         ("routed_mask_out", C.c_void_p), ("shared_mask_out", C.c_void_p),
         ("h_routed_out", C.c_void_p), ("h_shared_out", C.c_void_p),
         ("ids_in", C.c_void_p), ("weights_in", C.c_void_p),
-        ("tau", C.c_float), ("reserved2", C.c_int32),
+        ("tau", C.c_float), ("reserved2", C.c_int32), ("slot_n_off", C.c_void_p),
     ]
 
 

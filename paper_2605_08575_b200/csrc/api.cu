@@ -122,6 +122,7 @@ struct skb_layer {
   int32_t* d_kidx = nullptr;
   float* d_kval = nullptr;
   int32_t* d_kcnt = nullptr;
+  int32_t* d_slot_noff = nullptr;  // [K] per-slot drop counts (neuron budgets)
   uint8_t* d_mask_in_r = nullptr;
   uint8_t* d_mask_in_s = nullptr;
   uint8_t* d_mask_out_r = nullptr;
@@ -153,11 +154,12 @@ void free_workspace(skb_layer* L) {
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
                   L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
                   L->d_xb,       L->disp.tile_colrow, L->d_dec_lf,    L->d_dec_lm,
-                  L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr,      L->d_sg};
+                  L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr,      L->d_sg,
+                  L->d_slot_noff};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   L->d_x = L->d_y = L->d_logits = L->d_wts = L->d_h = L->d_kval = nullptr;
-  L->d_ids = L->d_kidx = L->d_kcnt = nullptr;
+  L->d_ids = L->d_kidx = L->d_kcnt = L->d_slot_noff = nullptr;
   L->disp = DispatchBuffers{};
   L->d_xs = nullptr;
   L->d_counters = nullptr;
@@ -257,6 +259,7 @@ int reserve_locked(skb_layer* L, int B) {
   SKB_TRY(dmalloc(&L->d_kidx, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kval, rows * g.Nh));
   SKB_TRY(dmalloc(&L->d_kcnt, rows));
+  SKB_TRY(dmalloc(&L->d_slot_noff, static_cast<size_t>(g.K)));
   SKB_TRY(dmalloc(&L->d_mask_in_r, BK * g.N));
   SKB_TRY(dmalloc(&L->d_mask_out_r, BK * g.N));
   if (g.has_shared) {
@@ -434,6 +437,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     return SKB_OK;
   }
 
+  const bool budget = a->mode == SKB_MODE_TOPK && a->slot_n_off != nullptr;
   int sel_mode, n_off_r = 0, n_off_s = 0;
   int max_keep = g.N > g.S ? g.N : g.S;
   if (a->mode == SKB_MODE_DENSE) {
@@ -442,7 +446,10 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sel_mode = kSelectTopk;
     n_off_r = n_off_of(a->s_routed, g.N);
     n_off_s = g.has_shared ? n_off_of(a->s_shared, g.S) : 0;
-    const int kr = g.N - n_off_r, ks = g.S - n_off_s;
+    int kr = g.N - n_off_r;
+    const int ks = g.S - n_off_s;
+    if (budget)  // per-slot counts: the largest survivor count bounds the lists
+      for (int sl = 0; sl < g.K; ++sl) kr = kr > g.N - a->slot_n_off[sl] ? kr : g.N - a->slot_n_off[sl];
     max_keep = kr > ks ? kr : ks;
   } else if (a->mode == SKB_MODE_THRESHOLD) {
     sel_mode = kSelectThreshold;
@@ -470,12 +477,14 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
     // threshold selection: the survivor count is data dependent; the masked GEMM covers every case
     if (sel_mode == kSelectThreshold) dense_down = true;
+    // per-slot counts: the stand-alone selection kernel is the one that takes them
+    if (budget) dense_down = true;
   }
   const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
 
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
-      sel_mode != kSelectThreshold &&
+      sel_mode != kSelectThreshold && !budget &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
                     SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
       ((a->flags & SKB_FLAG_FUSED_DECODE) ||
@@ -624,6 +633,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sa.n_off_shared = n_off_s;
     sa.mask_in_routed = d_mask_r;
     sa.mask_in_shared = d_mask_s;
+    if (budget) sa.slot_counts = L->d_slot_noff;
     if (sel_mode == kSelectThreshold) {
       sa.sg = L->d_sg;
       sa.tau = a->tau;
@@ -717,6 +727,10 @@ int check_args(const skb_layer* L, const skb_forward_args* a) {
     // SparsityLevel, activation.hpp:18-22
     if (!(a->s_routed >= 0.0 && a->s_routed <= 1.0) || !(a->s_shared >= 0.0 && a->s_shared <= 1.0))
       return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
+    if (a->slot_n_off != nullptr)
+      for (int sl = 0; sl < g.K; ++sl)  // budget.cpp:80-82
+        if (a->slot_n_off[sl] < 0 || a->slot_n_off[sl] > g.N)
+          return fail(SKB_ECONFIG, "apply_budget: keep_count outside [0, N]");
   }
   return SKB_OK;
 }
@@ -731,6 +745,10 @@ void fill_report(const skb_layer* L, const skb_forward_args* a, skb_report* r,
   uint64_t active = routed_neurons, active_sh = B * S;
   if (a->mode == SKB_MODE_TOPK) {
     active = B * K * (N - n_off_of(a->s_routed, g.N));
+    if (a->slot_n_off != nullptr) {
+      active = 0;
+      for (uint64_t sl = 0; sl < K; ++sl) active += B * (N - static_cast<uint64_t>(a->slot_n_off[sl]));
+    }
     if (g.has_shared) active_sh = B * (S - n_off_of(a->s_shared, g.S));
   } else if (a->mode == SKB_MODE_MASKED && host_routed_mask != nullptr) {
     active = 0;
@@ -1063,6 +1081,9 @@ int skb_layer_forward(skb_layer* L, const skb_forward_args* a, skb_report* repor
       ms = L->d_mask_in_s;
     }
   }
+  if (a->mode == SKB_MODE_TOPK && a->slot_n_off != nullptr)
+    SKB_CUDA(cudaMemcpyAsync(L->d_slot_noff, a->slot_n_off, static_cast<size_t>(g.K) * 4,
+                             cudaMemcpyHostToDevice, s));
   const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
   if (a->mode == SKB_MODE_ROUTE_ONLY) {
     rc = forward_core(L, a, L->d_x, nullptr, nullptr, nullptr, nullptr, nullptr, s, false);
@@ -1156,6 +1177,8 @@ int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stre
   if (a->batch > L->cap_batch)
     return fail(SKB_ESHAPE, "forward_device: batch %d exceeds reserved capacity %d; call skb_layer_reserve",
                 a->batch, L->cap_batch);
+  if (a->mode == SKB_MODE_TOPK && a->slot_n_off != nullptr)
+    return fail(SKB_ECONFIG, "forward_device: per-slot neuron budgets need skb_layer_forward");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : L->stream;
   const bool timing = (a->flags & SKB_FLAG_TIME_STAGES) != 0;
   rc = forward_core(L, a, a->x, a->y, a->mode == SKB_MODE_MASKED ? a->routed_mask_in : nullptr,

@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 
   int n_off = 0;
   if (mode == kSelectTopk) {
-    n_off = a.counts ? a.counts[row] : (routed ? a.n_off_routed : a.n_off_shared);
+    n_off = a.counts ? a.counts[row]
+                     : (routed ? (a.slot_counts ? a.slot_counts[slot % a.K] : a.n_off_routed)
+                               : a.n_off_shared);
     if (n_off <= 0) mode = kSelectAll;  // activation.cpp:35
   }
 
@@ -178,7 +180,9 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
   }
   int n_off = 0;
   if (mode == kSelectTopk) {
-    n_off = a.counts ? a.counts[row] : (routed ? a.n_off_routed : a.n_off_shared);
+    n_off = a.counts ? a.counts[row]
+                     : (routed ? (a.slot_counts ? a.slot_counts[slot % a.K] : a.n_off_routed)
+                               : a.n_off_shared);
     if (n_off <= 0) mode = kSelectAll;  // activation.cpp:35
   }
   const bool drop_everything = (mode == kSelectTopk) && n_off >= n;  // activation.cpp:36-39

@@ -116,6 +116,7 @@ struct SelectArgs {
   const float* sg;               // kSelectThreshold: silu(gate) [rows][Nh]; a routed neuron is kept
   float tau;                     //   iff |sg| >= tau (activation.cpp:62-72); shared rows keep all
   const int32_t* counts;         // optional per-row n_off override (stage API), else NULL
+  const int32_t* slot_counts;    // optional per-slot n_off of routed rows, [K] (neuron budgets)
   const int32_t* perm;           // row -> flat slot (masks are slot-major); NULL = identity
   const uint8_t* mask_in_routed; // kSelectGiven: [B*K][N] slot-major
   const uint8_t* mask_in_shared; // kSelectGiven: [B][S] or NULL (=> keep all)

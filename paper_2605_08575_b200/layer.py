@@ -292,7 +292,8 @@ class MoELayerWeights:
 
 def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_shared=0.0,
              masks: Optional[MaskSet] = None, flags: int = 0, capture: bool = False,
-             y_out: Optional[np.ndarray] = None, tau: float = 0.0) -> ForwardReport:
+             y_out: Optional[np.ndarray] = None, tau: float = 0.0,
+             slot_n_off=None) -> ForwardReport:
     L = _lib.load()
     cfg = w.config
     x = np.ascontiguousarray(x, dtype=np.float32)
@@ -308,6 +309,12 @@ def _forward(w: MoELayerWeights, x: np.ndarray, mode: int, s_routed=0.0, s_share
     a.tau = float(tau)
     a.x, a.y = x.ctypes.data, y.ctypes.data
     keep = [x, y]
+    if slot_n_off is not None:
+        sn = np.ascontiguousarray(slot_n_off, dtype=np.int32).reshape(-1)
+        if sn.size != K:
+            raise ShapeError(f"per-slot counts: need top_k={K} entries, got {sn.size}")
+        a.slot_n_off = sn.ctypes.data
+        keep.append(sn)
     if mode == MODE_MASKED:
         r = np.ascontiguousarray(masks.routed, dtype=np.uint8).reshape(-1)
         a.routed_mask_in, a.routed_mask_len = r.ctypes.data, r.size
@@ -421,6 +428,89 @@ def forward_sparse(w: MoELayerWeights, x, threshold: float, threads: int = 1, *,
         raise ConfigError("forward_sparse: threshold must be >= 0")
     return _forward(w, x, MODE_THRESHOLD, flags=flags, capture=capture, y_out=y_out,
                     tau=float(threshold))
+
+
+# ---- neuron budgets (budget.hpp, budget.cpp) -------------------------------------------------
+@dataclass
+class BudgetRatios:
+    """Distribution ratios of the three router-weight groups (budget.hpp:15-20)."""
+    r0: float = 1.0
+    r1: float = 1.0
+    r2: float = 1.0
+
+
+@dataclass
+class ExpertGroups:
+    """Slot indices by router weight: g0 the floor(K/3) heaviest, g1 the next floor(K/3), g2 the
+    rest (budget.hpp:22-28)."""
+    g0: list = field(default_factory=list)
+    g1: list = field(default_factory=list)
+    g2: list = field(default_factory=list)
+
+
+def group_experts(topk_weights) -> ExpertGroups:
+    """budget.cpp:15-35: stable descending order, so equal weights keep slot order."""
+    wts = [float(v) for v in np.asarray(topk_weights, np.float32).reshape(-1)]
+    k = len(wts)
+    if k < 1:
+        raise ConfigError("group_experts: need at least one slot")
+    order = sorted(range(k), key=lambda i: -wts[i])  # sorted() is stable
+    third = k // 3
+    return ExpertGroups(order[:third], order[third:2 * third], order[2 * third:])
+
+
+def allocate_budget(top_k: int, d_ffn: int, s_active: float, groups: ExpertGroups,
+                    ratios: BudgetRatios):
+    """budget.cpp:37-76: per-slot survivor counts for a budget of s_active * K * d_ffn neurons,
+    n_e = clamp(floor(budget * r_x / sum_x(r_x |g_x|) + 0.5), 0, d_ffn) for the slots of g_x."""
+    import math
+    if not (0.0 <= s_active <= 1.0):
+        raise ConfigError("allocate_budget: s_active must lie in [0, 1]")
+    if ratios.r0 < 0.0 or ratios.r1 < 0.0 or ratios.r2 < 0.0:
+        raise ConfigError("allocate_budget: ratios must be non-negative")
+    denom = (ratios.r0 * float(len(groups.g0)) + ratios.r1 * float(len(groups.g1)) +
+             ratios.r2 * float(len(groups.g2)))
+    if not (denom > 0.0):
+        raise ConfigError("allocate_budget: no ratio mass on non-empty groups")
+    budget = s_active * top_k * d_ffn
+    counts = [0] * top_k
+    assigned = 0
+    for members, ratio in ((groups.g0, ratios.r0), (groups.g1, ratios.r1), (groups.g2, ratios.r2)):
+        n_e = min(max(int(math.floor(budget * ratio / denom + 0.5)), 0), d_ffn)
+        for slot in members:
+            if slot < 0 or slot >= top_k:
+                raise IndexError_(f"allocate_budget: slot {slot} outside [0, {top_k})")
+            counts[slot] = n_e
+            assigned += 1
+    if assigned != top_k:
+        raise ConfigError("allocate_budget: groups must partition the slots")
+    return counts
+
+
+def apply_budget(h, keep_count: int) -> np.ndarray:
+    """budget.cpp:78-85: keep the keep_count largest-|h| entries of one slot (on the device)."""
+    n = int(np.size(h))
+    if keep_count < 0 or keep_count > n:
+        raise ConfigError("apply_budget: keep_count outside [0, N]")
+    return mask_smallest_magnitudes(h, n - keep_count)
+
+
+def forward_budget_sparse(w: MoELayerWeights, x, sparsity: float, ratios: BudgetRatios,
+                          mask_shared: bool = False, *, flags: int = 0,
+                          capture: bool = False) -> ForwardReport:
+    """The reference CLI's budget analysis mode (tools/main.cpp:271-345) as one device forward:
+    per routing slot, apply_budget with the count allocate_budget gives its router-weight group
+    (slots are in descending router weight, so slot s has rank s for every token); with
+    mask_shared the shared expert gets a plain top-k mask at `sparsity` (R+S).  Numerically
+    forward_masked_dense on those masks, with masked W_down rows skipped."""
+    cfg = w.config
+    lvl = SparsityLevel(sparsity)
+    groups = group_experts(np.arange(cfg.top_k, 0, -1, dtype=np.float32))  # rank = slot
+    counts = allocate_budget(cfg.top_k, cfg.d_ffn, 1.0 - lvl.s, groups, ratios)
+    n_off_slots = [cfg.d_ffn - c for c in counts]
+    return _forward(w, x, MODE_TOPK, s_routed=lvl.s,
+                    s_shared=lvl.s if (mask_shared and cfg.has_shared) else 0.0, flags=flags,
+                    capture=capture, slot_n_off=n_off_slots)
 
 
 # ---- the dense/sparse switch (engine.hpp:52-89, engine.cpp:371-420) ---------------------------

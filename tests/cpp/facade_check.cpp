@@ -127,6 +127,28 @@ int main() {
       return 1;
     }
   }
+  // neuron budgets (budget_test.cpp:47-54): 3:2:1 over K=6, N=8, half active; the budgeted forward
+  {
+    const std::vector<float> wts = {0.3f, 0.25f, 0.2f, 0.15f, 0.07f, 0.03f};
+    const std::vector<int> counts =
+        b200::allocate_budget(6, 8, 0.5, b200::group_experts(wts), BudgetRatios{3.0, 2.0, 1.0});
+    const float hrow[3] = {1.0f, -3.0f, 2.0f};
+    MaskSet bm;
+    const ForwardReport budgeted =
+        b200::forward_budget_sparse(w, x, SparsityLevel(0.5), BudgetRatios{}, true, &bm);
+    // equal ratios == the plain top-k forward (other kernels at this batch: compare to tolerance)
+    double bdiff = 0.0;
+    for (std::size_t i = 0; i < fused.outputs.data.size(); ++i)
+      bdiff = std::fmax(bdiff, std::fabs(budgeted.outputs.data[i] - fused.outputs.data[i]));
+    std::uint64_t bkept = 0;
+    for (auto b : bm.routed) bkept += b;
+    if (counts != std::vector<int>{6, 6, 4, 4, 2, 2} ||
+        b200::apply_budget(hrow, 3, 2) != std::vector<std::uint8_t>{0, 1, 1} || bdiff > 1e-5 ||
+        bkept != kept || budgeted.active_neurons_total != kept) {
+      std::printf("FAIL: neuron budgets\n");
+      return 1;
+    }
+  }
   bool threw = false;
   try {
     Matrix bad(2, 64);

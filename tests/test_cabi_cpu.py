@@ -47,7 +47,7 @@ def test_library_does_not_link_the_oracle_or_torch(lib):
 def test_struct_layouts_match_header(lib):
     assert C.sizeof(lib.SkbConfig) == 32
     assert C.sizeof(lib.SkbReport) == 72
-    assert C.sizeof(lib.SkbForwardArgs) == 16 + 16 + 8 * 14 + 8  # + tau, reserved2 (ABI 3)
+    assert C.sizeof(lib.SkbForwardArgs) == 16 + 16 + 8 * 14 + 8 + 8  # + tau, reserved2, slot_n_off (ABI 3)
 
 
 def test_config_validate_matches_reference_messages(lib):
@@ -184,3 +184,57 @@ def test_generate_tokens_matches_the_oracle_bit_for_bit(lib):
         assert out.tobytes() == np.asarray(ref, np.float32).tobytes()
     assert L.skb_generate_tokens(0, 8, 1, None) == 2  # ConfigError, model.cpp:169-171
     assert b"batch >= 1" in L.skb_last_error()
+
+
+# ---------------------------------------------------------------------------------------------
+# neuron budgets: host arithmetic of budget.cpp (KATs of proj/tests/budget_test.cpp:16-137)
+# ---------------------------------------------------------------------------------------------
+def test_group_experts_and_allocate_budget_hand_cases(lib):
+    import paper_2605_08575_b200 as skb
+    g = skb.group_experts([0.3, 0.25, 0.2, 0.15, 0.07, 0.03])
+    assert (g.g0, g.g1, g.g2) == ([0, 1], [2, 3], [4, 5])
+    g7 = skb.group_experts([0.7, 0.6, 0.5, 0.4, 0.3, 0.2, 0.1])
+    assert (len(g7.g0), len(g7.g1), len(g7.g2)) == (2, 2, 3)
+    g1 = skb.group_experts([1.0])
+    assert (g1.g0, g1.g1, g1.g2) == ([], [], [0])
+    gt = skb.group_experts([0.2, 0.5, 0.2, 0.1, 0.5, 0.1])  # ties toward the lower slot
+    assert (gt.g0, gt.g1, gt.g2) == ([1, 4], [0, 2], [3, 5])
+    with pytest.raises(skb.ConfigError):
+        skb.group_experts([])
+
+    counts = skb.allocate_budget(6, 8, 0.5, g, skb.BudgetRatios(3.0, 2.0, 1.0))
+    assert counts == [6, 6, 4, 4, 2, 2] and sum(counts) == 24
+    ge = skb.group_experts([0.4, 0.3, 0.2, 0.06, 0.03, 0.01])
+    assert skb.allocate_budget(6, 16, 0.25, ge, skb.BudgetRatios()) == [4] * 6
+    g3 = skb.group_experts([0.5, 0.3, 0.2])
+    assert skb.allocate_budget(3, 8, 0.0, g3, skb.BudgetRatios(3.0, 2.0, 1.0)) == [0, 0, 0]
+    for bad in (skb.BudgetRatios(0.0, 0.0, 0.0), skb.BudgetRatios(-1.0, 1.0, 1.0)):
+        with pytest.raises(skb.ConfigError):
+            skb.allocate_budget(3, 8, 0.5, g3, bad)
+    with pytest.raises(skb.ConfigError):  # K = 1: all mass must sit on g2
+        skb.allocate_budget(1, 8, 0.5, g1, skb.BudgetRatios(3.0, 2.0, 0.0))
+    assert skb.allocate_budget(1, 8, 0.5, g1, skb.BudgetRatios(3.0, 2.0, 1.0)) == [4]
+    with pytest.raises(skb.ConfigError):
+        skb.allocate_budget(3, 8, 1.5, g3, skb.BudgetRatios())
+    with pytest.raises(skb.ConfigError):  # groups must partition the slots
+        skb.allocate_budget(3, 8, 0.5, skb.ExpertGroups([0], [1], []), skb.BudgetRatios())
+    with pytest.raises(IndexError):
+        skb.allocate_budget(3, 8, 0.5, skb.ExpertGroups([0], [1], [7]), skb.BudgetRatios())
+
+    # rounding slack and clamping bounds, monotone in r0 (budget_test.cpp:90-137)
+    rng = np.random.default_rng(53)
+    for _ in range(200):
+        k, n = int(rng.integers(1, 9)), int(rng.integers(1, 65))
+        s_act = float(rng.random())
+        r = skb.BudgetRatios(rng.random() * 4, rng.random() * 4, rng.random() * 4 + 0.01)
+        groups = skb.group_experts(rng.random(k).astype(np.float32) + 0.01)
+        c = skb.allocate_budget(k, n, s_act, groups, r)
+        assert all(0 <= v <= n for v in c) and sum(c) <= k * n
+        denom = r.r0 * len(groups.g0) + r.r1 * len(groups.g1) + r.r2 * len(groups.g2)
+        shares = [s_act * k * n * q / denom for q in (r.r0, r.r1, r.r2)]
+        if all(0.0 <= sh <= n for sh in shares):
+            assert abs(sum(c) - s_act * k * n) <= k / 2.0 + 3.0
+    gm = skb.group_experts([0.5, 0.25, 0.13, 0.07, 0.03, 0.02])
+    seq = [skb.allocate_budget(6, 32, 0.4, gm, skb.BudgetRatios(r0, 1.0, 1.0))[gm.g0[0]]
+           for r0 in (0.5, 1.0, 2.0, 4.0, 8.0)]
+    assert seq == sorted(seq)

@@ -894,3 +894,74 @@ def test_step_obeys_the_tipping_rule(skb, oracle):
     assert skb.step(layer, x, 0.01, skb.SwitchTable(4)).path_used == 0
     assert skb.step(layer, x, 0.01, skb.SwitchTable(1)).path_used == 0
     assert skb.step(layer, x, 0.01, skb.SwitchTable()).path_used == 1
+
+
+# ---------------------------------------------------------------------------------------------
+# neuron budgets: apply_budget and the budgeted forward (budget_test.cpp:139-162, main.cpp:271-345)
+# ---------------------------------------------------------------------------------------------
+def test_apply_budget_hand_cases_and_equal_ratio_equivalence(skb, oracle):
+    h = np.array([1.0, -3.0, 2.0], np.float32)
+    assert skb.apply_budget(h, 3).tolist() == [1, 1, 1]
+    assert skb.apply_budget(h, 0).tolist() == [0, 0, 0]
+    assert skb.apply_budget(h, 2).tolist() == [0, 1, 1]
+    for bad in (4, -1):
+        with pytest.raises(skb.ConfigError):
+            skb.apply_budget(h, bad)
+    for trial in range(40):  # equal-ratio budgets reproduce plain top-k masks bit for bit
+        n = 8 if trial % 2 == 0 else 16
+        s_active = 0.5 if trial % 4 < 2 else 0.25
+        row = oracle.fill_symmetric(n, 61 + trial, 0, 1.0)
+        keep = int(np.floor(s_active * n + 0.5))
+        np.testing.assert_array_equal(skb.apply_budget(row, keep),
+                                      skb.topk_mask(row, skb.SparsityLevel(1.0 - s_active)))
+
+
+@pytest.mark.parametrize("case", [(8, 6, 96, 160, 0, True, 19), (16, 4, 256, 192, 64, True, 5),
+                                  (8, 2, 128, 96, 0, False, 33), (32, 8, 256, 128, 0, True, 70)])
+@pytest.mark.parametrize("mask_shared", [False, True])
+def test_forward_budget_sparse_vs_oracle(skb, oracle, case, mask_shared):
+    E, K, D, N, S, renorm, B = case
+    if mask_shared and not S:
+        pytest.skip("no shared expert")
+    cfg = Config(E, K, D, N, S, renorm)
+    w, x = rounded_case(oracle, cfg, seed=E + K, scale=0.1, batch=B, token_seed=8)
+    layer = make_layer(skb, w)
+    ratios, sparsity = skb.BudgetRatios(3.0, 2.0, 1.0), 0.5
+    rep = skb.forward_budget_sparse(layer, x, sparsity, ratios, mask_shared, capture=True)
+    # the reference's analysis mode: per token group_experts on ITS weights, allocate_budget,
+    # apply_budget per slot on the oracle's h, then the masked-dense layer
+    _, _, cap = oracle.forward(w, x, capture=True)
+    np.testing.assert_array_equal(rep.routes.ids, cap["ids"])
+    masks = np.zeros((B, K, N), np.uint8)
+    for t in range(B):
+        counts = skb.allocate_budget(K, N, 1.0 - sparsity, skb.group_experts(cap["weights"][t]), ratios)
+        for s in range(K):
+            masks[t, s] = oracle.mask_smallest(cap["h_routed"][t, s], N - counts[s])
+    shared = None
+    if mask_shared:
+        shared = np.stack([oracle.topk_mask(cap["h_shared"][t], sparsity)[1] for t in range(B)])
+    agree = np.mean(rep.masks.routed == masks)
+    assert agree >= MASK_AGREEMENT, agree
+    if mask_shared:
+        assert np.mean(rep.masks.shared == shared) >= MASK_AGREEMENT
+    y_same, _ = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if mask_shared else None)
+    assert max_rel_diff(rep.outputs, y_same) <= TOL_FP32_ACCUM
+    # every slot keeps exactly its group's count
+    expect = skb.allocate_budget(K, N, 1.0 - sparsity,
+                                 skb.group_experts(np.arange(K, 0, -1, dtype=np.float32)), ratios)
+    np.testing.assert_array_equal(rep.masks.routed.sum(axis=2), np.tile(expect, (B, 1)))
+    assert rep.active_neurons_total == B * sum(expect)
+
+
+def test_equal_ratio_budget_is_the_plain_topk_forward(skb, oracle):
+    cfg = Config(8, 6, 96, 160, 48, True)
+    w, x = rounded_case(oracle, cfg, seed=5, scale=0.1, batch=23, token_seed=2)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    a = skb.forward_budget_sparse(layer, x, 0.5, skb.BudgetRatios(), True, capture=True)
+    b = skb.forward_topk_sparse(layer, x, lvl, lvl, capture=True, flags=skb.FLAG_DENSE_DOWN)
+    np.testing.assert_array_equal(a.masks.routed, b.masks.routed)
+    np.testing.assert_array_equal(a.masks.shared, b.masks.shared)
+    assert a.outputs.tobytes() == b.outputs.tobytes()
+    with pytest.raises(skb.ShapeError):
+        skb.layer._forward(layer, x, skb.MODE_TOPK, s_routed=0.5, slot_n_off=[1, 2])
