@@ -43,7 +43,9 @@ typedef enum skb_status {
   SKB_ECONFIG = 2,   /* sparsekit::ConfigError   */
   SKB_EINDEX = 3,    /* sparsekit::IndexError    */
   SKB_EINTERNAL = 4, /* sparsekit::InternalError */
-  SKB_ECUDA = 5      /* no reference analogue: CUDA runtime/driver failure */
+  SKB_ECUDA = 5,     /* no reference analogue: CUDA runtime/driver failure */
+  SKB_EFORMAT = 6,   /* sparsekit::FormatError; byte offset in skb_last_error_offset() */
+  SKB_EIO = 7        /* sparsekit::IoError       */
 } skb_status;
 
 /* MoEConfig, proj/include/sparsekit/model.hpp:15-29, as fixed-width ints. */
@@ -239,6 +241,21 @@ int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask);
 
 /* round-half-up count used by topk_mask (host arithmetic, no device needed). */
 int skb_n_off(double s, int n, int32_t* out);
+
+/* The "MOE1" weight file (save_weights / load_weights / weight_file_size,
+ * proj/src/model.cpp:180-282): magic "MOE1", six little-endian u32 (n_experts, top_k, d_model,
+ * d_ffn, d_shared, flags: bit 0 has_shared, bit 1 renormalize), then fp32 little-endian
+ * matrices: router, per expert gate / up / down_t, then the shared expert's three.
+ * skb_layer_load maps the file and builds the device image straight from it (no host copy of
+ * the fp32 weights); header checks, their order, messages and byte offsets follow load_weights.
+ * Errors: SKB_EIO (cannot open), SKB_EFORMAT (+ skb_last_error_offset()).  align_block = 64. */
+int skb_layer_load(const char* path, int device, skb_config* cfg_out, skb_layer** out);
+int skb_save_weights(const skb_config* cfg, const float* router, const float* const* gate,
+                     const float* const* up, const float* const* down_t, const float* shared_gate,
+                     const float* shared_up, const float* shared_down_t, const char* path);
+uint64_t skb_weight_file_size(const skb_config* cfg);
+/* Byte offset carried by the last SKB_EFORMAT on this thread (FormatError::offset). */
+uint64_t skb_last_error_offset(void);
 
 /* generate_tokens(), proj/src/model.cpp:168-178 over SplitMix64::next_gaussian
  * (proj/include/sparsekit/rng.hpp:42-55): batch*d_model standard normals, Box-Muller in double

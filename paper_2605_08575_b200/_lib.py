@@ -10,7 +10,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libsparsekit_b200.so")
 
-SKB_OK, SKB_ESHAPE, SKB_ECONFIG, SKB_EINDEX, SKB_EINTERNAL, SKB_ECUDA = range(6)
+SKB_OK, SKB_ESHAPE, SKB_ECONFIG, SKB_EINDEX, SKB_EINTERNAL, SKB_ECUDA, SKB_EFORMAT, SKB_EIO = range(8)
 MODE_DENSE, MODE_TOPK, MODE_MASKED, MODE_ROUTE_ONLY, MODE_THRESHOLD = 0, 1, 2, 3, 4
 FLAG_FAST_ROUTER, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES, FLAG_NO_PDL = 1, 2, 4, 8
 FLAG_GATHER_DOWN, FLAG_DENSE_DOWN, FLAG_BF16_H, FLAG_NO_FUSED_DECODE = 16, 32, 64, 128
@@ -26,6 +26,7 @@ EXPORTS = (
     "skb_layer_forward", "skb_layer_forward_device", "skb_layer_stage_times",
     "skb_layer_last_launches", "skb_layer_weight_bytes", "skb_route", "skb_align_dispatch",
     "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off", "skb_generate_tokens",
+    "skb_layer_load", "skb_save_weights", "skb_weight_file_size", "skb_last_error_offset",
 )
 
 
@@ -99,5 +100,11 @@ def load() -> C.CDLL:
     L.skb_topk_mask.argtypes = [vp, C.c_int, C.c_int, C.c_double, vp]
     L.skb_n_off.argtypes = [C.c_double, C.c_int, C.POINTER(i32)]
     L.skb_generate_tokens.argtypes = [C.c_int32, C.c_int32, C.c_uint64, vp]
+    L.skb_layer_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(SkbConfig), C.POINTER(vp)]
+    L.skb_save_weights.argtypes = [C.POINTER(SkbConfig), vp, vp, vp, vp, vp, vp, vp, C.c_char_p]
+    L.skb_weight_file_size.argtypes = [C.POINTER(SkbConfig)]
+    L.skb_weight_file_size.restype = C.c_uint64
+    L.skb_last_error_offset.argtypes = []
+    L.skb_last_error_offset.restype = C.c_uint64
     _lib = L
     return L

@@ -1,6 +1,10 @@
 // api.cu -- the C ABI of include/sparsekit_b200.h: host-side validation (same order and
 // messages as the reference), device weight image, workspaces, stage sequencing.
 #include <cstdarg>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cstdio>
 #include <cstring>
 #include <cmath>
@@ -18,6 +22,7 @@ using namespace skb;
 namespace {
 
 thread_local std::string g_err;
+thread_local uint64_t g_err_offset = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -832,6 +837,161 @@ int skb_n_off(double s, int n, int32_t* out) {
   if (!(s >= 0.0 && s <= 1.0)) return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
   if (n < 0 || out == nullptr) return fail(SKB_ESHAPE, "n_off: bad arguments");
   *out = n_off_of(s, n);
+  return SKB_OK;
+}
+
+// ---- "MOE1" weight files (proj/src/model.cpp:180-282) ---------------------------------------
+
+uint64_t skb_last_error_offset(void) { return g_err_offset; }
+
+uint64_t skb_weight_file_size(const skb_config* c) {
+  if (c == nullptr) return 0;
+  const uint64_t D = static_cast<uint64_t>(c->d_model) * sizeof(float);
+  uint64_t n = 28 + static_cast<uint64_t>(c->n_experts) * D +
+               3ull * c->n_experts * static_cast<uint64_t>(c->d_ffn) * D;
+  if (c->has_shared) n += 3ull * static_cast<uint64_t>(c->d_shared) * D;
+  return n;
+}
+
+static int format_error(uint64_t at, const char* what) {
+  g_err_offset = at;
+  return fail(SKB_EFORMAT, "%s (offset %llu)", what, static_cast<unsigned long long>(at));
+}
+
+static bool host_is_little_endian() {
+  const uint32_t probe = 1;
+  unsigned char b;
+  std::memcpy(&b, &probe, 1);
+  return b == 1;
+}
+
+int skb_layer_load(const char* path, int device, skb_config* cfg_out, skb_layer** out) {
+  if (path == nullptr || out == nullptr) return fail(SKB_EINTERNAL, "layer_load: null argument");
+  if (!host_is_little_endian())
+    return fail(SKB_EINTERNAL, "layer_load: the mapped-file loader needs a little-endian host");
+  const int fd = ::open(path, O_RDONLY);
+  if (fd < 0) return fail(SKB_EIO, "cannot open for reading: %s", path);
+  struct stat st {};
+  if (::fstat(fd, &st) != 0) {
+    ::close(fd);
+    return fail(SKB_EIO, "cannot open for reading: %s", path);
+  }
+  const uint64_t size = static_cast<uint64_t>(st.st_size);
+  const unsigned char* base = nullptr;
+  if (size > 0) {
+    void* m = ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+    if (m == MAP_FAILED) {
+      ::close(fd);
+      return fail(SKB_EIO, "cannot open for reading: %s", path);
+    }
+    base = static_cast<const unsigned char*>(m);
+  }
+  ::close(fd);
+  auto done = [&](int rc) {
+    if (base != nullptr) ::munmap(const_cast<unsigned char*>(base), size);
+    return rc;
+  };
+  // the reference reads 4 bytes at a time: a short file stops at the last whole word
+  const uint64_t whole = size / 4 * 4;
+  if (size < 4) return done(format_error(0, "truncated file"));
+  if (std::memcmp(base, "MOE1", 4) != 0) return done(format_error(0, "bad magic, expected MOE1"));
+  if (size < 28) return done(format_error(whole, "truncated file"));
+  auto u32 = [&](uint64_t off) {
+    return static_cast<uint32_t>(base[off]) | (static_cast<uint32_t>(base[off + 1]) << 8) |
+           (static_cast<uint32_t>(base[off + 2]) << 16) | (static_cast<uint32_t>(base[off + 3]) << 24);
+  };
+  skb_config c{};
+  c.n_experts = static_cast<int32_t>(u32(4));
+  c.top_k = static_cast<int32_t>(u32(8));
+  c.d_model = static_cast<int32_t>(u32(12));
+  c.d_ffn = static_cast<int32_t>(u32(16));
+  c.d_shared = static_cast<int32_t>(u32(20));
+  const uint32_t flags = u32(24);
+  c.has_shared = (flags & 1u) ? 1 : 0;
+  c.renormalize = (flags & 2u) ? 1 : 0;
+  c.align_block = 64;
+  if (c.n_experts < 1) return done(format_error(4, "header: n_experts < 1"));
+  if (c.top_k < 1 || c.top_k > c.n_experts)
+    return done(format_error(8, "header: top_k outside [1, n_experts]"));
+  if (c.d_model < 1) return done(format_error(12, "header: d_model < 1"));
+  if (c.d_ffn < 1) return done(format_error(16, "header: d_ffn < 1"));
+  if ((c.has_shared != 0) != (c.d_shared > 0))
+    return done(format_error(20, "header: shared flag disagrees with d_shared"));
+  const uint64_t want = skb_weight_file_size(&c);
+  if (size < want) return done(format_error(whole, "truncated file"));
+  if (size > want) return done(format_error(want, "trailing bytes after weight payload"));
+
+  const size_t E = static_cast<size_t>(c.n_experts);
+  const uint64_t mat = static_cast<uint64_t>(c.d_ffn) * c.d_model * sizeof(float);
+  const unsigned char* p = base + 28;
+  const float* router = reinterpret_cast<const float*>(p);  // 28 is a multiple of 4
+  p += E * c.d_model * sizeof(float);
+  std::vector<const float*> gate(E), up(E), down(E);
+  for (size_t e = 0; e < E; ++e) {
+    gate[e] = reinterpret_cast<const float*>(p);
+    up[e] = reinterpret_cast<const float*>(p + mat);
+    down[e] = reinterpret_cast<const float*>(p + 2 * mat);
+    p += 3 * mat;
+  }
+  const float *sg = nullptr, *su = nullptr, *sd = nullptr;
+  if (c.has_shared) {
+    const uint64_t smat = static_cast<uint64_t>(c.d_shared) * c.d_model * sizeof(float);
+    sg = reinterpret_cast<const float*>(p);
+    su = reinterpret_cast<const float*>(p + smat);
+    sd = reinterpret_cast<const float*>(p + 2 * smat);
+  }
+  if (cfg_out != nullptr) *cfg_out = c;
+  return done(skb_layer_create(&c, router, gate.data(), up.data(), down.data(), sg, su, sd, device, out));
+}
+
+int skb_save_weights(const skb_config* cfg, const float* router, const float* const* gate,
+                     const float* const* up, const float* const* down_t, const float* shared_gate,
+                     const float* shared_up, const float* shared_down_t, const char* path) {
+  int rc = validate_cfg(cfg);  // save_weights validates first (model.cpp:191)
+  if (rc) return rc;
+  if (path == nullptr || router == nullptr || gate == nullptr || up == nullptr || down_t == nullptr ||
+      (cfg->has_shared && (shared_gate == nullptr || shared_up == nullptr || shared_down_t == nullptr)))
+    return fail(SKB_EINTERNAL, "save_weights: null argument");
+  FILE* f = std::fopen(path, "wb");
+  if (f == nullptr) return fail(SKB_EIO, "cannot open for writing: %s", path);
+  auto put_u32 = [&](uint32_t v) {
+    const unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                                static_cast<unsigned char>(v >> 16), static_cast<unsigned char>(v >> 24)};
+    std::fwrite(b, 1, 4, f);
+  };
+  const bool le = host_is_little_endian();
+  auto put_matrix = [&](const float* m, size_t count) {
+    if (le) {
+      std::fwrite(m, sizeof(float), count, f);
+    } else {
+      for (size_t i = 0; i < count; ++i) {
+        uint32_t bits;
+        std::memcpy(&bits, m + i, 4);
+        put_u32(bits);
+      }
+    }
+  };
+  std::fwrite("MOE1", 1, 4, f);
+  put_u32(static_cast<uint32_t>(cfg->n_experts));
+  put_u32(static_cast<uint32_t>(cfg->top_k));
+  put_u32(static_cast<uint32_t>(cfg->d_model));
+  put_u32(static_cast<uint32_t>(cfg->d_ffn));
+  put_u32(static_cast<uint32_t>(cfg->d_shared));
+  put_u32((cfg->has_shared ? 1u : 0u) | (cfg->renormalize ? 2u : 0u));
+  const size_t D = static_cast<size_t>(cfg->d_model);
+  put_matrix(router, static_cast<size_t>(cfg->n_experts) * D);
+  for (int e = 0; e < cfg->n_experts; ++e) {
+    put_matrix(gate[e], static_cast<size_t>(cfg->d_ffn) * D);
+    put_matrix(up[e], static_cast<size_t>(cfg->d_ffn) * D);
+    put_matrix(down_t[e], static_cast<size_t>(cfg->d_ffn) * D);
+  }
+  if (cfg->has_shared) {
+    put_matrix(shared_gate, static_cast<size_t>(cfg->d_shared) * D);
+    put_matrix(shared_up, static_cast<size_t>(cfg->d_shared) * D);
+    put_matrix(shared_down_t, static_cast<size_t>(cfg->d_shared) * D);
+  }
+  const bool bad = std::ferror(f) != 0;
+  if (std::fclose(f) != 0 || bad) return fail(SKB_EIO, "write failed");
   return SKB_OK;
 }
 

@@ -48,13 +48,30 @@ class CudaError(RuntimeError):
     pass
 
 
+class FormatError(RuntimeError):
+    """File-format violation; carries the byte offset where parsing stopped (errors.hpp:36-43)."""
+
+    def __init__(self, msg: str, offset: int = 0):
+        super().__init__(msg)
+        self.offset = offset
+
+
+class IoError(RuntimeError):
+    pass
+
+
 _ERR = {_lib.SKB_ESHAPE: ShapeError, _lib.SKB_ECONFIG: ConfigError, _lib.SKB_EINDEX: IndexError_,
         _lib.SKB_EINTERNAL: InternalError, _lib.SKB_ECUDA: CudaError}
 
 
 def _check(rc: int) -> None:
     if rc != 0:
-        raise _ERR.get(rc, InternalError)(_lib.load().skb_last_error().decode())
+        msg = _lib.load().skb_last_error().decode()
+        if rc == _lib.SKB_EFORMAT:
+            raise FormatError(msg, int(_lib.load().skb_last_error_offset()))
+        if rc == _lib.SKB_EIO:
+            raise IoError(msg)
+        raise _ERR.get(rc, InternalError)(msg)
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -197,6 +214,18 @@ class MoELayerWeights:
         h = C.c_void_p()
         _check(L.skb_layer_create(C.byref(cfg), _ptr(r), g, u, d, _ptr(sh[0]), _ptr(sh[1]),
                                   _ptr(sh[2]), device, C.byref(h)))
+        return cls(config, h.value)
+
+    @classmethod
+    def load(cls, path, device: int = 0) -> "MoELayerWeights":
+        """load_weights (proj/src/model.cpp:218-282) straight into the device image: the "MOE1"
+        file is mapped and converted expert by expert, no host copy of the fp32 weights.
+        Raises FormatError (with .offset) / IoError like the reference."""
+        cfg = SkbConfig()
+        h = C.c_void_p()
+        _check(_lib.load().skb_layer_load(str(path).encode(), device, C.byref(cfg), C.byref(h)))
+        config = MoEConfig(cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ffn, bool(cfg.has_shared),
+                           cfg.d_shared, bool(cfg.renormalize), cfg.align_block)
         return cls(config, h.value)
 
     @classmethod
@@ -428,6 +457,35 @@ def forward_sparse(w: MoELayerWeights, x, threshold: float, threads: int = 1, *,
         raise ConfigError("forward_sparse: threshold must be >= 0")
     return _forward(w, x, MODE_THRESHOLD, flags=flags, capture=capture, y_out=y_out,
                     tau=float(threshold))
+
+
+# ---- "MOE1" weight files (model.hpp:59-63, model.cpp:180-282) ---------------------------------
+def weight_file_size(config: MoEConfig) -> int:
+    cfg = config.c()
+    return int(_lib.load().skb_weight_file_size(C.byref(cfg)))
+
+
+def save_weights(config: MoEConfig, path, router, gate, up, down_t, shared_gate=None,
+                 shared_up=None, shared_down_t=None) -> None:
+    """save_weights, model.cpp:190-216 (host arrays in, file out; validates the config first)."""
+    config.validate()
+    E = config.n_experts
+    keep = []
+
+    def mats(m):
+        ptrs = []
+        for e in range(E):
+            a = np.ascontiguousarray(m[e], dtype=np.float32)
+            keep.append(a)
+            ptrs.append(a.ctypes.data)
+        return (C.c_void_p * E)(*ptrs)
+
+    r = np.ascontiguousarray(router, dtype=np.float32)
+    sh = [None if m is None else np.ascontiguousarray(m, dtype=np.float32)
+          for m in (shared_gate, shared_up, shared_down_t)]
+    cfg = config.c()
+    _check(_lib.load().skb_save_weights(C.byref(cfg), _ptr(r), mats(gate), mats(up), mats(down_t),
+                                        _ptr(sh[0]), _ptr(sh[1]), _ptr(sh[2]), str(path).encode()))
 
 
 # ---- neuron budgets (budget.hpp, budget.cpp) -------------------------------------------------

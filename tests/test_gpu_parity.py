@@ -7,6 +7,8 @@ Bars (BASELINE.json north_star):
     operands, and <= 1e-2 against the oracle on the unrounded fp32 operands;
   * end-to-end selection masks agree on >= 99.9 % of neurons.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -965,3 +967,56 @@ def test_equal_ratio_budget_is_the_plain_topk_forward(skb, oracle):
     assert a.outputs.tobytes() == b.outputs.tobytes()
     with pytest.raises(skb.ShapeError):
         skb.layer._forward(layer, x, skb.MODE_TOPK, s_routed=0.5, slot_n_off=[1, 2])
+
+
+# ---------------------------------------------------------------------------------------------
+# golden fixtures of the unmodified reference (tests/golden/make_golden.py)
+# ---------------------------------------------------------------------------------------------
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_cuda_layer_vs_the_reference_outputs_on_file(skb):
+    """No oracle in the loop: the device layer against outputs the reference itself produced."""
+    g = np.load(os.path.join(GOLDEN, "layer_e8k2d96n160s48.npz"))
+    cfg = skb.MoEConfig(8, 2, 96, 160, True, 48, True, 64)
+    layer = skb.MoELayerWeights.generate_synthetic(cfg, 11, 0.1)  # bf16 image == round_bf16
+    x = g["x"]
+    assert max_rel_diff(skb.forward_dense(layer, x).outputs, g["y_dense"]) <= TOL_FP32_ACCUM
+    lvl = skb.SparsityLevel(0.5)
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl, capture=True)
+    assert np.mean(rep.masks.routed.reshape(-1) == g["routed"].reshape(-1)) >= MASK_AGREEMENT
+    assert np.mean(rep.masks.shared.reshape(-1) == g["shared"].reshape(-1)) >= MASK_AGREEMENT
+    masks = skb.MaskSet(g["routed"].reshape(5, 2, 160), g["shared"].reshape(5, 48))
+    masked = skb.forward_masked_dense(layer, x, masks)
+    assert max_rel_diff(masked.outputs, g["y_masked"]) <= TOL_FP32_ACCUM
+    assert masked.active_neurons_total == int(g["rep_masked"][0])
+    if np.array_equal(rep.masks.routed.reshape(-1), g["routed"].reshape(-1)):
+        assert max_rel_diff(rep.outputs, g["y_masked"]) <= TOL_FP32_ACCUM
+    sp = skb.forward_sparse(layer, x, 0.05)
+    assert max_rel_diff(sp.outputs, g["y_sparse"]) <= TOL_BF16
+    want = [int(v) for v in g["rep_sparse"]]
+    got = [sp.macs.gate_macs, sp.macs.up_macs, sp.macs.down_macs, sp.macs.other_macs,
+           sp.active_neurons_total, sp.tiles_total, sp.tiles_skipped]
+    assert got[0] == want[0] and got[3] == want[3] and got[5] == want[5]
+    assert abs(got[4] - want[4]) <= 2  # a survivor within float noise of tau may flip
+    if got[4] == want[4]:
+        assert got == want and max_rel_diff(sp.outputs, g["y_sparse"]) <= TOL_FP32_ACCUM
+
+
+@pytest.mark.parametrize("name,cfg,seed", [("moe1_e4k2d8n16_seed1.moe", Config(4, 2, 8, 16, 0, True), 1),
+                                           ("moe1_e3k2d8n8s4_seed7.moe", Config(3, 2, 8, 8, 4, False), 7)])
+def test_layer_loaded_from_a_reference_file(skb, oracle, name, cfg, seed):
+    """load_weights into the device image == the same weights ingested from arrays."""
+    loaded = skb.MoELayerWeights.load(os.path.join(GOLDEN, name))
+    c = loaded.config
+    assert (c.n_experts, c.top_k, c.d_model, c.d_ffn, c.d_shared, c.has_shared, c.renormalize) == (
+        cfg.n_experts, cfg.top_k, cfg.d_model, cfg.d_ffn, cfg.d_shared, bool(cfg.has_shared),
+        cfg.renormalize)
+    w = oracle.generate_synthetic(cfg, seed, 0.05)
+    from_arrays = make_layer(skb, w)
+    x = oracle.round_bf16(oracle.generate_tokens(7, cfg.d_model, 3))
+    a = skb.forward_dense(loaded, x)
+    b = skb.forward_dense(from_arrays, x)
+    assert a.outputs.tobytes() == b.outputs.tobytes()
+    y_ref, _ = oracle.forward(w.rounded_bf16(), x)
+    assert max_rel_diff(a.outputs, y_ref) <= TOL_FP32_ACCUM
