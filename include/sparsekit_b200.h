@@ -100,6 +100,12 @@ enum {
 #define SKB_FLAG_FUSED_DECODE 0x100u   /* batches <= 16: take the persistent decode kernel even where
                                           the cost model prefers the staged kernels */
 
+#define SKB_FLAG_NO_PAIRED_BLOCKS 0x200u /* batch GEMMs: one 128-row weight block per CTA instead of
+                                           two sharing each token tile (A/B measurements) */
+
+#define SKB_FLAG_PAIRED_BLOCKS 0x400u    /* batch GEMMs: pair weight blocks whenever the token tile is
+                                           >= 64 rows, whatever the grid-size heuristic says (tests) */
+
 #define SKB_N_STAGES 6 /* router, dispatch, gateup, select, down, combine */
 
 typedef struct skb_forward_args {

@@ -15,6 +15,8 @@ MODE_DENSE, MODE_TOPK, MODE_MASKED, MODE_ROUTE_ONLY, MODE_THRESHOLD = 0, 1, 2, 3
 FLAG_FAST_ROUTER, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES, FLAG_NO_PDL = 1, 2, 4, 8
 FLAG_GATHER_DOWN, FLAG_DENSE_DOWN, FLAG_BF16_H, FLAG_NO_FUSED_DECODE = 16, 32, 64, 128
 FLAG_FUSED_DECODE = 256
+FLAG_NO_PAIRED_BLOCKS = 0x200
+FLAG_PAIRED_BLOCKS = 0x400
 N_STAGES = 6
 STAGE_NAMES = ("router", "dispatch", "gateup", "select", "down", "combine")
 

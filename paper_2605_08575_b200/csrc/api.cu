@@ -574,6 +574,19 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   while (kTileCases[tn_idx] != tn) ++tn_idx;
   const int max_tiles = max_tiles_for(g, B, tn);
 
+  // Paired weight blocks (gateup.cu): worth it once the tile list alone covers most SMs with
+  // half as many CTAs; below that the extra CTAs' parallelism is worth more than the bytes.
+  const int est_tiles = (g.E < BK ? g.E : BK) + (g.has_shared ? 1 : 0);
+  const auto pair_for = [&](int mblocks) {
+    return tn >= 64 && !(a->flags & SKB_FLAG_NO_PAIRED_BLOCKS) &&
+           ((a->flags & SKB_FLAG_PAIRED_BLOCKS) ||
+            est_tiles * ceil_div(mblocks, 2) * 4 >= L->n_sms * 3);
+  };
+  // gate/up: measured slower paired (Granite shape batch 256: 25.5 -> 29.7 us stage time, half as
+  // many CTAs each with the same bytes in flight); only on request
+  const bool pair_gateup = (a->flags & SKB_FLAG_PAIRED_BLOCKS) && pair_for(g.Np / kNeuronBlock);
+  const bool pair_down = pair_for(g.Dp128 / 128);
+
   tm.mark();
   if (d_ids_in != nullptr) {
     // external routing: ids (and weights, default 1) are given; only the dispatch runs
@@ -615,7 +628,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   else
     launches += launch_gateup_tc(ctx, &L->tmap_w, token_tiles ? &L->tmap_xb : &L->tmap_x[tn_idx],
                                  tn, L->disp, max_tiles, g, L->d_h, token_tiles,
-                                 sel_mode == kSelectThreshold ? L->d_sg : nullptr);
+                                 sel_mode == kSelectThreshold ? L->d_sg : nullptr, pair_gateup);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel
@@ -658,7 +671,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   if (dense_down) {
     launches += launch_down_tc(ctx, &L->tmap_wdt, g.has_shared ? &L->tmap_wdt_shared : nullptr,
                                L->tmap_hb[tn_idx], nsplit, tn, L->disp, max_tiles, g,
-                               L->d_slot_out);
+                               L->d_slot_out, pair_down);
     tm.mark();
     launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y);
     tm.mark();

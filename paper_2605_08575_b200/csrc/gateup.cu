@@ -38,10 +38,15 @@ constexpr int kATileBytes = 128 * kBlockK * 2;  // 16 KB: 128 rows x 128 B
 
 constexpr int kMaxSplit = 3;
 __host__ __device__ constexpr int b_tile_bytes(int tn) { return tn * kBlockK * 2; }
-__host__ __device__ constexpr int stage_bytes(int tn, int mode) {
-  return kATileBytes + (mode == 0 ? 1 : kMaxSplit) * b_tile_bytes(tn);
+// MB = 128-row A blocks per CTA.  MB = 2 ("paired blocks"): two weight blocks of the same expert
+// share every token tile a CTA fetches, so the bytes an SM ingests per unit of work drop by 25 %
+// (gate/up) to 37 % (down, three h terms per tile).  Measured bound of these kernels is per-SM
+// ingest (~45 GB/s per SM when all SMs pull, tools/micro/stream_bw.cu), not HBM.
+__host__ __device__ constexpr int stage_bytes(int tn, int mode, int mb = 1) {
+  return mb * kATileBytes + (mode == 0 ? 1 : kMaxSplit) * b_tile_bytes(tn);
 }
-__host__ __device__ constexpr int num_stages(int tn, int mode) {
+__host__ __device__ constexpr int num_stages(int tn, int mode, int mb = 1) {
+  if (mb == 2) return mode == 0 ? (tn <= 64 ? 5 : 4) : (tn <= 64 ? 3 : 2);
   // MODE 0: <= ~110 KB per CTA so that two CTAs share an SM (grids larger than the SM count then
   // run in one wave and one CTA's prologue/epilogue overlaps the other's stream); ~100 KB in
   // flight per CTA is still several times the latency-bandwidth product per SM.
@@ -49,8 +54,9 @@ __host__ __device__ constexpr int num_stages(int tn, int mode) {
                    : (tn <= 16 ? 9 : (tn <= 32 ? 7 : (tn <= 64 ? 5 : 3)));
 }
 __host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
-__host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode) {
-  return num_stages(tn, mode) * stage_bytes(tn, mode) + 1024 /*alignment slack*/ + 256 /*barriers*/;
+__host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode, int mb = 1) {
+  return num_stages(tn, mode, mb) * stage_bytes(tn, mode, mb) + 1024 /*alignment slack*/ +
+         256 /*barriers*/;
 }
 
 }  // namespace
@@ -72,17 +78,18 @@ struct TcArgs {
   int nsplit;                          // MODE 1: B operands accumulated per K block (1 or 3)
 };
 
-template <int TN, int MODE>
-__global__ void __launch_bounds__(kGateupThreads, MODE == 0 ? 2 : 1)
+template <int TN, int MODE, int MB>
+__global__ void __launch_bounds__(kGateupThreads, (MODE == 0 && MB == 1) ? 2 : 1)
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,
                   const __grid_constant__ CUtensorMap tmap_b1,
                   const __grid_constant__ CUtensorMap tmap_b2, const TcArgs a) {
-  constexpr int kStages = num_stages(TN, MODE);
-  constexpr int kStageBytes = stage_bytes(TN, MODE);
+  constexpr int kStages = num_stages(TN, MODE, MB);
+  constexpr int kStageBytes = stage_bytes(TN, MODE, MB);
   constexpr int kBTile = b_tile_bytes(TN);
-  constexpr uint32_t kTmemCols = tmem_cols(TN);
+  constexpr int kAll = MB * kATileBytes;  // A tiles of one stage; the B tiles follow
+  constexpr uint32_t kTmemCols = tmem_cols(TN) * MB;
   constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
 
   extern __shared__ uint8_t smem_raw[];
@@ -128,7 +135,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
     row0 = a.tile_row0[tile];
     nrows = a.tile_nrows[tile];
     shared_expert = e >= a.n_experts;
-    active = static_cast<int>(blockIdx.x) < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
+    active = static_cast<int>(blockIdx.x) * MB < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
   }
 
   if (active) {
@@ -140,7 +147,10 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
     const bool own_map = (MODE == 1) && shared_expert;
     const CUtensorMap* map_a = own_map ? &tmap_a_shared : &tmap_a;
     const int a_row = (own_map ? 0 : (shared_expert ? a.n_experts : e) * a.rows_per_expert) +
-                      static_cast<int>(blockIdx.x) * 128;
+                      static_cast<int>(blockIdx.x) * MB * 128;
+    // A blocks this CTA really has (an odd block count leaves the last CTA with one)
+    const int n_mb = min(MB, (shared_expert ? a.mblocks_shared : a.mblocks_routed) -
+                                 static_cast<int>(blockIdx.x) * MB);
 
     if (warp == 0) {
       if (lane == 0) {
@@ -148,18 +158,21 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           const int s = kb % kStages;
           const uint32_t ph = (kb / kStages) & 1u;
           mbar_wait(empty_bar(s), ph ^ 1u);
-          mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * kBTile);
+          mbar_arrive_expect_tx(full_bar(s), n_mb * kATileBytes + nsplit * kBTile);
           const uint32_t a_smem = smem_base + s * kStageBytes;
           // tiled image: tile (a_row / 128, kb) is 128 consecutive rows of the 64-column view
-          tma_load_2d(a_smem, map_a, 0, ((a_row >> 7) * num_k_blocks + kb) * 128, full_bar(s),
-                      kPolicyEvictFirst);
-          tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s),
-                      kPolicyEvictLast);
+#pragma unroll
+          for (int m = 0; m < MB; ++m)
+            if (m < n_mb)
+              tma_load_2d(a_smem + m * kATileBytes, map_a, 0,
+                          (((a_row >> 7) + m) * num_k_blocks + kb) * 128, full_bar(s),
+                          kPolicyEvictFirst);
+          tma_load_2d(a_smem + kAll, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
           if (MODE == 1 && nsplit > 1) {
-            tma_load_2d(a_smem + kATileBytes + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
+            tma_load_2d(a_smem + kAll + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
                         kPolicyEvictLast);
-            tma_load_2d(a_smem + kATileBytes + 2 * kBTile, &tmap_b2, kb * kBlockK, row0,
-                        full_bar(s), kPolicyEvictLast);
+            tma_load_2d(a_smem + kAll + 2 * kBTile, &tmap_b2, kb * kBlockK, row0, full_bar(s),
+                        kPolicyEvictLast);
           }
         }
       }
@@ -171,16 +184,21 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           mbar_wait(full_bar(s), ph);
           tc_fence_after();
           const uint32_t a_smem = smem_base + s * kStageBytes;
-          const uint64_t a_desc = make_smem_desc_sw128(a_smem);
 #pragma unroll
-          for (int sp = 0; sp < (MODE == 0 ? 1 : kMaxSplit); ++sp) {
-            if (sp < nsplit) {
-              const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes + sp * kBTile);
+          for (int m = 0; m < MB; ++m) {
+            if (m < n_mb) {
+              const uint64_t a_desc = make_smem_desc_sw128(a_smem + m * kATileBytes);
 #pragma unroll
-              for (int k = 0; k < kBlockK / 16; ++k) {
-                // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
-                umma_bf16(tmem_base, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
-                          (kb | k | sp) != 0 ? 1u : 0u);
+              for (int sp = 0; sp < (MODE == 0 ? 1 : kMaxSplit); ++sp) {
+                if (sp < nsplit) {
+                  const uint64_t b_desc = make_smem_desc_sw128(a_smem + kAll + sp * kBTile);
+#pragma unroll
+                  for (int k = 0; k < kBlockK / 16; ++k) {
+                    // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
+                    umma_bf16(tmem_base + static_cast<uint32_t>(m * TN), a_desc + 2u * k,
+                              b_desc + 2u * k, kIdesc, (kb | k | sp) != 0 ? 1u : 0u);
+                  }
+                }
               }
             }
           }
@@ -194,14 +212,17 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int m_valid = shared_expert ? a.m_shared : a.m_routed;
       mbar_wait(tmem_full_bar, 0);
       tc_fence_after();
+#pragma unroll 1
+      for (int m = 0; m < n_mb; ++m) {
+      const uint32_t tmem_blk = tmem_base + static_cast<uint32_t>(m * TN);
       if (MODE == 0) {
-        const int n = static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15);
+        const int n = (static_cast<int>(blockIdx.x) * MB + m) * kNeuronBlock + 16 * q + (lane & 15);
         const bool is_gate_lane = lane < 16;
 #pragma unroll 1
         for (int c0 = 0; c0 < TN; c0 += 16) {
           if (c0 >= nrows) break;
           uint32_t v[16];
-          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+          tmem_ld_32x32b_x16(tmem_blk + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 16; c += 2) {
@@ -226,12 +247,12 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           }
         }
       } else {
-        const int d = static_cast<int>(blockIdx.x) * 128 + 32 * q + lane;
+        const int d = (static_cast<int>(blockIdx.x) * MB + m) * 128 + 32 * q + lane;
 #pragma unroll 1
         for (int c0 = 0; c0 < TN; c0 += 16) {
           if (c0 >= nrows) break;
           uint32_t v[16];
-          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+          tmem_ld_32x32b_x16(tmem_blk + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
           tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 16; ++c)
@@ -239,6 +260,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
               a.out[static_cast<size_t>(row0 + c0 + c) * a.out_stride + d] = __uint_as_float(v[c]);
         }
       }
+      }  // A blocks
       tc_fence_before();
     }
   }
@@ -258,14 +280,14 @@ static int pick_tile_case(int tile_tokens) {
   return 256;
 }
 
-template <int TN, int MODE>
+template <int TN, int MODE, int MB = 1>
 static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
                            const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
                            const TcArgs& a, int grid_x, int max_tiles) {
   static bool attr_set = false;
-  constexpr int smem = gateup_smem_bytes(TN, MODE);
+  constexpr int smem = gateup_smem_bytes(TN, MODE, MB);
   if (!attr_set) {
-    cudaFuncSetAttribute(grouped_tc_kernel<TN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(grouped_tc_kernel<TN, MODE, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     attr_set = true;
   }
@@ -276,15 +298,15 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
   cfg.attrs = attr;
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
-  cfg.gridDim = dim3(grid_x, max_tiles);
+  cfg.gridDim = dim3(ceil_div(grid_x, MB), max_tiles);
   cfg.blockDim = dim3(kGateupThreads);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, grouped_tc_kernel<TN, MODE>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
+  cudaLaunchKernelEx(&cfg, grouped_tc_kernel<TN, MODE, MB>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
 }
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles, float* sg) {
+                     float* h, bool token_tiles, float* sg, bool pair_blocks) {
   TcArgs a{};
   a.sg_out = sg;
   a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;
@@ -303,6 +325,14 @@ int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUte
   a.rows_per_expert = 2 * g.Np;
   a.nsplit = 1;
   const int gx = a.mblocks_routed > a.mblocks_shared ? a.mblocks_routed : a.mblocks_shared;
+  if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
+    launch_tc_case<64, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles);
+    return 1;
+  }
+  if (pair_blocks && pick_tile_case(tile_tokens) == 128) {
+    launch_tc_case<128, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles);
+    return 1;
+  }
   switch (pick_tile_case(tile_tokens)) {
     case 16: launch_tc_case<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
     case 32: launch_tc_case<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
@@ -316,7 +346,7 @@ int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUte
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
-                   const Geometry& g, float* slot_out) {
+                   const Geometry& g, float* slot_out, bool pair_blocks) {
   TcArgs a{};
   a.tile_expert = d.tile_expert;
   a.tile_row0 = d.tile_row0;
@@ -333,6 +363,14 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
   a.nsplit = nsplit;
   const CUtensorMap* sh = tmap_wdt_shared ? tmap_wdt_shared : tmap_wdt;
   const int gx = a.mblocks_routed;
+  if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
+    launch_tc_case<64, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles);
+    return 1;
+  }
+  if (pair_blocks && pick_tile_case(tile_tokens) >= 128) {
+    launch_tc_case<128, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles);
+    return 1;
+  }
   switch (pick_tile_case(tile_tokens)) {
     case 16: launch_tc_case<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
     case 32: launch_tc_case<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;

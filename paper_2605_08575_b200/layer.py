@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (FLAG_BF16_H, FLAG_DENSE_DOWN, FLAG_FAST_ROUTER, FLAG_GATHER_DOWN,  # noqa: F401
-                   FLAG_FUSED_DECODE, FLAG_NO_FUSED_DECODE, FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,
+                   FLAG_FUSED_DECODE, FLAG_NO_FUSED_DECODE, FLAG_NO_PAIRED_BLOCKS, FLAG_PAIRED_BLOCKS, FLAG_NO_PDL, FLAG_SIMT_GATEUP, FLAG_TIME_STAGES,
                    MODE_DENSE, MODE_MASKED, MODE_ROUTE_ONLY, MODE_THRESHOLD, MODE_TOPK, STAGE_NAMES,
                    SkbConfig,
                    SkbForwardArgs,

@@ -1020,3 +1020,31 @@ def test_layer_loaded_from_a_reference_file(skb, oracle, name, cfg, seed):
     assert a.outputs.tobytes() == b.outputs.tobytes()
     y_ref, _ = oracle.forward(w.rounded_bf16(), x)
     assert max_rel_diff(a.outputs, y_ref) <= TOL_FP32_ACCUM
+
+
+# ---------------------------------------------------------------------------------------------
+# batch GEMMs with paired weight blocks (two 128-row blocks per CTA share each token tile)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", [(4, 2, 96, 160, 0, True, 100),     # TN 128; 3 gate/up blocks, 1 down block
+                                  (8, 2, 320, 256, 0, True, 150),    # TN 64; 4 and 3 blocks
+                                  (4, 2, 256, 200, 136, True, 120),  # shared expert with its own block counts
+                                  (6, 3, 130, 70, 0, False, 97)])    # ragged everything
+def test_paired_blocks_match_single_blocks_and_oracle(skb, oracle, case):
+    E, K, D, N, S, renorm, B = case
+    cfg = Config(E, K, D, N, S, renorm)
+    w, x = rounded_case(oracle, cfg, seed=E * 7 + K, scale=0.1, batch=B, token_seed=12)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    sh = lvl if S else None
+    base = skb.FLAG_DENSE_DOWN
+    paired = skb.forward_topk_sparse(layer, x, lvl, sh, flags=base | skb.FLAG_PAIRED_BLOCKS, capture=True)
+    single = skb.forward_topk_sparse(layer, x, lvl, sh, flags=base | skb.FLAG_NO_PAIRED_BLOCKS, capture=True)
+    # the same MMAs in the same order into separate accumulators: bit-identical
+    assert paired.h_routed.tobytes() == single.h_routed.tobytes()
+    assert paired.outputs.tobytes() == single.outputs.tobytes()
+    np.testing.assert_array_equal(paired.masks.routed, single.masks.routed)
+    y_same, _ = oracle.forward(w, x, paired.masks.routed, paired.masks.shared if S else None)
+    assert max_rel_diff(paired.outputs, y_same) <= TOL_FP32_ACCUM
+    dense_p = skb.forward_dense(layer, x, flags=base | skb.FLAG_PAIRED_BLOCKS)
+    y_ref, _ = oracle.forward(w, x)
+    assert max_rel_diff(dense_p.outputs, y_ref) <= TOL_FP32_ACCUM
