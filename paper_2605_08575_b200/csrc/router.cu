@@ -761,30 +761,46 @@ int launch_dispatch(const LaunchCtx& ctx, const int32_t* ids, int B, int K, int 
 }
 
 // Token permutation: xs[row] = bf16(x[token(row)]); pad columns [D, Dp) stay zero (memset once).
+// One warp per row, 8 rows per CTA, eight 128-bit loads in flight per lane (a CTA per row was
+// 2048 tiny CTAs at batch 256: launch- and latency-bound).
 __global__ void __launch_bounds__(256) permute_tokens_kernel(const float* __restrict__ x,
                                                              const int32_t* __restrict__ perm,
-                                                             int BK, int K, int D, int Dp,
+                                                             int BK, int rows, int K, int D, int Dp,
                                                              __nv_bfloat16* __restrict__ xs) {
   pdl_wait();
   pdl_launch_dependents();
-  const int row = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
   const int t = (row < BK) ? perm[row] / K : row - BK;
   const float* src = x + static_cast<size_t>(t) * D;
   __nv_bfloat16* dst = xs + static_cast<size_t>(row) * Dp;
   if ((D % 4) == 0) {
     const float4* s4 = reinterpret_cast<const float4*>(src);
     uint2* d2 = reinterpret_cast<uint2*>(dst);
-    for (int q = threadIdx.x; q < D / 4; q += blockDim.x) {
-      const float4 v = __ldg(s4 + q);
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
-      uint2 o;
-      o.x = *reinterpret_cast<uint32_t*>(&lo);
-      o.y = *reinterpret_cast<uint32_t*>(&hi);
-      d2[q] = o;
+    const int nq = D / 4;
+    for (int q0 = 0; q0 < nq; q0 += 256) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u * 32 + lane;
+        if (q < nq) v[u] = __ldg(s4 + q);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u * 32 + lane;
+        if (q < nq) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v[u].x, v[u].y);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(v[u].z, v[u].w);
+          uint2 o;
+          o.x = *reinterpret_cast<uint32_t*>(&lo);
+          o.y = *reinterpret_cast<uint32_t*>(&hi);
+          d2[q] = o;
+        }
+      }
     }
   } else {
-    for (int dd = threadIdx.x; dd < D; dd += blockDim.x) dst[dd] = __float2bfloat16_rn(src[dd]);
+    for (int dd = lane; dd < D; dd += 32) dst[dd] = __float2bfloat16_rn(src[dd]);
   }
 }
 
@@ -798,8 +814,9 @@ int launch_permute_tokens(const LaunchCtx& ctx, const float* x, const int32_t* p
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   cfg.stream = ctx.stream;
   cfg.blockDim = dim3(256);
-  cfg.gridDim = dim3(B * K + (has_shared ? B : 0));
-  cudaLaunchKernelEx(&cfg, permute_tokens_kernel, x, perm, B * K, K, D, Dp, xs);
+  const int rows = B * K + (has_shared ? B : 0);
+  cfg.gridDim = dim3(ceil_div(rows, 8));
+  cudaLaunchKernelEx(&cfg, permute_tokens_kernel, x, perm, B * K, rows, K, D, Dp, xs);
   return 1;
 }
 
