@@ -145,7 +145,11 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 // index order = (lane, j) order, so tie ranks and survivor positions come from one warp scan of
 // per-lane counts instead of a ballot per element.  Same outputs as select_rows_kernel, bit for
 // bit; no block barriers.
-template <int NPL>
+// LEAN: the batch hot case, checked by the launcher -- uniform top-k over full rows (n == 32 *
+// NPL == kext, 0 < n_off < n, no shared rows of another length), outputs = masked bf16 terms only.
+// Every bounds check, mode branch and optional output folds away (the generic instantiation
+// issues ~2200 warp instructions per row, most of them predicated off).
+template <int NPL, bool LEAN>
 __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(SelectArgs a) {
   __shared__ uint32_t pick_scratch[kSelWarps][36];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -153,20 +157,20 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
   pdl_wait();
   pdl_launch_dependents();
   if (row >= a.rows) return;
-  const bool routed = row < a.BK;
-  const int n = routed ? a.N : a.S;
-  const int slot = routed ? (a.perm ? a.perm[row] : row) : row - a.BK;
+  const bool routed = LEAN || row < a.BK;
+  const int n = LEAN ? 32 * NPL : (routed ? a.N : a.S);
+  const int slot = LEAN ? 0 : (routed ? (a.perm ? a.perm[row] : row) : row - a.BK);
   const float* hrow = a.h + static_cast<size_t>(row) * a.Nh;
-  int32_t* kidx = a.kept_idx ? a.kept_idx + static_cast<size_t>(row) * a.Nh : nullptr;
-  float* kval = a.kept_val ? a.kept_val + static_cast<size_t>(row) * a.Nh : nullptr;
-  __nv_bfloat16* hb = a.hb ? a.hb + static_cast<size_t>(row) * a.Nh : nullptr;
-  uint8_t* mout = routed ? (a.mask_out_routed ? a.mask_out_routed + static_cast<size_t>(slot) * n
+  int32_t* kidx = (!LEAN && a.kept_idx) ? a.kept_idx + static_cast<size_t>(row) * a.Nh : nullptr;
+  float* kval = (!LEAN && a.kept_val) ? a.kept_val + static_cast<size_t>(row) * a.Nh : nullptr;
+  __nv_bfloat16* hb = (LEAN || a.hb) ? a.hb + static_cast<size_t>(row) * a.Nh : nullptr;
+  uint8_t* mout = LEAN ? nullptr : routed ? (a.mask_out_routed ? a.mask_out_routed + static_cast<size_t>(slot) * n
                                               : nullptr)
                          : (a.mask_out_shared ? a.mask_out_shared + static_cast<size_t>(slot) * n
                                               : nullptr);
   const uint8_t* min_ = nullptr;
-  int mode = a.mode;
-  if (mode == kSelectGiven) {
+  int mode = LEAN ? kSelectTopk : a.mode;
+  if (!LEAN && mode == kSelectGiven) {
     min_ = routed ? a.mask_in_routed + static_cast<size_t>(slot) * n
                   : (a.mask_in_shared ? a.mask_in_shared + static_cast<size_t>(slot) * n : nullptr);
     if (min_ == nullptr) mode = kSelectAll;
@@ -174,25 +178,25 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
   // threshold selection (forward_sparse): |silu(gate)| >= tau on routed rows, the shared expert
   // stays dense (engine.cpp:352)
   const float* sgrow = nullptr;
-  if (mode == kSelectThreshold) {
+  if (!LEAN && mode == kSelectThreshold) {
     if (routed) sgrow = a.sg + static_cast<size_t>(row) * a.Nh;
     else mode = kSelectAll;
   }
-  int n_off = 0;
-  if (mode == kSelectTopk) {
+  int n_off = LEAN ? a.n_off_routed : 0;
+  if (!LEAN && mode == kSelectTopk) {
     n_off = a.counts ? a.counts[row]
                      : (routed ? (a.slot_counts ? a.slot_counts[slot % a.K] : a.n_off_routed)
                                : a.n_off_shared);
     if (n_off <= 0) mode = kSelectAll;  // activation.cpp:35
   }
-  const bool drop_everything = (mode == kSelectTopk) && n_off >= n;  // activation.cpp:36-39
+  const bool drop_everything = !LEAN && (mode == kSelectTopk) && n_off >= n;  // activation.cpp:36-39
 
   const int i0 = lane * NPL;
-  const bool vec = (a.Nh & 3) == 0;  // rows start 16-byte aligned
+  const bool vec = LEAN || (a.Nh & 3) == 0;  // rows start 16-byte aligned
   auto load_row = [&](const float* src, float (&dst)[NPL]) {
 #pragma unroll
     for (int v = 0; v < NPL; v += 4) {
-      if (vec && i0 + v + 4 <= n) {
+      if (vec && (LEAN || i0 + v + 4 <= n)) {
         const float4 q = *reinterpret_cast<const float4*>(src + i0 + v);
         dst[v] = q.x;
         dst[v + 1] = q.y;
@@ -207,13 +211,13 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
   float hv[NPL];
   load_row(hrow, hv);
   unsigned keepbits = 0u;  // bit j: neuron i0 + j survives
-  if (mode == kSelectAll) {
+  if (!LEAN && mode == kSelectAll) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) keepbits |= (i0 + j < n) ? (1u << j) : 0u;
-  } else if (mode == kSelectGiven) {
+  } else if (!LEAN && mode == kSelectGiven) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) keepbits |= (i0 + j < n && min_[i0 + j] != 0) ? (1u << j) : 0u;
-  } else if (mode == kSelectThreshold) {
+  } else if (!LEAN && mode == kSelectThreshold) {
     float sg[NPL];
     load_row(sgrow, sg);
 #pragma unroll
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
     uint32_t kr[NPL];
 #pragma unroll
     for (int j = 0; j < NPL; ++j)
-      kr[j] = (i0 + j < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
+      kr[j] = (LEAN || i0 + j < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
     const RowPick pk = warp_binary_pick<NPL>(kr, n, n_off, pick_scratch[warp]);
     int my_ties = 0;
 #pragma unroll
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
       const bool tie = kr[j] == pk.pivot;
-      const bool above = kr[j] > pk.pivot && kr[j] != 0xffffffffu;
+      const bool above = kr[j] > pk.pivot && (LEAN || kr[j] != 0xffffffffu);
       keepbits |= (above || (tie && tie_rank >= pk.ties_to_drop)) ? (1u << j) : 0u;
       tie_rank += tie ? 1 : 0;
     }
@@ -256,8 +260,8 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
       if (i0 + j < n) mout[i0 + j] = static_cast<uint8_t>((keepbits >> j) & 1u);
   }
   if (hb) {
-    const int kext = routed ? a.kext_routed : a.kext_shared;
-    const bool vec8 = (a.Nh & 7) == 0 && (kext & 7) == 0;
+    const int kext = LEAN ? 32 * NPL : (routed ? a.kext_routed : a.kext_shared);
+    const bool vec8 = LEAN || ((a.Nh & 7) == 0 && (kext & 7) == 0);
 #pragma unroll
     for (int j = 0; j < NPL; ++j) hv[j] = ((keepbits >> j) & 1u) ? hv[j] : 0.0f;
     for (int sp = 0; sp < a.nsplit; ++sp) {
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
                  (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16);
         }
         if (vec8) {
-          if (i0 + v < kext) *reinterpret_cast<uint4*>(dst + i0 + v) = make_uint4(w[0], w[1], w[2], w[3]);
+          if (LEAN || i0 + v < kext) *reinterpret_cast<uint4*>(dst + i0 + v) = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -307,9 +311,24 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
   // CTA per row (latency).
   if (span <= 1024 && a.rows >= 64) {
     cfg.gridDim = dim3(ceil_div(a.rows, kSelWarps));
-    if (span <= 256) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<8>, a);
-    else if (span <= 512) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<16>, a);
-    else cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<32>, a);
+    // the batch hot case gets the instantiation with everything else compiled out
+    const int n = a.N;
+    const bool uniform_rows = a.rows == a.BK || (a.S == a.N && a.n_off_shared == a.n_off_routed &&
+                                                 a.kext_shared == a.kext_routed);
+    const bool lean = a.mode == kSelectTopk && a.counts == nullptr && a.slot_counts == nullptr &&
+                      a.mask_out_routed == nullptr && a.mask_out_shared == nullptr &&
+                      a.kept_idx == nullptr && a.hb != nullptr && uniform_rows &&
+                      a.kext_routed == n && (a.Nh & 7) == 0 && a.n_off_routed > 0 &&
+                      a.n_off_routed < n && (n == 256 || n == 512 || n == 1024);
+    if (lean) {
+      if (n == 256) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<8, true>, a);
+      else if (n == 512) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<16, true>, a);
+      else cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<32, true>, a);
+      return 1;
+    }
+    if (span <= 256) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<8, false>, a);
+    else if (span <= 512) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<16, false>, a);
+    else cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<32, false>, a);
     return 1;
   }
   cfg.gridDim = dim3(a.rows);

@@ -1048,3 +1048,27 @@ def test_paired_blocks_match_single_blocks_and_oracle(skb, oracle, case):
     dense_p = skb.forward_dense(layer, x, flags=base | skb.FLAG_PAIRED_BLOCKS)
     y_ref, _ = oracle.forward(w, x)
     assert max_rel_diff(dense_p.outputs, y_ref) <= TOL_FP32_ACCUM
+
+
+@pytest.mark.parametrize("case", [(8, 2, 128, 256, 0, True, 64), (4, 2, 96, 512, 0, True, 70),
+                                  (4, 1, 64, 1024, 0, True, 90), (4, 2, 96, 256, 256, True, 48)])
+@pytest.mark.parametrize("s", [0.5, 0.9, 0.004])
+def test_lean_batch_selection_equals_the_generic_kernel(skb, oracle, case, s):
+    """Without mask capture, full 256/512/1024-neuron rows take the specialised selection kernel;
+    with capture the generic one runs.  Same outputs bit for bit, and right against the oracle."""
+    E, K, D, N, S, renorm, B = case
+    cfg = Config(E, K, D, N, S, renorm)
+    w, x = rounded_case(oracle, cfg, seed=N + B, scale=0.1, batch=B, token_seed=21)
+    if s == 0.5:  # exact ties across the pivot: duplicate activations by duplicating neurons
+        for m in (w.gate, w.up, w.down_t):
+            m[:, 1::2] = m[:, 0::2]
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(s)
+    sh = lvl if S else None
+    lean = skb.forward_topk_sparse(layer, x, lvl, sh, flags=skb.FLAG_DENSE_DOWN)
+    generic = skb.forward_topk_sparse(layer, x, lvl, sh, flags=skb.FLAG_DENSE_DOWN, capture=True)
+    assert lean.outputs.tobytes() == generic.outputs.tobytes()
+    y_same, _ = oracle.forward(w, x, generic.masks.routed, generic.masks.shared if S else None)
+    assert max_rel_diff(lean.outputs, y_same) <= TOL_FP32_ACCUM
+    ref_masks, _ = oracle.build_topk_masks(w, x, s, 1)
+    assert np.mean(generic.masks.routed.reshape(-1) == ref_masks.reshape(-1)) >= MASK_AGREEMENT
