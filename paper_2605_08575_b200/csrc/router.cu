@@ -252,11 +252,11 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
           }
         }
       } else {
-        // unaligned / odd d_model: plain loads by the whole producer warp
+        // unaligned / odd d_model: plain loads by the whole producer warp, handed over with two
+        // block barriers per sub-chunk (generic-proxy stores; rare path, kept simple)
 #pragma unroll 1
         for (int sc = 0; sc < nsub; ++sc) {
           const int slot = sc % kRfStages;
-          mbar_wait(empty_bar(slot), ((sc / kRfStages) & 1u) ^ 1u);
           const int d0 = sc * kRfSub;
           const int n = min(kRfSub, D - d0);
           float* dst = rf_smem + slot * kRfRows * kRfRow;
@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
 #pragma unroll 1
             for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(full_bar(slot));
+          __syncthreads();  // filled
+          __syncthreads();  // consumed
         }
       }
       return;
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
 #ifdef SKB_DEBUG_TIMING
       const long long tw0 = clock64();
 #endif
-      mbar_wait(full_bar(slot), (sc / kRfStages) & 1u);
+      if (vec_ok) mbar_wait(full_bar(slot), (sc / kRfStages) & 1u);
+      else __syncthreads();  // filled (fallback path)
 #ifdef SKB_DEBUG_TIMING
       t_wait += clock64() - tw0;
 #endif
@@ -309,8 +310,12 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
       }
 #pragma unroll 1
       for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_bar(slot));
+      if (vec_ok) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_bar(slot));
+      } else {
+        __syncthreads();  // consumed (fallback path)
+      }
     }
     RF_T(2);
 #ifdef SKB_DEBUG_TIMING

@@ -17,4 +17,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:deco
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:grouped_tc -s 12 -c 2 -o gpurun_out/prof_tc_granite_b256 -f python bench.py --steps 6 --warmup 3 --no-sweep --no-cpu --no-graph > gpurun_out/ncu_full_g.log 2>&1
 timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -k "fused_decode_matches or batch_invariant or falls_back or forward_topk_vs_oracle or forward_sparse or budget or paired or reference_file or reference_outputs" > gpurun_out/sanitizer_memcheck.log 2>&1; tail -4 gpurun_out/sanitizer_memcheck.log
 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 600 -k "fused_decode_matches and (case0 or case3)" > gpurun_out/sanitizer_racecheck.log 2>&1; tail -3 gpurun_out/sanitizer_racecheck.log
+timeout 1100 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 900 -k "lean_batch or paired_blocks or align_dispatch or forward_budget or forward_sparse_vs" > gpurun_out/sanitizer_racecheck_batch.log 2>&1; tail -3 gpurun_out/sanitizer_racecheck_batch.log
 ls -la gpurun_out | tail -30
