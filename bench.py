@@ -46,6 +46,10 @@ WORKLOADS = {
     "maverick": dict(name="Llama-4-Maverick", E=128, K=1, D=5120, N=8192, S=8192),
 }
 SEED, SCALE = 1, 0.05          # generate_synthetic defaults of the reference CLI (tools/main.cpp:157)
+# calibrate_tau(target 0.5) of the unmodified reference on generate_synthetic(seed 1, 0.05) rounded
+# to bf16 (oracle/_ref in the build container: RefLayer.calibrate_tau(0.5), defaults of
+# tools/main.cpp: 16 calibration tokens seed 3, sample cap 2^20, sampler seed 4)
+THRESHOLD_TAU = {"granite": 0.2473328560590744, "olmoe": 0.2645798623561859}
 SWEEP_S = (0.0, 0.25, 0.5, 0.75, 0.9)
 W_BYTES = 2                    # bf16 weight image
 
@@ -182,6 +186,11 @@ class Point:
 
     def _enqueue(self, s, flags=0):
         S = self.shape["S"]
+        if isinstance(s, tuple):  # ("tau", value): the threshold runtime path, forward_sparse
+            self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
+                                      mode=self.skb.MODE_THRESHOLD, tau=s[1], flags=flags,
+                                      stream=self.torch.cuda.current_stream().cuda_stream or 1)
+            return
         self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
                                   mode=self.skb.MODE_TOPK, s_routed=s, s_shared=s if S else 0.0,
                                   flags=flags,
@@ -473,6 +482,20 @@ def run_ours(args):
                           "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
                           "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
                           "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+        # the threshold runtime path (forward_sparse) on the same workload,
+        # tau = the reference's calibrate_tau for a 0.5 target on these synthetic weights
+        if args.workload in THRESHOLD_TAU:
+            tau = THRESHOLD_TAU[args.workload]
+            tms, _ = pt.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
+            m = float(np.mean(tms))
+            rep = skb.forward_sparse(layer, pt.x_host[0], tau)
+            entry = {"workload": shape["name"], "batch": B, "mode": "threshold (forward_sparse)",
+                     "tau": tau, "achieved_routed_sparsity": round(rep.achieved_routed_sparsity, 4),
+                     "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
+                     "tiles_skipped_frac": round(rep.tiles_skipped / max(1, rep.tiles_total), 4)}
+            if not args.no_cpu and world == 1:
+                entry["cpu_reference"] = cpu_reference_sparse(shape, B, tau)
+            sweep.append(entry)
         # the other batch sizes of this workload's range (configs[1]: batch 1-256), s = 0.5
         for bb in (1, 16, 64):
             if bb == B:
@@ -592,6 +615,20 @@ def cpu_reference(shape, B, s, reps):
             "ms_per_step": round(t * 1e3, 2),
             "sample": f"full batch {B}, build_topk_masks(s={s}) + forward_masked_dense, "
                       f"threads={cores}, median of {reps}"}
+
+
+def cpu_reference_sparse(shape, B, tau):
+    """forward_sparse of the unmodified reference on the host cores (one timed call)."""
+    cores = os.cpu_count() or 1
+    lay, _ = _ref_layer(shape)
+    if lay is None:
+        return None
+    x = make_tokens(B, shape["D"], 2)
+    t0 = time.perf_counter()
+    lay.forward_sparse(x, tau, threads=cores)
+    t = time.perf_counter() - t0
+    return {"value": round(B / t, 2), "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "ms_per_step": round(t * 1e3, 2), "sample": f"full batch {B}, forward_sparse, one call"}
 
 
 def run_reference(args):

@@ -299,12 +299,14 @@ class MoELayerWeights:
     # -- device-pointer entry for the benchmark's value leg and for stream capture --
     def forward_device(self, x_ptr: int, y_ptr: int, batch: int, mode: int = MODE_TOPK,
                        s_routed: float = 0.0, s_shared: float = 0.0, flags: int = 0,
-                       stream: int = 0, ids_in_ptr: int = 0, weights_in_ptr: int = 0) -> None:
+                       stream: int = 0, ids_in_ptr: int = 0, weights_in_ptr: int = 0,
+                       tau: float = 0.0) -> None:
         """All pointers are device pointers.  ids_in_ptr: external routing ([batch][top_k] int32
         expert ids of this layer); weights_in_ptr 0 => un-weighted slot outputs."""
         a = SkbForwardArgs()
         a.batch, a.mode, a.flags = batch, mode, flags
         a.s_routed, a.s_shared = s_routed, s_shared
+        a.tau = tau  # MODE_THRESHOLD only
         a.x, a.y = x_ptr, y_ptr
         a.ids_in, a.weights_in = ids_in_ptr or None, weights_in_ptr or None
         _check(_lib.load().skb_layer_forward_device(self._h, C.byref(a), C.c_void_p(stream), None))
