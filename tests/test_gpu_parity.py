@@ -1072,3 +1072,43 @@ def test_lean_batch_selection_equals_the_generic_kernel(skb, oracle, case, s):
     assert max_rel_diff(lean.outputs, y_same) <= TOL_FP32_ACCUM
     ref_masks, _ = oracle.build_topk_masks(w, x, s, 1)
     assert np.mean(generic.masks.routed.reshape(-1) == ref_masks.reshape(-1)) >= MASK_AGREEMENT
+
+
+# ---------------------------------------------------------------------------------------------
+# re-entrancy: calls on one handle are serialised, results do not depend on who else is calling
+# (engine_test.cpp:337-353 checks independence of `threads`; the device analogue is callers)
+# ---------------------------------------------------------------------------------------------
+def test_concurrent_callers_on_one_layer_and_on_two_layers(skb, oracle):
+    import threading
+    cfg = Config(8, 2, 96, 160, 48, True)
+    w, _ = rounded_case(oracle, cfg, seed=17, scale=0.1, batch=1, token_seed=1)
+    layer_a, layer_b = make_layer(skb, w), make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    batches = [1, 7, 40, 3, 64, 16]
+    xs = [oracle.round_bf16(oracle.generate_tokens(b, cfg.d_model, 50 + i)) for i, b in enumerate(batches)]
+    want = [skb.forward_topk_sparse(layer_a, x, lvl, lvl).outputs.copy() for x in xs]
+    want_sparse = [skb.forward_sparse(layer_a, x, 0.05).outputs.copy() for x in xs]
+    errors = []
+
+    def worker(layer, offset):
+        try:
+            for it in range(12):
+                i = (it + offset) % len(xs)
+                got = skb.forward_topk_sparse(layer, xs[i], lvl, lvl).outputs
+                if got.tobytes() != want[i].tobytes():
+                    errors.append(("topk", offset, i))
+                got = skb.forward_sparse(layer, xs[i], 0.05).outputs
+                if got.tobytes() != want_sparse[i].tobytes():
+                    errors.append(("threshold", offset, i))
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(layer_a, 0)),
+               threading.Thread(target=worker, args=(layer_a, 3)),
+               threading.Thread(target=worker, args=(layer_b, 1)),
+               threading.Thread(target=worker, args=(layer_b, 4))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:5]
