@@ -50,8 +50,10 @@ __host__ __device__ constexpr int num_stages(int tn, int mode, int mb = 1) {
   // MODE 0: <= ~110 KB per CTA so that two CTAs share an SM (grids larger than the SM count then
   // run in one wave and one CTA's prologue/epilogue overlaps the other's stream); ~100 KB in
   // flight per CTA is still several times the latency-bandwidth product per SM.
+  // MODE 1, small token tiles: many short tiles (8 K blocks at d_ffn 512), so two CTAs per SM --
+  // one tile's ramp and epilogue under the other's stream -- beat one CTA with a deep ring
   return mode == 0 ? (tn <= 16 ? 6 : (tn <= 32 ? 5 : (tn <= 64 ? 4 : (tn <= 128 ? 3 : 2))))
-                   : (tn <= 16 ? 9 : (tn <= 32 ? 7 : (tn <= 64 ? 5 : 3)));
+                   : (tn <= 16 ? 4 : (tn <= 32 ? 3 : (tn <= 64 ? 5 : 3)));
 }
 __host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
 __host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode, int mb = 1) {
@@ -79,7 +81,7 @@ struct TcArgs {
 };
 
 template <int TN, int MODE, int MB>
-__global__ void __launch_bounds__(kGateupThreads, (MODE == 0 && MB == 1) ? 2 : 1)
+__global__ void __launch_bounds__(kGateupThreads, ((MODE == 0 || TN <= 32) && MB == 1) ? 2 : 1)
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,
