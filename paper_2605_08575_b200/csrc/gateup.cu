@@ -52,8 +52,8 @@ __host__ __device__ constexpr int num_stages(int tn, int mode, int mb = 1) {
   // flight per CTA is still several times the latency-bandwidth product per SM.
   // MODE 1, small token tiles: many short tiles (8 K blocks at d_ffn 512), so two CTAs per SM --
   // one tile's ramp and epilogue under the other's stream -- beat one CTA with a deep ring
-  return mode == 0 ? (tn <= 16 ? 6 : (tn <= 32 ? 5 : (tn <= 64 ? 4 : (tn <= 128 ? 3 : 2))))
-                   : (tn <= 16 ? 4 : (tn <= 32 ? 3 : (tn <= 64 ? 5 : 3)));
+  return mode == 0 ? (tn <= 16 ? 4 : (tn <= 32 ? 5 : (tn <= 64 ? 4 : (tn <= 128 ? 3 : 2))))
+                   : (tn <= 16 ? 2 : (tn <= 32 ? 3 : (tn <= 64 ? 5 : 3)));
 }
 __host__ __device__ constexpr int tmem_cols(int tn) { return tn < 32 ? 32 : tn; }
 __host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode, int mb = 1) {
@@ -81,7 +81,7 @@ struct TcArgs {
 };
 
 template <int TN, int MODE, int MB>
-__global__ void __launch_bounds__(kGateupThreads, ((MODE == 0 || TN <= 32) && MB == 1) ? 2 : 1)
+__global__ void __launch_bounds__(kGateupThreads, (MB == 2) ? 1 : ((MODE == 1 && TN <= 16) ? 4 : ((MODE == 0 && TN <= 16) ? 3 : ((MODE == 0 || TN <= 32) ? 2 : 1))))
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,
