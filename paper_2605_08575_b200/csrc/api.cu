@@ -391,7 +391,9 @@ struct StageTimer {
 // shape; which is faster depends on how much the per-(token, slot) row gather of the fused
 // kernel moves against one pass over the routed experts' W_down.  Linear models fitted to
 // measurements on B200 (tools/fused_vs_staged.py: Granite, OLMoE, Qwen3.5 and GPT-OSS shapes,
-// batches 1-16, s = 0.5; the fused model is within 5 % of every point): microseconds from MB.
+// batches 1-16, s = 0.5; refitted after the staged kernels' small-tile changes -- on the 40
+// measured points the choice is never more than 2.2 % slower than the better path): microseconds
+// from MB.
 bool decode_fused_preferred(const Geometry& g, int B, double keep_r, double keep_s) {
   const double E = g.E, K = g.K;
   const double U = E * (1.0 - std::pow(1.0 - K / E, B));  // expected distinct routed experts
@@ -401,8 +403,10 @@ bool decode_fused_preferred(const Geometry& g, int B, double keep_r, double keep
   const double vd = (U * g.N + (g.has_shared ? g.S : 0.0)) * row_mb;
   const double R = K + (g.has_shared ? 1.0 : 0.0);
   const double fused = 27.9 + 0.248 * gup + (g.Dp <= 2048 ? 0.237 : 0.519) * vg + 0.232 * B * R;
-  const double staged = 59.4 + 0.222 * gup + 0.111 * vd;
-  return fused <= 1.04 * staged;
+  // staged kernels: a fixed chain of launches whose router part grows with d_model (the exact
+  // logit chains are d_model dependent adds long), plus one pass over the routed experts
+  const double staged = 32.0 + 10.34 * (g.Dp / 1024.0) + 0.1814 * (gup + 0.5 * vd);
+  return fused <= staged;
 }
 
 // Enqueues every stage of one forward on `stream`.  x/y (and masks in MASKED mode) are device

@@ -403,8 +403,15 @@ __global__ void __launch_bounds__(256) router_logits_fast_kernel(const float* __
   if (lane == 0) logits[static_cast<size_t>(t) * E + e] = acc;
 }
 
+// Batches up to this size run route() and the dispatch inside the router kernel (its last CTA);
+// above it they are parallel kernels of their own.  Measured (tools/fused_vs_staged.py, staged
+// column): the in-kernel tail costs ~2.8 us per token (one warp per token block routes its tokens
+// one after the other, one warp sorts all slots), so it only pays for one or two tokens.
+// (Granite shape batch 8: 66.7 -> 54.3 us, OLMoE shape batch 8: 146 -> 130-143 us with the limit at 2.)
+static constexpr int fuse_route_max_batch() { return 2; }
+
 bool router_token_tiles(int B, int K, bool want) {
-  return want && B <= 16 && B <= 2 * kRfTB && B * K <= kSmallSlots;
+  return want && B <= 16 && B <= fuse_route_max_batch() && B * K <= kSmallSlots;
 }
 
 int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
@@ -440,7 +447,7 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   a.logits_ready = (r.fast || r.x == nullptr) ? 1 : 0;
   // decode batches: everything in the router kernel (no launch boundaries); larger batches:
   // route() and the dispatch are parallel kernels of their own
-  a.fuse_route = (r.B <= 2 * kRfTB) ? 1 : 0;
+  a.fuse_route = (r.B <= fuse_route_max_batch()) ? 1 : 0;
   a.fuse_dispatch = (a.fuse_route && r.dispatch != nullptr && r.B * r.K <= kSmallSlots) ? 1 : 0;
   a.has_shared = r.has_shared;
   a.tile_tokens = r.tile_tokens;

@@ -360,9 +360,13 @@ def test_invariants(skb, oracle):
         half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl, flags=flags)
         whole = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=flags)
         np.testing.assert_array_equal(half.outputs, whole.outputs[:3])
+    half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl, flags=skb.FLAG_FUSED_DECODE)
+    full = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=skb.FLAG_FUSED_DECODE)
+    np.testing.assert_array_equal(half.outputs, full.outputs[:3])  # both: the fused decode kernel
+    # the automatic choice (a cost model over shape and batch) may differ between the two calls
     half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl)
     full = skb.forward_topk_sparse(layer, x, lvl, lvl)
-    np.testing.assert_array_equal(half.outputs, full.outputs[:3])  # both: the fused decode kernel
+    assert max_rel_diff(half.outputs, full.outputs[:3]) <= TOL_FP32_ACCUM
     # PDL on/off and repeated calls are bit-identical
     again = skb.forward_topk_sparse(layer, x, skb.SparsityLevel(0.5), skb.SparsityLevel(0.5),
                                     flags=skb.FLAG_NO_PDL)

@@ -10,10 +10,10 @@ for name in sys.argv[1:]:
     cfg = skb.MoEConfig(E, K, D, N, S > 0, S, True, 64)
     layer = skb.MoELayerWeights.generate_synthetic(cfg, 1, 0.05)
     layer.reserve(16)
-    for B in (1, 2, 4, 8, 12, 16):
+    for B in (1, 2, 3, 4, 6, 8, 10, 12, 14, 16):
         x = torch.randn(B, D, device='cuda'); y = torch.empty_like(x)
         out = []
-        for flags in (0, skb.FLAG_NO_FUSED_DECODE):
+        for flags in (skb.FLAG_FUSED_DECODE, skb.FLAG_NO_FUSED_DECODE, 0, skb.FLAG_DENSE_DOWN, skb.FLAG_GATHER_DOWN):
             ts = []
             for i in range(23):
                 flush.zero_()
@@ -25,4 +25,6 @@ for name in sys.argv[1:]:
                 e1.record(); torch.cuda.synchronize()
                 if i >= 3: ts.append(e0.elapsed_time(e1) * 1e3)
             out.append(float(np.mean(ts)))
-        print(f'{name:8s} B={B:2d}  fused {out[0]:7.1f} us   staged {out[1]:7.1f} us')
+        pick = 'fused' if abs(out[2] - out[0]) < abs(out[2] - out[1]) else 'staged'
+        best = 'fused' if out[0] <= out[1] else 'staged'
+        print(f'{name:8s} B={B:2d}  fused {out[0]:7.1f} us   staged {out[1]:7.1f} us   auto {out[2]:7.1f} us  dense {out[3]:7.1f}  gather {out[4]:7.1f}  picks {pick:6s} best {best:6s} {"" if pick == best or abs(out[0]-out[1]) < 0.03*min(out[:2]) else "<-- WRONG"}')
