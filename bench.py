@@ -63,6 +63,17 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def tensor_peak():
+    """Dense bf16 TFLOP/s: the sustained figure (the kernel is timed inside a long step)."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        if "bf16_tflops_sustained" in d:
+            return float(d["bf16_tflops_sustained"]), "measured sustained (MEASURED_PEAKS.json)"
+    return 1400.0, "fallback (B200_PROFILING.md)"
+
+
 def n_off(s, n):
     # topk_mask, proj/src/activation.cpp:54-60
     return int(min(max(np.floor(s * n + 0.5), 0), n))
@@ -449,13 +460,35 @@ def run_ours(args):
             traffic, traffic_src = int(tr[key]["bytes"]), tr[key]["capture"]
     except (OSError, ValueError, KeyError):
         pass
-    roofline = {"bound": "hbm", "kernel": dom_name,
-                "achieved": round(dom_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(dom_gbs / hbm_peak, 4), "traffic": traffic,
-                "traffic_source": traffic_src, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": int(dom_bytes),
-                "kernel_ms": round(stages[dom], 5),
-                "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
+    # algorithmic FLOPs of that kernel: gate/up 2 * rows * 2N * D, down 2 * kept * D
+    rows_r, rows_s = B * shape["K"], (B if shape["S"] else 0)
+    if launches_per_step == 1:
+        dom_flops = None
+    elif dom == "gateup":
+        dom_flops = 2.0 * (rows_r * 2 * shape["N"] + rows_s * 2 * shape["S"]) * shape["D"]
+    else:
+        dom_flops = 2.0 * (rows_r * (shape["N"] - n_off(s, shape["N"])) +
+                           rows_s * (shape["S"] - n_off(s, shape["S"]))) * shape["D"]
+    tf_peak, tf_src = tensor_peak()
+    tensor_bound = dom_flops is not None and dom_flops / (tf_peak * 1e12) > dom_bytes / (hbm_peak * 1e9)
+    if tensor_bound:
+        dom_tf = dom_flops / (stages[dom] * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": dom_name, "achieved": round(dom_tf, 1),
+                    "peak": tf_peak, "unit": "TFLOP/s", "frac": round(dom_tf / tf_peak, 4),
+                    "traffic": None, "traffic_source": None, "peak_source": tf_src,
+                    "algorithmic_flops_per_launch": int(dom_flops),
+                    "algorithmic_bytes_per_launch": int(dom_bytes),
+                    "hbm_frac": round(dom_gbs / hbm_peak, 4),
+                    "kernel_ms": round(stages[dom], 5),
+                    "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
+    else:
+        roofline = {"bound": "hbm", "kernel": dom_name,
+                    "achieved": round(dom_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(dom_gbs / hbm_peak, 4), "traffic": traffic,
+                    "traffic_source": traffic_src, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": int(dom_bytes),
+                    "kernel_ms": round(stages[dom], 5),
+                    "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
     layer_gbs = mean_bytes["total"] / (ms_per_step * 1e-3) / 1e9
 
     # ---- end to end through the host-buffer entry point ----

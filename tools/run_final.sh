@@ -9,6 +9,7 @@ timeout 600 python bench.py --workload olmoe --batch 1 --no-sweep > gpurun_out/b
 timeout 600 python bench.py --workload qwen35 --batch 16 --no-sweep --no-cpu > gpurun_out/bench_qwen35_b16.json 2> gpurun_out/bench_qwen35_b16.err
 timeout 600 python bench.py --workload qwen35 --batch 64 --no-sweep --no-cpu > gpurun_out/bench_qwen35_b64.json 2> gpurun_out/bench_qwen35_b64.err
 timeout 600 python bench.py --workload gptoss --batch 1 --no-sweep --no-cpu > gpurun_out/bench_gptoss_b1.json 2> gpurun_out/bench_gptoss_b1.err
+timeout 600 python bench.py --workload gptoss --batch 4096 --steps 20 --warmup 3 --no-sweep --no-cpu > gpurun_out/bench_gptoss_b4096.json 2> gpurun_out/bench_gptoss_b4096.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
 K='regex:router_|route_|dispatch|permute|grouped_tc|select_rows|down_cluster|combine|decode_fused'
 timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -s 60 -c 48 --csv --log-file gpurun_out/launches_granite_b256.csv python bench.py --steps 10 --warmup 3 --no-sweep --no-cpu --no-graph > gpurun_out/ncu_g.log 2>&1
