@@ -27,7 +27,7 @@ constexpr int kRfEB = 8;        // experts per CTA
 constexpr int kRfTB = 4;        // tokens per CTA
 constexpr int kRfSub = 512;     // floats per sub-chunk (one mbarrier wait costs ~300 cycles of the
                                 // chain: measured 18.0k cycles at 128, so waits are kept rare)
-constexpr int kRfStages = 4;    // ring depth
+constexpr int kRfStages = 4;    // ring depth (maximum; large grids run with 2, see launch_router)
 constexpr int kRfRow = kRfSub + 4;  // padded row stride (floats): conflict-free LDS.128
 constexpr int kRfRows = kRfEB + kRfTB;
 constexpr int kRfSmemFloats = kRfStages * kRfRows * kRfRow;
@@ -168,6 +168,7 @@ struct RouterFusedArgs {
   int fuse_dispatch;  // 1: the last CTA also builds the dispatch (B*K <= kSmallSlots)
   int has_shared, tile_tokens;
   int n_eb;            // expert blocks (CTAs per token block that run chains)
+  int stages;          // ring depth of this launch
   __nv_bfloat16* xb;   // token tiles: bf16 copy of x, [B][Dp]; written by CTA column n_eb
   int Dp;
   float* logits;
@@ -191,12 +192,13 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e0 = blockIdx.x * kRfEB, t0 = blockIdx.y * kRfTB;
   const int D = a.D;
-  const uint32_t bar_base = smem_u32(rf_smem + kRfSmemFloats);
+  const int nst = a.stages;  // ring depth of this launch (2 .. kRfStages)
+  const uint32_t bar_base = smem_u32(rf_smem + nst * kRfRows * kRfRow);
   auto full_bar = [&](int s) { return bar_base + 8u * s; };
-  auto empty_bar = [&](int s) { return bar_base + 8u * (kRfStages + s); };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (nst + s); };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRfStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
@@ -235,8 +237,8 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
           const float* xsrc = a.x + static_cast<size_t>(t0) * D;
 #pragma unroll 1
           for (int sc = 0; sc < nsub; ++sc) {
-            const int slot = sc % kRfStages;
-            mbar_wait(empty_bar(slot), ((sc / kRfStages) & 1u) ^ 1u);
+            const int slot = sc % nst;
+            mbar_wait(empty_bar(slot), ((sc / nst) & 1u) ^ 1u);
             const int d0 = sc * kRfSub;
             const uint32_t bytes = static_cast<uint32_t>(min(kRfSub, D - d0)) * 4u;
             mbar_arrive_expect_tx(full_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
         // block barriers per sub-chunk (generic-proxy stores; rare path, kept simple)
 #pragma unroll 1
         for (int sc = 0; sc < nsub; ++sc) {
-          const int slot = sc % kRfStages;
+          const int slot = sc % nst;
           const int d0 = sc * kRfSub;
           const int n = min(kRfSub, D - d0);
           float* dst = rf_smem + slot * kRfRows * kRfRow;
@@ -284,11 +286,11 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
 #endif
 #pragma unroll 1
     for (int sc = 0; sc < nsub; ++sc) {
-      const int slot = sc % kRfStages;
+      const int slot = sc % nst;
 #ifdef SKB_DEBUG_TIMING
       const long long tw0 = clock64();
 #endif
-      if (vec_ok) mbar_wait(full_bar(slot), (sc / kRfStages) & 1u);
+      if (vec_ok) mbar_wait(full_bar(slot), (sc / nst) & 1u);
       else __syncthreads();  // filled (fallback path)
 #ifdef SKB_DEBUG_TIMING
       t_wait += clock64() - tw0;
@@ -463,7 +465,18 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   if (!(a.logits_ready && !a.fuse_route)) {
     cfg.gridDim = dim3(a.n_eb + (token_tiles ? 1 : 0), ceil_div(r.B, kRfTB));
     cfg.blockDim = dim3(64);
-    cfg.dynamicSmemBytes = smem;
+    // One chain warp per CTA is latency-bound (a dependent add every 4 cycles), so what matters
+    // for a grid of many CTAs is how many are resident: a ring of 2 instead of 4 sub-chunks
+    // halves the shared memory and doubles the CTAs per SM (prefill: 4096 CTAs, 14 waves -> 7).
+    static int n_sms = 0;
+    if (n_sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long n_ctas = static_cast<long>(cfg.gridDim.x) * cfg.gridDim.y;
+    a.stages = n_ctas > 2L * n_sms ? 2 : kRfStages;
+    cfg.dynamicSmemBytes = static_cast<size_t>(a.stages) * kRfRows * kRfRow * 4 + 2 * a.stages * 8;
     cudaLaunchKernelEx(&cfg, router_fused_kernel, a);
     ++launches;
   }
