@@ -586,9 +586,15 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
            ((a->flags & SKB_FLAG_PAIRED_BLOCKS) ||
             est_tiles * ceil_div(mblocks, 2) * 4 >= L->n_sms * 3);
   };
-  // gate/up: measured slower paired (Granite shape batch 256: 25.5 -> 29.7 us stage time, half as
-  // many CTAs each with the same bytes in flight); only on request
-  const bool pair_gateup = (a->flags & SKB_FLAG_PAIRED_BLOCKS) && pair_for(g.Np / kNeuronBlock);
+  // gate/up: slower paired while the grid is about one CTA per SM (Granite shape batch 256: 25.5 ->
+  // 29.7 us stage time; GPT-OSS shape prefill with one CTA per SM: 0.77 -> 0.87 ms -- nothing hides a
+  // tile's ramp and epilogue); with two CTAs per SM on a two-stage ring each, a grid of several
+  // waves gains (GPT-OSS shape, 4096 tokens: 0.77 -> 0.71 ms).  Hence: only for such grids.
+  const long paired_gateup_ctas =
+      static_cast<long>(est_tiles + BK / tn) * ceil_div(g.Np / kNeuronBlock, 2);
+  const bool pair_gateup =
+      !(a->flags & SKB_FLAG_NO_PAIRED_BLOCKS) && tn >= 64 &&
+      ((a->flags & SKB_FLAG_PAIRED_BLOCKS) || (tn == 128 && paired_gateup_ctas >= 4L * L->n_sms));
   const bool pair_down = pair_for(g.Dp128 / 128);
 
   tm.mark();

@@ -46,7 +46,8 @@ __host__ __device__ constexpr int stage_bytes(int tn, int mode, int mb = 1) {
   return mb * kATileBytes + (mode == 0 ? 1 : kMaxSplit) * b_tile_bytes(tn);
 }
 __host__ __device__ constexpr int num_stages(int tn, int mode, int mb = 1) {
-  if (mb == 2) return mode == 0 ? (tn <= 64 ? 5 : 4) : (tn <= 64 ? 3 : 2);
+  // MODE 0, 128-token tiles: two stages of 48 KB so that two CTAs share an SM (prefill grids)
+  if (mb == 2) return mode == 0 ? (tn <= 64 ? 5 : 2) : (tn <= 64 ? 3 : 2);
   // MODE 0: <= ~110 KB per CTA so that two CTAs share an SM (grids larger than the SM count then
   // run in one wave and one CTA's prologue/epilogue overlaps the other's stream); ~100 KB in
   // flight per CTA is still several times the latency-bandwidth product per SM.
@@ -81,7 +82,7 @@ struct TcArgs {
 };
 
 template <int TN, int MODE, int MB>
-__global__ void __launch_bounds__(kGateupThreads, (MB == 2) ? 1 : ((MODE == 1 && TN <= 16) ? 4 : ((MODE == 0 && TN <= 16) ? 3 : ((MODE == 0 || TN <= 32) ? 2 : 1))))
+__global__ void __launch_bounds__(kGateupThreads, (MB == 2) ? ((MODE == 0 && TN == 128) ? 2 : 1) : ((MODE == 1 && TN <= 16) ? 4 : ((MODE == 0 && TN <= 16) ? 3 : ((MODE == 0 || TN <= 32) ? 2 : 1))))
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,
