@@ -1116,3 +1116,21 @@ def test_concurrent_callers_on_one_layer_and_on_two_layers(skb, oracle):
     for t in threads:
         t.join()
     assert not errors, errors[:5]
+
+
+def test_multiwave_batch_takes_paired_gate_up_and_matches(skb, oracle):
+    """A batch large enough for several waves of gate/up CTAs: the automatic choice pairs weight
+    blocks (two CTAs per SM), the dispatch falls back to the segment kernel (575 chunks).  Same
+    bits as the unpaired kernels; right against the oracle."""
+    cfg = Config(8, 4, 64, 512, 0, True)
+    B = 4600
+    w, x = rounded_case(oracle, cfg, seed=41, scale=0.1, batch=B, token_seed=6)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    auto = skb.forward_topk_sparse(layer, x, lvl)
+    single = skb.forward_topk_sparse(layer, x, lvl, flags=skb.FLAG_NO_PAIRED_BLOCKS, capture=True)
+    assert auto.outputs.tobytes() == single.outputs.tobytes()
+    y_same, _ = oracle.forward(w, x, single.masks.routed, None)
+    assert max_rel_diff(auto.outputs, y_same) <= TOL_FP32_ACCUM
+    ref_masks, _ = oracle.build_topk_masks(w, x, 0.5, 0)
+    assert np.mean(single.masks.routed.reshape(-1) == ref_masks.reshape(-1)) >= MASK_AGREEMENT
