@@ -70,6 +70,23 @@ int encode_bf16_2d(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, u
   return SKB_OK;
 }
 
+// 3-D view for the fused decode kernel: {64 bf16 columns, rows, planes}, row and plane strides in
+// bytes, box = {64, box_rows, box_planes}, 128-byte swizzle.
+int encode_bf16_3d(CUtensorMap* map, void* base, uint64_t rows, uint64_t planes, uint64_t row_stride,
+                   uint64_t plane_stride, uint32_t box_rows, uint32_t box_planes) {
+  int rc = load_encode();
+  if (rc) return rc;
+  cuuint64_t gdim[3] = {static_cast<cuuint64_t>(kBlockK), rows, planes};
+  cuuint64_t gstride[2] = {row_stride, plane_stride};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), box_rows, box_planes};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, gdim, gstride, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SKB_ECUDA, "cuTensorMapEncodeTiled (3-D) failed with CUresult %d", (int)r);
+  return SKB_OK;
+}
+
 int n_off_of(double s, int n) {
   // topk_mask, proj/src/activation.cpp:54-60
   const long raw = static_cast<long>(std::floor(s * n + 0.5));
@@ -101,6 +118,7 @@ struct skb_layer {
   __nv_bfloat16* d_wdt_shared = nullptr;  // [Dp128][Sp]
   uint64_t weight_bytes = 0;
   CUtensorMap tmap_w{};
+  CUtensorMap tmap_w3{};  // fused decode kernel: quarter-tile pieces of the same image
   CUtensorMap tmap_wdt{}, tmap_wdt_shared{};
 
   // workspaces, sized for cap_batch
@@ -119,6 +137,7 @@ struct skb_layer {
   CUtensorMap tmap_x[5]{};
   __nv_bfloat16* d_xb = nullptr;  // decode: bf16 token rows [max(cap,16)][Dp] (token-indexed tiles)
   CUtensorMap tmap_xb{};
+  CUtensorMap tmap_xb3{};  // fused decode kernel: {64, 16 tokens, K blocks}
   float* d_h = nullptr;
   float* d_sg = nullptr;  // silu(gate) of every row (threshold selection, forward_sparse)
   __nv_bfloat16* d_hb = nullptr;  // masked activations, [3][rows][Nh] bf16 terms
@@ -135,8 +154,7 @@ struct skb_layer {
 
   // fused decode kernel (decode.cu)
   int n_sms = 0;
-  float* d_dec_lf = nullptr;
-  float* d_dec_lm = nullptr;
+  float* d_dec_p0 = nullptr;
   float* d_dec_hc = nullptr;
   float* d_dec_part = nullptr;
   unsigned* d_dec_ctr = nullptr;
@@ -158,7 +176,7 @@ void free_workspace(skb_layer* L) {
                   L->d_kval,     L->d_kcnt,      L->d_mask_in_r,
                   L->d_mask_in_s, L->d_mask_out_r, L->d_mask_out_s, L->d_counters,
                   L->d_hb,       L->d_slot_out,  L->d_ids_stage,    L->d_wts_stage,
-                  L->d_xb,       L->disp.tile_colrow, L->d_dec_lf,    L->d_dec_lm,
+                  L->d_xb,       L->disp.tile_colrow, L->d_dec_p0,
                   L->d_dec_hc,   L->d_dec_part,  L->d_dec_ctr,      L->d_sg,
                   L->d_slot_noff};
   for (void* p : ptrs)
@@ -173,7 +191,7 @@ void free_workspace(skb_layer* L) {
   L->d_ids_stage = nullptr;
   L->d_wts_stage = nullptr;
   L->d_xb = nullptr;
-  L->d_dec_lf = L->d_dec_lm = L->d_dec_hc = L->d_dec_part = nullptr;
+  L->d_dec_p0 = L->d_dec_hc = L->d_dec_part = nullptr;
   L->d_dec_ctr = nullptr;
   L->d_sg = nullptr;
   L->d_mask_in_r = L->d_mask_in_s = L->d_mask_out_r = L->d_mask_out_s = nullptr;
@@ -229,6 +247,8 @@ int reserve_locked(skb_layer* L, int B) {
     SKB_TRY(dmalloc(&L->d_xb, xb_rows * g.Dp));
     SKB_CUDA(cudaMemsetAsync(L->d_xb, 0, xb_rows * g.Dp * sizeof(__nv_bfloat16), L->stream));
     SKB_TRY(encode_bf16_2d(&L->tmap_xb, L->d_xb, xb_rows, g.Dp, 16));
+    SKB_TRY(encode_bf16_3d(&L->tmap_xb3, L->d_xb, 16, g.Dp / kBlockK,
+                           static_cast<uint64_t>(g.Dp) * 2, kBlockK * 2, 16, 4));
   }
   {
     const size_t n_counters = 2 + static_cast<size_t>(cap);
@@ -237,10 +257,10 @@ int reserve_locked(skb_layer* L, int B) {
   }
   if (decode_fused_eligible(g, 1)) {
     const size_t crow = 16 * static_cast<size_t>(decode_cand_rows(g.K)) + 16;
-    SKB_TRY(dmalloc(&L->d_dec_lf, 16 * static_cast<size_t>(g.E)));
-    SKB_TRY(dmalloc(&L->d_dec_lm, 16 * static_cast<size_t>(g.E)));
-    SKB_TRY(dmalloc(&L->d_dec_hc, 2 * crow * g.Nh));
-    SKB_CUDA(cudaMemsetAsync(L->d_dec_hc, 0, 2 * crow * g.Nh * sizeof(float), L->stream));
+    SKB_TRY(dmalloc(&L->d_dec_p0, static_cast<size_t>(decode_p0_words(g))));
+    SKB_CUDA(cudaMemsetAsync(L->d_dec_p0, 0, decode_p0_words(g) * sizeof(float), L->stream));
+    SKB_TRY(dmalloc(&L->d_dec_hc, crow * g.Nh));
+    SKB_CUDA(cudaMemsetAsync(L->d_dec_hc, 0, crow * g.Nh * sizeof(float), L->stream));
     SKB_TRY(dmalloc(&L->d_dec_part,
                     16 * static_cast<size_t>(decode_cand_rows(g.K) + 1) *
                         decode_chunks(g, 1, g.N > g.S ? g.N : g.S, L->n_sms) * g.Dp));
@@ -363,6 +383,9 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
   cudaMemsetAsync(L->d_wd, 0, wd_rows * g.Dp * 2, L->stream);
   // tiled images: the tensor maps see them as [n_tiles * 128][64] (tiled_index())
   rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows * (g.Dp / kBlockK), kBlockK, 128);
+  if (!rc)  // the same image as planes of 128 x 64 tiles: a box is 32 rows of 4 consecutive tiles
+    rc = encode_bf16_3d(&L->tmap_w3, L->d_wgu, 128, gu_rows / 128 * (g.Dp / kBlockK), kBlockK * 2,
+                        128 * kBlockK * 2, 32, 4);
   if (!rc)
     rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt,
                         static_cast<uint64_t>(g.E) * g.Dp128 * (g.Np / kBlockK), kBlockK, 128);
@@ -514,8 +537,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dl.CH = decode_chunks(g, B, max_keep, L->n_sms);
     dl.capture = capture_h || want_masks;
     dl.xb = L->d_xb;
-    dl.lf = L->d_dec_lf;
-    dl.lm = L->d_dec_lm;
+    dl.p0 = L->d_dec_p0;
     dl.logits = L->d_logits;
     dl.ids = L->d_ids;
     dl.wts = L->d_wts;
@@ -530,7 +552,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     tm.mark();
     tm.mark();
     tm.mark();
-    launches += launch_decode_fused(ctx, &L->tmap_w, &L->tmap_xb, dl, g, L->n_sms);
+    launches += launch_decode_fused(ctx, &L->tmap_w3, &L->tmap_xb3, dl, g, L->n_sms);
     tm.mark();
     if (want_masks) {
       SelectArgs sa{};

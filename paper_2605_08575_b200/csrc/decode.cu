@@ -1,40 +1,50 @@
-// decode.cu -- the whole layer for decode batches (B <= 16) as ONE persistent launch.
+// decode.cu -- the whole layer for decode batches (B <= 16) as ONE persistent launch, software
+// pipelined: the down projection of an expert runs while the gate/up weights of the next
+// experts are still streaming.
 //
-// Why one kernel: at decode sizes the layer moves ~10-100 MB, i.e. 10-20 us of HBM time, and
-// every kernel boundary (launch, drain, refill of the memory pipeline) costs 2-5 us of that.
-// The stages of the reference path (proj/src/engine.cpp:94-191) map onto phases of one grid of
-// numSMs CTAs (one per SM, all co-resident), chained by counters in global memory:
+// Why one kernel: at decode sizes the layer moves ~10-100 MB, i.e. 10-20 us of HBM time; every
+// kernel boundary costs 2-3 us of drain + launch + refill, and a cold burst out of HBM ramps for
+// ~3 us before it reaches full rate (tools/micro/burst.cu: 64 MB in 14 us, 16 MB in 5.5 us).  So
+// the stages of the reference path (proj/src/engine.cpp:94-191) are ROLES of one grid of numSMs
+// CTAs (one per SM, all co-resident), each role on its own warps, chained through global memory:
 //
-//   P0  fast router logits.  lf[t][e] = x[t].router[e] by a parallel (not order-faithful)
-//       reduction, together with A[t][e] = sum |x.router|.  The reference's logit (ascending-index
-//       float accumulation, proj/src/linalg.cpp:22-40) differs from lf by at most
-//       m = 2*gamma_D*A (gamma_D = D*u/(1-D*u), u = 2^-24: the standard recursive-summation
-//       bound, applied to both sums).  Every expert whose interval [lf-m, lf+m] reaches the K-th
-//       largest lower end is a CANDIDATE of the token; the reference's top-K set is provably a
-//       subset.  Typically K candidates, sometimes K+1.  (More than K+4, non-finite values, or
-//       a threshold more than 60 below the maximum -- the exp underflow region where
-//       probabilities tie -- and the CTA simply waits for the exact routing instead.)
-//   CH  exact routing, concurrently.  Two dedicated warps per CTA run the order-faithful logit
-//       chains (the D dependent float adds of the reference, ~6 cycles each) while the gate/up
-//       stream runs; the last chain to finish a token block runs route() (proj/src/router.cpp:
-//       13-68) for it.  Expert ids, slot order and weights are therefore the reference's bit for
-//       bit, and their latency (5-10 us) is hidden behind P1.
-//   P1  gate/up + SwiGLU for the union of candidate experts: work item = (expert, 64 neurons);
-//       tcgen05.mma 128x16x16 (gate and up rows interleaved on M, the <=16 tokens on N),
-//       TMEM accumulators double-buffered, weights streamed once by TMA through a 9-stage ring
-//       (~160 KB in flight per SM).  The epilogue stores h and, in top-k mode, adds each value
-//       to a 512-bin histogram of its row (bins = exponent + 3 mantissa bits of |h|).
-//   P2  neuron selection + down projection.  Work unit = (token, slot, row chunk).  The unit
-//       loads its h row, locates the pivot bucket from the histogram, ranks only the bucket's
-//       members (bit-exact mask_smallest_magnitudes, proj/src/activation.cpp:31-52, including the
-//       lower-index-first tie rule), takes its share of the survivors in ascending index order
-//       and streams exactly those W_down rows (coalesced 128-bit loads, fp32 accumulation in
-//       registers).  Dropped neurons cost no HBM bytes.
-//   P3  combine: y[t] = sum_s w(t,s) * (sum_chunks partial), slots ascending, shared expert
-//       last with weight 1 (proj/src/router.cpp:109-132, engine.cpp:168-173), fixed order.
+//   warps 4-11 "D role" (256 threads)
+//     P0  fast router logits, split over (expert, d_model slice) units on all CTAs: partial
+//         lf = x.router and A = sum |x.router| per slice, published as {bits, epoch} words that the
+//         readers poll -- no grid barrier.  The reference's logit (ascending-index float
+//         accumulation, proj/src/linalg.cpp:22-40) differs from lf by at most m = 2*gamma_D*A
+//         (gamma_D = D*u/(1-D*u), u = 2^-24).  Every expert whose interval [lf-m, lf+m] reaches
+//         the K-th largest lower end is a CANDIDATE of the token; the reference's top-K set is
+//         provably a subset.  Typically K candidates, sometimes K+1.  (More than K+4, non-finite
+//         values, or a threshold more than 60 below the maximum -- the exp underflow region where
+//         probabilities tie -- and the CTA waits for the exact routing instead.)
+//     P2  neuron selection + down projection.  Work unit = (token, candidate, neuron-index
+//         chunk), dealt round-robin in the order the experts finish.  The unit waits (one polite
+//         poller) for its expert's piece counter, loads the h row, finds the pivot bucket from a
+//         512-bin histogram and ranks only the bucket's members (bit-exact
+//         mask_smallest_magnitudes, proj/src/activation.cpp:31-52, lower index first on ties),
+//         and streams exactly the surviving W_down rows of its chunk with direct 128-bit loads,
+//         16 in flight per thread, fp32 accumulation in registers.  Dropped neurons cost no HBM
+//         bytes.
+//     P3  combine: y[t] = sum_s w(t,s) * (sum_chunks partial), slots ascending, shared expert
+//         last with weight 1 (proj/src/router.cpp:109-132, engine.cpp:168-173), fixed order.
+//   warps 1, 2, 0 "G role": TMA producer, tcgen05.mma issuer, epilogue
+//     gate/up + SwiGLU for the shared expert (streams from the first microsecond: it does not
+//     depend on the routing) and then for the union of candidate experts, in EXPERT-MAJOR order
+//     over all CTAs: a piece = 16 neurons (their 16 gate + 16 up rows) x all of d_model, read as
+//     one 3-D TMA box {64 columns, 32 rows, 4 K-blocks} per ring stage out of the 128-row tiled
+//     image.  The MMA is the 128x16x16 instruction on a tile whose rows 32..127 are whatever
+//     follows in shared memory (their accumulator lanes are never read).  Expert u is complete
+//     -- and its down projection starts -- after 1/n_u of the stream, not at its end.
+//   warp 3 "CH role": exact routing.  The order-faithful logit chains (the D dependent float
+//     adds of the reference) run on the last CTAs from the first microsecond; the last chain of
+//     a token block runs route() (proj/src/router.cpp:13-68).  Ids, slot order and weights are
+//     the reference's bit for bit; only P3 needs them.
 //
-// No float atomics anywhere: results are deterministic and, for a given (shape, batch), do not
-// depend on timing.
+// No float atomics anywhere: results are deterministic and, for a given shape, a token's result
+// does not depend on the rest of the batch.
+#include <mutex>
+
 #include "route_device.cuh"
 #include "select_device.cuh"
 #include "tc_ptx.cuh"
@@ -43,66 +53,131 @@ namespace skb {
 
 namespace {
 
-constexpr int kDecThreads = 256;
-constexpr int kDecTokens = 16;                     // MMA N
-constexpr int kDecATile = 128 * kBlockK * 2;       // 16 KB
-constexpr int kDecBTile = kDecTokens * kBlockK * 2;  // 2 KB
-constexpr int kDecStageBytes = kDecATile + kDecBTile;
-constexpr int kDecStages = 9;
-constexpr int kDecWork = kDecStages * kDecStageBytes;  // 165888 B, reused by P0 / P2 scratch
+constexpr int kDecThreads = 384;  // 12 warps
+constexpr int kDThreads = 256;    // the D role: warps 4..11
+constexpr int kWarpEpi = 0, kWarpTma = 1, kWarpMma = 2, kWarpChain = 3, kWarpD0 = 4;
+constexpr int kDecTokens = 16;             // MMA N
+constexpr int kKBox = 4;                   // K blocks per ring stage
+constexpr int kStageA = kKBox * 32 * 128;  // 16 KB: 32 rows x 64 bf16 per K block
+constexpr int kStageB = kKBox * kDecTokens * 128;  // 8 KB
+constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kMaxStages = 8;
 constexpr int kHistBins = 512;
 constexpr int kHistBase = (135 << 3) - (kHistBins - 1);  // top bin = |h| >= 2^8
 constexpr int kMemberCap = 1024;
-constexpr int kMaxKpt = 32;  // keys per thread: N, S <= 8192
-constexpr int kMaxChunkRows = 2048;  // survivors per (row, chunk) unit
-constexpr int kGBatches = 8;         // W_down row batches (mbarriers) of the gather ring
+constexpr int kMaxN = 8192;  // N, S <= 8192
 
-// exact-chain ring (per CTA): 8 experts + 4 tokens per unit, 256-float sub-chunks
-constexpr int kChEB = 8, kChTB = 4, kChSub = 256, kChStages = 4;
+// exact-chain ring (per CTA): 8 experts + 4 tokens per unit, 128-float sub-chunks
+constexpr int kChEB = 8, kChTB = 4, kChSub = 128, kChStages = 4;
 constexpr int kChRow = kChSub + 4;
 constexpr int kChRows = kChEB + kChTB;
-constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 49920
+constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 25344
 
 constexpr int kDecMaxE = 256;
 constexpr int kDecMaxU = 256;  // union of candidate experts
+constexpr int kMaxND = 8;      // d_model slices of the fast logits
 
-// counters (unsigned words)
-enum { kCtrP0 = 0, kCtrExit = 1, kCtrRoute = 2, kCtrP2 = 3, kCtrChain = 4 /*[4]*/, kCtrH = 8 };
+// counters (unsigned words); everything but the epoch is back to zero when a launch ends
+enum {
+  kCtrEpoch = 0,
+  kCtrDone = 1,
+  kCtrExit = 2,
+  kCtrRoute = 3,
+  kCtrChain = 4,   // [4]
+  kCtrXb = 8,      // [16] uint2 {1, epoch}: bf16 token row t is in place
+  kCtrCnt = 40,    // [1 + kDecMaxU] finished gate/up pieces: [0] shared expert, [1 + u] union expert u
+  kCtrWords = kCtrCnt + 1 + kDecMaxU + 7
+};
 
 struct DecSmem {
-  // offsets from the 1024-aligned base
-  static constexpr int work = 0;
-  static constexpr int chain = kDecWork;
-  static constexpr int rowtab = chain + kChBytes;                  // int16 [kDecMaxU + 1][16]
-  static constexpr int uidx = rowtab + (kDecMaxU + 1) * 16 * 2;    // int16 [kDecMaxE]
-  static constexpr int ulist = uidx + kDecMaxE * 2;                // int16 [kDecMaxU]
-  static constexpr int cande = ulist + kDecMaxU * 2;               // int16 [16][20] candidate experts
-  static constexpr int cmask = cande + 16 * 20 * 2;                // uint32 [kDecMaxE]
-  static constexpr int rscr = cmask + kDecMaxE * 4;                // float [E + K + 8] route() scratch
-  static constexpr int bars = rscr + 1152;                         // 8-byte aligned
-  static constexpr int n_bars = 2 * kDecStages + 4 + 2 * kChStages + kGBatches;
-  static constexpr int misc = bars + n_bars * 8;                   // ints
-  static constexpr int total = misc + 64 * 4;
+  int ring, chain, keys, lst, hist, mlist, scr, gred, rowtab, uidx, ulist, cande, cmask, plist, rscr,
+      bars, misc, total;
 };
-static_assert(DecSmem::bars % 8 == 0, "barrier alignment");
-constexpr int kDecSmemBytes = DecSmem::total + 1024;
+constexpr int kNumBars = 2 * kMaxStages + 4 + kChStages;
+__host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax) {
+  DecSmem m;
+  const int nmax_pad = round_up(nmax, 256);
+  int o = 0;
+  m.ring = o;
+  o += stages * kStageBytes;
+  m.chain = o;  // also the landing zone of the last stage's 128-row operand over-read
+  o += kChBytes;
+  m.keys = o;
+  o += nmax_pad * 4;
+  m.lst = o;
+  o += nmax_pad * 2;
+  m.hist = o;
+  o += kHistBins * 4;
+  m.mlist = o;
+  o += (kMemberCap + 8) * 4;
+  m.scr = o;
+  o += 1024;
+  m.gred = o;
+  o += 8192;
+  m.rowtab = o;
+  o += (kDecMaxU + 1) * 16 * 2 + 32;
+  m.uidx = o;
+  o += kDecMaxE * 2;
+  m.ulist = o;
+  o += kDecMaxU * 2;
+  m.cande = o;
+  o += 16 * 20 * 2;
+  m.cmask = o;
+  o += kDecMaxE * 4;
+  m.plist = o;
+  o += 352 * 2;
+  m.rscr = o;
+  o += 1152;
+  m.bars = o;  // 8-byte aligned: every term above is a multiple of 8
+  o += kNumBars * 8;
+  m.misc = o;
+  o += 64 * 4;
+  m.total = o;
+  return m;
+}
+// dynamic shared memory: 227 KB minus the kernel's static shared memory (< 1 KB) and the
+// 1 KB alignment slack
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;
+inline int dec_stages_for(int nmax) {
+  const DecSmem z = dec_smem_layout(0, nmax);
+  int s = (kSmemBudget - z.total) / kStageBytes;
+  return s > kMaxStages ? kMaxStages : s;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// one polite poller: back off between probes so that 148 pollers do not eat L2 bandwidth
 __device__ __forceinline__ void spin_until(const unsigned* p, unsigned target) {
-  while (ld_acquire_u32(p) < target) {
-  }
+  while (ld_acquire_u32(p) < target) __nanosleep(64);
 }
 __device__ __forceinline__ uint2 ld_volatile_u2(const uint2* p) {
   uint2 v;
   asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_volatile_u2(uint2* p, uint32_t x, uint32_t y) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
 }
 __device__ __forceinline__ int hist_bin(uint32_t key) {
   const int b = static_cast<int>(key >> 20) - kHistBase;
@@ -119,6 +194,20 @@ __device__ __forceinline__ void fma8(const uint4& u, float hk, float* a) {
   a[7] = fmaf(__uint_as_float(u.w & 0xffff0000u), hk, a[7]);
 }
 
+// the D role's own barrier (256 threads, id 1); id 2 hands the candidate tables to the G role
+__device__ __forceinline__ void d_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+struct SelDRole {
+  __device__ static __forceinline__ int tid() { return threadIdx.x - kWarpD0 * 32; }
+  __device__ static __forceinline__ void sync() { d_sync(); }
+};
+constexpr int kTableBarThreads = kDThreads + 3 * 32;
+__device__ __forceinline__ void tables_arrive() {
+  asm volatile("bar.arrive 2, %0;" ::"n"(kTableBarThreads) : "memory");
+}
+__device__ __forceinline__ void tables_wait() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kTableBarThreads) : "memory");
+}
+
 }  // namespace
 
 #ifdef SKB_DEBUG_TIMING
@@ -128,32 +217,12 @@ __device__ __forceinline__ long long dec_gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// the dummy shared-memory load makes a stamp placed after a barrier wait for the barrier's
-// release (BAR.SYNC blocks at the next dependent instruction, not at issue)
-#define DEC_T(i) do { if (threadIdx.x == 0) { unsigned dmy; asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(dmy) : "r"(sm_u32 + DecSmem::misc + 252)); g_dec_dbg[blockIdx.x * 24 + (i) + (dmy & 0u)] = dec_gtime(); } } while (0)
-#define DEC_TW(w, i) do { if (threadIdx.x == (w) * 32) g_dec_dbg[blockIdx.x * 24 + (i)] = dec_gtime(); } while (0)
-#define DEC_G(i) do { if (threadIdx.x == 0) g_dec_dbg[blockIdx.x * 24 + (i)] = dec_gtime(); } while (0)
+// stamp i of this CTA, by thread `thr`
+#define DEC_STAMP(thr, i) do { if (threadIdx.x == (thr)) g_dec_dbg[blockIdx.x * 24 + (i)] = dec_gtime(); } while (0)
 extern "C" void skb_debug_dec(long long* out) { cudaMemcpyFromSymbol(out, g_dec_dbg, sizeof(g_dec_dbg)); }
 #else
-#define DEC_T(i) do { } while (0)
-#define DEC_TW(w, i) do { } while (0)
-#define DEC_G(i) do { } while (0)
+#define DEC_STAMP(thr, i) do { } while (0)
 #endif
-
-// One staged W_down row (bf16, in shared memory) times its activation, accumulated into the
-// thread's columns: column tile nt covers columns (nt * 256 + l) * 8 .. + 7.
-template <int NT>
-__device__ __forceinline__ void consume_row(const uint8_t* rowp, float hv, int LPR, int l,
-                                            float (&acc)[NT][8]) {
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int c8 = nt * 256 + l;
-    if (c8 < LPR) {
-      const uint4 u = *reinterpret_cast<const uint4*>(rowp + static_cast<size_t>(c8) * 16);
-      fma8(u, hv, acc[nt]);
-    }
-  }
-}
 
 struct DecodeArgs {
   const float* x;
@@ -164,14 +233,13 @@ struct DecodeArgs {
   int sel_mode, n_off_r, n_off_s;
   const uint8_t* mask_r;
   const uint8_t* mask_s;
-  int CM, CH, capture;
+  int CM, CH, capture, stages, ND, DS;
   __nv_bfloat16* xb;
-  float* lf;
-  float* lm;
+  uint2* p0;  // [16][E][ND][2] of {bits, epoch}: partial fast logit and partial sum of |products|
   float* logits;
   int32_t* ids;
   float* wts;
-  uint2* hc;  // [16 * CM + 16][Nh] of {bits of h, launch epoch}: data and flag in one 8-byte word
+  float* hc;  // [16 * CM + 16][Nh] activations of the candidate rows
   float* part;
   unsigned* ctr;
   float* y;
@@ -191,12 +259,14 @@ __device__ __forceinline__ float ord2f(uint32_t k) {
 }
 
 // Candidate experts of one token (one warp): every expert whose interval [lf - m, lf + m] reaches
-// the K-th largest lower end.  Returns true when the bound cannot be used (non-finite values,
-// the exp-underflow region, or more than CM candidates): the caller then waits for the exact
-// routing.  VPL = experts per lane.
+// the K-th largest lower end.  The fast logit of an expert is the sum of its ND slice partials in
+// slice order (every CTA forms the same sums, hence the same candidate sets); the partials are
+// polled until they carry this launch's epoch.  Returns true when the bound cannot be used
+// (non-finite values, the exp-underflow region, or more than CM candidates): the caller then
+// waits for the exact routing.  VPL = experts per lane.
 template <int VPL>
-__device__ __forceinline__ bool cand_token(const float* lf, const float* lm, int E, int K, int CM,
-                                           int t, uint32_t* cmask) {
+__device__ __forceinline__ bool cand_token(const uint2* p0t, int E, int ND, uint32_t epoch, float mfac,
+                                           int K, int CM, int t, uint32_t* cmask) {
   const int lane = threadIdx.x & 31;
   uint32_t lo[VPL];
   float hi[VPL];
@@ -206,7 +276,23 @@ __device__ __forceinline__ bool cand_token(const float* lf, const float* lm, int
   for (int i = 0; i < VPL; ++i) {
     const int e = i * 32 + lane;
     if (e < E) {
-      const float f = __ldcg(lf + e), m = __ldcg(lm + e);
+      float f = 0.0f, sa = 0.0f;
+#pragma unroll 1
+      for (int j = 0; j < ND; ++j) {
+        const uint2* p = p0t + (static_cast<size_t>(e) * ND + j) * 2;
+        uint2 a = ld_volatile_u2(p), b = ld_volatile_u2(p + 1);
+        while (a.y != epoch) {
+          __nanosleep(32);
+          a = ld_volatile_u2(p);
+        }
+        while (b.y != epoch) {
+          __nanosleep(32);
+          b = ld_volatile_u2(p + 1);
+        }
+        f = __fadd_rn(f, __uint_as_float(a.x));
+        sa = __fadd_rn(sa, __uint_as_float(b.x));
+      }
+      const float m = sa * mfac + 2e-5f;
       lo[i] = f2ord(f - m);
       hi[i] = f + m;
       mxk = max(mxk, f2ord(f));
@@ -248,173 +334,242 @@ __device__ __forceinline__ bool cand_token(const float* lf, const float* lm, int
   return bad;
 }
 
+// The surviving W_down rows lst[0..m) of one unit, dealt to G row groups (group g takes rows
+// g, g + G, ...), 16 loads of 16 bytes in flight per thread; thread l of a group owns the column
+// octets l, l + 256, ... of a row.  `keys` holds the row's activations (float bits).
+template <int NT>
+__device__ __forceinline__ void gather_rows(const __nv_bfloat16* wb, int Dp, int LPR,
+                                            const uint16_t* lst, int m, const uint32_t* keys, int G,
+                                            int g, int l, float (&acc)[NT][8]) {
+  constexpr int RB = 16 / NT;
+#pragma unroll 1
+  for (int k0 = g; k0 < m; k0 += RB * G) {
+    uint4 v[RB][NT];
+    float hv[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int k = k0 + r * G;
+      const bool ok = k < m;
+      const int idx = ok ? lst[k] : 0;
+      hv[r] = ok ? __uint_as_float(keys[idx]) : 0.0f;
+      const uint4* rp = reinterpret_cast<const uint4*>(wb + static_cast<size_t>(idx) * Dp);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c8 = nt * 256 + l;
+        v[r][nt] = (ok && c8 < LPR) ? ld_stream_u4(rp + c8) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) fma8(v[r][nt], hv[r], acc[nt]);
+  }
+}
+
 __global__ void __launch_bounds__(kDecThreads, 1)
-decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
-                    const __grid_constant__ CUtensorMap tmap_xb, const DecodeArgs a) {
+decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
+                    const __grid_constant__ CUtensorMap tmap_xb3, const DecodeArgs a) {
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   const uint32_t sm_u32 = smem_u32(sm);
-  uint8_t* work = sm + DecSmem::work;
-  int16_t* rowtab = reinterpret_cast<int16_t*>(sm + DecSmem::rowtab);
-  int16_t* uidx = reinterpret_cast<int16_t*>(sm + DecSmem::uidx);
-  int16_t* ulist = reinterpret_cast<int16_t*>(sm + DecSmem::ulist);
-  int16_t* cande = reinterpret_cast<int16_t*>(sm + DecSmem::cande);
-  uint32_t* cmask = reinterpret_cast<uint32_t*>(sm + DecSmem::cmask);
-  int* misc = reinterpret_cast<int*>(sm + DecSmem::misc);
-  // misc: 0 tmem ptr, 1 overflow flag, 2 n_u, 8.. P2 scalars, 24.. ncand[16], 40.. pairoff[17]
+  const int nmax = a.N > a.S ? a.N : a.S;
+  const DecSmem L = dec_smem_layout(a.stages, nmax);
+  int16_t* rowtab = reinterpret_cast<int16_t*>(sm + L.rowtab);
+  int16_t* uidx = reinterpret_cast<int16_t*>(sm + L.uidx);
+  int16_t* ulist = reinterpret_cast<int16_t*>(sm + L.ulist);
+  int16_t* cande = reinterpret_cast<int16_t*>(sm + L.cande);
+  uint32_t* cmask = reinterpret_cast<uint32_t*>(sm + L.cmask);
+  int16_t* plist = reinterpret_cast<int16_t*>(sm + L.plist);
+  int* misc = reinterpret_cast<int*>(sm + L.misc);
+  // misc: 0 tmem ptr, 1 overflow flag, 2 n_u, 3 n_pairs, 8.. unit scalars, 24.. ncand[16]
   int* ncand = misc + 24;
-  int* pairoff = misc + 40;
-  const uint32_t bar0 = sm_u32 + DecSmem::bars;
+  const uint32_t bar0 = sm_u32 + L.bars;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
-  auto empty_bar = [&](int s) { return bar0 + 8u * (kDecStages + s); };
-  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * kDecStages + b); };
-  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * kDecStages + 2 + b); };
-  auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + s); };
-  auto cempty_bar = [&](int s) { return bar0 + 8u * (2 * kDecStages + 4 + kChStages + s); };
-  auto gbar = [&](int h) { return bar0 + 8u * (2 * kDecStages + 4 + 2 * kChStages + h); };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kMaxStages + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * kMaxStages + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 2 + b); };
+  auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kMaxStages + 4 + s); };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grid = gridDim.x, bid = blockIdx.x;
-  const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp, CM = a.CM;
+  const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp, CM = a.CM, CH = a.CH;
   const int n_tb = ceil_div(B, kChTB), n_eb = ceil_div(E, kChEB);
+  const int stages = a.stages;
   const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
                       ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
+  // tag of this launch's P0 partials and token-row flags; issued first, consumed late
+  const uint32_t epoch = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrEpoch]) + 1u;
 
-  DEC_T(0);
-  DEC_G(16);
-  // the P2 barrier counter is monotonic: this launch waits for base + grid.  Read first thing
-  // (nobody can have passed P0 yet); the latency hides behind the prologue.
-  unsigned p2_base = 0;
-  if (tid == 0) {
-    p2_base = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrP2]);
-    misc[3] = static_cast<int>(p2_base + 1u);
-  }
+  DEC_STAMP(0, 0);
   // ---- prologue ----
   if (tid == 0) {
-    tma_prefetch_desc(&tmap_w);
-    tma_prefetch_desc(&tmap_xb);
-    for (int s = 0; s < kDecStages; ++s) {
+    tma_prefetch_desc(&tmap_w3);
+    tma_prefetch_desc(&tmap_xb3);
+    for (int s = 0; s < stages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), 4);
+      mbar_init(tempty_bar(b), 1);
     }
-    for (int s = 0; s < kChStages; ++s) {
-      mbar_init(cfull_bar(s), 1);
-      mbar_init(cempty_bar(s), 1);
-    }
-    for (int b = 0; b < kGBatches; ++b) mbar_init(gbar(b), 1);
+    for (int s = 0; s < kChStages; ++s) mbar_init(cfull_bar(s), 1);
     fence_barrier_init();
     misc[1] = 0;
   }
-  if (warp == 1) tmem_alloc(sm_u32 + DecSmem::misc, 32);
+  if (warp == kWarpMma) tmem_alloc(sm_u32 + L.misc, 32);
   for (int e = tid; e < kDecMaxE; e += kDecThreads) cmask[e] = 0u;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(misc);
-  // Tag of this launch's activations: h values travel from the P1 epilogue to P2 as 8-byte
-  // {bits, epoch} words, so a consumer that reads the right epoch has the value -- no fence, no
-  // counter, no polling thread between the two phases.
-  const uint32_t epoch = static_cast<uint32_t>(misc[3]);
 
-  // =====================================================================================
-  // P0: histogram zeroing, bf16 token rows, fast logits with error bounds
-  // =====================================================================================
-  for (int t = (bid - E % grid + grid) % grid; t < B; t += grid) {
-    const float* src = a.x + static_cast<size_t>(t) * D;
-    __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
-    for (int d = tid; d < D; d += kDecThreads) dst[d] = __float2bfloat16_rn(__ldg(src + d));
-  }
-  {
-    float* red = reinterpret_cast<float*>(work);  // [8 warps][4 tokens][2]
-    // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
-    const double u24 = 5.9604644775390625e-8;
-    const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
-#pragma unroll 1
-    for (int e = bid; e < E; e += grid) {
-      const float* wr = a.router + static_cast<size_t>(e) * D;
-#pragma unroll 1
-      for (int t0 = 0; t0 < B; t0 += 4) {
-        float pl[4] = {0.0f, 0.0f, 0.0f, 0.0f}, pa[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if (vec_ok) {
-          const float4* w4 = reinterpret_cast<const float4*>(wr);
-#pragma unroll 2
-          for (int q = tid; q < D / 4; q += kDecThreads) {
-            const float4 w = __ldg(w4 + q);
-#pragma unroll
-            for (int tt = 0; tt < 4; ++tt) {
-              if (t0 + tt < B) {
-                const float4 xv =
-                    __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t0 + tt) * D) + q);
-                pl[tt] = fmaf(w.x, xv.x, pl[tt]);
-                pl[tt] = fmaf(w.y, xv.y, pl[tt]);
-                pl[tt] = fmaf(w.z, xv.z, pl[tt]);
-                pl[tt] = fmaf(w.w, xv.w, pl[tt]);
-                pa[tt] = fmaf(fabsf(w.x), fabsf(xv.x), pa[tt]);
-                pa[tt] = fmaf(fabsf(w.y), fabsf(xv.y), pa[tt]);
-                pa[tt] = fmaf(fabsf(w.z), fabsf(xv.z), pa[tt]);
-                pa[tt] = fmaf(fabsf(w.w), fabsf(xv.w), pa[tt]);
-              }
-            }
-          }
-        } else {
-#pragma unroll 1
-          for (int d = tid; d < D; d += kDecThreads) {
-            const float w = __ldg(wr + d);
-#pragma unroll
-            for (int tt = 0; tt < 4; ++tt) {
-              if (t0 + tt < B) {
-                const float xv = __ldg(a.x + static_cast<size_t>(t0 + tt) * D + d);
-                pl[tt] = fmaf(w, xv, pl[tt]);
-                pa[tt] = fmaf(fabsf(w), fabsf(xv), pa[tt]);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int tt = 0; tt < 4; ++tt) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            pl[tt] += __shfl_xor_sync(0xffffffffu, pl[tt], o);
-            pa[tt] += __shfl_xor_sync(0xffffffffu, pa[tt], o);
-          }
-          if (lane == 0) {
-            red[(warp * 4 + tt) * 2 + 0] = pl[tt];
-            red[(warp * 4 + tt) * 2 + 1] = pa[tt];
-          }
-        }
-        __syncthreads();
-        if (tid < 4 && t0 + tid < B) {
-          float s = 0.0f, sa = 0.0f;
-#pragma unroll
-          for (int w = 0; w < kDecThreads / 32; ++w) {
-            s += red[(w * 4 + tid) * 2 + 0];
-            sa += red[(w * 4 + tid) * 2 + 1];
-          }
-          a.lf[static_cast<size_t>(t0 + tid) * E + e] = s;
-          a.lm[static_cast<size_t>(t0 + tid) * E + e] = sa * mfac + 2e-5f;
-        }
-        __syncthreads();
+  const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
+  const int KB = Dp / kBlockK;
+  const int KX = ceil_div(KB, kKBox);       // ring stages per piece
+  const int PE = 4 * NB;                    // pieces per routed expert
+  const int n_sh = 4 * NBs;                 // pieces of the shared expert (come first)
+
+  if (warp == kWarpTma) {
+    // =====================================================================================
+    // G role, producer: one 3-D box of the weight image + the matching token K blocks per stage
+    // =====================================================================================
+    if (lane == 0) {
+      // the bf16 token rows are written by the D role of B CTAs: wait for their flags
+      for (int t = 0; t < B; ++t) {
+        const uint2* f = reinterpret_cast<const uint2*>(a.ctr + kCtrXb) + t;
+        while (ld_volatile_u2(f).y != epoch) __nanosleep(32);
       }
+      __threadfence();
+      fence_proxy_async_all();
     }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    fence_proxy_async_all();
-    atomicAdd(&a.ctr[kCtrP0], 1u);
-  }
-  DEC_T(1);
-
-  // =====================================================================================
-  // Exact routing chains: warps 6 (consumer) and 7 (producer), on the LAST CTAs of the grid
-  // (the first ones carry the logit units and, at decode sizes, all the gate/up items).  They
-  // only read x and the router, so they start right away; their result is needed by P3.
-  // =====================================================================================
-  if (warp >= 6) {
-    float* ring = reinterpret_cast<float*>(sm + DecSmem::chain);
+    int gk = 0, p = bid;
+    auto produce = [&](int rb, int q) {
+#pragma unroll 1
+      for (int kx = 0; kx < KX; ++kx, ++gk) {
+        const int s = gk % stages;
+        mbar_wait(empty_bar(s), ((gk / stages) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(full_bar(s), kStageBytes);
+        const uint32_t dst = sm_u32 + L.ring + s * kStageBytes;
+        tma_load_3d(dst, &tmap_w3, 0, q * 32, rb * KB + kx * kKBox, full_bar(s), kPolicyEvictFirst);
+        tma_load_3d(dst + kStageA, &tmap_xb3, 0, 0, kx * kKBox, full_bar(s), kPolicyEvictLast);
+      }
+    };
+    if (lane == 0) {
+#pragma unroll 1
+      for (; p < n_sh; p += grid) produce(E * NB + (p >> 2), p & 3);
+    }
+    __syncwarp();
+    tables_wait();
+    if (lane == 0) {
+      const int n_u = misc[2];
+      DEC_STAMP(32, 2);
+#pragma unroll 1
+      for (; p < n_sh + n_u * PE; p += grid) {
+        const int pr = p - n_sh;
+        const int u = pr / PE, qq = pr % PE;
+        produce(static_cast<int>(ulist[u]) * NB + (qq >> 2), qq & 3);
+      }
+      DEC_STAMP(32, 3);
+    }
+  } else if (warp == kWarpMma) {
+    // =====================================================================================
+    // G role, MMA issuer: 128x16x16 on a tile whose first 32 rows are the piece
+    // =====================================================================================
+    constexpr uint32_t kIdesc = make_idesc_bf16(128, kDecTokens);
+    int gk = 0, li = 0, p = bid;
+    auto issue_piece = [&]() {
+      const int buf = li & 1;
+      mbar_wait(tempty_bar(buf), (((li >> 1) & 1u) ^ 1u));
+      tc_fence_after();
+#pragma unroll 1
+      for (int kx = 0; kx < KX; ++kx, ++gk) {
+        const int s = gk % stages;
+        mbar_wait(full_bar(s), (gk / stages) & 1u);
+        tc_fence_after();
+        const uint32_t st = sm_u32 + L.ring + s * kStageBytes;
+        const int nk = min(kKBox, KB - kx * kKBox);
+#pragma unroll 1
+        for (int j = 0; j < nk; ++j) {
+          const uint64_t a_desc = make_smem_desc_sw128(st + j * 4096);
+          const uint64_t b_desc = make_smem_desc_sw128(st + kStageA + j * 2048);
+#pragma unroll
+          for (int k = 0; k < kBlockK / 16; ++k)
+            umma_bf16(tmem_base + buf * kDecTokens, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
+                      (kx | j | k) != 0 ? 1u : 0u);
+        }
+        umma_commit(empty_bar(s));
+      }
+      umma_commit(tfull_bar(buf));
+      ++li;
+    };
+    if (lane == 0) {
+#pragma unroll 1
+      for (; p < n_sh; p += grid) issue_piece();
+    }
+    __syncwarp();
+    tables_wait();
+    if (lane == 0) {
+      const int n_u = misc[2];
+#pragma unroll 1
+      for (; p < n_sh + n_u * PE; p += grid) issue_piece();
+    }
+  } else if (warp == kWarpEpi) {
+    // =====================================================================================
+    // G role, epilogue: TMEM lanes 0-15 hold the gate rows, 16-31 the up rows of 16 neurons
+    // =====================================================================================
+    const bool is_gate_lane = lane < 16;
+    int li = 0, p = bid;
+    auto finish_piece = [&](int u /* -1: shared */, int nb, int q, int m_valid) {
+      const int buf = li & 1;
+      mbar_wait(tfull_bar(buf), (li >> 1) & 1u);
+      tc_fence_after();
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(tmem_base + buf * kDecTokens, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(buf));
+      const int n = nb * kNeuronBlock + 16 * q + (lane & 15);
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        if (c < B) {
+          const float mine0 = __uint_as_float(v[c]);
+          const float mine1 = __uint_as_float(v[c + 1]);
+          const float send = is_gate_lane ? mine1 : mine0;
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+          const float g = is_gate_lane ? mine0 : recv;
+          const float up = is_gate_lane ? recv : mine1;
+          const int col = c + (is_gate_lane ? 0 : 1);
+          if (col < B && n < m_valid) {
+            const int r = u < 0 ? kDecTokens * CM + col : rowtab[u * 16 + col];
+            if (r >= 0) a.hc[static_cast<size_t>(r) * a.Nh + n] = silu_f(g) * up;
+          }
+        }
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&a.ctr[kCtrCnt + 1 + u], 1u);
+      ++li;
+    };
+#pragma unroll 1
+    for (; p < n_sh; p += grid) finish_piece(-1, p >> 2, p & 3, a.S);
+    tables_wait();
+    const int n_u = misc[2];
+#pragma unroll 1
+    for (; p < n_sh + n_u * PE; p += grid) {
+      const int pr = p - n_sh;
+      const int u = pr / PE, qq = pr % PE;
+      finish_piece(u, qq >> 2, qq & 3, a.N);
+    }
+    DEC_STAMP(0, 4);
+  } else if (warp == kWarpChain) {
+    // =====================================================================================
+    // Exact routing chains on the LAST CTAs of the grid, one warp: lane 0 keeps a ring of 1-D
+    // bulk copies ahead of the 32 dependent chains (8 experts x 4 tokens).  They only read x and
+    // the router, so they start right away; their result is needed by P3 (and by caller-mask
+    // lookups).
+    // =====================================================================================
+    float* ring = reinterpret_cast<float*>(sm + L.chain);
     const int n_cu = n_eb * n_tb;
     const int nsub = ceil_div(D, kChSub);
     int gsc = 0;  // ring position, continues across units
@@ -423,159 +578,241 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
       const int eb = cu % n_eb, tb = cu / n_eb;
       const int e0 = eb * kChEB, t0 = tb * kChTB;
       const int n_e = min(kChEB, E - e0), n_t = min(kChTB, B - t0);
-      if (warp == 7) {
-        const float* wsrc = a.router + static_cast<size_t>(e0) * D;
-        const float* xsrc = a.x + static_cast<size_t>(t0) * D;
-        int psc = gsc;
+      const float* wsrc = a.router + static_cast<size_t>(e0) * D;
+      const float* xsrc = a.x + static_cast<size_t>(t0) * D;
+      auto issue = [&](int sc, int gidx) {  // lane 0: sub-chunk sc of this unit into its ring slot
+        const int slot = gidx % kChStages;
+        const int d0 = sc * kChSub;
+        const uint32_t bytes = static_cast<uint32_t>(min(kChSub, D - d0)) * 4u;
+        mbar_arrive_expect_tx(cfull_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
+        const uint32_t dst = smem_u32(ring + slot * kChRows * kChRow);
+#pragma unroll 1
+        for (int r = 0; r < n_e; ++r)
+          bulk_copy_g2s(dst + r * kChRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
+                        cfull_bar(slot));
+#pragma unroll 1
+        for (int r = 0; r < n_t; ++r)
+          bulk_copy_g2s(dst + (kChEB + r) * kChRow * 4, xsrc + static_cast<size_t>(r) * D + d0, bytes,
+                        cfull_bar(slot));
+      };
+      if (vec_ok && lane == 0)
+        for (int sc = 0; sc < nsub && sc < kChStages; ++sc) issue(sc, gsc + sc);
+      __syncwarp();
+      const int e_i = lane / kChTB, t_j = lane % kChTB;
+      const bool valid = (e_i < n_e) && (t_j < n_t);
+      float acc = 0.0f;
+      DEC_STAMP(kWarpChain * 32, 14);
+#pragma unroll 1
+      for (int sc = 0; sc < nsub; ++sc) {
+        const int gidx = gsc + sc;
+        const int slot = gidx % kChStages;
+        float* base = ring + slot * kChRows * kChRow;
+        const int n = min(kChSub, D - sc * kChSub);
         if (vec_ok) {
-          if (lane == 0) {
-#pragma unroll 1
-            for (int sc = 0; sc < nsub; ++sc, ++psc) {
-              const int slot = psc % kChStages;
-              mbar_wait(cempty_bar(slot), ((psc / kChStages) & 1u) ^ 1u);
-              const int d0 = sc * kChSub;
-              const uint32_t bytes = static_cast<uint32_t>(min(kChSub, D - d0)) * 4u;
-              mbar_arrive_expect_tx(cfull_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
-              const uint32_t dst = smem_u32(ring + slot * kChRows * kChRow);
-#pragma unroll 1
-              for (int r = 0; r < n_e; ++r)
-                bulk_copy_g2s(dst + r * kChRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
-                              cfull_bar(slot));
-#pragma unroll 1
-              for (int r = 0; r < n_t; ++r)
-                bulk_copy_g2s(dst + (kChEB + r) * kChRow * 4, xsrc + static_cast<size_t>(r) * D + d0,
-                              bytes, cfull_bar(slot));
-            }
-          }
+          mbar_wait(cfull_bar(slot), (gidx / kChStages) & 1u);
         } else {
+          // unaligned operands: the warp stages the sub-chunk itself
+          const int d0 = sc * kChSub;
 #pragma unroll 1
-          for (int sc = 0; sc < nsub; ++sc, ++psc) {
-            const int slot = psc % kChStages;
-            mbar_wait(cempty_bar(slot), ((psc / kChStages) & 1u) ^ 1u);
-            const int d0 = sc * kChSub;
-            const int n = min(kChSub, D - d0);
-            float* dst = ring + slot * kChRows * kChRow;
+          for (int r = 0; r < n_e + n_t; ++r) {
+            const float* src = (r < n_e) ? wsrc + static_cast<size_t>(r) * D + d0
+                                         : xsrc + static_cast<size_t>(r - n_e) * D + d0;
+            float* drow = base + ((r < n_e) ? r : kChEB + r - n_e) * kChRow;
 #pragma unroll 1
-            for (int r = 0; r < n_e + n_t; ++r) {
-              const float* src = (r < n_e) ? wsrc + static_cast<size_t>(r) * D + d0
-                                           : xsrc + static_cast<size_t>(r - n_e) * D + d0;
-              float* drow = dst + ((r < n_e) ? r : kChEB + r - n_e) * kChRow;
-#pragma unroll 1
-              for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(cfull_bar(slot));
+            for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
           }
-        }
-      } else {
-        const int e_i = lane / kChTB, t_j = lane % kChTB;
-        const bool valid = (e_i < n_e) && (t_j < n_t);
-        float acc = 0.0f;
-        int csc = gsc;
-        DEC_TW(6, 14);
-#pragma unroll 1
-        for (int sc = 0; sc < nsub; ++sc, ++csc) {
-          const int slot = csc % kChStages;
-          mbar_wait(cfull_bar(slot), (csc / kChStages) & 1u);
-          const float* base = ring + slot * kChRows * kChRow;
-          const float* wr = base + e_i * kChRow;
-          const float* xr = base + (kChEB + t_j) * kChRow;
-          const int n = min(kChSub, D - sc * kChSub);
-          const int n4 = n >> 2;
-#pragma unroll 8
-          for (int q = 0; q < n4; ++q) {
-            const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
-            const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
-            acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
-            acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
-            acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
-            acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
-          }
-#pragma unroll 1
-          for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
           __syncwarp();
-          if (lane == 0) mbar_arrive(cempty_bar(slot));
         }
-        DEC_TW(6, 15);
-        if (valid) a.logits[static_cast<size_t>(t0 + t_j) * E + e0 + e_i] = acc;
+        const float* wr = base + e_i * kChRow;
+        const float* xr = base + (kChEB + t_j) * kChRow;
+        const int n4 = n >> 2;
+#pragma unroll 8
+        for (int q = 0; q < n4; ++q) {
+          const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
+          const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
+          acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
+          acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
+          acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
+          acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
+        }
+#pragma unroll 1
+        for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
+        __syncwarp();  // every lane is done with the slot: lane 0 refills it
+        if (vec_ok && lane == 0 && sc + kChStages < nsub) issue(sc + kChStages, gidx + kChStages);
+      }
+      DEC_STAMP(kWarpChain * 32, 15);
+      if (valid) a.logits[static_cast<size_t>(t0 + t_j) * E + e0 + e_i] = acc;
+      __threadfence();
+      __syncwarp();
+      unsigned prev = 0;
+      if (lane == 0) prev = atomicAdd(&a.ctr[kCtrChain + tb], 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == static_cast<unsigned>(n_eb - 1)) {
+        // last chain of this token block: route() for its tokens
+        __threadfence();
+        float* scr = reinterpret_cast<float*>(sm + L.rscr);
+#pragma unroll 1
+        for (int tt = 0; tt < n_t; ++tt) {
+          const int t = t0 + tt;
+          warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, scr,
+                           a.ids + static_cast<size_t>(t) * K, a.wts + static_cast<size_t>(t) * K);
+        }
         __threadfence();
         __syncwarp();
-        unsigned prev = 0;
-        if (lane == 0) prev = atomicAdd(&a.ctr[kCtrChain + tb], 1u);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == static_cast<unsigned>(n_eb - 1)) {
-          // last chain of this token block: route() for its tokens
-          __threadfence();
-          float* scr = reinterpret_cast<float*>(sm + DecSmem::rscr);
-#pragma unroll 1
-          for (int tt = 0; tt < n_t; ++tt) {
-            const int t = t0 + tt;
-            warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, scr,
-                             a.ids + static_cast<size_t>(t) * K, a.wts + static_cast<size_t>(t) * K);
-          }
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) atomicAdd(&a.ctr[kCtrRoute], 1u);
-        }
+        if (lane == 0) atomicAdd(&a.ctr[kCtrRoute], 1u);
+        DEC_STAMP(kWarpChain * 32, 10);
       }
       gsc += nsub;
     }
-    DEC_TW(6, 10);
-  }
+  } else {
+    // =====================================================================================
+    // D role (warps 4..11)
+    // =====================================================================================
+    const int dtid = tid - kWarpD0 * 32, dwarp = dtid >> 5;
+    uint32_t* keys_s = reinterpret_cast<uint32_t*>(sm + L.keys);
+    uint16_t* lst = reinterpret_cast<uint16_t*>(sm + L.lst);
+    int* hist_s = reinterpret_cast<int*>(sm + L.hist);
+    uint32_t* mlist = reinterpret_cast<uint32_t*>(sm + L.mlist);
+    int* wc = reinterpret_cast<int*>(sm + L.scr);  // [8] warp counts, [8..16) second set
+    float* gred = reinterpret_cast<float*>(sm + L.gred);
+    int* p2 = misc + 8;  // 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount
 
-  // =====================================================================================
-  // P0 barrier, candidates (every CTA computes the same tables), P1
-  // =====================================================================================
-  if (warp < 6) {
-    if (tid == 0) {
-      spin_until(&a.ctr[kCtrP0], static_cast<unsigned>(grid));
-      fence_proxy_async_all();
-    }
-    asm volatile("bar.sync 2, 192;" ::: "memory");
-    DEC_T(2);
-#pragma unroll 1
-    for (int t = warp; t < B; t += 6) {
-      bool bad;
-      if (E <= 64)
-        bad = cand_token<2>(a.lf + t * E, a.lm + t * E, E, K, CM, t, cmask);
-      else if (E <= 128)
-        bad = cand_token<4>(a.lf + t * E, a.lm + t * E, E, K, CM, t, cmask);
-      else
-        bad = cand_token<8>(a.lf + t * E, a.lm + t * E, E, K, CM, t, cmask);
-      if (bad && lane == 0) misc[1] = 1;
-    }
-    asm volatile("bar.sync 2, 192;" ::: "memory");
-    if (misc[1] != 0) {
-      // rare: the bound could not separate the candidates -- wait for the exact routing
-      if (tid == 0) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
-      for (int e = tid; e < E; e += 192) cmask[e] = 0u;
-      asm volatile("bar.sync 2, 192;" ::: "memory");
-      for (int i = tid; i < B * K; i += 192) atomicOr(&cmask[__ldcg(a.ids + i)], 1u << (i / K));
-      asm volatile("bar.sync 2, 192;" ::: "memory");
-    }
-    // union list (ascending expert id) by warp 0
-    if (warp == 0) {
-      int run = 0;
-#pragma unroll 1
-      for (int base = 0; base < E; base += 32) {
-        const int e = base + lane;
-        const bool f = e < E && cmask[e] != 0u;
-        const unsigned b = __ballot_sync(0xffffffffu, f);
-        const int pos = run + __popc(b & ((1u << lane) - 1u));
-        if (e < E) uidx[e] = f ? static_cast<int16_t>(pos) : static_cast<int16_t>(-1);
-        if (f) ulist[pos] = static_cast<int16_t>(e);
-        run += __popc(b);
+    // ---- P0a: bf16 token rows for the TMA (token t on CTA (grid - 1 - t) % grid ... any) ----
+    for (int t = bid; t < B; t += grid) {
+      const float* src = a.x + static_cast<size_t>(t) * D;
+      __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
+      for (int d = dtid; d < D; d += kDThreads) dst[d] = __float2bfloat16_rn(__ldg(src + d));
+      __threadfence();
+      d_sync();
+      if (dtid == 0) {
+        fence_proxy_async_all();
+        st_volatile_u2(reinterpret_cast<uint2*>(a.ctr + kCtrXb) + t, 1u, epoch);
       }
-      if (lane == 0) misc[2] = run;
     }
-    asm volatile("bar.sync 2, 192;" ::: "memory");
-    const int n_u = misc[2];
-    // The TMA warp only needs the union list: it starts streaming now.  Warps 1-5 build the
-    // per-token tables (row table column, candidate list and count) meanwhile; the MMA issuer
-    // and the epilogue warps take up their roles after barrier 3.
-    if (warp != 0) {
+    // ---- P0b: fast logits of (expert, d_model slice) units ----
+    const int ND = a.ND, DS = a.DS;
+    {
+      float* red = gred;  // [8 warps][4 tokens][2]
 #pragma unroll 1
-      for (int t = warp - 1; t < kDecTokens; t += 5) {
+      for (int unit = (bid + grid - B % grid) % grid; unit < E * ND; unit += grid) {
+        const int e = unit / ND, j = unit % ND;
+        const int d0 = j * DS, d1 = min(D, d0 + DS);
+        const float* wr = a.router + static_cast<size_t>(e) * D;
+#pragma unroll 1
+        for (int t0 = 0; t0 < B; t0 += 4) {
+          float pl[4] = {0.0f, 0.0f, 0.0f, 0.0f}, pa[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          if (vec_ok) {
+            const float4* w4 = reinterpret_cast<const float4*>(wr);
+#pragma unroll 2
+            for (int q = d0 / 4 + dtid; q < d1 / 4; q += kDThreads) {
+              const float4 w = __ldg(w4 + q);
+#pragma unroll
+              for (int tt = 0; tt < 4; ++tt) {
+                if (t0 + tt < B) {
+                  const float4 xv =
+                      __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t0 + tt) * D) + q);
+                  pl[tt] = fmaf(w.x, xv.x, pl[tt]);
+                  pl[tt] = fmaf(w.y, xv.y, pl[tt]);
+                  pl[tt] = fmaf(w.z, xv.z, pl[tt]);
+                  pl[tt] = fmaf(w.w, xv.w, pl[tt]);
+                  pa[tt] = fmaf(fabsf(w.x), fabsf(xv.x), pa[tt]);
+                  pa[tt] = fmaf(fabsf(w.y), fabsf(xv.y), pa[tt]);
+                  pa[tt] = fmaf(fabsf(w.z), fabsf(xv.z), pa[tt]);
+                  pa[tt] = fmaf(fabsf(w.w), fabsf(xv.w), pa[tt]);
+                }
+              }
+            }
+          } else {
+#pragma unroll 1
+            for (int d = d0 + dtid; d < d1; d += kDThreads) {
+              const float w = __ldg(wr + d);
+#pragma unroll
+              for (int tt = 0; tt < 4; ++tt) {
+                if (t0 + tt < B) {
+                  const float xv = __ldg(a.x + static_cast<size_t>(t0 + tt) * D + d);
+                  pl[tt] = fmaf(w, xv, pl[tt]);
+                  pa[tt] = fmaf(fabsf(w), fabsf(xv), pa[tt]);
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int tt = 0; tt < 4; ++tt) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              pl[tt] += __shfl_xor_sync(0xffffffffu, pl[tt], o);
+              pa[tt] += __shfl_xor_sync(0xffffffffu, pa[tt], o);
+            }
+            if (lane == 0) {
+              red[(dwarp * 4 + tt) * 2 + 0] = pl[tt];
+              red[(dwarp * 4 + tt) * 2 + 1] = pa[tt];
+            }
+          }
+          d_sync();
+          if (dtid < 4 && t0 + dtid < B) {
+            float s = 0.0f, sa = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kDThreads / 32; ++w) {
+              s += red[(w * 4 + dtid) * 2 + 0];
+              sa += red[(w * 4 + dtid) * 2 + 1];
+            }
+            uint2* dst = a.p0 + ((static_cast<size_t>(t0 + dtid) * E + e) * ND + j) * 2;
+            st_volatile_u2(dst, __float_as_uint(s), epoch);
+            st_volatile_u2(dst + 1, __float_as_uint(sa), epoch);
+          }
+          d_sync();
+        }
+      }
+    }
+    DEC_STAMP(kWarpD0 * 32, 1);
+
+    // ---- candidates (every CTA computes the same tables) ----
+    {
+      // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
+      const double u24 = 5.9604644775390625e-8;
+      const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
+#pragma unroll 1
+      for (int t = dwarp; t < B; t += 8) {
+        const uint2* p0t = a.p0 + static_cast<size_t>(t) * E * ND * 2;
+        bool bad;
+        if (E <= 64)
+          bad = cand_token<2>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+        else if (E <= 128)
+          bad = cand_token<4>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+        else
+          bad = cand_token<8>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+        if (bad && lane == 0) misc[1] = 1;
+      }
+      d_sync();
+      if (misc[1] != 0) {
+        // rare: the bound could not separate the candidates -- wait for the exact routing
+        if (dtid == 0) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+        d_sync();
+        for (int e = dtid; e < E; e += kDThreads) cmask[e] = 0u;
+        d_sync();
+        for (int i = dtid; i < B * K; i += kDThreads) atomicOr(&cmask[__ldcg(a.ids + i)], 1u << (i / K));
+        d_sync();
+      }
+      // union list (ascending expert id) by D warp 0
+      if (dwarp == 0) {
+        int run = 0;
+#pragma unroll 1
+        for (int base = 0; base < E; base += 32) {
+          const int e = base + lane;
+          const bool f = e < E && cmask[e] != 0u;
+          const unsigned b = __ballot_sync(0xffffffffu, f);
+          const int pos = run + __popc(b & ((1u << lane) - 1u));
+          if (e < E) uidx[e] = f ? static_cast<int16_t>(pos) : static_cast<int16_t>(-1);
+          if (f) ulist[pos] = static_cast<int16_t>(e);
+          run += __popc(b);
+        }
+        if (lane == 0) misc[2] = run;
+      }
+      d_sync();
+      const int n_u = misc[2];
+      // per-token tables: row table column, candidate list and count
+#pragma unroll 1
+      for (int t = dwarp; t < kDecTokens; t += 8) {
         for (int u = lane; u <= n_u; u += 32) rowtab[u * 16 + t] = -1;
         __syncwarp();
         if (t < B) {
@@ -592,226 +829,66 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             }
             run += __popc(b);
           }
-          if (lane == 0) {
-            ncand[t] = run;
-            if (a.has_shared) rowtab[n_u * 16 + t] = static_cast<int16_t>(kDecTokens * CM + t);
-          }
+          if (lane == 0) ncand[t] = run;
         }
       }
-      asm volatile("bar.sync 3, 160;" ::: "memory");
-      if (tid == 32) {
+      d_sync();
+      tables_arrive();  // the G role may stream the routed experts now
+      DEC_STAMP(kWarpD0 * 32, 2);
+      // pair list in the order the experts finish: shared expert first, then union order
+      if (dwarp == 0) {
         int run = 0;
-        for (int t = 0; t < B; ++t) {
-          pairoff[t] = run;
-          run += ncand[t] + (a.has_shared ? 1 : 0);
+        if (a.has_shared) {
+          if (lane < B) plist[lane] = static_cast<int16_t>(n_u * 16 + lane);
+          run = B;
         }
-        pairoff[B] = run;
+#pragma unroll 1
+        for (int base = 0; base < n_u * 16; base += 32) {
+          const int i = base + lane;
+          const bool f = i < n_u * 16 && rowtab[i] >= 0;
+          const unsigned b = __ballot_sync(0xffffffffu, f);
+          if (f) plist[run + __popc(b & ((1u << lane) - 1u))] = static_cast<int16_t>(i);
+          run += __popc(b);
+        }
+        if (lane == 0) misc[3] = run;
       }
+      d_sync();
     }
-    DEC_T(3);
 
-    // ---- P1: gate/up + SwiGLU over (union expert, 64-neuron block) items ----
-    const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
-    const int n_items = n_u * NB + NBs;
-    const int KB = Dp / kBlockK;
-    if (warp == 0) {
-      if (lane == 0) {
-        int gk = 0;
+    // ---- P2: selection + down projection over (pair, neuron-index chunk) units ----
+    {
+      const int n_u = misc[2];
+      const int n_units = misc[3] * CH;
+      const int LPR = Dp >> 3;
+      const int NT = ceil_div(LPR, 256);
+      const int G = NT == 1 ? 256 / LPR : 1;
+      const int g = NT == 1 ? dtid / LPR : 0, l = NT == 1 ? dtid % LPR : dtid;
+      const bool lane_ok = g < G;
+      bool route_ready = false;
+      __shared__ SelScratch sel_sc;
 #pragma unroll 1
-        for (int it = bid; it < n_items; it += grid) {
-          const bool sh = it >= n_u * NB;
-          const int u = sh ? n_u : it / NB;
-          const int nb = sh ? it - n_u * NB : it % NB;
-          const int e = sh ? E : ulist[u];
-          const int a_row = e * 2 * a.Np + nb * 128;
-#pragma unroll 1
-          for (int kb = 0; kb < KB; ++kb, ++gk) {
-            const int s = gk % kDecStages;
-            mbar_wait(empty_bar(s), ((gk / kDecStages) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(full_bar(s), kDecStageBytes);
-            const uint32_t dst = sm_u32 + s * kDecStageBytes;
-            tma_load_2d(dst, &tmap_w, 0, ((a_row >> 7) * KB + kb) * 128, full_bar(s),
-                        kPolicyEvictFirst);
-            tma_load_2d(dst + kDecATile, &tmap_xb, kb * kBlockK, 0, full_bar(s), kPolicyEvictLast);
-          }
-        }
-      }
-    } else if (warp == 1) {
-      if (lane == 0) {
-        constexpr uint32_t kIdesc = make_idesc_bf16(128, kDecTokens);
-        int gk = 0, li = 0;
-#pragma unroll 1
-        for (int it = bid; it < n_items; it += grid, ++li) {
-          const int buf = li & 1;
-          mbar_wait(tempty_bar(buf), (((li >> 1) & 1u) ^ 1u));
-          tc_fence_after();
-#pragma unroll 1
-          for (int kb = 0; kb < KB; ++kb, ++gk) {
-            const int s = gk % kDecStages;
-            mbar_wait(full_bar(s), (gk / kDecStages) & 1u);
-            tc_fence_after();
-            const uint32_t a_smem = sm_u32 + s * kDecStageBytes;
-            const uint64_t a_desc = make_smem_desc_sw128(a_smem);
-            const uint64_t b_desc = make_smem_desc_sw128(a_smem + kDecATile);
-#pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k)
-              umma_bf16(tmem_base + buf * kDecTokens, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
-                        (kb | k) != 0 ? 1u : 0u);
-            umma_commit(empty_bar(s));
-          }
-          umma_commit(tfull_bar(buf));
-        }
-      }
-    } else {
-      const int q = warp & 3;
-      const bool is_gate_lane = lane < 16;
-      int li = 0;
-#pragma unroll 1
-      for (int it = bid; it < n_items; it += grid, ++li) {
-        const bool sh = it >= n_u * NB;
-        const int u = sh ? n_u : it / NB;
-        const int nb = sh ? it - n_u * NB : it % NB;
-        const int m_valid = sh ? a.S : a.N;
-        const int buf = li & 1;
-        mbar_wait(tfull_bar(buf), (li >> 1) & 1u);
-        tc_fence_after();
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + buf * kDecTokens, v);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(buf));
-        const int n = nb * kNeuronBlock + 16 * q + (lane & 15);
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          if (c < B) {
-            const float mine0 = __uint_as_float(v[c]);
-            const float mine1 = __uint_as_float(v[c + 1]);
-            const float send = is_gate_lane ? mine1 : mine0;
-            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-            const float g = is_gate_lane ? mine0 : recv;
-            const float up = is_gate_lane ? recv : mine1;
-            const int col = c + (is_gate_lane ? 0 : 1);
-            if (col < B && n < m_valid) {
-              const int r = rowtab[u * 16 + col];
-              if (r >= 0) {
-                const float hval = silu_f(g) * up;
-                a.hc[static_cast<size_t>(r) * a.Nh + n] = make_uint2(__float_as_uint(hval), epoch);
-              }
-            }
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  DEC_T(4);
-  DEC_G(17);
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, 32);
-  }
-
-  // =====================================================================================
-  // P2: selection + down projection over (token, candidate, row chunk) units.  Units are dealt
-  // in contiguous ranges, chunk index fastest, so a CTA that holds several chunks of one row
-  // selects once.  The chunking depends on the shape only -- not on the batch -- so the
-  // reduction tree of a token does not depend on what else is in the batch.  Candidates that the
-  // exact routing later rejects (rare) are computed and ignored by P3.
-  // =====================================================================================
-  const int n_u = misc[2];
-  const int CH = a.CH;
-  {
-        const int n_units = pairoff[B] * CH;
-    // scratch inside the (now idle) GEMM stage area, sized by the shape so that as many W_down
-    // rows as possible can be in flight
-    const int nmax_pad = round_up(a.N > a.S ? a.N : a.S, 256);
-    int so = 0;
-    uint16_t* lst_idx = reinterpret_cast<uint16_t*>(work + so);  // [nmax_pad] survivors of a run
-    so += nmax_pad * 2;
-    uint32_t* mlist = reinterpret_cast<uint32_t*>(work + so);  // [kMemberCap + 4] pivot bucket
-    so += 4352;
-    int* wc = reinterpret_cast<int*>(work + so);               // [kMaxKpt * 8] + [8]
-    so += 1280;
-    float* gred = reinterpret_cast<float*>(work + so);         // [G][Dp] <= 8 KB (NT == 1)
-    so += 8192;
-    int* hist_s = reinterpret_cast<int*>(work + so);           // [kHistBins] histogram of the row
-    so += kHistBins * 4;
-    uint32_t* keys_s = reinterpret_cast<uint32_t*>(work + so); // [nmax_pad] raw bits of h
-    so += nmax_pad * 4;
-    uint8_t* kf = work + so;                                   // [nmax_pad] keep flags
-    so += nmax_pad;
-    so = round_up(so, 1024);
-    uint8_t* rows_s = work + so;                               // TMA-staged W_down rows
-    const int row_bytes = Dp * 2;
-    const int n_slots = (kDecWork - so) / row_bytes;
-    int gb = 0;                                                    // batches issued so far (phase)
-    __shared__ SelScratch sel_sc;
-    int* p2 = misc + 8;  // 0 row, 1 e, 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount, 9 total, 10 slot
-    bool route_ready = false;
-    const int LPR = Dp >> 3;
-    const int NT = ceil_div(LPR, 256);
-    const int G = NT == 1 ? (256 / LPR > 0 ? 256 / LPR : 1) : 1;
-    // CTAs that host exact-routing chains (the last ones) take units only when the others
-    // cannot hold them all in one wave: their P2 would start after the chains
-    const int n_chain_ctas = min(n_eb * n_tb, grid);
-    const int gp = (n_units <= grid - n_chain_ctas) ? grid - n_chain_ctas : grid;
-    const int v0 = bid < gp ? static_cast<int>(static_cast<long long>(bid) * n_units / gp) : 0;
-    const int v1 = bid < gp ? static_cast<int>(static_cast<long long>(bid + 1) * n_units / gp) : 0;
-
-    int e = 0, n = 0, kpt = 0, cnt = 0, t = 0, q = 0;
-    bool routed = true;
-
-    // A CTA's units are consecutive: they form RUNS of chunks [c_a, c_b) of one row.  A run
-    // selects once and streams its rows through the gather ring without draining it between
-    // chunks; every chunk still produces its own partial, so the reduction tree is the same
-    // whatever the batch (and the run boundaries) -- only the latency of a chunk is paid once
-    // per run instead of once per chunk.
-#pragma unroll 1
-    for (int v = v0; v < v1;) {
-      const int pr = v / CH;
-      const int c_a = v % CH;
-      const int vb = min(v1, (pr + 1) * CH);
-      const int c_b = c_a + (vb - v);
-      v = vb;
-      {
-        t = 0;
-        while (t + 1 < B && pairoff[t + 1] <= pr) ++t;
-        q = pr - pairoff[t];
-        routed = q < ncand[t];
-        if (tid == 0) {
-          int ee, rr, slot = -1;
-          if (routed) {
-            ee = cande[t * CM + q];
-            rr = t * CM + q;
-            if (a.sel_mode == kSelectGiven) {
-              // caller masks are indexed by slot: the exact routing is needed here
-              if (!route_ready) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
-              for (int j = 0; j < K; ++j)
-                if (__ldcg(a.ids + t * K + j) == ee) slot = t * K + j;
-            }
-          } else {
-            ee = E;
-            rr = kDecTokens * CM + t;
-            slot = t;
-          }
-          p2[0] = rr;
-          p2[1] = ee;
-          p2[8] = 0;
-          p2[10] = slot;
-        }
-        route_ready = true;
-        __syncthreads();
-        DEC_T(8);
-        DEC_G(18);
-        const int row = p2[0];
-        e = p2[1];
-        const int slot = p2[10];
-        n = routed ? a.N : a.S;
+      for (int v = bid; v < n_units; v += grid) {
+        const int pu = plist[v / CH], c = v % CH;
+        const int u = pu >> 4, t = pu & 15;
+        const bool routed = u < n_u;
+        const int row = routed ? rowtab[pu] : kDecTokens * CM + t;
+        const int e = routed ? ulist[u] : E;
+        const int q = routed ? row - t * CM : CM;
+        const int n = routed ? a.N : a.S;
         int mode = a.sel_mode;
         const uint8_t* min_ = nullptr;
         if (mode == kSelectGiven) {
+          int slot = t;
           if (routed) {
+            // caller masks are indexed by slot: the exact routing is needed here
+            if (!route_ready) {
+              if (dtid == 0) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+              d_sync();
+              route_ready = true;
+            }
+            slot = -1;
+            for (int j = 0; j < K; ++j)
+              if (__ldcg(a.ids + t * K + j) == e) slot = t * K + j;
             min_ = slot >= 0 ? a.mask_r + static_cast<size_t>(slot) * n : nullptr;
             if (slot < 0) mode = -1;  // a candidate the exact routing rejected: nothing to do
           } else {
@@ -824,297 +901,182 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           n_off = routed ? a.n_off_r : a.n_off_s;
           if (n_off <= 0) mode = kSelectAll;
         }
-        kpt = ceil_div(n, kDecThreads);
-        const uint2* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
-        const bool want_hist = mode == kSelectTopk && n_off < n;
-        hist_s[2 * tid] = 0;
-        hist_s[2 * tid + 1] = 0;
-        __syncthreads();
-        // every element is read until it carries this launch's epoch (usually at once: the
-        // loads of a thread are issued back to back, four in flight)
-#pragma unroll 1
-        for (int i0 = tid; i0 < n; i0 += 4 * kDecThreads) {
-          uint2 v4[4];
-#pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int i = i0 + u4 * kDecThreads;
-            v4[u4] = i < n ? ld_volatile_u2(hrow + i) : make_uint2(0u, epoch);
-          }
-#pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int i = i0 + u4 * kDecThreads;
-            if (i < n) {
-              while (v4[u4].y != epoch) v4[u4] = ld_volatile_u2(hrow + i);
-              keys_s[i] = v4[u4].x;
-              if (want_hist) atomicAdd(&hist_s[hist_bin(v4[u4].x & 0x7fffffffu)], 1);
-            }
+        const int n0 = static_cast<int>(static_cast<long long>(c) * n / CH);
+        const int n1 = static_cast<int>(static_cast<long long>(c + 1) * n / CH);
+        const bool want_pick = mode == kSelectTopk && n_off < n;
+        const float* hrow = a.hc + static_cast<size_t>(row) * a.Nh;
+
+        // wait until every gate/up piece of this expert has landed (one polite poller)
+        if (dtid == 0) {
+          p2[8] = 0;
+          spin_until(&a.ctr[kCtrCnt + (routed ? 1 + u : 0)], static_cast<unsigned>(routed ? PE : n_sh));
+        }
+        hist_s[2 * dtid] = 0;
+        hist_s[2 * dtid + 1] = 0;
+        d_sync();
+        DEC_STAMP(kWarpD0 * 32, 8);
+        // the row's activations: everything in top-k mode, the chunk otherwise
+        {
+          const int i_lo = want_pick ? 0 : n0, i_hi = want_pick ? n : n1;
+#pragma unroll 4
+          for (int i = i_lo + dtid; i < i_hi; i += kDThreads) {
+            const uint32_t k = __float_as_uint(__ldcg(hrow + i));
+            keys_s[i] = k;
+            if (want_pick) atomicAdd(&hist_s[hist_bin(k & 0x7fffffffu)], 1);
           }
         }
-        __syncthreads();
-        const uint2 hh = want_hist ? make_uint2(static_cast<unsigned>(hist_s[2 * tid]),
-                                                static_cast<unsigned>(hist_s[2 * tid + 1]))
-                                   : make_uint2(0u, 0u);
+        d_sync();
 
         RowPick pk{0u, 0, true};
-        if (mode == kSelectAll) {
-          cnt = n;
-        } else if (mode == kSelectGiven) {
-          cnt = 0;  // counted by the prefix below
-        } else if (mode < 0) {
-          cnt = 0;
-        } else {
-          cnt = n_off >= n ? 0 : n - n_off;
-          if (cnt > 0) {
-            // ---- pivot bucket from the row's histogram ----
-            int incl = static_cast<int>(hh.x + hh.y);
+        if (want_pick) {
+          // ---- pivot bucket from the row's histogram ----
+          const uint2 hh = make_uint2(static_cast<unsigned>(hist_s[2 * dtid]),
+                                      static_cast<unsigned>(hist_s[2 * dtid + 1]));
+          int incl = static_cast<int>(hh.x + hh.y);
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int up = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl += up;
-            }
-            if (lane == 31) wc[warp] = incl;
-            for (int i = tid; i < kMemberCap + 4; i += kDecThreads) mlist[i] = 0xffffffffu;
-            __syncthreads();
-            int base = 0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w)
-              if (w < warp) base += wc[w];
-            incl += base;
-            const int excl = incl - static_cast<int>(hh.x + hh.y);
-            if (excl < n_off && n_off <= incl) {
-              const bool first = n_off <= excl + static_cast<int>(hh.x);
-              p2[2] = 2 * tid + (first ? 0 : 1);
-              p2[3] = first ? excl : excl + static_cast<int>(hh.x);
-              p2[4] = first ? static_cast<int>(hh.x) : static_cast<int>(hh.y);
-            }
-            __syncthreads();
-            const int bstar = p2[2], below_bins = p2[3], M = p2[4];
-            if (M <= kMemberCap) {
-#pragma unroll 1
-              for (int i = tid; i < n; i += kDecThreads) {
-                const uint32_t k = keys_s[i] & 0x7fffffffu;
-                if (hist_bin(k) == bstar) mlist[atomicAdd(&p2[8], 1)] = k;
-              }
-              __syncthreads();
-              const int rr = n_off - below_bins;  // 1-based rank inside the bucket
-              const int M4 = (M + 3) >> 2;
-              // one member per thread (the bucket rarely holds more than a few dozen keys)
-#pragma unroll 1
-              for (int mi = tid; mi < M; mi += kDecThreads) {
-                const uint32_t k = mlist[mi];
-                int lt = 0, le = 0;
-#pragma unroll 1
-                for (int q4 = 0; q4 < M4; ++q4) {
-                  const uint4 mm = *reinterpret_cast<const uint4*>(mlist + 4 * q4);
-                  lt += (mm.x < k) + (mm.y < k) + (mm.z < k) + (mm.w < k);
-                  le += (mm.x <= k) + (mm.y <= k) + (mm.z <= k) + (mm.w <= k);
-                }
-                if (lt < rr && rr <= le) {
-                  p2[5] = static_cast<int>(k);
-                  p2[6] = below_bins + lt;
-                  p2[7] = le - lt;
-                }
-              }
-              __syncthreads();
-              pk.pivot = static_cast<uint32_t>(p2[5]);
-              pk.ties_to_drop = n_off - p2[6];
-              pk.drop_all_ties = (pk.ties_to_drop == p2[7]);
-            } else {
-              // huge bucket (many equal / clamped values): the general search
-#pragma unroll 1
-              for (int i = tid; i < n; i += kDecThreads) keys_s[i] &= 0x7fffffffu;
-              __syncthreads();
-              pk = sel_kary_pick(keys_s, n, n_off, sel_sc);
-              __syncthreads();
-#pragma unroll 1
-              for (int i = tid; i < n; i += kDecThreads) keys_s[i] = ld_volatile_u2(hrow + i).x;
-            }
+          for (int o = 1; o < 32; o <<= 1) {
+            const int up = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += up;
           }
-        }
-        __syncthreads();
-        DEC_T(9);
-
-        // ---- keep flags kf[i] and their exclusive prefix in index order (wc[jj * 8 + warp]) ----
-        if (cnt > 0 || mode == kSelectGiven) {
-          const bool need_ties = (mode == kSelectTopk) && !pk.drop_all_ties;
-#pragma unroll 1
-          for (int pass = need_ties ? 0 : 1; pass < 2; ++pass) {
-            // pass 0: prefix over tie flags (only when some but not all ties are dropped);
-            // pass 1: prefix over keep flags
-#pragma unroll 1
-            for (int jj = 0; jj < kpt; ++jj) {
-              const int i = jj * kDecThreads + tid;
-              const bool valid = i < n;
-              const uint32_t k = valid ? (keys_s[i] & 0x7fffffffu) : 0u;
-              bool f;
-              if (pass == 0) {
-                f = valid && k == pk.pivot;
-              } else if (mode == kSelectAll) {
-                f = valid;
-              } else if (mode == kSelectGiven) {
-                f = valid && min_[i] != 0;
-              } else if (pk.drop_all_ties) {
-                f = valid && k > pk.pivot;
-              } else {
-                f = valid && (k > pk.pivot || (k == pk.pivot && kf[i] != 0));
-              }
-              const unsigned bal = __ballot_sync(0xffffffffu, f);
-              if (lane == 0) wc[jj * 8 + warp] = __popc(bal);
-              if (pass == 1 && valid) kf[i] = f ? 1 : 0;
-            }
-            __syncthreads();
-            {
-              // exclusive scan of wc[0 .. kpt*8) in (jj, warp) order: one entry per thread
-              const int ne = kpt * 8;
-              const int val = tid < ne ? wc[tid] : 0;
-              int incl = val;
+          if (lane == 31) wc[dwarp] = incl;
+          for (int i = dtid; i < kMemberCap + 4; i += kDThreads) mlist[i] = 0xffffffffu;
+          d_sync();
+          int base = 0;
 #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int up = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += up;
-              }
-              if (lane == 31) wc[kMaxKpt * 8 + warp] = incl;
-              __syncthreads();
-              int base = 0;
-#pragma unroll
-              for (int w = 0; w < 8; ++w)
-                if (w < warp) base += wc[kMaxKpt * 8 + w];
-              if (tid < ne) wc[tid] = base + incl - val;
-              if (tid == kDecThreads - 1) p2[9] = base + incl;  // total
-              __syncthreads();
-            }
-            if (pass == 0) {
-              // a tie survives when its rank among the ties (ascending index) >= ties_to_drop
-#pragma unroll 1
-              for (int jj = 0; jj < kpt; ++jj) {
-                const int i = jj * kDecThreads + tid;
-                const bool f = i < n && (keys_s[i] & 0x7fffffffu) == pk.pivot;
-                const unsigned bal = __ballot_sync(0xffffffffu, f);
-                const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
-                if (f) kf[i] = rank >= pk.ties_to_drop ? 1 : 0;
-              }
-              __syncthreads();
-            } else if (mode == kSelectGiven) {
-              cnt = p2[9];
-            }
+          for (int w = 0; w < 8; ++w)
+            if (w < dwarp) base += wc[w];
+          incl += base;
+          const int excl = incl - static_cast<int>(hh.x + hh.y);
+          if (excl < n_off && n_off <= incl) {
+            const bool first = n_off <= excl + static_cast<int>(hh.x);
+            p2[2] = 2 * dtid + (first ? 0 : 1);
+            p2[3] = first ? excl : excl + static_cast<int>(hh.x);
+            p2[4] = first ? static_cast<int>(hh.x) : static_cast<int>(hh.y);
           }
-        }
-      }
-      DEC_T(11);
-
-      // ---- survivors of the run's chunks, ascending index: ranks [c_a * C, min(cnt, c_b * C)) ----
-      const int C = ceil_div(cnt > 0 ? cnt : 1, CH);
-      const int lo = c_a * C;
-      const int hi_ = min(cnt, c_b * C);
-      const int m = hi_ > lo ? hi_ - lo : 0;
-      if (m > 0) {
+          d_sync();
+          const int bstar = p2[2], below_bins = p2[3], M = p2[4];
+          if (M <= kMemberCap) {
 #pragma unroll 1
-        for (int jj = 0; jj < kpt; ++jj) {
-          const int i = jj * kDecThreads + tid;
-          const bool f = i < n && kf[i] != 0;
-          const unsigned bal = __ballot_sync(0xffffffffu, f);
-          const int rank = wc[jj * 8 + warp] + __popc(bal & ((1u << lane) - 1u));
-          if (f && rank >= lo && rank < hi_) lst_idx[rank - lo] = static_cast<uint16_t>(i);
-        }
-      }
-      __syncthreads();
-      DEC_T(12);
-
-      // ---- gather: one 1-D bulk copy (TMA engine) per surviving W_down row into a ring of
-      // kGBatches batches of H rows (one mbarrier each) in shared memory, accumulated from there.
-      // Batches never straddle a chunk; the ring runs ahead across the chunks of the run.
-      // (Measured alternatives for a 32-row chunk: 32 direct 128-bit loads per thread, all in
-      // flight: 7.7 us; two-batch ring: 7.3 us; this ring: 6.9 us.  16-byte cp.async by all
-      // threads instead of bulk copies for 2 KB rows: 106 vs 96 us at Granite shape, batch 16.)
-      const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
-      const int H = max(1, min(C, n_slots / kGBatches));
-      const int nb_c = ceil_div(C, H);                 // batches of a full chunk
-      const int n_ch = ceil_div(m, C);                 // chunks of the run that have rows
-      const int Q = n_ch > 0 ? (n_ch - 1) * nb_c + ceil_div(m - (n_ch - 1) * C, H) : 0;
-      auto batch_rows = [&](int qq, int& p0, int& p1) {
-        const int j = min(qq / nb_c, n_ch - 1);
-        const int b = qq - j * nb_c;
-        p0 = j * C + b * H;
-        p1 = min(min(m, (j + 1) * C), p0 + H);
-      };
-      auto issue = [&](int qq) {
-        const int pos = (gb + qq) % kGBatches;
-        int p0, p1;
-        batch_rows(qq, p0, p1);
-        if (tid == 0) mbar_arrive_expect_tx(gbar(pos), static_cast<uint32_t>((p1 - p0) * row_bytes));
-        // convergent issue: lane l of warp w copies row p0 + w + 8 * l
-        for (int p = p0 + warp + 8 * lane; p < p1; p += kDecThreads)
-          bulk_copy_g2s(smem_u32(rows_s + static_cast<size_t>(pos * H + (p - p0)) * row_bytes),
-                        wb + static_cast<size_t>(lst_idx[p]) * Dp, static_cast<uint32_t>(row_bytes),
-                        gbar(pos));
-        __syncwarp();
-      };
-      const int g = NT == 1 ? tid / LPR : 0, l = NT == 1 ? tid % LPR : tid;
-      const bool lane_ok = g < G;
-      for (int qq = 0; qq < Q && qq < kGBatches; ++qq) issue(qq);
-      int qn = 0;  // next batch to consume
+            for (int i = dtid; i < n; i += kDThreads) {
+              const uint32_t k = keys_s[i] & 0x7fffffffu;
+              if (hist_bin(k) == bstar) mlist[atomicAdd(&p2[8], 1)] = k;
+            }
+            d_sync();
+            const int rr = n_off - below_bins;  // 1-based rank inside the bucket
+            const int M4 = (M + 3) >> 2;
+            // one member per thread (the bucket rarely holds more than a few dozen keys)
 #pragma unroll 1
-      for (int j = 0; j < c_b - c_a; ++j) {
-        float acc[4][8];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
-        const int cbase = j * C;  // first row of this chunk in the run's list
-        const int nb_j = j < n_ch ? ceil_div(min(C, m - cbase), H) : 0;
+            for (int mi = dtid; mi < M; mi += kDThreads) {
+              const uint32_t k = mlist[mi];
+              int lt = 0, le = 0;
 #pragma unroll 1
-        for (int b = 0; b < nb_j; ++b, ++qn) {
-          const int pos = (gb + qn) % kGBatches;
-          mbar_wait(gbar(pos), ((gb + qn) / kGBatches) & 1u);
-          int p0, p1;
-          batch_rows(qn, p0, p1);
-          const uint8_t* base = rows_s + static_cast<size_t>(pos * H) * row_bytes;
-          if (NT == 1) {
-            // group g owns the chunk's rows r with r % G == g (ascending); 4 rows are loaded
-            // before their FMAs so that the shared-memory latency is paid once per 4 rows
-            if (lane_ok) {
-              const int r0 = p0 - cbase;
-#pragma unroll 1
-              for (int p = p0 + ((g - r0 % G) + G) % G; p < p1; p += 4 * G) {
-                uint4 v4[4];
-                float hv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  const int pp = p + u * G;
-                  const bool ok = pp < p1;
-                  hv[u] = ok ? __uint_as_float(keys_s[lst_idx[pp]]) : 0.0f;
-                  v4[u] = ok ? *reinterpret_cast<const uint4*>(base + static_cast<size_t>(pp - p0) * row_bytes +
-                                                              static_cast<size_t>(l) * 16)
-                             : make_uint4(0u, 0u, 0u, 0u);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) fma8(v4[u], hv[u], acc[0]);
+              for (int q4 = 0; q4 < M4; ++q4) {
+                const uint4 mm = *reinterpret_cast<const uint4*>(mlist + 4 * q4);
+                lt += (mm.x < k) + (mm.y < k) + (mm.z < k) + (mm.w < k);
+                le += (mm.x <= k) + (mm.y <= k) + (mm.z <= k) + (mm.w <= k);
+              }
+              if (lt < rr && rr <= le) {
+                p2[5] = static_cast<int>(k);
+                p2[6] = below_bins + lt;
+                p2[7] = le - lt;
               }
             }
+            d_sync();
+            pk.pivot = static_cast<uint32_t>(p2[5]);
+            pk.ties_to_drop = n_off - p2[6];
+            pk.drop_all_ties = (pk.ties_to_drop == p2[7]);
           } else {
-#pragma unroll 2
-            for (int p = p0; p < p1; ++p)
-              consume_row<4>(base + static_cast<size_t>(p - p0) * row_bytes,
-                             __uint_as_float(keys_s[lst_idx[p]]), LPR, l, acc);
-          }
-          if (qn + kGBatches < Q) {
-            __syncthreads();  // this ring position is free again
-            issue(qn + kGBatches);
+            // huge bucket (many equal / clamped values): the general search; keys_s is masked in
+            // place and restored afterwards
+#pragma unroll 1
+            for (int i = dtid; i < n; i += kDThreads) keys_s[i] &= 0x7fffffffu;
+            d_sync();
+            pk = sel_kary_pick<SelDRole>(keys_s, n, n_off, sel_sc);
+            d_sync();
+#pragma unroll 1
+            for (int i = dtid; i < n; i += kDThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
+            d_sync();
           }
         }
-        // ---- this chunk's partial ----
-        float* pout =
-            a.part + (static_cast<size_t>(t * (CM + 1) + (routed ? q : CM)) * CH + (c_a + j)) * Dp;
+        DEC_STAMP(kWarpD0 * 32, 9);
+
+        // ---- survivors of the chunk [n0, n1), ascending index -> lst[0..m) ----
+        int m = 0;
+        if (mode >= 0 && !(mode == kSelectTopk && n_off >= n)) {
+          // rank of a pivot tie = number of ties at lower indices (ties_to_drop of them go first)
+          int tie_base = 0;
+          const bool need_ties = want_pick && !pk.drop_all_ties;
+          if (need_ties) {
+            int cnt = 0;
+#pragma unroll 1
+            for (int i = dtid; i < n0; i += kDThreads) cnt += ((keys_s[i] & 0x7fffffffu) == pk.pivot) ? 1 : 0;
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (lane == 0) wc[8 + dwarp] = cnt;
+            d_sync();
+#pragma unroll
+            for (int w = 0; w < 8; ++w) tie_base += wc[8 + w];
+            d_sync();  // wc[8..16) is rewritten by the first block below
+          }
+          int run = 0;  // survivors before the current 256-index block
+#pragma unroll 1
+          for (int i0 = n0; i0 < n1; i0 += kDThreads) {
+            const int i = i0 + dtid;
+            const bool valid = i < n1;
+            const uint32_t k = valid ? (keys_s[i] & 0x7fffffffu) : 0u;
+            const bool tie = need_ties && valid && k == pk.pivot;
+            const unsigned tb = __ballot_sync(0xffffffffu, tie);
+            bool f;
+            if (mode == kSelectAll) {
+              f = valid;
+            } else if (mode == kSelectGiven) {
+              f = valid && min_[i] != 0;
+            } else {
+              f = valid && k > pk.pivot;
+            }
+            if (need_ties) {
+              if (lane == 0) wc[8 + dwarp] = __popc(tb);
+              d_sync();
+              int tb_before = tie_base;
+#pragma unroll
+              for (int w = 0; w < 8; ++w) {
+                const int cw = wc[8 + w];
+                if (w < dwarp) tb_before += cw;
+                tie_base += cw;
+              }
+              if (tie) f = tb_before + __popc(tb & ((1u << lane) - 1u)) >= pk.ties_to_drop;
+            }
+            const unsigned fb = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) wc[dwarp] = __popc(fb);
+            d_sync();
+            int before = run;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              const int cw = wc[w];
+              if (w < dwarp) before += cw;
+              run += cw;
+            }
+            if (f) lst[before + __popc(fb & ((1u << lane) - 1u))] = static_cast<uint16_t>(i);
+            d_sync();  // wc is rewritten by the next block
+          }
+          m = run;
+        }
+        d_sync();
+        DEC_STAMP(kWarpD0 * 32, 12);
+
+        // ---- gather + partial ----
+        const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
+        float* pout = a.part + (static_cast<size_t>(t * (CM + 1) + q) * CH + c) * Dp;
         if (NT == 1) {
+          float acc[1][8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
+          if (lane_ok) gather_rows<1>(wb, Dp, LPR, lst, m, keys_s, G, g, l, acc);
           if (G > 1) {
-            __syncthreads();  // gred of the previous chunk has been read
             if (lane_ok) {
               float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
               d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
               d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
             }
-            __syncthreads();
-            for (int d = tid; d < Dp; d += kDecThreads) {
+            d_sync();
+            for (int d = dtid; d < Dp; d += kDThreads) {
               float sacc = gred[d];
               for (int gg = 1; gg < G; ++gg) sacc = __fadd_rn(sacc, gred[gg * Dp + d]);
               pout[d] = sacc;
@@ -1124,10 +1086,32 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
             d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
           }
+        } else if (NT == 2) {
+          float acc[2][8];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
+          gather_rows<2>(wb, Dp, LPR, lst, m, keys_s, 1, 0, l, acc);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int c8 = nt * 256 + dtid;
+            if (c8 < LPR) {
+              float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
+              d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
+              d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+            }
+          }
         } else {
+          float acc[4][8];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
+          gather_rows<4>(wb, Dp, LPR, lst, m, keys_s, 1, 0, l, acc);
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
-            const int c8 = nt * 256 + tid;
+            const int c8 = nt * 256 + dtid;
             if (c8 < LPR) {
               float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
               d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
@@ -1135,34 +1119,42 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
             }
           }
         }
+        DEC_STAMP(kWarpD0 * 32, 13);
+        d_sync();  // the unit's scratch is reused by the next one
       }
-      gb += Q;
-      DEC_T(13);
-      __syncthreads();  // scratch is reused by the next run
     }
+    __threadfence();
+    d_sync();
+    if (dtid == 0) atomicAdd(&a.ctr[kCtrDone], 1u);
+    DEC_STAMP(kWarpD0 * 32, 5);
   }
-  DEC_T(5);
+
+  // every role of this CTA is through: TMEM goes back, the ring becomes P3 scratch
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 32);
+  }
+  if (warp < kWarpD0) return;
 
   // =====================================================================================
-  // P3: grid barrier (partials + exact routing), then the ordered combine.  Each CTA owns a
-  // contiguous range of (token, 4 columns) outputs: all partials of a batch of 8 outputs are
+  // P3 (D role): grid barrier (partials + exact routing), then the ordered combine.  Each CTA owns
+  // a contiguous range of (token, 4 columns) outputs: all partials of a batch of 8 outputs are
   // fetched at once into shared memory, summed per slot over the chunks (ascending), then over
   // the slots (ascending, shared expert last with weight 1: router.cpp:109-132,
   // engine.cpp:168-173).
   // =====================================================================================
-  __syncthreads();
-  int* srow = reinterpret_cast<int*>(work);          // [B][R] candidate rank of every slot
-  float* swt = reinterpret_cast<float*>(work + 2048);  // [B][R] combine weights
   {
+    const int dtid = tid - kWarpD0 * 32;
+    uint8_t* work = sm + L.ring;
+    int* srow = reinterpret_cast<int*>(work);            // [B][R] candidate rank of every slot
+    float* swt = reinterpret_cast<float*>(work + 2048);  // [B][R] combine weights
     const int R = K + (a.has_shared ? 1 : 0);
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&a.ctr[kCtrP2], 1u);
-      spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
-    }
-    __syncthreads();
+    if (dtid == 0) spin_until(&a.ctr[kCtrRoute], static_cast<unsigned>(n_tb));
+    d_sync();
     // slot tables (the exact routing is known now); overlaps the wait for the other CTAs
-    for (int i = tid; i < B * R; i += kDecThreads) {
+    for (int i = dtid; i < B * R; i += kDThreads) {
       const int t = i / R, j = i % R;
       if (j < K) {
         const int ee = __ldcg(a.ids + t * K + j);
@@ -1173,18 +1165,22 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         swt[i] = 1.0f;
       }
     }
-    if (tid == 0) {
-      while (ld_acquire_u32(&a.ctr[kCtrP2]) - p2_base < static_cast<unsigned>(grid)) {
-      }
-      if (bid == 0) {
-        // every CTA is past its last read of these: back to rest for the next forward
-        a.ctr[kCtrP0] = 0u;
+    if (dtid == 0) {
+      spin_until(&a.ctr[kCtrDone], static_cast<unsigned>(grid));
+      // every CTA that gets here has read all the counters for the last time: the last one
+      // through puts them back to rest and opens the next epoch
+      if (atomicAdd(&a.ctr[kCtrExit], 1u) == static_cast<unsigned>(grid - 1)) {
+        const int n_u = misc[2];
+        a.ctr[kCtrDone] = 0u;
+        a.ctr[kCtrExit] = 0u;
         a.ctr[kCtrRoute] = 0u;
         for (int i = 0; i < 4; ++i) a.ctr[kCtrChain + i] = 0u;
+        for (int i = 0; i <= n_u; ++i) a.ctr[kCtrCnt + i] = 0u;
+        a.ctr[kCtrEpoch] = epoch;
       }
     }
-    __syncthreads();
-    DEC_T(6);
+    d_sync();
+    DEC_STAMP(kWarpD0 * 32, 6);
     const int RC = R * CH;
     const int D4 = Dp / 4;
     const int total4 = B * D4;
@@ -1198,7 +1194,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
     for (int qb = q0; qb < q1; qb += QB) {
       const int nq = min(QB, q1 - qb);
 #pragma unroll 2
-      for (int idx = tid; idx < nq * RC; idx += kDecThreads) {
+      for (int idx = dtid; idx < nq * RC; idx += kDThreads) {
         const int qi = idx / RC, rem = idx % RC;
         const int j = rem / CH, c = rem % CH;
         const int qq = qb + qi;
@@ -1207,8 +1203,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         buf[idx] = __ldcg(reinterpret_cast<const float4*>(
             a.part + (static_cast<size_t>(t * (CM + 1) + r) * CH + c) * Dp + d4 * 4));
       }
-      __syncthreads();
-      for (int idx = tid; idx < nq * R; idx += kDecThreads) {
+      d_sync();
+      for (int idx = dtid; idx < nq * R; idx += kDThreads) {
         const float4* pb = buf + static_cast<size_t>(idx) * CH;
         float4 sacc = pb[0];
 #pragma unroll 1
@@ -1221,15 +1217,15 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         }
         sj[idx] = sacc;
       }
-      __syncthreads();
-      if (tid < nq) {
-        const int qq = qb + tid;
+      d_sync();
+      if (dtid < nq) {
+        const int qq = qb + dtid;
         const int t = qq / D4, d4 = qq % D4;
         float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll 1
         for (int j = 0; j < R; ++j) {
           const float w = swt[t * R + j];
-          const float4 sv = sj[tid * R + j];
+          const float4 sv = sj[dtid * R + j];
           acc.x = __fadd_rn(acc.x, __fmul_rn(w, sv.x));
           acc.y = __fadd_rn(acc.y, __fmul_rn(w, sv.y));
           acc.z = __fadd_rn(acc.z, __fmul_rn(w, sv.z));
@@ -1245,7 +1241,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
           if (d4 * 4 + 3 < D) yo[3] = acc.w;
         }
       }
-      __syncthreads();
+      d_sync();
     }
     if (a.capture) {
       // h in slot order for the MaskSet / activation captures of the host API
@@ -1257,10 +1253,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         const int ee = rt ? __ldcg(a.ids + sl) : E;
         const int row = rt ? rowtab[uidx[ee] * 16 + t] : kDecTokens * CM + t;
         const int n = rt ? a.N : a.S;
-        const uint2* src = a.hc + static_cast<size_t>(row) * a.Nh;
+        const float* src = a.hc + static_cast<size_t>(row) * a.Nh;
         float* dst = a.h_cap + static_cast<size_t>(sl) * a.Nh;
-        for (int i = tid; i < n; i += kDecThreads) dst[i] = __uint_as_float(ld_volatile_u2(src + i).x);
-        if (tid == 0) {
+        for (int i = dtid; i < n; i += kDThreads) dst[i] = __ldcg(src + i);
+        if (dtid == 0) {
           a.row_expert[sl] = ee;
           if (rt) {
             a.inv[sl] = sl;
@@ -1269,25 +1265,19 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w,
         }
       }
     }
+    DEC_STAMP(kWarpD0 * 32, 7);
   }
-  DEC_T(7);
-  DEC_G(19);
 }
 
 bool decode_fused_eligible(const Geometry& g, int B) {
   const int nmax = g.N > g.S ? g.N : g.S;
-  if (!(B >= 1 && B <= kDecTokens && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxKpt * kDecThreads &&
-        g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288 &&
-        ceil_div(nmax, 32) <= kMaxChunkRows))
-    return false;
-  // the gather ring needs at least kGBatches W_down rows of shared memory (P2 scratch layout)
-  const int nmax_pad = round_up(nmax, 256);
-  const int so = round_up(2 * nmax_pad + 4352 + 1280 + 8192 + kHistBins * 4 + 5 * nmax_pad, 1024);
-  return (kDecWork - so) / (g.Dp * 2) >= kGBatches;
+  return B >= 1 && B <= kDecTokens && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxN &&
+         g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288 && dec_stages_for(nmax) >= 3;
 }
 
-int decode_counter_words() { return kCtrH + kDecMaxU + 8; }
+int decode_counter_words() { return kCtrWords; }
 int decode_cand_rows(int K) { return K + 4; }
+int decode_p0_words(const Geometry& g) { return 16 * g.E * kMaxND * 2 * 2; }
 int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
   // Batch-invariant by design (B is ignored): one token's units fill the grid once.
   (void)B;
@@ -1298,18 +1288,25 @@ int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
   if (ch > cap) ch = cap;
   if (ch > 32) ch = 32;
   if (ch < 1) ch = 1;
-  while (ch < 32 && ceil_div(keep_max, ch) > kMaxChunkRows) ++ch;  // survivor list capacity
   return ch;
 }
 
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_xb,
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_xb3,
                         const DecodeLaunch& d, const Geometry& g, int n_sms) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kDecSmemBytes);
-    attr_set = true;
+  // the opt-in is per device: set it on every launch path's first use of each device
+  static std::mutex mu;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      cudaFuncSetAttribute(decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemBudget + 1024);
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
   }
+  const int nmax = g.N > g.S ? g.N : g.S;
   DecodeArgs a{};
   a.x = d.x;
   a.router = d.router;
@@ -1335,13 +1332,22 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const C
   a.CM = decode_cand_rows(g.K);
   a.CH = d.CH;
   a.capture = d.capture ? 1 : 0;
+  a.stages = dec_stages_for(nmax);
+  {
+    // fast-logit units: (expert, d_model slice); as many slices as fill the grid once
+    int nd = n_sms / g.E;
+    if (nd < 1) nd = 1;
+    if (nd > kMaxND) nd = kMaxND;
+    const int ds = round_up(ceil_div(g.D, nd), 4);
+    a.ND = ceil_div(g.D, ds);
+    a.DS = ds;
+  }
   a.xb = d.xb;
-  a.lf = d.lf;
-  a.lm = d.lm;
+  a.p0 = reinterpret_cast<uint2*>(d.p0);
   a.logits = d.logits;
   a.ids = d.ids;
   a.wts = d.wts;
-  a.hc = reinterpret_cast<uint2*>(d.hc);
+  a.hc = d.hc;
   a.part = d.part;
   a.ctr = d.ctr;
   a.y = d.y;
@@ -1358,8 +1364,8 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const C
   cfg.stream = ctx.stream;
   cfg.gridDim = dim3(n_sms);
   cfg.blockDim = dim3(kDecThreads);
-  cfg.dynamicSmemBytes = kDecSmemBytes;
-  cudaLaunchKernelEx(&cfg, decode_fused_kernel, *tmap_w, *tmap_xb, a);
+  cfg.dynamicSmemBytes = dec_smem_layout(a.stages, nmax).total + 1024;
+  cudaLaunchKernelEx(&cfg, decode_fused_kernel, *tmap_w3, *tmap_xb3, a);
   return 1;
 }
 

@@ -20,6 +20,13 @@ struct SelScratch {
   int warp_cnt[2][kSelWarps];  // ballot prefix scratch of sel_block_rank (double buffered)
 };
 
+// Who runs a CTA-wide selection: the whole 256-thread CTA (select.cu, down.cu), or the eight
+// down-projection warps of the fused decode kernel behind a named barrier (decode.cu).
+struct SelWholeCta {
+  __device__ static __forceinline__ int tid() { return threadIdx.x; }
+  __device__ static __forceinline__ void sync() { __syncthreads(); }
+};
+
 // What survives in one row: keys > pivot, plus keys == pivot whose rank among the ties (by
 // ascending index) is >= ties_to_drop.
 struct RowPick {
@@ -54,10 +61,11 @@ __device__ __forceinline__ int sel_block_rank(bool flag, SelScratch& sc, int buf
 // shared-memory atomics (a 256-bin atomic histogram costs ~2 cycles per key per pass on the
 // SM's single shared-memory pipe and made the selection the slowest part of decode).
 // For n <= 1024 every warp keeps all keys in registers (32 per lane).
+template <class CTX = SelWholeCta>
 __device__ __forceinline__ RowPick sel_kary_pick(const uint32_t* keys, int n, int n_off,
                                                  SelScratch& sc) {
   static_assert(kSelWarps == 8, "one threshold per warp, 3 bits per step");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = CTX::tid() & 31, warp = CTX::tid() >> 5;
   const bool in_regs = n <= 1024;
   uint32_t kr[32];
   if (in_regs) {
@@ -95,7 +103,7 @@ __device__ __forceinline__ RowPick sel_kary_pick(const uint32_t* keys, int n, in
       c = __reduce_add_sync(0xffffffffu, c);
       if (lane == 0) sc.kcnt[buf][warp] = c;
     }
-    __syncthreads();
+    CTX::sync();
     int d = 0, nb = below;
 #pragma unroll
     for (int q = 0; q < 7; ++q) {

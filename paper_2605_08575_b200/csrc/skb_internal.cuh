@@ -166,12 +166,11 @@ struct DecodeLaunch {
   int CH;                          // row chunks per (token, slot): decode_chunks()
   bool capture;                    // also write h / inv / perm / row_expert in slot order
   __nv_bfloat16* xb;               // [16][Dp] bf16 token rows (TMA source)
-  float* lf;                       // [B][E] fast logits
-  float* lm;                       // [B][E] their error bounds
+  float* p0;                       // decode_p0_words() words: tagged partial fast logits
   float* logits;                   // [B][E] exact logits
   int32_t* ids;                    // [B][K]
   float* wts;                      // [B][K]
-  float* hc;                       // [16 * CM + 16][Nh][2] candidate rows of {h bits, epoch} words
+  float* hc;                       // [16 * CM + 16][Nh] activations of the candidate rows
   float* part;                     // [B][R][CH][Dp]
   unsigned* ctr;                   // decode_counter_words() zeroed words
   float* y;                        // [B][D]
@@ -183,8 +182,11 @@ struct DecodeLaunch {
 bool decode_fused_eligible(const Geometry& g, int B);
 int decode_counter_words();
 int decode_cand_rows(int K);
+int decode_p0_words(const Geometry& g);
 int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms);
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_xb,
+// tmap_w3: the gate/up image as {64 columns, 128 rows, tiles}, box {64, 32, 4}; tmap_xb3: the bf16
+// token rows as {64 columns, 16 rows, K blocks}, box {64, 16, 4}
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_xb3,
                         const DecodeLaunch& d, const Geometry& g, int n_sms);
 
 // weight image construction
