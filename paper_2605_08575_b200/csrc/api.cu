@@ -71,9 +71,10 @@ int encode_bf16_2d(CUtensorMap* map, void* base, uint64_t rows, uint64_t cols, u
 }
 
 // 3-D view for the fused decode kernel: {64 bf16 columns, rows, planes}, row and plane strides in
-// bytes, box = {64, box_rows, box_planes}, 128-byte swizzle.
+// bytes, box = {64, box_rows, box_planes}; 128-byte swizzle, or none (plain 128-byte rows for
+// consumers that read the stage with ordinary shared-memory loads).
 int encode_bf16_3d(CUtensorMap* map, void* base, uint64_t rows, uint64_t planes, uint64_t row_stride,
-                   uint64_t plane_stride, uint32_t box_rows, uint32_t box_planes) {
+                   uint64_t plane_stride, uint32_t box_rows, uint32_t box_planes, bool swizzle = true) {
   int rc = load_encode();
   if (rc) return rc;
   cuuint64_t gdim[3] = {static_cast<cuuint64_t>(kBlockK), rows, planes};
@@ -81,7 +82,8 @@ int encode_bf16_3d(CUtensorMap* map, void* base, uint64_t rows, uint64_t planes,
   cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), box_rows, box_planes};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, gdim, gstride, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SKB_ECUDA, "cuTensorMapEncodeTiled (3-D) failed with CUresult %d", (int)r);
   return SKB_OK;
@@ -137,7 +139,6 @@ struct skb_layer {
   CUtensorMap tmap_x[5]{};
   __nv_bfloat16* d_xb = nullptr;  // decode: bf16 token rows [max(cap,16)][Dp] (token-indexed tiles)
   CUtensorMap tmap_xb{};
-  CUtensorMap tmap_xb3{};  // fused decode kernel: {64, 16 tokens, K blocks}
   float* d_h = nullptr;
   float* d_sg = nullptr;  // silu(gate) of every row (threshold selection, forward_sparse)
   __nv_bfloat16* d_hb = nullptr;  // masked activations, [3][rows][Nh] bf16 terms
@@ -247,8 +248,6 @@ int reserve_locked(skb_layer* L, int B) {
     SKB_TRY(dmalloc(&L->d_xb, xb_rows * g.Dp));
     SKB_CUDA(cudaMemsetAsync(L->d_xb, 0, xb_rows * g.Dp * sizeof(__nv_bfloat16), L->stream));
     SKB_TRY(encode_bf16_2d(&L->tmap_xb, L->d_xb, xb_rows, g.Dp, 16));
-    SKB_TRY(encode_bf16_3d(&L->tmap_xb3, L->d_xb, 16, g.Dp / kBlockK,
-                           static_cast<uint64_t>(g.Dp) * 2, kBlockK * 2, 16, 4));
   }
   {
     const size_t n_counters = 2 + static_cast<size_t>(cap);
@@ -385,7 +384,7 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
   rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows * (g.Dp / kBlockK), kBlockK, 128);
   if (!rc)  // the same image as planes of 128 x 64 tiles: a box is 32 rows of 4 consecutive tiles
     rc = encode_bf16_3d(&L->tmap_w3, L->d_wgu, 128, gu_rows / 128 * (g.Dp / kBlockK), kBlockK * 2,
-                        128 * kBlockK * 2, 32, 4);
+                        128 * kBlockK * 2, 32, 4, /*swizzle=*/false);
   if (!rc)
     rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt,
                         static_cast<uint64_t>(g.E) * g.Dp128 * (g.Np / kBlockK), kBlockK, 128);
@@ -536,7 +535,6 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dl.mask_s = d_mask_s;
     dl.CH = decode_chunks(g, B, max_keep, L->n_sms);
     dl.capture = capture_h || want_masks;
-    dl.xb = L->d_xb;
     dl.p0 = L->d_dec_p0;
     dl.logits = L->d_logits;
     dl.ids = L->d_ids;
@@ -552,7 +550,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     tm.mark();
     tm.mark();
     tm.mark();
-    launches += launch_decode_fused(ctx, &L->tmap_w3, &L->tmap_xb3, dl, g, L->n_sms);
+    launches += launch_decode_fused(ctx, &L->tmap_w3, dl, g, L->n_sms);
     tm.mark();
     if (want_masks) {
       SelectArgs sa{};

@@ -1,23 +1,25 @@
-// decode.cu -- the whole layer for decode batches (B <= 16) as ONE persistent launch, software
+// decode.cu -- the whole layer for decode batches (B <= 8) as ONE persistent launch, software
 // pipelined: the down projection of an expert runs while the gate/up weights of the next
 // experts are still streaming.
 //
 // Why one kernel: at decode sizes the layer moves ~10-100 MB, i.e. 10-20 us of HBM time; every
 // kernel boundary costs 2-3 us of drain + launch + refill, and a cold burst out of HBM ramps for
-// ~3 us before it reaches full rate (tools/micro/burst.cu: 64 MB in 14 us, 16 MB in 5.5 us).  So
-// the stages of the reference path (proj/src/engine.cpp:94-191) are ROLES of one grid of numSMs
-// CTAs (one per SM, all co-resident), each role on its own warps, chained through global memory:
+// ~3 us before it reaches full rate (tools/micro/burst.cu: 64 MB in 14 us, 16 MB in 5.5 us, by
+// every access method).  So the stages of the reference path (proj/src/engine.cpp:94-191) are
+// ROLES of one grid of numSMs CTAs (one per SM, all co-resident), each role on its own warps,
+// chained through global memory:
 //
-//   warps 4-11 "D role" (256 threads)
+//   warps 6-13 "D role" (256 threads)
 //     P0  fast router logits, split over (expert, d_model slice) units on all CTAs: partial
 //         lf = x.router and A = sum |x.router| per slice, published as {bits, epoch} words that the
-//         readers poll -- no grid barrier.  The reference's logit (ascending-index float
-//         accumulation, proj/src/linalg.cpp:22-40) differs from lf by at most m = 2*gamma_D*A
-//         (gamma_D = D*u/(1-D*u), u = 2^-24).  Every expert whose interval [lf-m, lf+m] reaches
-//         the K-th largest lower end is a CANDIDATE of the token; the reference's top-K set is
-//         provably a subset.  Typically K candidates, sometimes K+1.  (More than K+4, non-finite
-//         values, or a threshold more than 60 below the maximum -- the exp underflow region where
-//         probabilities tie -- and the CTA waits for the exact routing instead.)
+//         readers poll (all words of a CTA in flight at once) -- no grid barrier.  The reference's
+//         logit (ascending-index float accumulation, proj/src/linalg.cpp:22-40) differs from lf
+//         by at most m = 2*gamma_D*A (gamma_D = D*u/(1-D*u), u = 2^-24).  Every expert whose
+//         interval [lf-m, lf+m] reaches the K-th largest lower end is a CANDIDATE of the token;
+//         the reference's top-K set is provably a subset.  Typically K candidates, sometimes K+1.
+//         (More than K+4, non-finite values, or a threshold more than 60 below the maximum -- the
+//         exp underflow region where probabilities tie -- and the CTA waits for the exact routing
+//         instead.)
 //     P2  neuron selection + down projection.  Work unit = (token, candidate, neuron-index
 //         chunk), dealt round-robin in the order the experts finish.  The unit waits (one polite
 //         poller) for its expert's piece counter, loads the h row, finds the pivot bucket from a
@@ -28,21 +30,26 @@
 //         bytes.
 //     P3  combine: y[t] = sum_s w(t,s) * (sum_chunks partial), slots ascending, shared expert
 //         last with weight 1 (proj/src/router.cpp:109-132, engine.cpp:168-173), fixed order.
-//   warps 1, 2, 0 "G role": TMA producer, tcgen05.mma issuer, epilogue
+//   warp 0 + warps 2-5 "G role": TMA producer, four consumer warps
 //     gate/up + SwiGLU for the shared expert (streams from the first microsecond: it does not
 //     depend on the routing) and then for the union of candidate experts, in EXPERT-MAJOR order
 //     over all CTAs: a piece = 16 neurons (their 16 gate + 16 up rows) x all of d_model, read as
-//     one 3-D TMA box {64 columns, 32 rows, 4 K-blocks} per ring stage out of the 128-row tiled
-//     image.  The MMA is the 128x16x16 instruction on a tile whose rows 32..127 are whatever
-//     follows in shared memory (their accumulator lanes are never read).  Expert u is complete
-//     -- and its down projection starts -- after 1/n_u of the stream, not at its end.
-//   warp 3 "CH role": exact routing.  The order-faithful logit chains (the D dependent float
+//     one 3-D TMA box {64 columns, 32 rows, 4 K-blocks} (16 KB) per ring stage out of the
+//     128-row tiled image.  With at most 8 tokens the contraction is a GEMV: a tensor-core tile
+//     would be 1/16 full and its operand staging (token tile TMA, UMMA issue, TMEM round trip)
+//     only adds latency to a stream whose cost is HBM bytes, so the consumers are plain fp32 FMAs
+//     straight out of the ring -- consumer warp w owns K-block w of every stage, lane l the
+//     16-byte column piece l%8 of rows l/8 + 4i; the tokens sit in shared memory as bf16.  (The
+//     batch kernels, gateup.cu, are the tcgen05 path.)  Expert u is complete -- and its down
+//     projection starts -- after 1/n_u of the stream, not at its end.
+//   warp 1 "CH role": exact routing.  The order-faithful logit chains (the D dependent float
 //     adds of the reference) run on the last CTAs from the first microsecond; the last chain of
 //     a token block runs route() (proj/src/router.cpp:13-68).  Ids, slot order and weights are
 //     the reference's bit for bit; only P3 needs them.
 //
 // No float atomics anywhere: results are deterministic and, for a given shape, a token's result
-// does not depend on the rest of the batch.
+// does not depend on the rest of the batch (the same FMA sequence per token for every batch size).
+#include <cstdlib>
 #include <mutex>
 
 #include "route_device.cuh"
@@ -53,25 +60,29 @@ namespace skb {
 
 namespace {
 
-constexpr int kDecThreads = 384;  // 12 warps
-constexpr int kDThreads = 256;    // the D role: warps 4..11
-constexpr int kWarpEpi = 0, kWarpTma = 1, kWarpMma = 2, kWarpChain = 3, kWarpD0 = 4;
-constexpr int kDecTokens = 16;             // MMA N
-constexpr int kKBox = 4;                   // K blocks per ring stage
-constexpr int kStageA = kKBox * 32 * 128;  // 16 KB: 32 rows x 64 bf16 per K block
-constexpr int kStageB = kKBox * kDecTokens * 128;  // 8 KB
-constexpr int kStageBytes = kStageA + kStageB;
-constexpr int kMaxStages = 8;
+constexpr int kDecThreads = 448;  // 14 warps
+constexpr int kDThreads = 256;    // the D role: warps 6..13
+constexpr int kWarpTma = 0, kWarpChain = 1, kWarpG0 = 2, kNumGWarps = 4, kWarpD0 = 6;
+constexpr int kGThreads = kNumGWarps * 32;
+constexpr int kDecMaxB = 8;
+constexpr int kDecTokens = 16;             // token stride of the row tables and of hc / part
+constexpr int kKBox = 4;                   // K blocks per ring stage = consumer warps
+constexpr int kStageBytes = kKBox * 32 * 128;  // 16 KB: 32 rows x 64 bf16 per K block
+constexpr int kMaxStages = 12;
+constexpr int kMinStages = 5;  // the exact-chain ring of the chain CTAs lives in the stage ring
 constexpr int kHistBins = 512;
 constexpr int kHistBase = (135 << 3) - (kHistBins - 1);  // top bin = |h| >= 2^8
 constexpr int kMemberCap = 1024;
 constexpr int kMaxN = 8192;  // N, S <= 8192
 
-// exact-chain ring (per CTA): 8 experts + 4 tokens per unit, 128-float sub-chunks
-constexpr int kChEB = 8, kChTB = 4, kChSub = 128, kChStages = 4;
+// exact-chain ring (chain CTAs only, in the stage ring's space): a unit is 8 experts x 4 tokens,
+// 512-float sub-chunks as 1-D bulk copies of 2 KB (the TMA engine spends ~40 ns + 1 ns per 30
+// bytes on a copy: short rows cost more than the chain they feed)
+constexpr int kChSub = 512, kChStages = 3;
 constexpr int kChRow = kChSub + 4;
-constexpr int kChRows = kChEB + kChTB;
-constexpr int kChBytes = kChStages * kChRows * kChRow * 4;  // 25344
+constexpr int kChBytes = kChStages * 12 * kChRow * 4;  // 74304
+static_assert(kChBytes <= kMinStages * kStageBytes, "the chain rings live in the stage ring");
+constexpr int kMaxChainCtas = 16;
 
 constexpr int kDecMaxE = 256;
 constexpr int kDecMaxU = 256;  // union of candidate experts
@@ -84,24 +95,26 @@ enum {
   kCtrExit = 2,
   kCtrRoute = 3,
   kCtrChain = 4,   // [4]
-  kCtrXb = 8,      // [16] uint2 {1, epoch}: bf16 token row t is in place
   kCtrCnt = 40,    // [1 + kDecMaxU] finished gate/up pieces: [0] shared expert, [1 + u] union expert u
   kCtrWords = kCtrCnt + 1 + kDecMaxU + 7
 };
 
 struct DecSmem {
-  int ring, chain, keys, lst, hist, mlist, scr, gred, rowtab, uidx, ulist, cande, cmask, plist, rscr,
-      bars, misc, total;
+  int ring, chain, xs, gpart, keys, lst, hist, mlist, scr, gred, rowtab, uidx, ulist, cande, cmask,
+      plist, rscr, bars, misc, total;
 };
-constexpr int kNumBars = 2 * kMaxStages + 4 + kChStages;
-__host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax) {
+constexpr int kNumBars = 2 * kMaxStages + kChStages;
+__host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax, int tb, int Dp) {
   DecSmem m;
   const int nmax_pad = round_up(nmax, 256);
   int o = 0;
   m.ring = o;
   o += stages * kStageBytes;
-  m.chain = o;  // also the landing zone of the last stage's 128-row operand over-read
-  o += kChBytes;
+  m.chain = m.ring;  // chain CTAs take no gate/up pieces
+  m.xs = o;  // bf16 token rows [tb][Dp]
+  o += round_up(tb * Dp * 2, 128);
+  m.gpart = o;  // [2][4 warps][tb][32] partial gate/up sums of a piece
+  o += 2 * kNumGWarps * tb * 32 * 4;
   m.keys = o;
   o += nmax_pad * 4;
   m.lst = o;
@@ -112,8 +125,8 @@ __host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax) {
   o += (kMemberCap + 8) * 4;
   m.scr = o;
   o += 1024;
-  m.gred = o;
-  o += 8192;
+  m.gred = o;  // gather reduction [G][Dp] floats (8 KB); P0: polled partials [B*E*ND] float2
+  o += 16384;
   m.rowtab = o;
   o += (kDecMaxU + 1) * 16 * 2 + 32;
   m.uidx = o;
@@ -138,12 +151,12 @@ __host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax) {
 // dynamic shared memory: 227 KB minus the kernel's static shared memory (< 1 KB) and the
 // 1 KB alignment slack
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;
-inline int dec_stages_for(int nmax) {
-  const DecSmem z = dec_smem_layout(0, nmax);
+inline int dec_tb_for(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : 8)); }
+inline int dec_stages_for(int nmax, int tb, int Dp) {
+  const DecSmem z = dec_smem_layout(0, nmax, tb, Dp);
   int s = (kSmemBudget - z.total) / kStageBytes;
   return s > kMaxStages ? kMaxStages : s;
 }
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -168,9 +181,6 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
                : "l"(p));
   return v;
 }
-__device__ __forceinline__ void fence_proxy_async_all() {
-  asm volatile("fence.proxy.async;" ::: "memory");
-}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2,
                                             uint32_t bar, uint64_t policy) {
   asm volatile(
@@ -194,18 +204,40 @@ __device__ __forceinline__ void fma8(const uint4& u, float hk, float* a) {
   a[7] = fmaf(__uint_as_float(u.w & 0xffff0000u), hk, a[7]);
 }
 
-// the D role's own barrier (256 threads, id 1); id 2 hands the candidate tables to the G role
+// 8 bf16 -> 8 floats, element order
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16);
+  f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16);
+  f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
+
+// the D role's own barrier (256 threads, id 1); id 2 hands the candidate tables to the G role;
+// id 3 is the consumer warps' barrier
 __device__ __forceinline__ void d_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void g_sync() { asm volatile("bar.sync 3, 128;" ::: "memory"); }
 struct SelDRole {
   __device__ static __forceinline__ int tid() { return threadIdx.x - kWarpD0 * 32; }
   __device__ static __forceinline__ void sync() { d_sync(); }
 };
-constexpr int kTableBarThreads = kDThreads + 3 * 32;
+// (two barriers, so that the producer does not wait for the consumers' token staging)
 __device__ __forceinline__ void tables_arrive() {
-  asm volatile("bar.arrive 2, %0;" ::"n"(kTableBarThreads) : "memory");
+  asm volatile("bar.arrive 2, %0;" ::"n"(kDThreads + 32) : "memory");
+  asm volatile("bar.arrive 4, %0;" ::"n"(kDThreads + kGThreads) : "memory");
 }
-__device__ __forceinline__ void tables_wait() {
-  asm volatile("bar.sync 2, %0;" ::"n"(kTableBarThreads) : "memory");
+__device__ __forceinline__ void tables_wait_producer() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kDThreads + 32) : "memory");
+}
+__device__ __forceinline__ void tables_wait_consumers() {
+  asm volatile("bar.sync 4, %0;" ::"n"(kDThreads + kGThreads) : "memory");
+}
+// whole rows of W_down into L2 ahead of the loads that consume them (TMA engine, no registers)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 }  // namespace
@@ -234,8 +266,8 @@ struct DecodeArgs {
   const uint8_t* mask_r;
   const uint8_t* mask_s;
   int CM, CH, capture, stages, ND, DS;
-  __nv_bfloat16* xb;
-  uint2* p0;  // [16][E][ND][2] of {bits, epoch}: partial fast logit and partial sum of |products|
+  int n_ch;  // dedicated chain CTAs (the last n_ch of the grid): no gate/up pieces, no P2 units
+  uint2* p0;  // [B][E][ND][2] of {bits, epoch}: partial fast logit and partial sum of |products|
   float* logits;
   int32_t* ids;
   float* wts;
@@ -259,14 +291,14 @@ __device__ __forceinline__ float ord2f(uint32_t k) {
 }
 
 // Candidate experts of one token (one warp): every expert whose interval [lf - m, lf + m] reaches
-// the K-th largest lower end.  The fast logit of an expert is the sum of its ND slice partials in
-// slice order (every CTA forms the same sums, hence the same candidate sets); the partials are
-// polled until they carry this launch's epoch.  Returns true when the bound cannot be used
-// (non-finite values, the exp-underflow region, or more than CM candidates): the caller then
-// waits for the exact routing.  VPL = experts per lane.
+// the K-th largest lower end.  pf[e] = {fast logit, sum of |products|} of the token (the slice
+// partials summed in slice order -- every CTA forms the same sums, hence the same candidate
+// sets).  Returns true when the bound cannot be used (non-finite values, the exp-underflow
+// region, or more than CM candidates): the caller then waits for the exact routing.
+// VPL = experts per lane.
 template <int VPL>
-__device__ __forceinline__ bool cand_token(const uint2* p0t, int E, int ND, uint32_t epoch, float mfac,
-                                           int K, int CM, int t, uint32_t* cmask) {
+__device__ __forceinline__ bool cand_token(const float2* pf, int stride, int E, float mfac, int K,
+                                           int CM, int t, uint32_t* cmask) {
   const int lane = threadIdx.x & 31;
   uint32_t lo[VPL];
   float hi[VPL];
@@ -276,23 +308,9 @@ __device__ __forceinline__ bool cand_token(const uint2* p0t, int E, int ND, uint
   for (int i = 0; i < VPL; ++i) {
     const int e = i * 32 + lane;
     if (e < E) {
-      float f = 0.0f, sa = 0.0f;
-#pragma unroll 1
-      for (int j = 0; j < ND; ++j) {
-        const uint2* p = p0t + (static_cast<size_t>(e) * ND + j) * 2;
-        uint2 a = ld_volatile_u2(p), b = ld_volatile_u2(p + 1);
-        while (a.y != epoch) {
-          __nanosleep(32);
-          a = ld_volatile_u2(p);
-        }
-        while (b.y != epoch) {
-          __nanosleep(32);
-          b = ld_volatile_u2(p + 1);
-        }
-        f = __fadd_rn(f, __uint_as_float(a.x));
-        sa = __fadd_rn(sa, __uint_as_float(b.x));
-      }
-      const float m = sa * mfac + 2e-5f;
+      const float2 v = pf[static_cast<size_t>(e) * stride];
+      const float f = v.x;
+      const float m = v.y * mfac + 2e-5f;
       lo[i] = f2ord(f - m);
       hi[i] = f + m;
       mxk = max(mxk, f2ord(f));
@@ -366,14 +384,14 @@ __device__ __forceinline__ void gather_rows(const __nv_bfloat16* wb, int Dp, int
   }
 }
 
+template <int TB>
 __global__ void __launch_bounds__(kDecThreads, 1)
-decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
-                    const __grid_constant__ CUtensorMap tmap_xb3, const DecodeArgs a) {
+decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArgs a) {
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   const uint32_t sm_u32 = smem_u32(sm);
   const int nmax = a.N > a.S ? a.N : a.S;
-  const DecSmem L = dec_smem_layout(a.stages, nmax);
+  const DecSmem L = dec_smem_layout(a.stages, nmax, TB, a.Dp);
   int16_t* rowtab = reinterpret_cast<int16_t*>(sm + L.rowtab);
   int16_t* uidx = reinterpret_cast<int16_t*>(sm + L.uidx);
   int16_t* ulist = reinterpret_cast<int16_t*>(sm + L.ulist);
@@ -381,264 +399,330 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
   uint32_t* cmask = reinterpret_cast<uint32_t*>(sm + L.cmask);
   int16_t* plist = reinterpret_cast<int16_t*>(sm + L.plist);
   int* misc = reinterpret_cast<int*>(sm + L.misc);
-  // misc: 0 tmem ptr, 1 overflow flag, 2 n_u, 3 n_pairs, 8.. unit scalars, 24.. ncand[16]
+  // misc: 1 overflow flag, 2 n_u, 3 n_pairs, 8.. unit scalars, 24.. ncand[16]
   int* ncand = misc + 24;
   const uint32_t bar0 = sm_u32 + L.bars;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kMaxStages + s); };
-  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * kMaxStages + b); };
-  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 2 + b); };
-  auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kMaxStages + 4 + s); };
+  auto cfull_bar = [&](int s) { return bar0 + 8u * (2 * kMaxStages + s); };
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grid = gridDim.x, bid = blockIdx.x;
   const int B = a.B, E = a.E, K = a.K, D = a.D, Dp = a.Dp, CM = a.CM, CH = a.CH;
-  const int n_tb = ceil_div(B, kChTB), n_eb = ceil_div(E, kChEB);
+  constexpr int ch_tb = 4, ch_eb = 8;  // chain unit shape (lane = expert * 4 + token)
+  const int n_tb = ceil_div(B, ch_tb), n_eb = ceil_div(E, ch_eb);
+  const int gwn = grid - a.n_ch;       // worker CTAs: gate/up pieces and P2 units
+  const bool worker = bid < gwn;
   const int stages = a.stages;
   const bool vec_ok = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
                       ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
-  // tag of this launch's P0 partials and token-row flags; issued first, consumed late
+  // tag of this launch's P0 partials; issued first, consumed late
   const uint32_t epoch = *reinterpret_cast<volatile const unsigned*>(&a.ctr[kCtrEpoch]) + 1u;
 
   DEC_STAMP(0, 0);
   // ---- prologue ----
-  if (tid == 0) {
-    tma_prefetch_desc(&tmap_w3);
-    tma_prefetch_desc(&tmap_xb3);
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), 1);
-    }
-    for (int s = 0; s < kChStages; ++s) mbar_init(cfull_bar(s), 1);
+  if (tid < stages) {
+    mbar_init(full_bar(tid), 1);
+    mbar_init(empty_bar(tid), kNumGWarps);
+    if (tid < kChStages) mbar_init(cfull_bar(tid), 1);
     fence_barrier_init();
-    misc[1] = 0;
+    if (tid == 0) {
+      tma_prefetch_desc(&tmap_w3);
+      misc[1] = 0;
+    }
   }
-  if (warp == kWarpMma) tmem_alloc(sm_u32 + L.misc, 32);
   for (int e = tid; e < kDecMaxE; e += kDecThreads) cmask[e] = 0u;
-  tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(misc);
 
   const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
   const int KB = Dp / kBlockK;
   const int KX = ceil_div(KB, kKBox);       // ring stages per piece
   const int PE = 4 * NB;                    // pieces per routed expert
   const int n_sh = 4 * NBs;                 // pieces of the shared expert (come first)
+  constexpr int kStoreWarps = (16 * TB + 31) / 32;  // consumer warps that store h of a piece
 
   if (warp == kWarpTma) {
     // =====================================================================================
-    // G role, producer: one 3-D box of the weight image + the matching token K blocks per stage
+    // G role, producer: one 3-D box of the weight image per stage
     // =====================================================================================
-    if (lane == 0) {
-      // the bf16 token rows are written by the D role of B CTAs: wait for their flags
-      for (int t = 0; t < B; ++t) {
-        const uint2* f = reinterpret_cast<const uint2*>(a.ctr + kCtrXb) + t;
-        while (ld_volatile_u2(f).y != epoch) __nanosleep(32);
-      }
-      __threadfence();
-      fence_proxy_async_all();
-    }
-    int gk = 0, p = bid;
+    int gk = 0, p = worker ? bid : 0x3fffffff;
     auto produce = [&](int rb, int q) {
 #pragma unroll 1
       for (int kx = 0; kx < KX; ++kx, ++gk) {
         const int s = gk % stages;
         mbar_wait(empty_bar(s), ((gk / stages) & 1u) ^ 1u);
         mbar_arrive_expect_tx(full_bar(s), kStageBytes);
-        const uint32_t dst = sm_u32 + L.ring + s * kStageBytes;
-        tma_load_3d(dst, &tmap_w3, 0, q * 32, rb * KB + kx * kKBox, full_bar(s), kPolicyEvictFirst);
-        tma_load_3d(dst + kStageA, &tmap_xb3, 0, 0, kx * kKBox, full_bar(s), kPolicyEvictLast);
+        tma_load_3d(sm_u32 + L.ring + s * kStageBytes, &tmap_w3, 0, q * 32, rb * KB + kx * kKBox,
+                    full_bar(s), kPolicyEvictFirst);
       }
     };
     if (lane == 0) {
 #pragma unroll 1
-      for (; p < n_sh; p += grid) produce(E * NB + (p >> 2), p & 3);
+      for (; p < n_sh; p += gwn) produce(E * NB + (p >> 2), p & 3);
     }
     __syncwarp();
-    tables_wait();
+    tables_wait_producer();
     if (lane == 0) {
       const int n_u = misc[2];
-      DEC_STAMP(32, 2);
+      DEC_STAMP(0, 11);
 #pragma unroll 1
-      for (; p < n_sh + n_u * PE; p += grid) {
+      for (; p < n_sh + n_u * PE; p += gwn) {
         const int pr = p - n_sh;
         const int u = pr / PE, qq = pr % PE;
         produce(static_cast<int>(ulist[u]) * NB + (qq >> 2), qq & 3);
       }
-      DEC_STAMP(32, 3);
+      DEC_STAMP(0, 3);
     }
-  } else if (warp == kWarpMma) {
+  } else if (warp >= kWarpG0 && warp < kWarpG0 + kNumGWarps) {
     // =====================================================================================
-    // G role, MMA issuer: 128x16x16 on a tile whose first 32 rows are the piece
+    // G role, consumers: warp gw owns K block gw of every stage; lane l holds the 16-byte
+    // column piece l % 8 of the rows l / 8 + 4 i (i < 8; rows 0-15 gate, 16-31 up).  Per token
+    // the FMA sequence is the same for every batch size.
     // =====================================================================================
-    constexpr uint32_t kIdesc = make_idesc_bf16(128, kDecTokens);
-    int gk = 0, li = 0, p = bid;
-    auto issue_piece = [&]() {
-      const int buf = li & 1;
-      mbar_wait(tempty_bar(buf), (((li >> 1) & 1u) ^ 1u));
-      tc_fence_after();
+    const int gw = warp - kWarpG0, gtid = tid - kWarpG0 * 32;
+    __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm + L.xs);
+    if (!worker) {
+      // chain CTA: nothing to stage
+    } else if (vec_ok) {
+      // four 16-byte loads in flight per thread (a dependent load per element would cost a cold
+      // miss each)
+      const int q4 = Dp / 4, tot4 = TB * q4;
+#pragma unroll 1
+      for (int i0 = gtid; i0 < tot4; i0 += 4 * kGThreads) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kGThreads;
+          const int t = i / q4, d = (i - t * q4) * 4;
+          v[u] = (i < tot4 && t < B && d < D)
+                     ? __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t) * D + d))
+                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kGThreads;
+          if (i < tot4) {
+            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(xs) + 2 * i;
+            dst[0] = __floats2bfloat162_rn(v[u].x, v[u].y);
+            dst[1] = __floats2bfloat162_rn(v[u].z, v[u].w);
+          }
+        }
+      }
+    } else {
+      for (int i = gtid; i < TB * Dp; i += kGThreads) {
+        const int t = i / Dp, d = i - t * Dp;
+        const float v = (t < B && d < D) ? __ldg(a.x + static_cast<size_t>(t) * D + d) : 0.0f;
+        xs[i] = __float2bfloat16_rn(v);
+      }
+    }
+    g_sync();
+    DEC_STAMP(kWarpG0 * 32, 16);
+    float* gpart = reinterpret_cast<float*>(sm + L.gpart);
+    const int c8 = lane & 7, rq = lane >> 3;
+    constexpr int TG = TB < 4 ? TB : 4;
+    int gk = 0, li = 0, p = worker ? bid : 0x3fffffff;
+    auto do_piece = [&](int u /* -1: shared */, int nb, int q, int m_valid) {
+      float acc[8][TB];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int t = 0; t < TB; ++t) acc[i][t] = 0.0f;
 #pragma unroll 1
       for (int kx = 0; kx < KX; ++kx, ++gk) {
         const int s = gk % stages;
         mbar_wait(full_bar(s), (gk / stages) & 1u);
-        tc_fence_after();
-        const uint32_t st = sm_u32 + L.ring + s * kStageBytes;
-        const int nk = min(kKBox, KB - kx * kKBox);
-#pragma unroll 1
-        for (int j = 0; j < nk; ++j) {
-          const uint64_t a_desc = make_smem_desc_sw128(st + j * 4096);
-          const uint64_t b_desc = make_smem_desc_sw128(st + kStageA + j * 2048);
+        const int kb = kx * kKBox + gw;
+        if (kb < KB) {
+          const uint4* wp = reinterpret_cast<const uint4*>(sm + L.ring + s * kStageBytes + gw * 4096) + lane;
+          uint4 wv[8];
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k)
-            umma_bf16(tmem_base + buf * kDecTokens, a_desc + 2u * k, b_desc + 2u * k, kIdesc,
-                      (kx | j | k) != 0 ? 1u : 0u);
+          for (int i = 0; i < 8; ++i) wv[i] = wp[32 * i];
+#pragma unroll
+          for (int tg = 0; tg < TB; tg += TG) {
+            float xf[TG][8];
+#pragma unroll
+            for (int tt = 0; tt < TG; ++tt) {
+              const uint4 xv = *reinterpret_cast<const uint4*>(xs + static_cast<size_t>(tg + tt) * Dp +
+                                                               kb * kBlockK + c8 * 8);
+              unpack8(xv, xf[tt]);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float wf[8];
+              unpack8(wv[i], wf);
+#pragma unroll
+              for (int tt = 0; tt < TG; ++tt)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[i][tg + tt] = fmaf(wf[e], xf[tt][e], acc[i][tg + tt]);
+            }
+          }
         }
-        umma_commit(empty_bar(s));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_bar(s));
       }
-      umma_commit(tfull_bar(buf));
-      ++li;
-    };
-    if (lane == 0) {
-#pragma unroll 1
-      for (; p < n_sh; p += grid) issue_piece();
-    }
-    __syncwarp();
-    tables_wait();
-    if (lane == 0) {
-      const int n_u = misc[2];
-#pragma unroll 1
-      for (; p < n_sh + n_u * PE; p += grid) issue_piece();
-    }
-  } else if (warp == kWarpEpi) {
-    // =====================================================================================
-    // G role, epilogue: TMEM lanes 0-15 hold the gate rows, 16-31 the up rows of 16 neurons
-    // =====================================================================================
-    const bool is_gate_lane = lane < 16;
-    int li = 0, p = bid;
-    auto finish_piece = [&](int u /* -1: shared */, int nb, int q, int m_valid) {
+      // sum over the 8 lanes of a row: butterfly that leaves row 4*b2 + 2*b1 + b0 on lane bits
+      // (b2 b1 b0) of every group of 8 -- 7 shuffles per token instead of 24, fixed order
       const int buf = li & 1;
-      mbar_wait(tfull_bar(buf), (li >> 1) & 1u);
-      tc_fence_after();
-      uint32_t v[16];
-      tmem_ld_32x32b_x16(tmem_base + buf * kDecTokens, v);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty_bar(buf));
-      const int n = nb * kNeuronBlock + 16 * q + (lane & 15);
+      const bool b2 = (lane & 4) != 0, b1 = (lane & 2) != 0, b0 = (lane & 1) != 0;
+      const int myrow = 4 * ((b2 ? 4 : 0) + (b1 ? 2 : 0) + (b0 ? 1 : 0)) + rq;
 #pragma unroll
-      for (int c = 0; c < 16; c += 2) {
-        if (c < B) {
-          const float mine0 = __uint_as_float(v[c]);
-          const float mine1 = __uint_as_float(v[c + 1]);
-          const float send = is_gate_lane ? mine1 : mine0;
-          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-          const float g = is_gate_lane ? mine0 : recv;
-          const float up = is_gate_lane ? recv : mine1;
-          const int col = c + (is_gate_lane ? 0 : 1);
-          if (col < B && n < m_valid) {
-            const int r = u < 0 ? kDecTokens * CM + col : rowtab[u * 16 + col];
+      for (int t = 0; t < TB; ++t) {
+        float v4[4], v2[2];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float keep = b2 ? acc[4 + k][t] : acc[k][t];
+          const float send = b2 ? acc[k][t] : acc[4 + k][t];
+          v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float keep = b1 ? v4[2 + k] : v4[k];
+          const float send = b1 ? v4[k] : v4[2 + k];
+          v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        const float keep = b0 ? v2[1] : v2[0];
+        const float send = b0 ? v2[0] : v2[1];
+        gpart[((buf * kNumGWarps + gw) * TB + t) * 32 + myrow] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+      g_sync();
+      if (gw < kStoreWarps) {
+        if (gtid < 16 * TB) {
+          const int j = gtid & 15, t = gtid >> 4;
+          const float* gp = gpart + (buf * kNumGWarps * TB + t) * 32;
+          float g = gp[j], up = gp[16 + j];
+#pragma unroll
+          for (int w = 1; w < kNumGWarps; ++w) {
+            g = __fadd_rn(g, gp[w * TB * 32 + j]);
+            up = __fadd_rn(up, gp[w * TB * 32 + 16 + j]);
+          }
+          const int n = nb * kNeuronBlock + 16 * q + j;
+          if (t < B && n < m_valid) {
+            const int r = u < 0 ? kDecTokens * CM + t : rowtab[u * 16 + t];
             if (r >= 0) a.hc[static_cast<size_t>(r) * a.Nh + n] = silu_f(g) * up;
           }
         }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(&a.ctr[kCtrCnt + 1 + u], 1u);
       }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(&a.ctr[kCtrCnt + 1 + u], 1u);
       ++li;
     };
 #pragma unroll 1
-    for (; p < n_sh; p += grid) finish_piece(-1, p >> 2, p & 3, a.S);
-    tables_wait();
+    for (; p < n_sh; p += gwn) do_piece(-1, p >> 2, p & 3, a.S);
+    tables_wait_consumers();
+    DEC_STAMP(kWarpG0 * 32, 17);
     const int n_u = misc[2];
 #pragma unroll 1
-    for (; p < n_sh + n_u * PE; p += grid) {
+    for (; p < n_sh + n_u * PE; p += gwn) {
       const int pr = p - n_sh;
       const int u = pr / PE, qq = pr % PE;
-      finish_piece(u, qq >> 2, qq & 3, a.N);
+      do_piece(u, qq >> 2, qq & 3, a.N);
+      if (p == bid + ((n_sh + gwn - 1 - bid) / gwn) * gwn) DEC_STAMP(kWarpG0 * 32, 18);
     }
-    DEC_STAMP(0, 4);
+    DEC_STAMP(kWarpG0 * 32, 4);
   } else if (warp == kWarpChain) {
     // =====================================================================================
-    // Exact routing chains on the LAST CTAs of the grid, one warp: lane 0 keeps a ring of 1-D
-    // bulk copies ahead of the 32 dependent chains (8 experts x 4 tokens).  They only read x and
-    // the router, so they start right away; their result is needed by P3 (and by caller-mask
-    // lookups).
+    // Exact routing chains on the LAST n_ch CTAs of the grid, which do nothing else (next to
+    // streaming warps a dependent-add chain runs three times slower), one warp of 32 dependent
+    // chains (8 experts x 4 tokens) behind a ring of 1-D bulk copies, one row per lane.  They
+    // only read x and the router, so they start right away; their result is needed by P3 (and by
+    // caller-mask lookups).
     // =====================================================================================
-    float* ring = reinterpret_cast<float*>(sm + L.chain);
+    float* ring = reinterpret_cast<float*>(sm + L.chain);   // [stages][rows][kChRow]
+    float* fring = ring;                                    // unaligned operands: [rows][kChRow]
     const int n_cu = n_eb * n_tb;
     const int nsub = ceil_div(D, kChSub);
+    const int ch_rows = ch_eb + ch_tb;
     int gsc = 0;  // ring position, continues across units
 #pragma unroll 1
-    for (int cu = grid - 1 - bid; cu < n_cu; cu += grid) {
+    for (int cu = worker ? n_cu : bid - gwn; cu < n_cu; cu += a.n_ch) {
       const int eb = cu % n_eb, tb = cu / n_eb;
-      const int e0 = eb * kChEB, t0 = tb * kChTB;
-      const int n_e = min(kChEB, E - e0), n_t = min(kChTB, B - t0);
+      const int e0 = eb * ch_eb, t0 = tb * ch_tb;
+      const int n_e = min(ch_eb, E - e0), n_t = min(ch_tb, B - t0);
+      const int e_i = lane / ch_tb, t_j = lane % ch_tb;
+      const bool valid = (e_i < n_e) && (t_j < n_t);
       const float* wsrc = a.router + static_cast<size_t>(e0) * D;
       const float* xsrc = a.x + static_cast<size_t>(t0) * D;
-      auto issue = [&](int sc, int gidx) {  // lane 0: sub-chunk sc of this unit into its ring slot
-        const int slot = gidx % kChStages;
-        const int d0 = sc * kChSub;
-        const uint32_t bytes = static_cast<uint32_t>(min(kChSub, D - d0)) * 4u;
-        mbar_arrive_expect_tx(cfull_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
-        const uint32_t dst = smem_u32(ring + slot * kChRows * kChRow);
-#pragma unroll 1
-        for (int r = 0; r < n_e; ++r)
-          bulk_copy_g2s(dst + r * kChRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
-                        cfull_bar(slot));
-#pragma unroll 1
-        for (int r = 0; r < n_t; ++r)
-          bulk_copy_g2s(dst + (kChEB + r) * kChRow * 4, xsrc + static_cast<size_t>(r) * D + d0, bytes,
-                        cfull_bar(slot));
-      };
-      if (vec_ok && lane == 0)
-        for (int sc = 0; sc < nsub && sc < kChStages; ++sc) issue(sc, gsc + sc);
-      __syncwarp();
-      const int e_i = lane / kChTB, t_j = lane % kChTB;
-      const bool valid = (e_i < n_e) && (t_j < n_t);
       float acc = 0.0f;
       DEC_STAMP(kWarpChain * 32, 14);
-#pragma unroll 1
-      for (int sc = 0; sc < nsub; ++sc) {
-        const int gidx = gsc + sc;
-        const int slot = gidx % kChStages;
-        float* base = ring + slot * kChRows * kChRow;
-        const int n = min(kChSub, D - sc * kChSub);
-        if (vec_ok) {
-          mbar_wait(cfull_bar(slot), (gidx / kChStages) & 1u);
-        } else {
-          // unaligned operands: the warp stages the sub-chunk itself
+      if (vec_ok) {
+        // the whole warp: sub-chunk sc of this unit into its ring slot, one row per lane
+        auto issue = [&](int sc, int gidx) {
+          const int slot = gidx % kChStages;
           const int d0 = sc * kChSub;
+          const uint32_t bytes = static_cast<uint32_t>(min(kChSub, D - d0)) * 4u;
+          if (lane == 0) mbar_arrive_expect_tx(cfull_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
+          __syncwarp();
+          const uint32_t dst = smem_u32(ring + slot * ch_rows * kChRow);
+          if (lane < n_e)
+            bulk_copy_g2s(dst + lane * kChRow * 4, wsrc + static_cast<size_t>(lane) * D + d0, bytes,
+                          cfull_bar(slot));
+          else if (lane - n_e < n_t)
+            bulk_copy_g2s(dst + (ch_eb + lane - n_e) * kChRow * 4,
+                          xsrc + static_cast<size_t>(lane - n_e) * D + d0, bytes, cfull_bar(slot));
+        };
+        for (int sc = 0; sc < nsub && sc < kChStages; ++sc) issue(sc, gsc + sc);
+        __syncwarp();
+#pragma unroll 1
+        for (int sc = 0; sc < nsub; ++sc) {
+          const int gidx = gsc + sc;
+          const int slot = gidx % kChStages;
+          const float* base = ring + slot * ch_rows * kChRow;
+          const int n4 = min(kChSub, D - sc * kChSub) >> 2;
+          mbar_wait(cfull_bar(slot), (gidx / kChStages) & 1u);
+          const float4* wr = reinterpret_cast<const float4*>(base + min(e_i, n_e - 1) * kChRow);
+          const float4* xr = reinterpret_cast<const float4*>(base + (ch_eb + min(t_j, n_t - 1)) * kChRow);
+          int q = 0;
+#pragma unroll 1
+          for (; q + 8 <= n4; q += 8) {
+            // every operand of 32 elements in registers first, then the 32 dependent adds
+            float4 w[8], xv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              w[j] = wr[q + j];
+              xv[j] = xr[q + j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              acc = __fadd_rn(acc, __fmul_rn(w[j].x, xv[j].x));
+              acc = __fadd_rn(acc, __fmul_rn(w[j].y, xv[j].y));
+              acc = __fadd_rn(acc, __fmul_rn(w[j].z, xv[j].z));
+              acc = __fadd_rn(acc, __fmul_rn(w[j].w, xv[j].w));
+            }
+          }
+#pragma unroll 1
+          for (; q < n4; ++q) {
+            const float4 w = wr[q], xv = xr[q];
+            acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
+            acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
+            acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
+            acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
+          }
+          __syncwarp();  // every lane is done with the slot: refill it
+          if (sc + kChStages < nsub) issue(sc + kChStages, gidx + kChStages);
+        }
+        gsc += nsub;
+      } else {
+        // unaligned operands: the warp stages each sub-chunk itself
+        const float* wsrc = a.router + static_cast<size_t>(e0) * D;
+#pragma unroll 1
+        for (int sc = 0; sc < nsub; ++sc) {
+          const int d0 = sc * kChSub;
+          const int n = min(kChSub, D - d0);
 #pragma unroll 1
           for (int r = 0; r < n_e + n_t; ++r) {
             const float* src = (r < n_e) ? wsrc + static_cast<size_t>(r) * D + d0
                                          : xsrc + static_cast<size_t>(r - n_e) * D + d0;
-            float* drow = base + ((r < n_e) ? r : kChEB + r - n_e) * kChRow;
+            float* drow = fring + ((r < n_e) ? r : ch_eb + r - n_e) * kChRow;
 #pragma unroll 1
             for (int i = lane; i < n; i += 32) drow[i] = __ldg(src + i);
           }
           __syncwarp();
+          const float* wr = fring + min(e_i, n_e - 1) * kChRow;
+          const float* xr = fring + (ch_eb + min(t_j, n_t - 1)) * kChRow;
+#pragma unroll 4
+          for (int i = 0; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
+          __syncwarp();
         }
-        const float* wr = base + e_i * kChRow;
-        const float* xr = base + (kChEB + t_j) * kChRow;
-        const int n4 = n >> 2;
-#pragma unroll 8
-        for (int q = 0; q < n4; ++q) {
-          const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
-          const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * q);
-          acc = __fadd_rn(acc, __fmul_rn(w.x, xv.x));
-          acc = __fadd_rn(acc, __fmul_rn(w.y, xv.y));
-          acc = __fadd_rn(acc, __fmul_rn(w.z, xv.z));
-          acc = __fadd_rn(acc, __fmul_rn(w.w, xv.w));
-        }
-#pragma unroll 1
-        for (int i = 4 * n4; i < n; ++i) acc = __fadd_rn(acc, __fmul_rn(wr[i], xr[i]));
-        __syncwarp();  // every lane is done with the slot: lane 0 refills it
-        if (vec_ok && lane == 0 && sc + kChStages < nsub) issue(sc + kChStages, gidx + kChStages);
       }
       DEC_STAMP(kWarpChain * 32, 15);
       if (valid) a.logits[static_cast<size_t>(t0 + t_j) * E + e0 + e_i] = acc;
@@ -662,11 +746,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
         if (lane == 0) atomicAdd(&a.ctr[kCtrRoute], 1u);
         DEC_STAMP(kWarpChain * 32, 10);
       }
-      gsc += nsub;
     }
   } else {
     // =====================================================================================
-    // D role (warps 4..11)
+    // D role (warps 6..13)
     // =====================================================================================
     const int dtid = tid - kWarpD0 * 32, dwarp = dtid >> 5;
     uint32_t* keys_s = reinterpret_cast<uint32_t*>(sm + L.keys);
@@ -677,24 +760,12 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
     float* gred = reinterpret_cast<float*>(sm + L.gred);
     int* p2 = misc + 8;  // 2 b*, 3 below_bins, 4 M, 5 pivot, 6 below, 7 equal, 8 mcount
 
-    // ---- P0a: bf16 token rows for the TMA (token t on CTA (grid - 1 - t) % grid ... any) ----
-    for (int t = bid; t < B; t += grid) {
-      const float* src = a.x + static_cast<size_t>(t) * D;
-      __nv_bfloat16* dst = a.xb + static_cast<size_t>(t) * Dp;
-      for (int d = dtid; d < D; d += kDThreads) dst[d] = __float2bfloat16_rn(__ldg(src + d));
-      __threadfence();
-      d_sync();
-      if (dtid == 0) {
-        fence_proxy_async_all();
-        st_volatile_u2(reinterpret_cast<uint2*>(a.ctr + kCtrXb) + t, 1u, epoch);
-      }
-    }
-    // ---- P0b: fast logits of (expert, d_model slice) units ----
+    // ---- P0: fast logits of (expert, d_model slice) units ----
     const int ND = a.ND, DS = a.DS;
     {
       float* red = gred;  // [8 warps][4 tokens][2]
 #pragma unroll 1
-      for (int unit = (bid + grid - B % grid) % grid; unit < E * ND; unit += grid) {
+      for (int unit = bid; unit < E * ND; unit += grid) {
         const int e = unit / ND, j = unit % ND;
         const int d0 = j * DS, d1 = min(D, d0 + DS);
         const float* wr = a.router + static_cast<size_t>(e) * D;
@@ -768,19 +839,64 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
 
     // ---- candidates (every CTA computes the same tables) ----
     {
+      // every partial of every token: all of this thread's words in flight before the first check
+      float2* pf = reinterpret_cast<float2*>(gred);
+      const int total = B * E * ND;
+#pragma unroll 1
+      for (int base = 0; base < total; base += kDThreads * 4) {
+        uint2 va[4], vb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = base + u * kDThreads + dtid;
+          if (i < total) {
+            va[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i));
+            vb[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i) + 1);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = base + u * kDThreads + dtid;
+          if (i < total) {
+            while (va[u].y != epoch) {
+              __nanosleep(20);
+              va[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i));
+            }
+            while (vb[u].y != epoch) {
+              __nanosleep(20);
+              vb[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i) + 1);
+            }
+            pf[i] = make_float2(__uint_as_float(va[u].x), __uint_as_float(vb[u].x));
+          }
+        }
+      }
+      d_sync();
+      // slice partials summed in slice order, in place at slice 0
+      if (ND > 1) {
+        for (int i = dtid; i < B * E; i += kDThreads) {
+          float f = 0.0f, sa = 0.0f;
+#pragma unroll 1
+          for (int j = 0; j < ND; ++j) {
+            const float2 v = pf[i * ND + j];
+            f = __fadd_rn(f, v.x);
+            sa = __fadd_rn(sa, v.y);
+          }
+          pf[i * ND] = make_float2(f, sa);
+        }
+        d_sync();
+      }
       // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
       const double u24 = 5.9604644775390625e-8;
       const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
 #pragma unroll 1
       for (int t = dwarp; t < B; t += 8) {
-        const uint2* p0t = a.p0 + static_cast<size_t>(t) * E * ND * 2;
+        const float2* pft = pf + static_cast<size_t>(t) * E * ND;
         bool bad;
         if (E <= 64)
-          bad = cand_token<2>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+          bad = cand_token<2>(pft, ND, E, mfac, K, CM, t, cmask);
         else if (E <= 128)
-          bad = cand_token<4>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+          bad = cand_token<4>(pft, ND, E, mfac, K, CM, t, cmask);
         else
-          bad = cand_token<8>(p0t, E, ND, epoch, mfac, K, CM, t, cmask);
+          bad = cand_token<8>(pft, ND, E, mfac, K, CM, t, cmask);
         if (bad && lane == 0) misc[1] = 1;
       }
       d_sync();
@@ -866,8 +982,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
       const bool lane_ok = g < G;
       bool route_ready = false;
       __shared__ SelScratch sel_sc;
+      // units are dealt from the CTA after the one that took the last gate/up piece
+      const int v_first = worker ? (bid - (n_sh + n_u * PE) % gwn + gwn) % gwn : n_units;
 #pragma unroll 1
-      for (int v = bid; v < n_units; v += grid) {
+      for (int v = v_first; v < n_units; v += gwn) {
         const int pu = plist[v / CH], c = v % CH;
         const int u = pu >> 4, t = pu & 15;
         const bool routed = u < n_u;
@@ -909,7 +1027,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
         // wait until every gate/up piece of this expert has landed (one polite poller)
         if (dtid == 0) {
           p2[8] = 0;
-          spin_until(&a.ctr[kCtrCnt + (routed ? 1 + u : 0)], static_cast<unsigned>(routed ? PE : n_sh));
+          spin_until(&a.ctr[kCtrCnt + (routed ? 1 + u : 0)], static_cast<unsigned>((routed ? PE : n_sh) * kStoreWarps));
         }
         hist_s[2 * dtid] = 0;
         hist_s[2 * dtid + 1] = 0;
@@ -1065,6 +1183,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
 
         // ---- gather + partial ----
         const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
+        // rows beyond the first batch of direct loads: into L2 now, so that the later batches do
+        // not pay a DRAM round trip each
+        for (int k = dtid; k < m; k += kDThreads)
+          bulk_prefetch_l2(wb + static_cast<size_t>(lst[k]) * Dp, static_cast<uint32_t>(Dp) * 2u);
         float* pout = a.part + (static_cast<size_t>(t * (CM + 1) + q) * CH + c) * Dp;
         if (NT == 1) {
           float acc[1][8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
@@ -1129,13 +1251,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
     DEC_STAMP(kWarpD0 * 32, 5);
   }
 
-  // every role of this CTA is through: TMEM goes back, the ring becomes P3 scratch
-  tc_fence_before();
+  // every role of this CTA is through: the ring becomes P3 scratch
   __syncthreads();
-  if (warp == kWarpMma) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, 32);
-  }
   if (warp < kWarpD0) return;
 
   // =====================================================================================
@@ -1165,6 +1282,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
         swt[i] = 1.0f;
       }
     }
+    DEC_STAMP(kWarpD0 * 32, 19);
     if (dtid == 0) {
       spin_until(&a.ctr[kCtrDone], static_cast<unsigned>(grid));
       // every CTA that gets here has read all the counters for the last time: the last one
@@ -1204,6 +1322,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
             a.part + (static_cast<size_t>(t * (CM + 1) + r) * CH + c) * Dp + d4 * 4));
       }
       d_sync();
+      DEC_STAMP(kWarpD0 * 32, 20);
       for (int idx = dtid; idx < nq * R; idx += kDThreads) {
         const float4* pb = buf + static_cast<size_t>(idx) * CH;
         float4 sacc = pb[0];
@@ -1271,8 +1390,9 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
 
 bool decode_fused_eligible(const Geometry& g, int B) {
   const int nmax = g.N > g.S ? g.N : g.S;
-  return B >= 1 && B <= kDecTokens && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxN &&
-         g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288 && dec_stages_for(nmax) >= 3;
+  return B >= 1 && B <= kDecMaxB && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxN &&
+         g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288 &&
+         dec_stages_for(nmax, dec_tb_for(B), g.Dp) >= kMinStages;
 }
 
 int decode_counter_words() { return kCtrWords; }
@@ -1291,9 +1411,10 @@ int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
   return ch;
 }
 
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_xb3,
-                        const DecodeLaunch& d, const Geometry& g, int n_sms) {
-  // the opt-in is per device: set it on every launch path's first use of each device
+
+template <int TB>
+static void launch_tb(const cudaLaunchConfig_t& cfg, const CUtensorMap* tmap_w3, const DecodeArgs& a) {
+  // the opt-in is per device: set it on the first launch on each device
   static std::mutex mu;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -1301,12 +1422,18 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   {
     std::lock_guard<std::mutex> lk(mu);
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-      cudaFuncSetAttribute(decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(decode_fused_kernel<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kSmemBudget + 1024);
       if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
   }
+  cudaLaunchKernelEx(&cfg, decode_fused_kernel<TB>, *tmap_w3, a);
+}
+
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const DecodeLaunch& d,
+                        const Geometry& g, int n_sms) {
   const int nmax = g.N > g.S ? g.N : g.S;
+  const int tb = dec_tb_for(d.B);
   DecodeArgs a{};
   a.x = d.x;
   a.router = d.router;
@@ -1332,7 +1459,15 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   a.CM = decode_cand_rows(g.K);
   a.CH = d.CH;
   a.capture = d.capture ? 1 : 0;
-  a.stages = dec_stages_for(nmax);
+  a.stages = dec_stages_for(nmax, tb, g.Dp);
+  if (const char* es = getenv("SKB_DEC_STAGES")) {  // experiments only
+    const int v = atoi(es);
+    if (v >= kMinStages && v <= a.stages) a.stages = v;
+  }
+  {
+    const int n_cu = ceil_div(g.E, 8) * ceil_div(d.B, 4);
+    a.n_ch = n_cu < kMaxChainCtas ? n_cu : kMaxChainCtas;
+  }
   {
     // fast-logit units: (expert, d_model slice); as many slices as fill the grid once
     int nd = n_sms / g.E;
@@ -1342,7 +1477,6 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
     a.ND = ceil_div(g.D, ds);
     a.DS = ds;
   }
-  a.xb = d.xb;
   a.p0 = reinterpret_cast<uint2*>(d.p0);
   a.logits = d.logits;
   a.ids = d.ids;
@@ -1364,8 +1498,13 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   cfg.stream = ctx.stream;
   cfg.gridDim = dim3(n_sms);
   cfg.blockDim = dim3(kDecThreads);
-  cfg.dynamicSmemBytes = dec_smem_layout(a.stages, nmax).total + 1024;
-  cudaLaunchKernelEx(&cfg, decode_fused_kernel, *tmap_w3, *tmap_xb3, a);
+  cfg.dynamicSmemBytes = dec_smem_layout(a.stages, nmax, tb, g.Dp).total + 1024;
+  switch (tb) {
+    case 1: launch_tb<1>(cfg, tmap_w3, a); break;
+    case 2: launch_tb<2>(cfg, tmap_w3, a); break;
+    case 4: launch_tb<4>(cfg, tmap_w3, a); break;
+    default: launch_tb<8>(cfg, tmap_w3, a); break;
+  }
   return 1;
 }
 

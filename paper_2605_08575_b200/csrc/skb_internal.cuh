@@ -153,7 +153,7 @@ int launch_down(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g);
 int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
                          int B, int K, int D, float* y);
 
-// Fused decode kernel (decode.cu): the whole layer for B <= 16 in one persistent launch.
+// Fused decode kernel (decode.cu): the whole layer for B <= 8 in one persistent launch.
 struct DecodeLaunch {
   const float* x;                  // [B][D]
   const float* router;             // [E][D]
@@ -165,7 +165,6 @@ struct DecodeLaunch {
   const uint8_t* mask_s;           // kSelectGiven: [B][S] or NULL
   int CH;                          // row chunks per (token, slot): decode_chunks()
   bool capture;                    // also write h / inv / perm / row_expert in slot order
-  __nv_bfloat16* xb;               // [16][Dp] bf16 token rows (TMA source)
   float* p0;                       // decode_p0_words() words: tagged partial fast logits
   float* logits;                   // [B][E] exact logits
   int32_t* ids;                    // [B][K]
@@ -184,10 +183,9 @@ int decode_counter_words();
 int decode_cand_rows(int K);
 int decode_p0_words(const Geometry& g);
 int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms);
-// tmap_w3: the gate/up image as {64 columns, 128 rows, tiles}, box {64, 32, 4}; tmap_xb3: the bf16
-// token rows as {64 columns, 16 rows, K blocks}, box {64, 16, 4}
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_xb3,
-                        const DecodeLaunch& d, const Geometry& g, int n_sms);
+// tmap_w3: the gate/up image as {64 columns, 128 rows, tiles}, box {64, 32, 4}, no swizzle
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const DecodeLaunch& d,
+                        const Geometry& g, int n_sms);
 
 // weight image construction
 int launch_pack_gateup(cudaStream_t s, const float* gate, const float* up, int n_rows, int D, int Dp,

@@ -361,7 +361,7 @@ def test_invariants(skb, oracle):
         whole = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=flags)
         np.testing.assert_array_equal(half.outputs, whole.outputs[:3])
     half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl, flags=skb.FLAG_FUSED_DECODE)
-    full = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=skb.FLAG_FUSED_DECODE)
+    full = skb.forward_topk_sparse(layer, x[:8], lvl, lvl, flags=skb.FLAG_FUSED_DECODE)
     np.testing.assert_array_equal(half.outputs, full.outputs[:3])  # both: the fused decode kernel
     # the automatic choice (a cost model over shape and batch) may differ between the two calls
     half = skb.forward_topk_sparse(layer, x[:3], lvl, lvl)
@@ -632,15 +632,16 @@ def test_ep_slices_reproduce_the_single_gpu_layer(skb, world):
 
 
 # ---------------------------------------------------------------------------------------------
-# the fused decode kernel (batches <= 16): its own edge cases
+# the fused decode kernel (batches <= 8): its own edge cases
 # ---------------------------------------------------------------------------------------------
 DECODE_CASES = [
     # E, K, D, N, S, renorm, B
     (64, 8, 256, 256, 0, True, 1),
-    (64, 8, 256, 256, 0, True, 16),
+    (64, 8, 256, 256, 0, True, 8),
+    (64, 8, 256, 256, 0, True, 2),
     (32, 8, 1024, 512, 0, True, 7),        # Granite shape
     (128, 1, 320, 1100, 1100, True, 5),    # top-1 + shared expert, ragged N (several keys/thread)
-    (256, 8, 192, 128, 64, False, 16),     # widest router the kernel takes, raw weights
+    (256, 8, 192, 128, 64, False, 8),      # widest router the kernel takes, raw weights
     (16, 16, 64, 64, 0, True, 3),          # K == E: every expert is routed
 ]
 
@@ -690,12 +691,12 @@ def test_fused_decode_matches_oracle_and_staged_kernels(skb, oracle, case):
 def test_fused_decode_is_batch_invariant_bit_for_bit(skb, oracle):
     # the row chunking depends on the shape only: a token's result does not depend on the batch
     cfg = Config(32, 4, 192, 320, 96, True)
-    w, x = rounded_case(oracle, cfg, seed=5, scale=0.1, batch=16, token_seed=11)
+    w, x = rounded_case(oracle, cfg, seed=5, scale=0.1, batch=8, token_seed=11)
     layer = make_layer(skb, w)
     lvl = skb.SparsityLevel(0.75)
     f = skb.FLAG_FUSED_DECODE
     whole = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=f).outputs
-    for b in (1, 2, 5, 9):
+    for b in (1, 2, 3, 5, 7):
         part = skb.forward_topk_sparse(layer, x[:b], lvl, lvl, flags=f).outputs
         np.testing.assert_array_equal(part, whole[:b])
     again = skb.forward_topk_sparse(layer, x, lvl, lvl, flags=f).outputs
@@ -729,7 +730,7 @@ def test_fused_decode_falls_back_to_exact_routing_when_the_bound_cannot_decide(s
 @pytest.mark.parametrize("shape,B,s", [
     ((64, 8, 2048, 1024, 0), 4, 0.5),       # OLMoE shape, small decode batch
     ((32, 4, 2880, 2880, 0), 2, 0.75),      # GPT-OSS-20B shape (two column tiles per W_down row)
-    ((256, 8, 2048, 512, 512), 16, 0.9),    # Qwen3.5-35B-A3B shape, R+S
+    ((256, 8, 2048, 512, 512), 8, 0.9),     # Qwen3.5-35B-A3B shape, R+S
     ((8, 1, 5120, 8192, 8192), 3, 0.9),     # Llama-4-Maverick shape with 8 of its 128 experts:
                                             # 32 keys per thread, three column tiles per row
 ])

@@ -22,8 +22,8 @@ for i in range(3):
         out=(C.c_longlong*(160*24))()
         L.skb_debug_dec(out)
         t=np.array(list(out)).reshape(160,24)
-        names={14:'chain start',15:'chain end',0:'start',1:'p0 arrive',2:'p0 barrier',3:'cand done',4:'p1 done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',20:'g issued',21:'g wait0',22:'g wait1',23:'g consumed',13:'p2 gather',5:'p2 done',6:'p2 barrier',7:'exit',10:'chain done'}
-        for k in (1,2,3,14,15,10,4,8,9,11,12,20,21,22,23,13,5,6,7):
+        names={14:'chain start',15:'chain end',0:'start',1:'p0 done',2:'tables',3:'tma issued',4:'g done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p3 barrier',7:'exit',10:'route done',11:'tma go',16:'x staged',17:'cons go',18:'piece1 done',19:'p3 tables',20:'p3 loaded'}
+        for k in (1,2,11,16,17,18,3,14,15,10,4,8,9,12,13,5,19,6,20,7):
             col=t[:148,k]-t[:148,0].min()
             col=col[t[:148,k]>0]
             if col.size: print(f'  {names[k]:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}')
@@ -33,7 +33,7 @@ for i in range(3):
             col=g[:,k]; col=col[col>0]-g0
             if col.size: print(f'  {nm:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d} (ns)')
         if i == 2:
-            ks=(0,1,2,3,14,15,10,4,8,9,11,12,13,5,6,7)
+            ks=(0,1,2,11,18,3,4,8,9,12,13,5,19,6,20,7)
             print('   cta ' + ' '.join(f'{names.get(k,k)[:9]:>9s}' for k in ks))
             for b in (0,1,31,32,63,64,100,127,128,143,144,145,146,147):
                 print(f'   {b:3d} ' + ' '.join(f'{(t[b,k]-t[:148,0].min() if t[b,k]>0 else -1):9d}' for k in ks))

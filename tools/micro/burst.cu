@@ -213,6 +213,18 @@ __global__ void __launch_bounds__(256) k_gather(const uint8_t* __restrict__ base
   if (threadIdx.x == 0) st[blockIdx.x].t1 = gtime();
 }
 
+
+// ---- touch: one 16-byte word every `step` bytes of a region (TLB / DRAM page warm-up experiment) ----
+__global__ void k_touch(const uint8_t* __restrict__ base, size_t bytes, size_t step, unsigned* sink) {
+  unsigned acc = 0;
+  for (size_t o = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * step; o < bytes; o += (size_t)gridDim.x * blockDim.x * step) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(base + o));
+    acc ^= v.x;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int main() {
@@ -254,6 +266,32 @@ int main() {
   auto pre = [&]() { CK(cudaMemsetAsync(flush, 0, 512ull << 20)); CK(cudaMemsetAsync(st, 0, sizeof(Stamp) * 1024)); };
   char name[160];
 
+
+  if (getenv("BURST5")) {
+    // is the ~3 us ramp of a cold burst address translation?  Same 64 MB ring stream, preceded (in its own launch,
+    // after the L2 flush) by a touch of one word per 2 MB / 64 KB / 4 KB of the region
+    const size_t bytes = 64ull << 20; const int grid = 148, chunk = 16384, stages = 9; const size_t smem = (size_t)stages * chunk + 16 * stages + 1024;
+    for (int rep = 0; rep < 3; ++rep) {
+      for (size_t step : {(size_t)0, (size_t)2 << 20, (size_t)65536, (size_t)4096}) {
+        uint8_t* p = region(bytes); pre();
+        if (step) k_touch<<<148, 256>>>(p, bytes, step, sink);
+        cudaEventRecord(e0); k_ring<0, 0><<<grid, 64, smem>>>(p, tm, bytes, chunk, stages, 0, st, kEvictFirst); cudaEventRecord(e1);
+        snprintf(name, sizeof name, "ring 64 MB after touch step=%zu", step); finish(name, grid, bytes);
+      }
+      // the touch covers the whole 6 GB buffer at 2 MB steps (what a kernel could do before it knows its experts)
+      { uint8_t* p = region(bytes); pre(); k_touch<<<148, 256>>>(buf, total, (size_t)2 << 20, sink);
+        cudaEventRecord(e0); k_ring<0, 0><<<grid, 64, smem>>>(p, tm, bytes, chunk, stages, 0, st, kEvictFirst); cudaEventRecord(e1);
+        finish("ring 64 MB after touch of 6 GB at 2 MB steps", grid, bytes); }
+      // back-to-back null + stream launches: what a launch costs when it queues behind another kernel
+      { uint8_t* p = region(4 * bytes); pre(); cudaEventRecord(e0);
+        for (int j = 0; j < 4; ++j) k_ring<0, 0><<<grid, 64, smem>>>(p + j * bytes, tm, bytes, chunk, stages, 0, st, kEvictFirst);
+        cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
+        printf("4 back-to-back ring launches of 64 MB: %.2f us per launch\n", ms * 1e3 / 4); }
+      { pre(); cudaEventRecord(e0); for (int j = 0; j < 16; ++j) k_null<<<nsm, 256>>>(st); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
+        printf("16 back-to-back null launches: %.2f us per launch\n", ms * 1e3 / 16); }
+    }
+    return 0;
+  }
   if (getenv("BURST4")) {
     // does the state the L2 flush leaves behind matter?  dirty lines (memset) vs clean lines (read sweep of another region)
     uint8_t* other; CK(cudaMalloc(&other, 512ull << 20)); CK(cudaMemset(other, 2, 512ull << 20));
