@@ -169,13 +169,26 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
+L2_BYTES = 126 << 20
+
+
 class Point:
-    """One (shape, batch, sparsity) measurement set-up on the current device."""
+    """One (shape, batch, sparsity) measurement set-up on the current device.
+
+    L2 policy of the timed region ("inputs larger than L2"): the steps run back to back over a
+    ROTATION of identical weight images (``layers``), image r with token batch r, sized so that
+    between two uses of one image the other images stream at least twice the L2 capacity --
+    every weight byte of a step comes out of HBM, and the lines it evicts are clean, as they are
+    when a model's layers follow each other.  (A memset flush leaves the L2 full of dirty lines
+    whose write-back rides on every miss of the next kernel: tools/micro/burst.cu measures a
+    64 MB burst at 14.4 us after a memset against 12.2 us after a read sweep.)"""
 
     RING = 8
 
-    def __init__(self, skb, torch, layer, shape, B):
+    def __init__(self, skb, torch, layer, shape, B, make_layer=None):
         self.skb, self.torch, self.layer, self.shape, self.B = skb, torch, layer, shape, B
+        self.make_layer = make_layer
+        self.layers = [layer]
         D = shape["D"]
         self.x_host = [make_tokens(B, D, 2 + i) for i in range(self.RING)]
         self.x_ring = [torch.from_numpy(x).cuda() for x in self.x_host]
@@ -183,6 +196,18 @@ class Point:
         self.y = torch.empty((B, D), dtype=torch.float32, device="cuda")
         self.flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
         layer.reserve(B)
+
+    def rotation(self, bytes_per_step):
+        """Grow the rotation so that (R - 1) * bytes_per_step >= 2 * L2 (bounded by memory)."""
+        want = 1 + int(np.ceil(2.0 * L2_BYTES / max(1.0, bytes_per_step)))
+        free, _ = self.torch.cuda.mem_get_info()
+        room = int((free - (8 << 30)) // max(1, self.layer.weight_bytes))
+        want = max(1, min(want, 1 + max(0, room), 16))
+        while len(self.layers) < want and self.make_layer is not None:
+            lay = self.make_layer(self.shape)
+            lay.reserve(self.B)
+            self.layers.append(lay)
+        return len(self.layers)
 
     def bytes_for(self, s):
         """Exact algorithmic bytes per ring slot (one capture forward each; untimed)."""
@@ -195,41 +220,93 @@ class Point:
                                          rep.masks.shared if S else None))
         return out
 
-    def _enqueue(self, s, flags=0):
+    def _enqueue(self, s, flags=0, layer=None, x=None):
         S = self.shape["S"]
+        layer = layer if layer is not None else self.layer
+        x = x if x is not None else self.x
         if isinstance(s, tuple):  # ("tau", value): the threshold runtime path, forward_sparse
-            self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
-                                      mode=self.skb.MODE_THRESHOLD, tau=s[1], flags=flags,
-                                      stream=self.torch.cuda.current_stream().cuda_stream or 1)
+            layer.forward_device(x.data_ptr(), self.y.data_ptr(), self.B,
+                                 mode=self.skb.MODE_THRESHOLD, tau=s[1], flags=flags,
+                                 stream=self.torch.cuda.current_stream().cuda_stream or 1)
             return
-        self.layer.forward_device(self.x.data_ptr(), self.y.data_ptr(), self.B,
-                                  mode=self.skb.MODE_TOPK, s_routed=s, s_shared=s if S else 0.0,
-                                  flags=flags,
-                                  # NULL would mean "the layer's own stream": name torch's
-                                  # default stream explicitly (cudaStreamLegacy == 0x1)
-                                  stream=self.torch.cuda.current_stream().cuda_stream or 1)
+        layer.forward_device(x.data_ptr(), self.y.data_ptr(), self.B,
+                             mode=self.skb.MODE_TOPK, s_routed=s, s_shared=s if S else 0.0,
+                             flags=flags,
+                             # NULL would mean "the layer's own stream": name torch's
+                             # default stream explicitly (cudaStreamLegacy == 0x1)
+                             stream=self.torch.cuda.current_stream().cuda_stream or 1)
 
-    def time_device(self, s, steps, warmup, use_graph=True):
-        """Per-step CUDA-event times (ms) of the device entry point; L2 flushed and the token
-        batch rotated between steps, both outside the per-step event pair."""
+    def time_device(self, s, steps, warmup, use_graph=True, flags=0):
+        """Milliseconds per step of the device entry point: `steps` forwards back to back inside
+        ONE CUDA-event pair, rotating over the weight images (see the class comment).  Returns
+        (ms_per_step, graphed)."""
         torch = self.torch
-        graph = None
+        R = len(self.layers)
+        xs = [self.x_ring[r % self.RING] for r in range(R)]
+        single, full = None, None
         if use_graph:
             try:
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(side):
-                    self._enqueue(s)  # warm (module load, attribute set) before capture
+                    for r in range(R):  # warm (module load, attribute set) before capture
+                        self._enqueue(s, flags, self.layers[r], xs[r])
                 torch.cuda.current_stream().wait_stream(side)
                 torch.cuda.synchronize()
-                graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph):
-                    self._enqueue(s)
+                single = []
+                for r in range(R):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        self._enqueue(s, flags, self.layers[r], xs[r])
+                    single.append(g)
+                if R > 1:
+                    full = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(full):
+                        for r in range(R):
+                            self._enqueue(s, flags, self.layers[r], xs[r])
             except Exception as exc:  # capture unsupported: direct launches
                 print(f"[bench] CUDA graph capture failed ({exc}); timing direct launches",
                       file=sys.stderr)
-                graph = None
+                single, full = None, None
                 torch.cuda.synchronize()
+
+        def run(n):
+            i = 0
+            while i < n:
+                if full is not None and n - i >= R:
+                    full.replay()
+                    i += R
+                    continue
+                r = i % R
+                if single is not None:
+                    single[r].replay()
+                else:
+                    self._enqueue(s, flags, self.layers[r], xs[r])
+                i += 1
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.flush.zero_()
+        run(-(-max(warmup, R) // R) * R)  # whole rotations, so that the timed run starts at image 0
+        e0.record()
+        run(steps)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps, single is not None
+
+    def time_isolated(self, s, steps, warmup):
+        """The same forward timed alone: one CUDA-event pair per step around a graph replay on an
+        idle GPU, 512 MiB memset before each (dirty L2).  Includes the ~5 us an isolated launch
+        costs between two events; reported beside the back-to-back figure."""
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._enqueue(s)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self._enqueue(s)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(steps)]
         for i in range(warmup + steps):
@@ -237,14 +314,11 @@ class Point:
             self.flush.zero_()
             if i >= warmup:
                 ev[i - warmup][0].record()
-            if graph is not None:
-                graph.replay()
-            else:
-                self._enqueue(s)
+            graph.replay()
             if i >= warmup:
                 ev[i - warmup][1].record()
         torch.cuda.synchronize()
-        return [a.elapsed_time(b) for a, b in ev], graph is not None
+        return float(np.mean([a.elapsed_time(b) for a, b in ev]))
 
     def time_stages(self, s, steps, warmup):
         """Per-stage CUDA-event times (ms, mean over steps), stages serialised (no PDL)."""
@@ -412,8 +486,9 @@ def run_ours(args):
         return skb.MoELayerWeights.generate_synthetic(cfg, SEED, SCALE, device=local)
 
     layer = mk_layer(shape)
-    pt = Point(skb, torch, layer, shape, B)
+    pt = Point(skb, torch, layer, shape, B, make_layer=mk_layer)
     bytes_ring = pt.bytes_for(s)
+    n_rot = pt.rotation(float(np.mean([b["total"] for b in bytes_ring])))
 
     sampler = ClockSampler(local)
     if rank == 0:
@@ -423,11 +498,11 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    times, graphed = pt.time_device(s, args.steps, args.warmup, use_graph=not args.no_graph)
+    ms_dev, graphed = pt.time_device(s, args.steps, args.warmup, use_graph=not args.no_graph)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    total_ms = float(sum(times))
+    total_ms = ms_dev * args.steps
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -444,6 +519,9 @@ def run_ours(args):
         # decode batches: the whole layer is ONE persistent launch (decode_fused_kernel); its
         # algorithmic bytes are the layer's, its duration the single stage the library reports
         dom, dom_name, dom_bytes = "gateup", "decode_fused_kernel", mean_bytes["total"]
+        stages = dict(stages)
+        stages["gateup_isolated_launch"] = stages["gateup"]
+        stages["gateup"] = ms_per_step  # the launch IS the step: its back-to-back duration
     else:
         dom = max(("gateup", "down"), key=lambda k: stages[k])
         dom_name = {"gateup": "grouped_tc_kernel<TN,0> (gate/up + SwiGLU)",
@@ -490,6 +568,8 @@ def run_ours(args):
                     "kernel_ms": round(stages[dom], 5),
                     "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
     layer_gbs = mean_bytes["total"] / (ms_per_step * 1e-3) / 1e9
+    # the same step timed alone after a memset flush (what round 1 reported)
+    iso_ms = pt.time_isolated(s, max(10, min(args.steps, 50)), 3)
 
     # ---- end to end through the host-buffer entry point ----
     e2e_steps = max(10, min(args.steps, 100))
@@ -504,74 +584,66 @@ def run_ours(args):
 
     # ---- sparsity sweep on this workload + the north-star point ----
     sweep = []
+
+    def entry(point, sh, bb, ss, br=None, flags=0, **extra):
+        br = br if br is not None else point.bytes_for(ss)
+        tot = float(np.mean([b["total"] for b in br]))
+        point.rotation(tot)
+        m, _ = point.time_device(ss, sw_steps, 3, use_graph=not args.no_graph, flags=flags)
+        return {"workload": sh["name"], "batch": bb, "sparsity": ss, "ms_per_step": round(m, 5),
+                "tokens_per_s": round(bb / (m * 1e-3), 1), "bytes_alg": int(tot),
+                "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
+                "weight_images_in_rotation": len(point.layers), **extra}
+
     if not args.no_sweep and rank == 0:
         sw_steps = max(20, min(args.steps, 100))
         for ss in SWEEP_S:
-            br = bytes_ring if ss == s else pt.bytes_for(ss)
-            tms, _ = pt.time_device(ss, sw_steps, 3, use_graph=not args.no_graph)
-            m = float(np.mean(tms))
-            tot = float(np.mean([b["total"] for b in br]))
-            sweep.append({"workload": shape["name"], "batch": B, "sparsity": ss,
-                          "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
-                          "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
-                          "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+            sweep.append(entry(pt, shape, B, ss, bytes_ring if ss == s else None))
+        # the 1e-2 (bf16) parity mode: h rounded to bf16 before the down projection
+        sweep.append(entry(pt, shape, B, s, bytes_ring, flags=skb.FLAG_BF16_H,
+                           accumulation="bf16 h (1e-2 parity mode, SKB_FLAG_BF16_H)"))
         # the threshold runtime path (forward_sparse) on the same workload,
         # tau = the reference's calibrate_tau for a 0.5 target on these synthetic weights
         if args.workload in THRESHOLD_TAU:
             tau = THRESHOLD_TAU[args.workload]
-            tms, _ = pt.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
-            m = float(np.mean(tms))
+            m, _ = pt.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
             rep = skb.forward_sparse(layer, pt.x_host[0], tau)
-            entry = {"workload": shape["name"], "batch": B, "mode": "threshold (forward_sparse)",
-                     "tau": tau, "achieved_routed_sparsity": round(rep.achieved_routed_sparsity, 4),
-                     "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
-                     "tiles_skipped_frac": round(rep.tiles_skipped / max(1, rep.tiles_total), 4)}
+            ent = {"workload": shape["name"], "batch": B, "mode": "threshold (forward_sparse)",
+                   "tau": tau, "achieved_routed_sparsity": round(rep.achieved_routed_sparsity, 4),
+                   "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
+                   "tiles_skipped_frac": round(rep.tiles_skipped / max(1, rep.tiles_total), 4)}
             if not args.no_cpu and world == 1:
-                entry["cpu_reference"] = cpu_reference_sparse(shape, B, tau)
-            sweep.append(entry)
+                ent["cpu_reference"] = cpu_reference_sparse(shape, B, tau)
+            sweep.append(ent)
         # the other batch sizes of this workload's range (configs[1]: batch 1-256), s = 0.5
         for bb in (1, 16, 64):
             if bb == B:
                 continue
-            pb = Point(skb, torch, layer, shape, bb)
-            br = pb.bytes_for(0.5)
-            tms, _ = pb.time_device(0.5, sw_steps, 3, use_graph=not args.no_graph)
-            m = float(np.mean(tms))
-            tot = float(np.mean([b["total"] for b in br]))
-            sweep.append({"workload": shape["name"], "batch": bb, "sparsity": 0.5,
-                          "ms_per_step": round(m, 5), "tokens_per_s": round(bb / (m * 1e-3), 1),
-                          "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
-                          "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+            pb = Point(skb, torch, layer, shape, bb, make_layer=mk_layer)
+            pb.layers = list(pt.layers)
+            for lay in pb.layers:
+                lay.reserve(bb)
+            sweep.append(entry(pb, shape, bb, 0.5))
+            pt.layers = list(pb.layers)  # keep images the larger rotation added
             del pb
         if args.workload != "olmoe" or B != 1:
             sh = WORKLOADS["olmoe"]
             l2 = mk_layer(sh)
-            p2 = Point(skb, torch, l2, sh, 1)
+            p2 = Point(skb, torch, l2, sh, 1, make_layer=mk_layer)
             for ss in SWEEP_S:
-                br = p2.bytes_for(ss)
-                tms, _ = p2.time_device(ss, sw_steps, 3, use_graph=not args.no_graph)
-                m = float(np.mean(tms))
-                tot = float(np.mean([b["total"] for b in br]))
-                sweep.append({"workload": sh["name"], "batch": 1, "sparsity": ss,
-                              "ms_per_step": round(m, 5), "tokens_per_s": round(1 / (m * 1e-3), 1),
-                              "bytes_alg": int(tot),
-                              "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
-                              "layer_frac_of_hbm_roofline":
-                                  round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
-                              **({"north_star_point": True} if ss == 0.5 else {})})
-            # decode batch sizes on the same shape (the single persistent launch), s = 0.5
+                e = entry(p2, sh, 1, ss)
+                if ss == 0.5:
+                    e["north_star_point"] = True
+                    e["ms_per_step_isolated_launch_dirty_l2"] = round(p2.time_isolated(ss, sw_steps, 3), 5)
+                sweep.append(e)
+            # decode batch sizes on the same shape, s = 0.5
             for bb in (2, 4, 8, 16):
-                pb = Point(skb, torch, l2, sh, bb)
-                br = pb.bytes_for(0.5)
-                tms, _ = pb.time_device(0.5, sw_steps, 3, use_graph=not args.no_graph)
-                m = float(np.mean(tms))
-                tot = float(np.mean([b["total"] for b in br]))
-                sweep.append({"workload": sh["name"], "batch": bb, "sparsity": 0.5,
-                              "ms_per_step": round(m, 5), "tokens_per_s": round(bb / (m * 1e-3), 1),
-                              "bytes_alg": int(tot),
-                              "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
-                              "layer_frac_of_hbm_roofline":
-                                  round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4)})
+                pb = Point(skb, torch, l2, sh, bb, make_layer=mk_layer)
+                pb.layers = list(p2.layers)
+                for lay in pb.layers:
+                    lay.reserve(bb)
+                sweep.append(entry(pb, sh, bb, 0.5))
                 del pb
             del p2, l2
 
@@ -593,11 +665,15 @@ def run_ours(args):
                        "sparsity": s, "batch_per_gpu": B,
                        "weights": f"generate_synthetic(seed={SEED}, scale={SCALE}) as bf16 image",
                        "parallelism": "single GPU" if world == 1 else f"token-sharded replicas x{world}",
-                       "l2": "512 MiB memset between steps (outside the per-step event pair) + "
-                             "ring of 8 token batches",
+                       "l2": f"inputs larger than L2: steps rotate over {n_rot} identical weight "
+                             f"images ({n_rot - 1} x {int(mean_bytes['total']) >> 20} MB of other "
+                             "weights stream between two uses of an image; L2 = 126 MB), image r "
+                             "with token batch r",
+                       "timing": "steps back to back inside one CUDA-event pair",
                        "launch": "CUDA graph replay" if graphed else "direct launches + PDL",
                        "accumulation": "fp32 (h kept fp32; 1e-5 parity mode)"},
             "layer_gbs": round(layer_gbs, 1), "layer_frac_of_hbm_roofline": round(layer_gbs / hbm_peak, 4),
+            "ms_per_step_isolated_launch_dirty_l2": round(iso_ms, 5),
             "bytes_alg_per_step": int(mean_bytes["total"]),
             "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
             "launches_per_step": int(launches_per_step), "clocks": clocks,

@@ -68,7 +68,7 @@ constexpr int kDecMaxB = 8;
 constexpr int kDecTokens = 16;             // token stride of the row tables and of hc / part
 constexpr int kKBox = 4;                   // K blocks per ring stage = consumer warps
 constexpr int kStageBytes = kKBox * 32 * 128;  // 16 KB: 32 rows x 64 bf16 per K block
-constexpr int kMaxStages = 12;
+constexpr int kMaxStages = 8;
 constexpr int kMinStages = 5;  // the exact-chain ring of the chain CTAs lives in the stage ring
 constexpr int kHistBins = 512;
 constexpr int kHistBase = (135 << 3) - (kHistBins - 1);  // top bin = |h| >= 2^8
@@ -100,17 +100,19 @@ enum {
 };
 
 struct DecSmem {
-  int ring, chain, xs, gpart, keys, lst, hist, mlist, scr, gred, rowtab, uidx, ulist, cande, cmask,
-      plist, rscr, bars, misc, total;
+  int ring, chain, gbuf, xs, gpart, keys, lst, hist, mlist, scr, gred, rowtab, uidx, ulist, cande,
+      cmask, plist, rscr, bars, misc, total;
 };
 constexpr int kNumBars = 2 * kMaxStages + kChStages;
-__host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax, int tb, int Dp) {
+__host__ __device__ inline DecSmem dec_smem_layout(int stages, int gb_rows, int nmax, int tb, int Dp) {
   DecSmem m;
   const int nmax_pad = round_up(nmax, 256);
   int o = 0;
   m.ring = o;
   o += stages * kStageBytes;
   m.chain = m.ring;  // chain CTAs take no gate/up pieces
+  m.gbuf = o;        // gb_rows rows of W_down staged by cp.async for the gather
+  o += gb_rows * Dp * 2;
   m.xs = o;  // bf16 token rows [tb][Dp]
   o += round_up(tb * Dp * 2, 128);
   m.gpart = o;  // [2][4 warps][tb][32] partial gate/up sums of a piece
@@ -152,10 +154,24 @@ __host__ __device__ inline DecSmem dec_smem_layout(int stages, int nmax, int tb,
 // 1 KB alignment slack
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;
 inline int dec_tb_for(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : 8)); }
-inline int dec_stages_for(int nmax, int tb, int Dp) {
-  const DecSmem z = dec_smem_layout(0, nmax, tb, Dp);
-  int s = (kSmemBudget - z.total) / kStageBytes;
-  return s > kMaxStages ? kMaxStages : s;
+// Split of what the fixed regions leave: a staging buffer of up to 80 KB of gathered W_down rows
+// and kMinStages..kMaxStages ring stages (deeper rings only lengthen every other request's queue:
+// 96 KB in flight per SM already saturates HBM, tools/micro/burst.cu).
+struct DecPlan {
+  int stages, gb_rows;
+};
+constexpr int kGbufMax = 80 * 1024;
+inline DecPlan dec_plan(int nmax, int tb, int Dp) {
+  const int room = kSmemBudget - dec_smem_layout(0, 0, nmax, tb, Dp).total;
+  int st = (room - kGbufMax) / kStageBytes;
+  if (st > kMaxStages) st = kMaxStages;
+  if (st < kMinStages) st = kMinStages;
+  int gb = room - st * kStageBytes;
+  if (gb > kGbufMax) gb = kGbufMax;
+  DecPlan p;
+  p.stages = st;
+  p.gb_rows = gb > 0 ? gb / (Dp * 2) : 0;
+  return p;
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -235,22 +251,19 @@ __device__ __forceinline__ void tables_wait_producer() {
 __device__ __forceinline__ void tables_wait_consumers() {
   asm volatile("bar.sync 4, %0;" ::"n"(kDThreads + kGThreads) : "memory");
 }
-// whole rows of W_down into L2 ahead of the loads that consume them (TMA engine, no registers)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 
 }  // namespace
 
 #ifdef SKB_DEBUG_TIMING
-__device__ long long g_dec_dbg[160 * 24];
+__device__ long long g_dec_dbg[160 * 32];
 __device__ __forceinline__ long long dec_gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// stamp i of this CTA, by thread `thr`
-#define DEC_STAMP(thr, i) do { if (threadIdx.x == (thr)) g_dec_dbg[blockIdx.x * 24 + (i)] = dec_gtime(); } while (0)
+// stamp i of this CTA, by thread `thr`: the SM's cycle counter (reading %globaltimer costs about a
+// microsecond); stamp 0 records {globaltimer, clock64} once, which places the CTA on the common axis
+#define DEC_STAMP(thr, i) do { if (threadIdx.x == (thr)) { if ((i) == 0) { g_dec_dbg[blockIdx.x * 32] = dec_gtime(); g_dec_dbg[blockIdx.x * 32 + 31] = clock64(); } else g_dec_dbg[blockIdx.x * 32 + (i)] = clock64(); } } while (0)
 extern "C" void skb_debug_dec(long long* out) { cudaMemcpyFromSymbol(out, g_dec_dbg, sizeof(g_dec_dbg)); }
 #else
 #define DEC_STAMP(thr, i) do { } while (0)
@@ -265,7 +278,7 @@ struct DecodeArgs {
   int sel_mode, n_off_r, n_off_s;
   const uint8_t* mask_r;
   const uint8_t* mask_s;
-  int CM, CH, capture, stages, ND, DS;
+  int CM, CH, capture, stages, gb_rows, ND, DS;
   int n_ch;  // dedicated chain CTAs (the last n_ch of the grid): no gate/up pieces, no P2 units
   uint2* p0;  // [B][E][ND][2] of {bits, epoch}: partial fast logit and partial sum of |products|
   float* logits;
@@ -291,9 +304,9 @@ __device__ __forceinline__ float ord2f(uint32_t k) {
 }
 
 // Candidate experts of one token (one warp): every expert whose interval [lf - m, lf + m] reaches
-// the K-th largest lower end.  pf[e] = {fast logit, sum of |products|} of the token (the slice
-// partials summed in slice order -- every CTA forms the same sums, hence the same candidate
-// sets).  Returns true when the bound cannot be used (non-finite values, the exp-underflow
+// the K-th largest lower end.  pf[e * stride + j] = {fast logit, sum of |products|} partials of
+// the token's `stride` d_model slices, summed here in slice order (every CTA forms the same
+// sums, hence the same candidate sets).  Returns true when the bound cannot be used (non-finite values, the exp-underflow
 // region, or more than CM candidates): the caller then waits for the exact routing.
 // VPL = experts per lane.
 template <int VPL>
@@ -308,9 +321,14 @@ __device__ __forceinline__ bool cand_token(const float2* pf, int stride, int E, 
   for (int i = 0; i < VPL; ++i) {
     const int e = i * 32 + lane;
     if (e < E) {
-      const float2 v = pf[static_cast<size_t>(e) * stride];
-      const float f = v.x;
-      const float m = v.y * mfac + 2e-5f;
+      float f = 0.0f, sa = 0.0f;  // slice partials summed in slice order
+#pragma unroll 1
+      for (int j = 0; j < stride; ++j) {
+        const float2 v = pf[static_cast<size_t>(e) * stride + j];
+        f = __fadd_rn(f, v.x);
+        sa = __fadd_rn(sa, v.y);
+      }
+      const float m = sa * mfac + 2e-5f;
       lo[i] = f2ord(f - m);
       hi[i] = f + m;
       mxk = max(mxk, f2ord(f));
@@ -352,36 +370,10 @@ __device__ __forceinline__ bool cand_token(const float2* pf, int stride, int E, 
   return bad;
 }
 
-// The surviving W_down rows lst[0..m) of one unit, dealt to G row groups (group g takes rows
-// g, g + G, ...), 16 loads of 16 bytes in flight per thread; thread l of a group owns the column
-// octets l, l + 256, ... of a row.  `keys` holds the row's activations (float bits).
-template <int NT>
-__device__ __forceinline__ void gather_rows(const __nv_bfloat16* wb, int Dp, int LPR,
-                                            const uint16_t* lst, int m, const uint32_t* keys, int G,
-                                            int g, int l, float (&acc)[NT][8]) {
-  constexpr int RB = 16 / NT;
-#pragma unroll 1
-  for (int k0 = g; k0 < m; k0 += RB * G) {
-    uint4 v[RB][NT];
-    float hv[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const int k = k0 + r * G;
-      const bool ok = k < m;
-      const int idx = ok ? lst[k] : 0;
-      hv[r] = ok ? __uint_as_float(keys[idx]) : 0.0f;
-      const uint4* rp = reinterpret_cast<const uint4*>(wb + static_cast<size_t>(idx) * Dp);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int c8 = nt * 256 + l;
-        v[r][nt] = (ok && c8 < LPR) ? ld_stream_u4(rp + c8) : make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) fma8(v[r][nt], hv[r], acc[nt]);
-  }
+// the general search behind the histogram pick (huge pivot buckets only): out of line, so that the
+// path every launch takes stays short
+__device__ __noinline__ RowPick kary_pick_cold(const uint32_t* keys, int n, int n_off, SelScratch& sc) {
+  return sel_kary_pick<SelDRole>(keys, n, n_off, sc);
 }
 
 template <int TB>
@@ -391,7 +383,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
   uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   const uint32_t sm_u32 = smem_u32(sm);
   const int nmax = a.N > a.S ? a.N : a.S;
-  const DecSmem L = dec_smem_layout(a.stages, nmax, TB, a.Dp);
+  const DecSmem L = dec_smem_layout(a.stages, a.gb_rows, nmax, TB, a.Dp);
   int16_t* rowtab = reinterpret_cast<int16_t*>(sm + L.rowtab);
   int16_t* uidx = reinterpret_cast<int16_t*>(sm + L.uidx);
   int16_t* ulist = reinterpret_cast<int16_t*>(sm + L.ulist);
@@ -431,6 +423,11 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
     }
   }
   for (int e = tid; e < kDecMaxE; e += kDecThreads) cmask[e] = 0u;
+  {
+    // row table: -1 = (expert, token) is not a candidate pair; at most B * CM union experts
+    uint32_t* rt32 = reinterpret_cast<uint32_t*>(rowtab);
+    for (int i = tid; i < (kDecMaxB * 20 + 1) * 8; i += kDecThreads) rt32[i] = 0xffffffffu;
+  }
   __syncthreads();
 
   const int NB = a.Np / kNeuronBlock, NBs = a.has_shared ? a.Sp / kNeuronBlock : 0;
@@ -763,22 +760,25 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
     // ---- P0: fast logits of (expert, d_model slice) units ----
     const int ND = a.ND, DS = a.DS;
     {
-      float* red = gred;  // [8 warps][4 tokens][2]
+      constexpr int TT = TB < 4 ? TB : 4;  // tokens per pass
+      float* red = gred;  // [8 warps][TT tokens][2]
 #pragma unroll 1
       for (int unit = bid; unit < E * ND; unit += grid) {
         const int e = unit / ND, j = unit % ND;
         const int d0 = j * DS, d1 = min(D, d0 + DS);
         const float* wr = a.router + static_cast<size_t>(e) * D;
 #pragma unroll 1
-        for (int t0 = 0; t0 < B; t0 += 4) {
-          float pl[4] = {0.0f, 0.0f, 0.0f, 0.0f}, pa[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int t0 = 0; t0 < B; t0 += TT) {
+          float pl[TT], pa[TT];
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt) pl[tt] = pa[tt] = 0.0f;
           if (vec_ok) {
             const float4* w4 = reinterpret_cast<const float4*>(wr);
 #pragma unroll 2
             for (int q = d0 / 4 + dtid; q < d1 / 4; q += kDThreads) {
               const float4 w = __ldg(w4 + q);
 #pragma unroll
-              for (int tt = 0; tt < 4; ++tt) {
+              for (int tt = 0; tt < TT; ++tt) {
                 if (t0 + tt < B) {
                   const float4 xv =
                       __ldg(reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t0 + tt) * D) + q);
@@ -798,7 +798,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
             for (int d = d0 + dtid; d < d1; d += kDThreads) {
               const float w = __ldg(wr + d);
 #pragma unroll
-              for (int tt = 0; tt < 4; ++tt) {
+              for (int tt = 0; tt < TT; ++tt) {
                 if (t0 + tt < B) {
                   const float xv = __ldg(a.x + static_cast<size_t>(t0 + tt) * D + d);
                   pl[tt] = fmaf(w, xv, pl[tt]);
@@ -808,24 +808,24 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
             }
           }
 #pragma unroll
-          for (int tt = 0; tt < 4; ++tt) {
+          for (int tt = 0; tt < TT; ++tt) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
               pl[tt] += __shfl_xor_sync(0xffffffffu, pl[tt], o);
               pa[tt] += __shfl_xor_sync(0xffffffffu, pa[tt], o);
             }
             if (lane == 0) {
-              red[(dwarp * 4 + tt) * 2 + 0] = pl[tt];
-              red[(dwarp * 4 + tt) * 2 + 1] = pa[tt];
+              red[(dwarp * TT + tt) * 2 + 0] = pl[tt];
+              red[(dwarp * TT + tt) * 2 + 1] = pa[tt];
             }
           }
           d_sync();
-          if (dtid < 4 && t0 + dtid < B) {
+          if (dtid < TT && t0 + dtid < B) {
             float s = 0.0f, sa = 0.0f;
 #pragma unroll
             for (int w = 0; w < kDThreads / 32; ++w) {
-              s += red[(w * 4 + dtid) * 2 + 0];
-              sa += red[(w * 4 + dtid) * 2 + 1];
+              s += red[(w * TT + dtid) * 2 + 0];
+              sa += red[(w * TT + dtid) * 2 + 1];
             }
             uint2* dst = a.p0 + ((static_cast<size_t>(t0 + dtid) * E + e) * ND + j) * 2;
             st_volatile_u2(dst, __float_as_uint(s), epoch);
@@ -870,25 +870,13 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         }
       }
       d_sync();
-      // slice partials summed in slice order, in place at slice 0
-      if (ND > 1) {
-        for (int i = dtid; i < B * E; i += kDThreads) {
-          float f = 0.0f, sa = 0.0f;
-#pragma unroll 1
-          for (int j = 0; j < ND; ++j) {
-            const float2 v = pf[i * ND + j];
-            f = __fadd_rn(f, v.x);
-            sa = __fadd_rn(sa, v.y);
-          }
-          pf[i * ND] = make_float2(f, sa);
-        }
-        d_sync();
-      }
+      DEC_STAMP(kWarpD0 * 32, 21);
       // margin = 2 * gamma_D * A, a little inflated for the rounding of A itself
-      const double u24 = 5.9604644775390625e-8;
-      const float mfac = static_cast<float>(2.02 * (D * u24) / (1.0 - D * u24));
-#pragma unroll 1
-      for (int t = dwarp; t < B; t += 8) {
+      const float u24 = 5.9604644775390625e-8f;
+      const float mfac = 2.02f * (D * u24) / (1.0f - D * u24);
+      DEC_STAMP(kWarpD0 * 32, 24);
+      if (dwarp < B) {
+        const int t = dwarp;
         const float2* pft = pf + static_cast<size_t>(t) * E * ND;
         bool bad;
         if (E <= 64)
@@ -899,6 +887,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
           bad = cand_token<8>(pft, ND, E, mfac, K, CM, t, cmask);
         if (bad && lane == 0) misc[1] = 1;
       }
+      DEC_STAMP(kWarpD0 * 32, 25);
       d_sync();
       if (misc[1] != 0) {
         // rare: the bound could not separate the candidates -- wait for the exact routing
@@ -909,43 +898,39 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         for (int i = dtid; i < B * K; i += kDThreads) atomicOr(&cmask[__ldcg(a.ids + i)], 1u << (i / K));
         d_sync();
       }
-      // union list (ascending expert id) by D warp 0
-      if (dwarp == 0) {
-        int run = 0;
+      DEC_STAMP(kWarpD0 * 32, 22);
+      // tables: warp t walks the experts once for token t -- position in the union of candidate
+      // experts (ascending id; every warp forms the same positions, warp 0 records them) and rank
+      // among the token's own candidates
+      {
+        const int t = dwarp;
+        const unsigned lt = (1u << lane) - 1u;
+        int run_u = 0, run_t = 0;
 #pragma unroll 1
         for (int base = 0; base < E; base += 32) {
           const int e = base + lane;
-          const bool f = e < E && cmask[e] != 0u;
-          const unsigned b = __ballot_sync(0xffffffffu, f);
-          const int pos = run + __popc(b & ((1u << lane) - 1u));
-          if (e < E) uidx[e] = f ? static_cast<int16_t>(pos) : static_cast<int16_t>(-1);
-          if (f) ulist[pos] = static_cast<int16_t>(e);
-          run += __popc(b);
-        }
-        if (lane == 0) misc[2] = run;
-      }
-      d_sync();
-      const int n_u = misc[2];
-      // per-token tables: row table column, candidate list and count
-#pragma unroll 1
-      for (int t = dwarp; t < kDecTokens; t += 8) {
-        for (int u = lane; u <= n_u; u += 32) rowtab[u * 16 + t] = -1;
-        __syncwarp();
-        if (t < B) {
-          int run = 0;
-#pragma unroll 1
-          for (int base = 0; base < E; base += 32) {
-            const int e = base + lane;
-            const bool f = e < E && ((cmask[e] >> t) & 1u);
-            const unsigned b = __ballot_sync(0xffffffffu, f);
+          const uint32_t cm = e < E ? cmask[e] : 0u;
+          const unsigned bu = __ballot_sync(0xffffffffu, cm != 0u);
+          const int upos = run_u + __popc(bu & lt);
+          if (t == 0 && e < E) {
+            uidx[e] = cm != 0u ? static_cast<int16_t>(upos) : static_cast<int16_t>(-1);
+            if (cm != 0u) ulist[upos] = static_cast<int16_t>(e);
+          }
+          if (t < B) {
+            const bool f = ((cm >> t) & 1u) != 0u;
+            const unsigned bt = __ballot_sync(0xffffffffu, f);
             if (f) {
-              const int r = run + __popc(b & ((1u << lane) - 1u));
-              rowtab[uidx[e] * 16 + t] = static_cast<int16_t>(t * CM + r);
+              const int r = run_t + __popc(bt & lt);
+              rowtab[upos * 16 + t] = static_cast<int16_t>(t * CM + r);
               cande[t * CM + r] = static_cast<int16_t>(e);
             }
-            run += __popc(b);
+            run_t += __popc(bt);
           }
-          if (lane == 0) ncand[t] = run;
+          run_u += __popc(bu);
+        }
+        if (lane == 0) {
+          if (t == 0) misc[2] = run_u;
+          if (t < B) ncand[t] = run_t;
         }
       }
       d_sync();
@@ -953,18 +938,30 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
       DEC_STAMP(kWarpD0 * 32, 2);
       // pair list in the order the experts finish: shared expert first, then union order
       if (dwarp == 0) {
+        const int n_u = misc[2];
         int run = 0;
         if (a.has_shared) {
           if (lane < B) plist[lane] = static_cast<int16_t>(n_u * 16 + lane);
           run = B;
         }
 #pragma unroll 1
-        for (int base = 0; base < n_u * 16; base += 32) {
-          const int i = base + lane;
-          const bool f = i < n_u * 16 && rowtab[i] >= 0;
-          const unsigned b = __ballot_sync(0xffffffffu, f);
-          if (f) plist[run + __popc(b & ((1u << lane) - 1u))] = static_cast<int16_t>(i);
-          run += __popc(b);
+        for (int base = 0; base < n_u; base += 32) {
+          const int u = base + lane;
+          uint32_t cm = u < n_u ? cmask[ulist[u]] : 0u;
+          const int cnt = __popc(cm);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+          }
+          int pos = run + incl - cnt;
+          while (cm != 0u) {
+            const int t = __ffs(cm) - 1;
+            cm &= cm - 1u;
+            plist[pos++] = static_cast<int16_t>(u * 16 + t);
+          }
+          run += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (lane == 0) misc[3] = run;
       }
@@ -1109,7 +1106,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
 #pragma unroll 1
             for (int i = dtid; i < n; i += kDThreads) keys_s[i] &= 0x7fffffffu;
             d_sync();
-            pk = sel_kary_pick<SelDRole>(keys_s, n, n_off, sel_sc);
+            pk = kary_pick_cold(keys_s, n, n_off, sel_sc);
             d_sync();
 #pragma unroll 1
             for (int i = dtid; i < n; i += kDThreads) keys_s[i] = __float_as_uint(__ldcg(hrow + i));
@@ -1181,63 +1178,91 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         d_sync();
         DEC_STAMP(kWarpD0 * 32, 12);
 
-        // ---- gather + partial ----
+        // ---- gather + partial: the unit's rows staged in shared memory by 16-byte cp.async
+        // copies (every row of a batch in flight at once, no registers held), then rolled FMA
+        // loops: thread l owns the column octets l, l + 256, ... ----
         const __nv_bfloat16* wb = routed ? a.wd + static_cast<size_t>(e) * a.Np * Dp : a.wd_shared;
-        // rows beyond the first batch of direct loads: into L2 now, so that the later batches do
-        // not pay a DRAM round trip each
-        for (int k = dtid; k < m; k += kDThreads)
-          bulk_prefetch_l2(wb + static_cast<size_t>(lst[k]) * Dp, static_cast<uint32_t>(Dp) * 2u);
         float* pout = a.part + (static_cast<size_t>(t * (CM + 1) + q) * CH + c) * Dp;
-        if (NT == 1) {
-          float acc[1][8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}};
-          if (lane_ok) gather_rows<1>(wb, Dp, LPR, lst, m, keys_s, G, g, l, acc);
-          if (G > 1) {
-            if (lane_ok) {
-              float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
-              d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
-              d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
-            }
-            d_sync();
-            for (int d = dtid; d < Dp; d += kDThreads) {
-              float sacc = gred[d];
-              for (int gg = 1; gg < G; ++gg) sacc = __fadd_rn(sacc, gred[gg * Dp + d]);
-              pout[d] = sacc;
-            }
-          } else if (lane_ok) {
-            float4* d4 = reinterpret_cast<float4*>(pout + l * 8);
-            d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
-            d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
-          }
-        } else if (NT == 2) {
-          float acc[2][8];
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
-          gather_rows<2>(wb, Dp, LPR, lst, m, keys_s, 1, 0, l, acc);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            const int c8 = nt * 256 + dtid;
-            if (c8 < LPR) {
-              float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
-              d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
-              d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
-            }
-          }
-        } else {
+        {
           float acc[4][8];
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
-          gather_rows<4>(wb, Dp, LPR, lst, m, keys_s, 1, 0, l, acc);
+          const uint4* gb = reinterpret_cast<const uint4*>(sm + L.gbuf);
+          const uint32_t gb_u32 = sm_u32 + L.gbuf;
+          const int RBS = a.gb_rows;
+          const int dr = kDThreads / LPR, dc = kDThreads % LPR;
+#pragma unroll 1
+          for (int k0 = 0; k0 < m; k0 += RBS) {
+            const int nr = min(RBS, m - k0);
+            {
+              int r = dtid / LPR, cc = dtid % LPR;
+#pragma unroll 1
+              while (r < nr) {
+                const __nv_bfloat16* src = wb + static_cast<size_t>(lst[k0 + r]) * Dp + cc * 8;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 gb_u32 + static_cast<uint32_t>(r * LPR + cc) * 16u),
+                             "l"(src)
+                             : "memory");
+                cc += dc;
+                r += dr;
+                if (cc >= LPR) {
+                  cc -= LPR;
+                  ++r;
+                }
+              }
+              asm volatile("cp.async.commit_group;" ::: "memory");
+              asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            d_sync();
+            if (NT == 1) {
+              // narrow rows: G row groups, group g takes rows g, g + G, ...
+              if (lane_ok) {
+#pragma unroll 2
+                for (int r = g; r < nr; r += G)
+                  fma8(gb[r * LPR + l], __uint_as_float(keys_s[lst[k0 + r]]), acc[0]);
+              }
+            } else {
+#pragma unroll 1
+              for (int r = 0; r < nr; ++r) {
+                const float hk = __uint_as_float(keys_s[lst[k0 + r]]);
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            const int c8 = nt * 256 + dtid;
-            if (c8 < LPR) {
-              float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
-              d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
-              d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+                for (int nt = 0; nt < 4; ++nt) {
+                  const int c8 = nt * kDThreads + dtid;
+                  if (c8 < LPR) fma8(gb[r * LPR + c8], hk, acc[nt]);
+                }
+              }
+            }
+            d_sync();  // the next batch overwrites the buffer
+          }
+          if (NT == 1) {
+            if (G > 1) {
+              if (lane_ok) {
+                float4* d4 = reinterpret_cast<float4*>(gred + static_cast<size_t>(g) * Dp + l * 8);
+                d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+                d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+              }
+              d_sync();
+              for (int d = dtid; d < Dp; d += kDThreads) {
+                float sacc = gred[d];
+                for (int gg = 1; gg < G; ++gg) sacc = __fadd_rn(sacc, gred[gg * Dp + d]);
+                pout[d] = sacc;
+              }
+            } else if (lane_ok) {
+              float4* d4 = reinterpret_cast<float4*>(pout + l * 8);
+              d4[0] = make_float4(acc[0][0], acc[0][1], acc[0][2], acc[0][3]);
+              d4[1] = make_float4(acc[0][4], acc[0][5], acc[0][6], acc[0][7]);
+            }
+          } else {
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int c8 = nt * kDThreads + dtid;
+              if (c8 < LPR) {
+                float4* d4 = reinterpret_cast<float4*>(pout + c8 * 8);
+                d4[0] = make_float4(acc[nt][0], acc[nt][1], acc[nt][2], acc[nt][3]);
+                d4[1] = make_float4(acc[nt][4], acc[nt][5], acc[nt][6], acc[nt][7]);
+              }
             }
           }
         }
@@ -1299,35 +1324,52 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
     }
     d_sync();
     DEC_STAMP(kWarpD0 * 32, 6);
-    const int RC = R * CH;
+    // Every thread takes one (output, slot, group of 8 chunks): one division chain per thread,
+    // its 8 partials in flight at once, summed in chunk order; then the groups of a slot in
+    // order, then the slots.  (Rolled and short: this code runs once per launch, out of a cold
+    // instruction cache.)
+    const int CG = (CH + 7) >> 3;
     const int D4 = Dp / 4;
     const int total4 = B * D4;
     constexpr int QB = 8;
-    float4* buf = reinterpret_cast<float4*>(work + 4096);  // [QB][R][CH]
-    float4* sj = buf + QB * RC;                            // [QB][R]
+    float4* sg = reinterpret_cast<float4*>(work + 4096);  // [QB][R][CG]
+    float4* sj = sg + QB * R * CG;                         // [QB][R]
     const bool y_vec = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0);
     const int q0 = static_cast<int>(static_cast<long long>(bid) * total4 / grid);
     const int q1 = static_cast<int>(static_cast<long long>(bid + 1) * total4 / grid);
 #pragma unroll 1
     for (int qb = q0; qb < q1; qb += QB) {
       const int nq = min(QB, q1 - qb);
-#pragma unroll 2
-      for (int idx = dtid; idx < nq * RC; idx += kDThreads) {
-        const int qi = idx / RC, rem = idx % RC;
-        const int j = rem / CH, c = rem % CH;
+#pragma unroll 1
+      for (int idx = dtid; idx < nq * R * CG; idx += kDThreads) {
+        const int cg = idx % CG, j = (idx / CG) % R, qi = idx / (CG * R);
         const int qq = qb + qi;
-        const int t = qq / D4, d4 = qq % D4;
+        const int t = qq / D4, d4 = qq - t * D4;
         const int r = srow[t * R + j];
-        buf[idx] = __ldcg(reinterpret_cast<const float4*>(
-            a.part + (static_cast<size_t>(t * (CM + 1) + r) * CH + c) * Dp + d4 * 4));
+        const float4* pp = reinterpret_cast<const float4*>(
+            a.part + (static_cast<size_t>(t * (CM + 1) + r) * CH + cg * 8) * Dp + d4 * 4);
+        const int nc = min(8, CH - cg * 8);
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = u < nc ? __ldcg(pp + static_cast<size_t>(u) * D4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 sacc = v[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) {
+          sacc.x = __fadd_rn(sacc.x, v[u].x);
+          sacc.y = __fadd_rn(sacc.y, v[u].y);
+          sacc.z = __fadd_rn(sacc.z, v[u].z);
+          sacc.w = __fadd_rn(sacc.w, v[u].w);
+        }
+        sg[idx] = sacc;
       }
       d_sync();
       DEC_STAMP(kWarpD0 * 32, 20);
       for (int idx = dtid; idx < nq * R; idx += kDThreads) {
-        const float4* pb = buf + static_cast<size_t>(idx) * CH;
+        const float4* pb = sg + static_cast<size_t>(idx) * CG;
         float4 sacc = pb[0];
 #pragma unroll 1
-        for (int c = 1; c < CH; ++c) {
+        for (int c = 1; c < CG; ++c) {
           const float4 pv = pb[c];
           sacc.x = __fadd_rn(sacc.x, pv.x);
           sacc.y = __fadd_rn(sacc.y, pv.y);
@@ -1392,7 +1434,8 @@ bool decode_fused_eligible(const Geometry& g, int B) {
   const int nmax = g.N > g.S ? g.N : g.S;
   return B >= 1 && B <= kDecMaxB && g.E <= kDecMaxE && g.K <= 16 && nmax <= kMaxN &&
          g.Dp <= 8192 && (g.Dp % 64) == 0 && g.E + g.K + 8 <= 288 &&
-         dec_stages_for(nmax, dec_tb_for(B), g.Dp) >= kMinStages;
+         dec_plan(nmax, dec_tb_for(B), g.Dp).stages >= kMinStages &&
+         dec_plan(nmax, dec_tb_for(B), g.Dp).gb_rows >= 2;
 }
 
 int decode_counter_words() { return kCtrWords; }
@@ -1402,7 +1445,7 @@ int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
   // Batch-invariant by design (B is ignored): one token's units fill the grid once.
   (void)B;
   const int R = g.K + (g.has_shared ? 1 : 0);
-  int ch = n_sms / (R + 1);  // room for one extra candidate per token in a single wave
+  int ch = 2 * n_sms / (R + 1);  // two waves of units: 16 rows per unit = one batch of loads
   int cap = keep_max / 8;  // at least ~8 rows per unit
   if (cap < 1) cap = 1;
   if (ch > cap) ch = cap;
@@ -1459,11 +1502,9 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   a.CM = decode_cand_rows(g.K);
   a.CH = d.CH;
   a.capture = d.capture ? 1 : 0;
-  a.stages = dec_stages_for(nmax, tb, g.Dp);
-  if (const char* es = getenv("SKB_DEC_STAGES")) {  // experiments only
-    const int v = atoi(es);
-    if (v >= kMinStages && v <= a.stages) a.stages = v;
-  }
+  const DecPlan plan = dec_plan(nmax, tb, g.Dp);
+  a.stages = plan.stages;
+  a.gb_rows = plan.gb_rows;
   {
     const int n_cu = ceil_div(g.E, 8) * ceil_div(d.B, 4);
     a.n_ch = n_cu < kMaxChainCtas ? n_cu : kMaxChainCtas;
@@ -1498,7 +1539,7 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   cfg.stream = ctx.stream;
   cfg.gridDim = dim3(n_sms);
   cfg.blockDim = dim3(kDecThreads);
-  cfg.dynamicSmemBytes = dec_smem_layout(a.stages, nmax, tb, g.Dp).total + 1024;
+  cfg.dynamicSmemBytes = dec_smem_layout(a.stages, a.gb_rows, nmax, tb, g.Dp).total + 1024;
   switch (tb) {
     case 1: launch_tb<1>(cfg, tmap_w3, a); break;
     case 2: launch_tb<2>(cfg, tmap_w3, a); break;

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle.pyoracle import Config, Weights
-from tests.helpers import SplitMix64, max_rel_diff, random_config
+from tests.helpers import SparseSynthModel, true_rel_err, SplitMix64, max_rel_diff, random_config
 
 pytestmark = pytest.mark.gpu
 
@@ -727,11 +727,33 @@ def test_fused_decode_falls_back_to_exact_routing_when_the_bound_cannot_decide(s
     np.testing.assert_array_equal(big.routes.ids, cap_big["ids"])
 
 
+def _check_outputs_vs_sparse_oracle(skb, oracle, shape, B, s, rep, x, n_sample, label):
+    """Outputs of `rep` against the double-precision scalar oracle (support.hpp:55-152) on the
+    routing and masks the device reports, for `n_sample` tokens; only the experts those tokens
+    route to are materialised (SplitMix64 jump-ahead).  Routing is checked for every token."""
+    E, K, D, N, S = shape
+    cfg = Config(E, K, D, N, S, True)
+    model = SparseSynthModel(oracle, cfg, 1, 0.05)
+    ids, wts = model.routing(x, K)
+    np.testing.assert_array_equal(rep.routes.ids, ids)
+    np.testing.assert_allclose(rep.routes.weights, wts, rtol=1e-6)
+    rng = np.random.default_rng(1)
+    sel = np.sort(rng.choice(B, size=min(B, n_sample), replace=False))
+    y = model.scalar_forward(x, ids, wts, rep.masks.routed, rep.masks.shared if S else None, tokens=sel)
+    err, rel = max_rel_diff(rep.outputs[sel], y), true_rel_err(rep.outputs[sel], y)
+    print(f"[{label}] E={E} K={K} D={D} N={N} S={S} B={B} s={s}: max_rel_diff={err:.3e} "
+          f"(reference metric, /max(1,|y|)), true relative error={rel:.3e}, max|y|={np.abs(y).max():.3f}")
+    assert err <= TOL_FP32_ACCUM
+    assert rel <= 10 * TOL_FP32_ACCUM
+
+
 @pytest.mark.parametrize("shape,B,s", [
+    ((64, 8, 2048, 1024, 0), 1, 0.5),       # OLMoE shape, the north-star point
     ((64, 8, 2048, 1024, 0), 4, 0.5),       # OLMoE shape, small decode batch
-    ((32, 4, 2880, 2880, 0), 2, 0.75),      # GPT-OSS-20B shape (two column tiles per W_down row)
+    ((32, 4, 2880, 2880, 0), 1, 0.5),       # GPT-OSS-20B shape, decode
+    ((32, 4, 2880, 2880, 0), 2, 0.75),      # (two column tiles per W_down row)
     ((256, 8, 2048, 512, 512), 8, 0.9),     # Qwen3.5-35B-A3B shape, R+S
-    ((8, 1, 5120, 8192, 8192), 3, 0.9),     # Llama-4-Maverick shape with 8 of its 128 experts:
+    ((8, 1, 5120, 8192, 8192), 2, 0.9),     # Llama-4-Maverick shape with 8 of its 128 experts:
                                             # 32 keys per thread, three column tiles per row
 ])
 def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
@@ -749,14 +771,33 @@ def test_fused_decode_full_shapes(skb, oracle, shape, B, s):
         for k in range(K):
             np.testing.assert_array_equal(
                 rep.masks.routed[t, k], oracle.mask_smallest(rep.h_routed[t, k], oracle.n_off(s, N)))
-    router = oracle.fill_symmetric(E * D, 1, 0, 0.05).reshape(E, D)
-    logits = np.stack([oracle.matvec(router, x[t]) for t in range(B)])
-    _, ids, wts = oracle.route(logits, K, True)
-    np.testing.assert_array_equal(rep.routes.ids, ids)
-    np.testing.assert_allclose(rep.routes.weights, wts, rtol=1e-6)
+    # outputs against the oracle (not against the repository's other kernels)
+    _check_outputs_vs_sparse_oracle(skb, oracle, shape, B, s, rep, x, n_sample=B, label="fused decode")
     staged = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None,
                                      flags=skb.FLAG_NO_FUSED_DECODE)
-    assert max_rel_diff(rep.outputs, staged.outputs) <= TOL_FP32_ACCUM
+    assert max_rel_diff(rep.outputs, staged.outputs) <= 2 * TOL_FP32_ACCUM  # two 1e-5 paths apart
+
+
+@pytest.mark.parametrize("shape,B,s,n_sample", [
+    ((32, 4, 2880, 2880, 0), 4096, 0.5, 6),       # configs[3] GPT-OSS-20B shape, prefill: the
+                                                  # automatic (paired, multi-wave) GEMM path
+    ((256, 8, 2048, 512, 512), 16, 0.5, 4),       # configs[2] shape, decode batch, R+S
+    ((128, 1, 5120, 8192, 8192), 1, 0.9, 1),      # configs[4] the FULL Llama-4-Maverick shape
+    ((128, 1, 5120, 8192, 8192), 64, 0.9, 4),     #   (43 GB device image), decode batches
+])
+def test_full_shape_outputs_vs_oracle(skb, oracle, shape, B, s, n_sample):
+    """BASELINE.json configs at full size through the automatic path choice: routing of every
+    token and the outputs of sampled tokens against the oracle."""
+    E, K, D, N, S = shape
+    cfg = Config(E, K, D, N, S, True)
+    layer = skb.MoELayerWeights.generate_synthetic(to_cfg(skb, cfg), 1, 0.05)
+    x = oracle.round_bf16(oracle.generate_tokens(B, D, 5))
+    lvl = skb.SparsityLevel(s)
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True)
+    keep = N - oracle.n_off(s, N)
+    assert np.all(rep.masks.routed.sum(axis=2) == keep)
+    _check_outputs_vs_sparse_oracle(skb, oracle, shape, B, s, rep, x, n_sample, label="automatic path")
+    layer.close()
 
 
 def test_pinned_output_buffers_are_written_in_place(skb, oracle):

@@ -331,3 +331,25 @@ def test_reference_error_codes(ref):
     assert ei.value.code == 2
     with pytest.raises(ValueError):
         RefLayer.synthetic(Config(4, 5, 8, 16), 1, 0.05)
+
+
+def test_sparse_synth_model_matches_the_full_oracle(oracle):
+    """The one-expert-at-a-time double-precision checker used by the full-shape GPU tests gives
+    the oracle's own answer on a shape small enough to materialise whole."""
+    from tests.helpers import SparseSynthModel
+    o = oracle
+    cfg = Config(8, 2, 48, 40, 24, True)
+    w_raw = o.generate_synthetic(cfg, 7, 0.1)
+    w = w_raw.rounded_bf16()
+    w.router = w_raw.router
+    x = o.round_bf16(o.generate_tokens(5, cfg.d_model, 3))
+    routed, shared = o.build_topk_masks(w, x, 0.5, 1)
+    y_ref, _, cap = o.forward(w, x, routed, shared, capture=True)
+    m = SparseSynthModel(o, cfg, 7, 0.1)
+    ids, wts = m.routing(x, cfg.top_k)
+    np.testing.assert_array_equal(ids, cap["ids"])
+    np.testing.assert_array_equal(wts, cap["weights"])
+    y = m.scalar_forward(x, ids, wts, routed.reshape(5, 2, 40), shared.reshape(5, 24), tokens=[0, 3, 4])
+    assert max_rel_diff(y, y_ref[[0, 3, 4]]) <= 1e-5
+    y_scalar = o.scalar_forward(w, x, routed, shared)
+    assert max_rel_diff(y, y_scalar[[0, 3, 4]]) <= 1e-6

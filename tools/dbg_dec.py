@@ -1,4 +1,4 @@
-import ctypes as C, numpy as np, sys
+import ctypes as C, numpy as np, sys, os
 sys.path.insert(0,'/root/repo')
 import paper_2605_08575_b200 as skb
 from paper_2605_08575_b200 import _lib
@@ -14,16 +14,30 @@ lvl=skb.SparsityLevel(0.5)
 ref=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None,flags=skb.FLAG_NO_FUSED_DECODE)
 import torch
 flush=torch.empty(512<<20,dtype=torch.uint8,device='cuda')
+ROT=int(os.environ.get('DBG_ROT','0'))  # >0: back-to-back launches rotating over ROT weight images (the bench's timed region)
+if ROT:
+    layers=[layer]+[skb.MoELayerWeights.generate_synthetic(cfg,1,0.05) for _ in range(ROT-1)]
+    xd=torch.from_numpy(x).cuda(); yd=torch.empty_like(xd)
+    for l in layers: l.reserve(B)
 for i in range(3):
-    flush.zero_(); torch.cuda.synchronize()
-    rep=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None)
+    (flush.zero_() if os.environ.get('DBG_DIRTY') else flush.sum()); torch.cuda.synchronize()
+    if ROT:
+        for j in range(4*ROT):
+            layers[j%ROT].forward_device(xd.data_ptr(), yd.data_ptr(), B, mode=skb.MODE_TOPK, s_routed=0.5, s_shared=0.5 if hs else 0.0, stream=1)
+        torch.cuda.synchronize()
+    rep=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None) if not ROT else ref
     print('launches', rep.launches, 'ref launches', ref.launches, 'maxdiff', float(np.abs(rep.outputs-ref.outputs).max()))
     if hasattr(L, 'skb_debug_dec'):
-        out=(C.c_longlong*(160*24))()
+        out=(C.c_longlong*(160*32))()
         L.skb_debug_dec(out)
-        t=np.array(list(out)).reshape(160,24)
-        names={14:'chain start',15:'chain end',0:'start',1:'p0 done',2:'tables',3:'tma issued',4:'g done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p3 barrier',7:'exit',10:'route done',11:'tma go',16:'x staged',17:'cons go',18:'piece1 done',19:'p3 tables',20:'p3 loaded'}
-        for k in (1,2,11,16,17,18,3,14,15,10,4,8,9,12,13,5,19,6,20,7):
+        t=np.array(list(out)).reshape(160,32)
+        # stamps are SM cycle counts: onto the common nanosecond axis through the {globaltimer, clock64} pair of stamp 0
+        clk0=t[:,31].copy(); gt0=t[:,0].copy()
+        for k in range(1,31):
+            nz=t[:,k]>0
+            t[nz,k]=gt0[nz]+((t[nz,k]-clk0[nz])/1.965).astype(np.int64)
+        names={14:'chain start',15:'chain end',0:'start',1:'p0 done',2:'tables',3:'tma issued',4:'g done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p3 barrier',7:'exit',10:'route done',11:'tma go',16:'x staged',17:'cons go',18:'piece1 done',19:'p3 tables',20:'p3 loaded',21:'polled',22:'cand done',23:'p3 pass1',24:'cand start',25:'cand tok'}
+        for k in (1,21,24,25,22,2,11,16,17,18,3,14,15,10,4,8,9,12,13,5,19,6,23,20,7):
             col=t[:148,k]-t[:148,0].min()
             col=col[t[:148,k]>0]
             if col.size: print(f'  {names[k]:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}')

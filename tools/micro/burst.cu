@@ -225,6 +225,28 @@ __global__ void k_touch(const uint8_t* __restrict__ base, size_t bytes, size_t s
   if (acc == 0x12345678u) *sink = acc;
 }
 
+
+// ---- latency: one warp per CTA, `hops` dependent 16-byte loads at a 1 MB + 4 KB stride (cold lines, cold pages) ----
+__global__ void k_chase(const uint8_t* __restrict__ base, size_t span, int hops, unsigned* sink, Stamp* st, long long* per) {
+  if (threadIdx.x == 0) {
+    st[blockIdx.x].t0 = gtime();
+    size_t off = ((size_t)blockIdx.x * 7919 * 4096) % span;
+    unsigned acc = 0;
+    long long t_prev = gtime();
+    for (int h = 0; h < hops; ++h) {
+      uint4 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(base + off));
+      acc += v.x;
+      off = (off + (1u << 20) + 4096 + (acc & 0)) % span;
+      const long long t = gtime();
+      if (blockIdx.x == 0 && h < 16) per[h] = t - t_prev;
+      t_prev = t;
+    }
+    if (acc == 0x12345678u) *sink = acc;
+    st[blockIdx.x].t1 = gtime();
+  }
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int main() {
@@ -267,6 +289,25 @@ int main() {
   char name[160];
 
 
+
+  if (getenv("BURST6")) {
+    // cold-DRAM load latency seen by one thread, after an L2 flush by memset (dirty lines) and by a read sweep (clean)
+    uint8_t* other; CK(cudaMalloc(&other, 512ull << 20)); CK(cudaMemset(other, 2, 512ull << 20));
+    for (int rep = 0; rep < 3; ++rep)
+      for (int mode = 0; mode < 2; ++mode)
+        for (int grid : {1, 148}) {
+          CK(cudaMemsetAsync(st, 0, sizeof(Stamp) * 1024));
+          if (mode == 0) CK(cudaMemsetAsync(flush, 0, 512ull << 20));
+          else k_ldg<16, 0><<<296, 512>>>((const uint4*)other, (512ull << 20) / 16, sink, st + 512);
+          cudaEventRecord(e0); k_chase<<<grid, 32>>>(buf, (size_t)4 << 30, 8, sink, st, pr); cudaEventRecord(e1);
+          CK(cudaEventSynchronize(e1));
+          long long h[8]; CK(cudaMemcpy(h, pr, sizeof(h), cudaMemcpyDeviceToHost));
+          printf("chase %s grid %3d: hops (ns)", mode == 0 ? "after memset    " : "after read sweep", grid);
+          for (int i = 0; i < 8; ++i) printf(" %lld", h[i]);
+          printf("\n");
+        }
+    return 0;
+  }
   if (getenv("BURST5")) {
     // is the ~3 us ramp of a cold burst address translation?  Same 64 MB ring stream, preceded (in its own launch,
     // after the L2 flush) by a touch of one word per 2 MB / 64 KB / 4 KB of the region
