@@ -512,6 +512,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     if (budget) dense_down = true;
   }
   const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
+  // 1e-5 parity mode: the tensor-core GEMMs fold long contractions chunk by chunk (gateup.cu)
+  const bool precise = !(a->flags & SKB_FLAG_BF16_H);
 
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
@@ -586,7 +588,9 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   int tn = 16;
   {
     const double want = 1.5 * static_cast<double>(BK) / g.E;
-    const int cap = dense_down ? 128 : 256;
+    // (and when the fp32-accumulation mode folds long contractions chunk by chunk: its master
+    // accumulator shares the TMEM with two chunk buffers, gateup.cu)
+    const int cap = (dense_down || precise) ? 128 : 256;
     while (tn < cap && tn < want) tn <<= 1;
   }
   // decode: token-indexed tiles built inside the router kernel (no expert-sorted token copy)
@@ -658,7 +662,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   else
     launches += launch_gateup_tc(ctx, &L->tmap_w, token_tiles ? &L->tmap_xb : &L->tmap_x[tn_idx],
                                  tn, L->disp, max_tiles, g, L->d_h, token_tiles,
-                                 sel_mode == kSelectThreshold ? L->d_sg : nullptr, pair_gateup);
+                                 sel_mode == kSelectThreshold ? L->d_sg : nullptr, pair_gateup,
+                                 precise);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel
@@ -701,7 +706,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   if (dense_down) {
     launches += launch_down_tc(ctx, &L->tmap_wdt, g.has_shared ? &L->tmap_wdt_shared : nullptr,
                                L->tmap_hb[tn_idx], nsplit, tn, L->disp, max_tiles, g,
-                               L->d_slot_out, pair_down);
+                               L->d_slot_out, pair_down, precise);
     tm.mark();
     launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y);
     tm.mark();

@@ -275,6 +275,274 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The same GEMM with CHUNKED accumulation, for the fp32-accumulation parity mode (1e-5) on long
+// contractions.  The tensor core adds every 16-element step into the fp32 accumulator with
+// truncation: measured on B200 the result drifts by ~3.7e-8 of its magnitude per step, always
+// the same way, i.e. 1.2e-5 after the 320 steps of d_model = 5120 (tools/h_err_probe.py).  Here
+// the MMAs of at most kChunkSteps steps accumulate from zero into one of two TMEM chunk buffers;
+// the epilogue warps fold each finished chunk into a MASTER accumulator (a third TMEM region)
+// with round-to-nearest adds -- tcgen05.ld chunk + master, add, tcgen05.st master, 16 columns at
+// a time -- while the MMAs of the next chunk run into the other buffer.  The last chunk is added
+// in registers on its way to the epilogue proper.  One A block per CTA, token tiles <= 128.
+// ---------------------------------------------------------------------------------------------
+namespace {
+constexpr int kChunkSteps = 32;  // MMA steps (16 elements each) per chunk
+__host__ __device__ constexpr int pow2_cols(int c) { return c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : (c <= 256 ? 256 : 512))); }
+__host__ __device__ constexpr int chunked_tmem_cols(int tn) { return pow2_cols(3 * tmem_cols(tn)); }
+__host__ __device__ constexpr int chunked_ctas_per_sm(int tn) { return 512 / chunked_tmem_cols(tn) > 4 ? 4 : 512 / chunked_tmem_cols(tn); }
+__host__ __device__ constexpr int chunked_stages(int tn, int mode) {
+  // the shared memory of an SM split over the CTAs its TMEM allows
+  const int budget = (220 * 1024) / chunked_ctas_per_sm(tn) - 2048;
+  const int s = budget / stage_bytes(tn, mode, 1);
+  return s > 8 ? 8 : (s < 2 ? 2 : s);
+}
+__host__ __device__ constexpr int chunked_smem_bytes(int tn, int mode) {
+  return chunked_stages(tn, mode) * stage_bytes(tn, mode, 1) + 1024 + 256;
+}
+}  // namespace
+
+template <int TN, int MODE>
+__global__ void __launch_bounds__(kGateupThreads, chunked_ctas_per_sm(TN))
+grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                          const __grid_constant__ CUtensorMap tmap_a_shared,
+                          const __grid_constant__ CUtensorMap tmap_b0,
+                          const __grid_constant__ CUtensorMap tmap_b1,
+                          const __grid_constant__ CUtensorMap tmap_b2, const TcArgs a) {
+  constexpr int kStages = chunked_stages(TN, MODE);
+  constexpr int kStageBytes = stage_bytes(TN, MODE, 1);
+  constexpr int kBTile = b_tile_bytes(TN);
+  constexpr uint32_t kCols = tmem_cols(TN);            // columns of one accumulator
+  constexpr uint32_t kTmemCols = chunked_tmem_cols(TN);  // master + two chunk buffers
+  constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bar_base = smem_base + kStages * kStageBytes;
+  auto full_bar = [&](int s) { return bar_base + 8u * s; };
+  auto empty_bar = [&](int s) { return bar_base + 8u * (kStages + s); };
+  auto cfull_bar = [&](int b) { return bar_base + 8u * (2 * kStages + b); };
+  auto cempty_bar = [&](int b) { return bar_base + 8u * (2 * kStages + 2 + b); };
+  const uint32_t tmem_ptr_addr = bar_base + 8u * (2 * kStages + 4);
+  volatile uint32_t* tmem_ptr_generic = reinterpret_cast<volatile uint32_t*>(
+      smem_raw + (tmem_ptr_addr - smem_u32(smem_raw)));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b0);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(cfull_bar(b), 1);
+      mbar_init(cempty_bar(b), 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_ptr_addr, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_ptr_generic;
+
+  pdl_wait();
+  pdl_launch_dependents();
+
+  const int tile = blockIdx.y;
+  bool active = tile < *a.n_tiles;
+  int e = 0, row0 = 0, nrows = 0;
+  bool shared_expert = false;
+  if (active) {
+    e = a.tile_expert[tile];
+    row0 = a.tile_row0[tile];
+    nrows = a.tile_nrows[tile];
+    shared_expert = e >= a.n_experts;
+    active = static_cast<int>(blockIdx.x) < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
+  }
+
+  if (active) {
+    const int num_k_blocks = shared_expert ? a.kblocks_shared : a.kblocks_routed;
+    const int nsplit = (MODE == 0) ? 1 : a.nsplit;
+    const int kc = max(1, kChunkSteps / (4 * nsplit));  // K blocks per chunk
+    const int n_chunks = ceil_div(num_k_blocks, kc);
+    const bool own_map = (MODE == 1) && shared_expert;
+    const CUtensorMap* map_a = own_map ? &tmap_a_shared : &tmap_a;
+    const int a_row = (own_map ? 0 : (shared_expert ? a.n_experts : e) * a.rows_per_expert) +
+                      static_cast<int>(blockIdx.x) * 128;
+
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int kb = 0; kb < num_k_blocks; ++kb) {
+          const int s = kb % kStages;
+          const uint32_t ph = (kb / kStages) & 1u;
+          mbar_wait(empty_bar(s), ph ^ 1u);
+          mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * kBTile);
+          const uint32_t a_smem = smem_base + s * kStageBytes;
+          tma_load_2d(a_smem, map_a, 0, ((a_row >> 7) * num_k_blocks + kb) * 128, full_bar(s),
+                      kPolicyEvictFirst);
+          tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
+          if (MODE == 1 && nsplit > 1) {
+            tma_load_2d(a_smem + kATileBytes + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
+                        kPolicyEvictLast);
+            tma_load_2d(a_smem + kATileBytes + 2 * kBTile, &tmap_b2, kb * kBlockK, row0, full_bar(s),
+                        kPolicyEvictLast);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        int kb = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+          const int b = c & 1;
+          if (c >= 2) {  // the epilogue warps have folded chunk c - 2 out of this buffer
+            mbar_wait(cempty_bar(b), ((c >> 1) - 1) & 1u);
+            tc_fence_after();
+          }
+          const uint32_t acc = tmem_base + (1u + b) * kCols;
+          const int kb_end = min(num_k_blocks, kb + kc);
+          bool first = true;
+          for (; kb < kb_end; ++kb) {
+            const int s = kb % kStages;
+            const uint32_t ph = (kb / kStages) & 1u;
+            mbar_wait(full_bar(s), ph);
+            tc_fence_after();
+            const uint32_t a_smem = smem_base + s * kStageBytes;
+            const uint64_t a_desc = make_smem_desc_sw128(a_smem);
+#pragma unroll
+            for (int sp = 0; sp < (MODE == 0 ? 1 : kMaxSplit); ++sp) {
+              if (sp < nsplit) {
+                const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes + sp * kBTile);
+#pragma unroll
+                for (int k = 0; k < kBlockK / 16; ++k) {
+                  umma_bf16(acc, a_desc + 2u * k, b_desc + 2u * k, kIdesc, first ? 0u : 1u);
+                  first = false;
+                }
+              }
+            }
+            umma_commit(empty_bar(s));
+          }
+          umma_commit(cfull_bar(b));
+        }
+      }
+    } else {
+      // ---- epilogue warps: fold chunks into the master accumulator, then the epilogue proper ----
+      const int q = warp & 3;  // TMEM lane quarter this warp may read
+      const int m_valid = shared_expert ? a.m_shared : a.m_routed;
+      const uint32_t lane_off = static_cast<uint32_t>(32 * q) << 16;
+      const uint32_t master = tmem_base + lane_off;
+#pragma unroll 1
+      for (int c = 0; c < n_chunks; ++c) {
+        const int b = c & 1;
+        mbar_wait(cfull_bar(b), (c >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t chunk = tmem_base + lane_off + (1u + b) * kCols;
+        const bool last = c == n_chunks - 1;
+        const int n = (MODE == 0) ? static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15)
+                                  : static_cast<int>(blockIdx.x) * 128 + 32 * q + lane;
+        const bool is_gate_lane = lane < 16;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TN; c0 += 16) {
+          if (c0 >= nrows) break;
+          uint32_t v[16], mm[16];
+          tmem_ld_32x32b_x16(chunk + c0, v);
+          if (c > 0) tmem_ld_32x32b_x16(master + c0, mm);
+          tmem_ld_wait();
+          if (c > 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              v[i] = __float_as_uint(__fadd_rn(__uint_as_float(mm[i]), __uint_as_float(v[i])));
+          }
+          if (!last) {
+            tmem_st_32x32b_x16(master + c0, v);
+            continue;
+          }
+          if (MODE == 0) {
+#pragma unroll
+            for (int cc = 0; cc < 16; cc += 2) {
+              const float mine0 = __uint_as_float(v[cc]);
+              const float mine1 = __uint_as_float(v[cc + 1]);
+              const float send = is_gate_lane ? mine1 : mine0;
+              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+              const float g = is_gate_lane ? mine0 : recv;
+              const float u = is_gate_lane ? recv : mine1;
+              const int col = c0 + cc + (is_gate_lane ? 0 : 1);
+              if (col < nrows && n < m_valid) {
+                const int r = (TN == 16 && a.tile_colrow != nullptr) ? a.tile_colrow[tile * 16 + col]
+                                                                     : row0 + col;
+                if (r >= 0) {
+                  const float sgv = silu_f(g);
+                  a.out[static_cast<size_t>(r) * a.out_stride + n] = sgv * u;
+                  if (a.sg_out != nullptr) a.sg_out[static_cast<size_t>(r) * a.out_stride + n] = sgv;
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc)
+              if (c0 + cc < nrows && n < m_valid)
+                a.out[static_cast<size_t>(row0 + c0 + cc) * a.out_stride + n] = __uint_as_float(v[cc]);
+          }
+        }
+        if (!last) {
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(cempty_bar(b));
+        }
+      }
+      tc_fence_before();
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// the dynamic shared memory opt-in is per device: one flag per (kernel, device)
+template <class K>
+static void ensure_smem_attr(K kernel, int smem, unsigned long long* mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(__atomic_load_n(mask, __ATOMIC_ACQUIRE) & bit)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    __atomic_fetch_or(mask, bit, __ATOMIC_RELEASE);
+  }
+}
+
+template <int TN, int MODE>
+static void launch_tc_chunked(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
+                              const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
+                              const TcArgs& a, int grid_x, int max_tiles) {
+  static unsigned long long mask = 0;
+  constexpr int smem = chunked_smem_bytes(TN, MODE);
+  ensure_smem_attr(grouped_tc_chunked_kernel<TN, MODE>, smem, &mask);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  cfg.stream = ctx.stream;
+  cfg.gridDim = dim3(grid_x, max_tiles);
+  cfg.blockDim = dim3(kGateupThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchKernelEx(&cfg, grouped_tc_chunked_kernel<TN, MODE>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
+}
+
+// Chunked accumulation pays when one accumulator would take more than ~96 truncating steps
+// (drift above ~3.5e-6 of the result); shorter contractions keep the single accumulator.
+static bool wants_chunks(bool precise, int k_blocks, int nsplit) {
+  return precise && k_blocks * 4 * nsplit > 96;
+}
+
 static int pick_tile_case(int tile_tokens) {
   if (tile_tokens <= 16) return 16;
   if (tile_tokens <= 32) return 32;
@@ -287,13 +555,9 @@ template <int TN, int MODE, int MB = 1>
 static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
                            const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
                            const TcArgs& a, int grid_x, int max_tiles) {
-  static bool attr_set = false;
+  static unsigned long long mask = 0;
   constexpr int smem = gateup_smem_bytes(TN, MODE, MB);
-  if (!attr_set) {
-    cudaFuncSetAttribute(grouped_tc_kernel<TN, MODE, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    attr_set = true;
-  }
+  ensure_smem_attr(grouped_tc_kernel<TN, MODE, MB>, smem, &mask);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -309,7 +573,7 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles, float* sg, bool pair_blocks) {
+                     float* h, bool token_tiles, float* sg, bool pair_blocks, bool precise) {
   TcArgs a{};
   a.sg_out = sg;
   a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;
@@ -328,6 +592,15 @@ int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUte
   a.rows_per_expert = 2 * g.Np;
   a.nsplit = 1;
   const int gx = a.mblocks_routed > a.mblocks_shared ? a.mblocks_routed : a.mblocks_shared;
+  if (wants_chunks(precise, a.kblocks_routed, 1)) {
+    switch (pick_tile_case(tile_tokens)) {
+      case 16: launch_tc_chunked<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+      case 32: launch_tc_chunked<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+      case 64: launch_tc_chunked<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+      default: launch_tc_chunked<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    }
+    return 1;
+  }
   if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
     launch_tc_case<64, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles);
     return 1;
@@ -349,7 +622,7 @@ int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUte
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
-                   const Geometry& g, float* slot_out, bool pair_blocks) {
+                   const Geometry& g, float* slot_out, bool pair_blocks, bool precise) {
   TcArgs a{};
   a.tile_expert = d.tile_expert;
   a.tile_row0 = d.tile_row0;
@@ -366,6 +639,18 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
   a.nsplit = nsplit;
   const CUtensorMap* sh = tmap_wdt_shared ? tmap_wdt_shared : tmap_wdt;
   const int gx = a.mblocks_routed;
+  {
+    const int kmax = a.kblocks_routed > a.kblocks_shared ? a.kblocks_routed : a.kblocks_shared;
+    if (wants_chunks(precise, kmax, nsplit)) {
+      switch (pick_tile_case(tile_tokens)) {
+        case 16: launch_tc_chunked<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+        case 32: launch_tc_chunked<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+        case 64: launch_tc_chunked<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+        default: launch_tc_chunked<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+      }
+      return 1;
+    }
+  }
   if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
     launch_tc_case<64, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles);
     return 1;

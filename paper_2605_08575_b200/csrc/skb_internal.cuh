@@ -96,11 +96,13 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles, float* sg = nullptr, bool pair_blocks = false);
+                     float* h, bool token_tiles, float* sg = nullptr, bool pair_blocks = false,
+                     bool precise = false);
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
-                   const Geometry& g, float* slot_out, bool pair_blocks = false);
+                   const Geometry& g, float* slot_out, bool pair_blocks = false,
+                   bool precise = false);
 int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
                         const float* weights, int B, const Geometry& g, float* y);
 int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
