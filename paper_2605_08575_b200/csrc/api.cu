@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cmath>
 #include <mutex>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -409,13 +410,12 @@ struct StageTimer {
   }
 };
 
-// Fused decode kernel or staged kernels for a batch <= 16?  Both are correct for every eligible
+// Fused decode kernel or staged kernels for a batch <= 4?  Both are correct for every eligible
 // shape; which is faster depends on how much the per-(token, slot) row gather of the fused
 // kernel moves against one pass over the routed experts' W_down.  Linear models fitted to
 // measurements on B200 (tools/fused_vs_staged.py: Granite, OLMoE, Qwen3.5 and GPT-OSS shapes,
-// batches 1-16, s = 0.5; refitted after the staged kernels' small-tile changes -- on the 40
-// measured points the choice is never more than 2.2 % slower than the better path): microseconds
-// from MB.
+// batches 1-4, s = 0.5, clean L2): microseconds from MB.  One and two tokens: the fused kernel
+// by 20-40 %; three: a tie; four: the staged kernels by 5-25 %.
 bool decode_fused_preferred(const Geometry& g, int B, double keep_r, double keep_s) {
   const double E = g.E, K = g.K;
   const double U = E * (1.0 - std::pow(1.0 - K / E, B));  // expected distinct routed experts
@@ -424,7 +424,8 @@ bool decode_fused_preferred(const Geometry& g, int B, double keep_r, double keep
   const double vg = (B * K * keep_r + (g.has_shared ? B * keep_s : 0.0)) * row_mb;
   const double vd = (U * g.N + (g.has_shared ? g.S : 0.0)) * row_mb;
   const double R = K + (g.has_shared ? 1.0 : 0.0);
-  const double fused = 27.9 + 0.248 * gup + (g.Dp <= 2048 ? 0.237 : 0.519) * vg + 0.232 * B * R;
+  double fused = 24.0 + 0.20 * gup + 0.30 * vg + 0.53 * B * R;
+  if (B >= 3) fused += 4.0 + 0.025 * gup;  // four tokens per consumer lane: slower per byte
   // staged kernels: a fixed chain of launches whose router part grows with d_model (the exact
   // logit chains are d_model dependent adds long), plus one pass over the routed experts
   const double staged = 32.0 + 10.34 * (g.Dp / 1024.0) + 0.1814 * (gup + 0.5 * vd);
@@ -892,12 +893,22 @@ int skb_n_off(double s, int n, int32_t* out) {
 
 uint64_t skb_last_error_offset(void) { return g_err_offset; }
 
+// Size of the file in 128-bit arithmetic (header fields are 31-bit values: their product wraps
+// 64 bits); false when it does not fit in 64 bits or a field is negative.
+static bool weight_file_size_checked(const skb_config* c, uint64_t* out) {
+  if (c->d_model < 0 || c->n_experts < 0 || c->d_ffn < 0 || c->d_shared < 0) return false;
+  const unsigned __int128 D = static_cast<unsigned __int128>(c->d_model) * sizeof(float);
+  unsigned __int128 n = 28 + static_cast<unsigned __int128>(c->n_experts) * D +
+                        static_cast<unsigned __int128>(3) * c->n_experts * c->d_ffn * D;
+  if (c->has_shared) n += static_cast<unsigned __int128>(3) * c->d_shared * D;
+  if (n > static_cast<unsigned __int128>(UINT64_MAX)) return false;
+  *out = static_cast<uint64_t>(n);
+  return true;
+}
+
 uint64_t skb_weight_file_size(const skb_config* c) {
-  if (c == nullptr) return 0;
-  const uint64_t D = static_cast<uint64_t>(c->d_model) * sizeof(float);
-  uint64_t n = 28 + static_cast<uint64_t>(c->n_experts) * D +
-               3ull * c->n_experts * static_cast<uint64_t>(c->d_ffn) * D;
-  if (c->has_shared) n += 3ull * static_cast<uint64_t>(c->d_shared) * D;
+  uint64_t n = 0;
+  if (c == nullptr || !weight_file_size_checked(c, &n)) return 0;
   return n;
 }
 
@@ -965,7 +976,9 @@ int skb_layer_load(const char* path, int device, skb_config* cfg_out, skb_layer*
   if (c.d_ffn < 1) return done(format_error(16, "header: d_ffn < 1"));
   if ((c.has_shared != 0) != (c.d_shared > 0))
     return done(format_error(20, "header: shared flag disagrees with d_shared"));
-  const uint64_t want = skb_weight_file_size(&c);
+  uint64_t want = 0;
+  if (!weight_file_size_checked(&c, &want))  // a payload no file can hold: the file is short
+    return done(format_error(whole, "truncated file"));
   if (size < want) return done(format_error(whole, "truncated file"));
   if (size > want) return done(format_error(want, "trailing bytes after weight payload"));
 
@@ -974,7 +987,14 @@ int skb_layer_load(const char* path, int device, skb_config* cfg_out, skb_layer*
   const unsigned char* p = base + 28;
   const float* router = reinterpret_cast<const float*>(p);  // 28 is a multiple of 4
   p += E * c.d_model * sizeof(float);
-  std::vector<const float*> gate(E), up(E), down(E);
+  std::vector<const float*> gate, up, down;
+  try {  // no exception may cross the C boundary
+    gate.resize(E);
+    up.resize(E);
+    down.resize(E);
+  } catch (const std::bad_alloc&) {
+    return done(fail(SKB_EINTERNAL, "layer_load: out of host memory for %zu expert pointers", E));
+  }
   for (size_t e = 0; e < E; ++e) {
     gate[e] = reinterpret_cast<const float*>(p);
     up[e] = reinterpret_cast<const float*>(p + mat);

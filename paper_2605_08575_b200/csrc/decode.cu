@@ -1,4 +1,4 @@
-// decode.cu -- the whole layer for decode batches (B <= 8) as ONE persistent launch, software
+// decode.cu -- the whole layer for decode batches (B <= 4) as ONE persistent launch, software
 // pipelined: the down projection of an expert runs while the gate/up weights of the next
 // experts are still streaming.
 //
@@ -35,7 +35,7 @@
 //     depend on the routing) and then for the union of candidate experts, in EXPERT-MAJOR order
 //     over all CTAs: a piece = 16 neurons (their 16 gate + 16 up rows) x all of d_model, read as
 //     one 3-D TMA box {64 columns, 32 rows, 4 K-blocks} (16 KB) per ring stage out of the
-//     128-row tiled image.  With at most 8 tokens the contraction is a GEMV: a tensor-core tile
+//     128-row tiled image.  With at most 4 tokens the contraction is a GEMV: a tensor-core tile
 //     would be 1/16 full and its operand staging (token tile TMA, UMMA issue, TMEM round trip)
 //     only adds latency to a stream whose cost is HBM bytes, so the consumers are plain fp32 FMAs
 //     straight out of the ring -- consumer warp w owns K-block w of every stage, lane l the
@@ -64,7 +64,7 @@ constexpr int kDecThreads = 448;  // 14 warps
 constexpr int kDThreads = 256;    // the D role: warps 6..13
 constexpr int kWarpTma = 0, kWarpChain = 1, kWarpG0 = 2, kNumGWarps = 4, kWarpD0 = 6;
 constexpr int kGThreads = kNumGWarps * 32;
-constexpr int kDecMaxB = 8;
+constexpr int kDecMaxB = 4;  // more tokens per consumer lane than this spill (and the staged kernels win anyway)
 constexpr int kDecTokens = 16;             // token stride of the row tables and of hc / part
 constexpr int kKBox = 4;                   // K blocks per ring stage = consumer warps
 constexpr int kStageBytes = kKBox * 32 * 128;  // 16 KB: 32 rows x 64 bf16 per K block
@@ -153,7 +153,7 @@ __host__ __device__ inline DecSmem dec_smem_layout(int stages, int gb_rows, int 
 // dynamic shared memory: 227 KB minus the kernel's static shared memory (< 1 KB) and the
 // 1 KB alignment slack
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 1024;
-inline int dec_tb_for(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : (B <= 4 ? 4 : 8)); }
+inline int dec_tb_for(int B) { return B <= 1 ? 1 : (B <= 2 ? 2 : 4); }
 // Split of what the fixed regions leave: a staging buffer of up to 80 KB of gathered W_down rows
 // and kMinStages..kMaxStages ring stages (deeper rings only lengthen every other request's queue:
 // 96 KB in flight per SM already saturates HBM, tools/micro/burst.cu).
@@ -1543,8 +1543,7 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   switch (tb) {
     case 1: launch_tb<1>(cfg, tmap_w3, a); break;
     case 2: launch_tb<2>(cfg, tmap_w3, a); break;
-    case 4: launch_tb<4>(cfg, tmap_w3, a); break;
-    default: launch_tb<8>(cfg, tmap_w3, a); break;
+    default: launch_tb<4>(cfg, tmap_w3, a); break;
   }
   return 1;
 }

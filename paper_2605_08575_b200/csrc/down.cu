@@ -407,11 +407,13 @@ static int launch_down_seg(const LaunchCtx& ctx, const DownArgs& a, const Geomet
     L = down_layout(SEG, R, cmax, nmax, ring);
   }
   if (L.total > 220 * 1024) return -1;
-  static int smem_set = 0;
-  if (L.total > smem_set) {
+  static int smem_set[64] = {};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (L.total > __atomic_load_n(&smem_set[dev & 63], __ATOMIC_ACQUIRE)) {
     cudaFuncSetAttribute(down_cluster_kernel<SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          L.total);
-    smem_set = L.total;
+    __atomic_store_n(&smem_set[dev & 63], L.total, __ATOMIC_RELEASE);
   }
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[2];

@@ -432,12 +432,21 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
     cudaLaunchKernelEx(&cfg, router_logits_fast_kernel, r.x, r.router, r.B, r.E, r.D, r.logits);
     ++launches;
   }
-  static bool attr_set = false;
+  // per device (function attributes and the SM count are per device; the C ABI takes a device)
+  static bool attr_set[64] = {};
+  static int sms_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int di = dev & 63;
   constexpr int smem = kRfSmemBytes;
-  if (!attr_set) {
+  if (!__atomic_load_n(&attr_set[di], __ATOMIC_ACQUIRE)) {
     cudaFuncSetAttribute(router_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms_of[di] = n;
+    __atomic_store_n(&attr_set[di], true, __ATOMIC_RELEASE);
   }
+  const int n_sms = sms_of[di];
   RouterFusedArgs a{};
   a.x = r.x;
   a.router = r.router;
@@ -468,12 +477,6 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
     // One chain warp per CTA is latency-bound (a dependent add every 4 cycles), so what matters
     // for a grid of many CTAs is how many are resident: a ring of 2 instead of 4 sub-chunks
     // halves the shared memory and doubles the CTAs per SM (prefill: 4096 CTAs, 14 waves -> 7).
-    static int n_sms = 0;
-    if (n_sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
     const long n_ctas = static_cast<long>(cfg.gridDim.x) * cfg.gridDim.y;
     a.stages = n_ctas > 2L * n_sms ? 2 : kRfStages;
     cfg.dynamicSmemBytes = static_cast<size_t>(a.stages) * kRfRows * kRfRow * 4 + 2 * a.stages * 8;

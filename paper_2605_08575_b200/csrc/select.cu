@@ -333,6 +333,17 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
   }
   cfg.gridDim = dim3(a.rows);
   cfg.dynamicSmemBytes = static_cast<size_t>(nmax) * sizeof(uint32_t);
+  if (cfg.dynamicSmemBytes > 40 * 1024) {
+    // rows beyond ~10K keys: above the 48 KB default together with the static scratch
+    static int smem_set[64] = {};  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int want = static_cast<int>(cfg.dynamicSmemBytes);
+    if (want > __atomic_load_n(&smem_set[dev & 63], __ATOMIC_ACQUIRE)) {
+      cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
+      __atomic_store_n(&smem_set[dev & 63], want, __ATOMIC_RELEASE);
+    }
+  }
   cudaLaunchKernelEx(&cfg, select_rows_kernel, a);
   return 1;
 }

@@ -155,7 +155,7 @@ int launch_down(const LaunchCtx& ctx, const DownArgs& a, const Geometry& g);
 int launch_combine_slots(const LaunchCtx& ctx, const float* slot_outputs, const float* weights,
                          int B, int K, int D, float* y);
 
-// Fused decode kernel (decode.cu): the whole layer for B <= 8 in one persistent launch.
+// Fused decode kernel (decode.cu): the whole layer for B <= 4 in one persistent launch.
 struct DecodeLaunch {
   const float* x;                  // [B][D]
   const float* router;             // [E][D]

@@ -135,3 +135,13 @@ def test_moe1_loader_format_errors(skb, tmp_path):
     assert e.value.offset == len(blob) and "trailing bytes" in str(e.value)
     with pytest.raises(skb.IoError):
         skb.MoELayerWeights.load(tmp_path / "missing.moe")
+
+
+def test_weight_file_size_does_not_wrap(skb):
+    """Header fields are 31-bit values: 3*E*N*D*4 wraps 64 bits for a crafted header.  The size is
+    formed in 128 bits and reported as 0 (no such file), so that the loader rejects the header
+    before it builds pointers past the mapping."""
+    big = skb.MoEConfig(2**31 - 1, 1, 2**31 - 1, 2**31 - 1, False, 0, True, 64)
+    assert skb.weight_file_size(big) == 0
+    ok = skb.MoEConfig(4, 2, 8, 16, False, 0, True, 64)
+    assert skb.weight_file_size(ok) == 28 + 4 * 8 * 4 + 3 * 4 * 16 * 8 * 4
