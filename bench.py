@@ -365,6 +365,9 @@ def run_ep(args, torch, dist, skb, rank, world, local):
     hbm_peak, peak_src = peaks()
     cfg = skb.MoEConfig(shape["E"], shape["K"], shape["D"], shape["N"], shape["S"] > 0, shape["S"],
                         True, 64)
+    if world > 1:
+        assert dist.get_world_size() == world and dist.get_backend() == "nccl", \
+            "the expert-parallel arm needs the NCCL process group of all ranks"
     backend = ep.CudaBackend(skb, cfg, SEED, SCALE, rank, world, device=local,
                              max_rows=max(64, 4 * B * shape["K"]))
     layer = ep.ExpertParallelLayer(backend)
@@ -439,11 +442,13 @@ def run_ep(args, torch, dist, skb, rank, world, local):
                                    f"d_model={D} d_ffn={shape['N']} d_shared={shape['S']}, "
                                    f"batch {B} decode per GPU, top-k neuron selection s={s}",
                        "sparsity": s, "batch_per_gpu": B,
-                       "parallelism": f"expert parallel x{world}: experts sharded, all-to-all-v "
-                                      "dispatch/combine over NCCL, shared expert replicated",
+                       "parallelism": f"expert parallel x{world}: experts sharded, ids all-gathered, "
+                                      "one packed bf16 all-to-all-v out and one fp32 back over "
+                                      "NCCL, shared expert replicated",
                        "l2": "512 MiB memset between steps (inside the timed pair is only the "
                              "layer) + ring of 8 token batches",
-                       "launch": "direct launches; the counts exchange synchronises once per step"},
+                       "launch": "direct launches; the send/receive matrix crosses to the host "
+                                 "once per step (NCCL takes split sizes from the host)"},
             "bytes_alg_per_step_rank0_upper_bound": int(bytes_alg),
             "roofline": {"bound": "hbm", "kernel": "whole EP step (rank 0)", "achieved": round(gbs, 1),
                          "peak": hbm_peak, "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
@@ -797,6 +802,24 @@ def main():
     ap.add_argument("--ep", action="store_true", help="expert-parallel arm (ep.py) at any rank count")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # started as a plain process: become N ranks (one per GPU) through torch.distributed.run,
+        # the way the driver launches the multi-GPU runs.  NCCL's communicator log goes to stderr.
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd, env=env))
+    if args.gpus > 1 and args.impl == "ours":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

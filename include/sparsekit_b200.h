@@ -269,6 +269,32 @@ uint64_t skb_last_error_offset(void);
  * the host's libm, no device needed; used by profile_tipping for its probe batches. */
 int skb_generate_tokens(int32_t batch, int32_t d_model, uint64_t seed, float* out);
 
+/* ---- expert-parallel data plane (device pointers, one process per GPU) --------------------
+ * The reference is single-process; these are the device halves of the exchange
+ * that shards its experts over ranks (proj/src/engine.cpp:132-165: experts are independent
+ * given their routed tokens; proj/src/router.cpp:119-130: the combine is a per-token sum over
+ * slots).  paper_2605_08575_b200/ep.py drives them around two NCCL all-to-all-v calls.
+ *
+ * skb_ep_plan: from the all-gathered routing ids_all [world][slots_per_rank] (flat slot
+ *   t*top_k+s per rank; ids < 0 pad a short batch) and the expert range starts expert_lo
+ *   [world+1]: counts [world][world] (slots src sends to dst), and for THIS rank's slots their
+ *   position in its send buffer (grouped by destination, ascending flat slot inside a group;
+ *   -1 for padding) and the expert id local to the destination.
+ * skb_ep_pack: token rows as bf16 into the packed send buffer, row stride skb_ep_row_stride():
+ *   [d_model bf16][int32 local expert id][pad to 16 bytes].
+ * skb_ep_unpack: received packed rows -> fp32 rows + ids (inputs of skb_layer_forward_device
+ *   with external routing).
+ * skb_ep_combine: y[t] = sum_s weights[t][s] * back[pos[t*top_k+s]] (+ shared[t]), slots
+ *   ascending, multiply and add rounded separately (router.cpp:119-130, engine.cpp:168-173). */
+int skb_ep_row_stride(int d_model);
+int skb_ep_plan(const int32_t* ids_all, int world, int slots_per_rank, const int32_t* expert_lo,
+                int rank, int32_t* counts, int32_t* pos, int32_t* local_ids, void* stream);
+int skb_ep_pack(const float* x, const int32_t* pos, const int32_t* local_ids, int slots, int top_k,
+                int d_model, uint8_t* send, void* stream);
+int skb_ep_unpack(const uint8_t* recv, int rows, int d_model, float* x, int32_t* ids, void* stream);
+int skb_ep_combine(const float* back, const int32_t* pos, const float* weights, const float* shared,
+                   int batch, int top_k, int d_model, float* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,7 @@ EXPORTS = (
     "skb_layer_last_launches", "skb_layer_weight_bytes", "skb_route", "skb_align_dispatch",
     "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off", "skb_generate_tokens",
     "skb_layer_load", "skb_save_weights", "skb_weight_file_size", "skb_last_error_offset",
+    "skb_ep_row_stride", "skb_ep_plan", "skb_ep_pack", "skb_ep_unpack", "skb_ep_combine",
 )
 
 
@@ -108,5 +109,10 @@ def load() -> C.CDLL:
     L.skb_weight_file_size.restype = C.c_uint64
     L.skb_last_error_offset.argtypes = []
     L.skb_last_error_offset.restype = C.c_uint64
+    L.skb_ep_row_stride.argtypes = [C.c_int]
+    L.skb_ep_plan.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp]
+    L.skb_ep_pack.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
+    L.skb_ep_unpack.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
+    L.skb_ep_combine.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
     _lib = L
     return L

@@ -18,7 +18,8 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libsparsekit_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["api.cu", "router.cu", "gateup.cu", "select.cu", "down.cu", "image.cu", "decode.cu"]
+SOURCES = ["api.cu", "router.cu", "gateup.cu", "select.cu", "down.cu", "image.cu", "decode.cu",
+           "ep.cu"]
 HEADERS = [os.path.join(CSRC, h) for h in ("skb_internal.cuh", "tc_ptx.cuh", "route_device.cuh",
                                            "select_device.cuh")] + [
     os.path.join(INCLUDE, "sparsekit_b200.h")]
@@ -31,7 +32,7 @@ NVCC_FLAGS = [
     "-I", INCLUDE,
 ]
 if os.environ.get("SKB_DEBUG_TIMING"):
-    NVCC_FLAGS.append("-DSKB_DEBUG_TIMING")  # in-kernel phase timestamps (tools/dbg_rf.py)
+    NVCC_FLAGS.append("-DSKB_DEBUG_TIMING")  # in-kernel phase timestamps (tools/dbg_dec.py)
 
 
 def _nvcc() -> str:

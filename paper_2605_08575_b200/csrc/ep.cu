@@ -1,0 +1,202 @@
+// ep.cu -- device side of the expert-parallel data plane (paper_2605_08575_b200/ep.py): the send /
+// receive matrix out of the all-gathered routing, the packed bf16 dispatch rows, and the ordered
+// combine at the home rank.  The reference is single-process; the partitioning
+// follows proj/src/engine.cpp:132-165 (experts independent given their tokens) and
+// proj/src/router.cpp:119-130 (per-token sum over slots, ascending, multiply and add rounded
+// separately).
+//
+// Packed dispatch row: [D bf16 token values][int32 local expert id][pad to 16 bytes].
+#include "../../include/sparsekit_b200.h"
+#include "skb_internal.cuh"
+
+namespace skb {
+
+namespace {
+
+constexpr int kPlanThreads = 1024;
+constexpr int kMaxWorld = 16;
+
+__device__ __forceinline__ int owner_of(int e, const int32_t* lo, int W) {
+  int r = 0;
+#pragma unroll 1
+  for (int i = 1; i < W; ++i)
+    if (e >= lo[i]) r = i;
+  return r;
+}
+
+// One CTA.  ids_all [W][Bmax][K] (ids < 0: padding of a short home batch).  Outputs:
+//   cnt [W][W]      slots rank src sends to rank dst
+//   pos [Bmax * K]  position of this rank's flat slot t*K+s in its send buffer (grouped by
+//                   destination rank, ascending flat slot inside a group), -1 for padding
+//   loc [Bmax * K]  expert id local to the destination rank
+__global__ void __launch_bounds__(kPlanThreads) ep_plan_kernel(const int32_t* __restrict__ ids_all,
+                                                               int W, int slots,
+                                                               const int32_t* __restrict__ lo, int rank,
+                                                               int32_t* __restrict__ cnt,
+                                                               int32_t* __restrict__ pos,
+                                                               int32_t* __restrict__ loc) {
+  __shared__ int s_cnt[kMaxWorld * kMaxWorld];
+  __shared__ int s_lo[kMaxWorld + 1];
+  __shared__ int s_part[kPlanThreads / 32][kMaxWorld];  // per-warp counts of the own slots
+  __shared__ int s_base[kMaxWorld];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < W * W; i += kPlanThreads) s_cnt[i] = 0;
+  if (tid <= W) s_lo[tid] = lo[tid];
+  __syncthreads();
+  // the whole matrix: integer atomics (the result does not depend on their order)
+  for (int i = tid; i < W * slots; i += kPlanThreads) {
+    const int e = ids_all[i];
+    if (e >= 0) atomicAdd(&s_cnt[(i / slots) * W + owner_of(e, s_lo, W)], 1);
+  }
+  __syncthreads();
+  for (int i = tid; i < W * W; i += kPlanThreads) cnt[i] = s_cnt[i];
+  if (tid < W) {  // start of every destination group in this rank's send buffer
+    int b = 0;
+    for (int d = 0; d < tid; ++d) b += s_cnt[rank * W + d];
+    s_base[tid] = b;
+  }
+  // own slots: thread t takes the contiguous range [t * per, (t + 1) * per) -- stable order
+  const int32_t* mine = ids_all + static_cast<size_t>(rank) * slots;
+  const int per = ceil_div(slots, kPlanThreads);
+  const int i0 = tid * per, i1 = min(slots, i0 + per);
+  int c[kMaxWorld];
+#pragma unroll
+  for (int d = 0; d < kMaxWorld; ++d) c[d] = 0;
+  for (int i = i0; i < i1; ++i) {
+    const int e = mine[i];
+    if (e >= 0) {
+      const int d = owner_of(e, s_lo, W);
+#pragma unroll
+      for (int dd = 0; dd < kMaxWorld; ++dd) c[dd] += (dd == d) ? 1 : 0;
+    }
+  }
+  // exclusive prefix over threads, per destination: warp scan, then the warps' totals
+  int excl[kMaxWorld];
+#pragma unroll
+  for (int d = 0; d < kMaxWorld; ++d) {
+    int v = c[d];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    excl[d] = v - c[d];
+    if (lane == 31 && d < W) s_part[warp][d] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < kMaxWorld; ++d) {
+    if (d < W) {
+      int b = s_base[d];
+      for (int w = 0; w < warp; ++w) b += s_part[w][d];
+      excl[d] += b;
+    }
+  }
+  for (int i = i0; i < i1; ++i) {
+    const int e = mine[i];
+    int p = -1, l = 0;
+    if (e >= 0) {
+      const int d = owner_of(e, s_lo, W);
+#pragma unroll
+      for (int dd = 0; dd < kMaxWorld; ++dd)
+        if (dd == d) p = excl[dd]++;
+      l = e - s_lo[d];
+    }
+    pos[i] = p;
+    loc[i] = l;
+  }
+}
+
+// one warp per flat slot: token row -> bf16 into its packed send row, local expert id behind it
+__global__ void __launch_bounds__(256) ep_pack_kernel(const float* __restrict__ x,
+                                                      const int32_t* __restrict__ pos,
+                                                      const int32_t* __restrict__ loc, int slots,
+                                                      int K, int D, int stride,
+                                                      uint8_t* __restrict__ send) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= slots) return;
+  const int p = pos[i];
+  if (p < 0) return;
+  const float* src = x + static_cast<size_t>(i / K) * D;
+  uint8_t* row = send + static_cast<size_t>(p) * stride;
+  __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(row);
+  for (int d = lane; d < D; d += 32) dst[d] = __float2bfloat16_rn(__ldg(src + d));
+  if (lane == 0) *reinterpret_cast<int32_t*>(row + static_cast<size_t>(D) * 2) = loc[i];
+}
+
+// receiver: packed rows -> fp32 token rows + local expert ids (the layer's external-routing inputs)
+__global__ void __launch_bounds__(256) ep_unpack_kernel(const uint8_t* __restrict__ recv, int rows,
+                                                        int D, int stride, float* __restrict__ x,
+                                                        int32_t* __restrict__ ids) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const uint8_t* row = recv + static_cast<size_t>(r) * stride;
+  const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(row);
+  float* dst = x + static_cast<size_t>(r) * D;
+  for (int d = lane; d < D; d += 32) dst[d] = __bfloat162float(src[d]);
+  if (lane == 0) ids[r] = *reinterpret_cast<const int32_t*>(row + static_cast<size_t>(D) * 2);
+}
+
+// home rank: y[t] = sum_s w(t, s) * back[pos(t, s)] in ascending slot order, multiply and add
+// rounded separately (router.cpp:119-130), then the shared expert's output (engine.cpp:168-173)
+__global__ void __launch_bounds__(256) ep_combine_kernel(const float* __restrict__ back,
+                                                         const int32_t* __restrict__ pos,
+                                                         const float* __restrict__ w,
+                                                         const float* __restrict__ shared, int B,
+                                                         int K, int D, float* __restrict__ y) {
+  const int t = blockIdx.y;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B || d >= D) return;
+  float acc = 0.0f;
+  for (int s = 0; s < K; ++s) {
+    const int p = pos[t * K + s];
+    acc = __fadd_rn(acc, __fmul_rn(w[t * K + s], back[static_cast<size_t>(p) * D + d]));
+  }
+  if (shared != nullptr) acc = __fadd_rn(acc, shared[static_cast<size_t>(t) * D + d]);
+  y[static_cast<size_t>(t) * D + d] = acc;
+}
+
+}  // namespace
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" {
+
+int skb_ep_row_stride(int d_model) { return round_up(d_model * 2 + 4, 16); }
+
+int skb_ep_plan(const int32_t* ids_all, int world, int slots_per_rank, const int32_t* expert_lo,
+                int rank, int32_t* counts, int32_t* pos, int32_t* local_ids, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || slots_per_rank < 0) return SKB_ECONFIG;
+  if (slots_per_rank == 0) return SKB_OK;
+  ep_plan_kernel<<<1, kPlanThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      ids_all, world, slots_per_rank, expert_lo, rank, counts, pos, local_ids);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_pack(const float* x, const int32_t* pos, const int32_t* local_ids, int slots, int top_k,
+                int d_model, uint8_t* send, void* stream) {
+  if (slots <= 0) return SKB_OK;
+  ep_pack_kernel<<<ceil_div(slots, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, pos, local_ids, slots, top_k, d_model, skb_ep_row_stride(d_model), send);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_unpack(const uint8_t* recv, int rows, int d_model, float* x, int32_t* ids, void* stream) {
+  if (rows <= 0) return SKB_OK;
+  ep_unpack_kernel<<<ceil_div(rows, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      recv, rows, d_model, skb_ep_row_stride(d_model), x, ids);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_combine(const float* back, const int32_t* pos, const float* weights, const float* shared,
+                   int batch, int top_k, int d_model, float* y, void* stream) {
+  if (batch <= 0) return SKB_OK;
+  ep_combine_kernel<<<dim3(ceil_div(d_model, 256), batch), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      back, pos, weights, shared, batch, top_k, d_model, y);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+}  // extern "C"

@@ -8,22 +8,28 @@ combine is a per-token sum over slots (proj/src/router.cpp:119-130).
 
 Per forward, rank r ("home" of its own tokens x_r):
   1. route:    ids, weights = route(route_logits(x_r))            full router, replicated
-  2. dispatch: all-to-all-v of the routed token rows to the ranks that own ids // E_local
-               (counts first, then rows + local expert ids), rows sorted by destination
-  3. experts:  un-weighted slot outputs of the received rows through the local experts
+  2. plan:     all-gather of the ids (B*K*4 bytes per rank); every rank then derives the WHOLE
+               send/receive matrix on the device (csrc/ep.cu: ep_plan_kernel) -- no count
+               exchange; the matrix crosses to the host once, because NCCL's all-to-all-v takes
+               its split sizes from the host (the one synchronisation of the step)
+  3. dispatch: ONE all-to-all-v of packed rows [D bf16 | int32 local expert id], grouped by
+               destination rank, ascending flat slot inside a group (ep_pack_kernel)
+  4. experts:  un-weighted slot outputs of the received rows through the local experts
                (external routing, top-k neuron selection at s_routed)
-  4. combine:  all-to-all-v back, un-sort, y = sum_s w_s * out_s in ascending slot order with
-               multiply and add rounded separately (router.cpp:119-130), then the shared
-               expert's output (replicated, computed at home with its own ratio) last
-               (engine.cpp:168-173)
+  5. combine:  ONE all-to-all-v back (fp32: the 1e-5 parity mode), then y = sum_s w_s * out_s in
+               ascending slot order with multiply and add rounded separately
+               (router.cpp:119-130) and the shared expert's output (replicated, computed at home
+               with its own ratio) last (engine.cpp:168-173) -- ep_combine_kernel
 
-Selection and routing are per-(token, slot) local, so expert ids and masks are identical to the
-single-GPU layer; outputs agree to the fp32 tolerance (the single-GPU kernels fold the weights
-into a different, equally fixed, reduction tree).
+Tokens cross the wire as bf16 (what the device image of the layer multiplies anyway: the expert
+GEMMs round their operands to bf16), so results equal the single-GPU layer's on bf16-representable
+tokens.  Selection and routing are per-(token, slot) local, so expert ids and masks are identical
+to the single-GPU layer; outputs agree to the fp32 tolerance (the single-GPU kernels fold the
+weights into a different, equally fixed, reduction tree).
 
-`Backend` isolates the three local computations so that the host-side logic (sorting, counts,
-all-to-all, un-sorting, combine order) is exercised by multi-process gloo tests on CPU tensors
-with an oracle backend, and by the CUDA backend (the C ABI) on the device.
+`Backend` isolates the local computations so that the host-side logic (plan, split sizes,
+all-to-all, combine order) is exercised by multi-process gloo tests on CPU tensors with an
+oracle backend, and by the CUDA backend (the C ABI) on the device.
 """
 from __future__ import annotations
 
@@ -43,11 +49,24 @@ class Backend(Protocol):
     def route(self, x: torch.Tensor):  # -> ids [B, K] int32, weights [B, K] float32
         ...
 
+    def plan(self, ids_all: torch.Tensor, expert_lo: torch.Tensor, rank: int):
+        ...  # ids_all [W, Bmax*K] int32 -> counts [W, W] int32, pos [Bmax*K] int32, local [Bmax*K] int32
+
+    def pack(self, x: torch.Tensor, pos: torch.Tensor, local: torch.Tensor, n_send: int) -> torch.Tensor:
+        ...  # -> uint8 [n_send, row_stride] packed bf16 rows + local expert ids
+
+    def unpack(self, recv: torch.Tensor, d_model: int):
+        ...  # uint8 [M, row_stride] -> rows [M, D] float32, local_ids [M] int32
+
     def experts(self, rows: torch.Tensor, local_ids: torch.Tensor, s: float) -> torch.Tensor:
         ...  # rows [M, D], local_ids [M] int32 in [0, e_hi - e_lo) -> un-weighted outputs [M, D]
 
     def shared(self, x: torch.Tensor, s: float) -> torch.Tensor:
         ...  # [B, D] -> shared-expert output [B, D]
+
+    def combine(self, back: torch.Tensor, pos: torch.Tensor, w: torch.Tensor,
+                shared: Optional[torch.Tensor]) -> torch.Tensor:
+        ...  # back [n_send, D], pos [B*K], w [B, K] -> y [B, D]
 
 
 def owner_ranges(n_experts: int, world: int):
@@ -61,27 +80,32 @@ def owner_ranges(n_experts: int, world: int):
     return out
 
 
+def row_stride(d_model: int) -> int:
+    """Bytes of one packed dispatch row: [D bf16][int32 local expert id], padded to 16."""
+    return (d_model * 2 + 4 + 15) // 16 * 16
+
+
 class ExpertParallelLayer:
-    def __init__(self, backend: Backend, group: Optional[dist.ProcessGroup] = None):
+    def __init__(self, backend: Backend, group: Optional[dist.ProcessGroup] = None,
+                 max_batch: Optional[int] = None):
+        """`max_batch`: the largest home batch of any rank (all ranks pass the same value); the
+        all-gathered ids are padded to it.  None: every rank's batch has the same size."""
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.max_batch = max_batch
         self.ranges = owner_ranges(backend.n_experts, self.world)
         assert self.ranges[self.rank] == (backend.e_lo, backend.e_hi), \
             "backend expert range does not match owner_ranges()"
-        # expert id -> owner rank
-        owner = torch.empty(backend.n_experts, dtype=torch.int64)
-        for r, (lo, hi) in enumerate(self.ranges):
-            owner[lo:hi] = r
-        self._owner_cpu = owner
-        self._owner = {}
+        self._lo_cpu = torch.tensor([r[0] for r in self.ranges] + [backend.n_experts], dtype=torch.int32)
+        self._lo = {}
         self.last_stats = {}
 
-    def _owner_on(self, device):
-        if device not in self._owner:
-            self._owner[device] = self._owner_cpu.to(device)
-        return self._owner[device]
+    def _lo_on(self, device):
+        if device not in self._lo:
+            self._lo[device] = self._lo_cpu.to(device)
+        return self._lo[device]
 
     def _all_to_all(self, send: torch.Tensor, send_counts, recv_counts) -> torch.Tensor:
         recv = send.new_empty((int(sum(recv_counts)),) + tuple(send.shape[1:]))
@@ -93,50 +117,50 @@ class ExpertParallelLayer:
         return recv
 
     def forward(self, x: torch.Tensor, s_routed: float, s_shared: float = 0.0) -> torch.Tensor:
-        b, K = self.b, self.b.top_k
+        b, K, W = self.b, self.b.top_k, self.world
         B, D = x.shape
         dev = x.device
         ids, w = b.route(x)                                   # [B, K]
-        flat = ids.reshape(-1).to(torch.int64)                # flat slot i = t * K + s
-        dest = self._owner_on(dev)[flat]
-        order = torch.argsort(dest, stable=True)              # slots grouped by owner rank
-        send_counts = torch.bincount(dest, minlength=self.world)
-        # counts exchange (tiny), then the rows and their local expert ids
-        if self.world > 1:
-            recv_counts = torch.empty_like(send_counts)
-            dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        Bmax = self.max_batch if self.max_batch is not None else B
+        assert B <= Bmax
+        mine = ids.reshape(-1)
+        if B < Bmax:                                          # short batch: pad with -1
+            mine = torch.cat([mine, mine.new_full(((Bmax - B) * K,), -1)])
+        if W > 1:
+            flat_all = torch.empty(W * Bmax * K, dtype=torch.int32, device=dev)
+            dist.all_gather_into_tensor(flat_all, mine.contiguous(), group=self.group)
+            ids_all = flat_all.view(W, Bmax * K)
         else:
-            recv_counts = send_counts.clone()
-        sc, rc = send_counts.tolist(), recv_counts.tolist()
-        tok = torch.div(order, K, rounding_mode="floor")
-        rows = x.index_select(0, tok)                         # [B*K, D] sorted by destination
-        lo_of_dest = torch.tensor([r[0] for r in self.ranges], device=dev)[dest[order]]
-        local = (flat[order] - lo_of_dest).to(torch.int32)
-        rows_in = self._all_to_all(rows, sc, rc)
-        ids_in = self._all_to_all(local, sc, rc)
+            ids_all = mine.reshape(1, -1)
+        counts, pos, local = b.plan(ids_all, self._lo_on(dev), self.rank)
+        cm = counts.cpu()                                     # the step's one host synchronisation
+        sc, rc = cm[self.rank].tolist(), cm[:, self.rank].tolist()
+        send = b.pack(x, pos, local, int(sum(sc)))
+        # the shared expert does not depend on the exchange: enqueue it before the all-to-all so
+        # that it runs under the transfer (replicated weights, own sparsity ratio)
+        sh = b.shared(x, s_shared) if b.has_shared else None
+        recv = self._all_to_all(send, sc, rc)
+        rows_in, ids_in = b.unpack(recv, D)
         out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
-        out_sorted = self._all_to_all(out_in, rc, sc)         # back to the home ranks
-        slot_out = torch.empty_like(out_sorted)
-        slot_out[order] = out_sorted                          # un-sort to flat slot order
-        slot_out = slot_out.view(B, K, D)
-        y = torch.zeros((B, D), dtype=x.dtype, device=dev)
-        for s in range(K):                                    # ascending slots, mul then add
-            y = y + w[:, s:s + 1] * slot_out[:, s, :]
-        if b.has_shared:
-            y = y + b.shared(x, s_shared)
+        back = self._all_to_all(out_in, rc, sc)               # back to the home ranks, send order
+        y = b.combine(back, pos, w, sh)
         self.last_stats = {"sent_rows": sc, "recv_rows": rc,
-                           "dispatch_bytes": int(sum(sc)) * D * x.element_size(),
-                           "combine_bytes": int(sum(rc)) * D * x.element_size()}
+                           "dispatch_bytes": int(sum(sc)) * row_stride(D),
+                           "combine_bytes": int(sum(rc)) * D * 4,
+                           "host_syncs": 1, "collectives": (1 if W > 1 else 0) + 2 * (W > 1)}
         return y
 
 
 class CudaBackend:
     """The C-ABI layer as EP backend: an experts slice + (optionally) a shared-expert slice of
-    generate_synthetic(full, seed, scale), both resident on this rank's GPU."""
+    generate_synthetic(full, seed, scale), both resident on this rank's GPU; plan / pack / unpack
+    / combine are the kernels of csrc/ep.cu."""
 
     def __init__(self, skb, full_cfg, seed: int, scale: float, rank: int, world: int,
                  device: int = 0, max_rows: int = 1024):
+        from . import _lib
         self.skb = skb
+        self.L = _lib.load()
         self.n_experts, self.top_k = full_cfg.n_experts, full_cfg.top_k
         self.e_lo, self.e_hi = owner_ranges(full_cfg.n_experts, world)[rank]
         self.has_shared = bool(full_cfg.has_shared)
@@ -156,6 +180,10 @@ class CudaBackend:
         # handle 0, so name it explicitly (cudaStreamLegacy == 0x1)
         return torch.cuda.current_stream().cuda_stream or 1
 
+    def _ok(self, rc, what):
+        if rc != 0:
+            raise RuntimeError(f"{what} failed with status {rc}")
+
     def route(self, x):
         B = x.shape[0]
         ids = torch.empty((B, self.top_k), dtype=torch.int32, device=x.device)
@@ -163,6 +191,33 @@ class CudaBackend:
         self.slice.reserve(B)
         self.slice.route_device(x.data_ptr(), ids.data_ptr(), w.data_ptr(), B, stream=self._stream())
         return ids, w
+
+    def plan(self, ids_all, expert_lo, rank):
+        W, slots = ids_all.shape
+        dev = ids_all.device
+        counts = torch.empty((W, W), dtype=torch.int32, device=dev)
+        pos = torch.empty(slots, dtype=torch.int32, device=dev)
+        local = torch.empty(slots, dtype=torch.int32, device=dev)
+        self._ok(self.L.skb_ep_plan(ids_all.contiguous().data_ptr(), W, slots, expert_lo.data_ptr(),
+                                    rank, counts.data_ptr(), pos.data_ptr(), local.data_ptr(),
+                                    self._stream()), "skb_ep_plan")
+        return counts, pos, local
+
+    def pack(self, x, pos, local, n_send):
+        B, D = x.shape
+        send = torch.empty((n_send, row_stride(D)), dtype=torch.uint8, device=x.device)
+        self._ok(self.L.skb_ep_pack(x.contiguous().data_ptr(), pos.data_ptr(), local.data_ptr(),
+                                    B * self.top_k, self.top_k, D, send.data_ptr(), self._stream()),
+                 "skb_ep_pack")
+        return send
+
+    def unpack(self, recv, d_model):
+        M = recv.shape[0]
+        rows = torch.empty((M, d_model), dtype=torch.float32, device=recv.device)
+        ids = torch.empty(M, dtype=torch.int32, device=recv.device)
+        self._ok(self.L.skb_ep_unpack(recv.data_ptr(), M, d_model, rows.data_ptr(), ids.data_ptr(),
+                                      self._stream()), "skb_ep_unpack")
+        return rows, ids
 
     def experts(self, rows, local_ids, s):
         M = rows.shape[0]
@@ -183,4 +238,14 @@ class CudaBackend:
         self.shared_slice.forward_device(x.data_ptr(), y.data_ptr(), B, mode=self.skb.MODE_TOPK,
                                          s_routed=s, stream=self._stream(),
                                          ids_in_ptr=self._zero_ids[B].data_ptr())
+        return y
+
+    def combine(self, back, pos, w, shared):
+        B, K = w.shape
+        D = back.shape[1] if back.dim() == 2 else self.D
+        y = torch.empty((B, D), dtype=torch.float32, device=w.device)
+        self._ok(self.L.skb_ep_combine(back.contiguous().data_ptr(), pos.data_ptr(),
+                                       w.contiguous().data_ptr(),
+                                       shared.data_ptr() if shared is not None else None,
+                                       B, K, D, y.data_ptr(), self._stream()), "skb_ep_combine")
         return y

@@ -1,6 +1,7 @@
 """Expert parallelism, host-side logic: 2 (and 3) gloo ranks on CPU tensors with an oracle
-backend against the single-process oracle layer.  Covers destination sorting, the counts and
-rows all-to-all-v, un-sorting, combine order and the replicated shared expert -- everything of
+backend against the single-process oracle layer.  Covers the all-gathered plan (send/receive
+matrix, positions), the packed rows all-to-all-v, the combine order, padded ragged batches and the
+replicated shared expert -- everything of
 paper_2605_08575_b200/ep.py except the CUDA kernels behind the backend (tests/test_gpu_parity.py)."""
 import os
 import socket
@@ -58,6 +59,61 @@ class OracleBackend:
             self._ffn(w.shared_gate, w.shared_up, w.shared_down_t, x[t].numpy(), s)
             for t in range(x.shape[0])]))
 
+    # ---- CPU restatement of csrc/ep.cu (plan / pack / unpack / combine) ----
+    def plan(self, ids_all, expert_lo, rank):
+        ids = ids_all.numpy()
+        lo = expert_lo.numpy()
+        W, slots = ids.shape
+        owner = np.where(ids >= 0, np.searchsorted(lo[1:W], np.maximum(ids, 0), side="right"), -1)
+        counts = np.zeros((W, W), np.int32)
+        for src in range(W):
+            for dst in range(W):
+                counts[src, dst] = int(np.count_nonzero(owner[src] == dst))
+        base = np.concatenate([[0], np.cumsum(counts[rank])[:-1]])
+        pos = np.full(slots, -1, np.int32)
+        local = np.zeros(slots, np.int32)
+        nxt = base.copy()
+        for i in range(slots):               # ascending flat slot inside every destination group
+            d = owner[rank, i]
+            if d >= 0:
+                pos[i] = nxt[d]
+                nxt[d] += 1
+                local[i] = ids[rank, i] - lo[d]
+        return torch.from_numpy(counts), torch.from_numpy(pos), torch.from_numpy(local)
+
+    def pack(self, x, pos, local, n_send):
+        from paper_2605_08575_b200.ep import row_stride
+        B, D = x.shape
+        K = self.top_k
+        send = np.zeros((n_send, row_stride(D)), np.uint8)
+        xb = (self.o.round_bf16(x.numpy()).view(np.uint32) >> 16).astype(np.uint16)  # bf16 bits
+        for i in range(B * K):
+            p = int(pos[i])
+            if p >= 0:
+                send[p, :2 * D] = xb[i // K].view(np.uint8)
+                send[p, 2 * D:2 * D + 4] = np.array([int(local[i])], np.int32).view(np.uint8)
+        return torch.from_numpy(send)
+
+    def unpack(self, recv, d_model):
+        r = recv.numpy()
+        M = r.shape[0]
+        bits = r[:, :2 * d_model].copy().view(np.uint16).astype(np.uint32) << 16
+        rows = bits.view(np.float32).reshape(M, d_model)
+        ids = r[:, 2 * d_model:2 * d_model + 4].copy().view(np.int32).reshape(M)
+        return torch.from_numpy(rows.copy()), torch.from_numpy(ids.copy())
+
+    def combine(self, back, pos, w, shared):
+        B, K = w.shape
+        bk = back.numpy()
+        y = np.zeros((B, bk.shape[1] if bk.ndim == 2 and bk.shape[0] else self.w.cfg.d_model), np.float32)
+        wn = w.numpy()
+        for t in range(B):
+            for s in range(K):               # ascending slots, multiply and add rounded separately
+                y[t] = y[t] + (wn[t, s] * bk[int(pos[t * K + s])]).astype(np.float32)
+            if shared is not None:
+                y[t] = y[t] + shared[t].numpy()
+        return torch.from_numpy(y)
+
 
 def _free_port():
     with socket.socket() as s:
@@ -75,12 +131,13 @@ def _worker(rank, world, port, case, out_dir):
         o = Oracle.get()
         cfg = Config(E, K, D, N, S, True)
         w = o.generate_synthetic(cfg, 5, 0.1)
-        x = o.generate_tokens(B, D, 7)
+        x = o.round_bf16(o.generate_tokens(B, D, 7))  # tokens cross the wire as bf16
         # ragged home batches: rank r takes tokens [lo, hi)
         cuts = np.linspace(0, B, world + 1).astype(int)
         cuts[1] = min(B, cuts[1] + 1) if world > 1 else cuts[1]
         mine = x[cuts[rank]:cuts[rank + 1]]
-        layer = ExpertParallelLayer(OracleBackend(w, rank, world))
+        max_batch = int(max(cuts[r + 1] - cuts[r] for r in range(world)))
+        layer = ExpertParallelLayer(OracleBackend(w, rank, world), max_batch=max_batch)
         y = layer.forward(torch.from_numpy(mine.copy()), s, s if S else 0.0)
         np.save(os.path.join(out_dir, f"y{rank}.npy"), y.numpy())
         np.save(os.path.join(out_dir, f"stats{rank}.npy"),
@@ -105,7 +162,7 @@ def test_ep_matches_single_process_oracle(tmp_path, world, case):
     o = Oracle.get()
     cfg = Config(E, K, D, N, S, True)
     w = o.generate_synthetic(cfg, 5, 0.1)
-    x = o.generate_tokens(B, D, 7)
+    x = o.round_bf16(o.generate_tokens(B, D, 7))
     routed, shared = o.build_topk_masks(w, x, s, mode=1 if S else 0)
     y_ref, _ = o.forward(w, x, routed, shared)
     y = np.concatenate([np.load(tmp_path / f"y{r}.npy") for r in range(world)])

@@ -517,6 +517,94 @@ def test_full_shapes_properties(skb, oracle, shape, B, s):
 
 
 # ---------------------------------------------------------------------------------------------
+# expert-parallel data plane on the device (world 1: the same kernels, no collective)
+# ---------------------------------------------------------------------------------------------
+def test_ep_plan_pack_combine_kernels_match_the_cpu_restatement(skb, oracle):
+    """csrc/ep.cu against the CPU restatement the gloo tests run (tests/test_ep_gloo.py), for a
+    4-rank plan seen from rank 2: counts matrix, positions, local ids, packed rows, combine."""
+    torch = pytest.importorskip("torch")
+    from paper_2605_08575_b200 import ep
+    from tests.test_ep_gloo import OracleBackend
+    from paper_2605_08575_b200 import _lib
+    L = _lib.load()
+    E, K, D, W, B, rank = 10, 3, 72, 4, 7, 2
+    rng = np.random.default_rng(3)
+    ids_all = np.stack([np.stack([rng.permutation(E)[:K] for _ in range(B)]).reshape(-1)
+                        for _ in range(W)]).astype(np.int32)
+    ids_all[1, -2 * K:] = -1          # a short batch on rank 1
+    ids_all[rank, -K:] = -1           # and on the home rank
+    lo = np.array([r[0] for r in ep.owner_ranges(E, W)] + [E], np.int32)
+
+    class _W:  # the restatement only needs these
+        class cfg:
+            n_experts, top_k, has_shared, d_model = E, K, False, D
+    ob = OracleBackend.__new__(OracleBackend)
+    ob.o, ob.top_k = oracle, K
+    ob.w = _W
+    c_ref, p_ref, l_ref = ob.plan(torch.from_numpy(ids_all), torch.from_numpy(lo), rank)
+    d_ids, d_lo = torch.from_numpy(ids_all).cuda(), torch.from_numpy(lo).cuda()
+    counts = torch.empty((W, W), dtype=torch.int32, device="cuda")
+    pos = torch.empty(B * K, dtype=torch.int32, device="cuda")
+    loc = torch.empty(B * K, dtype=torch.int32, device="cuda")
+    assert L.skb_ep_plan(d_ids.data_ptr(), W, B * K, d_lo.data_ptr(), rank, counts.data_ptr(),
+                         pos.data_ptr(), loc.data_ptr(), 1) == 0
+    np.testing.assert_array_equal(counts.cpu().numpy(), c_ref.numpy())
+    np.testing.assert_array_equal(pos.cpu().numpy(), p_ref.numpy())
+    valid = p_ref.numpy() >= 0
+    np.testing.assert_array_equal(loc.cpu().numpy()[valid], l_ref.numpy()[valid])
+    x = oracle.generate_tokens(B, D, 9)  # not bf16-representable: the pack rounds (RN)
+    n_send = int(c_ref.numpy()[rank].sum())
+    send_ref = ob.pack(torch.from_numpy(x), p_ref, l_ref, n_send).numpy()
+    send = torch.zeros((n_send, ep.row_stride(D)), dtype=torch.uint8, device="cuda")
+    dx = torch.from_numpy(x).cuda()
+    assert L.skb_ep_pack(dx.data_ptr(), pos.data_ptr(), loc.data_ptr(), B * K, K, D,
+                         send.data_ptr(), 1) == 0
+    np.testing.assert_array_equal(send.cpu().numpy()[:, :2 * D + 4], send_ref[:, :2 * D + 4])
+    rows = torch.empty((n_send, D), dtype=torch.float32, device="cuda")
+    rid = torch.empty(n_send, dtype=torch.int32, device="cuda")
+    assert L.skb_ep_unpack(send.data_ptr(), n_send, D, rows.data_ptr(), rid.data_ptr(), 1) == 0
+    r_ref, i_ref = ob.unpack(torch.from_numpy(send_ref), D)
+    np.testing.assert_array_equal(rows.cpu().numpy(), r_ref.numpy())
+    np.testing.assert_array_equal(rid.cpu().numpy(), i_ref.numpy())
+    back = rng.standard_normal((n_send, D)).astype(np.float32)
+    w = rng.random((B - 1, K)).astype(np.float32)   # the home batch is one token short
+    sh = rng.standard_normal((B - 1, D)).astype(np.float32)
+    y_ref = ob.combine(torch.from_numpy(back), p_ref, torch.from_numpy(w), torch.from_numpy(sh)).numpy()
+    y = torch.empty((B - 1, D), dtype=torch.float32, device="cuda")
+    assert L.skb_ep_combine(torch.from_numpy(back).cuda().data_ptr(), pos.data_ptr(),
+                            torch.from_numpy(w).cuda().data_ptr(), torch.from_numpy(sh).cuda().data_ptr(),
+                            B - 1, K, D, y.data_ptr(), 1) == 0
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
+
+
+@pytest.mark.parametrize("shape,B,s", [((16, 4, 256, 192, 64), 9, 0.5), ((8, 1, 320, 256, 0), 33, 0.9)])
+def test_ep_layer_world_1_equals_the_single_gpu_layer(skb, oracle, shape, B, s):
+    """ExpertParallelLayer over the CUDA backend with one rank (plan, pack, unpack, external-routing
+    forward, combine; no collective) against the single-GPU layer and the oracle."""
+    torch = pytest.importorskip("torch")
+    from paper_2605_08575_b200 import ep
+    E, K, D, N, S = shape
+    cfg = Config(E, K, D, N, S, True)
+    scfg = to_cfg(skb, cfg)
+    backend = ep.CudaBackend(skb, scfg, 1, 0.05, 0, 1, device=0, max_rows=4 * B * K)
+    layer = ep.ExpertParallelLayer(backend)
+    x = oracle.round_bf16(oracle.generate_tokens(B, D, 2))
+    y = layer.forward(torch.from_numpy(x).cuda(), s, s if S else 0.0)
+    torch.cuda.synchronize()
+    assert layer.last_stats["host_syncs"] == 1 and sum(layer.last_stats["sent_rows"]) == B * K
+    single = skb.MoELayerWeights.generate_synthetic(scfg, 1, 0.05)
+    lvl = skb.SparsityLevel(s)
+    rep = skb.forward_topk_sparse(single, x, lvl, lvl if S else None, capture=True)
+    assert max_rel_diff(y.cpu().numpy(), rep.outputs) <= TOL_FP32_ACCUM
+    w_raw = oracle.generate_synthetic(cfg, 1, 0.05)
+    w = w_raw.rounded_bf16()
+    w.router = w_raw.router
+    y_ref, _ = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if S else None)
+    assert max_rel_diff(y.cpu().numpy(), y_ref) <= TOL_FP32_ACCUM
+
+
+# ---------------------------------------------------------------------------------------------
 # C++ facade on the device
 # ---------------------------------------------------------------------------------------------
 def _lcg_fill(shape, state):
