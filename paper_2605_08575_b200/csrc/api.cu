@@ -489,22 +489,19 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     sel_mode = kSelectGiven;
   }
 
-  // Down-projection path of the staged kernels (batches above 16; smaller ones take the fused
-  // decode kernel).  Gathering surviving rows per (token, slot) moves B*K*keep rows through L2;
-  // the dense masked GEMM streams each routed expert's W_down once.  Measured on B200
-  // (tools/path_probe.py, L2 flushed): Qwen3.5 shape B=64 s=.5 gather 482 us / dense 353 us, s=.9
-  // 463 / 371; B=32 295 / 278; OLMoE shape B=32 261 / 232; Granite shape B=32 99 / 69 -- the
-  // gather only pays when it touches a small fraction of the rows the GEMM would stream.  The
-  // decision depends only on (shape, batch, s), so it is identical for forward_dense and
-  // forward_topk_sparse at s = 0.
-  bool dense_down;
+  // Down-projection path of the staged kernels (batches above 4; smaller ones take the fused
+  // decode kernel, which gathers).  Gathering surviving rows per (token, slot) moves B*K*keep rows
+  // through L2; the dense masked GEMM streams each routed expert's W_down once.  Measured on B200
+  // (tools/path_probe.py, tools/fused_vs_staged.py, tools/ep_probe.py; us, gather / dense):
+  // Qwen3.5 shape B=64 s=.5 482 / 353, s=.9 463 / 371; B=32 295 / 278; OLMoE shape B=32 261 / 232,
+  // B=8 158 / 140, B=5 116 / 100; Granite shape B=32 99 / 69, B=8 58 / 52; GPT-OSS shape B=8
+  // 257 / 211; Llama-4-Maverick shape, 64 rows with external routing at s=.9 (the expert-parallel
+  // step, gather volume 10 % of the dense one) 1931 / 631 -- the cluster gather kernel loses at
+  // every staged batch size, so the masked GEMM is the default and the gather a forced option
+  // (SKB_FLAG_GATHER_DOWN; the tests keep it honest).  The decision is identical for
+  // forward_dense and forward_topk_sparse at s = 0.
+  bool dense_down = true;
   {
-    const double keep_r = sel_mode == kSelectTopk ? g.N - n_off_r : g.N;
-    const double keep_s = sel_mode == kSelectTopk ? g.S - n_off_s : g.S;
-    const double gather_rows = static_cast<double>(BK) * keep_r + (g.has_shared ? B * keep_s : 0.0);
-    const double dense_rows =
-        static_cast<double>(g.E < BK ? g.E : BK) * g.N + (g.has_shared ? g.S : 0.0);
-    dense_down = gather_rows > 0.15 * dense_rows;
     if (a->flags & SKB_FLAG_GATHER_DOWN) dense_down = false;
     if (a->flags & SKB_FLAG_DENSE_DOWN) dense_down = true;
     // threshold selection: the survivor count is data dependent; the masked GEMM covers every case
