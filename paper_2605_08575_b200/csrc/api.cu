@@ -509,7 +509,11 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     // per-slot counts: the stand-alone selection kernel is the one that takes them
     if (budget) dense_down = true;
   }
-  const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 3;
+  // masked activations of the dense down projection as bf16 terms: one (1e-2 mode), or two --
+  // 16 mantissa bits, measured 3e-7..1e-6 of the output on every BASELINE shape
+  // (tools/h_err_probe.py); a third term (exact) bought nothing the 1e-5 bar can see and cost a
+  // third of the GEMM's MMA steps and token-tile traffic
+  const int nsplit = (a->flags & SKB_FLAG_BF16_H) ? 1 : 2;
   // 1e-5 parity mode: the tensor-core GEMMs fold long contractions chunk by chunk (gateup.cu)
   const bool precise = !(a->flags & SKB_FLAG_BF16_H);
 

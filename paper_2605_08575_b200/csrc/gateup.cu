@@ -22,9 +22,10 @@
 //     D[128, TN] = A[128, Np] * B[TN, Np]^T
 //   A = 128 output columns of the expert's W_down^T image ([Dp128][Np], K-major);
 //   B = TN rows of the MASKED activations (dropped neurons are zeros) as bf16.  To keep the
-//       fp32-accumulation parity mode (1e-5), h is split into three bf16 terms b0+b1+b2 == h
-//       exactly; the three products accumulate into the same TMEM tile (nsplit = 3).  nsplit = 1
-//       is the bf16 mode (1e-2).
+//       fp32-accumulation parity mode (1e-5), h is split into bf16 terms b0 + b1 (+ b2): two
+//       terms carry 16 mantissa bits (residual <= 2^-18 |h| per element, i.e. ~1e-6 of the
+//       output after the sum), three are exact; the products accumulate into the same TMEM tile.
+//       nsplit = 1 is the bf16 mode (1e-2).
 //   D is stored un-weighted per row (slot); combine_rows_kernel applies the router weights.
 #include "skb_internal.cuh"
 #include "tc_ptx.cuh"
@@ -171,12 +172,12 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                           (((a_row >> 7) + m) * num_k_blocks + kb) * 128, full_bar(s),
                           kPolicyEvictFirst);
           tma_load_2d(a_smem + kAll, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
-          if (MODE == 1 && nsplit > 1) {
+          if (MODE == 1 && nsplit > 1)
             tma_load_2d(a_smem + kAll + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
                         kPolicyEvictLast);
+          if (MODE == 1 && nsplit > 2)
             tma_load_2d(a_smem + kAll + 2 * kBTile, &tmap_b2, kb * kBlockK, row0, full_bar(s),
                         kPolicyEvictLast);
-          }
         }
       }
     } else if (warp == 1) {
@@ -385,12 +386,12 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
           tma_load_2d(a_smem, map_a, 0, ((a_row >> 7) * num_k_blocks + kb) * 128, full_bar(s),
                       kPolicyEvictFirst);
           tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
-          if (MODE == 1 && nsplit > 1) {
+          if (MODE == 1 && nsplit > 1)
             tma_load_2d(a_smem + kATileBytes + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
                         kPolicyEvictLast);
+          if (MODE == 1 && nsplit > 2)
             tma_load_2d(a_smem + kATileBytes + 2 * kBTile, &tmap_b2, kb * kBlockK, row0, full_bar(s),
                         kPolicyEvictLast);
-          }
         }
       }
     } else if (warp == 1) {

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
+python tools/h_err_probe.py 2>&1 | tail -5
 timeout 2400 python -m pytest tests -m gpu -q --timeout 600 -x 2>&1 | tail -4
-timeout 600 python bench.py --ep --workload maverick --batch 64 --sparsity 0.9 --steps 50 --warmup 5 --no-cpu > gpurun_out/bench_ep_maverick_w1.json 2> gpurun_out/bench_ep_maverick_w1.err; python -c "
-import json; d=json.load(open('gpurun_out/bench_ep_maverick_w1.json')); print('EP maverick w1', d['ms_per_step'], d['roofline']['frac'])"
+timeout 900 python bench.py --no-cpu --no-sweep > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 300 gpurun_out/bench_default.err
+python -c "
+import json; d=json.load(open('gpurun_out/bench_default.json')); print(d['ms_per_step'], d['layer_frac_of_hbm_roofline'], d['roofline']['stage_ms'])"
