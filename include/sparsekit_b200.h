@@ -248,6 +248,21 @@ int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask);
 /* round-half-up count used by topk_mask (host arithmetic, no device needed). */
 int skb_n_off(double s, int n, int32_t* out);
 
+/* The threshold variant's stage functions (proj/include/sparsekit/activation.hpp:41-60).
+ * skb_threshold_mask: threshold_mask (proj/src/activation.cpp:62-72) over rows*n gate
+ *   pre-activations: keep iff |silu(g)| >= tau; tau < 0 or NaN -> SKB_ECONFIG.
+ * skb_default_capacity: default_capacity (activation.cpp:74-77): top_k*d_ffn rounded up to 32.
+ * skb_compact_active: compact_active (activation.cpp:79-114), one ActiveIndexRow per token:
+ *   masks [batch][top_k][d_ffn] (masks_len bytes; a mismatch is SKB_ESHAPE as in the reference),
+ *   topk_ids [batch][top_k] -> flat [batch][capacity] of expert*d_ffn+neuron in (slot ascending,
+ *   neuron ascending) order padded with -1, active_per_slot [batch][top_k] (clamped where the
+ *   list is full), total_active [batch].  capacity < 0 -> SKB_ECONFIG. */
+int skb_threshold_mask(const float* gate_raw, int rows, int n, float tau, uint8_t* mask);
+int skb_default_capacity(int top_k, int d_ffn);
+int skb_compact_active(const uint8_t* masks, uint64_t masks_len, const int32_t* topk_ids, int batch,
+                       int top_k, int d_ffn, int capacity, int32_t* flat, int32_t* active_per_slot,
+                       int32_t* total_active);
+
 /* The "MOE1" weight file (save_weights / load_weights / weight_file_size,
  * proj/src/model.cpp:180-282): magic "MOE1", six little-endian u32 (n_experts, top_k, d_model,
  * d_ffn, d_shared, flags: bit 0 has_shared, bit 1 renormalize), then fp32 little-endian

@@ -29,6 +29,7 @@ EXPORTS = (
     "skb_layer_last_launches", "skb_layer_weight_bytes", "skb_route", "skb_align_dispatch",
     "skb_combine", "skb_mask_smallest", "skb_topk_mask", "skb_n_off", "skb_generate_tokens",
     "skb_layer_load", "skb_save_weights", "skb_weight_file_size", "skb_last_error_offset",
+    "skb_threshold_mask", "skb_default_capacity", "skb_compact_active",
     "skb_ep_row_stride", "skb_ep_plan", "skb_ep_pack", "skb_ep_unpack", "skb_ep_combine",
 )
 
@@ -109,6 +110,9 @@ def load() -> C.CDLL:
     L.skb_weight_file_size.restype = C.c_uint64
     L.skb_last_error_offset.argtypes = []
     L.skb_last_error_offset.restype = C.c_uint64
+    L.skb_threshold_mask.argtypes = [vp, C.c_int, C.c_int, C.c_float, vp]
+    L.skb_default_capacity.argtypes = [C.c_int, C.c_int]
+    L.skb_compact_active.argtypes = [vp, C.c_uint64, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]
     L.skb_ep_row_stride.argtypes = [C.c_int]
     L.skb_ep_plan.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp]
     L.skb_ep_pack.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]

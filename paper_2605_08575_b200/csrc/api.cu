@@ -1608,6 +1608,67 @@ int skb_mask_smallest(const float* h, int rows, int n, const int32_t* counts, ui
   return SKB_OK;
 }
 
+int skb_threshold_mask(const float* gate_raw, int rows, int n, float tau, uint8_t* mask) {
+  if (!(tau >= 0.0f)) return fail(SKB_ECONFIG, "threshold must be >= 0");
+  if (rows < 0 || n < 0) return fail(SKB_ESHAPE, "threshold_mask: negative size");
+  const size_t total = static_cast<size_t>(rows) * n;
+  if (total == 0) return SKB_OK;
+  if (gate_raw == nullptr || mask == nullptr) return fail(SKB_ESHAPE, "threshold_mask: null buffer");
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  float* dg = nullptr;
+  uint8_t* dm = nullptr;
+  if ((rc = dmalloc(&dg, total)) || (rc = dmalloc(&dm, total))) return rc;
+  cudaMemcpy(dg, gate_raw, total * 4, cudaMemcpyHostToDevice);
+  launch_threshold_mask(nullptr, dg, total, tau, dm);
+  cudaError_t e = cudaMemcpy(mask, dm, total, cudaMemcpyDeviceToHost);
+  cudaFree(dg);
+  cudaFree(dm);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "threshold_mask: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
+int skb_default_capacity(int top_k, int d_ffn) { return (top_k * d_ffn + 31) / 32 * 32; }
+
+int skb_compact_active(const uint8_t* masks, uint64_t masks_len, const int32_t* topk_ids, int batch,
+                       int top_k, int d_ffn, int capacity, int32_t* flat, int32_t* active_per_slot,
+                       int32_t* total_active) {
+  if (capacity < 0) return fail(SKB_ECONFIG, "compact_active: capacity must be >= 0");
+  if (batch < 0 || top_k < 0 || d_ffn < 0) return fail(SKB_ESHAPE, "compact_active: negative size");
+  const size_t slots = static_cast<size_t>(batch) * top_k;
+  if (masks_len != slots * static_cast<size_t>(d_ffn))
+    return fail(SKB_ESHAPE, "compact_active: mask size %llu != slots * d_ffn",
+                static_cast<unsigned long long>(masks_len));
+  if (batch == 0) return SKB_OK;
+  int rc = stage_device_ready();
+  if (rc) return rc;
+  uint8_t* dm = nullptr;
+  int32_t *di = nullptr, *df = nullptr, *dp = nullptr, *dt = nullptr;
+  const size_t fl = static_cast<size_t>(batch) * (capacity > 0 ? capacity : 1);
+  if ((rc = dmalloc(&dm, masks_len ? masks_len : 1)) || (rc = dmalloc(&di, slots ? slots : 1)) ||
+      (rc = dmalloc(&df, fl)) || (rc = dmalloc(&dp, slots ? slots : 1)) ||
+      (rc = dmalloc(&dt, static_cast<size_t>(batch))))
+    return rc;
+  if (masks_len) cudaMemcpy(dm, masks, masks_len, cudaMemcpyHostToDevice);
+  if (slots) cudaMemcpy(di, topk_ids, slots * 4, cudaMemcpyHostToDevice);
+  launch_compact_active(nullptr, dm, di, batch, top_k, d_ffn, capacity, df, dp, dt);
+  cudaError_t e = cudaSuccess;
+  if (capacity > 0)
+    e = cudaMemcpy(flat, df, static_cast<size_t>(batch) * capacity * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && slots) e = cudaMemcpy(active_per_slot, dp, slots * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(total_active, dt, static_cast<size_t>(batch) * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dm);
+  cudaFree(di);
+  cudaFree(df);
+  cudaFree(dp);
+  cudaFree(dt);
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess)
+    return fail(SKB_ECUDA, "compact_active: %s", cudaGetErrorString(e));
+  return SKB_OK;
+}
+
 int skb_topk_mask(const float* h, int rows, int n, double s, uint8_t* mask) {
   if (!(s >= 0.0 && s <= 1.0)) return fail(SKB_ECONFIG, "sparsity must lie in [0, 1]");
   if (rows < 1 || n < 1) return fail(SKB_ESHAPE, "topk_mask: rows and n must be >= 1");

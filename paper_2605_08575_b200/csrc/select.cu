@@ -348,4 +348,71 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
   return 1;
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// The threshold variant's index layout (activation.cpp:62-114): keep iff |silu(g)| >= tau, then
+// per token the flat list of kept (expert * N + neuron) indices in (slot ascending, neuron
+// ascending) order, padded with -1 to `capacity`, clamped where the list is full.
+// ---------------------------------------------------------------------------------------------
+// silu with the exponential evaluated in double and rounded to float: what glibc's expf returns,
+// so that values within an ulp of tau fall on the reference's side (activation.cpp:15)
+__device__ __forceinline__ float silu_ref(float x) {
+  return __fdiv_rn(x, __fadd_rn(1.0f, static_cast<float>(exp(static_cast<double>(-x)))));
+}
+
+__global__ void __launch_bounds__(256) threshold_mask_kernel(const float* __restrict__ g, size_t n,
+                                                             float tau, uint8_t* __restrict__ mask) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) mask[i] = fabsf(silu_ref(g[i])) >= tau ? 1 : 0;
+}
+
+// One CTA per token.  masks [K][N] of the token, ids [K]; flat [capacity], per_slot [K], total [1].
+__global__ void __launch_bounds__(kSelectThreads) compact_active_kernel(
+    const uint8_t* __restrict__ masks, const int32_t* __restrict__ ids, int K, int N, int capacity,
+    int32_t* __restrict__ flat, int32_t* __restrict__ per_slot, int32_t* __restrict__ total) {
+  __shared__ SelScratch sc;
+  const int t = blockIdx.x, tid = threadIdx.x;
+  masks += static_cast<size_t>(t) * K * N;
+  ids += static_cast<size_t>(t) * K;
+  flat += static_cast<size_t>(t) * capacity;
+  per_slot += static_cast<size_t>(t) * K;
+  for (int i = tid; i < capacity; i += kSelectThreads) flat[i] = -1;
+  __syncthreads();
+  int write_base = 0, buf = 0;
+  for (int s = 0; s < K; ++s) {
+    const uint8_t* m = masks + static_cast<size_t>(s) * N;
+    const int base = ids[s] * N;
+    int running = 0;  // survivors of this slot before the current block of 256 neurons
+    for (int i0 = 0; i0 < N; i0 += kSelectThreads) {
+      const int i = i0 + tid;
+      const bool keep = i < N && m[i] != 0;
+      int blk_total = 0;
+      const int rank = sel_block_rank(keep, sc, buf, blk_total);
+      buf ^= 1;
+      const int wpos = write_base + running + rank;
+      if (keep && wpos < capacity) flat[wpos] = base + i;
+      running += blk_total;
+    }
+    const int room = capacity - write_base;
+    const int actual = running < room ? running : room;
+    if (tid == 0) per_slot[s] = actual;
+    write_base += actual;
+  }
+  if (tid == 0) total[t] = write_base;
+}
+
+int launch_threshold_mask(cudaStream_t s, const float* g, size_t n, float tau, uint8_t* mask) {
+  if (n == 0) return 0;
+  threshold_mask_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(g, n, tau, mask);
+  return 1;
+}
+
+int launch_compact_active(cudaStream_t s, const uint8_t* masks, const int32_t* ids, int batch, int K,
+                          int N, int capacity, int32_t* flat, int32_t* per_slot, int32_t* total) {
+  if (batch == 0) return 0;
+  compact_active_kernel<<<batch, kSelectThreads, 0, s>>>(masks, ids, K, N, capacity, flat, per_slot,
+                                                         total);
+  return 1;
+}
+
 }  // namespace skb

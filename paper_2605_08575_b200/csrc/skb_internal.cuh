@@ -134,6 +134,10 @@ struct SelectArgs {
   int kext_routed, kext_shared;  // columns written per row (Np / Sp; pad columns are zeros)
 };
 int launch_select(const LaunchCtx& ctx, const SelectArgs& a);
+// threshold variant, stage API (activation.cpp:62-114)
+int launch_threshold_mask(cudaStream_t s, const float* g, size_t n, float tau, uint8_t* mask);
+int launch_compact_active(cudaStream_t s, const uint8_t* masks, const int32_t* ids, int batch, int K,
+                          int N, int capacity, int32_t* flat, int32_t* per_slot, int32_t* total);
 
 struct DownArgs {
   const __nv_bfloat16* wd;         // [E][Np][Dp]

@@ -736,6 +736,53 @@ def topk_mask(h, s: SparsityLevel) -> np.ndarray:
     return mask[0] if one else mask
 
 
+K_PAD_INDEX = -1  # activation.hpp: kPadIndex
+
+
+@dataclass
+class ActiveIndexRow:
+    """activation.hpp:41-49: flat[capacity] of expert * d_ffn + neuron, padded with -1."""
+    flat: np.ndarray
+    active_per_slot: np.ndarray
+    total_active: int
+
+
+def threshold_mask(gate_out, threshold: float) -> np.ndarray:
+    """activation.hpp:52 / activation.cpp:62-72: keep iff |silu(g)| >= threshold."""
+    g = np.ascontiguousarray(gate_out, dtype=np.float32)
+    mask = np.empty(g.shape, np.uint8)
+    rows = 1 if g.ndim <= 1 else int(np.prod(g.shape[:-1]))
+    n = g.shape[-1] if g.ndim else 1
+    _check(_lib.load().skb_threshold_mask(_ptr(g) if g.size else None, rows, n, float(threshold),
+                                          _ptr(mask) if g.size else None))
+    return mask
+
+
+def default_capacity(top_k: int, d_ffn: int) -> int:
+    """activation.cpp:74-77."""
+    return int(_lib.load().skb_default_capacity(top_k, d_ffn))
+
+
+def compact_active(masks, topk_ids, d_ffn: int, capacity: int):
+    """activation.hpp:58-60 / activation.cpp:79-114.  masks: [slots * d_ffn] with topk_ids [slots]
+    -> one ActiveIndexRow; masks [batch, slots, d_ffn] with topk_ids [batch, slots] -> a list."""
+    masks = np.ascontiguousarray(masks, dtype=np.uint8)
+    ids = np.ascontiguousarray(topk_ids, dtype=np.int32)
+    one = ids.ndim == 1
+    ids2 = ids.reshape(1, -1) if one else ids
+    batch, K = ids2.shape
+    cap = max(int(capacity), 0)
+    flat = np.empty((batch, cap), np.int32)
+    per = np.empty((batch, K), np.int32)
+    tot = np.empty(batch, np.int32)
+    _check(_lib.load().skb_compact_active(_ptr(masks) if masks.size else None, masks.size,
+                                          _ptr(ids2) if ids2.size else None, batch, K, d_ffn,
+                                          int(capacity), _ptr(flat) if flat.size else None,
+                                          _ptr(per) if per.size else None, _ptr(tot)))
+    rows = [ActiveIndexRow(flat[t], per[t], int(tot[t])) for t in range(batch)]
+    return rows[0] if one else rows
+
+
 def n_off(s: float, n: int) -> int:
     out = C.c_int32()
     _check(_lib.load().skb_n_off(s, n, C.byref(out)))

@@ -517,6 +517,73 @@ def test_full_shapes_properties(skb, oracle, shape, B, s):
 
 
 # ---------------------------------------------------------------------------------------------
+# the threshold variant's stage functions (activation_test.cpp:79-198)
+# ---------------------------------------------------------------------------------------------
+def test_threshold_mask_hand_cases_and_bit_exact(skb, oracle):
+    gate = np.array([2.0, -2.0, 0.01], np.float32)
+    np.testing.assert_array_equal(skb.threshold_mask(gate, 0.0), [1, 1, 1])
+    np.testing.assert_array_equal(skb.threshold_mask(gate, 1e30), [0, 0, 0])
+    np.testing.assert_array_equal(skb.threshold_mask(gate, 0.5), [1, 0, 0])  # |silu| ~ 1.762 .238 .005
+    with pytest.raises(skb.ConfigError):
+        skb.threshold_mask(gate, -1.0)
+    with pytest.raises(skb.ConfigError):
+        skb.threshold_mask(gate, float("nan"))
+    # bit-exact against the oracle, thresholds placed ON values of |silu(g)| (the >= boundary)
+    rng = SplitMix64(13)
+    g = np.array([(rng.unit() * 2 - 1) * 2.0 for _ in range(4096)], np.float32)
+    sil = np.abs(np.array([oracle.lib.ork_silu(float(v)) for v in g], np.float32))
+    for tau in [0.0, 0.01, 0.05, 0.3, 1.0, 5.0] + [float(v) for v in sil[:64]]:
+        rc, ref = oracle.threshold_mask(g, tau)
+        assert rc == 0
+        np.testing.assert_array_equal(skb.threshold_mask(g, tau), ref)
+    # the active count is non-increasing in the threshold
+    counts = [int(skb.threshold_mask(g, t).sum()) for t in (0.0, 0.01, 0.05, 0.1, 0.3, 1.0, 5.0)]
+    assert counts == sorted(counts, reverse=True)
+
+
+def test_compact_active_hand_cases_round_trip_and_bit_exact(skb, oracle):
+    assert [skb.default_capacity(1, 4), skb.default_capacity(2, 64), skb.default_capacity(3, 8),
+            skb.default_capacity(2, 16)] == [32, 128, 32, 32]
+    row = skb.compact_active(np.zeros(4, np.uint8), [2], 4, 8)
+    assert row.total_active == 0 and list(row.active_per_slot) == [0] and np.all(row.flat == -1)
+    row = skb.compact_active([1, 0, 1, 0], [2], 4, 32)
+    assert row.total_active == 2 and list(row.flat[:3]) == [8, 10, -1]
+    row = skb.compact_active([1, 1, 1, 0], [0], 4, 1)   # truncation keeps the first index
+    assert row.total_active == 1 and list(row.active_per_slot) == [1] and list(row.flat) == [0]
+    row = skb.compact_active([1, 1, 1, 1], [1, 0], 2, 3)  # the second slot takes what is left
+    assert list(row.active_per_slot) == [2, 1] and row.total_active == 3 and list(row.flat) == [2, 3, 0]
+    with pytest.raises(skb.ConfigError):
+        skb.compact_active([1, 0], [0], 2, -1)
+    with pytest.raises(skb.ShapeError):
+        skb.compact_active([1, 0, 1], [0], 2, 4)
+    # random cases: the oracle's list bit for bit (incl. capacities that clamp), batched, and the
+    # round trip back to the masks
+    rng = SplitMix64(41)
+    for trial in range(30):
+        K = 1 + rng.below(4)
+        N = 1 + rng.below(700)
+        Bt = 1 + rng.below(5)
+        cap = skb.default_capacity(K, N) if trial % 3 else rng.below(K * N + 1)
+        masks = np.array([rng.below(2) for _ in range(Bt * K * N)], np.uint8).reshape(Bt, K, N)
+        ids = np.array([rng.below(8) for _ in range(Bt * K)], np.int32).reshape(Bt, K)
+        rows = skb.compact_active(masks, ids, N, cap)
+        for t in range(Bt):
+            rc, flat, per, tot = oracle.compact_active(masks[t], ids[t], N, cap)
+            assert rc == 0
+            np.testing.assert_array_equal(rows[t].flat, flat)
+            np.testing.assert_array_equal(rows[t].active_per_slot, per)
+            assert rows[t].total_active == tot
+            if cap >= int(masks[t].sum()):
+                rebuilt = np.zeros((K, N), np.uint8)
+                cur = 0
+                for s_ in range(K):
+                    for k in range(per[s_]):
+                        rebuilt[s_, flat[cur + k] - ids[t, s_] * N] = 1
+                    cur += per[s_]
+                np.testing.assert_array_equal(rebuilt, masks[t])
+
+
+# ---------------------------------------------------------------------------------------------
 # expert-parallel data plane on the device (world 1: the same kernels, no collective)
 # ---------------------------------------------------------------------------------------------
 def test_ep_plan_pack_combine_kernels_match_the_cpu_restatement(skb, oracle):
