@@ -34,7 +34,9 @@
 #include <chrono>
 #include <cmath>
 #include <numeric>
+#include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <initializer_list>
 #include <map>
 #include <mutex>
@@ -263,6 +265,95 @@ inline MaskSet build_topk_masks(const MoELayerWeights& w, const Matrix& tokens, 
   return m;
 }
 
+// ---- quality sweep and its report file (profiler.hpp:38-83) ----
+// profiler.cpp:76-99
+inline double mean_relative_error(const Matrix& outputs, const Matrix& dense_outputs) {
+  if (outputs.rows != dense_outputs.rows || outputs.cols != dense_outputs.cols)
+    throw ShapeError("mean_relative_error: shape mismatch");
+  double total = 0.0;
+  int used = 0;
+  for (int t = 0; t < outputs.rows; ++t) {
+    const float* y = outputs.data.data() + static_cast<std::size_t>(t) * outputs.cols;
+    const float* d = dense_outputs.data.data() + static_cast<std::size_t>(t) * outputs.cols;
+    double err2 = 0.0, ref2 = 0.0;
+    for (int c = 0; c < outputs.cols; ++c) {
+      const double dv = d[c], e = static_cast<double>(y[c]) - dv;
+      err2 += e * e;
+      ref2 += dv * dv;
+    }
+    const double ref = std::sqrt(ref2);
+    if (ref >= 1e-12) {
+      total += std::sqrt(err2) / ref;
+      ++used;
+    }
+  }
+  return used ? total / used : 0.0;
+}
+
+// profiler.hpp:66-69: every point is one fused top-k forward on the device (the selection runs
+// inside the layer; same masks and outputs as build_topk_masks + forward_masked_dense).
+// Metric: any callable (outputs, dense outputs) -> double, or nullptr for 1 - rel_error.
+template <class Metric = std::nullptr_t>
+inline SweepResult sweep_cutoff(const MoELayerWeights& w, const Matrix& eval_tokens,
+                                const double* targets, std::size_t n_targets, double retention,
+                                SweepMode mode, Metric metric = nullptr) {
+  if (n_targets == 0) throw ConfigError("sweep_cutoff: no targets");
+  for (std::size_t i = 0; i < n_targets; ++i) {
+    if (!(targets[i] >= 0.0 && targets[i] <= 1.0))
+      throw ConfigError("sweep_cutoff: targets must lie in [0, 1]");
+    if (i && !(targets[i] > targets[i - 1]))
+      throw ConfigError("sweep_cutoff: targets must be strictly increasing");
+  }
+  if (!(retention > 0.0 && retention <= 1.0))
+    throw ConfigError("sweep_cutoff: retention must lie in (0, 1]");
+  const MoEConfig& cfg = w.config;
+  const ForwardReport dense = b200::forward_dense(w, eval_tokens);
+  const bool rs = mode == SweepMode::kRoutedAndShared && cfg.has_shared;
+  const auto point_at = [&](double target) {
+    MaskSet masks;
+    const SparsityLevel lvl(target);
+    const ForwardReport rep =
+        forward_topk_sparse(w, eval_tokens, lvl, rs ? lvl : SparsityLevel(0.0), 1, &masks);
+    SweepPoint p;
+    p.target = target;
+    p.rel_error = b200::mean_relative_error(rep.outputs, dense.outputs);
+    if constexpr (std::is_same<Metric, std::nullptr_t>::value)
+      p.quality = 1.0 - p.rel_error;
+    else
+      p.quality = metric(rep.outputs, dense.outputs);
+    p.achieved_routed = rep.achieved_routed_sparsity;
+    std::uint64_t shared_off = 0;
+    if (rs)
+      for (std::uint8_t m : masks.shared) shared_off += m ? 0 : 1;
+    const std::uint64_t routed = static_cast<std::uint64_t>(eval_tokens.rows) * cfg.top_k * cfg.d_ffn;
+    const std::uint64_t per_token = static_cast<std::uint64_t>(cfg.top_k) * cfg.d_ffn + cfg.d_shared;
+    p.achieved_total = static_cast<double>(routed - rep.active_neurons_total + shared_off) /
+                       static_cast<double>(static_cast<std::uint64_t>(eval_tokens.rows) * per_token);
+    p.path = mode == SweepMode::kRoutedOnly ? "R" : "R+S";
+    return p;
+  };
+  const SweepPoint zero = point_at(0.0);  // the floor always refers to the zero-sparsity point
+  SweepResult out;
+  for (std::size_t i = 0; i < n_targets; ++i)
+    out.points.push_back(targets[i] == 0.0 ? zero : point_at(targets[i]));
+  for (const SweepPoint& p : out.points)
+    if (p.quality >= retention * zero.quality && p.target > out.cutoff) out.cutoff = p.target;
+  return out;
+}
+
+// profiler.hpp:79-83 (C stdio instead of <filesystem>/<fstream>: the facade stays header-light)
+inline void emit_report(const SweepResult& result, const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "w");
+  if (!f) throw IoError("cannot open for writing: " + path);
+  bool ok = std::fputs("target,achieved_total,achieved_routed,quality,rel_error,path\n", f) >= 0;
+  for (const SweepPoint& p : result.points)
+    ok = ok && std::fprintf(f, "%.9g,%.9g,%.9g,%.9g,%.9g,%s\n", p.target, p.achieved_total,
+                            p.achieved_routed, p.quality, p.rel_error, p.path.c_str()) > 0;
+  if (!result.points.empty()) ok = ok && std::fprintf(f, "# cutoff=%.9g\n", result.cutoff) > 0;
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) throw IoError("write failed: " + path);
+}
+
 // model.cpp:168-178: the standard-normal token batch profile_tipping probes with (host libm,
 // bit-identical to the reference's generate_tokens on the same host).
 inline Matrix generate_tokens(int batch, int d_model, std::uint64_t seed) {
@@ -393,6 +484,26 @@ inline std::vector<std::uint8_t> topk_mask(const float* h, std::size_t n, Sparsi
   std::vector<std::uint8_t> mask(n);
   detail::check(skb_topk_mask(h, 1, static_cast<int>(n), s.s, mask.data()));
   return mask;
+}
+
+// activation.hpp:42-64: the threshold variant's stage functions (pointer + length where the
+// reference takes std::span, so that the facade compiles as C++17)
+inline std::vector<std::uint8_t> threshold_mask(const float* gate_out, std::size_t n, float threshold) {
+  std::vector<std::uint8_t> mask(n);
+  detail::check(skb_threshold_mask(gate_out, 1, static_cast<int>(n), threshold, mask.data()));
+  return mask;
+}
+inline int default_capacity(int top_k, int d_ffn) { return skb_default_capacity(top_k, d_ffn); }
+inline ActiveIndexRow compact_active(const std::uint8_t* masks, std::size_t n_masks,
+                                     const std::int32_t* topk_ids, std::size_t n_slots, int d_ffn,
+                                     int capacity) {
+  ActiveIndexRow row;
+  row.flat.assign(static_cast<std::size_t>(capacity > 0 ? capacity : 0), kPadIndex);
+  row.active_per_slot.assign(n_slots, 0);
+  detail::check(skb_compact_active(masks, n_masks, topk_ids, 1, static_cast<int>(n_slots), d_ffn,
+                                   capacity, row.flat.data(), row.active_per_slot.data(),
+                                   &row.total_active));
+  return row;
 }
 
 // ---- neuron budgets (budget.hpp:29-44, budget.cpp) ----

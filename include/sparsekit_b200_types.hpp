@@ -37,6 +37,14 @@ struct InternalError : std::logic_error {
   explicit InternalError(const std::string& m) : std::logic_error(m) {}
 };
 
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct FormatError : std::runtime_error {  // errors.hpp:36-43: carries the byte offset
+  FormatError(const std::string& m, std::uint64_t at) : std::runtime_error(m), offset(at) {}
+  std::uint64_t offset;
+};
+
 struct Matrix {
   int rows = 0, cols = 0;
   std::vector<float> data;
@@ -85,8 +93,30 @@ struct SparsityLevel {
   }
 };
 
+// activation.hpp:17, 53-57
+constexpr std::int32_t kPadIndex = -1;
+struct ActiveIndexRow {
+  std::vector<std::int32_t> flat;             // capacity entries
+  std::vector<std::int32_t> active_per_slot;  // one count per slot
+  std::int32_t total_active = 0;
+};
+
 enum class ExecPath { kDense, kSparse };
 enum class SweepMode { kRoutedOnly, kRoutedAndShared };
+
+// profiler.hpp:49-61
+struct SweepPoint {
+  double target = 0.0;
+  double achieved_total = 0.0;
+  double achieved_routed = 0.0;
+  double quality = 0.0;
+  double rel_error = 0.0;
+  std::string path;  // "R" or "R+S"
+};
+struct SweepResult {
+  std::vector<SweepPoint> points;
+  double cutoff = 0.0;
+};
 
 struct ForwardReport {
   Matrix outputs;

@@ -368,6 +368,10 @@ class Ref:
         L.ref_scalar_forward.argtypes = [C.c_void_p, f32p, C.c_int, C.c_void_p, C.c_void_p, f32p]
         L.ref_calibrate_tau.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_uint64, C.c_uint64,
                                         C.c_uint64, C.POINTER(C.c_double)]
+        f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+        L.ref_sweep_cutoff.argtypes = [C.c_void_p, f32p, C.c_int, f64p, C.c_int, C.c_double, C.c_int,
+                                       f64p, C.POINTER(C.c_double), C.c_char_p]
+        L.ref_emit_report.argtypes = [f64p, C.c_int, C.c_char_p, C.c_double, C.c_char_p]
         L.ref_route.argtypes = [f32p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, f32p]
         L.ref_align_dispatch.argtypes = [i32p, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p,
                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
@@ -502,6 +506,17 @@ class RefLayer:
         self._check(self.ref.lib.ref_scalar_forward(self.h, x, x.shape[0], _opt(routed),
                                                     _opt(shared), y))
         return y
+
+    def sweep_cutoff(self, x, targets, retention, mode=1, csv=None):
+        """profiler.cpp:152-219 (default metric) -> (points [n][5], cutoff); csv: emit_report path."""
+        x = np.ascontiguousarray(x, np.float32)
+        t = np.ascontiguousarray(targets, np.float64)
+        pts = np.zeros((t.size, 5), np.float64)
+        cut = C.c_double()
+        self._check(self.ref.lib.ref_sweep_cutoff(self.h, x, x.shape[0], t, t.size, retention, mode,
+                                                  pts, C.byref(cut),
+                                                  None if csv is None else str(csv).encode()))
+        return pts, cut.value
 
     def calibrate_tau(self, target, calib_batch=16, token_seed=3, sample_cap=1 << 20, seed=4):
         tau = C.c_double()

@@ -251,6 +251,42 @@ int ref_calibrate_tau(void* h, double target_total, int calib_batch, std::uint64
   });
 }
 
+// sweep_cutoff (profiler.cpp:152-219) with the default quality metric; points as rows of
+// {target, achieved_total, achieved_routed, quality, rel_error}; optionally emit_report to a file.
+int ref_sweep_cutoff(void* h, const float* x, int batch, const double* targets, int n_targets,
+                     double retention, int mode, double* points, double* cutoff, const char* csv) {
+  auto* w = static_cast<sk::MoELayerWeights*>(h);
+  return guarded([&] {
+    const sk::SweepResult r = sk::sweep_cutoff(
+        *w, to_matrix(x, batch, w->config.d_model),
+        std::span<const double>(targets, static_cast<std::size_t>(n_targets)), retention,
+        mode == 1 ? sk::SweepMode::kRoutedAndShared : sk::SweepMode::kRoutedOnly);
+    for (std::size_t i = 0; i < r.points.size(); ++i) {
+      const sk::SweepPoint& p = r.points[i];
+      double* o = points + 5 * i;
+      o[0] = p.target, o[1] = p.achieved_total, o[2] = p.achieved_routed, o[3] = p.quality, o[4] = p.rel_error;
+    }
+    *cutoff = r.cutoff;
+    if (csv != nullptr) sk::emit_report(r, csv);
+  });
+}
+
+// emit_report (profiler.cpp:221-243) of caller-given points: pins the file format
+int ref_emit_report(const double* points, int n, const char* label, double cutoff, const char* csv) {
+  return guarded([&] {
+    sk::SweepResult r;
+    for (int i = 0; i < n; ++i) {
+      sk::SweepPoint p;
+      const double* o = points + 5 * i;
+      p.target = o[0], p.achieved_total = o[1], p.achieved_routed = o[2], p.quality = o[3], p.rel_error = o[4];
+      p.path = label;
+      r.points.push_back(p);
+    }
+    r.cutoff = cutoff;
+    sk::emit_report(r, csv);
+  });
+}
+
 // ---- stage functions -----------------------------------------------------
 
 int ref_route(const float* logits, int batch, int n_experts, int top_k, int renorm,

@@ -662,6 +662,139 @@ def build_topk_masks(w: MoELayerWeights, tokens, s: SparsityLevel,
     return MaskSet(rep.masks.routed, rep.masks.shared if shared is not None else None)
 
 
+# ---- quality sweep and its report file (profiler.hpp:38-83) ------------------------------------
+REPORT_HEADER = "target,achieved_total,achieved_routed,quality,rel_error,path"
+
+
+@dataclass
+class SweepPoint:
+    """profiler.hpp:49-56"""
+    target: float = 0.0
+    achieved_total: float = 0.0
+    achieved_routed: float = 0.0
+    quality: float = 0.0
+    rel_error: float = 0.0
+    path: str = ""   # "R" or "R+S"
+
+
+@dataclass
+class SweepResult:
+    """profiler.hpp:58-61"""
+    points: list = field(default_factory=list)
+    cutoff: float = 0.0
+
+
+def mean_relative_error(outputs, dense_outputs) -> float:
+    """profiler.cpp:76-99: mean over tokens of ||y - y_dense|| / ||y_dense|| in double; tokens
+    whose dense norm is below 1e-12 are left out; no token left: 0."""
+    y = np.asarray(outputs, np.float64)
+    d = np.asarray(dense_outputs, np.float64)
+    if y.shape != d.shape:
+        raise ShapeError("mean_relative_error: shape mismatch")
+    ref = np.sqrt((d * d).sum(axis=1))
+    err = np.sqrt(((y - d) ** 2).sum(axis=1))
+    ok = ref >= 1e-12
+    return float((err[ok] / ref[ok]).mean()) if ok.any() else 0.0
+
+
+def sweep_cutoff(w: MoELayerWeights, eval_tokens, targets: Sequence[float], retention: float,
+                 mode: int = SWEEP_ROUTED_AND_SHARED, metric=None) -> SweepResult:
+    """profiler.hpp:66-69 / profiler.cpp:152-219: the masked-dense quality sweep, every point one
+    fused top-k forward on the device (selection inside the layer instead of build_topk_masks +
+    forward_masked_dense; same masks, same outputs)."""
+    targets = [float(t) for t in targets]
+    if not targets:
+        raise ConfigError("sweep_cutoff: no targets")
+    for i, t in enumerate(targets):
+        if not (0.0 <= t <= 1.0):
+            raise ConfigError("sweep_cutoff: targets must lie in [0, 1]")
+        if i > 0 and not (t > targets[i - 1]):
+            raise ConfigError("sweep_cutoff: targets must be strictly increasing")
+    if not (0.0 < retention <= 1.0):
+        raise ConfigError("sweep_cutoff: retention must lie in (0, 1]")
+    cfg = w.config
+    x = np.ascontiguousarray(eval_tokens, np.float32)
+    dense = forward_dense(w, x)
+    with_shared = mode == SWEEP_ROUTED_AND_SHARED and cfg.has_shared
+    label = "R" if mode == SWEEP_ROUTED_ONLY else "R+S"
+    B = x.shape[0]
+
+    def evaluate(target: float) -> SweepPoint:
+        lvl = SparsityLevel(target)
+        rep = forward_topk_sparse(w, x, lvl, lvl if with_shared else None, capture=True)
+        rel = mean_relative_error(rep.outputs, dense.outputs)
+        masked_shared = int((rep.masks.shared == 0).sum()) if with_shared else 0
+        routed_neurons = B * cfg.top_k * cfg.d_ffn
+        masked_routed = routed_neurons - rep.active_neurons_total
+        per_token = cfg.top_k * cfg.d_ffn + cfg.d_shared
+        return SweepPoint(target=target,
+                          achieved_total=(masked_routed + masked_shared) / float(B * per_token),
+                          achieved_routed=rep.achieved_routed_sparsity,
+                          quality=metric(rep.outputs, dense.outputs) if metric else 1.0 - rel,
+                          rel_error=rel, path=label)
+
+    baseline = evaluate(0.0)  # the quality floor always refers to the zero-sparsity point
+    res = SweepResult()
+    for t in targets:
+        res.points.append(baseline if t == 0.0 else evaluate(t))
+    floor = retention * baseline.quality
+    for p in res.points:
+        if p.quality >= floor:
+            res.cutoff = max(res.cutoff, p.target)
+    return res
+
+
+def emit_report(result: SweepResult, path) -> None:
+    """profiler.hpp:79-82 / profiler.cpp:221-243: CSV, 9 significant digits, '# cutoff=' trailer."""
+    try:
+        with open(path, "w", newline="") as f:
+            f.write(REPORT_HEADER + "\n")
+            for p in result.points:
+                f.write("%.9g,%.9g,%.9g,%.9g,%.9g,%s\n" % (p.target, p.achieved_total,
+                                                           p.achieved_routed, p.quality,
+                                                           p.rel_error, p.path))
+            if result.points:
+                f.write("# cutoff=%.9g\n" % result.cutoff)
+    except OSError as exc:
+        raise IoError(f"cannot open for writing: {path}") from exc
+
+
+def read_report(path) -> SweepResult:
+    """profiler.cpp:245-286; FormatError carries the byte offset of the offending line."""
+    try:
+        with open(path, "r", newline="") as f:
+            text = f.read()
+    except OSError as exc:
+        raise IoError(f"cannot open for reading: {path}") from exc
+    lines = text.split("\n")
+    if text.endswith("\n"):
+        lines = lines[:-1]
+    if not lines or lines[0] != REPORT_HEADER:
+        raise FormatError("missing report header", 0)
+    offset = len(lines[0]) + 1
+    res = SweepResult()
+    for line in lines[1:]:
+        if line.startswith("# cutoff="):
+            res.cutoff = _strtod(line[9:])
+        elif line:
+            parts = line.split(",", 5)
+            if len(parts) < 5:
+                raise FormatError("short report row", offset)
+            if len(parts) < 6:
+                raise FormatError("report row missing path", offset)
+            vals = [_strtod(v) for v in parts[:5]]
+            res.points.append(SweepPoint(*vals, path=parts[5]))
+        offset += len(line) + 1
+    return res
+
+
+def _strtod(text: str) -> float:
+    """strtod semantics: the longest numeric prefix, 0.0 when there is none."""
+    import re
+    m = re.match(r"\s*[-+]?(?:inf(?:inity)?|nan|(?:\d+\.?\d*|\.\d+)(?:[eE][-+]?\d+)?)", text, re.I)
+    return float(m.group(0)) if m else 0.0
+
+
 # ---- stage functions --------------------------------------------------------------------------
 def route(logits, top_k: int, renormalize: bool) -> RouteResult:
     """router.hpp:34 / router.cpp:13-68."""

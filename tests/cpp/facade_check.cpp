@@ -149,6 +149,25 @@ int main() {
       return 1;
     }
   }
+  {
+    // threshold stage functions (activation_test.cpp:117-153) and the quality sweep + report file
+    const std::uint8_t m4[] = {1, 1, 1, 1};
+    const std::int32_t id2[] = {1, 0};
+    const ActiveIndexRow row = b200::compact_active(m4, 4, id2, 2, 2, 3);
+    const float gate3[] = {2.0f, -2.0f, 0.01f};
+    const double targets[] = {0.0, 0.5, 0.9};
+    const SweepResult sw = b200::sweep_cutoff(w, x, targets, 3, 0.5, SweepMode::kRoutedAndShared);
+    b200::emit_report(sw, "facade_report.csv");
+    if (row.flat != std::vector<std::int32_t>{2, 3, 0} || row.total_active != 3 ||
+        row.active_per_slot != std::vector<std::int32_t>{2, 1} || b200::default_capacity(3, 8) != 32 ||
+        b200::threshold_mask(gate3, 3, 0.5f) != std::vector<std::uint8_t>{1, 0, 0} ||
+        sw.points.size() != 3 || sw.points[0].rel_error != 0.0 || sw.points[0].quality != 1.0 ||
+        !(sw.points[1].rel_error > 0.0) || !(sw.points[2].rel_error >= sw.points[1].rel_error) ||
+        sw.points[2].path != "R+S" || sw.points[1].achieved_routed != 0.5) {
+      std::printf("FAIL: threshold stage functions / sweep_cutoff\n");
+      return 1;
+    }
+  }
   bool threw = false;
   try {
     Matrix bad(2, 64);

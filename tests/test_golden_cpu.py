@@ -145,3 +145,36 @@ def test_weight_file_size_does_not_wrap(skb):
     assert skb.weight_file_size(big) == 0
     ok = skb.MoEConfig(4, 2, 8, 16, False, 0, True, 64)
     assert skb.weight_file_size(ok) == 28 + 4 * 8 * 4 + 3 * 4 * 16 * 8 * 4
+
+
+def test_report_file_is_the_reference_byte_for_byte(skb, ref, tmp_path):
+    """emit_report / read_report (profiler.cpp:221-286): our writer against the reference's own on
+    the same points, the parse back, and the FormatError offsets."""
+    import numpy as np
+    pts = np.array([[0.0, 0.0, 0.0, 1.0, 0.0],
+                    [0.25, 0.249987654321, 0.25, 0.987654321987, 1.2345678912e-2],
+                    [0.5, 0.5, 0.5, 1.0 / 3.0, 2.0 / 3.0],
+                    [0.9, 0.8999999999, 0.9, 1e-12, 123456789.123]], np.float64)
+    theirs = tmp_path / "ref.csv"
+    assert ref.lib.ref_emit_report(pts, len(pts), b"R+S", 0.5, str(theirs).encode()) == 0
+    res = skb.SweepResult([skb.SweepPoint(*row, path="R+S") for row in pts], 0.5)
+    ours = tmp_path / "ours.csv"
+    skb.emit_report(res, ours)
+    assert ours.read_bytes() == theirs.read_bytes()
+    back = skb.read_report(theirs)
+    assert back.cutoff == 0.5 and len(back.points) == 4 and back.points[1].path == "R+S"
+    assert back.points[2].quality == float("%.9g" % (1.0 / 3.0))
+    empty = tmp_path / "empty.csv"
+    skb.emit_report(skb.SweepResult(), empty)
+    assert empty.read_text() == skb.REPORT_HEADER + "\n"   # no cutoff line without points
+    bad = tmp_path / "bad.csv"
+    bad.write_text("not the header\n")
+    with pytest.raises(skb.FormatError) as e:
+        skb.read_report(bad)
+    assert e.value.offset == 0
+    bad.write_text(skb.REPORT_HEADER + "\n0,0,0,1,0,R\n0.5,0.5\n")
+    with pytest.raises(skb.FormatError) as e:
+        skb.read_report(bad)
+    assert e.value.offset == len(skb.REPORT_HEADER) + 1 + len("0,0,0,1,0,R") + 1
+    with pytest.raises(skb.IoError):
+        skb.read_report(tmp_path / "missing.csv")

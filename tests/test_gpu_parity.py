@@ -517,6 +517,38 @@ def test_full_shapes_properties(skb, oracle, shape, B, s):
 
 
 # ---------------------------------------------------------------------------------------------
+# the quality sweep (profiler_test.cpp:147-186) on the device
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sweep_cutoff_matches_the_reference(skb, oracle, ref, mode, tmp_path):
+    from oracle.pyoracle import RefLayer
+    cfg = Config(8, 2, 64, 96, 32, True)
+    lay = RefLayer.synthetic(cfg, 3, 0.1).round_bf16()
+    w = lay.weights()
+    x = oracle.round_bf16(oracle.generate_tokens(6, cfg.d_model, 11))
+    targets = [0.0, 0.25, 0.5, 0.75, 0.9]
+    pts_ref, cut_ref = lay.sweep_cutoff(x, targets, 0.9, mode, csv=tmp_path / "ref.csv")
+    layer = make_layer(skb, w)
+    res = skb.sweep_cutoff(layer, x, targets, 0.9, mode)
+    assert [p.path for p in res.points] == ["R" if mode == 0 else "R+S"] * 5
+    got = np.array([[p.target, p.achieved_total, p.achieved_routed, p.quality, p.rel_error]
+                    for p in res.points])
+    np.testing.assert_array_equal(got[:, :3], pts_ref[:, :3])        # counts: exact
+    np.testing.assert_allclose(got[:, 3:], pts_ref[:, 3:], atol=2e-6)  # fp32 outputs: 1e-5 class
+    assert res.cutoff == cut_ref
+    assert got[0, 4] == 0.0 and got[0, 3] == 1.0   # the zero-sparsity point is the dense forward
+    skb.emit_report(res, tmp_path / "ours.csv")
+    back = skb.read_report(tmp_path / "ours.csv")
+    assert back.cutoff == float("%.9g" % res.cutoff) and len(back.points) == 5
+    with pytest.raises(skb.ConfigError):
+        skb.sweep_cutoff(layer, x, [], 0.9, mode)
+    with pytest.raises(skb.ConfigError):
+        skb.sweep_cutoff(layer, x, [0.5, 0.25], 0.9, mode)
+    with pytest.raises(skb.ConfigError):
+        skb.sweep_cutoff(layer, x, [0.5], 0.0, mode)
+
+
+# ---------------------------------------------------------------------------------------------
 # the threshold variant's stage functions (activation_test.cpp:79-198)
 # ---------------------------------------------------------------------------------------------
 def test_threshold_mask_hand_cases_and_bit_exact(skb, oracle):
