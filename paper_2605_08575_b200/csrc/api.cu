@@ -122,6 +122,7 @@ struct skb_layer {
   uint64_t weight_bytes = 0;
   CUtensorMap tmap_w{};
   CUtensorMap tmap_w3{};  // fused decode kernel: quarter-tile pieces of the same image
+  CUtensorMap tmap_w3g{};  // ... and the 16 gate rows of a quarter (threshold mode)
   CUtensorMap tmap_wdt{}, tmap_wdt_shared{};
 
   // workspaces, sized for cap_batch
@@ -387,6 +388,9 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
     rc = encode_bf16_3d(&L->tmap_w3, L->d_wgu, 128, gu_rows / 128 * (g.Dp / kBlockK), kBlockK * 2,
                         128 * kBlockK * 2, 32, 4, /*swizzle=*/false);
   if (!rc)
+    rc = encode_bf16_3d(&L->tmap_w3g, L->d_wgu, 128, gu_rows / 128 * (g.Dp / kBlockK), kBlockK * 2,
+                        128 * kBlockK * 2, 16, 4, /*swizzle=*/false);
+  if (!rc)
     rc = encode_bf16_2d(&L->tmap_wdt, L->d_wdt,
                         static_cast<uint64_t>(g.E) * g.Dp128 * (g.Np / kBlockK), kBlockK, 128);
   if (!rc && g.has_shared)
@@ -519,11 +523,13 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
 
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
-      sel_mode != kSelectThreshold && !budget &&
+      !budget &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
                     SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
       ((a->flags & SKB_FLAG_FUSED_DECODE) ||
-       decode_fused_preferred(g, B, sel_mode == kSelectTopk ? g.N - n_off_r : g.N,
+       decode_fused_preferred(g, B,
+                              sel_mode == kSelectTopk ? g.N - n_off_r
+                                                      : (sel_mode == kSelectThreshold ? g.N / 2 : g.N),
                               sel_mode == kSelectTopk ? g.S - n_off_s : g.S))) {
     const bool want_masks = d_mask_out_r != nullptr || d_mask_out_s != nullptr;
     DecodeLaunch dl{};
@@ -535,6 +541,9 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dl.sel_mode = sel_mode;
     dl.n_off_r = n_off_r;
     dl.n_off_s = n_off_s;
+    dl.tau = a->tau;
+    dl.wgu = L->d_wgu;
+    dl.kcnt = L->d_kcnt;
     dl.mask_r = d_mask_r;
     dl.mask_s = d_mask_s;
     dl.CH = decode_chunks(g, B, max_keep, L->n_sms);
@@ -554,7 +563,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     tm.mark();
     tm.mark();
     tm.mark();
-    launches += launch_decode_fused(ctx, &L->tmap_w3, dl, g, L->n_sms);
+    launches += launch_decode_fused(ctx, &L->tmap_w3, &L->tmap_w3g, dl, g, L->n_sms);
     tm.mark();
     if (want_masks) {
       SelectArgs sa{};
@@ -573,6 +582,12 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
       sa.n_off_shared = n_off_s;
       sa.mask_in_routed = d_mask_r;
       sa.mask_in_shared = d_mask_s;
+      if (sel_mode == kSelectThreshold) {
+        // the fused kernel's routed rows hold silu(gate) in this mode (the up projection is
+        // only ever computed for the survivors)
+        sa.sg = L->d_h;
+        sa.tau = a->tau;
+      }
       LaunchCtx plain{stream, false};
       launches += launch_select(plain, sa);
     }

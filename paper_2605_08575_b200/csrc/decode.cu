@@ -96,7 +96,8 @@ enum {
   kCtrRoute = 3,
   kCtrChain = 4,   // [4]
   kCtrCnt = 40,    // [1 + kDecMaxU] finished gate/up pieces: [0] shared expert, [1 + u] union expert u
-  kCtrWords = kCtrCnt + 1 + kDecMaxU + 7
+  kCtrKept = kCtrCnt + 1 + kDecMaxU + 7,  // [16 * 20] threshold mode: survivors per candidate row
+  kCtrWords = kCtrKept + 16 * 20
 };
 
 struct DecSmem {
@@ -276,6 +277,9 @@ struct DecodeArgs {
   const __nv_bfloat16* wd_shared;
   int B, E, K, D, Dp, N, Np, S, Sp, Nh, has_shared, renorm;
   int sel_mode, n_off_r, n_off_s;
+  float tau;                     // kSelectThreshold: a routed neuron is kept iff |silu(g)| >= tau
+  const __nv_bfloat16* wgu;      // the tiled gate/up image (threshold mode gathers W_up rows from it)
+  int32_t* kcnt;                 // kSelectThreshold: survivors per flat slot [B*K]
   const uint8_t* mask_r;
   const uint8_t* mask_s;
   int CM, CH, capture, stages, gb_rows, ND, DS;
@@ -378,7 +382,8 @@ __device__ __noinline__ RowPick kary_pick_cold(const uint32_t* keys, int n, int 
 
 template <int TB>
 __global__ void __launch_bounds__(kDecThreads, 1)
-decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArgs a) {
+decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
+                    const __grid_constant__ CUtensorMap tmap_w3g, const DecodeArgs a) {
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   const uint32_t sm_u32 = smem_u32(sm);
@@ -436,6 +441,12 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
   const int PE = 4 * NB;                    // pieces per routed expert
   const int n_sh = 4 * NBs;                 // pieces of the shared expert (come first)
   constexpr int kStoreWarps = (16 * TB + 31) / 32;  // consumer warps that store h of a piece
+  // Threshold mode (forward_sparse, engine.cpp:229-369): the routed experts stream their GATE
+  // rows only -- a piece is the 2 x 16 gate rows of two tile quarters (32 neurons), two TMA boxes
+  // of 16 rows per stage; the up rows are gathered later, only for the surviving neurons.
+  const bool thr = a.sel_mode == kSelectThreshold;
+  const int PEr = thr ? 2 * NB : PE;                 // pieces per routed expert
+  constexpr int kStoreWarpsG = TB;                   // threshold pieces: 32 x TB outputs
 
   if (warp == kWarpTma) {
     // =====================================================================================
@@ -462,10 +473,25 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
       const int n_u = misc[2];
       DEC_STAMP(0, 11);
 #pragma unroll 1
-      for (; p < n_sh + n_u * PE; p += gwn) {
+      for (; p < n_sh + n_u * PEr; p += gwn) {
         const int pr = p - n_sh;
-        const int u = pr / PE, qq = pr % PE;
-        produce(static_cast<int>(ulist[u]) * NB + (qq >> 2), qq & 3);
+        const int u = pr / PEr, qq = pr % PEr;
+        if (!thr) {
+          produce(static_cast<int>(ulist[u]) * NB + (qq >> 2), qq & 3);
+        } else {
+          const int rb = static_cast<int>(ulist[u]) * NB + (qq >> 1), hq = qq & 1;
+#pragma unroll 1
+          for (int kx = 0; kx < KX; ++kx, ++gk) {
+            const int s = gk % stages;
+            mbar_wait(empty_bar(s), ((gk / stages) & 1u) ^ 1u);
+            mbar_arrive_expect_tx(full_bar(s), kStageBytes);
+            const uint32_t dst = sm_u32 + L.ring + s * kStageBytes;
+            tma_load_3d(dst, &tmap_w3g, 0, (2 * hq) * 32, rb * KB + kx * kKBox, full_bar(s),
+                        kPolicyEvictFirst);
+            tma_load_3d(dst + kStageBytes / 2, &tmap_w3g, 0, (2 * hq + 1) * 32, rb * KB + kx * kKBox,
+                        full_bar(s), kPolicyEvictFirst);
+          }
+        }
       }
       DEC_STAMP(0, 3);
     }
@@ -517,7 +543,9 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
     const int c8 = lane & 7, rq = lane >> 3;
     constexpr int TG = TB < 4 ? TB : 4;
     int gk = 0, li = 0, p = worker ? bid : 0x3fffffff;
-    auto do_piece = [&](int u /* -1: shared */, int nb, int q, int m_valid) {
+    auto do_piece = [&](int u /* -1: shared */, int nb, int q, int m_valid, bool gate_only) {
+      // stage layout: one box of 32 rows per plane, or two boxes of 16 gate rows
+      const int plane_stride = gate_only ? 2048 : 4096, half_stride = gate_only ? kStageBytes / 2 : 2048;
       float acc[8][TB];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -529,10 +557,11 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         mbar_wait(full_bar(s), (gk / stages) & 1u);
         const int kb = kx * kKBox + gw;
         if (kb < KB) {
-          const uint4* wp = reinterpret_cast<const uint4*>(sm + L.ring + s * kStageBytes + gw * 4096) + lane;
+          const uint8_t* wp = sm + L.ring + s * kStageBytes + gw * plane_stride + lane * 16;
           uint4 wv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) wv[i] = wp[32 * i];
+          for (int i = 0; i < 8; ++i)
+            wv[i] = *reinterpret_cast<const uint4*>(wp + (i >> 2) * half_stride + (i & 3) * 512);
 #pragma unroll
           for (int tg = 0; tg < TB; tg += TG) {
             float xf[TG][8];
@@ -581,7 +610,24 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         gpart[((buf * kNumGWarps + gw) * TB + t) * 32 + myrow] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
       }
       g_sync();
-      if (gw < kStoreWarps) {
+      if (gate_only) {
+        // 32 gate rows = 32 consecutive neurons: store silu(g), the value the mask is taken of
+        if (gw < kStoreWarpsG) {
+          const int j = lane, t = gw;
+          const float* gp = gpart + (buf * kNumGWarps * TB + t) * 32;
+          float g = gp[j];
+#pragma unroll
+          for (int w = 1; w < kNumGWarps; ++w) g = __fadd_rn(g, gp[w * TB * 32 + j]);
+          const int n = nb * kNeuronBlock + 32 * q + j;
+          if (t < B && n < m_valid) {
+            const int r = rowtab[u * 16 + t];
+            if (r >= 0) a.hc[static_cast<size_t>(r) * a.Nh + n] = silu_f(g);
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(&a.ctr[kCtrCnt + 1 + u], 1u);
+        }
+      } else if (gw < kStoreWarps) {
         if (gtid < 16 * TB) {
           const int j = gtid & 15, t = gtid >> 4;
           const float* gp = gpart + (buf * kNumGWarps * TB + t) * 32;
@@ -604,15 +650,18 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
       ++li;
     };
 #pragma unroll 1
-    for (; p < n_sh; p += gwn) do_piece(-1, p >> 2, p & 3, a.S);
+    for (; p < n_sh; p += gwn) do_piece(-1, p >> 2, p & 3, a.S, false);
     tables_wait_consumers();
     DEC_STAMP(kWarpG0 * 32, 17);
     const int n_u = misc[2];
 #pragma unroll 1
-    for (; p < n_sh + n_u * PE; p += gwn) {
+    for (; p < n_sh + n_u * PEr; p += gwn) {
       const int pr = p - n_sh;
-      const int u = pr / PE, qq = pr % PE;
-      do_piece(u, qq >> 2, qq & 3, a.N);
+      const int u = pr / PEr, qq = pr % PEr;
+      if (thr)
+        do_piece(u, qq >> 1, qq & 1, a.N, true);
+      else
+        do_piece(u, qq >> 2, qq & 3, a.N, false);
       if (p == bid + ((n_sh + gwn - 1 - bid) / gwn) * gwn) DEC_STAMP(kWarpG0 * 32, 18);
     }
     DEC_STAMP(kWarpG0 * 32, 4);
@@ -980,7 +1029,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
       bool route_ready = false;
       __shared__ SelScratch sel_sc;
       // units are dealt from the CTA after the one that took the last gate/up piece
-      const int v_first = worker ? (bid - (n_sh + n_u * PE) % gwn + gwn) % gwn : n_units;
+      const int v_first = worker ? (bid - (n_sh + n_u * PEr) % gwn + gwn) % gwn : n_units;
 #pragma unroll 1
       for (int v = v_first; v < n_units; v += gwn) {
         const int pu = plist[v / CH], c = v % CH;
@@ -1011,6 +1060,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
             if (min_ == nullptr) mode = kSelectAll;
           }
         }
+        if (mode == kSelectThreshold && !routed) mode = kSelectAll;  // the shared expert stays dense
         int n_off = 0;
         if (mode == kSelectTopk) {
           n_off = routed ? a.n_off_r : a.n_off_s;
@@ -1024,7 +1074,9 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         // wait until every gate/up piece of this expert has landed (one polite poller)
         if (dtid == 0) {
           p2[8] = 0;
-          spin_until(&a.ctr[kCtrCnt + (routed ? 1 + u : 0)], static_cast<unsigned>((routed ? PE : n_sh) * kStoreWarps));
+          spin_until(&a.ctr[kCtrCnt + (routed ? 1 + u : 0)],
+                     static_cast<unsigned>(routed ? (thr ? PEr * kStoreWarpsG : PE * kStoreWarps)
+                                                  : n_sh * kStoreWarps));
         }
         hist_s[2 * dtid] = 0;
         hist_s[2 * dtid + 1] = 0;
@@ -1145,6 +1197,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
               f = valid;
             } else if (mode == kSelectGiven) {
               f = valid && min_[i] != 0;
+            } else if (mode == kSelectThreshold) {
+              f = valid && __uint_as_float(k) >= a.tau;  // k = bits of |silu(g)| (activation.cpp:62-72)
             } else {
               f = valid && k > pk.pivot;
             }
@@ -1191,11 +1245,36 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
             for (int i = 0; i < 8; ++i) acc[nt][i] = 0.0f;
           const uint4* gb = reinterpret_cast<const uint4*>(sm + L.gbuf);
           const uint32_t gb_u32 = sm_u32 + L.gbuf;
-          const int RBS = a.gb_rows;
+          // threshold mode: the buffer holds the W_down rows AND the W_up rows of a batch; the
+          // up rows come out of the tiled gate/up image (128-byte segments, one per K block)
+          const bool thr_unit = mode == kSelectThreshold;
+          const int RBS = thr_unit ? max(1, a.gb_rows / 2) : a.gb_rows;
+          float* hval = reinterpret_cast<float*>(mlist);  // [RBS] silu(g) * u of the batch's rows
+          if (thr_unit && dtid == 0) atomicAdd(&a.ctr[kCtrKept + row], static_cast<unsigned>(m));
           const int dr = kDThreads / LPR, dc = kDThreads % LPR;
 #pragma unroll 1
           for (int k0 = 0; k0 < m; k0 += RBS) {
             const int nr = min(RBS, m - k0);
+            if (thr_unit) {
+              int r = dtid / LPR, cc = dtid % LPR;
+#pragma unroll 1
+              while (r < nr) {
+                const int nn = lst[k0 + r];
+                const size_t tile = (static_cast<size_t>(e) * NB + (nn >> 6)) * KB + (cc >> 3);
+                const __nv_bfloat16* src =
+                    a.wgu + (tile * 128 + gateup_row(nn & 63, 1)) * kBlockK + (cc & 7) * 8;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 gb_u32 + static_cast<uint32_t>((RBS + r) * LPR + cc) * 16u),
+                             "l"(src)
+                             : "memory");
+                cc += dc;
+                r += dr;
+                if (cc >= LPR) {
+                  cc -= LPR;
+                  ++r;
+                }
+              }
+            }
             {
               int r = dtid / LPR, cc = dtid % LPR;
 #pragma unroll 1
@@ -1216,17 +1295,38 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
               asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
             d_sync();
+            if (thr_unit) {
+              // u = W_up[n] . x_t for the batch's rows, one warp per row; h = silu(g) * u
+              const __nv_bfloat16* xt = reinterpret_cast<const __nv_bfloat16*>(sm + L.xs) +
+                                        static_cast<size_t>(t) * Dp;
+#pragma unroll 1
+              for (int r = dwarp; r < nr; r += 8) {
+                float sacc = 0.0f;
+#pragma unroll 2
+                for (int cc = lane; cc < LPR; cc += 32) {
+                  float wf[8], xf[8];
+                  unpack8(gb[(RBS + r) * LPR + cc], wf);
+                  unpack8(*reinterpret_cast<const uint4*>(xt + cc * 8), xf);
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) sacc = fmaf(wf[i], xf[i], sacc);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+                if (lane == 0) hval[r] = __uint_as_float(keys_s[lst[k0 + r]]) * sacc;
+              }
+              d_sync();
+            }
             if (NT == 1) {
               // narrow rows: G row groups, group g takes rows g, g + G, ...
               if (lane_ok) {
 #pragma unroll 2
                 for (int r = g; r < nr; r += G)
-                  fma8(gb[r * LPR + l], __uint_as_float(keys_s[lst[k0 + r]]), acc[0]);
+                  fma8(gb[r * LPR + l], thr_unit ? hval[r] : __uint_as_float(keys_s[lst[k0 + r]]), acc[0]);
               }
             } else {
 #pragma unroll 1
               for (int r = 0; r < nr; ++r) {
-                const float hk = __uint_as_float(keys_s[lst[k0 + r]]);
+                const float hk = thr_unit ? hval[r] : __uint_as_float(keys_s[lst[k0 + r]]);
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
                   const int c8 = nt * kDThreads + dtid;
@@ -1310,6 +1410,16 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
     DEC_STAMP(kWarpD0 * 32, 19);
     if (dtid == 0) {
       spin_until(&a.ctr[kCtrDone], static_cast<unsigned>(grid));
+      if (thr) {
+        // survivors per flat slot for the report's tile accounting (engine.cpp:341-348), read
+        // before the counters go back to rest
+        for (int sl = bid; sl < B * K; sl += grid) {
+          const int tt = sl / K;
+          const int ee = __ldcg(a.ids + sl);
+          a.kcnt[sl] = static_cast<int32_t>(ld_acquire_u32(&a.ctr[kCtrKept + rowtab[uidx[ee] * 16 + tt]]));
+          a.inv[sl] = sl;
+        }
+      }
       // every CTA that gets here has read all the counters for the last time: the last one
       // through puts them back to rest and opens the next epoch
       if (atomicAdd(&a.ctr[kCtrExit], 1u) == static_cast<unsigned>(grid - 1)) {
@@ -1319,6 +1429,8 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3, const DecodeArg
         a.ctr[kCtrRoute] = 0u;
         for (int i = 0; i < 4; ++i) a.ctr[kCtrChain + i] = 0u;
         for (int i = 0; i <= n_u; ++i) a.ctr[kCtrCnt + i] = 0u;
+        if (thr)
+          for (int i = 0; i < 16 * 20; ++i) a.ctr[kCtrKept + i] = 0u;
         a.ctr[kCtrEpoch] = epoch;
       }
     }
@@ -1456,7 +1568,8 @@ int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms) {
 
 
 template <int TB>
-static void launch_tb(const cudaLaunchConfig_t& cfg, const CUtensorMap* tmap_w3, const DecodeArgs& a) {
+static void launch_tb(const cudaLaunchConfig_t& cfg, const CUtensorMap* tmap_w3,
+                      const CUtensorMap* tmap_w3g, const DecodeArgs& a) {
   // the opt-in is per device: set it on the first launch on each device
   static std::mutex mu;
   static bool attr_set[64] = {};
@@ -1470,11 +1583,11 @@ static void launch_tb(const cudaLaunchConfig_t& cfg, const CUtensorMap* tmap_w3,
       if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
   }
-  cudaLaunchKernelEx(&cfg, decode_fused_kernel<TB>, *tmap_w3, a);
+  cudaLaunchKernelEx(&cfg, decode_fused_kernel<TB>, *tmap_w3, *tmap_w3g, a);
 }
 
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const DecodeLaunch& d,
-                        const Geometry& g, int n_sms) {
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_w3g,
+                        const DecodeLaunch& d, const Geometry& g, int n_sms) {
   const int nmax = g.N > g.S ? g.N : g.S;
   const int tb = dec_tb_for(d.B);
   DecodeArgs a{};
@@ -1495,6 +1608,9 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   a.has_shared = g.has_shared;
   a.renorm = g.renorm;
   a.sel_mode = d.sel_mode;
+  a.tau = d.tau;
+  a.wgu = d.wgu;
+  a.kcnt = d.kcnt;
   a.n_off_r = d.n_off_r;
   a.n_off_s = d.n_off_s;
   a.mask_r = d.mask_r;
@@ -1541,9 +1657,9 @@ int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const 
   cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = dec_smem_layout(a.stages, a.gb_rows, nmax, tb, g.Dp).total + 1024;
   switch (tb) {
-    case 1: launch_tb<1>(cfg, tmap_w3, a); break;
-    case 2: launch_tb<2>(cfg, tmap_w3, a); break;
-    default: launch_tb<4>(cfg, tmap_w3, a); break;
+    case 1: launch_tb<1>(cfg, tmap_w3, tmap_w3g, a); break;
+    case 2: launch_tb<2>(cfg, tmap_w3, tmap_w3g, a); break;
+    default: launch_tb<4>(cfg, tmap_w3, tmap_w3g, a); break;
   }
   return 1;
 }

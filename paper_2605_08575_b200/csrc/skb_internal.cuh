@@ -167,6 +167,9 @@ struct DecodeLaunch {
   const __nv_bfloat16* wd_shared;  // [Sp][Dp] or NULL
   int B;
   int sel_mode, n_off_r, n_off_s;  // kSelect*
+  float tau;                       // kSelectThreshold
+  const __nv_bfloat16* wgu;        // tiled gate/up image (threshold mode gathers W_up rows)
+  int32_t* kcnt;                   // kSelectThreshold: survivors per flat slot [B*K]
   const uint8_t* mask_r;           // kSelectGiven: [B*K][N]
   const uint8_t* mask_s;           // kSelectGiven: [B][S] or NULL
   int CH;                          // row chunks per (token, slot): decode_chunks()
@@ -189,9 +192,10 @@ int decode_counter_words();
 int decode_cand_rows(int K);
 int decode_p0_words(const Geometry& g);
 int decode_chunks(const Geometry& g, int B, int keep_max, int n_sms);
-// tmap_w3: the gate/up image as {64 columns, 128 rows, tiles}, box {64, 32, 4}, no swizzle
-int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const DecodeLaunch& d,
-                        const Geometry& g, int n_sms);
+// tmap_w3: the gate/up image as {64 columns, 128 rows, tiles}, box {64, 32, 4}, no swizzle;
+// tmap_w3g: the same view with box {64, 16, 4} (the gate rows of one tile quarter)
+int launch_decode_fused(const LaunchCtx& ctx, const CUtensorMap* tmap_w3, const CUtensorMap* tmap_w3g,
+                        const DecodeLaunch& d, const Geometry& g, int n_sms);
 
 // weight image construction
 int launch_pack_gateup(cudaStream_t s, const float* gate, const float* up, int n_rows, int D, int Dp,

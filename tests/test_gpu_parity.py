@@ -1044,14 +1044,35 @@ def _sparse_accounting(cfg, masks_routed):
                 tiles_total=B * token_tiles, tiles_skipped=int((token_tiles - tiles).sum()))
 
 
+FUSED_SPARSE_CASES = [
+    # E, K, D, N, S, renorm, B -- the fused decode kernel's threshold mode: gate rows streamed, the
+    # up and down rows of the survivors gathered (the paper's production path)
+    (64, 8, 256, 256, 0, True, 1),
+    (32, 4, 1024, 320, 96, True, 3),      # shared expert (dense), ragged N, four tokens per lane
+    (16, 2, 2880, 192, 0, False, 2),      # rows wider than one pass of the gather threads
+    (128, 1, 320, 1100, 0, True, 4),
+]
+
+
+@pytest.mark.parametrize("case", FUSED_SPARSE_CASES)
+@pytest.mark.parametrize("tau", [0.0, 0.02, 0.2])
+def test_forward_sparse_fused_decode_vs_oracle(skb, oracle, case, tau):
+    rep = _check_forward_sparse(skb, oracle, case, tau, skb.FLAG_FUSED_DECODE)
+    assert rep.launches <= 2, "the single persistent launch (+ mask export)"
+
+
 @pytest.mark.parametrize("case", [SMALL_CASES[1], SMALL_CASES[3], SMALL_CASES[4], SMALL_CASES[6]])
 @pytest.mark.parametrize("tau", [0.0, 0.02, 0.2])
 def test_forward_sparse_vs_oracle(skb, oracle, case, tau):
+    _check_forward_sparse(skb, oracle, case, tau, skb.FLAG_NO_FUSED_DECODE)
+
+
+def _check_forward_sparse(skb, oracle, case, tau, flags):
     E, K, D, N, S, renorm, B = case
     cfg = Config(E, K, D, N, S, renorm)
     w, x = rounded_case(oracle, cfg, seed=E * 13 + N, scale=0.1, batch=B, token_seed=4)
     layer = make_layer(skb, w)
-    rep = skb.forward_sparse(layer, x, tau, capture=True)
+    rep = skb.forward_sparse(layer, x, tau, capture=True, flags=flags)
     rc, y_ref, rep_ref = oracle.forward_sparse(w, x, tau)
     assert rc == 0
     # masks: |silu(gate)| >= tau with the gate of the oracle's own fp32 matvec; values within
@@ -1084,6 +1105,7 @@ def test_forward_sparse_vs_oracle(skb, oracle, case, tau):
         assert rep.active_neurons_total == rep_ref.active_neurons_total
         assert rep.macs.up_macs == rep_ref.up_macs and rep.macs.other_macs == rep_ref.other_macs
         assert rep.tiles_total == rep_ref.tiles_total and rep.tiles_skipped == rep_ref.tiles_skipped
+    return rep
 
 
 def test_forward_sparse_limits_and_errors(skb, oracle):

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q --timeout 600 -x 2>&1 | tail -6
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q --timeout 300 -x -k "forward_sparse" 2>&1 | tail -25
