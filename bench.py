@@ -642,6 +642,26 @@ def run_ours(args):
                     e["north_star_point"] = True
                     e["ms_per_step_isolated_launch_dirty_l2"] = round(p2.time_isolated(ss, sw_steps, 3), 5)
                 sweep.append(e)
+            # the threshold runtime path on the same point (fused decode kernel: the gate rows
+            # stream alone, W_up / W_down rows are gathered for the survivors): algorithmic bytes
+            # = router + gate of the routed experts + 2 x surviving rows + token/output rows
+            tau = THRESHOLD_TAU["olmoe"]
+            tb = []
+            for xh in p2.x_host:
+                rp = skb.forward_sparse(l2, xh, tau, capture=True)
+                kept = int(np.asarray(rp.masks.routed).sum())
+                nexp = len(np.unique(np.asarray(rp.routes.ids)))
+                tb.append(sh["E"] * sh["D"] * W_BYTES + nexp * sh["N"] * sh["D"] * W_BYTES +
+                          2 * kept * sh["D"] * W_BYTES + sh["D"] * 8)
+            tot = float(np.mean(tb))
+            p2.rotation(tot)
+            m, _ = p2.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
+            sweep.append({"workload": sh["name"], "batch": 1, "mode": "threshold (forward_sparse)",
+                          "tau": tau, "achieved_routed_sparsity": round(rp.achieved_routed_sparsity, 4),
+                          "ms_per_step": round(m, 5), "tokens_per_s": round(1 / (m * 1e-3), 1),
+                          "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
+                          "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
+                          "weight_images_in_rotation": len(p2.layers)})
             # decode batch sizes on the same shape, s = 0.5
             for bb in (2, 4, 8, 16):
                 pb = Point(skb, torch, l2, sh, bb, make_layer=mk_layer)

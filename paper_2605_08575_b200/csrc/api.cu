@@ -116,6 +116,8 @@ struct skb_layer {
   float* d_router = nullptr;
   __nv_bfloat16* d_wgu = nullptr;
   __nv_bfloat16* d_wd = nullptr;
+  __nv_bfloat16* d_wu = nullptr;          // W_up rows [E][Np][Dp], row-major like W_down: the
+                                          // threshold mode of the fused decode kernel gathers them
   __nv_bfloat16* d_wd_shared = nullptr;
   __nv_bfloat16* d_wdt = nullptr;         // W_down^T image [E][Dp128][Np] (dense down projection)
   __nv_bfloat16* d_wdt_shared = nullptr;  // [Dp128][Sp]
@@ -366,6 +368,7 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
   rc = dmalloc(&L->d_router, static_cast<size_t>(L->route_E) * g.D);
   if (!rc) rc = dmalloc(&L->d_wgu, gu_rows * g.Dp);
   if (!rc) rc = dmalloc(&L->d_wd, wd_rows * g.Dp);
+  if (!rc && decode_fused_eligible(g, 1)) rc = dmalloc(&L->d_wu, static_cast<size_t>(g.E) * g.Np * g.Dp);
   if (rc) {
     skb_layer_destroy(L);
     return rc;
@@ -378,10 +381,12 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
   }
   L->d_wd_shared = g.has_shared ? L->d_wd + static_cast<size_t>(g.E) * g.Np * g.Dp : nullptr;
   L->d_wdt_shared = g.has_shared ? L->d_wdt + static_cast<size_t>(g.E) * g.Dp128 * g.Np : nullptr;
-  L->weight_bytes = static_cast<uint64_t>(g.E) * g.D * 4 + (gu_rows + wd_rows) * g.Dp * 2 + wdt_elems * 2;
+  L->weight_bytes = static_cast<uint64_t>(g.E) * g.D * 4 + (gu_rows + wd_rows) * g.Dp * 2 + wdt_elems * 2 +
+                    (L->d_wu ? static_cast<uint64_t>(g.E) * g.Np * g.Dp * 2 : 0);
   cudaMemsetAsync(L->d_wdt, 0, wdt_elems * 2, L->stream);
   cudaMemsetAsync(L->d_wgu, 0, gu_rows * g.Dp * 2, L->stream);
   cudaMemsetAsync(L->d_wd, 0, wd_rows * g.Dp * 2, L->stream);
+  if (L->d_wu) cudaMemsetAsync(L->d_wu, 0, static_cast<size_t>(g.E) * g.Np * g.Dp * 2, L->stream);
   // tiled images: the tensor maps see them as [n_tiles * 128][64] (tiled_index())
   rc = encode_bf16_2d(&L->tmap_w, L->d_wgu, gu_rows * (g.Dp / kBlockK), kBlockK, 128);
   if (!rc)  // the same image as planes of 128 x 64 tiles: a box is 32 rows of 4 consecutive tiles
@@ -523,7 +528,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
 
   // Decode batches: the whole layer as one persistent launch (decode.cu).
   if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
-      !budget &&
+      !budget && (sel_mode != kSelectThreshold || L->d_wu != nullptr) &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
                     SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
       ((a->flags & SKB_FLAG_FUSED_DECODE) ||
@@ -542,7 +547,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     dl.n_off_r = n_off_r;
     dl.n_off_s = n_off_s;
     dl.tau = a->tau;
-    dl.wgu = L->d_wgu;
+    dl.wu = L->d_wu;
     dl.kcnt = L->d_kcnt;
     dl.mask_r = d_mask_r;
     dl.mask_s = d_mask_s;
@@ -1135,6 +1140,8 @@ int skb_layer_create(const skb_config* cfg, const float* router, const float* co
     if (e == cudaSuccess) e = cudaMemcpyAsync(sb, up[ex], bytes, cudaMemcpyHostToDevice, L->stream);
     launch_pack_gateup(L->stream, sa, sb, g.N, g.D, g.Dp,
                        L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
+    if (L->d_wu)
+      launch_pack_rows(L->stream, sb, g.N, g.D, g.Dp, L->d_wu + static_cast<size_t>(ex) * g.Np * g.Dp);
     if (e == cudaSuccess) e = cudaMemcpyAsync(sa, down_t[ex], bytes, cudaMemcpyHostToDevice, L->stream);
     launch_pack_rows(L->stream, sa, g.N, g.D, g.Dp, L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
     launch_pack_down_t(L->stream, sa, g.N, g.D, g.Np,
@@ -1181,6 +1188,9 @@ int skb_layer_create_synthetic(const skb_config* cfg, uint64_t seed, float scale
                         L->d_wgu + static_cast<size_t>(ex) * 2 * g.Np * g.Dp);
     launch_synth_rows_bf16(L->stream, seed, scale, base + 2 * ND, g.N, g.Np, g.D, g.Dp,
                            L->d_wd + static_cast<size_t>(ex) * g.Np * g.Dp);
+    if (L->d_wu)
+      launch_synth_rows_bf16(L->stream, seed, scale, base + ND, g.N, g.Np, g.D, g.Dp,
+                             L->d_wu + static_cast<size_t>(ex) * g.Np * g.Dp);
     launch_synth_down_t(L->stream, seed, scale, base + 2 * ND, g.N, g.D, g.Np,
                         L->d_wdt + static_cast<size_t>(ex) * g.Dp128 * g.Np);
   }
@@ -1245,6 +1255,9 @@ int skb_layer_create_synthetic_slice(const skb_config* full, uint64_t seed, floa
                         L->d_wgu + static_cast<size_t>(j) * 2 * g.Np * g.Dp);
     launch_synth_rows_bf16(L->stream, seed, scale, od, g.N, g.Np, g.D, g.Dp,
                            L->d_wd + static_cast<size_t>(j) * g.Np * g.Dp);
+    if (L->d_wu)
+      launch_synth_rows_bf16(L->stream, seed, scale, ou, g.N, g.Np, g.D, g.Dp,
+                             L->d_wu + static_cast<size_t>(j) * g.Np * g.Dp);
     launch_synth_down_t(L->stream, seed, scale, od, g.N, g.D, g.Np,
                         L->d_wdt + static_cast<size_t>(j) * g.Dp128 * g.Np);
   }
@@ -1291,6 +1304,7 @@ void skb_layer_destroy(skb_layer* L) {
   if (L->d_router) cudaFree(L->d_router);
   if (L->d_wgu) cudaFree(L->d_wgu);
   if (L->d_wd) cudaFree(L->d_wd);
+  if (L->d_wu) cudaFree(L->d_wu);
   if (L->d_wdt) cudaFree(L->d_wdt);
   for (auto& ev : L->ev)
     if (ev) cudaEventDestroy(ev);

@@ -168,7 +168,7 @@ struct DecodeLaunch {
   int B;
   int sel_mode, n_off_r, n_off_s;  // kSelect*
   float tau;                       // kSelectThreshold
-  const __nv_bfloat16* wgu;        // tiled gate/up image (threshold mode gathers W_up rows)
+  const __nv_bfloat16* wu;         // W_up rows [E][Np][Dp] (threshold mode gathers them)
   int32_t* kcnt;                   // kSelectThreshold: survivors per flat slot [B*K]
   const uint8_t* mask_r;           // kSelectGiven: [B*K][N]
   const uint8_t* mask_s;           // kSelectGiven: [B][S] or NULL

@@ -23,7 +23,7 @@ for i in range(3):
     (flush.zero_() if os.environ.get('DBG_DIRTY') else flush.sum()); torch.cuda.synchronize()
     if ROT:
         for j in range(4*ROT):
-            layers[j%ROT].forward_device(xd.data_ptr(), yd.data_ptr(), B, mode=skb.MODE_TOPK, s_routed=0.5, s_shared=0.5 if hs else 0.0, stream=1)
+            layers[j%ROT].forward_device(xd.data_ptr(), yd.data_ptr(), B, stream=1, **(dict(mode=skb.MODE_THRESHOLD, tau=float(os.environ['DBG_TAU']), flags=skb.FLAG_FUSED_DECODE) if os.environ.get('DBG_TAU') else dict(mode=skb.MODE_TOPK, s_routed=0.5, s_shared=0.5 if hs else 0.0)))
         torch.cuda.synchronize()
     rep=skb.forward_topk_sparse(layer,x,lvl,lvl if hs else None) if not ROT else ref
     print('launches', rep.launches, 'ref launches', ref.launches, 'maxdiff', float(np.abs(rep.outputs-ref.outputs).max()))
