@@ -50,6 +50,20 @@ SEED, SCALE = 1, 0.05          # generate_synthetic defaults of the reference CL
 # to bf16 (oracle/_ref in the build container: RefLayer.calibrate_tau(0.5), defaults of
 # tools/main.cpp: 16 calibration tokens seed 3, sample cap 2^20, sampler seed 4)
 THRESHOLD_TAU = {"granite": 0.2473328560590744, "olmoe": 0.2645798623561859}
+
+
+def calibrated_tau(workload, use_reference):
+    """tau for a 0.5 routed-sparsity target: the reference's own calibrate chain, run here on the
+    host cores (oracle/_ref, cpu_baseline leg) when allowed and present; else the value it gave
+    in the build container (above)."""
+    if use_reference:
+        try:
+            lay, _ = _ref_layer(WORKLOADS[workload])
+            if lay is not None:
+                return float(lay.calibrate_tau(0.5)), "reference calibrate_tau(0.5), this run"
+        except Exception as exc:  # the baseline leg must not take the bench down
+            print(f"[bench] calibrate_tau failed ({exc}); using the recorded value", file=sys.stderr)
+    return THRESHOLD_TAU[workload], "reference calibrate_tau(0.5), recorded in the build container"
 SWEEP_S = (0.0, 0.25, 0.5, 0.75, 0.9)
 W_BYTES = 2                    # bf16 weight image
 
@@ -79,10 +93,15 @@ def n_off(s, n):
     return int(min(max(np.floor(s * n + 0.5), 0), n))
 
 
+_TOKEN_SOURCE = [None]  # (batch, d_model, seed) -> float32 [batch, d_model]
+
+
 def make_tokens(B, D, seed):
-    """Synthetic N(0,1) tokens, rounded to bf16-representable fp32 (both arms see the same)."""
-    rng = np.random.default_rng(seed)
-    x = rng.standard_normal((B, D), dtype=np.float32)
+    """generate_tokens(B, D, seed) of the reference (proj/src/model.cpp:168-178; seed
+    2 + iteration) rounded to bf16-representable fp32, so that both arms see the same operands.
+    Our arm draws them through the C ABI's host function skb_generate_tokens, the reference arm
+    through the reference's own generate_tokens (bit-identical: tests/test_oracle_cpu.py)."""
+    x = np.ascontiguousarray(_TOKEN_SOURCE[0](B, D, seed), dtype=np.float32).reshape(B, D).copy()
     u = x.view(np.uint32).astype(np.uint64)
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
     return u.astype(np.uint32).view(np.float32).reshape(B, D)
@@ -478,6 +497,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2605_08575_b200 as skb
+    _TOKEN_SOURCE[0] = skb.generate_tokens
 
     if args.ep or (world > 1 and args.workload in ("maverick", "gptoss")):
         return run_ep(args, torch, dist, skb, rank, world, local)
@@ -611,11 +631,12 @@ def run_ours(args):
         # the threshold runtime path (forward_sparse) on the same workload,
         # tau = the reference's calibrate_tau for a 0.5 target on these synthetic weights
         if args.workload in THRESHOLD_TAU:
-            tau = THRESHOLD_TAU[args.workload]
+            tau, tau_src = calibrated_tau(args.workload, not args.no_cpu and world == 1)
             m, _ = pt.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
             rep = skb.forward_sparse(layer, pt.x_host[0], tau)
             ent = {"workload": shape["name"], "batch": B, "mode": "threshold (forward_sparse)",
-                   "tau": tau, "achieved_routed_sparsity": round(rep.achieved_routed_sparsity, 4),
+                   "tau": tau, "tau_source": tau_src,
+                   "achieved_routed_sparsity": round(rep.achieved_routed_sparsity, 4),
                    "ms_per_step": round(m, 5), "tokens_per_s": round(B / (m * 1e-3), 1),
                    "tiles_skipped_frac": round(rep.tiles_skipped / max(1, rep.tiles_total), 4)}
             if not args.no_cpu and world == 1:
@@ -645,7 +666,7 @@ def run_ours(args):
             # the threshold runtime path on the same point (fused decode kernel: the gate rows
             # stream alone, W_up / W_down rows are gathered for the survivors): algorithmic bytes
             # = router + gate of the routed experts + 2 x surviving rows + token/output rows
-            tau = THRESHOLD_TAU["olmoe"]
+            tau, tau_src = calibrated_tau("olmoe", not args.no_cpu and world == 1)
             tb = []
             for xh in p2.x_host:
                 rp = skb.forward_sparse(l2, xh, tau, capture=True)
@@ -657,7 +678,8 @@ def run_ours(args):
             p2.rotation(tot)
             m, _ = p2.time_device(("tau", tau), sw_steps, 3, use_graph=not args.no_graph)
             sweep.append({"workload": sh["name"], "batch": 1, "mode": "threshold (forward_sparse)",
-                          "tau": tau, "achieved_routed_sparsity": round(rp.achieved_routed_sparsity, 4),
+                          "tau": tau, "tau_source": tau_src,
+                          "achieved_routed_sparsity": round(rp.achieved_routed_sparsity, 4),
                           "ms_per_step": round(m, 5), "tokens_per_s": round(1 / (m * 1e-3), 1),
                           "bytes_alg": int(tot), "layer_gbs": round(tot / (m * 1e-3) / 1e9, 1),
                           "layer_frac_of_hbm_roofline": round(tot / (m * 1e-3) / 1e9 / hbm_peak, 4),
@@ -770,6 +792,8 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    from oracle.pyoracle import Oracle
+    _TOKEN_SOURCE[0] = Oracle.get().generate_tokens
     shape = WORKLOADS[args.workload]
     B, s = args.batch, args.sparsity
     cores = os.cpu_count() or 1

@@ -179,9 +179,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// one polite poller: back off between probes so that 148 pollers do not eat L2 bandwidth
+// One poller per CTA, probes back to back: a probe is an L2 round trip (~0.6 us) and 148 of them
+// in flight are no load, while __nanosleep -- whatever its argument -- was measured to put the
+// poller away for microseconds (the candidate exchange waited 3-6 us instead of ~1).
 __device__ __forceinline__ void spin_until(const unsigned* p, unsigned target) {
-  while (ld_acquire_u32(p) < target) __nanosleep(64);
+  while (ld_acquire_u32(p) < target) {
+  }
 }
 __device__ __forceinline__ uint2 ld_volatile_u2(const uint2* p) {
   uint2 v;
@@ -877,8 +880,11 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
               sa += red[(w * TT + dtid) * 2 + 1];
             }
             uint2* dst = a.p0 + ((static_cast<size_t>(t0 + dtid) * E + e) * ND + j) * 2;
-            st_volatile_u2(dst, __float_as_uint(s), epoch);
-            st_volatile_u2(dst + 1, __float_as_uint(sa), epoch);
+            // published with 64-bit exchanges: performed at L2 at once
+            atomicExch(reinterpret_cast<unsigned long long*>(dst),
+                       (static_cast<unsigned long long>(epoch) << 32) | __float_as_uint(s));
+            atomicExch(reinterpret_cast<unsigned long long*>(dst + 1),
+                       (static_cast<unsigned long long>(epoch) << 32) | __float_as_uint(sa));
           }
           d_sync();
         }
@@ -887,6 +893,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
     DEC_STAMP(kWarpD0 * 32, 1);
 
     // ---- candidates (every CTA computes the same tables) ----
+    DEC_STAMP(kWarpD0 * 32, 26);
     {
       // every partial of every token: all of this thread's words in flight before the first check
       float2* pf = reinterpret_cast<float2*>(gred);
@@ -906,14 +913,9 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
         for (int u = 0; u < 4; ++u) {
           const int i = base + u * kDThreads + dtid;
           if (i < total) {
-            while (va[u].y != epoch) {
-              __nanosleep(20);
-              va[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i));
-            }
-            while (vb[u].y != epoch) {
-              __nanosleep(20);
-              vb[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i) + 1);
-            }
+            DEC_STAMP(kWarpD0 * 32, 27);
+            while (va[u].y != epoch) va[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i));
+            while (vb[u].y != epoch) vb[u] = ld_volatile_u2(a.p0 + 2 * static_cast<size_t>(i) + 1);
             pf[i] = make_float2(__uint_as_float(va[u].x), __uint_as_float(vb[u].x));
           }
         }

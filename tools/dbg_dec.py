@@ -36,8 +36,8 @@ for i in range(3):
         for k in range(1,31):
             nz=t[:,k]>0
             t[nz,k]=gt0[nz]+((t[nz,k]-clk0[nz])/1.965).astype(np.int64)
-        names={14:'chain start',15:'chain end',0:'start',1:'p0 done',2:'tables',3:'tma issued',4:'g done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p3 barrier',7:'exit',10:'route done',11:'tma go',16:'x staged',17:'cons go',18:'piece1 done',19:'p3 tables',20:'p3 loaded',21:'polled',22:'cand done',23:'p3 pass1',24:'cand start',25:'cand tok'}
-        for k in (1,21,24,25,22,2,11,16,17,18,3,14,15,10,4,8,9,12,13,5,19,6,23,20,7):
+        names={14:'chain start',15:'chain end',0:'start',1:'p0 done',2:'tables',3:'tma issued',4:'g done',8:'p2 ready',9:'p2 pivot',11:'p2 prefix',12:'p2 list',13:'p2 gather',5:'p2 done',6:'p3 barrier',7:'exit',10:'route done',11:'tma go',16:'x staged',17:'cons go',18:'piece1 done',19:'p3 tables',20:'p3 loaded',21:'polled',22:'cand done',23:'p3 pass1',24:'cand start',25:'cand tok',26:'poll start',27:'probe1 back'}
+        for k in (1,26,27,21,24,25,22,2,11,16,17,18,3,14,15,10,4,8,9,12,13,5,19,6,23,20,7):
             col=t[:148,k]-t[:148,0].min()
             col=col[t[:148,k]>0]
             if col.size: print(f'  {names[k]:12s} n {col.size:3d} min {col.min():7d} med {int(np.median(col)):7d} max {col.max():7d}')
