@@ -517,6 +517,42 @@ def test_full_shapes_properties(skb, oracle, shape, B, s):
 
 
 # ---------------------------------------------------------------------------------------------
+# chunked tensor-core accumulation (long contractions in the 1e-5 mode)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", [
+    # E, K, D, N, S, B: contraction lengths that are not multiples of the 32-step chunk, a shared
+    # expert whose K extent differs from the routed experts', every token-tile size
+    (4, 2, 1600, 1100, 700, 40),     # gate/up 25 K blocks (100 steps), down 18 / 11 K blocks x 2 terms
+    (6, 1, 2112, 320, 1344, 9),      # 33 K blocks; the shared expert's down projection alone is long
+    (8, 2, 3136, 192, 0, 300),       # 49 K blocks, 128-token tiles, short down projection (not chunked)
+    (2, 2, 1664, 2048, 0, 130),      # both chunked, tiles of 128 with a ragged tail
+])
+def test_chunked_accumulation_ragged_shapes_vs_oracle(skb, oracle, case):
+    E, K, D, N, S, B = case
+    cfg = Config(E, K, D, N, S, True)
+    w, x = rounded_case(oracle, cfg, seed=E + N, scale=0.05, batch=B, token_seed=13)
+    layer = make_layer(skb, w)
+    lvl = skb.SparsityLevel(0.5)
+    f = skb.FLAG_NO_FUSED_DECODE
+    rep = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, capture=True, flags=f)
+    y_same, _, cap = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if S else None, capture=True)
+    np.testing.assert_array_equal(rep.routes.ids, cap["ids"])
+    assert max_rel_diff(rep.h_routed, cap["h_routed"]) <= TOL_FP32_ACCUM
+    err = max_rel_diff(rep.outputs, y_same)
+    assert err <= TOL_FP32_ACCUM, err
+    # against double precision (the oracle's own fp32 sums carry ~1e-6 at these lengths)
+    y64 = oracle.scalar_forward(w, x, rep.masks.routed, rep.masks.shared if S else None)
+    assert true_rel_err(rep.outputs, y64) <= 5e-6
+    # the bf16 mode takes the single-accumulator kernels: its own bar
+    rep16 = skb.forward_topk_sparse(layer, x, lvl, lvl if S else None, flags=f | skb.FLAG_BF16_H)
+    assert max_rel_diff(rep16.outputs, y_same) <= TOL_BF16
+    # dense mode through the same chunked kernels
+    dense = skb.forward_dense(layer, x, flags=f)
+    y_dense, _ = oracle.forward(w, x)
+    assert max_rel_diff(dense.outputs, y_dense) <= TOL_FP32_ACCUM
+
+
+# ---------------------------------------------------------------------------------------------
 # the quality sweep (profiler_test.cpp:147-186) on the device
 # ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("mode", [0, 1])
