@@ -449,6 +449,10 @@ def run_ep(args, torch, dist, skb, rank, world, local):
                  + (2 * shape["S"] * D * 2 + min(shape["S"], B * keep_s) * D * 2 if shape["S"] else 0)
                  + B * D * 8)
     clocks = sampler.stop() if rank == 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the reference CPU layer beside it, on a bounded sample of this rank's batch
+        cpu = cpu_reference(shape, min(B, 256), s, reps=1)
     if rank == 0:
         gbs = bytes_alg / (ms * 1e-3) / 1e9
         print(json.dumps({
@@ -475,7 +479,7 @@ def run_ep(args, torch, dist, skb, rank, world, local):
             "e2e": {"value": round(world * B / (e2e_ms * 1e-3), 1), "unit": "tokens/s",
                     "ms_per_step": round(e2e_ms, 5), "h2d_bytes_per_step": B * D * 4,
                     "d2h_bytes_per_step": B * D * 4},
-            "gpu_launches": None, "clocks": clocks, "cpu_baseline": None,
+            "gpu_launches": None, "clocks": clocks, "cpu_baseline": cpu,
             "ep_stats": layer.last_stats}))
     if world > 1:
         dist.barrier()
