@@ -310,6 +310,26 @@ int skb_ep_unpack(const uint8_t* recv, int rows, int d_model, float* x, int32_t*
 int skb_ep_combine(const float* back, const int32_t* pos, const float* weights, const float* shared,
                    int batch, int top_k, int d_model, float* y, void* stream);
 
+/* Combine without the second collective (combine direction): buffers that
+ * peers map through CUDA IPC (skb_ep_symm_alloc / _ipc_export / _ipc_import); the expert rank
+ * pushes its un-weighted row outputs into every home rank's `back` buffer at the positions that
+ * rank's plan expects and bumps a cumulative counter there (skb_ep_push_back; `expect` is this
+ * rank's own running total per expert rank, advanced by the same call from its counts row); the
+ * home rank's combine waits on its counters instead of on an all-to-all (skb_ep_combine_symm).
+ * With world == 1 the "peer" is the rank itself: the same kernels, checked against skb_ep_combine. */
+int skb_ep_symm_alloc(uint64_t bytes, void** ptr);
+int skb_ep_symm_free(void* ptr);
+int skb_ep_ipc_export(void* ptr, uint8_t* handle64);
+int skb_ep_ipc_import(const uint8_t* handle64, void** peer_ptr);
+int skb_ep_ipc_close(void* peer_ptr);
+int skb_ep_push_back(const float* out_rows, int rows, int d_model, const int32_t* counts, int world,
+                     int rank, float* const* peer_back, unsigned long long* const* peer_flag,
+                     unsigned long long* expect, uint32_t* done_ctr, void* stream);
+int skb_ep_combine_symm(const float* back, const unsigned long long* flag,
+                        const unsigned long long* expect, int world, const int32_t* pos,
+                        const float* weights, const float* shared, int batch, int top_k, int d_model,
+                        float* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

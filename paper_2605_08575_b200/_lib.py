@@ -31,6 +31,8 @@ EXPORTS = (
     "skb_layer_load", "skb_save_weights", "skb_weight_file_size", "skb_last_error_offset",
     "skb_threshold_mask", "skb_default_capacity", "skb_compact_active",
     "skb_ep_row_stride", "skb_ep_plan", "skb_ep_pack", "skb_ep_unpack", "skb_ep_combine",
+    "skb_ep_symm_alloc", "skb_ep_symm_free", "skb_ep_ipc_export", "skb_ep_ipc_import",
+    "skb_ep_ipc_close", "skb_ep_push_back", "skb_ep_combine_symm",
 )
 
 
@@ -118,5 +120,13 @@ def load() -> C.CDLL:
     L.skb_ep_pack.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
     L.skb_ep_unpack.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
     L.skb_ep_combine.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]
+    L.skb_ep_symm_alloc.argtypes = [C.c_uint64, C.POINTER(vp)]
+    L.skb_ep_symm_free.argtypes = [vp]
+    L.skb_ep_ipc_export.argtypes = [vp, vp]
+    L.skb_ep_ipc_import.argtypes = [vp, C.POINTER(vp)]
+    L.skb_ep_ipc_close.argtypes = [vp]
+    L.skb_ep_push_back.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
+    L.skb_ep_combine_symm.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, C.c_int, C.c_int,
+                                      vp, vp]
     _lib = L
     return L

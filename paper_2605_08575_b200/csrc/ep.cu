@@ -6,6 +6,8 @@
 // separately).
 //
 // Packed dispatch row: [D bf16 token values][int32 local expert id][pad to 16 bytes].
+#include <cstring>
+
 #include "../../include/sparsekit_b200.h"
 #include "skb_internal.cuh"
 
@@ -158,6 +160,101 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(const float* __restrict
   y[static_cast<size_t>(t) * D + d] = acc;
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Combine WITHOUT the second collective (combine direction): the expert rank
+// writes its un-weighted row outputs straight into the home ranks' `back` buffers over NVLink
+// peer mappings, in the position each home rank's plan expects them, and bumps a counter in the
+// home rank's memory; the home rank's combine kernel waits on its counters instead of on an
+// all-to-all.  Counters are cumulative (never reset): the plan keeps the running totals.
+//
+// Safe with one buffer per rank: a rank pushes step n+1 only after it has received the home
+// rank's step n+1 dispatch rows, which that rank's stream issues after its step n combine.
+// ---------------------------------------------------------------------------------------------
+
+// expected cumulative rows per expert rank at this home rank: expect[r] += cnt[rank][r]
+__global__ void ep_expect_kernel(const int32_t* __restrict__ cnt, int W, int rank,
+                                 unsigned long long* __restrict__ expect) {
+  const int r = threadIdx.x;
+  if (r < W) expect[r] += static_cast<unsigned long long>(cnt[rank * W + r]);
+}
+
+// one warp per received row: rows [roff(s), roff(s) + cnt[s][rank]) came from home rank s and go to
+// position base_s + k of its back buffer, base_s = sum_{d < rank} cnt[s][d]
+__global__ void __launch_bounds__(256) ep_push_back_kernel(const float* __restrict__ out, int M, int D,
+                                                           const int32_t* __restrict__ cnt, int W,
+                                                           int rank, float* const* __restrict__ peer_back,
+                                                           unsigned long long* const* __restrict__ peer_flag,
+                                                           unsigned* __restrict__ done_ctr) {
+  __shared__ int s_roff[kMaxWorld + 1], s_base[kMaxWorld];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < W; ++s) {
+      s_roff[s] = o;
+      o += cnt[s * W + rank];
+      int b = 0;
+      for (int d = 0; d < rank; ++d) b += cnt[s * W + d];
+      s_base[s] = b;
+    }
+    s_roff[W] = o;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r < M) {
+    int s = 0;
+    while (s + 1 < W && r >= s_roff[s + 1]) ++s;
+    const float4* src = reinterpret_cast<const float4*>(out + static_cast<size_t>(r) * D);
+    float* dst_row = peer_back[s] + static_cast<size_t>(s_base[s] + r - s_roff[s]) * D;
+    if ((D & 3) == 0 && (reinterpret_cast<uintptr_t>(dst_row) & 15) == 0) {
+      float4* dst = reinterpret_cast<float4*>(dst_row);
+      for (int d = lane; d < D / 4; d += 32) dst[d] = src[d];
+    } else {
+      for (int d = lane; d < D; d += 32) dst_row[d] = out[static_cast<size_t>(r) * D + d];
+    }
+  }
+  // the last CTA through publishes: every row of this launch is in place before any counter moves
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    if (threadIdx.x == 0) *done_ctr = 0u;
+    __threadfence_system();
+    if (static_cast<int>(threadIdx.x) < W) {
+      const int s = threadIdx.x;
+      const unsigned long long n = static_cast<unsigned long long>(cnt[s * W + rank]);
+      if (n) atomicAdd_system(peer_flag[s] + rank, n);
+    }
+  }
+}
+
+// the home rank: wait until every expert rank has delivered what the plan expects, then combine
+__global__ void __launch_bounds__(256) ep_combine_symm_kernel(
+    const float* __restrict__ back, const unsigned long long* __restrict__ flag,
+    const unsigned long long* __restrict__ expect, int W, const int32_t* __restrict__ pos,
+    const float* __restrict__ w, const float* __restrict__ shared, int B, int K, int D,
+    float* __restrict__ y) {
+  if (threadIdx.x < W) {
+    const volatile unsigned long long* f = flag + threadIdx.x;
+    const unsigned long long want = expect[threadIdx.x];
+    while (*f < want) {
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  const int t = blockIdx.y;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B || d >= D) return;
+  float acc = 0.0f;
+  for (int s = 0; s < K; ++s) {
+    const int p = pos[t * K + s];
+    acc = __fadd_rn(acc, __fmul_rn(w[t * K + s], __ldcv(back + static_cast<size_t>(p) * D + d)));
+  }
+  if (shared != nullptr) acc = __fadd_rn(acc, shared[static_cast<size_t>(t) * D + d]);
+  y[static_cast<size_t>(t) * D + d] = acc;
+}
 }  // namespace
 }  // namespace skb
 
@@ -196,6 +293,53 @@ int skb_ep_combine(const float* back, const int32_t* pos, const float* weights, 
   if (batch <= 0) return SKB_OK;
   ep_combine_kernel<<<dim3(ceil_div(d_model, 256), batch), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       back, pos, weights, shared, batch, top_k, d_model, y);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+/* ---- peer-memory combine (no second collective) ---- */
+int skb_ep_symm_alloc(uint64_t bytes, void** ptr) {
+  if (ptr == nullptr) return SKB_EINTERNAL;
+  if (cudaMalloc(ptr, bytes ? bytes : 16) != cudaSuccess) return SKB_ECUDA;
+  return cudaMemset(*ptr, 0, bytes ? bytes : 16) == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+int skb_ep_symm_free(void* ptr) { return cudaFree(ptr) == cudaSuccess ? SKB_OK : SKB_ECUDA; }
+int skb_ep_ipc_export(void* ptr, uint8_t* handle64) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, ptr) != cudaSuccess) return SKB_ECUDA;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, 64);
+  return SKB_OK;
+}
+int skb_ep_ipc_import(const uint8_t* handle64, void** peer_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  return cudaIpcOpenMemHandle(peer_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? SKB_OK
+                                                                                          : SKB_ECUDA;
+}
+int skb_ep_ipc_close(void* peer_ptr) {
+  return cudaIpcCloseMemHandle(peer_ptr) == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_push_back(const float* out_rows, int rows, int d_model, const int32_t* counts, int world,
+                     int rank, float* const* peer_back, unsigned long long* const* peer_flag,
+                     unsigned long long* expect, uint32_t* done_ctr, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return SKB_ECONFIG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ep_expect_kernel<<<1, 32, 0, s>>>(counts, world, rank, expect);
+  const int grid = rows > 0 ? ceil_div(rows, 8) : 1;
+  ep_push_back_kernel<<<grid, 256, 0, s>>>(out_rows, rows, d_model, counts, world, rank, peer_back,
+                                           peer_flag, done_ctr);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_combine_symm(const float* back, const unsigned long long* flag,
+                        const unsigned long long* expect, int world, const int32_t* pos,
+                        const float* weights, const float* shared, int batch, int top_k, int d_model,
+                        float* y, void* stream) {
+  if (batch <= 0) return SKB_OK;
+  if (world < 1 || world > kMaxWorld) return SKB_ECONFIG;
+  ep_combine_symm_kernel<<<dim3(ceil_div(d_model, 256), batch), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      back, flag, expect, world, pos, weights, shared, batch, top_k, d_model, y);
   return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
 }
 

@@ -87,9 +87,13 @@ def row_stride(d_model: int) -> int:
 
 class ExpertParallelLayer:
     def __init__(self, backend: Backend, group: Optional[dist.ProcessGroup] = None,
-                 max_batch: Optional[int] = None):
+                 max_batch: Optional[int] = None, peer_combine: bool = False,
+                 peer_rows: int = 0):
         """`max_batch`: the largest home batch of any rank (all ranks pass the same value); the
-        all-gathered ids are padded to it.  None: every rank's batch has the same size."""
+        all-gathered ids are padded to it.  None: every rank's batch has the same size.
+        `peer_combine`: the combine direction without a collective -- expert
+        ranks write their row outputs straight into the home ranks' peer-mapped buffers (room
+        for `peer_rows` rows) and the home combine waits on counters; CUDA backend only."""
         self.b = backend
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -101,6 +105,9 @@ class ExpertParallelLayer:
         self._lo_cpu = torch.tensor([r[0] for r in self.ranges] + [backend.n_experts], dtype=torch.int32)
         self._lo = {}
         self.last_stats = {}
+        self.peer = None
+        if peer_combine:
+            self.peer = backend.symm_setup(peer_rows, self.world, self.rank, group)
 
     def _lo_on(self, device):
         if device not in self._lo:
@@ -142,12 +149,17 @@ class ExpertParallelLayer:
         recv = self._all_to_all(send, sc, rc)
         rows_in, ids_in = b.unpack(recv, D)
         out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
-        back = self._all_to_all(out_in, rc, sc)               # back to the home ranks, send order
-        y = b.combine(back, pos, w, sh)
+        if self.peer is not None:                             # no second collective
+            b.push_back(out_in, counts, self.peer, self.rank)
+            y = b.combine_symm(self.peer, pos, w, sh)
+        else:
+            back = self._all_to_all(out_in, rc, sc)           # back to the home ranks, send order
+            y = b.combine(back, pos, w, sh)
         self.last_stats = {"sent_rows": sc, "recv_rows": rc,
                            "dispatch_bytes": int(sum(sc)) * row_stride(D),
                            "combine_bytes": int(sum(rc)) * D * 4,
-                           "host_syncs": 1, "collectives": (1 if W > 1 else 0) + 2 * (W > 1)}
+                           "host_syncs": 1,
+                           "collectives": (1 if W > 1 else 0) + (2 - (self.peer is not None)) * (W > 1)}
         return y
 
 
@@ -248,4 +260,54 @@ class CudaBackend:
                                        w.contiguous().data_ptr(),
                                        shared.data_ptr() if shared is not None else None,
                                        B, K, D, y.data_ptr(), self._stream()), "skb_ep_combine")
+        return y
+
+    # ---- combine over peer-mapped buffers (csrc/ep.cu: ep_push_back_kernel, ep_combine_symm_kernel)
+    def symm_setup(self, max_rows, world, rank, group=None):
+        """One `back` buffer [max_rows][D] fp32 and `world` cumulative counters per rank, exported
+        through CUDA IPC and mapped by every peer (world 1: the rank maps itself)."""
+        import ctypes as C
+        L, D = self.L, self.D
+        back, flag = C.c_void_p(), C.c_void_p()
+        self._ok(L.skb_ep_symm_alloc(max(1, max_rows) * D * 4, C.byref(back)), "skb_ep_symm_alloc")
+        self._ok(L.skb_ep_symm_alloc(8 * 16, C.byref(flag)), "skb_ep_symm_alloc")
+        peers_back, peers_flag = [back.value] * world, [flag.value] * world
+        if world > 1:
+            h = torch.zeros(128, dtype=torch.uint8)
+            self._ok(L.skb_ep_ipc_export(back, h.data_ptr()), "skb_ep_ipc_export")
+            self._ok(L.skb_ep_ipc_export(flag, h.data_ptr() + 64), "skb_ep_ipc_export")
+            dev = torch.device("cuda", torch.cuda.current_device())
+            allh = torch.empty(world * 128, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(allh, h.to(dev), group=group)
+            allh = allh.cpu()
+            for r in range(world):
+                if r == rank:
+                    continue
+                pb, pf = C.c_void_p(), C.c_void_p()
+                self._ok(L.skb_ep_ipc_import(allh[r * 128:].data_ptr(), C.byref(pb)), "skb_ep_ipc_import")
+                self._ok(L.skb_ep_ipc_import(allh[r * 128 + 64:].data_ptr(), C.byref(pf)), "skb_ep_ipc_import")
+                peers_back[r], peers_flag[r] = pb.value, pf.value
+        dev = torch.device("cuda", torch.cuda.current_device())
+        return {"back": back.value, "flag": flag.value, "max_rows": max_rows,
+                "peer_back": torch.tensor(peers_back, dtype=torch.int64, device=dev),
+                "peer_flag": torch.tensor(peers_flag, dtype=torch.int64, device=dev),
+                "expect": torch.zeros(16, dtype=torch.int64, device=dev),
+                "done": torch.zeros(1, dtype=torch.int32, device=dev), "world": world}
+
+    def push_back(self, out_rows, counts, peer, rank):
+        M = out_rows.shape[0]
+        self._ok(self.L.skb_ep_push_back(out_rows.contiguous().data_ptr() if M else None, M, self.D,
+                                         counts.data_ptr(), peer["world"], rank,
+                                         peer["peer_back"].data_ptr(), peer["peer_flag"].data_ptr(),
+                                         peer["expect"].data_ptr(), peer["done"].data_ptr(),
+                                         self._stream()), "skb_ep_push_back")
+
+    def combine_symm(self, peer, pos, w, shared):
+        B, K = w.shape
+        y = torch.empty((B, self.D), dtype=torch.float32, device=w.device)
+        self._ok(self.L.skb_ep_combine_symm(peer["back"], peer["flag"], peer["expect"].data_ptr(),
+                                            peer["world"], pos.data_ptr(), w.contiguous().data_ptr(),
+                                            shared.data_ptr() if shared is not None else None,
+                                            B, K, self.D, y.data_ptr(), self._stream()),
+                 "skb_ep_combine_symm")
         return y

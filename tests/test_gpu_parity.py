@@ -737,6 +737,14 @@ def test_ep_layer_world_1_equals_the_single_gpu_layer(skb, oracle, shape, B, s):
     w.router = w_raw.router
     y_ref, _ = oracle.forward(w, x, rep.masks.routed, rep.masks.shared if S else None)
     assert max_rel_diff(y.cpu().numpy(), y_ref) <= TOL_FP32_ACCUM
+    # the combine over peer-mapped buffers (no second collective; here the rank is its own peer):
+    # same rows, same positions, same order -> bit for bit, step after step (cumulative counters)
+    peer_layer = ep.ExpertParallelLayer(backend, peer_combine=True, peer_rows=B * K)
+    for _ in range(3):
+        y2 = peer_layer.forward(torch.from_numpy(x).cuda(), s, s if S else 0.0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y2.cpu().numpy(), y.cpu().numpy())
+    assert peer_layer.last_stats["collectives"] == 0
 
 
 # ---------------------------------------------------------------------------------------------
