@@ -1320,17 +1320,22 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
               }
               d_sync();
             }
+            if (!thr_unit) {
+              // the rows' activations side by side (two dependent shared-memory loads per row
+              // otherwise sit in front of every FMA group of the loops below)
+              for (int r = dtid; r < nr; r += kDThreads) hval[r] = __uint_as_float(keys_s[lst[k0 + r]]);
+              d_sync();
+            }
             if (NT == 1) {
               // narrow rows: G row groups, group g takes rows g, g + G, ...
               if (lane_ok) {
-#pragma unroll 2
-                for (int r = g; r < nr; r += G)
-                  fma8(gbh[r * LPR + l], thr_unit ? hval[r] : __uint_as_float(keys_s[lst[k0 + r]]), acc[0]);
+#pragma unroll 4
+                for (int r = g; r < nr; r += G) fma8(gbh[r * LPR + l], hval[r], acc[0]);
               }
             } else {
-#pragma unroll 1
+#pragma unroll 2
               for (int r = 0; r < nr; ++r) {
-                const float hk = thr_unit ? hval[r] : __uint_as_float(keys_s[lst[k0 + r]]);
+                const float hk = hval[r];
 #pragma unroll
                 for (int nt = 0; nt < 4; ++nt) {
                   const int c8 = nt * kDThreads + dtid;
