@@ -599,6 +599,9 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": int(dom_bytes),
                     "kernel_ms": round(stages[dom], 5),
                     "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
+    if roofline["bound"] == "hbm" and roofline["frac"] > 1.0:
+        roofline["note"] = ("above 1: the peak is the measured COPY bandwidth (reads + writes); a "
+                            "read-only weight stream can exceed it (B200 spec 8 TB/s)")
     layer_gbs = mean_bytes["total"] / (ms_per_step * 1e-3) / 1e9
     # the same step timed alone after a memset flush (what round 1 reported)
     iso_ms = pt.time_isolated(s, max(10, min(args.steps, 50)), 3)
