@@ -25,7 +25,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:grou
 python tools/summarize_ncu.py gpurun_out/ncu_full_decode_fused_olmoe_b1.ncu-rep > gpurun_out/ncu_full_decode_fused_olmoe_b1.txt 2>&1
 python tools/summarize_ncu.py gpurun_out/ncu_full_grouped_tc_granite_b256.ncu-rep > gpurun_out/ncu_full_grouped_tc_granite_b256.txt 2>&1
 python tools/summarize_ncu.py gpurun_out/ncu_full_chunked_gptoss_b4096.ncu-rep > gpurun_out/ncu_full_chunked_gptoss_b4096.txt 2>&1
-python tools/make_traffic_json.py gpurun_out/ncu_traffic.json olmoe:1:decode_fused=gpurun_out/ncu_full_decode_fused_olmoe_b1.ncu-rep:decode_fused granite:256:gateup=gpurun_out/ncu_full_grouped_tc_granite_b256.ncu-rep:"(int)0" gptoss:4096:gateup=gpurun_out/ncu_full_chunked_gptoss_b4096.ncu-rep:"(int)0"
+python tools/make_traffic_json.py gpurun_out/ncu_traffic.json olmoe:1:decode_fused=gpurun_out/ncu_full_decode_fused_olmoe_b1.ncu-rep:decode_fused "granite:256:gateup=gpurun_out/ncu_full_grouped_tc_granite_b256.ncu-rep:grouped_tc_kernel<128, 0" "gptoss:4096:gateup=gpurun_out/ncu_full_chunked_gptoss_b4096.ncu-rep:grouped_tc_chunked_kernel<128, 0"
 timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 900 -k "fused_decode_matches or batch_invariant or falls_back or forward_sparse_fused or caller_masks or ep_ or compact_active or threshold_mask or forward_topk_vs_oracle or paired" > gpurun_out/sanitizer_memcheck.log 2>&1; tail -4 gpurun_out/sanitizer_memcheck.log
 timeout 1100 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 900 -k "(fused_decode_matches and (case0 or case3)) or (forward_sparse_fused and case1)" > gpurun_out/sanitizer_racecheck.log 2>&1; tail -3 gpurun_out/sanitizer_racecheck.log
 timeout 600 compute-sanitizer --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x --timeout 500 -k "fused_decode_matches and case0" > gpurun_out/sanitizer_synccheck.log 2>&1; tail -3 gpurun_out/sanitizer_synccheck.log
