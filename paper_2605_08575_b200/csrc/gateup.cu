@@ -38,6 +38,7 @@ constexpr int kGateupThreads = 192;
 constexpr int kATileBytes = 128 * kBlockK * 2;  // 16 KB: 128 rows x 128 B
 
 constexpr int kMaxSplit = 3;
+constexpr uint32_t kPartBoxBytes = 32 * kBlockK * 2;  // a 32-row box of the token operand (4 KB)
 __host__ __device__ constexpr int b_tile_bytes(int tn) { return tn * kBlockK * 2; }
 // MB = 128-row A blocks per CTA.  MB = 2 ("paired blocks"): two weight blocks of the same expert
 // share every token tile a CTA fetches, so the bytes an SM ingests per unit of work drop by 25 %
@@ -65,12 +66,41 @@ __host__ __device__ constexpr int gateup_smem_bytes(int tn, int mode, int mb = 1
 
 }  // namespace
 
+#ifdef SKB_DEBUG_TIMING
+// per-CTA phase stamps of grouped_tc_kernel (tools/dbg_tc.py): [MODE][cta][8]
+__device__ long long g_tc_dbg[2 * 1024 * 8];
+#define TC_STAMP(thr, i)                                                                         \
+  do {                                                                                           \
+    const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                        \
+    if (threadIdx.x == (thr) && cta_ < 1024) {                                                   \
+      long long* p_ = g_tc_dbg + (MODE * 1024 + cta_) * 8;                                       \
+      if ((i) == 0) {                                                                            \
+        long long t_;                                                                            \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+        p_[0] = t_;                                                                              \
+        p_[7] = clock64();                                                                       \
+      } else {                                                                                   \
+        p_[i] = clock64();                                                                       \
+      }                                                                                          \
+    }                                                                                            \
+  } while (0)
+extern "C" void skb_debug_tc(long long* out) { cudaMemcpyFromSymbol(out, g_tc_dbg, sizeof(g_tc_dbg)); }
+extern "C" void skb_debug_tc_clear() {
+  static long long z[2 * 1024 * 8];
+  cudaMemcpyToSymbol(g_tc_dbg, z, sizeof(z));
+}
+#else
+#define TC_STAMP(thr, i) do { } while (0)
+#endif
+
 struct TcArgs {
   const int32_t* tile_expert;
   const int32_t* tile_row0;
   const int32_t* tile_nrows;
   const int32_t* n_tiles;
   const int32_t* tile_colrow;  // token-indexed tiles (MODE 0, TN 16): [tile][16] h row or -1
+  const void* a_base;         // the A image behind tmap_a (L2 prefetch), or nullptr
+  const void* a_shared_base;  // ... behind tmap_a_shared
   float* out;       // MODE 0: h [rows][out_stride];  MODE 1: slot outputs [rows][out_stride]
   float* sg_out;    // MODE 0, optional: silu(gate) [rows][out_stride] (threshold selection)
   int out_stride;
@@ -80,6 +110,8 @@ struct TcArgs {
   int kblocks_routed, kblocks_shared;  // 64-element K blocks
   int rows_per_expert;                 // A-image rows per routed expert
   int nsplit;                          // MODE 1: B operands accumulated per K block (1 or 3)
+  int early_tiles;  // the tile list was written at least two kernels upstream: readable -- and the
+                    // weight stream startable -- before the programmatic-launch wait
 };
 
 template <int TN, int MODE, int MB>
@@ -88,13 +120,15 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   const __grid_constant__ CUtensorMap tmap_a_shared,
                   const __grid_constant__ CUtensorMap tmap_b0,
                   const __grid_constant__ CUtensorMap tmap_b1,
-                  const __grid_constant__ CUtensorMap tmap_b2, const TcArgs a) {
+                  const __grid_constant__ CUtensorMap tmap_b2,
+                  const __grid_constant__ CUtensorMap tmap_s0,
+                  const __grid_constant__ CUtensorMap tmap_s1,
+                  const __grid_constant__ CUtensorMap tmap_s2, const TcArgs a) {
   constexpr int kStages = num_stages(TN, MODE, MB);
   constexpr int kStageBytes = stage_bytes(TN, MODE, MB);
   constexpr int kBTile = b_tile_bytes(TN);
   constexpr int kAll = MB * kATileBytes;  // A tiles of one stage; the B tiles follow
   constexpr uint32_t kTmemCols = tmem_cols(TN) * MB;
-  constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -110,6 +144,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  TC_STAMP(0, 0);
   // ---- prologue: nothing here reads memory written by the previous kernel ----
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
@@ -127,8 +162,18 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_ptr_generic;
 
-  pdl_wait();
-  pdl_launch_dependents();
+  // Programmatic dependent launch: this kernel's CTAs start while the previous kernel (token
+  // permute / selection) is still running and wait for it below.  The tile list is older than
+  // that (dispatch, at least two kernels upstream, complete before the previous kernel released
+  // its own wait), and the weights are constants: so the ring's first stages of the A operand are
+  // requested -- and the rest of this CTA's weight blocks prefetched into the L2 -- BEFORE the
+  // wait; only the token operand waits.  Hides the tile-list reads and the first HBM latency
+  // (~2.5 us per GEMM) under the previous kernel's tail.
+  if (!a.early_tiles) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
+  TC_STAMP(0, 1);
 
   const int tile = blockIdx.y;
   bool active = tile < *a.n_tiles;
@@ -141,36 +186,82 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
     shared_expert = e >= a.n_experts;
     active = static_cast<int>(blockIdx.x) * MB < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
   }
+  const int num_k_blocks = shared_expert ? a.kblocks_shared : a.kblocks_routed;
+  const int nsplit = (MODE == 0) ? 1 : a.nsplit;
+  // A tile with fewer token rows than TN (the usual case: tiles are cut per expert) fetches only
+  // the 32-row boxes that hold rows and multiplies only round_up(nrows, 16) columns.
+  const int n32 = (nrows + 31) >> 5;
+  const bool part = TN >= 64 && n32 * 32 < TN;
+  const uint32_t b_bytes = part ? static_cast<uint32_t>(n32) * kPartBoxBytes : kBTile;
+  const uint32_t idesc = make_idesc_bf16(128, part ? ((nrows + 15) & ~15) : TN);
+  // first A-image row of this (expert, block).  MODE 0: the shared expert's rows follow the
+  // routed experts in one image; MODE 1: the shared expert has its own tensor map (its K
+  // extent differs).
+  const bool own_map = (MODE == 1) && shared_expert;
+  const CUtensorMap* map_a = own_map ? &tmap_a_shared : &tmap_a;
+  const int a_row = (own_map ? 0 : (shared_expert ? a.n_experts : e) * a.rows_per_expert) +
+                    static_cast<int>(blockIdx.x) * MB * 128;
+  // A blocks this CTA really has (an odd block count leaves the last CTA with one)
+  const int n_mb = min(MB, (shared_expert ? a.mblocks_shared : a.mblocks_routed) -
+                               static_cast<int>(blockIdx.x) * MB);
+
+  int preloaded = 0;  // stages whose A tiles are already in flight (producer thread only)
+  if (a.early_tiles) {
+    if (active && warp == 0 && lane == 0) {
+      preloaded = min(kStages, num_k_blocks);
+      // tiled image: tile (a_row / 128, kb) is 128 consecutive rows of the 64-column view
+      for (int kb = 0; kb < preloaded; ++kb) {
+        mbar_arrive_expect_tx(full_bar(kb), n_mb * kATileBytes + nsplit * b_bytes);
+#pragma unroll
+        for (int m = 0; m < MB; ++m)
+          if (m < n_mb)
+            tma_load_2d(smem_base + kb * kStageBytes + m * kATileBytes, map_a, 0,
+                        (((a_row >> 7) + m) * num_k_blocks + kb) * 128, full_bar(kb),
+                        kPolicyEvictFirst);
+      }
+      // the blocks' remaining K tiles: 16 KB each, contiguous per block in the tiled image
+      const char* img = reinterpret_cast<const char*>(own_map ? a.a_shared_base : a.a_base);
+      if (img != nullptr)
+        for (int m = 0; m < n_mb; ++m)
+          for (int kb = preloaded; kb < num_k_blocks; ++kb)
+            l2_prefetch(img + (static_cast<size_t>((a_row >> 7) + m) * num_k_blocks + kb) * kATileBytes,
+                        kATileBytes);
+    }
+    pdl_wait();
+    pdl_launch_dependents();
+  }
 
   if (active) {
-    const int num_k_blocks = shared_expert ? a.kblocks_shared : a.kblocks_routed;
-    const int nsplit = (MODE == 0) ? 1 : a.nsplit;
-    // first A-image row of this (expert, block).  MODE 0: the shared expert's rows follow the
-    // routed experts in one image; MODE 1: the shared expert has its own tensor map (its K
-    // extent differs).
-    const bool own_map = (MODE == 1) && shared_expert;
-    const CUtensorMap* map_a = own_map ? &tmap_a_shared : &tmap_a;
-    const int a_row = (own_map ? 0 : (shared_expert ? a.n_experts : e) * a.rows_per_expert) +
-                      static_cast<int>(blockIdx.x) * MB * 128;
-    // A blocks this CTA really has (an odd block count leaves the last CTA with one)
-    const int n_mb = min(MB, (shared_expert ? a.mblocks_shared : a.mblocks_routed) -
-                                 static_cast<int>(blockIdx.x) * MB);
-
     if (warp == 0) {
       if (lane == 0) {
         for (int kb = 0; kb < num_k_blocks; ++kb) {
           const int s = kb % kStages;
           const uint32_t ph = (kb / kStages) & 1u;
-          mbar_wait(empty_bar(s), ph ^ 1u);
-          mbar_arrive_expect_tx(full_bar(s), n_mb * kATileBytes + nsplit * kBTile);
           const uint32_t a_smem = smem_base + s * kStageBytes;
-          // tiled image: tile (a_row / 128, kb) is 128 consecutive rows of the 64-column view
+          if (kb >= preloaded) {
+            mbar_wait(empty_bar(s), ph ^ 1u);
+            mbar_arrive_expect_tx(full_bar(s), n_mb * kATileBytes + nsplit * b_bytes);
 #pragma unroll
-          for (int m = 0; m < MB; ++m)
-            if (m < n_mb)
-              tma_load_2d(a_smem + m * kATileBytes, map_a, 0,
-                          (((a_row >> 7) + m) * num_k_blocks + kb) * 128, full_bar(s),
-                          kPolicyEvictFirst);
+            for (int m = 0; m < MB; ++m)
+              if (m < n_mb)
+                tma_load_2d(a_smem + m * kATileBytes, map_a, 0,
+                            (((a_row >> 7) + m) * num_k_blocks + kb) * 128, full_bar(s),
+                            kPolicyEvictFirst);
+          }
+          if (kb == num_k_blocks - 1) TC_STAMP(0, 2);
+          if (part) {
+            for (int j = 0; j < n32; ++j) {
+              const uint32_t dst = a_smem + kAll + j * kPartBoxBytes;
+              tma_load_2d(dst, &tmap_s0, kb * kBlockK, row0 + 32 * j, full_bar(s), kPolicyEvictLast);
+              if (MODE == 1 && nsplit > 1)
+                tma_load_2d(dst + kBTile, &tmap_s1, kb * kBlockK, row0 + 32 * j, full_bar(s),
+                            kPolicyEvictLast);
+              if (MODE == 1 && nsplit > 2)
+                tma_load_2d(dst + 2 * kBTile, &tmap_s2, kb * kBlockK, row0 + 32 * j, full_bar(s),
+                            kPolicyEvictLast);
+            }
+            continue;
+          }
           tma_load_2d(a_smem + kAll, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
           if (MODE == 1 && nsplit > 1)
             tma_load_2d(a_smem + kAll + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
@@ -187,6 +278,8 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           const uint32_t ph = (kb / kStages) & 1u;
           mbar_wait(full_bar(s), ph);
           tc_fence_after();
+          if (kb == 0) TC_STAMP(32, 3);
+          if (kb == num_k_blocks - 1) TC_STAMP(32, 4);
           const uint32_t a_smem = smem_base + s * kStageBytes;
 #pragma unroll
           for (int m = 0; m < MB; ++m) {
@@ -200,7 +293,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
                   for (int k = 0; k < kBlockK / 16; ++k) {
                     // +32 bytes per UMMA K step (16 bf16) inside the 128-byte swizzle row
                     umma_bf16(tmem_base + static_cast<uint32_t>(m * TN), a_desc + 2u * k,
-                              b_desc + 2u * k, kIdesc, (kb | k | sp) != 0 ? 1u : 0u);
+                              b_desc + 2u * k, idesc, (kb | k | sp) != 0 ? 1u : 0u);
                   }
                 }
               }
@@ -216,6 +309,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int m_valid = shared_expert ? a.m_shared : a.m_routed;
       mbar_wait(tmem_full_bar, 0);
       tc_fence_after();
+      TC_STAMP(64, 5);
 #pragma unroll 1
       for (int m = 0; m < n_mb; ++m) {
       const uint32_t tmem_blk = tmem_base + static_cast<uint32_t>(m * TN);
@@ -266,6 +360,7 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
       }
       }  // A blocks
       tc_fence_before();
+      TC_STAMP(64, 6);
     }
   }
 
@@ -309,13 +404,15 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
                           const __grid_constant__ CUtensorMap tmap_a_shared,
                           const __grid_constant__ CUtensorMap tmap_b0,
                           const __grid_constant__ CUtensorMap tmap_b1,
-                          const __grid_constant__ CUtensorMap tmap_b2, const TcArgs a) {
+                          const __grid_constant__ CUtensorMap tmap_b2,
+                          const __grid_constant__ CUtensorMap tmap_s0,
+                          const __grid_constant__ CUtensorMap tmap_s1,
+                          const __grid_constant__ CUtensorMap tmap_s2, const TcArgs a) {
   constexpr int kStages = chunked_stages(TN, MODE);
   constexpr int kStageBytes = stage_bytes(TN, MODE, 1);
   constexpr int kBTile = b_tile_bytes(TN);
   constexpr uint32_t kCols = tmem_cols(TN);            // columns of one accumulator
   constexpr uint32_t kTmemCols = chunked_tmem_cols(TN);  // master + two chunk buffers
-  constexpr uint32_t kIdesc = make_idesc_bf16(128, TN);
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -368,6 +465,11 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
   if (active) {
     const int num_k_blocks = shared_expert ? a.kblocks_shared : a.kblocks_routed;
     const int nsplit = (MODE == 0) ? 1 : a.nsplit;
+    // partial token tiles: only the 32-row boxes that hold rows (see grouped_tc_kernel)
+    const int n32 = (nrows + 31) >> 5;
+    const bool part = TN >= 64 && n32 * 32 < TN;
+    const uint32_t b_bytes = part ? static_cast<uint32_t>(n32) * kPartBoxBytes : kBTile;
+    const uint32_t idesc = make_idesc_bf16(128, part ? ((nrows + 15) & ~15) : TN);
     const int kc = max(1, kChunkSteps / (4 * nsplit));  // K blocks per chunk
     const int n_chunks = ceil_div(num_k_blocks, kc);
     const bool own_map = (MODE == 1) && shared_expert;
@@ -381,10 +483,23 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
           const int s = kb % kStages;
           const uint32_t ph = (kb / kStages) & 1u;
           mbar_wait(empty_bar(s), ph ^ 1u);
-          mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * kBTile);
+          mbar_arrive_expect_tx(full_bar(s), kATileBytes + nsplit * b_bytes);
           const uint32_t a_smem = smem_base + s * kStageBytes;
           tma_load_2d(a_smem, map_a, 0, ((a_row >> 7) * num_k_blocks + kb) * 128, full_bar(s),
                       kPolicyEvictFirst);
+          if (part) {
+            for (int j = 0; j < n32; ++j) {
+              const uint32_t dst = a_smem + kATileBytes + j * kPartBoxBytes;
+              tma_load_2d(dst, &tmap_s0, kb * kBlockK, row0 + 32 * j, full_bar(s), kPolicyEvictLast);
+              if (MODE == 1 && nsplit > 1)
+                tma_load_2d(dst + kBTile, &tmap_s1, kb * kBlockK, row0 + 32 * j, full_bar(s),
+                            kPolicyEvictLast);
+              if (MODE == 1 && nsplit > 2)
+                tma_load_2d(dst + 2 * kBTile, &tmap_s2, kb * kBlockK, row0 + 32 * j, full_bar(s),
+                            kPolicyEvictLast);
+            }
+            continue;
+          }
           tma_load_2d(a_smem + kATileBytes, &tmap_b0, kb * kBlockK, row0, full_bar(s), kPolicyEvictLast);
           if (MODE == 1 && nsplit > 1)
             tma_load_2d(a_smem + kATileBytes + kBTile, &tmap_b1, kb * kBlockK, row0, full_bar(s),
@@ -419,7 +534,7 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
                 const uint64_t b_desc = make_smem_desc_sw128(a_smem + kATileBytes + sp * kBTile);
 #pragma unroll
                 for (int k = 0; k < kBlockK / 16; ++k) {
-                  umma_bf16(acc, a_desc + 2u * k, b_desc + 2u * k, kIdesc, first ? 0u : 1u);
+                  umma_bf16(acc, a_desc + 2u * k, b_desc + 2u * k, idesc, first ? 0u : 1u);
                   first = false;
                 }
               }
@@ -521,7 +636,8 @@ static void ensure_smem_attr(K kernel, int smem, unsigned long long* mask) {
 template <int TN, int MODE>
 static void launch_tc_chunked(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
                               const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
-                              const TcArgs& a, int grid_x, int max_tiles) {
+                              const CUtensorMap* ts /*[3]: 32-row boxes*/, const TcArgs& a, int grid_x,
+                              int max_tiles) {
   static unsigned long long mask = 0;
   constexpr int smem = chunked_smem_bytes(TN, MODE);
   ensure_smem_attr(grouped_tc_chunked_kernel<TN, MODE>, smem, &mask);
@@ -535,7 +651,8 @@ static void launch_tc_chunked(const LaunchCtx& ctx, const CUtensorMap* ta, const
   cfg.gridDim = dim3(grid_x, max_tiles);
   cfg.blockDim = dim3(kGateupThreads);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, grouped_tc_chunked_kernel<TN, MODE>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
+  cudaLaunchKernelEx(&cfg, grouped_tc_chunked_kernel<TN, MODE>, *ta, *ta_sh, *tb0, *tb1, *tb2, ts[0],
+                     ts[MODE == 1 ? 1 : 0], ts[MODE == 1 ? 2 : 0], a);
 }
 
 // Chunked accumulation pays when one accumulator would take more than ~96 truncating steps
@@ -555,7 +672,8 @@ static int pick_tile_case(int tile_tokens) {
 template <int TN, int MODE, int MB = 1>
 static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CUtensorMap* ta_sh,
                            const CUtensorMap* tb0, const CUtensorMap* tb1, const CUtensorMap* tb2,
-                           const TcArgs& a, int grid_x, int max_tiles) {
+                           const CUtensorMap* ts /*[3]: 32-row boxes*/, const TcArgs& a, int grid_x,
+                           int max_tiles) {
   static unsigned long long mask = 0;
   constexpr int smem = gateup_smem_bytes(TN, MODE, MB);
   ensure_smem_attr(grouped_tc_kernel<TN, MODE, MB>, smem, &mask);
@@ -569,13 +687,17 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
   cfg.gridDim = dim3(ceil_div(grid_x, MB), max_tiles);
   cfg.blockDim = dim3(kGateupThreads);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, grouped_tc_kernel<TN, MODE, MB>, *ta, *ta_sh, *tb0, *tb1, *tb2, a);
+  cudaLaunchKernelEx(&cfg, grouped_tc_kernel<TN, MODE, MB>, *ta, *ta_sh, *tb0, *tb1, *tb2, ts[0],
+                     ts[MODE == 1 ? 1 : 0], ts[MODE == 1 ? 2 : 0], a);
 }
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
-                     int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
-                     float* h, bool token_tiles, float* sg, bool pair_blocks, bool precise) {
+                     const CUtensorMap* tmap_x32, int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
+                     float* h, bool token_tiles, float* sg, bool pair_blocks, bool precise,
+                     bool early_tiles, const void* w_image) {
   TcArgs a{};
+  a.early_tiles = early_tiles ? 1 : 0;
+  a.a_base = a.a_shared_base = w_image;
   a.sg_out = sg;
   a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;
   a.tile_expert = d.tile_expert;
@@ -595,36 +717,40 @@ int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUte
   const int gx = a.mblocks_routed > a.mblocks_shared ? a.mblocks_routed : a.mblocks_shared;
   if (wants_chunks(precise, a.kblocks_routed, 1)) {
     switch (pick_tile_case(tile_tokens)) {
-      case 16: launch_tc_chunked<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-      case 32: launch_tc_chunked<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-      case 64: launch_tc_chunked<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-      default: launch_tc_chunked<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+      case 16: launch_tc_chunked<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+      case 32: launch_tc_chunked<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+      case 64: launch_tc_chunked<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+      default: launch_tc_chunked<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
     }
     return 1;
   }
   if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
-    launch_tc_case<64, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles);
+    launch_tc_case<64, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles);
     return 1;
   }
   if (pair_blocks && pick_tile_case(tile_tokens) == 128) {
-    launch_tc_case<128, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles);
+    launch_tc_case<128, 0, 2>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles);
     return 1;
   }
   switch (pick_tile_case(tile_tokens)) {
-    case 16: launch_tc_case<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-    case 32: launch_tc_case<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-    case 64: launch_tc_case<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-    case 128: launch_tc_case<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
-    default: launch_tc_case<256, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, a, gx, max_tiles); break;
+    case 16: launch_tc_case<16, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+    case 32: launch_tc_case<32, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+    case 64: launch_tc_case<64, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+    case 128: launch_tc_case<128, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
+    default: launch_tc_case<256, 0>(ctx, tmap_w, tmap_w, tmap_x, tmap_x, tmap_x, tmap_x32, a, gx, max_tiles); break;
   }
   return 1;
 }
 
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
-                   int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
-                   const Geometry& g, float* slot_out, bool pair_blocks, bool precise) {
+                   const CUtensorMap* tmap_hb32 /*[3]*/, int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
+                   const Geometry& g, float* slot_out, bool pair_blocks, bool precise,
+                   bool early_tiles, const void* wdt_image, const void* wdt_shared_image) {
   TcArgs a{};
+  a.early_tiles = early_tiles ? 1 : 0;
+  a.a_base = wdt_image;
+  a.a_shared_base = wdt_shared_image;
   a.tile_expert = d.tile_expert;
   a.tile_row0 = d.tile_row0;
   a.tile_nrows = d.tile_nrows;
@@ -644,27 +770,27 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
     const int kmax = a.kblocks_routed > a.kblocks_shared ? a.kblocks_routed : a.kblocks_shared;
     if (wants_chunks(precise, kmax, nsplit)) {
       switch (pick_tile_case(tile_tokens)) {
-        case 16: launch_tc_chunked<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-        case 32: launch_tc_chunked<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-        case 64: launch_tc_chunked<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-        default: launch_tc_chunked<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+        case 16: launch_tc_chunked<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+        case 32: launch_tc_chunked<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+        case 64: launch_tc_chunked<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+        default: launch_tc_chunked<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
       }
       return 1;
     }
   }
   if (pair_blocks && pick_tile_case(tile_tokens) == 64) {
-    launch_tc_case<64, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles);
+    launch_tc_case<64, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles);
     return 1;
   }
   if (pair_blocks && pick_tile_case(tile_tokens) >= 128) {
-    launch_tc_case<128, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles);
+    launch_tc_case<128, 1, 2>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles);
     return 1;
   }
   switch (pick_tile_case(tile_tokens)) {
-    case 16: launch_tc_case<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-    case 32: launch_tc_case<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-    case 64: launch_tc_case<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
-    default: launch_tc_case<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, a, gx, max_tiles); break;
+    case 16: launch_tc_case<16, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+    case 32: launch_tc_case<32, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+    case 64: launch_tc_case<64, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
+    default: launch_tc_case<128, 1>(ctx, tmap_wdt, sh, tmap_hb, tmap_hb + 1, tmap_hb + 2, tmap_hb32, a, gx, max_tiles); break;
   }
   return 1;
 }

@@ -95,14 +95,15 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
                        int block, int32_t* sorted_out, int32_t* expert_of_block, int32_t* counts2);
 
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
-                     int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
+                     const CUtensorMap* tmap_x32 /*32-row boxes*/, int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
                      float* h, bool token_tiles, float* sg = nullptr, bool pair_blocks = false,
-                     bool precise = false);
+                     bool precise = false, bool early_tiles = false, const void* w_image = nullptr);
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
-                   int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
+                   const CUtensorMap* tmap_hb32 /*[3], 32-row boxes*/, int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
                    const Geometry& g, float* slot_out, bool pair_blocks = false,
-                   bool precise = false);
+                   bool precise = false, bool early_tiles = false, const void* wdt_image = nullptr,
+                   const void* wdt_shared_image = nullptr);
 int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
                         const float* weights, int B, const Geometry& g, float* y);
 int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
@@ -212,6 +213,7 @@ int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, i
 int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
                         int Kp, __nv_bfloat16* dst);
 int launch_fill_f32(cudaStream_t s, float* dst, float value, size_t count);
+int launch_l2_prefetch(cudaStream_t s, const void* base, size_t bytes);
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
                      float* dst);
 
