@@ -108,8 +108,6 @@ struct skb_layer {
   Geometry g{};
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux_stream = nullptr;  // L2 prefetch of the weight image beside the routing front-end
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int l2_bytes = 0;
   std::mutex mu;
 
@@ -366,9 +364,6 @@ int new_layer(const skb_config* cfg, int device, skb_layer** out, int route_E = 
     return fail(SKB_ECUDA, "cudaStreamCreate failed: %s", cudaGetErrorString(e));
   }
   for (auto& ev : L->ev) cudaEventCreate(&ev);
-  cudaStreamCreateWithFlags(&L->aux_stream, cudaStreamNonBlocking);
-  cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming);
   cudaDeviceGetAttribute(&L->l2_bytes, cudaDevAttrL2CacheSize, device);
   const size_t gu_rows = static_cast<size_t>(g.E) * 2 * g.Np + 2 * static_cast<size_t>(g.Sp);
   const size_t wd_rows = static_cast<size_t>(g.E) * g.Np + g.Sp;
@@ -650,22 +645,6 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
       ((a->flags & SKB_FLAG_PAIRED_BLOCKS) || (tn == 128 && paired_gateup_ctas >= 4L * L->n_sms));
   const bool pair_down = pair_for(g.Dp128 / 128);
 
-  // Weight image into the L2 while the routing front-end runs (EXPERIMENT: SKB_L2PF=1 gate/up,
-  // 2 = gate/up + W_down^T)
-  bool forked = false;
-  {
-    static const int pf = getenv("SKB_L2PF") ? atoi(getenv("SKB_L2PF")) : 0;
-    if (pf && !timing && BK >= 3 * g.E) {
-      const size_t gu = static_cast<size_t>(g.E) * 2 * g.Np * g.Dp * 2;
-      const size_t dn = static_cast<size_t>(g.E) * g.Dp128 * g.Np * 2;
-      cudaEventRecord(L->ev_fork, stream);
-      cudaStreamWaitEvent(L->aux_stream, L->ev_fork, 0);
-      launches += launch_l2_prefetch(L->aux_stream, L->d_wgu, gu);
-      if (pf >= 2) launches += launch_l2_prefetch(L->aux_stream, L->d_wdt, dn);
-      cudaEventRecord(L->ev_join, L->aux_stream);
-      forked = true;
-    }
-  }
   tm.mark();
   if (d_ids_in != nullptr) {
     // external routing: ids (and weights, default 1) are given; only the dispatch runs
@@ -749,10 +728,17 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   tm.mark();
 
   if (dense_down) {
+    // W_down^T blocks prefetched into the L2 while the CTAs wait for the selection kernel: pays
+    // when the image is small enough to sit there (Granite shape batch 256: the down stage starts
+    // 2.5 us earlier); on a long stream the prefetches only queue ahead of the demand loads
+    // (Qwen3.5 shape batch 64: stage time 79 -> 93 us)
+    const bool prefetch_wdt =
+        static_cast<size_t>(g.E) * g.Dp128 * g.Np * 2 <= static_cast<size_t>(L->l2_bytes) / 2;
     launches += launch_down_tc(ctx, &L->tmap_wdt, g.has_shared ? &L->tmap_wdt_shared : nullptr,
                                L->tmap_hb[tn_idx], L->tmap_hb[1], nsplit, tn, L->disp, max_tiles, g,
-                               L->d_slot_out, pair_down, precise, /*early_tiles=*/true, L->d_wdt,
-                               L->d_wdt_shared);
+                               L->d_slot_out, pair_down, precise, /*early_tiles=*/true,
+                               prefetch_wdt ? L->d_wdt : nullptr,
+                               prefetch_wdt ? L->d_wdt_shared : nullptr);
     tm.mark();
     launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y);
     tm.mark();
@@ -786,7 +772,6 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     tm.mark();
     tm.mark();
   }
-  if (forked) cudaStreamWaitEvent(stream, L->ev_join, 0);
   L->last_launches = launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SKB_ECUDA, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -1334,9 +1319,6 @@ void skb_layer_destroy(skb_layer* L) {
   for (auto& ev : L->ev)
     if (ev) cudaEventDestroy(ev);
   if (L->stream) cudaStreamDestroy(L->stream);
-  if (L->aux_stream) cudaStreamDestroy(L->aux_stream);
-  if (L->ev_fork) cudaEventDestroy(L->ev_fork);
-  if (L->ev_join) cudaEventDestroy(L->ev_join);
   delete L;
 }
 

@@ -114,6 +114,50 @@ struct TcArgs {
                     // weight stream startable -- before the programmatic-launch wait
 };
 
+// MODE 0 epilogue of 16 accumulator columns held by one warp: lanes 0-15 hold gate(n) for the
+// columns, lanes 16-31 hold up(n).  One exchange per column pair -- gate lanes finish column c,
+// up lanes finish column c + 1 -- then the eight SwiGLUs of a lane as interleaved straight-line
+// chains (silu8), then the stores.
+template <int TN>
+__device__ __forceinline__ void swiglu_store16(const uint32_t (&v)[16], int lane, int c0, int nrows,
+                                               int n, int m_valid, int row0, int tile,
+                                               const TcArgs& a) {
+  const bool is_gate_lane = lane < 16;
+  float gv[8], uv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float mine0 = __uint_as_float(v[2 * c]);
+    const float mine1 = __uint_as_float(v[2 * c + 1]);
+    const float recv = __shfl_xor_sync(0xffffffffu, is_gate_lane ? mine1 : mine0, 16);
+    gv[c] = is_gate_lane ? mine0 : recv;
+    uv[c] = is_gate_lane ? recv : mine1;
+  }
+  silu8(gv);
+  const int colb = c0 + (is_gate_lane ? 0 : 1);
+  if (TN == 16 && a.tile_colrow != nullptr) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int col = colb + 2 * c;
+      const int r = (col < nrows && n < m_valid) ? a.tile_colrow[tile * 16 + col] : -1;
+      if (r >= 0) {
+        a.out[static_cast<size_t>(r) * a.out_stride + n] = gv[c] * uv[c];
+        if (a.sg_out != nullptr) a.sg_out[static_cast<size_t>(r) * a.out_stride + n] = gv[c];
+      }
+    }
+  } else {
+    float* orow = a.out + static_cast<size_t>(row0 + colb) * a.out_stride + n;
+    float* srow = a.sg_out ? a.sg_out + static_cast<size_t>(row0 + colb) * a.out_stride + n : nullptr;
+    const size_t step = 2 * static_cast<size_t>(a.out_stride);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (colb + 2 * c < nrows && n < m_valid) {
+        orow[c * step] = gv[c] * uv[c];
+        if (srow != nullptr) srow[c * step] = gv[c];
+      }
+    }
+  }
+}
+
 template <int TN, int MODE, int MB>
 __global__ void __launch_bounds__(kGateupThreads, (MB == 2) ? ((MODE == 0 && TN == 128) ? 2 : 1) : ((MODE == 1 && TN <= 16) ? 4 : ((MODE == 0 && TN <= 16) ? 3 : ((MODE == 0 || TN <= 32) ? 2 : 1))))
 grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -315,47 +359,36 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const uint32_t tmem_blk = tmem_base + static_cast<uint32_t>(m * TN);
       if (MODE == 0) {
         const int n = (static_cast<int>(blockIdx.x) * MB + m) * kNeuronBlock + 16 * q + (lane & 15);
-        const bool is_gate_lane = lane < 16;
 #pragma unroll 1
         for (int c0 = 0; c0 < TN; c0 += 16) {
           if (c0 >= nrows) break;
           uint32_t v[16];
           tmem_ld_32x32b_x16(tmem_blk + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
           tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 16; c += 2) {
-            // lanes 0-15 hold gate(n) for columns c, c+1; lanes 16-31 hold up(n).  One
-            // exchange: gate lanes finish column c, up lanes finish column c+1.
-            const float mine0 = __uint_as_float(v[c]);
-            const float mine1 = __uint_as_float(v[c + 1]);
-            const float send = is_gate_lane ? mine1 : mine0;
-            const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-            const float g = is_gate_lane ? mine0 : recv;
-            const float u = is_gate_lane ? recv : mine1;
-            const int col = c0 + c + (is_gate_lane ? 0 : 1);
-            if (col < nrows && n < m_valid) {
-              const int r = (TN == 16 && a.tile_colrow != nullptr) ? a.tile_colrow[tile * 16 + col]
-                                                                   : row0 + col;
-              if (r >= 0) {
-                const float sgv = silu_f(g);
-                a.out[static_cast<size_t>(r) * a.out_stride + n] = sgv * u;
-                if (a.sg_out != nullptr) a.sg_out[static_cast<size_t>(r) * a.out_stride + n] = sgv;
-              }
-            }
-          }
+          swiglu_store16<TN>(v, lane, c0, nrows, n, m_valid, row0, tile, a);
         }
       } else {
         const int d = (static_cast<int>(blockIdx.x) * MB + m) * 128 + 32 * q + lane;
+        // 32 columns per TMEM round trip
 #pragma unroll 1
-        for (int c0 = 0; c0 < TN; c0 += 16) {
+        for (int c0 = 0; c0 < TN; c0 += 32) {
           if (c0 >= nrows) break;
-          uint32_t v[16];
-          tmem_ld_32x32b_x16(tmem_blk + (static_cast<uint32_t>(32 * q) << 16) + c0, v);
+          uint32_t v0[16], v1[16];
+          const uint32_t taddr = tmem_blk + (static_cast<uint32_t>(32 * q) << 16) + c0;
+          tmem_ld_32x32b_x16(taddr, v0);
+          if (TN >= 32) tmem_ld_32x32b_x16(taddr + 16, v1);
           tmem_ld_wait();
+          float* orow = a.out + static_cast<size_t>(row0 + c0) * a.out_stride + d;
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             if (c0 + c < nrows && d < m_valid)
-              a.out[static_cast<size_t>(row0 + c0 + c) * a.out_stride + d] = __uint_as_float(v[c]);
+              orow[static_cast<size_t>(c) * a.out_stride] = __uint_as_float(v0[c]);
+          if (TN >= 32) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c0 + 16 + c < nrows && d < m_valid)
+                orow[static_cast<size_t>(16 + c) * a.out_stride] = __uint_as_float(v1[c]);
+          }
         }
       }
       }  // A blocks
@@ -559,7 +592,6 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
         const bool last = c == n_chunks - 1;
         const int n = (MODE == 0) ? static_cast<int>(blockIdx.x) * kNeuronBlock + 16 * q + (lane & 15)
                                   : static_cast<int>(blockIdx.x) * 128 + 32 * q + lane;
-        const bool is_gate_lane = lane < 16;
 #pragma unroll 1
         for (int c0 = 0; c0 < TN; c0 += 16) {
           if (c0 >= nrows) break;
@@ -577,25 +609,7 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
             continue;
           }
           if (MODE == 0) {
-#pragma unroll
-            for (int cc = 0; cc < 16; cc += 2) {
-              const float mine0 = __uint_as_float(v[cc]);
-              const float mine1 = __uint_as_float(v[cc + 1]);
-              const float send = is_gate_lane ? mine1 : mine0;
-              const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-              const float g = is_gate_lane ? mine0 : recv;
-              const float u = is_gate_lane ? recv : mine1;
-              const int col = c0 + cc + (is_gate_lane ? 0 : 1);
-              if (col < nrows && n < m_valid) {
-                const int r = (TN == 16 && a.tile_colrow != nullptr) ? a.tile_colrow[tile * 16 + col]
-                                                                     : row0 + col;
-                if (r >= 0) {
-                  const float sgv = silu_f(g);
-                  a.out[static_cast<size_t>(r) * a.out_stride + n] = sgv * u;
-                  if (a.sg_out != nullptr) a.sg_out[static_cast<size_t>(r) * a.out_stride + n] = sgv;
-                }
-              }
-            }
+            swiglu_store16<TN>(v, lane, c0, nrows, n, m_valid, row0, tile, a);
           } else {
 #pragma unroll
             for (int cc = 0; cc < 16; ++cc)

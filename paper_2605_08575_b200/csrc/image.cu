@@ -138,25 +138,6 @@ int launch_fill_f32(cudaStream_t s, float* dst, float value, size_t count) {
   fill_f32_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, value, count);
   return 1;
 }
-// L2 prefetch of a weight range: one cp.async.bulk.prefetch.L2 of kPrefetchChunk bytes per thread.
-// Fire and forget -- the kernel retires as soon as the requests are issued; HBM fills the L2
-// while the routing front-end (which touches ~1 MB) runs.
-constexpr unsigned kPrefetchChunk = 4096;
-__global__ void __launch_bounds__(256) l2_prefetch_kernel(const char* __restrict__ base, size_t bytes) {
-  const size_t i = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kPrefetchChunk;
-  if (i >= bytes) return;
-  const size_t left = bytes - i;
-  const unsigned n = left < kPrefetchChunk ? static_cast<unsigned>(left & ~size_t{15}) : kPrefetchChunk;
-  if (n)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + i), "r"(n) : "memory");
-}
-int launch_l2_prefetch(cudaStream_t s, const void* base, size_t bytes) {
-  if (bytes == 0) return 0;
-  const size_t chunks = (bytes + kPrefetchChunk - 1) / kPrefetchChunk;
-  l2_prefetch_kernel<<<static_cast<unsigned>((chunks + 255) / 256), 256, 0, s>>>(
-      static_cast<const char*>(base), bytes);
-  return 1;
-}
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
                      float* dst) {
   synth_f32_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(seed, scale, off,

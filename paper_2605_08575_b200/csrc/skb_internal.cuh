@@ -213,7 +213,6 @@ int launch_pack_down_t(cudaStream_t s, const float* down_t, int n_rows, int D, i
 int launch_synth_down_t(cudaStream_t s, uint64_t seed, float scale, uint64_t off, int n_rows, int D,
                         int Kp, __nv_bfloat16* dst);
 int launch_fill_f32(cudaStream_t s, float* dst, float value, size_t count);
-int launch_l2_prefetch(cudaStream_t s, const void* base, size_t bytes);
 int launch_synth_f32(cudaStream_t s, uint64_t seed, float scale, uint64_t off, uint64_t count,
                      float* dst);
 
