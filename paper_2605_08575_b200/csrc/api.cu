@@ -255,7 +255,7 @@ int reserve_locked(skb_layer* L, int B) {
     SKB_TRY(encode_bf16_2d(&L->tmap_xb, L->d_xb, xb_rows, g.Dp, 16));
   }
   {
-    const size_t n_counters = 2 + static_cast<size_t>(cap);
+    const size_t n_counters = 4 + static_cast<size_t>(cap);  // router counters + grid-barrier pair
     SKB_TRY(dmalloc(&L->d_counters, n_counters));
     SKB_CUDA(cudaMemsetAsync(L->d_counters, 0, n_counters * sizeof(unsigned), L->stream));
   }
@@ -645,6 +645,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
       ((a->flags & SKB_FLAG_PAIRED_BLOCKS) || (tn == 128 && paired_gateup_ctas >= 4L * L->n_sms));
   const bool pair_down = pair_for(g.Dp128 / 128);
 
+  bool permuted = false;  // the router stage wrote the expert-sorted token copy itself
   tm.mark();
   if (d_ids_in != nullptr) {
     // external routing: ids (and weights, default 1) are given; only the dispatch runs
@@ -674,10 +675,15 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     r.tile_tokens = tn;
     r.xb = token_tiles ? L->d_xb : nullptr;
     r.Dp = g.Dp;
+    if (!token_tiles && !(a->flags & SKB_FLAG_FAST_ROUTER)) {
+      r.xs = L->d_xs;
+      r.grid_bar = L->d_counters + 2 + L->cap_batch;
+    }
+    permuted = router_fuses_permute(r);
     launches += launch_router(ctx, r);
   }
   tm.mark();
-  if (!token_tiles)
+  if (!token_tiles && !permuted)
     launches += launch_permute_tokens(ctx, d_x, L->disp.perm, B, g.K, g.D, g.Dp, g.has_shared,
                                       L->d_xs);
   tm.mark();
@@ -687,7 +693,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
     launches += launch_gateup_tc(ctx, &L->tmap_w, token_tiles ? &L->tmap_xb : &L->tmap_x[tn_idx],
                                  &L->tmap_x[1], tn, L->disp, max_tiles, g, L->d_h, token_tiles,
                                  sel_mode == kSelectThreshold ? L->d_sg : nullptr, pair_gateup,
-                                 precise, /*early_tiles=*/!token_tiles, /*prefetch image=*/nullptr);
+                                 precise, /*early_tiles=*/!token_tiles && !permuted,
+                                 /*prefetch image=*/nullptr);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel

@@ -159,6 +159,200 @@ __global__ void __launch_bounds__(128) route_tokens_kernel(const float* __restri
                    weights + static_cast<size_t>(t) * K);
 }
 
+// ---------------------------------------------------------------------------------------------
+// route() + dispatch + token permutation of a batch as ONE kernel (batches whose CTAs are all
+// resident): a warp per token, 4 tokens per CTA.
+//   1. every warp routes its token (ids, weights to global memory);
+//   2. grid barrier (arrive counter + generation word, self-resetting: graph-replay safe);
+//   3. every CTA reads all B*K expert ids (L2) into two shared-memory histograms -- slots of the
+//      whole batch and slots before its own first slot -- so that it can place its own 4*K slots
+//      of the stable counting sort without any other CTA: pos = off[e] + before[e] + rank;
+//      CTA 0 also writes the expert offsets and the tile list;
+//   4. every warp converts its token to bf16 ONCE and writes the K (+1 shared) expert-sorted
+//      copies the gate/up GEMM reads.
+// Same perm / inv / tile list as dispatch_kernel, bit for bit.  Replaces three launches
+// (route_tokens_kernel, dispatch_chunks_kernel: a single CTA, permute_tokens_kernel) whose
+// boundaries and single-CTA latency were ~10 us of the Granite-shape batch-256 step.
+// ---------------------------------------------------------------------------------------------
+struct RouteDispatchArgs {
+  const float* logits;
+  const float* x;
+  int B, E, K, renorm, D, Dp, has_shared, tile_tokens;
+  int32_t* ids;
+  float* weights;
+  DispatchBuffers d;
+  __nv_bfloat16* xs;
+  unsigned* bar;  // {arrivals, generation}
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a) {
+  extern __shared__ __align__(16) float rd_smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = a.E, K = a.K, BK = a.B * a.K;
+  const int rt_words = round_up(E, 4) + round_up(K, 4);
+  float* rt = rd_smem + static_cast<size_t>(warp) * rt_words;
+  int32_t* tot = reinterpret_cast<int32_t*>(rd_smem + 4 * static_cast<size_t>(rt_words));  // [E]
+  int32_t* bef = tot + E;           // [E] slots before this CTA's first slot, per expert
+  int32_t* off = bef + E;           // [E + 1]
+  int32_t* tile_off = off + E + 1;  // [E + 1]
+  int32_t* pos_s = tile_off + E + 1;  // [4 * K] rows of this CTA's slots
+  const int t = blockIdx.x * 4 + warp;
+  for (int i = tid; i < 2 * E; i += 128) tot[i] = 0;
+
+  pdl_wait();
+  pdl_launch_dependents();
+  if (t < a.B)
+    warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, rt,
+                     a.ids + static_cast<size_t>(t) * K, a.weights + static_cast<size_t>(t) * K);
+
+  // ---- grid barrier ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned gen = ld_acquire_gpu_u32(a.bar + 1);
+    const unsigned old = atomicAdd(a.bar, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(a.bar, 0u);
+      __threadfence();
+      atomicAdd(a.bar + 1, 1u);
+    } else {
+      while (ld_acquire_gpu_u32(a.bar + 1) == gen) {
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- histograms over all slots ----
+  const int s0 = blockIdx.x * 4 * K;  // first flat slot of this CTA
+  for (int i = tid; i < BK; i += 128) {
+    const int e = __ldcg(a.ids + i);
+    atomicAdd(&tot[e], 1);
+    if (i < s0) atomicAdd(&bef[e], 1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int run = 0, trun = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int c = e < E ? tot[e] : 0;
+      const int tl = ceil_div(c, a.tile_tokens);
+      int ia = c, ib = tl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ua = __shfl_up_sync(0xffffffffu, ia, o);
+        const int ub = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+          ia += ua;
+          ib += ub;
+        }
+      }
+      if (e < E) {
+        off[e] = run + ia - c;
+        tile_off[e] = trun + ib - tl;
+      }
+      run += __shfl_sync(0xffffffffu, ia, 31);
+      trun += __shfl_sync(0xffffffffu, ib, 31);
+    }
+    if (lane == 0) {
+      off[E] = run;
+      tile_off[E] = trun;
+    }
+    __syncwarp();
+    // ---- this CTA's slots, in flat order, 32 at a time ----
+    const int n_own = max(0, min(4 * K, BK - s0));
+    for (int j0 = 0; j0 < n_own; j0 += 32) {
+      const int j = j0 + lane;
+      const int i = s0 + j;
+      const int e = j < n_own ? __ldcg(a.ids + i) : -1 - lane;  // distinct negatives: no matches
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      if (j < n_own) {
+        const int pos = off[e] + bef[e] + rank;
+        a.d.perm[pos] = i;
+        a.d.inv[i] = pos;
+        a.d.row_expert[pos] = e;
+        pos_s[j] = pos;
+      }
+      __syncwarp();
+      if (j < n_own && rank == 0) bef[e] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  if (blockIdx.x == 0) {
+    for (int e = tid; e <= E; e += 128) a.d.expert_off[e] = off[e];
+    // tile list: expert-major, tile_tokens rows per tile, then the shared expert's tiles
+    for (int e = tid; e < E; e += 128) {
+      const int c = tot[e];
+      const int nt = ceil_div(c, a.tile_tokens);
+      for (int j = 0; j < nt; ++j) {
+        const int ti = tile_off[e] + j;
+        a.d.tile_expert[ti] = e;
+        a.d.tile_row0[ti] = off[e] + j * a.tile_tokens;
+        a.d.tile_nrows[ti] = min(a.tile_tokens, c - j * a.tile_tokens);
+      }
+    }
+    int n_tiles = tile_off[E];
+    if (a.has_shared) {
+      const int nsh = ceil_div(a.B, a.tile_tokens);
+      for (int j = tid; j < nsh; j += 128) {
+        a.d.tile_expert[n_tiles + j] = E;
+        a.d.tile_row0[n_tiles + j] = BK + j * a.tile_tokens;
+        a.d.tile_nrows[n_tiles + j] = min(a.tile_tokens, a.B - j * a.tile_tokens);
+      }
+      n_tiles += nsh;
+    }
+    if (tid == 0) *a.d.n_tiles = n_tiles;
+  }
+
+  // ---- token permutation: the token's bf16 row, K (+1) copies ----
+  if (t < a.B) {
+    if (a.has_shared && lane == 0) a.d.row_expert[BK + t] = E;
+    const float* src = a.x + static_cast<size_t>(t) * a.D;
+    const int copies = K + (a.has_shared ? 1 : 0);
+    if ((a.D % 4) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      const int nq = a.D / 4;
+      for (int q0 = 0; q0 < nq; q0 += 256) {
+        uint2 o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = q0 + u * 32 + lane;
+          if (q < nq) {
+            const float4 v = __ldg(s4 + q);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+            o[u].x = *reinterpret_cast<uint32_t*>(&lo);
+            o[u].y = *reinterpret_cast<uint32_t*>(&hi);
+          }
+        }
+        for (int k = 0; k < copies; ++k) {
+          const int row = k < K ? pos_s[warp * K + k] : BK + t;
+          uint2* d2 = reinterpret_cast<uint2*>(a.xs + static_cast<size_t>(row) * a.Dp);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * 32 + lane;
+            if (q < nq) d2[q] = o[u];
+          }
+        }
+      }
+    } else {
+      for (int k = 0; k < copies; ++k) {
+        const int row = k < K ? pos_s[warp * K + k] : BK + t;
+        __nv_bfloat16* dst = a.xs + static_cast<size_t>(row) * a.Dp;
+        for (int dd = lane; dd < a.D; dd += 32) dst[dd] = __float2bfloat16_rn(src[dd]);
+      }
+    }
+  }
+}
+
 struct RouterFusedArgs {
   const float* x;
   const float* router;
@@ -412,6 +606,22 @@ __global__ void __launch_bounds__(256) router_logits_fast_kernel(const float* __
 // (Granite shape batch 8: 66.7 -> 54.3 us, OLMoE shape batch 8: 146 -> 130-143 us with the limit at 2.)
 static constexpr int fuse_route_max_batch() { return 2; }
 
+static size_t route_dispatch_smem(int E, int K) {
+  return (4 * static_cast<size_t>(round_up(E, 4) + round_up(K, 4)) + 4 * static_cast<size_t>(E) + 2 +
+          4 * static_cast<size_t>(K)) * 4;
+}
+
+// One launch for route + dispatch + permutation: the grid barrier inside needs every CTA resident
+// (4 tokens per CTA, 128 threads, a few KB of shared memory: 8+ CTAs per SM), and every CTA reads
+// all B*K ids, which stops paying on large batches.
+bool router_fuses_permute(const RouterLaunch& r) {
+  if (r.xs == nullptr || r.grid_bar == nullptr || r.dispatch == nullptr || r.x == nullptr) return false;
+  if (r.B <= fuse_route_max_batch()) return false;
+  if (static_cast<long>(r.B) * r.K > 4096) return false;
+  if (route_dispatch_smem(r.E, r.K) > 40 * 1024) return false;
+  return ceil_div(r.B, 4) <= 4 * 132;
+}
+
 bool router_token_tiles(int B, int K, bool want) {
   return want && B <= 16 && B <= fuse_route_max_batch() && B * K <= kSmallSlots;
 }
@@ -482,6 +692,29 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
     cfg.dynamicSmemBytes = static_cast<size_t>(a.stages) * kRfRows * kRfRow * 4 + 2 * a.stages * 8;
     cudaLaunchKernelEx(&cfg, router_fused_kernel, a);
     ++launches;
+  }
+  if (!a.fuse_route && router_fuses_permute(r)) {
+    RouteDispatchArgs rd{};
+    rd.logits = r.logits;
+    rd.x = r.x;
+    rd.B = r.B;
+    rd.E = r.E;
+    rd.K = r.K;
+    rd.renorm = r.renorm;
+    rd.D = r.D;
+    rd.Dp = r.Dp;
+    rd.has_shared = r.has_shared;
+    rd.tile_tokens = r.tile_tokens;
+    rd.ids = r.ids;
+    rd.weights = r.weights;
+    rd.d = *r.dispatch;
+    rd.xs = r.xs;
+    rd.bar = r.grid_bar;
+    cfg.gridDim = dim3(ceil_div(r.B, 4));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = route_dispatch_smem(r.E, r.K);
+    cudaLaunchKernelEx(&cfg, route_dispatch_kernel, rd);
+    return launches + 1;
   }
   if (!a.fuse_route) {
     cfg.gridDim = dim3(ceil_div(r.B, 4));

@@ -83,7 +83,13 @@ struct RouterLaunch {
   // GEMM reads token rows directly, no expert-sorted copy (no permute kernel)
   __nv_bfloat16* xb;
   int Dp;
+  // batches: route + dispatch + token permutation as one kernel (router.cu: route_dispatch_kernel)
+  // when the expert-sorted token copy `xs` and the two grid-barrier words are given
+  __nv_bfloat16* xs;
+  unsigned* grid_bar;
 };
+// true when launch_router() will also write the expert-sorted token copy (no permute kernel)
+bool router_fuses_permute(const RouterLaunch& r);
 // true when launch_router() will build token-indexed tiles for this call
 bool router_token_tiles(int B, int K, bool want);
 int launch_router(const LaunchCtx& ctx, const RouterLaunch& r);
