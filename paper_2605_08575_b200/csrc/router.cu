@@ -423,29 +423,28 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
                         ((reinterpret_cast<uintptr_t>(a.router) & 15) == 0);
     const int n_e = min(kRfEB, a.E - e0), n_t = min(kRfTB, a.B - t0);  // valid rows
     if (warp == 1) {
-      // ---- producer: one elected lane feeds the ring with 1-D bulk copies (TMA engine); the
-      // chain warp never spends an issue slot on staging ----
+      // ---- producer: the ring is fed with 1-D bulk copies (TMA engine), one row per lane -- a
+      // copy costs its issuing thread ~40 ns + bytes / 30 GB/s, so twelve 2 KB rows issued by one
+      // lane (1.3 us per sub-chunk) starved the chains (1.05 us per sub-chunk); the chain warp
+      // never spends an issue slot on staging ----
       if (vec_ok) {
-        if (lane == 0) {
-          const float* wsrc = a.router + static_cast<size_t>(e0) * D;
-          const float* xsrc = a.x + static_cast<size_t>(t0) * D;
+        // ring row of this lane: lanes [0, n_e) a router row, lanes [kRfEB, kRfEB + n_t) a token
+        const bool w_lane = lane < n_e, x_lane = lane >= kRfEB && lane - kRfEB < n_t;
+        const float* src = w_lane ? a.router + static_cast<size_t>(e0 + lane) * D
+                                  : a.x + static_cast<size_t>(t0 + (x_lane ? lane - kRfEB : 0)) * D;
 #pragma unroll 1
-          for (int sc = 0; sc < nsub; ++sc) {
-            const int slot = sc % nst;
+        for (int sc = 0; sc < nsub; ++sc) {
+          const int slot = sc % nst;
+          const int d0 = sc * kRfSub;
+          const uint32_t bytes = static_cast<uint32_t>(min(kRfSub, D - d0)) * 4u;
+          if (lane == 0) {
             mbar_wait(empty_bar(slot), ((sc / nst) & 1u) ^ 1u);
-            const int d0 = sc * kRfSub;
-            const uint32_t bytes = static_cast<uint32_t>(min(kRfSub, D - d0)) * 4u;
             mbar_arrive_expect_tx(full_bar(slot), bytes * static_cast<uint32_t>(n_e + n_t));
-            const uint32_t dst = smem_u32(rf_smem + slot * kRfRows * kRfRow);
-#pragma unroll 1
-            for (int r = 0; r < n_e; ++r)
-              bulk_copy_g2s(dst + r * kRfRow * 4, wsrc + static_cast<size_t>(r) * D + d0, bytes,
-                            full_bar(slot));
-#pragma unroll 1
-            for (int r = 0; r < n_t; ++r)
-              bulk_copy_g2s(dst + (kRfEB + r) * kRfRow * 4, xsrc + static_cast<size_t>(r) * D + d0,
-                            bytes, full_bar(slot));
           }
+          __syncwarp();
+          const uint32_t dst = smem_u32(rf_smem + slot * kRfRows * kRfRow);
+          if (w_lane || x_lane)
+            bulk_copy_g2s(dst + lane * kRfRow * 4, src + d0, bytes, full_bar(slot));
         }
       } else {
         // unaligned / odd d_model: plain loads by the whole producer warp, handed over with two

@@ -149,14 +149,38 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
 // NPL == kext, 0 < n_off < n, no shared rows of another length), outputs = masked bf16 terms only.
 // Every bounds check, mode branch and optional output folds away (the generic instantiation
 // issues ~2200 warp instructions per row, most of them predicated off).
+#ifdef SKB_DEBUG_TIMING
+// per-warp phase stamps of the lean batch selection (tools/dbg_tc.py): [row][8]
+__device__ long long g_sel_dbg[4096 * 8];
+#define SEL_STAMP(i)                                                              \
+  do {                                                                            \
+    if (LEAN && lane == 0 && row < 4096) {                                        \
+      if ((i) == 0) {                                                             \
+        long long t_;                                                             \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+        g_sel_dbg[row * 8] = t_;                                                  \
+        g_sel_dbg[row * 8 + 7] = clock64();                                       \
+      } else {                                                                    \
+        g_sel_dbg[row * 8 + (i)] = clock64();                                     \
+      }                                                                           \
+    }                                                                             \
+  } while (0)
+extern "C" void skb_debug_sel(long long* out) { cudaMemcpyFromSymbol(out, g_sel_dbg, sizeof(g_sel_dbg)); }
+#else
+#define SEL_STAMP(i) do { } while (0)
+#endif
+
 template <int NPL, bool LEAN>
 __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(SelectArgs a) {
   __shared__ uint32_t pick_scratch[kSelWarps][36];
+  __shared__ __align__(16) int pick_hist[LEAN ? kSelWarps : 1][256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x * kSelWarps + warp;
+  SEL_STAMP(0);
   pdl_wait();
   pdl_launch_dependents();
   if (row >= a.rows) return;
+  SEL_STAMP(1);
   const bool routed = LEAN || row < a.BK;
   const int n = LEAN ? 32 * NPL : (routed ? a.N : a.S);
   const int slot = LEAN ? 0 : (routed ? (a.perm ? a.perm[row] : row) : row - a.BK);
@@ -228,7 +252,10 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
 #pragma unroll
     for (int j = 0; j < NPL; ++j)
       kr[j] = (LEAN || i0 + j < n) ? (__float_as_uint(hv[j]) & 0x7fffffffu) : 0xffffffffu;
-    const RowPick pk = warp_binary_pick<NPL>(kr, n, n_off, pick_scratch[warp]);
+    SEL_STAMP(2);
+    const RowPick pk = LEAN ? warp_hist_pick<NPL>(kr, n_off, pick_hist[LEAN ? warp : 0], pick_scratch[warp])
+                            : warp_binary_pick<NPL>(kr, n, n_off, pick_scratch[warp]);
+    SEL_STAMP(3);
     int my_ties = 0;
 #pragma unroll
     for (int j = 0; j < NPL; ++j) my_ties += (kr[j] == pk.pivot) ? 1 : 0;
@@ -293,6 +320,21 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_warp_kernel(Select
     const int total = __reduce_add_sync(0xffffffffu, my_kept);
     if (lane == 0) a.kept_cnt[row] = total;
   }
+  SEL_STAMP(4);
+}
+
+static bool select_is_lean(const SelectArgs& a) {
+  const int nmax = a.N > a.S ? a.N : a.S;
+  const int kmax = a.hb ? (a.kext_routed > a.kext_shared ? a.kext_routed : a.kext_shared) : nmax;
+  const int span = nmax > kmax ? nmax : kmax;
+  if (!(span <= 1024 && a.rows >= 64)) return false;
+  const int n = a.N;
+  const bool uniform_rows = a.rows == a.BK || (a.S == a.N && a.n_off_shared == a.n_off_routed &&
+                                               a.kext_shared == a.kext_routed);
+  return a.mode == kSelectTopk && a.counts == nullptr && a.slot_counts == nullptr &&
+         a.mask_out_routed == nullptr && a.mask_out_shared == nullptr && a.kept_idx == nullptr &&
+         a.hb != nullptr && uniform_rows && a.kext_routed == n && (a.Nh & 7) == 0 &&
+         a.n_off_routed > 0 && a.n_off_routed < n && (n == 256 || n == 512 || n == 1024);
 }
 
 int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
@@ -313,14 +355,7 @@ int launch_select(const LaunchCtx& ctx, const SelectArgs& a) {
     cfg.gridDim = dim3(ceil_div(a.rows, kSelWarps));
     // the batch hot case gets the instantiation with everything else compiled out
     const int n = a.N;
-    const bool uniform_rows = a.rows == a.BK || (a.S == a.N && a.n_off_shared == a.n_off_routed &&
-                                                 a.kext_shared == a.kext_routed);
-    const bool lean = a.mode == kSelectTopk && a.counts == nullptr && a.slot_counts == nullptr &&
-                      a.mask_out_routed == nullptr && a.mask_out_shared == nullptr &&
-                      a.kept_idx == nullptr && a.hb != nullptr && uniform_rows &&
-                      a.kext_routed == n && (a.Nh & 7) == 0 && a.n_off_routed > 0 &&
-                      a.n_off_routed < n && (n == 256 || n == 512 || n == 1024);
-    if (lean) {
+    if (select_is_lean(a)) {
       if (n == 256) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<8, true>, a);
       else if (n == 512) cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<16, true>, a);
       else cudaLaunchKernelEx(&cfg, select_rows_warp_kernel<32, true>, a);

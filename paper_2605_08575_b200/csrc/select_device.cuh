@@ -296,6 +296,129 @@ __device__ __forceinline__ RowPick warp_binary_pick(const uint32_t (&kr)[NPL], i
   return pk;
 }
 
+// The same pick by radix histograms (the batch hot path: rows without fillers, keys in registers).
+// warp_binary_pick narrows the pivot's interval one bit -- one warp reduce -- at a time: ~30
+// dependent steps, measured 3.3 us per 512-neuron row (median, up to 6) with 14 rows per SM in
+// flight.  Here a pass drops the keys of the current interval into 256 equal-width bins of the
+// warp's own shared-memory histogram (8 bits of the key per pass), a warp scan of the bin counts
+// finds the bin that holds the n_off-th smallest key, and as soon as that bin holds at most 32
+// keys they are ranked against each other directly (one key per lane, 32 shuffles).  Typically
+// two passes + the ranking: ~10 dependent phases.  Every lane returns the same RowPick, bit for
+// bit the one warp_binary_pick returns.
+//   hist: 256 ints, scratch: 33 words, both private to the warp.
+template <int NPL>
+__device__ __forceinline__ RowPick warp_hist_pick(const uint32_t (&kr)[NPL], int n_off, int* hist,
+                                                  uint32_t* scratch) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    mn = min(mn, kr[j]);
+    mx = max(mx, kr[j]);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  RowPick pk;
+  if (mn == mx) {  // one value: the lowest n_off indices go
+    pk.pivot = mn;
+    pk.ties_to_drop = n_off;
+    pk.drop_all_ties = false;
+    return pk;
+  }
+  int b = 31 - __clz(mn ^ mx);           // the interval is [p, p + 2^(b+1))
+  uint32_t p = mn & ~((2u << b) - 1u);   // (b == 31: 2u << 31 wraps to 0, the mask to 0: p = 0)
+  int below = 0;                         // keys < p
+  int r = n_off;                         // 1-based rank of the pivot among the keys >= p
+  int m_in = 0;                          // keys inside the final interval
+  while (true) {
+    const int shift = b + 1 > 8 ? b + 1 - 8 : 0;  // bin width 2^shift, at most 256 bins
+    const uint32_t span = (2u << b) - 1u;         // interval width - 1
+    __syncwarp();
+    *reinterpret_cast<int4*>(hist + 8 * lane) = make_int4(0, 0, 0, 0);
+    *reinterpret_cast<int4*>(hist + 8 * lane + 4) = make_int4(0, 0, 0, 0);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const uint32_t d = kr[j] - p;
+      if (d <= span) atomicAdd(&hist[d >> shift], 1);
+    }
+    __syncwarp();
+    const int4 h0 = *reinterpret_cast<const int4*>(hist + 8 * lane);
+    const int4 h1 = *reinterpret_cast<const int4*>(hist + 8 * lane + 4);
+    const int hq[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    const int tot = ((hq[0] + hq[1]) + (hq[2] + hq[3])) + ((hq[4] + hq[5]) + (hq[6] + hq[7]));
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - tot;
+    // exactly one lane's eight bins hold rank r
+    int bin = 0, under = 0, m = 0;
+    if (excl < r && r <= incl) {
+      int run = excl;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (run < r && r <= run + hq[q]) {
+          bin = 8 * lane + q;
+          under = run;
+          m = hq[q];
+        }
+        run += hq[q];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, excl < r && r <= incl)) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    under = __shfl_sync(0xffffffffu, under, src);
+    m = __shfl_sync(0xffffffffu, m, src);
+    below += under;
+    r -= under;
+    p += static_cast<uint32_t>(bin) << shift;
+    if (shift == 0) {  // the bin is one key value
+      pk.pivot = p;
+      pk.ties_to_drop = n_off - below;
+      pk.drop_all_ties = (pk.ties_to_drop == m);
+      return pk;
+    }
+    b = shift - 1;
+    m_in = m;
+    if (m <= 32) break;
+  }
+  // at most 32 keys left in [p, p + 2^(b+1)): one per lane, ranked against each other
+  const uint32_t span = (2u << b) - 1u;
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) cnt += (kr[j] - p <= span) ? 1 : 0;
+  int pos = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, pos, o);
+    if (lane >= o) pos += t;
+  }
+  pos -= cnt;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < NPL; ++j)
+    if (kr[j] - p <= span) scratch[pos++] = kr[j];
+  __syncwarp();
+  const uint32_t mine = lane < m_in ? scratch[lane] : 0xffffffffu;
+  int lt = 0, le = 0;
+  for (int i = 0; i < m_in; ++i) {
+    const uint32_t v = __shfl_sync(0xffffffffu, mine, i);
+    lt += (v < mine) ? 1 : 0;
+    le += (v <= mine) ? 1 : 0;
+  }
+  const bool hit = lane < m_in && lt < r && r <= le;
+  const int src = __ffs(__ballot_sync(0xffffffffu, hit)) - 1;
+  pk.pivot = __shfl_sync(0xffffffffu, mine, src);
+  below += __shfl_sync(0xffffffffu, lt, src);
+  const int ties = __shfl_sync(0xffffffffu, le - lt, src);
+  pk.ties_to_drop = n_off - below;
+  pk.drop_all_ties = (pk.ties_to_drop == ties);
+  return pk;
+}
+
 // exclusive prefix sum over the lanes of a warp
 __device__ __forceinline__ int warp_excl_scan(int v) {
   const int lane = threadIdx.x & 31;

@@ -46,3 +46,15 @@ for it in range(3):
             if col.size:
                 print(f'  {names[k]:18s} n {col.size:4d} min {col.min():8.0f} med {np.median(col):8.0f} '
                       f'p90 {np.percentile(col, 90):8.0f} max {col.max():8.0f} ns')
+    if hasattr(L, 'skb_debug_sel') and base is not None:
+        so = np.zeros(4096 * 8, dtype=np.int64)
+        L.skb_debug_sel.argtypes = [C.c_void_p]
+        L.skb_debug_sel(so.ctypes.data_as(C.c_void_p))
+        m = so.reshape(4096, 8).astype(np.float64)
+        m = m[m[:, 0] > 0]
+        gt0, clk0 = m[:, 0].copy(), m[:, 7].copy()
+        print(f'--- selection: {m.shape[0]} rows')
+        for k, nm in ((0, 'start'), (1, 'tile ready'), (2, 'row loaded'), (3, 'pivot found'), (4, 'stored')):
+            col = gt0 - base if k == 0 else gt0 + (m[:, k] - clk0) / 1.965 - base
+            print(f'  {nm:18s} n {col.size:4d} min {col.min():8.0f} med {np.median(col):8.0f} '
+                  f'p90 {np.percentile(col, 90):8.0f} max {col.max():8.0f} ns')
