@@ -182,14 +182,30 @@ struct RouteDispatchArgs {
   float* weights;
   DispatchBuffers d;
   __nv_bfloat16* xs;
-  unsigned* bar;  // {arrivals, generation}
+  unsigned* bar;  // grid-barrier word: arrivals | generation << 16
 };
 
+__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+  uint2 o;
+  o.x = *reinterpret_cast<uint32_t*>(&lo);
+  o.y = *reinterpret_cast<uint32_t*>(&hi);
+  return o;
+}
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+#ifdef SKB_DEBUG_TIMING
+__device__ long long g_rd_dbg[16];
+#define RD_T(i) do { if (blockIdx.x == gridDim.x / 2 && threadIdx.x == 0) g_rd_dbg[i] = clock64(); } while (0)
+extern "C" void skb_debug_rd(long long* out) { cudaMemcpyFromSymbol(out, g_rd_dbg, sizeof(g_rd_dbg)); }
+#else
+#define RD_T(i) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a) {
   extern __shared__ __align__(16) float rd_smem[];
@@ -205,30 +221,47 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   const int t = blockIdx.x * 4 + warp;
   for (int i = tid; i < 2 * E; i += 128) tot[i] = 0;
 
+  RD_T(0);
+  // the token row is an input of the layer, not of the previous kernel: loaded and converted
+  // before the programmatic-launch wait (first 1024 columns; longer rows stream later)
+  const bool vec_row = (a.D % 4) == 0;
+  const int nq = a.D / 4;
+  uint2 o0[8];
+  if (t < a.B && vec_row) {
+    const float4* s4 = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(t) * a.D);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = u * 32 + lane;
+      if (q < nq) o0[u] = pack_bf16x4(__ldg(s4 + q));
+    }
+  }
   pdl_wait();
   pdl_launch_dependents();
+  RD_T(1);
   if (t < a.B)
     warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, rt,
                      a.ids + static_cast<size_t>(t) * K, a.weights + static_cast<size_t>(t) * K);
 
   // ---- grid barrier ----
+  RD_T(2);
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    const unsigned gen = ld_acquire_gpu_u32(a.bar + 1);
+    // one word: arrivals in the low 16 bits, generation above.  The last arriver's single add
+    // clears the arrivals and bumps the generation; everybody else learnt the generation from
+    // its own arrival and spins until it changes.  At rest the low bits are 0 again.
     const unsigned old = atomicAdd(a.bar, 1u);
-    if (old == gridDim.x - 1) {
-      atomicExch(a.bar, 0u);
-      __threadfence();
-      atomicAdd(a.bar + 1, 1u);
+    if ((old & 0xffffu) == gridDim.x - 1) {
+      atomicAdd(a.bar, 0x10000u - gridDim.x);
     } else {
-      while (ld_acquire_gpu_u32(a.bar + 1) == gen) {
+      while ((ld_acquire_gpu_u32(a.bar) >> 16) == (old >> 16)) {
       }
     }
   }
   __syncthreads();
 
   // ---- histograms over all slots ----
+  RD_T(3);
   const int s0 = blockIdx.x * 4 * K;  // first flat slot of this CTA
   for (int i = tid; i < BK; i += 128) {
     const int e = __ldcg(a.ids + i);
@@ -236,6 +269,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
     if (i < s0) atomicAdd(&bef[e], 1);
   }
   __syncthreads();
+  RD_T(4);
   if (warp == 0) {
     int run = 0, trun = 0;
     for (int e0 = 0; e0 < E; e0 += 32) {
@@ -285,6 +319,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
     }
   }
   __syncthreads();
+  RD_T(5);
 
   if (blockIdx.x == 0) {
     for (int e = tid; e <= E; e += 128) a.d.expert_off[e] = off[e];
@@ -313,25 +348,20 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   }
 
   // ---- token permutation: the token's bf16 row, K (+1) copies ----
+  RD_T(6);
   if (t < a.B) {
     if (a.has_shared && lane == 0) a.d.row_expert[BK + t] = E;
     const float* src = a.x + static_cast<size_t>(t) * a.D;
     const int copies = K + (a.has_shared ? 1 : 0);
-    if ((a.D % 4) == 0) {
+    if (vec_row) {
       const float4* s4 = reinterpret_cast<const float4*>(src);
-      const int nq = a.D / 4;
       for (int q0 = 0; q0 < nq; q0 += 256) {
         uint2 o[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int q = q0 + u * 32 + lane;
-          if (q < nq) {
-            const float4 v = __ldg(s4 + q);
-            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
-            o[u].x = *reinterpret_cast<uint32_t*>(&lo);
-            o[u].y = *reinterpret_cast<uint32_t*>(&hi);
-          }
+          if (q0 == 0) o[u] = o0[u];
+          else if (q < nq) o[u] = pack_bf16x4(__ldg(s4 + q));
         }
         for (int k = 0; k < copies; ++k) {
           const int row = k < K ? pos_s[warp * K + k] : BK + t;
@@ -351,6 +381,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
       }
     }
   }
+  RD_T(7);
 }
 
 struct RouterFusedArgs {

@@ -296,7 +296,7 @@ __device__ __forceinline__ RowPick warp_binary_pick(const uint32_t (&kr)[NPL], i
   return pk;
 }
 
-// The same pick by radix histograms (the batch hot path: rows without fillers, keys in registers).
+// The same pick by radix histograms (the batch path: keys in registers).
 // warp_binary_pick narrows the pivot's interval one bit -- one warp reduce -- at a time: ~30
 // dependent steps, measured 3.3 us per 512-neuron row (median, up to 6) with 14 rows per SM in
 // flight.  Here a pass drops the keys of the current interval into 256 equal-width bins of the
@@ -310,14 +310,17 @@ template <int NPL>
 __device__ __forceinline__ RowPick warp_hist_pick(const uint32_t (&kr)[NPL], int n_off, int* hist,
                                                   uint32_t* scratch) {
   const int lane = threadIdx.x & 31;
-  uint32_t mn = 0xffffffffu, mx = 0u;
+  // slots past the end of a row hold 0xffffffff: as signed values they never win the maximum,
+  // and key - p exceeds every interval width below, so no later phase sees them
+  uint32_t mn = 0xffffffffu;
+  int mxs = -1;
 #pragma unroll
   for (int j = 0; j < NPL; ++j) {
     mn = min(mn, kr[j]);
-    mx = max(mx, kr[j]);
+    mxs = max(mxs, static_cast<int>(kr[j]));
   }
   mn = __reduce_min_sync(0xffffffffu, mn);
-  mx = __reduce_max_sync(0xffffffffu, mx);
+  const uint32_t mx = static_cast<uint32_t>(__reduce_max_sync(0xffffffffu, mxs));
   RowPick pk;
   if (mn == mx) {  // one value: the lowest n_off indices go
     pk.pivot = mn;

@@ -58,3 +58,10 @@ for it in range(3):
             col = gt0 - base if k == 0 else gt0 + (m[:, k] - clk0) / 1.965 - base
             print(f'  {nm:18s} n {col.size:4d} min {col.min():8.0f} med {np.median(col):8.0f} '
                   f'p90 {np.percentile(col, 90):8.0f} max {col.max():8.0f} ns')
+    if hasattr(L, 'skb_debug_rd'):
+        ro = np.zeros(16, dtype=np.int64)
+        L.skb_debug_rd.argtypes = [C.c_void_p]
+        L.skb_debug_rd(ro.ctypes.data_as(C.c_void_p))
+        nm = ['start', 'pdl passed', 'routed', 'barrier passed', 'histograms', 'slots placed', 'tile list', 'permuted']
+        print('--- route_dispatch (middle CTA, ns from its start): ' +
+              ', '.join(f'{nm[k]} {(ro[k] - ro[0]) / 1.965:.0f}' for k in range(1, 8)))

@@ -1,5 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-bash tools/run_pf.sh 2>&1
-python bench.py --no-sweep --no-cpu --workload olmoe --batch 16 2>/dev/null | python -c "
-import sys, json
-d = json.loads(sys.stdin.readline()); print('olmoe B=16', d['ms_per_step'], d['roofline']['stage_ms'])"
+# timeline of the staged batch path (phase stamps compiled in with SKB_DEBUG_TIMING)
+SKB_DEBUG_TIMING=1 python paper_2605_08575_b200/build.py --force 2>&1 | grep -i " error"
+timeout 300 python tools/dbg_tc.py granite 256 | tail -25
+python paper_2605_08575_b200/build.py --force 2>&1 | grep -i " error"
