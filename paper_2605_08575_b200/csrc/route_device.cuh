@@ -85,11 +85,26 @@ __device__ __forceinline__ void warp_route_token_small(const float* __restrict__
 // ascending float sum for the denominator, IEEE division, then K rounds of warp arg-max under
 // the reference's total order (probability descending, expert id ascending on ties).
 // `sc` is round_up(E, 4) + K floats of shared scratch private to the warp.
+__device__ inline void warp_route_token_any(const float* __restrict__ row, int E, int K, int renorm,
+                                            float* sc, int32_t* out_ids, float* out_w);
 __device__ inline void warp_route_token(const float* __restrict__ row, int E, int K, int renorm,
                                  float* sc, int32_t* out_ids, float* out_w) {
   if (E <= 32) return warp_route_token_small<1>(row, E, K, renorm, sc, out_ids, out_w);
   if (E <= 64) return warp_route_token_small<2>(row, E, K, renorm, sc, out_ids, out_w);
   if (E <= 128) return warp_route_token_small<4>(row, E, K, renorm, sc, out_ids, out_w);
+  warp_route_token_any(row, E, K, renorm, sc, out_ids, out_w);
+}
+// One variant only (kernels that are instantiated per expert-count class keep their code short:
+// code that runs once per CTA costs its instruction fetch).  V = 1, 2, 4: E <= 32 * V; 0: any E.
+template <int V>
+__device__ __forceinline__ void warp_route_token_v(const float* __restrict__ row, int E, int K,
+                                                   int renorm, float* sc, int32_t* out_ids,
+                                                   float* out_w) {
+  if (V == 0) warp_route_token_any(row, E, K, renorm, sc, out_ids, out_w);
+  else warp_route_token_small<(V == 0 ? 1 : V)>(row, E, K, renorm, sc, out_ids, out_w);
+}
+__device__ inline void warp_route_token_any(const float* __restrict__ row, int E, int K, int renorm,
+                                            float* sc, int32_t* out_ids, float* out_w) {
   const int lane = threadIdx.x & 31;
   float mx = -INFINITY;
   for (int e = lane; e < E; e += 32) {

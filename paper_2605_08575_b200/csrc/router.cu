@@ -207,19 +207,27 @@ extern "C" void skb_debug_rd(long long* out) { cudaMemcpyFromSymbol(out, g_rd_db
 #define RD_T(i) do { } while (0)
 #endif
 
-__global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a) {
+// 4 token warps + 4 helper warps (16 warps: the kernel itself 0.4 us shorter, the step 2 us
+// longer -- the big CTAs keep the next kernel's CTAs from becoming resident beside them)
+constexpr int kRdThreads = 256;
+constexpr int kRdGroups = kRdThreads / 128;
+template <int RV>  // route() variant: warp_route_token_v
+__global__ void __launch_bounds__(kRdThreads) route_dispatch_kernel(RouteDispatchArgs a) {
   extern __shared__ __align__(16) float rd_smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int E = a.E, K = a.K, BK = a.B * a.K;
   const int rt_words = round_up(E, 4) + round_up(K, 4);
-  float* rt = rd_smem + static_cast<size_t>(warp) * rt_words;
+  float* rt = rd_smem + static_cast<size_t>(warp & 3) * rt_words;
   int32_t* tot = reinterpret_cast<int32_t*>(rd_smem + 4 * static_cast<size_t>(rt_words));  // [E]
   int32_t* bef = tot + E;           // [E] slots before this CTA's first slot, per expert
   int32_t* off = bef + E;           // [E + 1]
   int32_t* tile_off = off + E + 1;  // [E + 1]
   int32_t* pos_s = tile_off + E + 1;  // [4 * K] rows of this CTA's slots
-  const int t = blockIdx.x * 4 + warp;
-  for (int i = tid; i < 2 * E; i += 128) tot[i] = 0;
+  // warps 0-3 own the CTA's four tokens; the other warps help with the histograms and write
+  // their share of each token's copies
+  const int tw = warp & 3, half = warp >> 2;
+  const int t = blockIdx.x * 4 + tw;
+  for (int i = tid; i < 2 * E; i += kRdThreads) tot[i] = 0;
 
   RD_T(0);
   // the token row is an input of the layer, not of the previous kernel: loaded and converted
@@ -238,9 +246,9 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   pdl_wait();
   pdl_launch_dependents();
   RD_T(1);
-  if (t < a.B)
-    warp_route_token(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, rt,
-                     a.ids + static_cast<size_t>(t) * K, a.weights + static_cast<size_t>(t) * K);
+  if (t < a.B && half == 0)
+    warp_route_token_v<RV>(a.logits + static_cast<size_t>(t) * E, E, K, a.renorm, rt,
+                           a.ids + static_cast<size_t>(t) * K, a.weights + static_cast<size_t>(t) * K);
 
   // ---- grid barrier ----
   RD_T(2);
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   // ---- histograms over all slots ----
   RD_T(3);
   const int s0 = blockIdx.x * 4 * K;  // first flat slot of this CTA
-  for (int i = tid; i < BK; i += 128) {
+  for (int i = tid; i < BK; i += kRdThreads) {
     const int e = __ldcg(a.ids + i);
     atomicAdd(&tot[e], 1);
     if (i < s0) atomicAdd(&bef[e], 1);
@@ -322,9 +330,9 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   RD_T(5);
 
   if (blockIdx.x == 0) {
-    for (int e = tid; e <= E; e += 128) a.d.expert_off[e] = off[e];
+    for (int e = tid; e <= E; e += kRdThreads) a.d.expert_off[e] = off[e];
     // tile list: expert-major, tile_tokens rows per tile, then the shared expert's tiles
-    for (int e = tid; e < E; e += 128) {
+    for (int e = tid; e < E; e += kRdThreads) {
       const int c = tot[e];
       const int nt = ceil_div(c, a.tile_tokens);
       for (int j = 0; j < nt; ++j) {
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
     int n_tiles = tile_off[E];
     if (a.has_shared) {
       const int nsh = ceil_div(a.B, a.tile_tokens);
-      for (int j = tid; j < nsh; j += 128) {
+      for (int j = tid; j < nsh; j += kRdThreads) {
         a.d.tile_expert[n_tiles + j] = E;
         a.d.tile_row0[n_tiles + j] = BK + j * a.tile_tokens;
         a.d.tile_nrows[n_tiles + j] = min(a.tile_tokens, a.B - j * a.tile_tokens);
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
   // ---- token permutation: the token's bf16 row, K (+1) copies ----
   RD_T(6);
   if (t < a.B) {
-    if (a.has_shared && lane == 0) a.d.row_expert[BK + t] = E;
+    if (a.has_shared && lane == 0 && half == 0) a.d.row_expert[BK + t] = E;
     const float* src = a.x + static_cast<size_t>(t) * a.D;
     const int copies = K + (a.has_shared ? 1 : 0);
     if (vec_row) {
@@ -363,8 +371,8 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
           if (q0 == 0) o[u] = o0[u];
           else if (q < nq) o[u] = pack_bf16x4(__ldg(s4 + q));
         }
-        for (int k = 0; k < copies; ++k) {
-          const int row = k < K ? pos_s[warp * K + k] : BK + t;
+        for (int k = half; k < copies; k += kRdGroups) {
+          const int row = k < K ? pos_s[tw * K + k] : BK + t;
           uint2* d2 = reinterpret_cast<uint2*>(a.xs + static_cast<size_t>(row) * a.Dp);
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -374,8 +382,8 @@ __global__ void __launch_bounds__(128) route_dispatch_kernel(RouteDispatchArgs a
         }
       }
     } else {
-      for (int k = 0; k < copies; ++k) {
-        const int row = k < K ? pos_s[warp * K + k] : BK + t;
+      for (int k = half; k < copies; k += kRdGroups) {
+        const int row = k < K ? pos_s[tw * K + k] : BK + t;
         __nv_bfloat16* dst = a.xs + static_cast<size_t>(row) * a.Dp;
         for (int dd = lane; dd < a.D; dd += 32) dst[dd] = __float2bfloat16_rn(src[dd]);
       }
@@ -642,7 +650,7 @@ static size_t route_dispatch_smem(int E, int K) {
 }
 
 // One launch for route + dispatch + permutation: the grid barrier inside needs every CTA resident
-// (4 tokens per CTA, 128 threads, a few KB of shared memory: 8+ CTAs per SM), and every CTA reads
+// (4 tokens per CTA, 256 threads, a few KB of shared memory: 8 CTAs per SM), and every CTA reads
 // all B*K ids, which stops paying on large batches.
 bool router_fuses_permute(const RouterLaunch& r) {
   if (r.xs == nullptr || r.grid_bar == nullptr || r.dispatch == nullptr || r.x == nullptr) return false;
@@ -741,9 +749,12 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
     rd.xs = r.xs;
     rd.bar = r.grid_bar;
     cfg.gridDim = dim3(ceil_div(r.B, 4));
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(kRdThreads);
     cfg.dynamicSmemBytes = route_dispatch_smem(r.E, r.K);
-    cudaLaunchKernelEx(&cfg, route_dispatch_kernel, rd);
+    if (r.E <= 32) cudaLaunchKernelEx(&cfg, route_dispatch_kernel<1>, rd);
+    else if (r.E <= 64) cudaLaunchKernelEx(&cfg, route_dispatch_kernel<2>, rd);
+    else if (r.E <= 128) cudaLaunchKernelEx(&cfg, route_dispatch_kernel<4>, rd);
+    else cudaLaunchKernelEx(&cfg, route_dispatch_kernel<0>, rd);
     return launches + 1;
   }
   if (!a.fuse_route) {

@@ -65,3 +65,10 @@ for it in range(3):
         nm = ['start', 'pdl passed', 'routed', 'barrier passed', 'histograms', 'slots placed', 'tile list', 'permuted']
         print('--- route_dispatch (middle CTA, ns from its start): ' +
               ', '.join(f'{nm[k]} {(ro[k] - ro[0]) / 1.965:.0f}' for k in range(1, 8)))
+    if hasattr(L, 'skb_debug_rf'):
+        ro = np.zeros(16, dtype=np.int64)
+        L.skb_debug_rf.argtypes = [C.c_void_p]
+        L.skb_debug_rf(ro.ctypes.data_as(C.c_void_p))
+        print('--- router_fused (last CTA to write, ns from its start): ' +
+              f'pdl passed {(ro[1]-ro[0])/1.965:.0f}, first sub-chunk in {(ro[8]-ro[0])/1.965:.0f}, '
+              f'chains done {(ro[2]-ro[0])/1.965:.0f}, waited on the ring {ro[9]/1.965:.0f}')

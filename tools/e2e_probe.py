@@ -1,39 +1,40 @@
-"""Where the end-to-end step goes: Python mirror vs the bare C call, pinned buffers, L2 flushed."""
-import ctypes as C, sys, time, numpy as np, torch
+"""Where the end-to-end time of the host-buffer call goes (Granite shape, batch 256): the PCIe copies
+alone, the device stages alone, and the whole call."""
+import sys, time, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2605_08575_b200 as skb
-from paper_2605_08575_b200 import _lib
 E, K, D, N = 32, 8, 1024, 512
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 cfg = skb.MoEConfig(E, K, D, N, False, 0, True, 64)
 layer = skb.MoELayerWeights.generate_synthetic(cfg, 1, 0.05)
-flush = torch.empty(512 << 20, dtype=torch.uint8, device='cuda')
-L = _lib.load()
-for B in (1, 256):
-    x = torch.randn(B, D).pin_memory(); y = torch.empty(B, D).pin_memory()
-    lvl = skb.SparsityLevel(0.5)
-    a = _lib.SkbForwardArgs(); a.batch, a.mode = B, skb.MODE_TOPK; a.s_routed = 0.5
-    a.x, a.y = x.data_ptr(), y.data_ptr()
-    rep = _lib.SkbReport()
-    for name in ("python mirror", "bare C call", "bare C call, no flush"):
-        ts = []
-        for i in range(60):
-            if "no flush" not in name:
-                flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if name == "python mirror":
-                skb.forward_topk_sparse(layer, x.numpy(), lvl, None, y_out=y.numpy())
-            else:
-                L.skb_layer_forward(layer._h, C.byref(a), C.byref(rep))
-            t1 = time.perf_counter()
-            if i >= 10: ts.append((t1 - t0) * 1e6)
-        print(f'B={B:4d} {name:24s} {np.mean(ts):7.1f} us  (min {np.min(ts):6.1f})')
-    # the copies alone
-    d = torch.empty(B, D, device='cuda')
+layer.reserve(B)
+xh = torch.randn(B, D).pin_memory(); yh = torch.empty(B, D).pin_memory()
+xd = torch.empty(B, D, device='cuda'); yd = torch.empty(B, D, device='cuda')
+lvl = skb.SparsityLevel(0.5)
+st = torch.cuda.Stream()
+def timeit(fn, n=200, warm=20):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
     ts = []
-    for i in range(60):
-        torch.cuda.synchronize(); t0 = time.perf_counter()
-        d.copy_(x, non_blocking=True); y.copy_(d, non_blocking=True); torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        if i >= 10: ts.append((t1 - t0) * 1e6)
-    print(f'B={B:4d} H2D + D2H copies alone     {np.mean(ts):7.1f} us')
+    for _ in range(n):
+        t0 = time.perf_counter(); fn(); ts.append((time.perf_counter() - t0) * 1e6)
+    return float(np.median(ts)), float(np.mean(ts))
+def copies():
+    with torch.cuda.stream(st):
+        xd.copy_(xh, non_blocking=True); yh.copy_(yd, non_blocking=True)
+    st.synchronize()
+def h2d():
+    with torch.cuda.stream(st):
+        xd.copy_(xh, non_blocking=True)
+    st.synchronize()
+def dev():
+    layer.forward_device(xd.data_ptr(), yd.data_ptr(), B, stream=st.cuda_stream, mode=skb.MODE_TOPK, s_routed=0.5, s_shared=0.0)
+    st.synchronize()
+def whole():
+    skb.forward_topk_sparse(layer, xh.numpy(), lvl, None, y_out=yh.numpy())
+xn, yn = xh.numpy(), yh.numpy()
+def whole_np():
+    skb.forward_topk_sparse(layer, xn, lvl, None, y_out=yn)
+for name, fn in (('h2d 1 copy + sync', h2d), ('h2d + d2h + sync', copies), ('device stages + sync', dev), ('forward_topk_sparse (host buffers)', whole), ('... numpy views hoisted', whole_np)):
+    med, mean = timeit(fn)
+    print(f'{name:40s} median {med:7.1f} us  mean {mean:7.1f} us')
