@@ -694,7 +694,9 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                                  &L->tmap_x[1], tn, L->disp, max_tiles, g, L->d_h, token_tiles,
                                  sel_mode == kSelectThreshold ? L->d_sg : nullptr, pair_gateup,
                                  precise, /*early_tiles=*/!token_tiles && !permuted,
-                                 /*prefetch image=*/nullptr);
+                                 /*prefetch image=*/nullptr,
+                                 permuted ? reinterpret_cast<const int*>(L->d_counters + 3 + L->cap_batch)
+                                          : nullptr);
   tm.mark();
 
   // Gather path: the selection runs inside the down kernel; the stand-alone selection kernel

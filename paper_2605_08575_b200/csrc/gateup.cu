@@ -110,6 +110,7 @@ struct TcArgs {
   int kblocks_routed, kblocks_shared;  // 64-element K blocks
   int rows_per_expert;                 // A-image rows per routed expert
   int nsplit;                          // MODE 1: B operands accumulated per K block (1 or 3)
+  const int* tiles_flag;  // MODE 0: non-zero once the tile list is written (implies early_tiles)
   int early_tiles;  // the tile list was written at least two kernels upstream: readable -- and the
                     // weight stream startable -- before the programmatic-launch wait
 };
@@ -213,20 +214,31 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
   // requested -- and the rest of this CTA's weight blocks prefetched into the L2 -- BEFORE the
   // wait; only the token operand waits.  Hides the tile-list reads and the first HBM latency
   // (~2.5 us per GEMM) under the previous kernel's tail.
-  if (!a.early_tiles) {
+  // (When the kernel directly upstream writes the tile list -- route_dispatch_kernel -- it raises
+  // a flag as soon as the list is out, before it copies the tokens: the CTAs here poll that flag
+  // instead, and the early start survives.  router_fused_kernel lowers the flag again.)
+  if (a.tiles_flag != nullptr) {
+    if (threadIdx.x == 0) {
+      int seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(a.tiles_flag) : "memory");
+      } while (seen == 0);
+    }
+    __syncthreads();
+  } else if (!a.early_tiles) {
     pdl_wait();
     pdl_launch_dependents();
   }
   TC_STAMP(0, 1);
 
   const int tile = blockIdx.y;
-  bool active = tile < *a.n_tiles;
+  bool active = tile < __ldcg(a.n_tiles);
   int e = 0, row0 = 0, nrows = 0;
   bool shared_expert = false;
   if (active) {
-    e = a.tile_expert[tile];
-    row0 = a.tile_row0[tile];
-    nrows = a.tile_nrows[tile];
+    e = __ldcg(a.tile_expert + tile);
+    row0 = __ldcg(a.tile_row0 + tile);
+    nrows = __ldcg(a.tile_nrows + tile);
     shared_expert = e >= a.n_experts;
     active = static_cast<int>(blockIdx.x) * MB < (shared_expert ? a.mblocks_shared : a.mblocks_routed);
   }
@@ -708,9 +720,10 @@ static void launch_tc_case(const LaunchCtx& ctx, const CUtensorMap* ta, const CU
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      const CUtensorMap* tmap_x32, int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
                      float* h, bool token_tiles, float* sg, bool pair_blocks, bool precise,
-                     bool early_tiles, const void* w_image) {
+                     bool early_tiles, const void* w_image, const int* tiles_flag) {
   TcArgs a{};
-  a.early_tiles = early_tiles ? 1 : 0;
+  a.tiles_flag = tiles_flag;
+  a.early_tiles = (early_tiles || tiles_flag != nullptr) ? 1 : 0;
   a.a_base = a.a_shared_base = w_image;
   a.sg_out = sg;
   a.tile_colrow = token_tiles ? d.tile_colrow : nullptr;

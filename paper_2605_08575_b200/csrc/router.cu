@@ -353,6 +353,10 @@ __global__ void __launch_bounds__(kRdThreads) route_dispatch_kernel(RouteDispatc
       n_tiles += nsh;
     }
     if (tid == 0) *a.d.n_tiles = n_tiles;
+    // the gate/up CTAs, resident behind this kernel, may read the list from here on
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(a.bar + 1, 1u);
   }
 
   // ---- token permutation: the token's bf16 row, K (+1) copies ----
@@ -408,6 +412,7 @@ struct RouterFusedArgs {
   int32_t* ids;
   float* weights;
   unsigned* counters;  // [0] = finished token blocks, [1 + tb] = finished expert blocks of tb
+  unsigned* tiles_flag;  // see route_dispatch_kernel, or nullptr
   DispatchBuffers d;
 };
 
@@ -442,6 +447,9 @@ __global__ void __launch_bounds__(64) router_fused_kernel(RouterFusedArgs a) {
   pdl_wait();
   pdl_launch_dependents();
   RF_T(1);
+  // "tile list written" flag of this step's route_dispatch_kernel: down again (every reader of
+  // the previous step finished kernels ago)
+  if (a.tiles_flag != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.tiles_flag = 0u;
 
   if (a.xb != nullptr && static_cast<int>(blockIdx.x) == a.n_eb) {
     // conversion CTAs (token tiles): xb[t] = bf16(x[t]) for this token block, in parallel with
@@ -714,6 +722,7 @@ int launch_router(const LaunchCtx& ctx, const RouterLaunch& r) {
   a.ids = r.ids;
   a.weights = r.weights;
   a.counters = r.counters;
+  a.tiles_flag = router_fuses_permute(r) ? r.grid_bar + 1 : nullptr;
   if (r.dispatch) a.d = *r.dispatch;
   a.n_eb = a.logits_ready ? 1 : ceil_div(r.E, kRfEB);
   const bool token_tiles = a.fuse_dispatch && router_token_tiles(r.B, r.K, r.xb != nullptr);

@@ -86,7 +86,7 @@ struct RouterLaunch {
   // batches: route + dispatch + token permutation as one kernel (router.cu: route_dispatch_kernel)
   // when the expert-sorted token copy `xs` and the two grid-barrier words are given
   __nv_bfloat16* xs;
-  unsigned* grid_bar;
+  unsigned* grid_bar;  // [0] barrier word, [1] "tile list written" flag (polled by the gate/up CTAs)
 };
 // true when launch_router() will also write the expert-sorted token copy (no permute kernel)
 bool router_fuses_permute(const RouterLaunch& r);
@@ -103,7 +103,8 @@ int launch_plan_export(const LaunchCtx& ctx, const int32_t* perm, const int32_t*
 int launch_gateup_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_w, const CUtensorMap* tmap_x,
                      const CUtensorMap* tmap_x32 /*32-row boxes*/, int tile_tokens, const DispatchBuffers& d, int max_tiles, const Geometry& g,
                      float* h, bool token_tiles, float* sg = nullptr, bool pair_blocks = false,
-                     bool precise = false, bool early_tiles = false, const void* w_image = nullptr);
+                     bool precise = false, bool early_tiles = false, const void* w_image = nullptr,
+                     const int* tiles_flag = nullptr);
 int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    const CUtensorMap* tmap_hb32 /*[3], 32-row boxes*/, int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
