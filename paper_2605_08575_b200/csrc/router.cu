@@ -1197,17 +1197,19 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
   // The token's row indices and weights first (one round trip for all slots), then the slot
   // rows eight at a time with every load in flight before the first add: the kernel is two or
   // three memory round trips long instead of two per slot.
+  // (Rows and weights come from the router stage, kernels upstream of the down projection this
+  // kernel waits for: they are read BEFORE the programmatic-launch wait.)
   __shared__ int32_t rs[kMaxExperts + 1];
   __shared__ float ws[kMaxExperts + 1];
-  pdl_wait();
-  pdl_launch_dependents();
   const int t = blockIdx.y;
   const int R = K + has_shared;
   for (int s = threadIdx.x; s < R; s += blockDim.x) {
-    rs[s] = s < K ? inv[t * K + s] : B * K + t;
-    ws[s] = s < K ? weights[t * K + s] : 1.0f;
+    rs[s] = s < K ? __ldcg(inv + t * K + s) : B * K + t;
+    ws[s] = s < K ? __ldcg(weights + t * K + s) : 1.0f;
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
   const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (c4 >= D) return;
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
