@@ -11,7 +11,7 @@
 namespace skb {
 
 __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs a) {
-  extern __shared__ uint32_t keys[];  // [max(N,S)]
+  extern __shared__ __align__(16) uint32_t keys[];  // [max(N,S)]
   __shared__ SelScratch sc;
   __shared__ __align__(16) SelHistScratch hs;
 
@@ -64,13 +64,57 @@ __global__ void __launch_bounds__(kSelectThreads) select_rows_kernel(SelectArgs 
     if (n_off >= n) {
       drop_everything = true;  // activation.cpp:36-39
     } else {
-      for (int i = tid; i < n; i += kSelectThreads)
-        keys[i] = __float_as_uint(hrow[i]) & 0x7fffffffu;
+      if ((n & 3) == 0 && (a.Nh & 3) == 0) {
+        for (int i = 4 * tid; i < n; i += 4 * kSelectThreads) {
+          const uint4 q = *reinterpret_cast<const uint4*>(hrow + i);
+          *reinterpret_cast<uint4*>(keys + i) =
+              make_uint4(q.x & 0x7fffffffu, q.y & 0x7fffffffu, q.z & 0x7fffffffu, q.w & 0x7fffffffu);
+        }
+      } else {
+        for (int i = tid; i < n; i += kSelectThreads)
+          keys[i] = __float_as_uint(hrow[i]) & 0x7fffffffu;
+      }
       __syncthreads();
       const RowPick pk = sel_hist_pick(keys, n, n_off, hs, sc);
       pivot = pk.pivot;
       ties_to_drop = pk.ties_to_drop;
       drop_all_ties = pk.drop_all_ties;
+    }
+  }
+
+  // ---- fast path (prefill rows too long for the warp kernel: GPT-OSS shape, 2880 neurons x
+  // 16384 rows): no ties at the pivot to order, no lists, no mask export -- four neurons per
+  // thread, 128-bit reads of h and the keys, one 64-bit store per bf16 term ----
+  if (mode == kSelectTopk && !drop_everything && drop_all_ties && kidx == nullptr &&
+      a.kept_cnt == nullptr && mout == nullptr && hb != nullptr && (n & 3) == 0 && (a.Nh & 3) == 0) {
+    const int kext4 = routed ? a.kext_routed : a.kext_shared;
+    if ((kext4 & 3) == 0 && (a.hb_split_stride & 3) == 0) {
+      for (int i = 4 * tid; i < kext4; i += 4 * kSelectThreads) {
+        float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (i < n) {
+          const float4 hv4 = *reinterpret_cast<const float4*>(hrow + i);
+          const uint4 k4 = *reinterpret_cast<const uint4*>(keys + i);
+          v[0] = k4.x > pivot ? hv4.x : 0.0f;
+          v[1] = k4.y > pivot ? hv4.y : 0.0f;
+          v[2] = k4.z > pivot ? hv4.z : 0.0f;
+          v[3] = k4.w > pivot ? hv4.w : 0.0f;
+        }
+        for (int sp = 0; sp < a.nsplit; ++sp) {
+          uint32_t w[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const __nv_bfloat16 lo = __float2bfloat16_rn(v[2 * q]);
+            const __nv_bfloat16 hi = __float2bfloat16_rn(v[2 * q + 1]);
+            v[2 * q] = __fsub_rn(v[2 * q], __bfloat162float(lo));
+            v[2 * q + 1] = __fsub_rn(v[2 * q + 1], __bfloat162float(hi));
+            w[q] = static_cast<uint32_t>(__bfloat16_as_ushort(lo)) |
+                   (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16);
+          }
+          *reinterpret_cast<uint2*>(hb + static_cast<size_t>(sp) * a.hb_split_stride + i) =
+              make_uint2(w[0], w[1]);
+        }
+      }
+      return;
     }
   }
 
