@@ -665,7 +665,29 @@ bool router_fuses_permute(const RouterLaunch& r) {
   if (r.B <= fuse_route_max_batch()) return false;
   if (static_cast<long>(r.B) * r.K > 4096) return false;
   if (route_dispatch_smem(r.E, r.K) > 40 * 1024) return false;
-  return ceil_div(r.B, 4) <= 4 * 132;
+  // every CTA of the grid must be resident at once: asked of the runtime, per device and
+  // expert-count class, with the largest shared-memory request the limit above allows
+  static int resident[64][4] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int cls = r.E <= 32 ? 0 : (r.E <= 64 ? 1 : (r.E <= 128 ? 2 : 3));
+  int cap = __atomic_load_n(&resident[dev & 63][cls], __ATOMIC_ACQUIRE);
+  if (cap == 0) {
+    int per_sm = 0, sms = 0;
+    const size_t smem = 40 * 1024;
+    cudaError_t e = cudaSuccess;
+    switch (cls) {
+      case 0: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_dispatch_kernel<1>, kRdThreads, smem); break;
+      case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_dispatch_kernel<2>, kRdThreads, smem); break;
+      case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_dispatch_kernel<4>, kRdThreads, smem); break;
+      default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, route_dispatch_kernel<0>, kRdThreads, smem); break;
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (e == cudaSuccess && per_sm > 0 && sms > 0) ? per_sm * sms : -1;
+    __atomic_store_n(&resident[dev & 63][cls], cap, __ATOMIC_RELEASE);
+  }
+  // (half of it: the previous kernel's last CTAs and the next kernel's first share the SMs)
+  return cap > 0 && ceil_div(r.B, 4) <= cap / 2;
 }
 
 bool router_token_tiles(int B, int K, bool want) {
