@@ -198,6 +198,7 @@ SMALL_CASES = [
     (3, 3, 72, 65, 1, True, 2),
     (32, 8, 512, 256, 0, True, 64),
     (6, 1, 200, 320, 320, True, 33),
+    (5, 2, 70, 96, 0, True, 7),           # d_model not a multiple of 4: the scalar staging paths
 ]
 
 
