@@ -428,6 +428,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
     if (tid == 0) {
       tma_prefetch_desc(&tmap_w3);
       misc[1] = 0;
+      misc[4] = 0;  // consumer warps that are through with the ring (threshold mode reuses it)
     }
   }
   for (int e = tid; e < kDecMaxE; e += kDecThreads) cmask[e] = 0u;
@@ -666,6 +667,13 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
       else
         do_piece(u, qq >> 2, qq & 3, a.N, false);
       if (p == bid + ((n_sh + gwn - 1 - bid) / gwn) * gwn) DEC_STAMP(kWarpG0 * 32, 18);
+    }
+    // this warp has read its last ring stage: once all consumer warps say so, the D role may
+    // stage gathered rows in the ring (threshold mode, below)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      atomicAdd(&misc[4], 1);
     }
     DEC_STAMP(kWarpG0 * 32, 4);
   } else if (warp == kWarpChain) {
@@ -1254,8 +1262,21 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
           const int kinds = thr_unit ? 2 : 1;
           // one batch when the unit's rows fit; otherwise two half-buffers, the copies of batch
           // k + 1 in flight while batch k is consumed (cp.async groups complete in order)
-          const bool piped = m * kinds > a.gb_rows;
-          const int RBS = max(1, a.gb_rows / (kinds * (piped ? 2 : 1)));
+          // (threshold mode, once this CTA's gate stream is over -- every consumer warp through
+          // with the ring: the W_up rows of the unit go into the idle ring, the W_down rows into
+          // the gather buffer, and the whole unit is ONE batch, one round trip instead of ~four)
+          bool split = false;
+          if (thr_unit && m * kinds > a.gb_rows && m <= a.gb_rows &&
+              static_cast<size_t>(m) * LPR * 16 <= static_cast<size_t>(stages) * kStageBytes) {
+            if (dtid == 0) wc[16] = *reinterpret_cast<volatile int*>(&misc[4]) == kNumGWarps ? 1 : 0;
+            d_sync();
+            split = wc[16] != 0;
+            d_sync();
+          }
+          const bool piped = !split && m * kinds > a.gb_rows;
+          const int RBS = split ? m : max(1, a.gb_rows / (kinds * (piped ? 2 : 1)));
+          const uint32_t up_u32 = split ? sm_u32 + L.ring : 0u;   // W_up rows of the batch
+          const uint4* up_ptr = reinterpret_cast<const uint4*>(sm + L.ring);
           float* hval = reinterpret_cast<float*>(mlist);  // [RBS] silu(g) * u of the batch's rows
           if (thr_unit && dtid == 0) atomicAdd(&a.ctr[kCtrKept + row], static_cast<unsigned>(m));
           const int dr = kDThreads / LPR, dc = kDThreads % LPR;
@@ -1272,10 +1293,10 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
 #pragma unroll 1
               while (r < nr) {
                 const __nv_bfloat16* src = wsrc + static_cast<size_t>(lst[k0 + r]) * Dp + cc * 8;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 base + static_cast<uint32_t>((kind * RBS + r) * LPR + cc) * 16u),
-                             "l"(src)
-                             : "memory");
+                const uint32_t dst =
+                    (split && kind == 1) ? up_u32 + static_cast<uint32_t>(r * LPR + cc) * 16u
+                                         : base + static_cast<uint32_t>((kind * RBS + r) * LPR + cc) * 16u;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
                 cc += dc;
                 r += dr;
                 if (cc >= LPR) {
@@ -1309,7 +1330,7 @@ decode_fused_kernel(const __grid_constant__ CUtensorMap tmap_w3,
 #pragma unroll 2
                 for (int cc = lane; cc < LPR; cc += 32) {
                   float wf[8], xf[8];
-                  unpack8(gbh[(RBS + r) * LPR + cc], wf);
+                  unpack8(split ? up_ptr[r * LPR + cc] : gbh[(RBS + r) * LPR + cc], wf);
                   unpack8(*reinterpret_cast<const uint4*>(xt + cc * 8), xf);
 #pragma unroll
                   for (int i = 0; i < 8; ++i) sacc = fmaf(wf[i], xf[i], sacc);
