@@ -325,6 +325,17 @@ int skb_ep_ipc_close(void* peer_ptr);
 int skb_ep_push_back(const float* out_rows, int rows, int d_model, const int32_t* counts, int world,
                      int rank, float* const* peer_back, unsigned long long* const* peer_flag,
                      unsigned long long* expect, uint32_t* done_ctr, void* stream);
+/* The dispatch direction the same way (no first all-to-all either): the home rank packs its token
+ * rows straight into the owner ranks' receive buffers (peer-mapped, `skb_ep_row_stride` bytes per
+ * row) at the rows the owners' view of the plan expects, and bumps cumulative counters there
+ * (skb_ep_push_rows); the owner's unpack waits on its counters (skb_ep_unpack_symm; `expect` is
+ * the owner's own running total per source rank, advanced by the call). */
+int skb_ep_push_rows(const float* x, const int32_t* pos, const int32_t* local_ids, int slots, int top_k,
+                     int d_model, const int32_t* counts, int world, int rank, uint8_t* const* peer_recv,
+                     unsigned long long* const* peer_flag, uint32_t* done_ctr, void* stream);
+int skb_ep_unpack_symm(const uint8_t* recv, const unsigned long long* flag, unsigned long long* expect,
+                       const int32_t* counts, int world, int rank, int rows, int d_model, float* x,
+                       int32_t* ids, void* stream);
 int skb_ep_combine_symm(const float* back, const unsigned long long* flag,
                         const unsigned long long* expect, int world, const int32_t* pos,
                         const float* weights, const float* shared, int batch, int top_k, int d_model,

@@ -255,6 +255,94 @@ __global__ void __launch_bounds__(256) ep_combine_symm_kernel(
   if (shared != nullptr) acc = __fadd_rn(acc, shared[static_cast<size_t>(t) * D + d]);
   y[static_cast<size_t>(t) * D + d] = acc;
 }
+// ---------------------------------------------------------------------------------------------
+// Dispatch WITHOUT the first collective (dispatch direction): the home rank
+// packs a token row and writes it straight into the OWNER rank's receive buffer over the peer
+// mapping, at the row the owner's own view of the plan gives it -- rows of source rank s start at
+// sum_{s' < s} cnt[s'][owner], in s's send order -- and bumps a cumulative counter in the owner's
+// memory; the owner's unpack kernel waits on its counters instead of on an all-to-all.
+//
+// Safe with one receive buffer per rank: a peer pushes step n+1 only after the all-gather of the
+// step n+1 ids, a collective this rank's stream joins after its own step n unpack.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ep_push_rows_kernel(
+    const float* __restrict__ x, const int32_t* __restrict__ pos, const int32_t* __restrict__ loc,
+    int slots, int K, int D, int stride, const int32_t* __restrict__ cnt, int W, int rank,
+    uint8_t* const* __restrict__ peer_recv, unsigned long long* const* __restrict__ peer_flag,
+    unsigned* __restrict__ done_ctr) {
+  __shared__ int s_soff[kMaxWorld + 1], s_rbase[kMaxWorld];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int d = 0; d < W; ++d) {
+      s_soff[d] = o;  // this rank's send order: destination-major
+      o += cnt[rank * W + d];
+      int b = 0;
+      for (int sr = 0; sr < rank; ++sr) b += cnt[sr * W + d];
+      s_rbase[d] = b;  // where this rank's rows start in destination d's receive buffer
+    }
+    s_soff[W] = o;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i < slots) {
+    const int p = pos[i];
+    if (p >= 0) {
+      int d = 0;
+      while (d + 1 < W && p >= s_soff[d + 1]) ++d;
+      const float* src = x + static_cast<size_t>(i / K) * D;
+      uint8_t* row = peer_recv[d] + static_cast<size_t>(s_rbase[d] + p - s_soff[d]) * stride;
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(row);
+      for (int c = lane; c < D; c += 32) dst[c] = __float2bfloat16_rn(__ldg(src + c));
+      if (lane == 0) *reinterpret_cast<int32_t*>(row + static_cast<size_t>(D) * 2) = loc[i];
+    }
+  }
+  // the last CTA through publishes: every row of this launch is in place before any counter moves
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    if (threadIdx.x == 0) *done_ctr = 0u;
+    __threadfence_system();
+    if (static_cast<int>(threadIdx.x) < W) {
+      const int d = threadIdx.x;
+      const unsigned long long n = static_cast<unsigned long long>(cnt[rank * W + d]);
+      if (n) atomicAdd_system(peer_flag[d] + rank, n);
+    }
+  }
+}
+
+// expected cumulative rows per SOURCE rank at this owner rank: expect[s] += cnt[s][rank]
+__global__ void ep_expect_in_kernel(const int32_t* __restrict__ cnt, int W, int rank,
+                                    unsigned long long* __restrict__ expect) {
+  const int s = threadIdx.x;
+  if (s < W) expect[s] += static_cast<unsigned long long>(cnt[s * W + rank]);
+}
+
+// the owner rank: wait until every source rank has delivered what the plan expects, then unpack
+__global__ void __launch_bounds__(256) ep_unpack_symm_kernel(
+    const uint8_t* __restrict__ recv, const unsigned long long* __restrict__ flag,
+    const unsigned long long* __restrict__ expect, int W, int rows, int D, int stride,
+    float* __restrict__ x, int32_t* __restrict__ ids) {
+  if (threadIdx.x < W) {
+    const volatile unsigned long long* f = flag + threadIdx.x;
+    const unsigned long long want = expect[threadIdx.x];
+    while (*f < want) {
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const uint8_t* row = recv + static_cast<size_t>(r) * stride;
+  const unsigned short* src = reinterpret_cast<const unsigned short*>(row);
+  float* dst = x + static_cast<size_t>(r) * D;
+  for (int d = lane; d < D; d += 32) dst[d] = __bfloat162float(__ushort_as_bfloat16(__ldcv(src + d)));
+  if (lane == 0) ids[r] = __ldcv(reinterpret_cast<const int32_t*>(row + static_cast<size_t>(D) * 2));
+}
 }  // namespace
 }  // namespace skb
 
@@ -329,6 +417,29 @@ int skb_ep_push_back(const float* out_rows, int rows, int d_model, const int32_t
   const int grid = rows > 0 ? ceil_div(rows, 8) : 1;
   ep_push_back_kernel<<<grid, 256, 0, s>>>(out_rows, rows, d_model, counts, world, rank, peer_back,
                                            peer_flag, done_ctr);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_push_rows(const float* x, const int32_t* pos, const int32_t* local_ids, int slots, int top_k,
+                     int d_model, const int32_t* counts, int world, int rank, uint8_t* const* peer_recv,
+                     unsigned long long* const* peer_flag, uint32_t* done_ctr, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || slots < 0) return SKB_ECONFIG;
+  const int grid = slots > 0 ? ceil_div(slots, 8) : 1;
+  ep_push_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, pos, local_ids, slots, top_k, d_model, skb_ep_row_stride(d_model), counts, world, rank,
+      peer_recv, peer_flag, done_ctr);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_unpack_symm(const uint8_t* recv, const unsigned long long* flag, unsigned long long* expect,
+                       const int32_t* counts, int world, int rank, int rows, int d_model, float* x,
+                       int32_t* ids, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || rows < 0) return SKB_ECONFIG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ep_expect_in_kernel<<<1, 32, 0, s>>>(counts, world, rank, expect);
+  const int grid = rows > 0 ? ceil_div(rows, 8) : 1;
+  ep_unpack_symm_kernel<<<grid, 256, 0, s>>>(recv, flag, expect, world, rows, d_model,
+                                             skb_ep_row_stride(d_model), x, ids);
   return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
 }
 

@@ -88,7 +88,7 @@ def row_stride(d_model: int) -> int:
 class ExpertParallelLayer:
     def __init__(self, backend: Backend, group: Optional[dist.ProcessGroup] = None,
                  max_batch: Optional[int] = None, peer_combine: bool = False,
-                 peer_rows: int = 0):
+                 peer_rows: int = 0, peer_dispatch: bool = False):
         """`max_batch`: the largest home batch of any rank (all ranks pass the same value); the
         all-gathered ids are padded to it.  None: every rank's batch has the same size.
         `peer_combine`: the combine direction without a collective -- expert
@@ -106,8 +106,14 @@ class ExpertParallelLayer:
         self._lo = {}
         self.last_stats = {}
         self.peer = None
-        if peer_combine:
-            self.peer = backend.symm_setup(peer_rows, self.world, self.rank, group)
+        self.peer_dispatch = bool(peer_dispatch)
+        if peer_combine or peer_dispatch:
+            # `peer_dispatch`: the dispatch direction without a collective either -- the home rank
+            # packs its token rows straight into the owners' receive buffers (needs peer_combine's
+            # buffers too: both directions share the setup)
+            assert peer_combine, "peer_dispatch rides on the peer_combine setup"
+            self.peer = backend.symm_setup(peer_rows, self.world, self.rank, group,
+                                           **({"dispatch": True} if peer_dispatch else {}))
 
     def _lo_on(self, device):
         if device not in self._lo:
@@ -142,12 +148,17 @@ class ExpertParallelLayer:
         counts, pos, local = b.plan(ids_all, self._lo_on(dev), self.rank)
         cm = counts.cpu()                                     # the step's one host synchronisation
         sc, rc = cm[self.rank].tolist(), cm[:, self.rank].tolist()
-        send = b.pack(x, pos, local, int(sum(sc)))
-        # the shared expert does not depend on the exchange: enqueue it before the all-to-all so
-        # that it runs under the transfer (replicated weights, own sparsity ratio)
-        sh = b.shared(x, s_shared) if b.has_shared else None
-        recv = self._all_to_all(send, sc, rc)
-        rows_in, ids_in = b.unpack(recv, D)
+        if self.peer_dispatch:
+            b.push_rows(x, pos, local, counts, self.peer, self.rank)   # no first collective
+            sh = b.shared(x, s_shared) if b.has_shared else None
+            rows_in, ids_in = b.unpack_symm(self.peer, counts, self.rank, int(sum(rc)), D)
+        else:
+            send = b.pack(x, pos, local, int(sum(sc)))
+            # the shared expert does not depend on the exchange: enqueue it before the all-to-all
+            # so that it runs under the transfer (replicated weights, own sparsity ratio)
+            sh = b.shared(x, s_shared) if b.has_shared else None
+            recv = self._all_to_all(send, sc, rc)
+            rows_in, ids_in = b.unpack(recv, D)
         out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
         if self.peer is not None:                             # no second collective
             b.push_back(out_in, counts, self.peer, self.rank)
@@ -159,7 +170,8 @@ class ExpertParallelLayer:
                            "dispatch_bytes": int(sum(sc)) * row_stride(D),
                            "combine_bytes": int(sum(rc)) * D * 4,
                            "host_syncs": 1,
-                           "collectives": (1 if W > 1 else 0) + (2 - (self.peer is not None)) * (W > 1)}
+                           "collectives": (1 if W > 1 else 0) +
+                           (2 - (self.peer is not None) - self.peer_dispatch) * (W > 1)}
         return y
 
 
@@ -262,37 +274,74 @@ class CudaBackend:
                                        B, K, D, y.data_ptr(), self._stream()), "skb_ep_combine")
         return y
 
-    # ---- combine over peer-mapped buffers (csrc/ep.cu: ep_push_back_kernel, ep_combine_symm_kernel)
-    def symm_setup(self, max_rows, world, rank, group=None):
-        """One `back` buffer [max_rows][D] fp32 and `world` cumulative counters per rank, exported
-        through CUDA IPC and mapped by every peer (world 1: the rank maps itself)."""
+    # ---- exchange over peer-mapped buffers (csrc/ep.cu: ep_push_back_kernel, ep_combine_symm_kernel,
+    # ep_push_rows_kernel, ep_unpack_symm_kernel)
+    def symm_setup(self, max_rows, world, rank, group=None, dispatch=False):
+        """One `back` buffer [max_rows][D] fp32 and `world` cumulative counters per rank -- and, for
+        the dispatch direction, one `recv` buffer [max_rows][row_stride] with counters of its own
+        -- exported through CUDA IPC and mapped by every peer (world 1: the rank maps itself)."""
         import ctypes as C
         L, D = self.L, self.D
-        back, flag = C.c_void_p(), C.c_void_p()
-        self._ok(L.skb_ep_symm_alloc(max(1, max_rows) * D * 4, C.byref(back)), "skb_ep_symm_alloc")
-        self._ok(L.skb_ep_symm_alloc(8 * 16, C.byref(flag)), "skb_ep_symm_alloc")
-        peers_back, peers_flag = [back.value] * world, [flag.value] * world
+        rows = max(1, max_rows)
+        bufs = [("back", rows * D * 4), ("flag", 8 * 16)]
+        if dispatch:
+            bufs += [("recv", rows * row_stride(D)), ("dflag", 8 * 16)]
+        local = {}
+        for name, nbytes in bufs:
+            p = C.c_void_p()
+            self._ok(L.skb_ep_symm_alloc(nbytes, C.byref(p)), "skb_ep_symm_alloc")
+            local[name] = p
+        peers = {name: [local[name].value] * world for name, _ in bufs}
+        dev = torch.device("cuda", torch.cuda.current_device())
         if world > 1:
-            h = torch.zeros(128, dtype=torch.uint8)
-            self._ok(L.skb_ep_ipc_export(back, h.data_ptr()), "skb_ep_ipc_export")
-            self._ok(L.skb_ep_ipc_export(flag, h.data_ptr() + 64), "skb_ep_ipc_export")
-            dev = torch.device("cuda", torch.cuda.current_device())
-            allh = torch.empty(world * 128, dtype=torch.uint8, device=dev)
+            nb = 64 * len(bufs)
+            h = torch.zeros(nb, dtype=torch.uint8)
+            for i, (name, _) in enumerate(bufs):
+                self._ok(L.skb_ep_ipc_export(local[name], h.data_ptr() + 64 * i), "skb_ep_ipc_export")
+            allh = torch.empty(world * nb, dtype=torch.uint8, device=dev)
             dist.all_gather_into_tensor(allh, h.to(dev), group=group)
             allh = allh.cpu()
             for r in range(world):
                 if r == rank:
                     continue
-                pb, pf = C.c_void_p(), C.c_void_p()
-                self._ok(L.skb_ep_ipc_import(allh[r * 128:].data_ptr(), C.byref(pb)), "skb_ep_ipc_import")
-                self._ok(L.skb_ep_ipc_import(allh[r * 128 + 64:].data_ptr(), C.byref(pf)), "skb_ep_ipc_import")
-                peers_back[r], peers_flag[r] = pb.value, pf.value
-        dev = torch.device("cuda", torch.cuda.current_device())
-        return {"back": back.value, "flag": flag.value, "max_rows": max_rows,
-                "peer_back": torch.tensor(peers_back, dtype=torch.int64, device=dev),
-                "peer_flag": torch.tensor(peers_flag, dtype=torch.int64, device=dev),
-                "expect": torch.zeros(16, dtype=torch.int64, device=dev),
-                "done": torch.zeros(1, dtype=torch.int32, device=dev), "world": world}
+                for i, (name, _) in enumerate(bufs):
+                    pp = C.c_void_p()
+                    self._ok(L.skb_ep_ipc_import(allh[r * nb + 64 * i:].data_ptr(), C.byref(pp)),
+                             "skb_ep_ipc_import")
+                    peers[name][r] = pp.value
+        out = {"back": local["back"].value, "flag": local["flag"].value, "max_rows": max_rows,
+               "peer_back": torch.tensor(peers["back"], dtype=torch.int64, device=dev),
+               "peer_flag": torch.tensor(peers["flag"], dtype=torch.int64, device=dev),
+               "expect": torch.zeros(16, dtype=torch.int64, device=dev),
+               "done": torch.zeros(1, dtype=torch.int32, device=dev), "world": world}
+        if dispatch:
+            out.update({"recv": local["recv"].value, "dflag": local["dflag"].value,
+                        "peer_recv": torch.tensor(peers["recv"], dtype=torch.int64, device=dev),
+                        "peer_dflag": torch.tensor(peers["dflag"], dtype=torch.int64, device=dev),
+                        "dexpect": torch.zeros(16, dtype=torch.int64, device=dev),
+                        "ddone": torch.zeros(1, dtype=torch.int32, device=dev)})
+        return out
+
+    def push_rows(self, x, pos, local, counts, peer, rank):
+        """pack + dispatch in one kernel: token rows straight into the owners' receive buffers"""
+        B, D = x.shape
+        self._ok(self.L.skb_ep_push_rows(x.contiguous().data_ptr(), pos.data_ptr(), local.data_ptr(),
+                                         B * self.top_k, self.top_k, D, counts.data_ptr(),
+                                         peer["world"], rank, peer["peer_recv"].data_ptr(),
+                                         peer["peer_dflag"].data_ptr(), peer["ddone"].data_ptr(),
+                                         self._stream()), "skb_ep_push_rows")
+
+    def unpack_symm(self, peer, counts, rank, n_rows, d_model):
+        """wait for the peers' rows (cumulative counters), then unpack"""
+        dev = counts.device
+        rows = torch.empty((n_rows, d_model), dtype=torch.float32, device=dev)
+        ids = torch.empty(n_rows, dtype=torch.int32, device=dev)
+        assert n_rows <= max(1, peer["max_rows"]), "peer receive buffer too small for this step"
+        self._ok(self.L.skb_ep_unpack_symm(peer["recv"], peer["dflag"], peer["dexpect"].data_ptr(),
+                                           counts.data_ptr(), peer["world"], rank, n_rows, d_model,
+                                           rows.data_ptr(), ids.data_ptr(), self._stream()),
+                 "skb_ep_unpack_symm")
+        return rows, ids
 
     def push_back(self, out_rows, counts, peer, rank):
         M = out_rows.shape[0]

@@ -746,6 +746,14 @@ def test_ep_layer_world_1_equals_the_single_gpu_layer(skb, oracle, shape, B, s):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(y2.cpu().numpy(), y.cpu().numpy())
     assert peer_layer.last_stats["collectives"] == 0
+    # ... and the dispatch direction the same way (rows packed straight into the owner's receive
+    # buffer, the unpack waits on counters): no data-path collective left
+    both = ep.ExpertParallelLayer(backend, peer_combine=True, peer_dispatch=True, peer_rows=B * K)
+    for _ in range(3):
+        y3 = both.forward(torch.from_numpy(x).cuda(), s, s if S else 0.0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y3.cpu().numpy(), y.cpu().numpy())
+    assert both.last_stats["collectives"] == 0
 
 
 # ---------------------------------------------------------------------------------------------
