@@ -714,6 +714,91 @@ def test_ep_plan_pack_combine_kernels_match_the_cpu_restatement(skb, oracle):
     np.testing.assert_array_equal(y.cpu().numpy(), y_ref)
 
 
+def test_ep_peer_exchange_places_rows_like_the_collectives(skb, oracle):
+    """Both peer-memory directions with several ranks EMULATED on one GPU (every rank's buffers
+    live on this device, the "peer mappings" are plain pointers): the rows the owners unpack and
+    the rows the home ranks find in their back buffers must be what the two all-to-all-v
+    collectives would have delivered, in the same positions, over two consecutive steps
+    (cumulative counters)."""
+    torch = pytest.importorskip("torch")
+    from paper_2605_08575_b200 import ep, _lib
+    L = _lib.load()
+    E, K, D, W, B = 11, 3, 40, 3, 6
+    RS = ep.row_stride(D)
+    rng = np.random.default_rng(5)
+    lo = np.array([r[0] for r in ep.owner_ranges(E, W)] + [E], np.int32)
+    d_lo = torch.from_numpy(lo).cuda()
+    cap = W * B * K
+    recv = [torch.zeros((cap, RS), dtype=torch.uint8, device="cuda") for _ in range(W)]
+    backb = [torch.zeros((cap, D), dtype=torch.float32, device="cuda") for _ in range(W)]
+    dflag = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in range(W)]
+    bflag = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in range(W)]
+    dexp = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in range(W)]
+    bexp = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in range(W)]
+    done = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ptrs = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device="cuda")
+    p_recv, p_dflag, p_back, p_bflag = ptrs(recv), ptrs(dflag), ptrs(backb), ptrs(bflag)
+    for step in range(2):
+        ids_all = np.stack([np.stack([rng.permutation(E)[:K] for _ in range(B)]).reshape(-1)
+                            for _ in range(W)]).astype(np.int32)
+        ids_all[1, -K:] = -1  # a short batch on rank 1
+        d_ids = torch.from_numpy(ids_all).cuda()
+        xs = [torch.from_numpy(oracle.generate_tokens(B, D, 20 + 3 * step + r)).cuda() for r in range(W)]
+        counts = torch.empty((W, W), dtype=torch.int32, device="cuda")
+        pos, loc, send = [], [], []
+        for r in range(W):
+            pr = torch.empty(B * K, dtype=torch.int32, device="cuda")
+            lr = torch.empty(B * K, dtype=torch.int32, device="cuda")
+            assert L.skb_ep_plan(d_ids.data_ptr(), W, B * K, d_lo.data_ptr(), r, counts.data_ptr(),
+                                 pr.data_ptr(), lr.data_ptr(), 1) == 0
+            pos.append(pr)
+            loc.append(lr)
+        cm = counts.cpu().numpy()
+        for r in range(W):  # the collective path's send buffers
+            sr = torch.zeros((int(cm[r].sum()), RS), dtype=torch.uint8, device="cuda")
+            assert L.skb_ep_pack(xs[r].data_ptr(), pos[r].data_ptr(), loc[r].data_ptr(), B * K, K, D,
+                                 sr.data_ptr(), 1) == 0
+            send.append(sr.cpu().numpy())
+        soff = np.concatenate([np.zeros((W, 1), np.int64), np.cumsum(cm, axis=1)], axis=1)
+        # what all-to-all-v delivers to owner d: rank 0's segment for d, then rank 1's, ...
+        recv_ref = [np.concatenate([send[sr][soff[sr, d]:soff[sr, d + 1]] for sr in range(W)])
+                    for d in range(W)]
+        for r in range(W):
+            assert L.skb_ep_push_rows(xs[r].data_ptr(), pos[r].data_ptr(), loc[r].data_ptr(), B * K, K, D,
+                                      counts.data_ptr(), W, r, p_recv.data_ptr(), p_dflag.data_ptr(),
+                                      done.data_ptr(), 1) == 0
+        outs = []
+        for d in range(W):
+            n = int(cm[:, d].sum())
+            rows = torch.empty((n, D), dtype=torch.float32, device="cuda")
+            rid = torch.empty(n, dtype=torch.int32, device="cuda")
+            assert L.skb_ep_unpack_symm(recv[d].data_ptr(), dflag[d].data_ptr(), dexp[d].data_ptr(),
+                                        counts.data_ptr(), W, d, n, D, rows.data_ptr(), rid.data_ptr(),
+                                        1) == 0
+            rows_ref = torch.empty((n, D), dtype=torch.float32, device="cuda")
+            rid_ref = torch.empty(n, dtype=torch.int32, device="cuda")
+            assert L.skb_ep_unpack(torch.from_numpy(recv_ref[d]).cuda().data_ptr(), n, D,
+                                   rows_ref.data_ptr(), rid_ref.data_ptr(), 1) == 0
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(rows.cpu().numpy(), rows_ref.cpu().numpy())
+            np.testing.assert_array_equal(rid.cpu().numpy(), rid_ref.cpu().numpy())
+            outs.append(rows * (1.0 + d))  # stand-in for the experts' row outputs
+        # combine direction: owner d's rows go back to their home ranks in the homes' send order
+        roff = np.concatenate([np.zeros((1, W), np.int64), np.cumsum(cm, axis=0)], axis=0)
+        for d in range(W):
+            assert L.skb_ep_push_back(outs[d].data_ptr(), outs[d].shape[0], D, counts.data_ptr(), W, d,
+                                      p_back.data_ptr(), p_bflag.data_ptr(), bexp[d].data_ptr(),
+                                      done.data_ptr(), 1) == 0
+        torch.cuda.synchronize()
+        for h in range(W):
+            # what the second all-to-all-v delivers to home h: owner 0's rows for h, then owner 1's
+            back_ref = np.concatenate([outs[d].cpu().numpy()[roff[h, d]:roff[h + 1, d]] for d in range(W)])
+            np.testing.assert_array_equal(backb[h].cpu().numpy()[: back_ref.shape[0]], back_ref)
+            # the home rank's counters: cumulative rows received from every owner
+            want = bexp[h].cpu().numpy()[:W]
+            np.testing.assert_array_equal(bflag[h].cpu().numpy()[:W], want)
+
+
 @pytest.mark.parametrize("shape,B,s", [((16, 4, 256, 192, 64), 9, 0.5), ((8, 1, 320, 256, 0), 33, 0.9)])
 def test_ep_layer_world_1_equals_the_single_gpu_layer(skb, oracle, shape, B, s):
     """ExpertParallelLayer over the CUDA backend with one rank (plan, pack, unpack, external-routing
