@@ -389,8 +389,9 @@ def run_ep(args, torch, dist, skb, rank, world, local):
             "the expert-parallel arm needs the NCCL process group of all ranks"
     backend = ep.CudaBackend(skb, cfg, SEED, SCALE, rank, world, device=local,
                              max_rows=max(64, 4 * B * shape["K"]))
-    layer = ep.ExpertParallelLayer(backend, peer_combine=args.peer_combine or args.peer_dispatch,
-                                   peer_dispatch=args.peer_dispatch, peer_rows=world * B * shape["K"])
+    layer = ep.ExpertParallelLayer(backend, peer_combine=args.peer_combine or args.peer_dispatch or args.fused_push,
+                                   peer_dispatch=args.peer_dispatch, fused_push=args.fused_push,
+                                   peer_rows=world * B * shape["K"])
     xs = [torch.from_numpy(make_tokens(B, shape["D"], 2 + 17 * rank + i)).cuda() for i in range(8)]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     sampler = ClockSampler(local)
@@ -471,8 +472,9 @@ def run_ep(args, torch, dist, skb, rank, world, local):
                                        "receive buffers (no collective) and "
                                        if args.peer_dispatch else "one packed bf16 all-to-all-v out and ") +
                                       ("peer-memory stores back (no second collective)"
-                                       if (args.peer_combine or args.peer_dispatch)
+                                       if (args.peer_combine or args.peer_dispatch or args.fused_push)
                                        else "one fp32 all-to-all-v back") +
+                                      (" written by the expert layer's last kernel" if args.fused_push else "") +
                                       " over NCCL / NVLink, shared expert replicated",
                        "l2": "512 MiB memset between steps (inside the timed pair is only the "
                              "layer) + ring of 8 token batches",
@@ -859,6 +861,8 @@ def main():
     ap.add_argument("--ep", action="store_true", help="expert-parallel arm (ep.py) at any rank count")
     ap.add_argument("--peer-combine", action="store_true",
                     help="--ep: combine through peer-mapped buffers instead of the second all-to-all")
+    ap.add_argument("--fused-push", action="store_true",
+                    help="--ep --peer-combine: the expert layer's last kernel writes into the home buffers")
     ap.add_argument("--peer-dispatch", action="store_true",
                     help="--ep: both directions through peer-mapped buffers (no data-path collective)")
     args = ap.parse_args()

@@ -207,6 +207,12 @@ int skb_layer_forward(skb_layer* layer, const skb_forward_args* args, skb_report
  * skb_layer_reserve.  Capture pointers in args are ignored. */
 int skb_layer_forward_device(skb_layer* layer, const skb_forward_args* args, void* stream,
                              skb_report* report);
+/* The same with one destination per output row: row t of the result goes to y_rows[t] (device
+ * array of device pointers, each d_model floats; args->y is ignored).  Expert parallelism passes
+ * rows of the home ranks' peer-mapped buffers (skb_ep_back_ptrs), so that the layer's last kernel
+ * writes its outputs where they are combined -- no copy pass.  Dense and top-k modes. */
+int skb_layer_forward_device_rows(skb_layer* layer, const skb_forward_args* args, void* stream,
+                                  float* const* y_rows);
 
 /* Per-stage milliseconds of the last forward call (host or device entry) that
  * carried SKB_FLAG_TIME_STAGES; waits for that forward to finish.  ms must
@@ -336,6 +342,14 @@ int skb_ep_push_rows(const float* x, const int32_t* pos, const int32_t* local_id
 int skb_ep_unpack_symm(const uint8_t* recv, const unsigned long long* flag, unsigned long long* expect,
                        const int32_t* counts, int world, int rank, int rows, int d_model, float* x,
                        int32_t* ids, void* stream);
+/* Outputs pushed by the expert layer itself: skb_ep_back_ptrs fills ptrs[r] with the address of
+ * received row r's output in its home rank's `back` buffer (pass them to
+ * skb_layer_forward_device_rows); skb_ep_signal_back, enqueued after the layer, fences at system
+ * scope and bumps the home ranks' counters (it also advances `expect`, like skb_ep_push_back). */
+int skb_ep_back_ptrs(const int32_t* counts, int world, int rank, int rows, int d_model,
+                     float* const* peer_back, float** ptrs, void* stream);
+int skb_ep_signal_back(const int32_t* counts, int world, int rank,
+                       unsigned long long* const* peer_flag, unsigned long long* expect, void* stream);
 int skb_ep_combine_symm(const float* back, const unsigned long long* flag,
                         const unsigned long long* expect, int world, const int32_t* pos,
                         const float* weights, const float* shared, int batch, int top_k, int d_model,

@@ -33,7 +33,7 @@ EXPORTS = (
     "skb_ep_row_stride", "skb_ep_plan", "skb_ep_pack", "skb_ep_unpack", "skb_ep_combine",
     "skb_ep_symm_alloc", "skb_ep_symm_free", "skb_ep_ipc_export", "skb_ep_ipc_import",
     "skb_ep_ipc_close", "skb_ep_push_back", "skb_ep_combine_symm", "skb_ep_push_rows",
-    "skb_ep_unpack_symm",
+    "skb_ep_unpack_symm", "skb_ep_back_ptrs", "skb_ep_signal_back", "skb_layer_forward_device_rows",
 )
 
 
@@ -127,6 +127,9 @@ def load() -> C.CDLL:
     L.skb_ep_ipc_import.argtypes = [vp, C.POINTER(vp)]
     L.skb_ep_ipc_close.argtypes = [vp]
     L.skb_ep_push_back.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]
+    L.skb_ep_back_ptrs.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]
+    L.skb_ep_signal_back.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp]
+    L.skb_layer_forward_device_rows.argtypes = [vp, C.POINTER(SkbForwardArgs), vp, vp]
     L.skb_ep_push_rows.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp,
                                    vp]
     L.skb_ep_unpack_symm.argtypes = [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]

@@ -449,7 +449,8 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                  const uint8_t* d_mask_r, const uint8_t* d_mask_s, uint8_t* d_mask_out_r,
                  uint8_t* d_mask_out_s, cudaStream_t stream, bool timing,
                  const int32_t* d_ids_in = nullptr, const float* d_w_in = nullptr,
-                 int32_t* d_ids_out = nullptr, float* d_w_out = nullptr, bool capture_h = false) {
+                 int32_t* d_ids_out = nullptr, float* d_w_out = nullptr, bool capture_h = false,
+                 float* const* d_y_rows = nullptr) {
   const Geometry& g = L->g;
   const int B = a->batch;
   const int BK = B * g.K;
@@ -528,8 +529,10 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   // 1e-5 parity mode: the tensor-core GEMMs fold long contractions chunk by chunk (gateup.cu)
   const bool precise = !(a->flags & SKB_FLAG_BF16_H);
 
+  if (d_y_rows != nullptr && !dense_down)
+    return fail(SKB_ECONFIG, "forward: per-row output destinations need the dense down projection");
   // Decode batches: the whole layer as one persistent launch (decode.cu).
-  if (d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
+  if (d_y_rows == nullptr && d_ids_in == nullptr && L->d_dec_ctr != nullptr && decode_fused_eligible(g, B) &&
       !budget && (sel_mode != kSelectThreshold || L->d_wu != nullptr) &&
       !(a->flags & (SKB_FLAG_FAST_ROUTER | SKB_FLAG_SIMT_GATEUP | SKB_FLAG_DENSE_DOWN |
                     SKB_FLAG_GATHER_DOWN | SKB_FLAG_NO_FUSED_DECODE)) &&
@@ -749,7 +752,7 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                                prefetch_wdt ? L->d_wdt : nullptr,
                                prefetch_wdt ? L->d_wdt_shared : nullptr);
     tm.mark();
-    launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y);
+    launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y, d_y_rows);
     tm.mark();
   } else {
     DownArgs da{};
@@ -787,11 +790,11 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   return SKB_OK;
 }
 
-int check_args(const skb_layer* L, const skb_forward_args* a) {
+int check_args(const skb_layer* L, const skb_forward_args* a, bool y_elsewhere = false) {
   if (L == nullptr) return fail(SKB_EINTERNAL, "layer is null");
   if (a == nullptr) return fail(SKB_EINTERNAL, "args is null");
   const Geometry& g = L->g;
-  if (a->x == nullptr || (a->y == nullptr && a->mode != SKB_MODE_ROUTE_ONLY))
+  if (a->x == nullptr || (a->y == nullptr && a->mode != SKB_MODE_ROUTE_ONLY && !y_elsewhere))
     return fail(SKB_ESHAPE, "forward: x and y must be non-null");
   if (a->batch < 1) return fail(SKB_ESHAPE, "route: empty batch");  // router.cpp:16-18
   if (a->mode != SKB_MODE_DENSE && a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_MASKED &&
@@ -1470,6 +1473,23 @@ int skb_layer_forward_device(skb_layer* L, const skb_forward_args* a, void* stre
   else if (a->mode != SKB_MODE_ROUTE_ONLY)
     fill_report(L, a, report, nullptr, nullptr);
   return SKB_OK;
+}
+
+int skb_layer_forward_device_rows(skb_layer* L, const skb_forward_args* a, void* stream,
+                                  float* const* y_rows) {
+  int rc = check_args(L, a, /*y_elsewhere=*/true);
+  if (rc) return rc;
+  if (y_rows == nullptr) return fail(SKB_EINTERNAL, "forward_device_rows: y_rows is null");
+  if (a->batch > L->cap_batch)
+    return fail(SKB_ESHAPE, "forward_device_rows: batch %d exceeds reserved capacity %d; call skb_layer_reserve",
+                a->batch, L->cap_batch);
+  if (a->mode != SKB_MODE_TOPK && a->mode != SKB_MODE_DENSE)
+    return fail(SKB_ECONFIG, "forward_device_rows: dense and top-k modes only");
+  if (a->mode == SKB_MODE_TOPK && a->slot_n_off != nullptr)
+    return fail(SKB_ECONFIG, "forward_device_rows: per-slot neuron budgets need skb_layer_forward");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : L->stream;
+  return forward_core(L, a, a->x, nullptr, nullptr, nullptr, nullptr, nullptr, s, false, a->ids_in,
+                      a->weights_in, nullptr, nullptr, false, y_rows);
 }
 
 int skb_layer_stage_times(skb_layer* L, float* ms) {

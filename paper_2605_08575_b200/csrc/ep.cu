@@ -314,6 +314,44 @@ __global__ void __launch_bounds__(256) ep_push_rows_kernel(
   }
 }
 
+// where received row r's OUTPUT goes: its home rank's back buffer, the row that rank's plan
+// expects (the arithmetic of ep_push_back_kernel, as pointers for the expert layer's last kernel)
+__global__ void __launch_bounds__(256) ep_back_ptrs_kernel(const int32_t* __restrict__ cnt, int W,
+                                                           int rank, int M, int D,
+                                                           float* const* __restrict__ peer_back,
+                                                           float** __restrict__ ptrs) {
+  __shared__ int s_roff[kMaxWorld + 1], s_base[kMaxWorld];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < W; ++s) {
+      s_roff[s] = o;
+      o += cnt[s * W + rank];
+      int b = 0;
+      for (int d = 0; d < rank; ++d) b += cnt[s * W + d];
+      s_base[s] = b;
+    }
+    s_roff[W] = o;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  int s = 0;
+  while (s + 1 < W && r >= s_roff[s + 1]) ++s;
+  ptrs[r] = peer_back[s] + static_cast<size_t>(s_base[s] + r - s_roff[s]) * D;
+}
+
+// after the expert layer (stream order: its stores are complete): system fence, then the home
+// ranks' counters
+__global__ void ep_signal_back_kernel(const int32_t* __restrict__ cnt, int W, int rank,
+                                      unsigned long long* const* __restrict__ peer_flag) {
+  __threadfence_system();
+  const int s = threadIdx.x;
+  if (s < W) {
+    const unsigned long long n = static_cast<unsigned long long>(cnt[s * W + rank]);
+    if (n) atomicAdd_system(peer_flag[s] + rank, n);
+  }
+}
+
 // expected cumulative rows per SOURCE rank at this owner rank: expect[s] += cnt[s][rank]
 __global__ void ep_expect_in_kernel(const int32_t* __restrict__ cnt, int W, int rank,
                                     unsigned long long* __restrict__ expect) {
@@ -440,6 +478,24 @@ int skb_ep_unpack_symm(const uint8_t* recv, const unsigned long long* flag, unsi
   const int grid = rows > 0 ? ceil_div(rows, 8) : 1;
   ep_unpack_symm_kernel<<<grid, 256, 0, s>>>(recv, flag, expect, world, rows, d_model,
                                              skb_ep_row_stride(d_model), x, ids);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_back_ptrs(const int32_t* counts, int world, int rank, int rows, int d_model,
+                     float* const* peer_back, float** ptrs, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || rows < 0) return SKB_ECONFIG;
+  if (rows == 0) return SKB_OK;
+  ep_back_ptrs_kernel<<<ceil_div(rows, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      counts, world, rank, rows, d_model, peer_back, ptrs);
+  return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
+}
+
+int skb_ep_signal_back(const int32_t* counts, int world, int rank,
+                       unsigned long long* const* peer_flag, unsigned long long* expect, void* stream) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return SKB_ECONFIG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ep_expect_kernel<<<1, 32, 0, s>>>(counts, world, rank, expect);
+  ep_signal_back_kernel<<<1, 32, 0, s>>>(counts, world, rank, peer_flag);
   return cudaGetLastError() == cudaSuccess ? SKB_OK : SKB_ECUDA;
 }
 

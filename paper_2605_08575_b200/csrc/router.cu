@@ -1215,7 +1215,8 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
                                                            const int32_t* __restrict__ inv,
                                                            const float* __restrict__ weights,
                                                            int B, int K, int D, int Dp,
-                                                           int has_shared, float* __restrict__ y) {
+                                                           int has_shared, float* __restrict__ y,
+                                                           float* const* __restrict__ y_rows) {
   // The token's row indices and weights first (one round trip for all slots), then the slot
   // rows eight at a time with every load in flight before the first add: the kernel is two or
   // three memory round trips long instead of two per slot.
@@ -1261,11 +1262,15 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
       }
     }
   }
-  for (int i = 0; i < 4; ++i) if (c4 + i < D) y[static_cast<size_t>(t) * D + c4 + i] = acc[i];
+  // (y_rows: every token's output row has its own destination -- expert parallelism writes it
+  // straight into the home rank's peer-mapped buffer)
+  float* yo = y_rows != nullptr ? y_rows[t] : y + static_cast<size_t>(t) * D;
+  for (int i = 0; i < 4; ++i) if (c4 + i < D) yo[c4 + i] = acc[i];
 }
 
 int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
-                        const float* weights, int B, const Geometry& g, float* y) {
+                        const float* weights, int B, const Geometry& g, float* y,
+                        float* const* y_rows) {
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1276,7 +1281,7 @@ int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32
   cfg.gridDim = dim3(ceil_div(ceil_div(g.D, 4), 256), B);
   cfg.blockDim = dim3(256);
   cudaLaunchKernelEx(&cfg, combine_rows_kernel, slot_out, inv, weights, B, g.K, g.D, g.Dp,
-                     g.has_shared, y);
+                     g.has_shared, y, y_rows);
   return 1;
 }
 

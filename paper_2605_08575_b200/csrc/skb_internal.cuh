@@ -112,7 +112,8 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    bool precise = false, bool early_tiles = false, const void* wdt_image = nullptr,
                    const void* wdt_shared_image = nullptr);
 int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
-                        const float* weights, int B, const Geometry& g, float* y);
+                        const float* weights, int B, const Geometry& g, float* y,
+                        float* const* y_rows = nullptr);
 int launch_gateup_simt(const LaunchCtx& ctx, const __nv_bfloat16* wgu, const __nv_bfloat16* xs,
                        const int32_t* row_expert, int rows, const Geometry& g, float* h);
 

@@ -88,7 +88,7 @@ def row_stride(d_model: int) -> int:
 class ExpertParallelLayer:
     def __init__(self, backend: Backend, group: Optional[dist.ProcessGroup] = None,
                  max_batch: Optional[int] = None, peer_combine: bool = False,
-                 peer_rows: int = 0, peer_dispatch: bool = False):
+                 peer_rows: int = 0, peer_dispatch: bool = False, fused_push: bool = False):
         """`max_batch`: the largest home batch of any rank (all ranks pass the same value); the
         all-gathered ids are padded to it.  None: every rank's batch has the same size.
         `peer_combine`: the combine direction without a collective -- expert
@@ -106,6 +106,10 @@ class ExpertParallelLayer:
         self._lo = {}
         self.last_stats = {}
         self.peer = None
+        # `fused_push` (with peer_combine): the expert layer's combine kernel writes each output
+        # row into the home rank's buffer directly instead of a separate push pass
+        self.fused_push = bool(fused_push)
+        assert not fused_push or peer_combine, "fused_push rides on the peer_combine setup"
         self.peer_dispatch = bool(peer_dispatch)
         if peer_combine or peer_dispatch:
             # `peer_dispatch`: the dispatch direction without a collective either -- the home rank
@@ -159,11 +163,16 @@ class ExpertParallelLayer:
             sh = b.shared(x, s_shared) if b.has_shared else None
             recv = self._all_to_all(send, sc, rc)
             rows_in, ids_in = b.unpack(recv, D)
-        out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
-        if self.peer is not None:                             # no second collective
+        if self.peer is not None and self.fused_push:
+            # the expert layer's last kernel writes into the home ranks' buffers itself
+            b.experts_to_peers(rows_in, ids_in, s_routed, counts, self.peer, self.rank)
+            y = b.combine_symm(self.peer, pos, w, sh)
+        elif self.peer is not None:                           # no second collective
+            out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
             b.push_back(out_in, counts, self.peer, self.rank)
             y = b.combine_symm(self.peer, pos, w, sh)
         else:
+            out_in = b.experts(rows_in, ids_in, s_routed) if rows_in.shape[0] else rows_in
             back = self._all_to_all(out_in, rc, sc)           # back to the home ranks, send order
             y = b.combine(back, pos, w, sh)
         self.last_stats = {"sent_rows": sc, "recv_rows": rc,
@@ -342,6 +351,25 @@ class CudaBackend:
                                            rows.data_ptr(), ids.data_ptr(), self._stream()),
                  "skb_ep_unpack_symm")
         return rows, ids
+
+    def experts_to_peers(self, rows, local_ids, s, counts, peer, rank):
+        """The expert layer writes every output row straight into its home rank's back buffer
+        (skb_ep_back_ptrs + skb_layer_forward_device_rows), then the counters move
+        (skb_ep_signal_back): no output tensor, no copy pass."""
+        M = rows.shape[0]
+        if M:
+            rows = rows.contiguous()
+            ptrs = torch.empty(M, dtype=torch.int64, device=rows.device)
+            self._ok(self.L.skb_ep_back_ptrs(counts.data_ptr(), peer["world"], rank, M, self.D,
+                                             peer["peer_back"].data_ptr(), ptrs.data_ptr(),
+                                             self._stream()), "skb_ep_back_ptrs")
+            self.slice.reserve(M)
+            self.slice.forward_device_rows(rows.data_ptr(), ptrs.data_ptr(), M, mode=self.skb.MODE_TOPK,
+                                           s_routed=s, stream=self._stream(),
+                                           ids_in_ptr=local_ids.contiguous().data_ptr())
+        self._ok(self.L.skb_ep_signal_back(counts.data_ptr(), peer["world"], rank,
+                                           peer["peer_flag"].data_ptr(), peer["expect"].data_ptr(),
+                                           self._stream()), "skb_ep_signal_back")
 
     def push_back(self, out_rows, counts, peer, rank):
         M = out_rows.shape[0]

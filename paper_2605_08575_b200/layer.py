@@ -311,6 +311,19 @@ class MoELayerWeights:
         a.ids_in, a.weights_in = ids_in_ptr or None, weights_in_ptr or None
         _check(_lib.load().skb_layer_forward_device(self._h, C.byref(a), C.c_void_p(stream), None))
 
+    def forward_device_rows(self, x_ptr: int, y_rows_ptr: int, batch: int, mode: int = MODE_TOPK,
+                            s_routed: float = 0.0, s_shared: float = 0.0, flags: int = 0,
+                            stream: int = 0, ids_in_ptr: int = 0, weights_in_ptr: int = 0) -> None:
+        """forward_device with one destination per output row: y_rows_ptr is a device array of
+        `batch` device pointers (d_model floats each)."""
+        a = SkbForwardArgs()
+        a.batch, a.mode, a.flags = batch, mode, flags
+        a.s_routed, a.s_shared = s_routed, s_shared
+        a.x = x_ptr
+        a.ids_in, a.weights_in = ids_in_ptr or None, weights_in_ptr or None
+        _check(_lib.load().skb_layer_forward_device_rows(self._h, C.byref(a), C.c_void_p(stream),
+                                                         C.c_void_p(y_rows_ptr)))
+
     def route_device(self, x_ptr: int, ids_out_ptr: int, weights_out_ptr: int, batch: int,
                      flags: int = 0, stream: int = 0) -> None:
         """SKB_MODE_ROUTE_ONLY on device pointers: x [batch][D] -> ids / weights [batch][K_route]."""

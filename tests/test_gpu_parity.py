@@ -839,6 +839,13 @@ def test_ep_layer_world_1_equals_the_single_gpu_layer(skb, oracle, shape, B, s):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(y3.cpu().numpy(), y.cpu().numpy())
     assert both.last_stats["collectives"] == 0
+    # ... and with the expert layer's last kernel writing into the home buffers itself
+    fused = ep.ExpertParallelLayer(backend, peer_combine=True, peer_dispatch=True, fused_push=True,
+                                   peer_rows=B * K)
+    for _ in range(3):
+        y4 = fused.forward(torch.from_numpy(x).cuda(), s, s if S else 0.0)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(y4.cpu().numpy(), y.cpu().numpy())
 
 
 # ---------------------------------------------------------------------------------------------
