@@ -739,6 +739,10 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
   }
   tm.mark();
 
+  // Per-row destinations with one expert per row, weight 1 and no shared expert (the expert
+  // rank of expert parallelism): the combine would copy -- the GEMM's epilogue stores there itself.
+  const bool direct_rows = d_y_rows != nullptr && g.K == 1 && !g.has_shared && d_ids_in != nullptr &&
+                           d_w_in == nullptr;
   if (dense_down) {
     // W_down^T blocks prefetched into the L2 while the CTAs wait for the selection kernel: pays
     // when the image is small enough to sit there (Granite shape batch 256: the down stage starts
@@ -750,9 +754,11 @@ int forward_core(skb_layer* L, const skb_forward_args* a, const float* d_x, floa
                                L->tmap_hb[tn_idx], L->tmap_hb[1], nsplit, tn, L->disp, max_tiles, g,
                                L->d_slot_out, pair_down, precise, /*early_tiles=*/true,
                                prefetch_wdt ? L->d_wdt : nullptr,
-                               prefetch_wdt ? L->d_wdt_shared : nullptr);
+                               prefetch_wdt ? L->d_wdt_shared : nullptr,
+                               direct_rows ? d_y_rows : nullptr, direct_rows ? L->disp.perm : nullptr);
     tm.mark();
-    launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y, d_y_rows);
+    if (!direct_rows)
+      launches += launch_combine_rows(ctx, L->d_slot_out, L->disp.inv, L->d_wts, B, g, d_y, d_y_rows);
     tm.mark();
   } else {
     DownArgs da{};

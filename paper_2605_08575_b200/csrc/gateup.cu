@@ -111,6 +111,11 @@ struct TcArgs {
   int rows_per_expert;                 // A-image rows per routed expert
   int nsplit;                          // MODE 1: B operands accumulated per K block (1 or 3)
   const int* tiles_flag;  // MODE 0: non-zero once the tile list is written (implies early_tiles)
+  // MODE 1, optional: output row r (expert-sorted) goes to out_rows[out_perm[r]] instead of `out`
+  // -- expert parallelism with one expert per row and weight 1: the slot output IS the layer's
+  // output, stored straight into the home rank's peer-mapped buffer from the TMEM epilogue
+  float* const* out_rows;
+  const int32_t* out_perm;
   int early_tiles;  // the tile list was written at least two kernels upstream: readable -- and the
                     // weight stream startable -- before the programmatic-launch wait
 };
@@ -390,6 +395,27 @@ grouped_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
           tmem_ld_32x32b_x16(taddr, v0);
           if (TN >= 32) tmem_ld_32x32b_x16(taddr + 16, v1);
           tmem_ld_wait();
+          if (a.out_rows != nullptr) {
+            // lane c fetches the destination of column c0 + c once; the stores get it by shuffle
+            const int col = c0 + lane;
+            const unsigned long long mine =
+                (col < nrows && (TN >= 32 || lane < 16))
+                    ? reinterpret_cast<unsigned long long>(a.out_rows[a.out_perm[row0 + col]])
+                    : 0ull;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float* dst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, c));
+              if (c0 + c < nrows && d < m_valid) dst[d] = __uint_as_float(v0[c]);
+            }
+            if (TN >= 32) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                float* dst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, 16 + c));
+                if (c0 + 16 + c < nrows && d < m_valid) dst[d] = __uint_as_float(v1[c]);
+              }
+            }
+            continue;
+          }
           float* orow = a.out + static_cast<size_t>(row0 + c0) * a.out_stride + d;
 #pragma unroll
           for (int c = 0; c < 16; ++c)
@@ -624,9 +650,23 @@ grouped_tc_chunked_kernel(const __grid_constant__ CUtensorMap tmap_a,
             swiglu_store16<TN>(v, lane, c0, nrows, n, m_valid, row0, tile, a);
           } else {
 #pragma unroll
-            for (int cc = 0; cc < 16; ++cc)
-              if (c0 + cc < nrows && n < m_valid)
-                a.out[static_cast<size_t>(row0 + c0 + cc) * a.out_stride + n] = __uint_as_float(v[cc]);
+            if (a.out_rows != nullptr) {
+              const int col = c0 + lane;
+              const unsigned long long mine =
+                  (lane < 16 && col < nrows)
+                      ? reinterpret_cast<unsigned long long>(a.out_rows[a.out_perm[row0 + col]])
+                      : 0ull;
+#pragma unroll
+              for (int cc = 0; cc < 16; ++cc) {
+                float* dst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, mine, cc));
+                if (c0 + cc < nrows && n < m_valid) dst[n] = __uint_as_float(v[cc]);
+              }
+            } else {
+#pragma unroll
+              for (int cc = 0; cc < 16; ++cc)
+                if (c0 + cc < nrows && n < m_valid)
+                  a.out[static_cast<size_t>(row0 + c0 + cc) * a.out_stride + n] = __uint_as_float(v[cc]);
+            }
           }
         }
         if (!last) {
@@ -773,8 +813,11 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_wdt_shared, const CUtensorMap* tmap_hb /*[3]*/,
                    const CUtensorMap* tmap_hb32 /*[3]*/, int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
                    const Geometry& g, float* slot_out, bool pair_blocks, bool precise,
-                   bool early_tiles, const void* wdt_image, const void* wdt_shared_image) {
+                   bool early_tiles, const void* wdt_image, const void* wdt_shared_image,
+                   float* const* out_rows, const int32_t* out_perm) {
   TcArgs a{};
+  a.out_rows = out_rows;
+  a.out_perm = out_perm;
   a.early_tiles = early_tiles ? 1 : 0;
   a.a_base = wdt_image;
   a.a_shared_base = wdt_shared_image;

@@ -110,7 +110,8 @@ int launch_down_tc(const LaunchCtx& ctx, const CUtensorMap* tmap_wdt,
                    const CUtensorMap* tmap_hb32 /*[3], 32-row boxes*/, int nsplit, int tile_tokens, const DispatchBuffers& d, int max_tiles,
                    const Geometry& g, float* slot_out, bool pair_blocks = false,
                    bool precise = false, bool early_tiles = false, const void* wdt_image = nullptr,
-                   const void* wdt_shared_image = nullptr);
+                   const void* wdt_shared_image = nullptr, float* const* out_rows = nullptr,
+                   const int32_t* out_perm = nullptr);
 int launch_combine_rows(const LaunchCtx& ctx, const float* slot_out, const int32_t* inv,
                         const float* weights, int B, const Geometry& g, float* y,
                         float* const* y_rows = nullptr);
