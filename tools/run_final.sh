@@ -14,6 +14,7 @@ timeout 600 python bench.py --workload maverick --batch 1 --sparsity 0.9 --no-sw
 timeout 600 python bench.py --workload maverick --batch 64 --sparsity 0.9 --steps 50 --no-sweep --no-cpu > gpurun_out/bench_maverick_b64.json 2> gpurun_out/bench_maverick_b64.err
 timeout 600 python bench.py --ep --workload maverick --batch 64 --sparsity 0.9 --steps 50 --warmup 5 --no-cpu > gpurun_out/bench_ep_maverick_w1.json 2> gpurun_out/bench_ep_maverick_w1.err
 timeout 600 python bench.py --ep --workload gptoss --batch 4096 --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_ep_gptoss_w1.json 2> gpurun_out/bench_ep_gptoss_w1.err
+timeout 600 python bench.py --ep --peer-dispatch --fused-push --workload maverick --batch 64 --sparsity 0.9 --steps 50 --warmup 5 --no-cpu > gpurun_out/bench_ep_maverick_w1_peer.json 2> gpurun_out/bench_ep_maverick_w1_peer.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
 python tools/fused_vs_staged.py olmoe granite qwen gptoss 2>&1 | grep -v "B= [5-8]" > gpurun_out/fused_vs_staged.txt
 K='regex:router_|route_|dispatch|permute|grouped_tc|select_rows|down_cluster|combine|decode_fused|ep_'
